@@ -1,0 +1,298 @@
+"""Seeded synthetic inputs for the InstGenIE mask-aware step (test/bench input generators).
+
+This module is shared by the oracle (`oracle/`), the tests and `bench.py`.  It holds NONE
+of the method's arithmetic: it only draws numbers (weights, latents, text tokens, masks,
+sigma schedules, synthetic caches) and describes the model shapes and the weight-table
+layout as data.  See DESIGN.md "Input recipe".
+
+Random numbers come from a counter-based generator (SplitMix64 finaliser applied to
+key+index, key = SplitMix64(seed ^ FNV1a(name))) written with torch int64 ops, so CPU
+and CUDA produce bit-identical values.  Uniforms are odd multiples of 2^-24 in (-1, 1),
+exact in fp32; approximate normals are Irwin-Hall(4) sums rescaled to unit variance,
+computed in float64 and rounded once to fp32 (then to bf16 when asked).  No
+transcendental function touches a value that both sides consume.
+
+Masks are drawn on the host with numpy (rectangles and smooth "blobs") and
+passed as uint8 token bitmaps (nonzero = masked), so both sides see the same bytes.
+"""
+from __future__ import annotations
+
+import dataclasses
+import math
+from typing import Dict, List, Tuple
+
+import numpy as np
+import torch
+
+_M64 = (1 << 64) - 1
+
+
+def _s64(c: int) -> int:
+    """uint64 constant -> the int64 with the same bit pattern."""
+    c &= _M64
+    return c - (1 << 64) if c >= (1 << 63) else c
+
+
+_GAMMA = _s64(0x9E3779B97F4A7C15)
+_MIX1 = _s64(0xBF58476D1CE4E5B9)
+_MIX2 = _s64(0x94D049BB133111EB)
+
+
+def _lsr(z: torch.Tensor, k: int) -> torch.Tensor:
+    """Logical right shift of an int64 tensor (torch's >> is arithmetic)."""
+    return (z >> k) & ((1 << (64 - k)) - 1)
+
+
+def _mix(z: torch.Tensor) -> torch.Tensor:
+    z = (z ^ _lsr(z, 30)) * _MIX1
+    z = (z ^ _lsr(z, 27)) * _MIX2
+    return z ^ _lsr(z, 31)
+
+
+def _mix_int(z: int) -> int:
+    z &= _M64
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & _M64
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & _M64
+    return z ^ (z >> 31)
+
+
+def _fnv1a(name: str) -> int:
+    h = 0xCBF29CE484222325
+    for b in name.encode():
+        h = ((h ^ b) * 0x100000001B3) & _M64
+    return h
+
+
+def stream_key(seed: int, name: str) -> int:
+    return _mix_int((seed ^ _fnv1a(name)) + 0x9E3779B97F4A7C15)
+
+
+def _raw(key: int, n: int, offset: int, device) -> torch.Tensor:
+    idx = torch.arange(offset, offset + n, dtype=torch.int64, device=device)
+    z = idx * _GAMMA + _s64(key)
+    return _mix(z)
+
+
+def uniform(seed: int, name: str, shape, device="cpu", offset: int = 0) -> torch.Tensor:
+    """float64 tensor of odd multiples of 2^-24 in (-1, 1); identical on every device."""
+    n = int(np.prod(shape)) if len(shape) else 1
+    z = _raw(stream_key(seed, name), n, offset, device)
+    u24 = _lsr(z, 40)  # 24 high bits
+    v = (2 * u24 - (1 << 24) + 1).to(torch.float64) * (2.0 ** -24)
+    return v.reshape(shape)
+
+
+def normal(seed: int, name: str, shape, device="cpu") -> torch.Tensor:
+    """Irwin-Hall(4) approximate N(0,1), float64 (exact sums of 2^-24 multiples)."""
+    n = int(np.prod(shape)) if len(shape) else 1
+    s = torch.zeros(n, dtype=torch.float64, device=device)
+    for j in range(4):
+        s += uniform(seed, f"{name}#ih{j}", (n,), device)
+    # Var(U(-1,1)) = 1/3, four of them: 4/3 -> scale by sqrt(3/4)
+    return (s * math.sqrt(0.75)).reshape(shape)
+
+
+# --------------------------------------------------------------------------------------
+# Model shapes.  Data only.
+# --------------------------------------------------------------------------------------
+@dataclasses.dataclass(frozen=True)
+class ModelDesc:
+    name: str
+    n_double: int
+    n_single: int
+    hidden: int
+    heads: int
+    head_dim: int
+    mlp_hidden: int
+    lat_ch: int
+    grid_h: int
+    grid_w: int
+    txt_len: int
+    qk_norm: int = 1
+    rope: int = 1
+    rope_axes: Tuple[int, int, int] = (16, 56, 56)
+    rope_theta: float = 10000.0
+    ln_eps: float = 1e-6
+    pos_embed_2d: int = 0
+    context_pre_only_last: int = 0
+
+    @property
+    def L_img(self) -> int:
+        return self.grid_h * self.grid_w
+
+    @property
+    def L(self) -> int:
+        return self.L_img + self.txt_len
+
+    @property
+    def n_blocks(self) -> int:
+        return self.n_double + self.n_single
+
+
+TINY = ModelDesc("tiny", 0, 1, 64, 4, 16, 256, 16, 16, 16, 0, rope_axes=(4, 6, 6))
+TINY_DOUBLE = ModelDesc("tiny_double", 1, 1, 64, 4, 16, 256, 16, 16, 16, 8, rope_axes=(4, 6, 6))
+SD3 = ModelDesc("sd3_medium", 24, 0, 1536, 24, 64, 6144, 64, 32, 32, 333, qk_norm=0, rope=0,
+                rope_axes=(0, 0, 0), pos_embed_2d=1, context_pre_only_last=1)
+FLUX = ModelDesc("flux1_dev", 19, 38, 3072, 24, 128, 12288, 64, 64, 64, 512)
+# Small Flux-structured model for multi-block / multi-step parity (tiles span >1 CTA tile)
+FLUX_SMALL = ModelDesc("flux_small", 2, 2, 256, 2, 128, 1024, 64, 16, 16, 32)
+MODELS = {m.name: m for m in (TINY, TINY_DOUBLE, SD3, FLUX, FLUX_SMALL)}
+
+
+def weight_table(d: ModelDesc) -> List[Tuple[str, Tuple[int, ...], int]]:
+    """(name, shape, fan_in) in the fixed C-ABI table order (include/ig.h).
+
+    Matrices are [out, in] row-major, each followed by its bias [out]."""
+    H, C, Fm, dh = d.hidden, d.lat_ch, d.mlp_hidden, d.head_dim
+    t: List[Tuple[str, Tuple[int, ...], int]] = []
+
+    def lin(name, out, inp):
+        t.append((name + ".w", (out, inp), inp))
+        t.append((name + ".b", (out,), inp))
+
+    lin("img_in", H, C)
+    lin("t_mlp1", H, 256)
+    lin("t_mlp2", H, H)
+    lin("final_mod", 2 * H, H)
+    lin("proj_out", C, H)
+    if d.pos_embed_2d:
+        t.append(("pos_embed", (d.L_img, H), 0))
+    for i in range(d.n_double):
+        for s in ("img", "txt"):
+            p = f"double.{i}.{s}"
+            pre_only = d.context_pre_only_last and s == "txt" and i == d.n_double - 1
+            lin(p + ".mod", (2 if pre_only else 6) * H, H)
+            lin(p + ".qkv", 3 * H, H)
+            if d.qk_norm:
+                t.append((p + ".q_norm_g", (dh,), 0))
+                t.append((p + ".k_norm_g", (dh,), 0))
+            if not pre_only:
+                lin(p + ".proj", H, H)
+                lin(p + ".fc1", Fm, H)
+                lin(p + ".fc2", H, Fm)
+    for i in range(d.n_single):
+        p = f"single.{i}"
+        lin(p + ".mod", 3 * H, H)
+        lin(p + ".lin1", 3 * H + Fm, H)
+        if d.qk_norm:
+            t.append((p + ".q_norm_g", (dh,), 0))
+            t.append((p + ".k_norm_g", (dh,), 0))
+        lin(p + ".lin2", H, H + Fm)
+    return t
+
+
+def make_weight(d: ModelDesc, name: str, shape, fan_in: int, seed: int = 0, device="cpu",
+                dtype=torch.float32) -> torch.Tensor:
+    """One table tensor.  uniform(+-1/sqrt(fan_in)); modulation weights x0.1; norm gains 1."""
+    if name.endswith("_norm_g"):
+        return torch.ones(shape, dtype=dtype, device=device)
+    if name == "pos_embed":
+        v = uniform(seed, name, shape, device) * 0.5
+    else:
+        a = 1.0 / math.sqrt(fan_in)
+        if ".mod." in name or name.startswith("final_mod"):
+            a *= 0.1
+        v = uniform(seed, name, shape, device) * a
+    return v.to(torch.float32).to(dtype)
+
+
+def make_weights(d: ModelDesc, seed: int = 0, device="cpu", dtype=torch.float32,
+                 names=None) -> Dict[str, torch.Tensor]:
+    out = {}
+    for name, shape, fan_in in weight_table(d):
+        if names is not None and name not in names:
+            continue
+        out[name] = make_weight(d, name, shape, fan_in, seed, device, dtype)
+    return out
+
+
+# --------------------------------------------------------------------------------------
+# Per-request inputs
+# --------------------------------------------------------------------------------------
+def make_latent(d: ModelDesc, rid: int, device="cpu") -> torch.Tensor:
+    return normal(rid, "latent", (d.L_img, d.lat_ch), device).to(torch.float32)
+
+
+def make_txt(d: ModelDesc, rid: int, device="cpu", dtype=torch.float32) -> torch.Tensor:
+    return normal(rid, "txt", (d.txt_len, d.hidden), device).to(torch.float32).to(dtype)
+
+
+def make_cond(d: ModelDesc, rid: int, device="cpu") -> torch.Tensor:
+    return normal(rid, "cond_vec", (d.hidden,), device).to(torch.float32)
+
+
+def make_cache_kv(d: ModelDesc, template: int, n_steps: int, dtype=torch.float32, device="cpu"):
+    """A synthetic template cache K,V [steps][blocks][2][L_img][H] (cache 'from other
+    inputs'; used to test the edit step independently of cache recording)."""
+    shape = (n_steps, d.n_blocks, 2, d.L_img, d.hidden)
+    return normal(1000 + template, "cache_kv", shape, device).to(torch.float32).to(dtype)
+
+
+def flow_sigmas(n_steps: int, shift: float = 3.0) -> np.ndarray:
+    """Shift-3 flow schedule on linspace(1, 0, n+1) [proposal, SURVEY §8(d) config 3]."""
+    s = np.linspace(1.0, 0.0, n_steps + 1)
+    return (shift * s / (1.0 + (shift - 1.0) * s)).astype(np.float32)
+
+
+# --------------------------------------------------------------------------------------
+# Masks: uint8 token bitmaps, nonzero = masked (C-AMB 13-15)
+# --------------------------------------------------------------------------------------
+def rect_mask(d: ModelDesc, r0: int, r1: int, c0: int, c1: int) -> np.ndarray:
+    m = np.zeros((d.grid_h, d.grid_w), np.uint8)
+    m[r0:r1, c0:c1] = 1
+    return m.reshape(-1)
+
+
+def rect_mask_count(d: ModelDesc, n: int, rng: np.random.Generator) -> np.ndarray:
+    """Near-square rectangle holding exactly n tokens (last row ragged)."""
+    m = np.zeros(d.L_img, np.uint8)
+    if n <= 0:
+        return m
+    if n >= d.L_img:
+        m[:] = 1
+        return m
+    aspect = math.exp(rng.uniform(-0.5, 0.5))
+    w = int(min(d.grid_w, max(1, round(math.sqrt(n * aspect)))))
+    h = int(min(d.grid_h, math.ceil(n / w)))
+    while h * w < n:
+        w = min(d.grid_w, w + 1)
+        h = min(d.grid_h, math.ceil(n / w))
+    r0 = int(rng.integers(0, d.grid_h - h + 1))
+    c0 = int(rng.integers(0, d.grid_w - w + 1))
+    cnt = 0
+    for r in range(r0, r0 + h):
+        for c in range(c0, c0 + w):
+            if cnt < n:
+                m[r * d.grid_w + c] = 1
+                cnt += 1
+    return m
+
+
+def blob_mask_count(d: ModelDesc, n: int, rng: np.random.Generator) -> np.ndarray:
+    """Top-n tokens of a smooth field (3 Gaussian bumps + 0.1 noise); ties -> lower index."""
+    m = np.zeros(d.L_img, np.uint8)
+    if n <= 0:
+        return m
+    yy, xx = np.meshgrid(np.arange(d.grid_h), np.arange(d.grid_w), indexing="ij")
+    f = np.zeros((d.grid_h, d.grid_w))
+    for _ in range(3):
+        cy, cx = rng.uniform(0, d.grid_h), rng.uniform(0, d.grid_w)
+        s = rng.uniform(0.1, 0.3) * max(d.grid_h, d.grid_w)
+        f += np.exp(-((yy - cy) ** 2 + (xx - cx) ** 2) / (2 * s * s))
+    f = f.reshape(-1) + 0.1 * rng.standard_normal(d.L_img)
+    order = np.argsort(-f, kind="stable")
+    m[order[:min(n, d.L_img)]] = 1
+    return m
+
+
+def mixed_mask(d: ModelDesc, rid: int, lo: float = 0.05, hi: float = 0.60) -> np.ndarray:
+    """Headline mix: m ~ U[lo, hi], n_m = round(m L_img); even ids rectangles, odd blobs."""
+    rng = np.random.default_rng(7919 * rid + 17)
+    m = rng.uniform(lo, hi)
+    n = int(round(m * d.L_img))
+    return rect_mask_count(d, n, rng) if rid % 2 == 0 else blob_mask_count(d, n, rng)
+
+
+def tiny_rect_mask() -> np.ndarray:
+    """Config 1: rectangle rows 4-11 x cols 4-11 on the 16x16 grid (64 tokens, 25%)."""
+    return rect_mask(TINY, 4, 12, 4, 12)

@@ -1,0 +1,323 @@
+"""Pins for the float64 oracle (oracle/instgenie.py) against things other than itself:
+closed forms, the hand-evaluated worked example (tests/golden/), textbook library routines
+(torch float64), brute force on tiny inputs and the exactness invariants the paper fixes
+(all-ones mask == dense, empty mask == untouched, same-input cache => masked rows equal the
+dense rows; Table 1)."""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+import torch
+import torch.nn.functional as F
+
+import oracle
+import synth
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _np(t):
+    return t.double().numpy()
+
+
+# ---------------------------------------------------------------- a1 index build
+@pytest.mark.parametrize("seed", range(8))
+def test_index_build_matches_nonzero_and_partition(seed):
+    rng = np.random.default_rng(seed)
+    L = 4096
+    mask = (rng.random(L) < rng.random()).astype(np.uint8) * rng.integers(1, 255)
+    idx_m, idx_u, n = oracle.index_build(mask)
+    assert np.array_equal(idx_m, np.flatnonzero(mask))          # library routine
+    assert np.array_equal(idx_u, np.flatnonzero(mask == 0))
+    assert n == int((mask != 0).sum())                            # popcount
+    assert np.all(np.diff(idx_m) > 0) and np.all(np.diff(idx_u) > 0)  # ascending
+    assert np.array_equal(np.sort(np.concatenate([idx_m, idx_u])), np.arange(L))
+
+
+@pytest.mark.parametrize("kind", ["empty", "full", "single0", "last", "tiny_rect"])
+def test_index_build_degenerate(kind):
+    L = 4096
+    m = np.zeros(L, np.uint8)
+    if kind == "full":
+        m[:] = 1
+    elif kind == "single0":
+        m[0] = 1
+    elif kind == "last":
+        m[-1] = 1
+    elif kind == "tiny_rect":
+        m = synth.tiny_rect_mask()
+        L = 256
+    idx_m, idx_u, n = oracle.index_build(m)
+    brute = [i for i in range(L) if m[i]]
+    assert list(idx_m) == brute and n == len(brute) and len(idx_u) == L - n
+    if kind == "tiny_rect":   # rows 4-11 x cols 4-11 of 16x16: 64 tokens, 25% (config 1)
+        assert n == 64 and idx_m[0] == 4 * 16 + 4 and idx_m[-1] == 11 * 16 + 11
+
+
+def test_mask_ratio_spec_examples():
+    # [t,t,f,f] -> 0.5; all-false -> 0; all-true -> 1
+    for bits, r in (([1, 1, 0, 0], 0.5), ([0] * 8, 0.0), ([1] * 8, 1.0)):
+        assert oracle.index_build(np.array(bits, np.uint8))[2] / len(bits) == r
+
+
+# ---------------------------------------------------------------- primitives vs library
+def test_layernorm_rmsnorm_gelu_silu_match_torch():
+    g = torch.Generator().manual_seed(0)
+    x = torch.randn(7, 64, generator=g, dtype=torch.float64) * 3 + 1
+    assert np.allclose(oracle.layernorm(_np(x), 1e-6), _np(F.layer_norm(x, (64,), eps=1e-6)),
+                       rtol=1e-13, atol=1e-13)
+    gain = torch.rand(16, generator=g, dtype=torch.float64) + 0.5
+    ref = F.rms_norm(x.view(7, 4, 16), (16,), weight=gain, eps=1e-6).view(7, 64)
+    assert np.allclose(oracle.rmsnorm_heads(_np(x), _np(gain), 4, 1e-6), _np(ref), rtol=1e-13, atol=1e-13)
+    assert np.allclose(oracle.gelu_tanh(_np(x)), _np(F.gelu(x, approximate="tanh")), rtol=1e-13, atol=1e-14)
+    assert np.allclose(oracle.silu(_np(x)), _np(F.silu(x)), rtol=1e-13, atol=1e-14)
+
+
+@pytest.mark.parametrize("heads,n,L", [(1, 3, 5), (4, 17, 40), (2, 1, 129)])
+def test_attention_matches_torch_sdpa(heads, n, L):
+    g = torch.Generator().manual_seed(heads * 100 + n)
+    H = heads * 16
+    q, K, V = (torch.randn(r, H, generator=g, dtype=torch.float64) for r in (n, L, L))
+    ref = F.scaled_dot_product_attention(q.view(n, heads, 16).transpose(0, 1),
+                                         K.view(L, heads, 16).transpose(0, 1),
+                                         V.view(L, heads, 16).transpose(0, 1))
+    ref = ref.transpose(0, 1).reshape(n, H)
+    assert np.allclose(oracle.attention(_np(q), _np(K), _np(V), heads), _np(ref), rtol=1e-12, atol=1e-12)
+
+
+def test_attention_brute_force_loops():
+    rng = np.random.default_rng(3)
+    q, K, V = rng.standard_normal((2, 4)), rng.standard_normal((3, 4)), rng.standard_normal((3, 4))
+    out = oracle.attention(q, K, V, 2)
+    for i in range(2):
+        for h in range(2):
+            s = [sum(q[i, 2 * h + t] * K[j, 2 * h + t] for t in range(2)) / math.sqrt(2) for j in range(3)]
+            e = [math.exp(v) for v in s]
+            for t in range(2):
+                ref = sum(e[j] * V[j, 2 * h + t] for j in range(3)) / sum(e)
+                assert abs(out[i, 2 * h + t] - ref) < 1e-14
+
+
+def test_attention_zero_input_is_uniform():
+    # zero scores -> uniform weights -> output = mean of V rows
+    V = np.random.default_rng(1).standard_normal((9, 8))
+    out = oracle.attention(np.zeros((3, 8)), np.zeros((9, 8)), V, 2)
+    assert np.allclose(out, V.mean(axis=0, keepdims=True).repeat(3, 0), atol=1e-15)
+
+
+def test_attention_key_order_freedom():
+    # C-AMB 8: a joint permutation of K/V rows changes the output only by rounding
+    rng = np.random.default_rng(5)
+    q, K, V = rng.standard_normal((6, 32)), rng.standard_normal((50, 32)), rng.standard_normal((50, 32))
+    p = rng.permutation(50)
+    a, b = oracle.attention(q, K, V, 2), oracle.attention(q, K[p], V[p], 2)
+    assert np.max(np.abs(a - b)) <= 1e-12 * np.max(np.abs(a))
+
+
+def test_rope_is_complex_rotation():
+    # Textbook: pair (x0, x1) at angle phi == complex multiply (x0 + i x1) e^{i phi}
+    rng = np.random.default_rng(2)
+    axes, theta, heads = (4, 6, 6), 10000.0, 2
+    x = rng.standard_normal((5, 32))
+    pos = rng.integers(0, 16, size=(5, 3))
+    y = oracle.rope(x, pos, heads, axes, theta)
+    xc = x.reshape(5, heads, 8, 2)
+    ref = np.empty_like(xc)
+    j_glob = 0
+    for a, da in enumerate(axes):
+        for j in range(da // 2):
+            phi = pos[:, a] * theta ** (-2.0 * j / da)
+            z = (xc[:, :, j_glob, 0] + 1j * xc[:, :, j_glob, 1]) * np.exp(1j * phi)[:, None]
+            ref[:, :, j_glob, 0], ref[:, :, j_glob, 1] = z.real, z.imag
+            j_glob += 1
+    assert np.allclose(y, ref.reshape(5, 32), atol=1e-13)
+    assert np.allclose(oracle.rope(x, np.zeros((5, 3), np.int64), heads, axes, theta), x)  # text pos
+
+
+def test_rope_relative_position():
+    rng = np.random.default_rng(9)
+    q, k = rng.standard_normal((1, 16)), rng.standard_normal((1, 16))
+    ax = (4, 6, 6)
+    p1, p2, dlt = np.array([[0, 3, 5]]), np.array([[0, 7, 1]]), np.array([[0, 4, 9]])
+    a = oracle.rope(q, p1, 1, ax, 1e4) @ oracle.rope(k, p2, 1, ax, 1e4).T
+    b = oracle.rope(q, p1 + dlt, 1, ax, 1e4) @ oracle.rope(k, p2 + dlt, 1, ax, 1e4).T
+    assert abs(a - b).max() < 1e-12
+
+
+def test_sinusoid_closed_form():
+    e0 = oracle.sinusoid(0.0)
+    assert np.array_equal(e0[:128], np.ones(128)) and np.array_equal(e0[128:], np.zeros(128))
+    t = 731.0
+    e = oracle.sinusoid(t)
+    assert abs(e[0] - math.cos(t)) < 1e-15 and abs(e[128] - math.sin(t)) < 1e-15   # f_0 = 1
+    assert abs(e[127] - math.cos(t * 10000 ** (-127 / 128))) < 1e-12
+
+
+# ---------------------------------------------------------------- worked example (golden)
+def test_worked_example_golden():
+    gold = json.load(open(os.path.join(GOLD, "worked_example.json")))
+    x = np.array(gold["x"])
+    I = np.eye(2)
+    y, K, V = oracle.reduced_forward_full(x, I, I, I, I, I, I)
+    assert np.allclose(y, gold["dense_y"], atol=gold["atol"])
+    mask = np.array(gold["mask"], np.uint8)
+    ym = oracle.reduced_forward_masked_kvcache(x, mask, K, V, I, I, I, I, I, I)
+    assert np.allclose(ym[0], gold["masked_row_same_cache"], atol=gold["atol"])
+    K2, V2 = K.copy(), V.copy()
+    K2[0] = V2[0] = gold["other_template_token0_kv"]
+    ym2 = oracle.reduced_forward_masked_kvcache(x, mask, K2, V2, I, I, I, I, I, I)
+    assert np.allclose(ym2[0], gold["masked_row_other_cache"], atol=gold["atol"])
+
+
+def _reduced_desc(H, grid):
+    return synth.ModelDesc("reduced", 1, 0, H, 1, H, 4 * H, 4, grid, grid, 0, qk_norm=0, rope=0,
+                           rope_axes=(0, 0, 0))
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_flux_block_with_flags_off_reduces_to_spec_block(seed):
+    # C-AMB 5: h=1, no LN/mod/residual/gates/GELU/norm/RoPE => y = FF(Attn(x) W_o)
+    rng = np.random.default_rng(seed)
+    H, g = 8, 4
+    d = _reduced_desc(H, g)
+    L = d.L_img
+    Wq, Wk, Wv, Wo = (rng.standard_normal((H, H)) / 3 for _ in range(4))
+    W1, W2 = rng.standard_normal((H, 4 * H)) / 3, rng.standard_normal((4 * H, H)) / 3
+    x = rng.standard_normal((L, H))
+    y_full, K, V = oracle.reduced_forward_full(x, Wq, Wk, Wv, Wo, W1, W2)
+    W = {"double.0.img.qkv.w": np.concatenate([Wq, Wk, Wv], axis=1).T,
+         "double.0.img.proj.w": Wo.T, "double.0.img.fc1.w": W1.T, "double.0.img.fc2.w": W2.T}
+    flags = dict(adaln=False, residual=False, gelu=False)
+    mask = (rng.random(L) < 0.4).astype(np.uint8)
+    mask[0] = 1
+    idx_m, idx_u, _ = oracle.index_build(mask)
+    # cache = the reduced block's own K,V of the same x  ->  masked rows equal dense rows
+    _, yi = oracle.double_block_masked(d, W, 0, np.zeros((0, H)), x[idx_m], None, idx_m, idx_u,
+                                       np.stack([K, V]), flags)
+    ym = oracle.reduced_forward_masked_kvcache(x, mask, K, V, Wq, Wk, Wv, Wo, W1, W2)
+    assert np.allclose(yi, ym, rtol=1e-12, atol=1e-12)
+    assert np.allclose(yi, y_full[idx_m], rtol=1e-12, atol=1e-12)
+
+
+# ---------------------------------------------------------------- exactness invariants
+_SMALL = synth.ModelDesc("inv", 1, 1, 32, 2, 16, 64, 4, 8, 8, 3, rope_axes=(4, 6, 6))
+
+
+def _weights(d, seed=0):
+    return {k: _np(v) for k, v in synth.make_weights(d, seed).items()}
+
+
+def _inputs(d, rid):
+    return (_np(synth.make_latent(d, rid)), _np(synth.make_txt(d, rid)), _np(synth.make_cond(d, rid)))
+
+
+@pytest.fixture(scope="module")
+def small_model():
+    return _SMALL, _weights(_SMALL)
+
+
+def test_masked_rows_equal_dense_grid(small_model):
+    # S:141 grid: >=200 seeded cases, L<=64, H<=32, every bitmap-integral m in 1..L
+    d, W = small_model
+    sig = (0.8, 0.6)
+    cases = 0
+    for rid in range(4):
+        lat, txt, cond = _inputs(d, rid)
+        x1, kv = oracle.dense_step(d, W, lat, sig[0], sig[1], txt, cond, record=True)
+        rng = np.random.default_rng(rid)
+        for n in range(1, d.L_img + 1):
+            mask = np.zeros(d.L_img, np.uint8)
+            mask[rng.permutation(d.L_img)[:n]] = 1
+            y = oracle.edit_step(d, W, lat, mask, kv, sig[0], sig[1], txt, cond)
+            idx = np.flatnonzero(mask)
+            scale = np.abs(x1[idx]).max()
+            assert np.max(np.abs(y[idx] - x1[idx])) <= 1e-12 * scale, n
+            assert np.array_equal(y[mask == 0], lat[mask == 0])  # untouched (C-AMB 11)
+            cases += 1
+    assert cases >= 200
+
+
+def test_all_ones_equals_dense_and_empty_is_identity(small_model):
+    d, W = small_model
+    lat, txt, cond = _inputs(d, 7)
+    x1, _ = oracle.dense_step(d, W, lat, 1.0, 0.9, txt, cond)
+    ones = np.ones(d.L_img, np.uint8)
+    assert np.array_equal(oracle.edit_step(d, W, lat, ones, None, 1.0, 0.9, txt, cond), x1)
+    zero = np.zeros(d.L_img, np.uint8)
+    assert np.array_equal(oracle.edit_step(d, W, lat, zero, None, 1.0, 0.9, txt, cond), lat)
+
+
+def test_cache_miss_raises(small_model):
+    d, W = small_model
+    lat, txt, cond = _inputs(d, 1)
+    m = np.zeros(d.L_img, np.uint8)
+    m[3] = 1
+    with pytest.raises(KeyError):
+        oracle.edit_step(d, W, lat, m, None, 1.0, 0.9, txt, cond)
+
+
+def test_multistep_trajectory_invariant():
+    # 2-step tiny (config 1): a cache recorded along the dense trajectory keeps the masked
+    # rows on that trajectory step after step.
+    d = synth.TINY
+    W = _weights(d)
+    lat, txt, cond = _inputs(d, 0)
+    sig = [1.0, 0.5, 0.0]
+    _, cache, traj = oracle.cache_template(d, W, lat, txt, cond, sig)
+    mask = synth.tiny_rect_mask()
+    idx = np.flatnonzero(mask)
+    x = lat
+    for s in range(2):
+        x = oracle.edit_step(d, W, x, mask, cache[s], sig[s], sig[s + 1], txt, cond)
+        assert np.max(np.abs(x[idx] - traj[s + 1][idx])) <= 1e-12 * np.abs(traj[s + 1]).max()
+
+
+def test_cache_is_used_and_unmasked_permutation_free(small_model):
+    # A cache from other inputs moves the masked rows (the cache is really used) ...
+    d, W = small_model
+    lat, txt, cond = _inputs(d, 2)
+    lat_other, _, _ = _inputs(d, 3)
+    _, kv = oracle.dense_step(d, W, lat, 1.0, 0.9, txt, cond, record=True)
+    _, kv_o = oracle.dense_step(d, W, lat_other, 1.0, 0.9, txt, cond, record=True)
+    mask = np.zeros(d.L_img, np.uint8)
+    mask[10:30] = 1
+    a = oracle.edit_step(d, W, lat, mask, kv, 1.0, 0.9, txt, cond)
+    b = oracle.edit_step(d, W, lat, mask, kv_o, 1.0, 0.9, txt, cond)
+    assert np.max(np.abs(a - b)) > 1e-5   # rounding alone is ~1e-15
+    # ... and jointly permuting the unmasked tokens' cached K,V rows (keys carry their RoPE
+    # already) changes the masked rows only by rounding (C-AMB 8)
+    idx_u = np.flatnonzero(mask == 0)
+    p = idx_u[np.random.default_rng(0).permutation(len(idx_u))]
+    kvp = kv.copy()
+    kvp[:, :, idx_u] = kv[:, :, p]
+    c = oracle.edit_step(d, W, lat, mask, kvp, 1.0, 0.9, txt, cond)
+    assert np.max(np.abs(a - c)) <= 1e-12 * np.abs(a).max()
+
+
+# ---------------------------------------------------------------- Table 1 FLOP accounting
+def test_table1_macs_tiny_block():
+    d = synth.TINY
+    W = _weights(d)
+    H = d.hidden
+    vec = np.random.default_rng(0).standard_normal(H)
+    x_all = np.random.default_rng(1).standard_normal((d.L_img, H))
+    kv = np.random.default_rng(2).standard_normal((2, d.L_img, H))
+    res = {}
+    for name, mask in (("dense", np.ones(d.L_img, np.uint8)), ("masked", synth.tiny_rect_mask())):
+        idx_m, idx_u, n = oracle.index_build(mask)
+        oracle.reset_macs()
+        oracle.single_block_masked(d, W, 0, x_all[idx_m], vec, idx_m, idx_u, kv)
+        res[name] = oracle.MACS["linear"] + oracle.MACS["attn"] - 3 * H * H  # minus modulation
+    # SURVEY 8(c) derived: tiny dense block 41.94 MFLOP, 25% masked 10.49 MFLOP
+    assert 2 * res["dense"] == 41943040 and 2 * res["masked"] == 10485760
+    assert res["masked"] / res["dense"] == 0.25           # speedup 1/m exactly (L_txt = 0)
+
+
+def test_table1_flux_per_row_closed_form():
+    d = synth.FLUX
+    lin, att = 2 * oracle.macs_per_row_linear(d), 2 * oracle.macs_per_row_attn(d)
+    assert abs(lin / 1e9 - 12.910) < 1e-3 and abs(att / 1e9 - 3.2275) < 1e-4
+    F = lambda m: (lin + att) * (512 + 4096 * m) / 1e12
+    assert abs(F(0) - 8.262) < 1e-3 and abs(F(1) - 74.36) < 1e-2
