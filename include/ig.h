@@ -1,0 +1,184 @@
+/* ig.h — C ABI of libig, the B200-native mask-aware denoising step of InstGenIE
+ * (arXiv 2505.20600), K/V-caching variant (fig:transformer_alter).
+ *
+ * Citations: P:n = PAPER.md line n; S:n = SPEC.md line n; C-AMB k / §8(x) = the numbered
+ * readings in DESIGN.md (taken from SURVEY.md §8(c)).
+ *
+ * Conventions for every entry point
+ *  - Every call returns ig_status; IG_OK == 0.  No C++ exception crosses the ABI.
+ *    ig_last_error() returns a thread-local message for the last non-OK status.
+ *  - All argument, shape and compatibility checks run on the host BEFORE anything is
+ *    enqueued: a non-OK status means nothing was enqueued (no partial enqueue).
+ *  - "dev" pointers are CUDA device pointers on the context's device, "host" pointers are
+ *    host memory.  `stream` arguments are cudaStream_t passed as void* (NULL = the legacy
+ *    default stream).  Calls return after enqueue unless documented otherwise.
+ *  - Ownership: the caller owns every buffer it passes in (weights, latents, masks, text,
+ *    cond vectors, streams) and must keep them alive until the enqueued work completes.
+ *    The library owns ig_ctx workspaces, per-slot K/V staging rings, ig_mask index lists
+ *    and ig_cache storage (pinned host or device memory), freed by the *_free/_destroy calls.
+ *  - One host thread per ig_ctx.  Contexts on different devices are independent.
+ */
+#ifndef IG_H_
+#define IG_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  IG_OK = 0,
+  IG_EINVAL = 1,          /* invalid argument / shape mismatch        */
+  IG_ECACHE_INCOMPAT = 2, /* cache built for another model/schedule, or step out of range */
+  IG_ECACHE_MISS = 3,     /* 0 < n_m < L_img but no cache supplied                 */
+  IG_ENUMERIC = 4,        /* non-finite output (debug checks only)                  */
+  IG_ENOMEM = 5,          /* allocation failed or a step exceeds max_batch / max_rows      */
+  IG_ECUDA = 6,           /* CUDA runtime/driver error (message has cudaGetErrorString)    */
+  IG_EUNSUPPORTED = 7     /* shape the kernels do not support (see ig_ctx_create)          */
+} ig_status;
+
+typedef enum { IG_F32 = 0, IG_BF16 = 1 } ig_dtype;
+
+/* Model shape (Flux-/SD3-shaped DiT; the paper's X in R^{B x L x H}).
+ * L_img = grid_h*grid_w image tokens (latent (B,C,H,W) reshaped to (B, H*W, C)),
+ * L = txt_len + L_img.  Validated by ig_ctx_create.
+ * Constraints: hidden = heads*head_dim; head_dim in {16, 64, 128}; hidden % 64 == 0;
+ * mlp_hidden % 64 == 0; lat_ch % 4 == 0; rope_axes sum to head_dim when rope != 0. */
+typedef struct {
+  int n_double, n_single;   /* double-stream (img/txt weights) and single-stream blocks */
+  int hidden, heads, head_dim, mlp_hidden;
+  int lat_ch, grid_h, grid_w, txt_len;
+  int qk_norm;              /* per-head RMSNorm on q,k with gains (C-AMB 6)              */
+  int rope;                 /* 3-axis RoPE at ORIGINAL token positions (C-AMB 7)         */
+  int rope_axes[3];
+  float rope_theta, ln_eps;
+  int pos_embed_2d;         /* SD3: add pos_embed[token] at img_in                       */
+  int context_pre_only_last;/* SD3: last double block's text stream only feeds K/V      */
+  ig_dtype dtype;           /* IG_F32 = parity mode (fp32 SIMT), IG_BF16 = perf mode    */
+} ig_model_desc;
+
+/* Weight table (device pointers, caller-owned, dtype = desc.dtype except where noted),
+ * in this fixed order; matrices are [out, in] row-major (nn.Linear), each followed by its
+ * bias [out]:
+ *   img_in.w [H,C], img_in.b, t_mlp1.w [H,256], t_mlp1.b, t_mlp2.w [H,H], t_mlp2.b,
+ *   final_mod.w [2H,H], final_mod.b, proj_out.w [C,H], proj_out.b,
+ *   (pos_embed_2d) pos_embed [L_img,H],
+ *   for each double block i, for s in (img, txt):
+ *       mod.w [6H,H] (2H for a context-pre-only text stream), mod.b, qkv.w [3H,H], qkv.b,
+ *       (qk_norm) q_norm_g [d], k_norm_g [d],
+ *       (unless context-pre-only) proj.w [H,H], proj.b, fc1.w [F,H], fc1.b, fc2.w [H,F], fc2.b
+ *   for each single block i:
+ *       mod.w [3H,H], mod.b, lin1.w [3H+F,H], lin1.b, (qk_norm) q_norm_g, k_norm_g,
+ *       lin2.w [H,H+F], lin2.b
+ * Modulation chunk order: double (shift1, scale1, gate1, shift2, scale2, gate2); single
+ * (shift, scale, gate); final and context-pre-only (scale, shift).  ig_weight_count()
+ * returns the table length for a descriptor. */
+int ig_weight_count(const ig_model_desc* desc);
+
+typedef struct {
+  int max_batch;       /* continuous-batching slots (default 8)                    */
+  int max_rows;        /* max packed query rows per step, sum_r (L_txt + n_m,r) (default  */
+                       /* max_batch * L)                                                  */
+  int prefetch_depth;  /* D: layers the copy lane runs ahead of compute (default 2)       */
+  int copy_mode;       /* 0 = full-L per-layer cudaMemcpyAsync (v1), 1 = compacted:       */
+                       /*     unmasked rows only, zero-copy gather kernel on the copy lane */
+  int debug_checks;    /* 1 = check the latent for non-finite values after each step     */
+} ig_ctx_opts;
+
+typedef struct ig_ctx ig_ctx;
+typedef struct ig_cache ig_cache;
+typedef struct ig_mask ig_mask;
+
+/* Create a context on `device`.  weights: n_weights device pointers in table order.
+ * opts may be NULL (defaults).  Allocates workspaces and per-slot K/V rings
+ * (max_batch x (D+1) x 2 x L x H elements).  Errors: IG_EINVAL, IG_EUNSUPPORTED, IG_ENOMEM,
+ * IG_ECUDA. */
+ig_status ig_ctx_create(const ig_model_desc* desc, const void* const* weights, int n_weights,
+                        int device, const ig_ctx_opts* opts, ig_ctx** out);
+void ig_ctx_destroy(ig_ctx* ctx);
+
+typedef enum { IG_CACHE_HOST = 0, IG_CACHE_DEVICE = 1 } ig_cache_tier;
+
+/* Template cache: for every (step s, block b) the image-token K and V exactly as consumed
+ * by attention (post-bias, post-RMSNorm, post-RoPE; C-AMB 2), layout
+ * [n_steps][n_blocks][2 (K,V)][L_img][H], dtype = desc.dtype, in pinned host memory
+ * (IG_CACHE_HOST, "host memory ... for cached activations") or in HBM
+ * (IG_CACHE_DEVICE).  Bytes = n_steps*n_blocks*2*L_img*H*sizeof(dtype): twice the
+ * Y-cache size ("doubles the sizes of the cached activations"). */
+ig_status ig_cache_create(ig_ctx* ctx, int n_steps, int tier, ig_cache** out);
+
+/* Dense sampler over the template's own schedule (C-AMB 10; "pre-computed
+ * activations from previous requests"): runs n_steps full-token steps from `latent`
+ * (dev [L_img, lat_ch] fp32, updated in place along the trajectory), recording every
+ * (step, block) K/V into a new cache.  sigmas: host [n_steps+1].  txt: dev [txt_len, H]
+ * (desc.dtype), cond_vec: dev [H] fp32.  Uses slot 0's staging; must not run concurrently
+ * with ig_edit_step on the same ctx.  Synchronises `stream` before returning. */
+ig_status ig_cache_template(ig_ctx* ctx, float* latent, const void* txt, const float* cond_vec,
+                            const float* sigmas, int n_steps, int tier, void* stream,
+                            ig_cache** out);
+
+/* Raw storage of a cache: host or device pointer (per tier) and its size in bytes, for
+ * test I/O and for filling a synthetic cache.  The pointer stays owned by the cache. */
+ig_status ig_cache_storage(ig_cache* cache, void** ptr, size_t* bytes, int* tier);
+/* Deferred until no enqueued step references the cache (pin count). */
+void ig_cache_free(ig_cache* cache);
+
+/* a1 — index build (kernel a, C-AMB 13-16).  mask: dev uint8 [L_img], nonzero =
+ * masked.  Builds idx_m (ascending masked token indices) and idx_u (ascending complement)
+ * on the device and returns n_m to the host (one stream sync at admission, never on the
+ * step path).  n_masked may be NULL. */
+ig_status ig_mask_build(ig_ctx* ctx, const uint8_t* mask, void* stream, ig_mask** out,
+                        int* n_masked);
+/* Device pointers to idx_m [n_m] and idx_u [L_img - n_m] (int32) and n_m. */
+ig_status ig_mask_indices(const ig_mask* mask, const int32_t** idx_m, const int32_t** idx_u,
+                          int* n_m);
+void ig_mask_free(ig_mask* mask);
+
+typedef struct {
+  int slot;                /* continuous-batching slot 0..max_batch-1, stable for the       */
+                           /* request's life; distinct within one call                      */
+  float* latent;           /* dev [L_img, lat_ch] fp32, in/out: masked rows updated,         */
+                           /* unmasked rows untouched (C-AMB 11)                             */
+  const ig_mask* mask;
+  const ig_cache* cache;   /* NULL allowed only when n_m == L_img (ignored then, C-AMB 27)   */
+  int step;                /* index into the cache's schedule (C-AMB 9)                      */
+  float sigma, sigma_next; /* flow-matching Euler step; t = 1000*sigma (C-AMB 12)            */
+  const void* txt;         /* dev [txt_len, H] (desc.dtype)                                  */
+  const float* cond_vec;   /* dev [H] fp32                                                   */
+} ig_edit_req;
+
+/* One mask-aware denoising step for a ragged continuous batch (P:642-659 step-level
+ * continuous batching): for every block, only the [txt | masked image] rows of each
+ * request go through the GEMMs, their fresh K/V are merged by mask index
+ * with the template's cached unmasked-token K/V (fig:transformer_alter), masked-Q x full-KV
+ * attention runs ragged across the batch, and the final velocity is scattered into
+ * the masked latent rows.  The cache is prefetched layer by layer on the ctx copy stream,
+ * D layers ahead, with event hand-off.  Requests with n_m == 0 are skipped
+ * (no copies, latent bit-identical).  Enqueues on `stream`; returns after enqueue.
+ * Errors: IG_EINVAL, IG_ECACHE_MISS, IG_ECACHE_INCOMPAT, IG_ENOMEM, IG_ECUDA. */
+ig_status ig_edit_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, void* stream);
+
+/* Explicit warm-up: enqueue on the ctx copy stream the cached K/V of (req->cache,
+ * req->step, layer) into req->slot's staging buffer for that layer and record the slot's
+ * layer event.  ig_edit_step consumes a layer that was prefetched this way instead of
+ * copying it again (only for layers < prefetch_depth of the next step). */
+ig_status ig_prefetch_layer(ig_ctx* ctx, const ig_edit_req* req, int layer);
+
+const char* ig_last_error(void);
+
+/* Counters of the last ig_edit_step / ig_cache_template call on this ctx. */
+typedef struct {
+  long long kernel_launches;  /* libig kernels enqueued                      */
+  long long h2d_bytes;        /* cache bytes copied host->device            */
+  long long d2d_bytes;        /* cache bytes copied device->device          */
+  long long d2h_bytes;        /* cache bytes recorded device->host          */
+  long long rows;             /* packed query rows M                         */
+} ig_stats;
+ig_status ig_last_stats(const ig_ctx* ctx, ig_stats* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* IG_H_ */

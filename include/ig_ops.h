@@ -1,0 +1,38 @@
+/* ig_ops.h — per-kernel entry points of libig, exported for parity tests and benchmarks.
+ * Same conventions as ig.h (status codes, host-side validation before enqueue, void*
+ * streams, caller-owned device buffers).  These call exactly the kernels ig_edit_step uses.
+ */
+#ifndef IG_OPS_H_
+#define IG_OPS_H_
+#include "ig.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* a6/a9/a10 — C[M,N] = epi(A[M,K] B[N,K]^T + bias[N]) (kernel c).  dtype IG_BF16 runs the
+ * tcgen05/TMEM/TMA tensor-core GEMM (fp32 accumulate), IG_F32 the CUDA-core FFMA GEMM.
+ * A, B, bias have the given dtype; C is fp32 when out_f32 else dtype.  epi: 0 = store,
+ * 1 = GELU-tanh (C-AMB 6).  Row-major with leading dimensions in elements.  IG_BF16
+ * requires K % 64 == 0, N % 16 == 0, lda/ldb/ldc multiples of 8 and 16-byte aligned
+ * pointers (IG_EUNSUPPORTED otherwise). */
+ig_status ig_op_gemm(int dtype, const void* A, long long lda, const void* B, long long ldb,
+                     const void* bias, void* C, long long ldc, int M, int N, int K, int epi,
+                     int out_f32, void* stream);
+
+/* a8 — ragged attention (kernel d): for each segment s (host array
+ * segs[s] = {q_start, q_len, kv_index}) and head j: O[q rows, j] = softmax(Q K^T * scale) V
+ * where K = kv + kv_index*2*L*H ([L, H]) and V = K + L*H.  Q, O: [M, H] packed rows with
+ * leading dimensions ldq/ldo (elements); H = heads*head_dim.  scale = 1/sqrt(head_dim). */
+ig_status ig_op_attention(int dtype, const void* Q, long long ldq, void* O, long long ldo,
+                          const void* kv, const int32_t* segs, int nseg, int L, int heads,
+                          int head_dim, void* stream);
+
+/* Test/bench I/O helper: cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault) on `stream`
+ * followed by a stream synchronisation (any host/device combination, UVA pointers). */
+ig_status ig_copy(void* dst, const void* src, size_t bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,1002 @@
+// ig_api.cu — libig host runtime: contexts, masks, template caches, the mask-aware step
+// (ig_edit_step) and its layer-wise cache prefetch pipeline.  C ABI in include/ig.h.
+//
+// Step structure: batch assembly -> conditioning GEMVs -> entry gather +
+// img_in -> per block [LN+mod -> QKV GEMM -> (wait cache copy) -> QK-norm/RoPE/positional
+// K/V merge -> ragged attention -> (free buffer) -> out-proj (+MLP) with gated residual] ->
+// final layer -> Euler scatter.  The copy stream moves the template's cached K/V of block
+// b + R into ring buffer (b % R) while block b computes ("while loading the i-th
+// block, the computation stream can concurrently execute the computation of the (i-1)-th").
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/ig.h"
+#include "../../include/ig_ops.h"
+#include "kernels.h"
+
+using namespace ig;
+
+// ----------------------------------------------------------------------------------------
+// errors
+// ----------------------------------------------------------------------------------------
+static thread_local std::string g_err;
+
+static ig_status set_err(ig_status s, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return s;
+}
+
+#define CUDA_TRY(expr)                                                                     \
+  do {                                                                                     \
+    cudaError_t e_ = (expr);                                                               \
+    if (e_ != cudaSuccess)                                                                 \
+      return set_err(IG_ECUDA, "%s failed: %s (%s:%d)", #expr, cudaGetErrorString(e_),   \
+                     __FILE__, __LINE__);                                                  \
+  } while (0)
+
+extern "C" const char* ig_last_error(void) { return g_err.c_str(); }
+
+// ----------------------------------------------------------------------------------------
+// structures
+// ----------------------------------------------------------------------------------------
+namespace {
+struct LinW {
+  const void* w = nullptr;
+  const void* b = nullptr;
+  int out = 0, in = 0;
+};
+struct StreamW {
+  LinW mod, qkv, proj, fc1, fc2;
+  const void* qg = nullptr;
+  const void* kg = nullptr;
+  bool pre_only = false;
+  int mod_t = -1;  // index into ctx->mods
+};
+struct SingleW {
+  LinW mod, lin1, lin2;
+  const void* qg = nullptr;
+  const void* kg = nullptr;
+  int mod_t = -1;
+};
+struct ModT {
+  const LinW* w;
+  int k;
+  long long off;  // float offset inside one request's modulation row
+};
+constexpr int NSTAGE = 4;
+constexpr int MAXR = 8;  // max ring depth R = D + 1
+}  // namespace
+
+struct ig_mask {
+  int L_img = 0, n_m = 0;
+  int32_t* idx = nullptr;  // device: idx_m at [0, L_img), idx_u at [L_img, 2 L_img), n_m at [2 L_img]
+};
+
+struct ig_cache {
+  ig_model_desc desc{};
+  int n_steps = 0, tier = 0;
+  void* ptr = nullptr;     // pinned host (mapped) or device
+  void* dptr = nullptr;    // device-visible pointer (== ptr with UVA)
+  size_t bytes = 0;
+  mutable std::atomic<int> pins{0};
+  std::atomic<bool> zombie{false};
+  int device = 0;
+};
+
+struct ig_ctx {
+  ig_model_desc d{};
+  ig_ctx_opts o{};
+  int device = 0;
+  size_t esz = 4;
+  int H = 0, F = 0, C = 0, L = 0, Limg = 0, Lt = 0, nb = 0, R = 2;
+  std::vector<const void*> w;
+  LinW img_in, t1, t2, fmod, pout;
+  const void* pos_embed = nullptr;
+  std::vector<StreamW> dimg, dtxt;
+  std::vector<SingleW> sgl;
+  std::vector<ModT> mods;
+  long long mod_ld = 0;
+  int fmod_t = -1;
+  // device buffers
+  float *X = nullptr, *vel = nullptr, *temb = nullptr, *tmp = nullptr, *vec = nullptr,
+        *svec = nullptr, *modbuf = nullptr;
+  void *h = nullptr, *qkv = nullptr, *Q = nullptr, *cat = nullptr, *Ain = nullptr;
+  void* kv_arena = nullptr;
+  long long slot_stride = 0, buf_elems = 0;
+  float2* rope_tab = nullptr;
+  int rope_maxpos = 1;
+  GemvProb *gv_t1 = nullptr, *gv_t2 = nullptr, *gv_mod = nullptr;
+  int gv_mod_groups = 0;
+  std::vector<GemvProb> gv_mod_host;
+  // per-step descriptors: device ring + pinned host staging
+  size_t stage_bytes = 0;
+  char* h_stage[NSTAGE] = {};
+  char* d_stage[NSTAGE] = {};
+  cudaEvent_t ev_stage[NSTAGE] = {};
+  int stage_i = 0;
+  RowInfo* ri = nullptr;
+  // streams / events
+  cudaStream_t copy_st = nullptr;
+  cudaEvent_t ev_copy[MAXR] = {}, ev_comp[MAXR] = {}, ev_desc = nullptr;
+  // explicit prefetch bookkeeping: (slot, layer) -> (cache, step) already in the ring
+  struct Pref { const ig_cache* c = nullptr; int step = -1; };
+  std::vector<Pref> pref;  // [max_batch * R]
+  ig_mask* ones_mask = nullptr;
+  ig_stats stats{};
+  std::vector<ig_cache*> zombies;
+};
+
+// ----------------------------------------------------------------------------------------
+// helpers
+// ----------------------------------------------------------------------------------------
+static bool desc_equal(const ig_model_desc& a, const ig_model_desc& b) {
+  return memcmp(&a, &b, sizeof(a)) == 0;
+}
+
+extern "C" int ig_weight_count(const ig_model_desc* d) {
+  if (!d) return -1;
+  int n = 10 + (d->pos_embed_2d ? 1 : 0);
+  for (int i = 0; i < d->n_double; ++i)
+    for (int s = 0; s < 2; ++s) {
+      bool pre = d->context_pre_only_last && s == 1 && i == d->n_double - 1;
+      n += 4 + (d->qk_norm ? 2 : 0) + (pre ? 0 : 6);
+    }
+  n += d->n_single * (6 + (d->qk_norm ? 2 : 0));
+  return n;
+}
+
+static void free_cache_now(ig_cache* c) {
+  if (!c) return;
+  if (c->ptr) {
+    if (c->tier == IG_CACHE_HOST) cudaFreeHost(c->ptr);
+    else cudaFree(c->ptr);
+  }
+  delete c;
+}
+
+static void reap_zombies(ig_ctx* ctx) {
+  auto& z = ctx->zombies;
+  for (size_t i = 0; i < z.size();) {
+    if (z[i]->pins.load() == 0) {
+      free_cache_now(z[i]);
+      z.erase(z.begin() + i);
+    } else {
+      ++i;
+    }
+  }
+}
+
+static void CUDART_CB unpin_cb(void* p) {
+  ig_cache* c = (ig_cache*)p;
+  c->pins.fetch_sub(1);
+}
+
+// ----------------------------------------------------------------------------------------
+// kernel dispatch by dtype (fp32 parity mode -> CUDA cores; bf16 -> tensor cores)
+// ----------------------------------------------------------------------------------------
+static bool g_tc_gemm = true;   // tcgen05 GEMM for bf16 (set false only by IG_TEST_SIMT)
+static bool g_tc_attn = true;
+
+static void gemm(ig_ctx* ctx, const GemmArgs& g, cudaStream_t st) {
+  if (g.M <= 0 || g.N <= 0) return;
+  ctx->stats.kernel_launches++;
+  if (ctx->d.dtype == IG_F32) launch_gemm_simt<float>(g, st);
+  else if (g_tc_gemm && gemm_tc_supported(g)) launch_gemm_tc(g, st);
+  else launch_gemm_simt<bf16>(g, st);
+}
+
+static void attention(ig_ctx* ctx, const AttnArgs& a, cudaStream_t st) {
+  ctx->stats.kernel_launches++;
+  if (ctx->d.dtype == IG_F32) launch_attn_simt<float>(a, st);
+  else if (g_tc_attn && a.head_dim == 128) launch_attn_tc(a, st);
+  else launch_attn_simt<bf16>(a, st);
+}
+
+// ----------------------------------------------------------------------------------------
+// context
+// ----------------------------------------------------------------------------------------
+static ig_status validate_desc(const ig_model_desc* d) {
+  if (!d) return set_err(IG_EINVAL, "desc is NULL");
+  if (d->hidden <= 0 || d->heads <= 0 || d->head_dim <= 0 || d->hidden != d->heads * d->head_dim)
+    return set_err(IG_EINVAL, "hidden (%d) must equal heads (%d) * head_dim (%d)", d->hidden,
+                   d->heads, d->head_dim);
+  if (d->n_double < 0 || d->n_single < 0 || d->n_double + d->n_single <= 0)
+    return set_err(IG_EINVAL, "need at least one block");
+  if (d->grid_h <= 0 || d->grid_w <= 0 || d->lat_ch <= 0 || d->txt_len < 0 || d->mlp_hidden <= 0)
+    return set_err(IG_EINVAL, "bad grid/lat_ch/txt_len/mlp_hidden");
+  if (d->head_dim != 16 && d->head_dim != 64 && d->head_dim != 128)
+    return set_err(IG_EUNSUPPORTED, "head_dim %d not in {16, 64, 128}", d->head_dim);
+  if (d->hidden % 64 || d->mlp_hidden % 64 || d->lat_ch % 4)
+    return set_err(IG_EUNSUPPORTED, "hidden and mlp_hidden must be multiples of 64, lat_ch of 4");
+  if (d->rope && d->rope_axes[0] + d->rope_axes[1] + d->rope_axes[2] != d->head_dim)
+    return set_err(IG_EINVAL, "rope axes must sum to head_dim");
+  if (d->rope && ((d->rope_axes[0] | d->rope_axes[1] | d->rope_axes[2]) & 1))
+    return set_err(IG_EINVAL, "rope axes must be even");
+  if (d->dtype != IG_F32 && d->dtype != IG_BF16) return set_err(IG_EINVAL, "bad dtype");
+  if (d->context_pre_only_last && d->n_double <= 0)
+    return set_err(IG_EINVAL, "context_pre_only_last needs a double block");
+  return IG_OK;
+}
+
+static ig_status build_rope_table(ig_ctx* ctx) {
+  const ig_model_desc& d = ctx->d;
+  if (!d.rope) return IG_OK;
+  const int P = std::max(1, std::max(d.grid_h, d.grid_w));
+  const int pairs = d.head_dim / 2;
+  std::vector<float2> tab((size_t)pairs * P);
+  int e = 0;
+  for (int a = 0; a < 3; ++a) {
+    const int da = d.rope_axes[a];
+    for (int j = 0; j < da / 2; ++j, ++e) {
+      const double w = std::pow((double)d.rope_theta, -2.0 * j / da);
+      for (int p = 0; p < P; ++p) {
+        const double phi = p * w;
+        tab[(size_t)e * P + p] = make_float2((float)std::cos(phi), (float)std::sin(phi));
+      }
+    }
+  }
+  ctx->rope_maxpos = P;
+  CUDA_TRY(cudaMalloc(&ctx->rope_tab, tab.size() * sizeof(float2)));
+  CUDA_TRY(cudaMemcpy(ctx->rope_tab, tab.data(), tab.size() * sizeof(float2), cudaMemcpyHostToDevice));
+  return IG_OK;
+}
+
+extern "C" void ig_ctx_destroy(ig_ctx* ctx);
+
+extern "C" ig_status ig_ctx_create(const ig_model_desc* desc, const void* const* weights,
+                                   int n_weights, int device, const ig_ctx_opts* opts,
+                                   ig_ctx** out) {
+  if (!out) return set_err(IG_EINVAL, "out is NULL");
+  *out = nullptr;
+  ig_status s = validate_desc(desc);
+  if (s != IG_OK) return s;
+  const int nw = ig_weight_count(desc);
+  if (!weights || n_weights != nw)
+    return set_err(IG_EINVAL, "expected %d weight pointers, got %d", nw, n_weights);
+  for (int i = 0; i < nw; ++i)
+    if (!weights[i]) return set_err(IG_EINVAL, "weight %d is NULL", i);
+  ig_ctx_opts o{8, 0, 2, 0, 0};
+  if (opts) o = *opts;
+  if (o.max_batch <= 0) o.max_batch = 8;
+  if (o.max_batch > 16) return set_err(IG_EUNSUPPORTED, "max_batch > 16");
+  if (o.prefetch_depth <= 0) o.prefetch_depth = 2;
+  if (o.prefetch_depth + 1 > MAXR) return set_err(IG_EUNSUPPORTED, "prefetch_depth > %d", MAXR - 1);
+  if (o.copy_mode != 0 && o.copy_mode != 1) return set_err(IG_EINVAL, "copy_mode must be 0 or 1");
+  const int Lall = desc->txt_len + desc->grid_h * desc->grid_w;
+  if (o.max_rows <= 0) o.max_rows = o.max_batch * Lall;
+
+  CUDA_TRY(cudaSetDevice(device));
+  ig_ctx* ctx = new ig_ctx();
+  ctx->d = *desc;
+  ctx->o = o;
+  ctx->device = device;
+  ctx->esz = desc->dtype == IG_F32 ? 4 : 2;
+  ctx->H = desc->hidden; ctx->F = desc->mlp_hidden; ctx->C = desc->lat_ch;
+  ctx->Limg = desc->grid_h * desc->grid_w; ctx->Lt = desc->txt_len; ctx->L = Lall;
+  ctx->nb = desc->n_double + desc->n_single;
+  ctx->R = o.prefetch_depth + 1;
+  ctx->w.assign(weights, weights + nw);
+  const int H = ctx->H, F = ctx->F, C = ctx->C;
+
+  // resolve the weight table (order documented in ig.h)
+  int k = 0;
+  auto lin = [&](LinW& l, int outd, int ind) { l.w = weights[k++]; l.b = weights[k++]; l.out = outd; l.in = ind; };
+  lin(ctx->img_in, H, C);
+  lin(ctx->t1, H, 256);
+  lin(ctx->t2, H, H);
+  lin(ctx->fmod, 2 * H, H);
+  lin(ctx->pout, C, H);
+  if (desc->pos_embed_2d) ctx->pos_embed = weights[k++];
+  ctx->dimg.resize(desc->n_double);
+  ctx->dtxt.resize(desc->n_double);
+  for (int i = 0; i < desc->n_double; ++i)
+    for (int sidx = 0; sidx < 2; ++sidx) {
+      StreamW& sw = sidx == 0 ? ctx->dimg[i] : ctx->dtxt[i];
+      sw.pre_only = desc->context_pre_only_last && sidx == 1 && i == desc->n_double - 1;
+      lin(sw.mod, (sw.pre_only ? 2 : 6) * H, H);
+      lin(sw.qkv, 3 * H, H);
+      if (desc->qk_norm) { sw.qg = weights[k++]; sw.kg = weights[k++]; }
+      if (!sw.pre_only) { lin(sw.proj, H, H); lin(sw.fc1, F, H); lin(sw.fc2, H, F); }
+    }
+  ctx->sgl.resize(desc->n_single);
+  for (int i = 0; i < desc->n_single; ++i) {
+    SingleW& sw = ctx->sgl[i];
+    lin(sw.mod, 3 * H, H);
+    lin(sw.lin1, 3 * H + F, H);
+    if (desc->qk_norm) { sw.qg = weights[k++]; sw.kg = weights[k++]; }
+    lin(sw.lin2, H, H + F);
+  }
+  // modulation tensors and their offsets inside one request's modulation row
+  auto add_mod = [&](const LinW* l, int kk) {
+    ctx->mods.push_back({l, kk, ctx->mod_ld});
+    ctx->mod_ld += (long long)kk * H;
+    return (int)ctx->mods.size() - 1;
+  };
+  for (int i = 0; i < desc->n_double; ++i) {
+    ctx->dimg[i].mod_t = add_mod(&ctx->dimg[i].mod, 6);
+    if (ctx->Lt > 0) ctx->dtxt[i].mod_t = add_mod(&ctx->dtxt[i].mod, ctx->dtxt[i].pre_only ? 2 : 6);
+  }
+  for (int i = 0; i < desc->n_single; ++i) ctx->sgl[i].mod_t = add_mod(&ctx->sgl[i].mod, 3);
+  ctx->fmod_t = add_mod(&ctx->fmod, 2);
+
+  // workspaces
+  const long long Mx = o.max_rows, B = o.max_batch, es = (long long)ctx->esz;
+  auto dmalloc = [&](void** p, size_t bytes) -> bool { return cudaMalloc(p, std::max<size_t>(bytes, 256)) == cudaSuccess; };
+  bool okm = true;
+  okm &= dmalloc((void**)&ctx->X, Mx * H * 4);
+  okm &= dmalloc((void**)&ctx->vel, Mx * C * 4);
+  okm &= dmalloc((void**)&ctx->temb, B * 256 * 4);
+  okm &= dmalloc((void**)&ctx->tmp, B * H * 4);
+  okm &= dmalloc((void**)&ctx->vec, B * H * 4);
+  okm &= dmalloc((void**)&ctx->svec, B * H * 4);
+  okm &= dmalloc((void**)&ctx->modbuf, B * ctx->mod_ld * 4);
+  okm &= dmalloc(&ctx->h, Mx * H * es);
+  okm &= dmalloc(&ctx->qkv, Mx * 3 * H * es);
+  okm &= dmalloc(&ctx->Q, Mx * H * es);
+  okm &= dmalloc(&ctx->cat, Mx * (H + F) * es);
+  okm &= dmalloc(&ctx->Ain, Mx * C * es);
+  okm &= dmalloc((void**)&ctx->ri, Mx * sizeof(RowInfo));
+  ctx->buf_elems = 2LL * ctx->L * H;
+  ctx->slot_stride = ctx->buf_elems * ctx->R;
+  okm &= dmalloc(&ctx->kv_arena, (size_t)(B * ctx->slot_stride * es));
+  if (!okm) { ig_ctx_destroy(ctx); return set_err(IG_ENOMEM, "workspace allocation failed"); }
+  cudaMemset(ctx->kv_arena, 0, (size_t)(B * ctx->slot_stride * es));
+  cudaMemset(ctx->X, 0, Mx * H * 4);
+  if ((s = build_rope_table(ctx)) != IG_OK) { ig_ctx_destroy(ctx); return s; }
+
+  // static GEMV problem lists (a3)
+  std::vector<GemvProb> p1(1), p2(1);
+  p1[0] = GemvProb{ctx->t1.w, ctx->t1.b, ctx->temb, ctx->tmp, nullptr, H, 256, 256, H, 0, 1, 0};
+  p2[0] = GemvProb{ctx->t2.w, ctx->t2.b, ctx->tmp, ctx->vec, nullptr, H, H, H, H, 0, 0, 0};
+  constexpr int ROWS_PER_GROUP = 32;
+  int groups = 0;
+  for (auto& m : ctx->mods) {
+    GemvProb g{m.w->w, m.w->b, ctx->svec, ctx->modbuf + m.off, nullptr, m.k * H, H, H,
+               (int)ctx->mod_ld, 0, 0, groups};
+    groups += (g.N + ROWS_PER_GROUP - 1) / ROWS_PER_GROUP;
+    ctx->gv_mod_host.push_back(g);
+  }
+  ctx->gv_mod_groups = groups;
+  okm &= dmalloc((void**)&ctx->gv_t1, sizeof(GemvProb));
+  okm &= dmalloc((void**)&ctx->gv_t2, sizeof(GemvProb));
+  okm &= dmalloc((void**)&ctx->gv_mod, ctx->gv_mod_host.size() * sizeof(GemvProb));
+  if (!okm) { ig_ctx_destroy(ctx); return set_err(IG_ENOMEM, "workspace allocation failed"); }
+  cudaMemcpy(ctx->gv_t1, p1.data(), sizeof(GemvProb), cudaMemcpyHostToDevice);
+  cudaMemcpy(ctx->gv_t2, p2.data(), sizeof(GemvProb), cudaMemcpyHostToDevice);
+  cudaMemcpy(ctx->gv_mod, ctx->gv_mod_host.data(), ctx->gv_mod_host.size() * sizeof(GemvProb),
+             cudaMemcpyHostToDevice);
+
+  // per-step descriptor staging: ReqDev[B] + AttnSeg[2B] + KvGatherReq[nb * B]
+  ctx->stage_bytes = B * sizeof(ReqDev) + 2 * B * sizeof(AttnSeg) + (size_t)ctx->nb * B * sizeof(KvGatherReq) + 1024;
+  for (int i = 0; i < NSTAGE; ++i) {
+    if (cudaHostAlloc((void**)&ctx->h_stage[i], ctx->stage_bytes, cudaHostAllocDefault) != cudaSuccess ||
+        cudaMalloc((void**)&ctx->d_stage[i], ctx->stage_bytes) != cudaSuccess) {
+      ig_ctx_destroy(ctx);
+      return set_err(IG_ENOMEM, "staging allocation failed");
+    }
+    cudaEventCreateWithFlags(&ctx->ev_stage[i], cudaEventDisableTiming);
+  }
+  cudaStreamCreateWithFlags(&ctx->copy_st, cudaStreamNonBlocking);
+  for (int i = 0; i < MAXR; ++i) {
+    cudaEventCreateWithFlags(&ctx->ev_copy[i], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&ctx->ev_comp[i], cudaEventDisableTiming);
+  }
+  cudaEventCreateWithFlags(&ctx->ev_desc, cudaEventDisableTiming);
+  ctx->pref.assign((size_t)B * ctx->R, ig_ctx::Pref{});
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) { ig_ctx_destroy(ctx); return set_err(IG_ECUDA, "ctx init: %s", cudaGetErrorString(e)); }
+  *out = ctx;
+  return IG_OK;
+}
+
+extern "C" void ig_ctx_destroy(ig_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  cudaDeviceSynchronize();
+  for (auto* z : ctx->zombies) free_cache_now(z);
+  void* bufs[] = {ctx->X, ctx->vel, ctx->temb, ctx->tmp, ctx->vec, ctx->svec, ctx->modbuf, ctx->h,
+                  ctx->qkv, ctx->Q, ctx->cat, ctx->Ain, ctx->ri, ctx->kv_arena, ctx->rope_tab,
+                  ctx->gv_t1, ctx->gv_t2, ctx->gv_mod};
+  for (void* b : bufs) if (b) cudaFree(b);
+  for (int i = 0; i < NSTAGE; ++i) {
+    if (ctx->h_stage[i]) cudaFreeHost(ctx->h_stage[i]);
+    if (ctx->d_stage[i]) cudaFree(ctx->d_stage[i]);
+    if (ctx->ev_stage[i]) cudaEventDestroy(ctx->ev_stage[i]);
+  }
+  for (int i = 0; i < MAXR; ++i) {
+    if (ctx->ev_copy[i]) cudaEventDestroy(ctx->ev_copy[i]);
+    if (ctx->ev_comp[i]) cudaEventDestroy(ctx->ev_comp[i]);
+  }
+  if (ctx->ev_desc) cudaEventDestroy(ctx->ev_desc);
+  if (ctx->copy_st) cudaStreamDestroy(ctx->copy_st);
+  if (ctx->ones_mask) { cudaFree(ctx->ones_mask->idx); delete ctx->ones_mask; }
+  delete ctx;
+}
+
+extern "C" ig_status ig_last_stats(const ig_ctx* ctx, ig_stats* out) {
+  if (!ctx || !out) return set_err(IG_EINVAL, "NULL argument");
+  *out = ctx->stats;
+  return IG_OK;
+}
+
+// ----------------------------------------------------------------------------------------
+// masks (a1): kernel (a) builds idx_m / idx_u on the device; n_m comes back with one sync
+// at admission (CS5), never on the step path.
+// ----------------------------------------------------------------------------------------
+extern "C" ig_status ig_mask_build(ig_ctx* ctx, const uint8_t* mask, void* stream, ig_mask** out,
+                                   int* n_masked) {
+  if (!ctx || !mask || !out) return set_err(IG_EINVAL, "NULL argument");
+  *out = nullptr;
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  ig_mask* m = new ig_mask();
+  m->L_img = ctx->Limg;
+  if (cudaMalloc(&m->idx, (2 * ctx->Limg + 1) * sizeof(int32_t)) != cudaSuccess) {
+    delete m;
+    return set_err(IG_ENOMEM, "mask index allocation failed");
+  }
+  launch_mask_index(mask, ctx->Limg, m->idx, m->idx + ctx->Limg, m->idx + 2 * ctx->Limg, st);
+  int32_t n = 0;
+  cudaError_t e = cudaMemcpyAsync(&n, m->idx + 2 * ctx->Limg, sizeof(int32_t), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) {
+    cudaFree(m->idx);
+    delete m;
+    return set_err(IG_ECUDA, "mask build: %s", cudaGetErrorString(e));
+  }
+  m->n_m = n;
+  if (n_masked) *n_masked = n;
+  *out = m;
+  return IG_OK;
+}
+
+extern "C" ig_status ig_mask_indices(const ig_mask* m, const int32_t** idx_m, const int32_t** idx_u,
+                                     int* n_m) {
+  if (!m) return set_err(IG_EINVAL, "mask is NULL");
+  if (idx_m) *idx_m = m->idx;
+  if (idx_u) *idx_u = m->idx + m->L_img;
+  if (n_m) *n_m = m->n_m;
+  return IG_OK;
+}
+
+extern "C" void ig_mask_free(ig_mask* m) {
+  if (!m) return;
+  cudaFree(m->idx);
+  delete m;
+}
+
+static ig_status get_ones_mask(ig_ctx* ctx, ig_mask** out) {
+  if (!ctx->ones_mask) {
+    uint8_t* ones = nullptr;
+    CUDA_TRY(cudaMalloc(&ones, ctx->Limg));
+    CUDA_TRY(cudaMemset(ones, 1, ctx->Limg));
+    ig_status s = ig_mask_build(ctx, ones, nullptr, &ctx->ones_mask, nullptr);
+    cudaFree(ones);
+    if (s != IG_OK) return s;
+  }
+  *out = ctx->ones_mask;
+  return IG_OK;
+}
+
+// ----------------------------------------------------------------------------------------
+// caches
+// ----------------------------------------------------------------------------------------
+static size_t cache_bytes(const ig_ctx* ctx, int n_steps) {
+  return (size_t)n_steps * ctx->nb * 2 * ctx->Limg * ctx->H * ctx->esz;
+}
+
+extern "C" ig_status ig_cache_create(ig_ctx* ctx, int n_steps, int tier, ig_cache** out) {
+  if (!ctx || !out) return set_err(IG_EINVAL, "NULL argument");
+  *out = nullptr;
+  if (n_steps <= 0) return set_err(IG_EINVAL, "n_steps must be positive");
+  if (tier != IG_CACHE_HOST && tier != IG_CACHE_DEVICE) return set_err(IG_EINVAL, "bad tier");
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  ig_cache* c = new ig_cache();
+  c->desc = ctx->d;
+  c->n_steps = n_steps;
+  c->tier = tier;
+  c->device = ctx->device;
+  c->bytes = cache_bytes(ctx, n_steps);
+  cudaError_t e;
+  if (tier == IG_CACHE_HOST) {
+    e = cudaHostAlloc(&c->ptr, c->bytes, cudaHostAllocMapped | cudaHostAllocPortable);
+    if (e == cudaSuccess) e = cudaHostGetDevicePointer(&c->dptr, c->ptr, 0);
+  } else {
+    e = cudaMalloc(&c->ptr, c->bytes);
+    c->dptr = c->ptr;
+  }
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    if (c->ptr) { if (tier == IG_CACHE_HOST) cudaFreeHost(c->ptr); else cudaFree(c->ptr); }
+    delete c;
+    return set_err(IG_ENOMEM, "cache allocation of %zu bytes failed: %s", cache_bytes(ctx, n_steps),
+                   cudaGetErrorString(e));
+  }
+  *out = c;
+  return IG_OK;
+}
+
+extern "C" ig_status ig_cache_storage(ig_cache* c, void** ptr, size_t* bytes, int* tier) {
+  if (!c) return set_err(IG_EINVAL, "cache is NULL");
+  if (ptr) *ptr = c->ptr;
+  if (bytes) *bytes = c->bytes;
+  if (tier) *tier = c->tier;
+  return IG_OK;
+}
+
+static std::mutex g_zombie_mu;
+static std::vector<ig_cache*> g_zombies;  // caches freed while pinned (no ctx at hand)
+
+extern "C" void ig_cache_free(ig_cache* c) {
+  if (!c) return;
+  std::lock_guard<std::mutex> lk(g_zombie_mu);
+  // reap earlier zombies whose pins dropped
+  for (size_t i = 0; i < g_zombies.size();) {
+    if (g_zombies[i]->pins.load() == 0) { free_cache_now(g_zombies[i]); g_zombies.erase(g_zombies.begin() + i); }
+    else ++i;
+  }
+  if (c->pins.load() == 0) free_cache_now(c);
+  else { c->zombie = true; g_zombies.push_back(c); }
+}
+
+// ----------------------------------------------------------------------------------------
+// the step
+// ----------------------------------------------------------------------------------------
+struct StepReq {
+  const ig_edit_req* r;
+  const ig_mask* m;
+  bool use_cache;
+};
+
+// Enqueue the cached K/V of block b for every cache-using request into ring buffer b % R.
+static void issue_copy(ig_ctx* ctx, const std::vector<StepReq>& sr, const KvGatherReq* kvg_dev,
+                       const std::vector<KvGatherReq>& kvg_host, int b, bool any_cache,
+                       int max_nu) {
+  if (!any_cache) return;
+  const int buf = b % ctx->R;
+  cudaStreamWaitEvent(ctx->copy_st, ctx->ev_comp[buf], 0);
+  const int n = (int)sr.size();
+  if (ctx->o.copy_mode == 1) {
+    ctx->stats.kernel_launches++;
+    launch_kv_gather(kvg_dev + (size_t)b * n, n, max_nu, ctx->Lt, ctx->H, (int)ctx->esz, ctx->copy_st);
+    for (int q = 0; q < n; ++q)
+      if (sr[q].use_cache) {
+        const long long by = 2LL * kvg_host[(size_t)b * n + q].n_u * ctx->H * ctx->esz;
+        if (sr[q].r->cache->tier == IG_CACHE_HOST) ctx->stats.h2d_bytes += by; else ctx->stats.d2d_bytes += by;
+      }
+  } else {
+    const size_t plane = (size_t)ctx->Limg * ctx->H * ctx->esz;
+    for (int q = 0; q < n; ++q) {
+      if (!sr[q].use_cache) continue;
+      const ig_edit_req* r = sr[q].r;
+      const int slot = r->slot;
+      auto& pf = ctx->pref[(size_t)slot * ctx->R + buf];
+      const bool prefetched = (pf.c == r->cache && pf.step == r->step && b < ctx->R);
+      pf = ig_ctx::Pref{};
+      if (prefetched) continue;
+      const char* src = (const char*)r->cache->ptr + ((size_t)r->step * ctx->nb + b) * 2 * plane;
+      char* dst = (char*)ctx->kv_arena + ((size_t)slot * ctx->slot_stride + (size_t)buf * ctx->buf_elems) * ctx->esz;
+      const size_t txt_off = (size_t)ctx->Lt * ctx->H * ctx->esz;
+      const size_t vplane = (size_t)ctx->L * ctx->H * ctx->esz;
+      cudaMemcpyAsync(dst + txt_off, src, plane, cudaMemcpyDefault, ctx->copy_st);
+      cudaMemcpyAsync(dst + vplane + txt_off, src + plane, plane, cudaMemcpyDefault, ctx->copy_st);
+      if (r->cache->tier == IG_CACHE_HOST) ctx->stats.h2d_bytes += 2 * plane; else ctx->stats.d2d_bytes += 2 * plane;
+    }
+  }
+  cudaEventRecord(ctx->ev_copy[buf], ctx->copy_st);
+}
+
+template <typename T>
+static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStream_t st,
+                          ig_cache* record, int record_step) {
+  const int H = ctx->H, F = ctx->F, C = ctx->C, Lt = ctx->Lt, nb = ctx->nb, R = ctx->R;
+  const long long es = (long long)ctx->esz;
+  ctx->stats = ig_stats{};
+  // ---- host validation (nothing enqueued before this passes) ----
+  if (n < 0 || n > ctx->o.max_batch) return set_err(IG_EINVAL, "n=%d outside [0, max_batch=%d]", n, ctx->o.max_batch);
+  if (n > 0 && !reqs) return set_err(IG_EINVAL, "reqs is NULL");
+  std::vector<StepReq> sr;
+  unsigned slots_seen = 0;
+  for (int i = 0; i < n; ++i) {
+    const ig_edit_req& r = reqs[i];
+    if (r.slot < 0 || r.slot >= ctx->o.max_batch) return set_err(IG_EINVAL, "req %d: slot %d out of range", i, r.slot);
+    if (slots_seen & (1u << r.slot)) return set_err(IG_EINVAL, "req %d: duplicate slot %d", i, r.slot);
+    slots_seen |= 1u << r.slot;
+    if (!r.mask || !r.latent || !r.cond_vec || (Lt > 0 && !r.txt))
+      return set_err(IG_EINVAL, "req %d: NULL mask/latent/txt/cond_vec", i);
+    if (r.mask->L_img != ctx->Limg) return set_err(IG_EINVAL, "req %d: mask built for another model", i);
+    const int nm = r.mask->n_m;
+    if (nm == 0) continue;  // nothing to compute, latent stays bit-identical
+    const bool need = nm < ctx->Limg;
+    if (need) {
+      if (!r.cache) return set_err(IG_ECACHE_MISS, "req %d: 0 < n_m=%d < L_img and no cache (S:134)", i, nm);
+      if (!desc_equal(r.cache->desc, ctx->d)) return set_err(IG_ECACHE_INCOMPAT, "req %d: cache built for another model", i);
+      if (r.step < 0 || r.step >= r.cache->n_steps)
+        return set_err(IG_ECACHE_INCOMPAT, "req %d: step %d outside the cache schedule [0, %d)", i, r.step, r.cache->n_steps);
+      if (r.cache->zombie) return set_err(IG_EINVAL, "req %d: cache was freed", i);
+    }
+    sr.push_back({&r, r.mask, need});
+  }
+  const int na = (int)sr.size();
+  if (na == 0) return IG_OK;
+  const int M_txt = na * Lt;
+  int M = M_txt;
+  bool any_cache = false;
+  int max_nu = 0;
+  for (auto& s : sr) {
+    M += s.m->n_m;
+    any_cache |= s.use_cache;
+    if (s.use_cache) max_nu = std::max(max_nu, ctx->Limg - s.m->n_m);
+  }
+  if (M > ctx->o.max_rows) return set_err(IG_ENOMEM, "step needs %d rows > max_rows %d", M, ctx->o.max_rows);
+  const int M_img = M - M_txt;
+  ctx->stats.rows = M;
+
+  // ---- descriptors -> pinned staging -> device (one small H2D) ----
+  const int si = ctx->stage_i;
+  ctx->stage_i = (si + 1) % NSTAGE;
+  CUDA_TRY(cudaEventSynchronize(ctx->ev_stage[si]));  // the step that used this slot is done
+  char* hs = ctx->h_stage[si];
+  char* ds = ctx->d_stage[si];
+  ReqDev* hreq = (ReqDev*)hs;
+  AttnSeg* hseg = (AttnSeg*)(hs + ctx->o.max_batch * sizeof(ReqDev));
+  KvGatherReq* hkvg = (KvGatherReq*)((char*)hseg + 2 * ctx->o.max_batch * sizeof(AttnSeg));
+  ReqDev* dreq = (ReqDev*)ds;
+  AttnSeg* dseg = (AttnSeg*)(ds + ctx->o.max_batch * sizeof(ReqDev));
+  KvGatherReq* dkvg = (KvGatherReq*)((char*)dseg + 2 * ctx->o.max_batch * sizeof(AttnSeg));
+  int nseg = 0, max_q = 0;
+  int img_row = M_txt;
+  for (int q = 0; q < na; ++q) {
+    const ig_edit_req* r = sr[q].r;
+    ReqDev& d = hreq[q];
+    d.slot = r->slot;
+    d.n_m = sr[q].m->n_m;
+    d.txt_row0 = q * Lt;
+    d.img_row0 = img_row;
+    d.idx_m = sr[q].m->idx;
+    d.idx_u = sr[q].m->idx + ctx->Limg;
+    d.latent = r->latent;
+    d.txt = r->txt;
+    d.cond = r->cond_vec;
+    d.sigma = r->sigma;
+    d.dsig = r->sigma_next - r->sigma;
+    d.has_cache = sr[q].use_cache;
+    const long long kvb = (long long)r->slot * ctx->slot_stride;
+    if (Lt > 0) { hseg[nseg++] = AttnSeg{q * Lt, Lt, kvb}; max_q = std::max(max_q, Lt); }
+    hseg[nseg++] = AttnSeg{img_row, d.n_m, kvb};
+    max_q = std::max(max_q, d.n_m);
+    img_row += d.n_m;
+  }
+  std::vector<KvGatherReq> kvg_host;
+  if (any_cache && ctx->o.copy_mode == 1) {
+    kvg_host.resize((size_t)nb * na);
+    const size_t plane = (size_t)ctx->Limg * H;
+    for (int b = 0; b < nb; ++b)
+      for (int q = 0; q < na; ++q) {
+        KvGatherReq g{};
+        const ig_edit_req* r = sr[q].r;
+        if (sr[q].use_cache) {
+          const char* base = (const char*)r->cache->dptr + (((size_t)r->step * nb + b) * 2 * plane) * es;
+          g.srcK = base;
+          g.srcV = base + plane * es;
+          g.idx_u = sr[q].m->idx + ctx->Limg;
+          g.n_u = ctx->Limg - sr[q].m->n_m;
+          char* dst = (char*)ctx->kv_arena + ((size_t)r->slot * ctx->slot_stride + (size_t)(b % R) * ctx->buf_elems) * es;
+          g.dstK = dst;
+          g.dstV = dst + (size_t)ctx->L * H * es;
+        }
+        kvg_host[(size_t)b * na + q] = g;
+        hkvg[(size_t)b * na + q] = g;
+      }
+  }
+  const size_t desc_bytes = (char*)(hkvg + (any_cache && ctx->o.copy_mode == 1 ? (size_t)nb * na : 0)) - hs;
+  CUDA_TRY(cudaMemcpyAsync(ds, hs, desc_bytes, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaEventRecord(ctx->ev_desc, st));
+  if (any_cache) CUDA_TRY(cudaStreamWaitEvent(ctx->copy_st, ctx->ev_desc, 0));
+  for (auto& s : sr) if (s.use_cache) { s.r->cache->pins.fetch_add(1); }
+
+  // ---- prefetch the first R blocks (copy lane) ----
+  for (int b = 0; b < std::min(R, nb); ++b) issue_copy(ctx, sr, dkvg, kvg_host, b, any_cache, max_nu);
+
+  T* h = (T*)ctx->h;
+  T* qkv = (T*)ctx->qkv;
+  T* cat = (T*)ctx->cat;
+  const long long ldcat = H + F;
+  auto& stats = ctx->stats;
+
+  // ---- a2/a4: rows + gather; a3: conditioning ----
+  launch_build_rows<T>(dreq, na, Lt, C, H, M_txt, M, ctx->ri, ctx->X, (T*)ctx->Ain, st);
+  launch_timestep_embed(dreq, na, ctx->temb, st);
+  launch_gemv<T>(ctx->gv_t1, 1, (H + 31) / 32, na, 256, st);
+  launch_gemv<T>(ctx->gv_t2, 1, (H + 31) / 32, na, H, st);
+  launch_add_cond(dreq, na, H, ctx->vec, st);
+  launch_silu(ctx->vec, ctx->svec, (long long)na * H, st);
+  launch_gemv<T>(ctx->gv_mod, (int)ctx->gv_mod_host.size(), ctx->gv_mod_groups, na, H, st);
+  stats.kernel_launches += 7;
+  {  // img_in (+ SD3 pos_embed) into the fp32 residual X
+    GemmArgs g{};
+    g.A = ctx->Ain; g.lda = C; g.B = ctx->img_in.w; g.ldb = C; g.bias = ctx->img_in.b;
+    g.C = ctx->X + (long long)M_txt * H; g.ldc = H; g.M = M_img; g.N = H; g.K = C;
+    g.epi = EPI_POS; g.ri = ctx->ri; g.ri_off = M_txt; g.pos = ctx->pos_embed; g.pos_ld = H;
+    gemm(ctx, g, st);
+  }
+  const float* mod = ctx->modbuf;
+  const long long mld = ctx->mod_ld;
+  auto ln_mod = [&](int r0, int r1, int mod_t, int shift_c, int scale_c) {
+    if (r1 <= r0) return;
+    const long long off = ctx->mods[mod_t].off;
+    launch_ln_mod<T>(ctx->X, H, r0, r1, ctx->ri, mod + off, (int)mld, shift_c * H, scale_c * H,
+                     ctx->d.ln_eps, h, H, st);
+    stats.kernel_launches++;
+  };
+  auto gemm_rows = [&](int r0, int r1, const void* A, long long lda, const void* B, const void* bias,
+                       int N, int K, void* Cp, long long ldc, int epi, const float* gate, int out_f32) {
+    if (r1 <= r0) return;
+    GemmArgs g{};
+    g.A = (const char*)A + (long long)r0 * lda * es; g.lda = lda;
+    g.B = B; g.ldb = K; g.bias = bias;
+    g.M = r1 - r0; g.N = N; g.K = K; g.epi = epi; g.out_f32 = out_f32;
+    g.ri = ctx->ri; g.ri_off = r0;
+    if (epi == EPI_GATED_RES) {
+      g.C = (float*)Cp + (long long)r0 * ldc; g.gate = gate; g.gate_ld = mld;
+    } else {
+      g.C = (char*)Cp + (long long)r0 * ldc * (out_f32 ? 4 : es);
+    }
+    g.ldc = ldc;
+    gemm(ctx, g, st);
+  };
+  auto qkv_post = [&](int r0, int r1, const void* qg, const void* kg, int buf) {
+    if (r1 <= r0) return;
+    QkvPost p{};
+    p.qkv = qkv; p.ld_qkv = 3 * H; p.Q = ctx->Q; p.kv_arena = ctx->kv_arena;
+    p.slot_stride = ctx->slot_stride; p.buf_off = (long long)buf * ctx->buf_elems;
+    p.L = ctx->L; p.H = H; p.qg = qg; p.kg = kg; p.rope_tab = ctx->rope_tab;
+    p.rope_maxpos = ctx->rope_maxpos;
+    p.ax1_pair = ctx->d.rope_axes[0] / 2; p.ax2_pair = (ctx->d.rope_axes[0] + ctx->d.rope_axes[1]) / 2;
+    p.heads = ctx->d.heads; p.head_dim = ctx->d.head_dim; p.grid_w = ctx->d.grid_w;
+    p.qk_norm = ctx->d.qk_norm; p.rope = ctx->d.rope; p.r0 = r0; p.r1 = r1;
+    launch_qkv_post<T>(p, ctx->ri, st);
+    stats.kernel_launches++;
+  };
+  auto attn = [&](int buf) {
+    AttnArgs a{};
+    a.Q = ctx->Q; a.ldq = H; a.O = cat; a.ldo = ldcat; a.kv_arena = ctx->kv_arena;
+    a.kv_off = (long long)buf * ctx->buf_elems; a.segs = dseg; a.nseg = nseg; a.max_qlen = max_q;
+    a.L = ctx->L; a.heads = ctx->d.heads; a.head_dim = ctx->d.head_dim;
+    a.scale = 1.0f / sqrtf((float)ctx->d.head_dim);
+    attention(ctx, a, st);
+  };
+  // cache recording (template mode): image-token K/V of ring buffer -> cache[s][b]
+  auto record_kv = [&](int b, int buf) {
+    if (!record) return;
+    cudaEventRecord(ctx->ev_comp[buf], st);
+    cudaStreamWaitEvent(ctx->copy_st, ctx->ev_comp[buf], 0);
+    const size_t plane = (size_t)ctx->Limg * H * es;
+    char* dst = (char*)record->ptr + ((size_t)record_step * nb + b) * 2 * plane;
+    const char* src = (const char*)ctx->kv_arena + ((size_t)sr[0].r->slot * ctx->slot_stride + (size_t)buf * ctx->buf_elems) * es;
+    const size_t txt_off = (size_t)Lt * H * es;
+    const size_t vplane = (size_t)ctx->L * H * es;
+    cudaMemcpyAsync(dst, src + txt_off, plane, cudaMemcpyDefault, ctx->copy_st);
+    cudaMemcpyAsync(dst + plane, src + vplane + txt_off, plane, cudaMemcpyDefault, ctx->copy_st);
+    if (record->tier == IG_CACHE_HOST) stats.d2h_bytes += 2 * plane; else stats.d2d_bytes += 2 * plane;
+    cudaEventRecord(ctx->ev_copy[buf], ctx->copy_st);
+  };
+  auto wait_copy = [&](int buf) {
+    if (any_cache || record) cudaStreamWaitEvent(st, ctx->ev_copy[buf], 0);
+  };
+
+  // ---- blocks ----
+  for (int b = 0; b < nb; ++b) {
+    const int buf = b % R;
+    if (b < ctx->d.n_double) {
+      const StreamW& wi = ctx->dimg[b];
+      const StreamW& wt = ctx->dtxt[b];
+      ln_mod(M_txt, M, wi.mod_t, 0, 1);
+      if (Lt) ln_mod(0, M_txt, wt.mod_t, wt.pre_only ? 1 : 0, wt.pre_only ? 0 : 1);
+      gemm_rows(M_txt, M, h, H, wi.qkv.w, wi.qkv.b, 3 * H, H, qkv, 3 * H, EPI_STORE, nullptr, 0);
+      if (Lt) gemm_rows(0, M_txt, h, H, wt.qkv.w, wt.qkv.b, 3 * H, H, qkv, 3 * H, EPI_STORE, nullptr, 0);
+      wait_copy(buf);
+      qkv_post(M_txt, M, wi.qg, wi.kg, buf);
+      if (Lt) qkv_post(0, M_txt, wt.qg, wt.kg, buf);
+      attn(buf);
+      record_kv(b, buf);
+      cudaEventRecord(ctx->ev_comp[buf], st);
+      if (b + R < nb) issue_copy(ctx, sr, dkvg, kvg_host, b + R, any_cache, max_nu);
+      const long long gi = ctx->mods[wi.mod_t].off;
+      gemm_rows(M_txt, M, cat, ldcat, wi.proj.w, wi.proj.b, H, H, ctx->X, H, EPI_GATED_RES, mod + gi + 2 * H, 0);
+      ln_mod(M_txt, M, wi.mod_t, 3, 4);
+      gemm_rows(M_txt, M, h, H, wi.fc1.w, wi.fc1.b, F, H, cat + H, ldcat, EPI_GELU, nullptr, 0);
+      gemm_rows(M_txt, M, cat + H, ldcat, wi.fc2.w, wi.fc2.b, H, F, ctx->X, H, EPI_GATED_RES, mod + gi + 5 * H, 0);
+      if (Lt && !wt.pre_only) {
+        const long long gt = ctx->mods[wt.mod_t].off;
+        gemm_rows(0, M_txt, cat, ldcat, wt.proj.w, wt.proj.b, H, H, ctx->X, H, EPI_GATED_RES, mod + gt + 2 * H, 0);
+        ln_mod(0, M_txt, wt.mod_t, 3, 4);
+        gemm_rows(0, M_txt, h, H, wt.fc1.w, wt.fc1.b, F, H, cat + H, ldcat, EPI_GELU, nullptr, 0);
+        gemm_rows(0, M_txt, cat + H, ldcat, wt.fc2.w, wt.fc2.b, H, F, ctx->X, H, EPI_GATED_RES, mod + gt + 5 * H, 0);
+      }
+    } else {
+      const SingleW& ws = ctx->sgl[b - ctx->d.n_double];
+      ln_mod(0, M, ws.mod_t, 0, 1);
+      gemm_rows(0, M, h, H, ws.lin1.w, ws.lin1.b, 3 * H, H, qkv, 3 * H, EPI_STORE, nullptr, 0);
+      const char* w_u = (const char*)ws.lin1.w + 3LL * H * H * es;
+      const char* b_u = (const char*)ws.lin1.b + 3LL * H * es;
+      gemm_rows(0, M, h, H, w_u, b_u, F, H, cat + H, ldcat, EPI_GELU, nullptr, 0);
+      wait_copy(buf);
+      qkv_post(0, M, ws.qg, ws.kg, buf);
+      attn(buf);
+      record_kv(b, buf);
+      cudaEventRecord(ctx->ev_comp[buf], st);
+      if (b + R < nb) issue_copy(ctx, sr, dkvg, kvg_host, b + R, any_cache, max_nu);
+      const long long gs = ctx->mods[ws.mod_t].off;
+      gemm_rows(0, M, cat, ldcat, ws.lin2.w, ws.lin2.b, H, H + F, ctx->X, H, EPI_GATED_RES, mod + gs + 2 * H, 0);
+    }
+  }
+  // ---- a11: final layer + Euler scatter ----
+  ln_mod(M_txt, M, ctx->fmod_t, 1, 0);  // final chunk order (scale, shift)
+  gemm_rows(M_txt, M, h, H, ctx->pout.w, ctx->pout.b, C, H, ctx->vel - (long long)M_txt * C, C, EPI_STORE, nullptr, 1);
+  launch_scatter_euler(dreq, na, M_img, ctx->ri, M_txt, C, ctx->vel, st);
+  stats.kernel_launches++;
+  // the copy lane must not run ahead into the next step's buffers before compute is done
+  CUDA_TRY(cudaEventRecord(ctx->ev_stage[si], st));
+  for (auto& s : sr)
+    if (s.use_cache) CUDA_TRY(cudaLaunchHostFunc(st, unpin_cb, (void*)s.r->cache));
+  if (record) CUDA_TRY(cudaStreamWaitEvent(st, ctx->ev_copy[(nb - 1) % R], 0));
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_err(IG_ECUDA, "step enqueue: %s", cudaGetErrorString(e));
+  return IG_OK;
+}
+
+static ig_status step_dispatch(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStream_t st,
+                               ig_cache* record, int record_step) {
+  if (ctx->d.dtype == IG_F32) return run_step<float>(ctx, reqs, n, st, record, record_step);
+  return run_step<bf16>(ctx, reqs, n, st, record, record_step);
+}
+
+extern "C" ig_status ig_edit_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, void* stream) {
+  if (!ctx) return set_err(IG_EINVAL, "ctx is NULL");
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  reap_zombies(ctx);
+  ig_status s = step_dispatch(ctx, reqs, n, (cudaStream_t)stream, nullptr, 0);
+  if (s == IG_OK && ctx->o.debug_checks) {
+    CUDA_TRY(cudaStreamSynchronize((cudaStream_t)stream));
+    for (int i = 0; i < n; ++i) {
+      std::vector<float> lat((size_t)ctx->Limg * ctx->C);
+      CUDA_TRY(cudaMemcpy(lat.data(), reqs[i].latent, lat.size() * 4, cudaMemcpyDeviceToHost));
+      for (float v : lat)
+        if (!std::isfinite(v)) return set_err(IG_ENUMERIC, "req %d: non-finite latent after step", i);
+    }
+  }
+  return s;
+}
+
+extern "C" ig_status ig_cache_template(ig_ctx* ctx, float* latent, const void* txt, const float* cond_vec,
+                                       const float* sigmas, int n_steps, int tier, void* stream,
+                                       ig_cache** out) {
+  if (!ctx || !latent || !cond_vec || !sigmas || !out || (ctx->Lt > 0 && !txt))
+    return set_err(IG_EINVAL, "NULL argument");
+  *out = nullptr;
+  if (n_steps <= 0) return set_err(IG_EINVAL, "n_steps must be positive");
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  ig_mask* ones = nullptr;
+  ig_status s = get_ones_mask(ctx, &ones);
+  if (s != IG_OK) return s;
+  ig_cache* c = nullptr;
+  if ((s = ig_cache_create(ctx, n_steps, tier, &c)) != IG_OK) return s;
+  cudaStream_t st = (cudaStream_t)stream;
+  ig_stats total{};
+  for (int k = 0; k < n_steps; ++k) {
+    ig_edit_req r{};
+    r.slot = 0; r.latent = latent; r.mask = ones; r.cache = nullptr; r.step = k;
+    r.sigma = sigmas[k]; r.sigma_next = sigmas[k + 1]; r.txt = txt; r.cond_vec = cond_vec;
+    s = step_dispatch(ctx, &r, 1, st, c, k);
+    if (s != IG_OK) { free_cache_now(c); return s; }
+    total.kernel_launches += ctx->stats.kernel_launches;
+    total.d2h_bytes += ctx->stats.d2h_bytes;
+    total.d2d_bytes += ctx->stats.d2d_bytes;
+    total.rows += ctx->stats.rows;
+  }
+  cudaError_t e = cudaStreamSynchronize(st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->copy_st);
+  if (e != cudaSuccess) { free_cache_now(c); return set_err(IG_ECUDA, "cache_template: %s", cudaGetErrorString(e)); }
+  ctx->stats = total;
+  *out = c;
+  return IG_OK;
+}
+
+extern "C" ig_status ig_prefetch_layer(ig_ctx* ctx, const ig_edit_req* r, int layer) {
+  if (!ctx || !r) return set_err(IG_EINVAL, "NULL argument");
+  if (layer < 0 || layer >= ctx->nb) return set_err(IG_EINVAL, "layer %d out of range", layer);
+  if (layer >= ctx->R) return set_err(IG_EINVAL, "layer %d beyond the ring depth %d", layer, ctx->R);
+  if (r->slot < 0 || r->slot >= ctx->o.max_batch) return set_err(IG_EINVAL, "slot out of range");
+  if (!r->cache) return set_err(IG_ECACHE_MISS, "no cache");
+  if (!desc_equal(r->cache->desc, ctx->d)) return set_err(IG_ECACHE_INCOMPAT, "cache built for another model");
+  if (r->step < 0 || r->step >= r->cache->n_steps) return set_err(IG_ECACHE_INCOMPAT, "step out of range");
+  if (ctx->o.copy_mode != 0) return set_err(IG_EUNSUPPORTED, "explicit prefetch needs copy_mode 0");
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  const int buf = layer % ctx->R;
+  const size_t es = ctx->esz, H = ctx->H;
+  const size_t plane = (size_t)ctx->Limg * H * es;
+  CUDA_TRY(cudaStreamWaitEvent(ctx->copy_st, ctx->ev_comp[buf], 0));
+  const char* src = (const char*)r->cache->ptr + ((size_t)r->step * ctx->nb + layer) * 2 * plane;
+  char* dst = (char*)ctx->kv_arena + ((size_t)r->slot * ctx->slot_stride + (size_t)buf * ctx->buf_elems) * es;
+  const size_t txt_off = (size_t)ctx->Lt * H * es, vplane = (size_t)ctx->L * H * es;
+  CUDA_TRY(cudaMemcpyAsync(dst + txt_off, src, plane, cudaMemcpyDefault, ctx->copy_st));
+  CUDA_TRY(cudaMemcpyAsync(dst + vplane + txt_off, src + plane, plane, cudaMemcpyDefault, ctx->copy_st));
+  CUDA_TRY(cudaEventRecord(ctx->ev_copy[buf], ctx->copy_st));
+  ctx->pref[(size_t)r->slot * ctx->R + buf] = ig_ctx::Pref{r->cache, r->step};
+  return IG_OK;
+}
+
+// ----------------------------------------------------------------------------------------
+// per-kernel ops (include/ig_ops.h)
+// ----------------------------------------------------------------------------------------
+extern "C" ig_status ig_op_gemm(int dtype, const void* A, long long lda, const void* B, long long ldb,
+                                const void* bias, void* Cp, long long ldc, int M, int N, int K, int epi,
+                                int out_f32, void* stream) {
+  if (!A || !B || !Cp) return set_err(IG_EINVAL, "NULL argument");
+  if (M < 0 || N <= 0 || K <= 0) return set_err(IG_EINVAL, "bad shape");
+  if (epi != EPI_STORE && epi != EPI_GELU) return set_err(IG_EINVAL, "ig_op_gemm: epi must be 0 or 1");
+  GemmArgs g{};
+  g.A = A; g.lda = lda; g.B = B; g.ldb = ldb; g.bias = bias; g.C = Cp; g.ldc = ldc;
+  g.M = M; g.N = N; g.K = K; g.epi = epi; g.out_f32 = out_f32;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (dtype == IG_F32) launch_gemm_simt<float>(g, st);
+  else if (dtype == IG_BF16) {
+    if (!gemm_tc_supported(g)) return set_err(IG_EUNSUPPORTED, "shape not supported by the tcgen05 GEMM");
+    launch_gemm_tc(g, st);
+  } else return set_err(IG_EINVAL, "bad dtype");
+  CUDA_TRY(cudaGetLastError());
+  return IG_OK;
+}
+
+extern "C" ig_status ig_op_attention(int dtype, const void* Q, long long ldq, void* O, long long ldo,
+                                     const void* kv, const int32_t* segs, int nseg, int L, int heads,
+                                     int head_dim, void* stream) {
+  if (!Q || !O || !kv || !segs || nseg <= 0 || L <= 0 || heads <= 0) return set_err(IG_EINVAL, "bad argument");
+  if (head_dim != 16 && head_dim != 64 && head_dim != 128) return set_err(IG_EUNSUPPORTED, "head_dim");
+  std::vector<AttnSeg> hs(nseg);
+  int maxq = 0;
+  const long long H = (long long)heads * head_dim;
+  for (int i = 0; i < nseg; ++i) {
+    hs[i] = AttnSeg{segs[3 * i], segs[3 * i + 1], (long long)segs[3 * i + 2] * 2 * L * H};
+    if (hs[i].q_len < 0 || hs[i].q_start < 0) return set_err(IG_EINVAL, "bad segment");
+    maxq = std::max(maxq, hs[i].q_len);
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  AttnSeg* dsegs = nullptr;
+  CUDA_TRY(cudaMallocAsync((void**)&dsegs, nseg * sizeof(AttnSeg), st));
+  CUDA_TRY(cudaMemcpyAsync(dsegs, hs.data(), nseg * sizeof(AttnSeg), cudaMemcpyHostToDevice, st));
+  AttnArgs a{};
+  a.Q = Q; a.ldq = ldq; a.O = O; a.ldo = ldo; a.kv_arena = kv; a.kv_off = 0; a.segs = dsegs;
+  a.nseg = nseg; a.max_qlen = maxq; a.L = L; a.heads = heads; a.head_dim = head_dim;
+  a.scale = 1.0f / sqrtf((float)head_dim);
+  if (dtype == IG_F32) launch_attn_simt<float>(a, st);
+  else if (dtype == IG_BF16) {
+    if (g_tc_attn && head_dim == 128) launch_attn_tc(a, st);
+    else launch_attn_simt<bf16>(a, st);
+  } else return set_err(IG_EINVAL, "bad dtype");
+  CUDA_TRY(cudaFreeAsync(dsegs, st));
+  CUDA_TRY(cudaStreamSynchronize(st));  // host segment vector lifetime
+  CUDA_TRY(cudaGetLastError());
+  return IG_OK;
+}
+
+extern "C" ig_status ig_copy(void* dst, const void* src, size_t bytes, void* stream) {
+  if ((!dst || !src) && bytes) return set_err(IG_EINVAL, "NULL argument");
+  cudaStream_t st = (cudaStream_t)stream;
+  CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return IG_OK;
+}

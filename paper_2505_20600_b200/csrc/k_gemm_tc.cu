@@ -1,0 +1,301 @@
+// k_gemm_tc.cu — kernel (c): persistent tcgen05/TMEM/TMA tensor-core GEMM, bf16 in, fp32
+// accumulate, with the step's fused epilogues (bias, GELU-tanh, gated residual into the fp32
+// residual stream, positional-embedding add).  C[M,N] = A[M,K] B[N,K]^T: the masked-row
+// projections / MLP of the mask-aware step (P:384-386 token-wise ops on masked rows only;
+// Table 1 rows XW and (XW1)W2).
+//
+// Structure (one CTA per SM, persistent over output tiles, static round-robin schedule):
+//   warp 0      TMA producer: A tile [128 x 64] and B tile [BN x 64] per stage, SWIZZLE_128B
+//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer (M=128, N=BN, K=16)
+//   warps 4..7  epilogue: tcgen05.ld (thread = output row) -> epilogue math -> global stores
+// Pipelines: smem full/empty mbarriers (TMA <-> MMA), TMEM full/empty (MMA <-> epilogue) with
+// a double-buffered accumulator so tile i's epilogue overlaps tile i+1's mainloop.
+// Fixed tile shape and K order independent of M: batch-invariant (SURVEY §8(c) bitwise
+// requirement 1).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <mutex>
+#include "kernels.h"
+#include "tc_common.cuh"
+
+namespace ig {
+
+namespace {
+constexpr int BM = 128, BK = 64;
+constexpr int NUM_THREADS = 256;
+
+template <int BN>
+struct Cfg {
+  static constexpr int STAGES = BN == 256 ? 4 : 6;
+  static constexpr int A_BYTES = BM * BK * 2;
+  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int TMEM_COLS = 2 * BN;  // double-buffered fp32 accumulator
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+};
+
+// epilogue for one 32-column chunk of one row held in registers
+template <int BN>
+__device__ __forceinline__ void epilogue_chunk(const GemmArgs& g, int row, int col0, const uint32_t (&r)[32],
+                                               const RowInfo* info) {
+  float v[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+  const bf16* bias = reinterpret_cast<const bf16*>(g.bias);
+  const bool full = col0 + 32 <= g.N;
+  if (bias) {
+    if (full) {
+      const uint4* b4 = reinterpret_cast<const uint4*>(bias + col0);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        uint4 u = b4[q];
+        const bf16* hb = reinterpret_cast<const bf16*>(&u);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) v[q * 8 + e] += __bfloat162float(hb[e]);
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 32; ++i)
+        if (col0 + i < g.N) v[i] += __bfloat162float(bias[col0 + i]);
+    }
+  }
+  switch (g.epi) {
+    case EPI_GELU:
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] = gelu_tanh(v[i]);
+      // fallthrough
+    case EPI_STORE: {
+      if (g.out_f32) {
+        float* c = reinterpret_cast<float*>(g.C) + (long long)row * g.ldc + col0;
+        if (full) {
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            reinterpret_cast<float4*>(c)[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+        } else {
+          for (int i = 0; i < 32; ++i)
+            if (col0 + i < g.N) c[i] = v[i];
+        }
+      } else {
+        bf16* c = reinterpret_cast<bf16*>(g.C) + (long long)row * g.ldc + col0;
+        if (full) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            uint4 u;
+            uint32_t* w = reinterpret_cast<uint32_t*>(&u);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              __nv_bfloat162 p = __floats2bfloat162_rn(v[q * 8 + 2 * e], v[q * 8 + 2 * e + 1]);
+              w[e] = *reinterpret_cast<uint32_t*>(&p);
+            }
+            reinterpret_cast<uint4*>(c)[q] = u;
+          }
+        } else {
+          for (int i = 0; i < 32; ++i)
+            if (col0 + i < g.N) c[i] = __float2bfloat16_rn(v[i]);
+        }
+      }
+      break;
+    }
+    case EPI_GATED_RES: {
+      float* x = reinterpret_cast<float*>(g.C) + (long long)row * g.ldc + col0;
+      const float* gt = g.gate + (long long)info->req * g.gate_ld + col0;
+      if (full) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          float4 xv = reinterpret_cast<float4*>(x)[q];
+          float4 gv = reinterpret_cast<const float4*>(gt)[q];
+          xv.x += gv.x * v[4 * q];
+          xv.y += gv.y * v[4 * q + 1];
+          xv.z += gv.z * v[4 * q + 2];
+          xv.w += gv.w * v[4 * q + 3];
+          reinterpret_cast<float4*>(x)[q] = xv;
+        }
+      } else {
+        for (int i = 0; i < 32; ++i)
+          if (col0 + i < g.N) x[i] += gt[i] * v[i];
+      }
+      break;
+    }
+    case EPI_POS: {
+      float* x = reinterpret_cast<float*>(g.C) + (long long)row * g.ldc + col0;
+      const bf16* pos = g.pos ? reinterpret_cast<const bf16*>(g.pos) + (long long)info->tok * g.pos_ld + col0 : nullptr;
+      for (int i = 0; i < 32; ++i)
+        if (col0 + i < g.N) x[i] = v[i] + (pos ? __bfloat162float(pos[i]) : 0.f);
+      break;
+    }
+  }
+}
+
+template <int BN>
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   const GemmArgs g, int num_m, int num_n) {
+  using C = Cfg<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + C::STAGES * C::A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
+  uint64_t* empty = full + C::STAGES;
+  uint64_t* tfull = empty + C::STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int num_tiles = num_m * num_n;
+  const int num_k = (g.K + BK - 1) / BK;
+
+  if (warp == 0 && lane == 0) {
+    tc::tma_prefetch_desc(&tmA);
+    tc::tma_prefetch_desc(&tmB);
+    for (int s = 0; s < C::STAGES; ++s) {
+      tc::mbar_init(&full[s], 1);
+      tc::mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      tc::mbar_init(&tfull[a], 1);
+      tc::mbar_init(&tempty[a], 4);
+    }
+    tc::fence_barrier_init();
+  }
+  if (warp == 1) tc::tmem_alloc<C::TMEM_COLS>(tmem_slot);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ===== TMA producer =====
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        const int m0 = (t / num_n) * BM, n0 = (t % num_n) * BN;
+        for (int kb = 0; kb < num_k; ++kb) {
+          tc::mbar_wait(&empty[stage], phase ^ 1);
+          tc::mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
+          tc::tma_load_2d(sA + stage * C::A_BYTES, &tmA, &full[stage], kb * BK, m0);
+          tc::tma_load_2d(sB + stage * C::B_BYTES, &tmB, &full[stage], kb * BK, n0);
+          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ===== MMA issuer =====
+      constexpr uint32_t idesc = tc::idesc_bf16(BM, BN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        tc::mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc::tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < num_k; ++kb) {
+          tc::mbar_wait(&full[stage], phase);
+          tc::tc_fence_after();
+          const uint32_t a_addr = tc::smem_u32(sA + stage * C::A_BYTES);
+          const uint32_t b_addr = tc::smem_u32(sB + stage * C::B_BYTES);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            const uint64_t ad = tc::sdesc_sw128(a_addr + k * 32, 16, 1024);
+            const uint64_t bd = tc::sdesc_sw128(b_addr + k * 32, 16, 1024);
+            tc::mma_bf16_ss(d_tmem, ad, bd, idesc, (kb | k) != 0);
+          }
+          tc::mma_commit(&empty[stage]);
+          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+        }
+        tc::mma_commit(&tfull[acc]);
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      }
+    }
+  } else if (warp >= 4) {  // ===== epilogue =====
+    const int quad = warp & 3;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      const int m0 = (t / num_n) * BM, n0 = (t % num_n) * BN;
+      tc::mbar_wait(&tfull[acc], acc_phase);
+      tc::tc_fence_after();
+      const int row = m0 + quad * 32 + lane;
+      RowInfo info{0, 0, 0, 0};
+      if (row < g.M && g.ri && (g.epi == EPI_GATED_RES || g.epi == EPI_POS)) info = g.ri[g.ri_off + row];
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 32) {
+        uint32_t r[32];
+        tc::tmem_ld32(tmem_base + ((uint32_t)(quad * 32) << 16) + acc * BN + c, r);
+        tc::tmem_ld_wait();
+        if (row < g.M && n0 + c < g.N) epilogue_chunk<BN>(g, row, n0 + c, r, &info);
+      }
+      tc::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&tempty[acc]);
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+    }
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tc::tmem_dealloc<C::TMEM_COLS>(tmem_base);
+}
+
+// ---- host side -----------------------------------------------------------------------------
+PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+std::once_flag g_encode_once;
+int g_num_sms = 0;
+
+void init_driver() {
+  std::call_once(g_encode_once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+    g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaFuncSetAttribute(gemm_tc_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<256>::SMEM);
+    cudaFuncSetAttribute(gemm_tc_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<128>::SMEM);
+  });
+}
+
+// 2-D bf16 tensor map over a row-major [rows, cols] matrix with leading dimension ld, box
+// [box_rows, 64 cols], 128-byte swizzle; out-of-bounds reads fill zeros.
+bool make_tmap(CUtensorMap* m, const void* ptr, long long rows, long long cols, long long ld, int box_rows) {
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * 2)};
+  cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+}  // namespace
+
+bool gemm_tc_supported(const GemmArgs& g) {
+  auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  if (!al16(g.A) || !al16(g.B) || (g.lda & 7) || (g.ldb & 7) || (g.K & 7)) return false;
+  if (g.epi == EPI_STORE || g.epi == EPI_GELU) {
+    if (!al16(g.C) || (g.ldc & (g.out_f32 ? 3 : 7))) return false;
+  } else {
+    if (!al16(g.C) || (g.ldc & 3)) return false;
+    if (g.epi == EPI_GATED_RES && (!al16(g.gate) || (g.gate_ld & 3))) return false;
+  }
+  if (g.bias && !al16(g.bias)) return false;
+  return true;
+}
+
+void launch_gemm_tc(const GemmArgs& g, cudaStream_t st) {
+  if (g.M <= 0 || g.N <= 0) return;
+  init_driver();
+  const bool wide = g.N > 128;
+  const int BN = wide ? 256 : 128;
+  CUtensorMap ta, tb;
+  make_tmap(&ta, g.A, g.M, g.K, g.lda, BM);
+  make_tmap(&tb, g.B, g.N, g.K, g.ldb, BN);
+  const int num_m = (g.M + BM - 1) / BM, num_n = (g.N + BN - 1) / BN;
+  const int tiles = num_m * num_n;
+  const int grid = tiles < g_num_sms ? tiles : g_num_sms;
+  if (wide) gemm_tc_kernel<256><<<grid, NUM_THREADS, Cfg<256>::SMEM, st>>>(ta, tb, g, num_m, num_n);
+  else gemm_tc_kernel<128><<<grid, NUM_THREADS, Cfg<128>::SMEM, st>>>(ta, tb, g, num_m, num_n);
+}
+
+}  // namespace ig

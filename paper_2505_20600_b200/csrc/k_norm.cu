@@ -1,0 +1,205 @@
+// k_norm.cu — conditioning (a3) and the LN + modulate prologue (a5).  All HBM-bound.
+#include "kernels.h"
+
+namespace ig {
+
+// ======================================================================================
+// a3: sinusoid(1000 sigma) [cos | sin], f_k = exp(-ln(1e4) k / 128) (C-ALG 2, cos first).
+// Arguments up to 1000 rad: computed in double, rounded once to fp32.
+// ======================================================================================
+__global__ void temb_kernel(const ReqDev* __restrict__ reqs, int n, float* __restrict__ temb) {
+  const int r = blockIdx.x, k = threadIdx.x;  // 128 threads
+  if (r >= n) return;
+  const double t = 1000.0 * (double)reqs[r].sigma;
+  const double f = exp(-9.210340371976184 * (double)k / 128.0);  // ln(10000)
+  temb[r * 256 + k] = (float)cos(t * f);
+  temb[r * 256 + 128 + k] = (float)sin(t * f);
+}
+
+void launch_timestep_embed(const ReqDev* reqs, int n, float* temb, cudaStream_t st) {
+  temb_kernel<<<n, 128, 0, st>>>(reqs, n, temb);
+}
+
+__global__ void silu_kernel(const float* __restrict__ x, float* __restrict__ y, long long count) {
+  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < count) y[i] = silu(x[i]);
+}
+void launch_silu(const float* x, float* y, long long count, cudaStream_t st) {
+  silu_kernel<<<(unsigned)((count + 255) / 256), 256, 0, st>>>(x, y, count);
+}
+
+__global__ void add_cond_kernel(const ReqDev* __restrict__ reqs, int H, float* __restrict__ vec) {
+  const int r = blockIdx.y;
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c < H) vec[(long long)r * H + c] += reqs[r].cond[c];
+}
+void launch_add_cond(const ReqDev* reqs, int n, int H, float* vec, cudaStream_t st) {
+  dim3 grid((H + 255) / 256, n);
+  add_cond_kernel<<<grid, 256, 0, st>>>(reqs, H, vec);
+}
+
+// ======================================================================================
+// Batched GEMV over a problem list (one launch for all blocks' modulation vectors):
+// y[r][j] = x[r] . W[j] + b[j] (+ addv[r][j]) (optional SiLU), r < n (requests).
+// Each warp owns 4 output rows j; x chunks staged in shared memory and shared by the
+// CTA's 8 warps; weights streamed with 16-byte loads (HBM-bound: 6.5 GB/step for Flux).
+// ======================================================================================
+constexpr int GV_ROWS_PER_WARP = 4, GV_WARPS = 8, GV_KCH = 512, GV_MAXN = 16;
+
+template <typename T> struct Vec8;
+template <> struct Vec8<bf16> {
+  static __device__ __forceinline__ void load(const bf16* p, float* out) {
+    int4 v = *reinterpret_cast<const int4*>(p);
+    const bf16* h = reinterpret_cast<const bf16*>(&v);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) out[i] = __bfloat162float(h[i]);
+  }
+};
+template <> struct Vec8<float> {
+  static __device__ __forceinline__ void load(const float* p, float* out) {
+    float4 a = *reinterpret_cast<const float4*>(p);
+    float4 b = *reinterpret_cast<const float4*>(p + 4);
+    out[0] = a.x; out[1] = a.y; out[2] = a.z; out[3] = a.w;
+    out[4] = b.x; out[5] = b.y; out[6] = b.z; out[7] = b.w;
+  }
+};
+
+template <typename T>
+__global__ void __launch_bounds__(GV_WARPS * 32) gemv_kernel(const GemvProb* __restrict__ probs,
+                                                             int nprob, int n) {
+  __shared__ float xs[GV_MAXN][GV_KCH];
+  // locate the problem of this CTA (groups of GV_WARPS*GV_ROWS_PER_WARP rows)
+  const int g = blockIdx.x;
+  int pi = 0;
+  while (pi + 1 < nprob && probs[pi + 1].row_group0 <= g) ++pi;
+  const GemvProb P = probs[pi];
+  const int row0 = (g - P.row_group0) * GV_WARPS * GV_ROWS_PER_WARP;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int jbase = row0 + warp * GV_ROWS_PER_WARP;
+  const T* W = reinterpret_cast<const T*>(P.W);
+  float acc[GV_ROWS_PER_WARP][GV_MAXN];
+#pragma unroll
+  for (int a = 0; a < GV_ROWS_PER_WARP; ++a)
+#pragma unroll
+    for (int r = 0; r < GV_MAXN; ++r) acc[a][r] = 0.f;
+  for (int k0 = 0; k0 < P.K; k0 += GV_KCH) {
+    const int kc = min(GV_KCH, P.K - k0);
+    __syncthreads();
+    for (int i = threadIdx.x; i < n * GV_KCH; i += blockDim.x) {
+      const int r = i / GV_KCH, k = i % GV_KCH;
+      xs[r][k] = (k < kc) ? P.x[(long long)r * P.ldx + k0 + k] : 0.f;
+    }
+    __syncthreads();
+    // lane handles 8-element chunks c = lane, lane+32, ... (kc multiple of 8)
+    for (int c = lane * 8; c < kc; c += 256) {
+      float w[GV_ROWS_PER_WARP][8];
+#pragma unroll
+      for (int a = 0; a < GV_ROWS_PER_WARP; ++a) {
+        const int j = jbase + a;
+        if (j < P.N) Vec8<T>::load(W + (long long)j * P.K + k0 + c, w[a]);
+        else {
+#pragma unroll
+          for (int e = 0; e < 8; ++e) w[a][e] = 0.f;
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < GV_MAXN; ++r) {
+        if (r < n) {
+          float xv[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) xv[e] = xs[r][c + e];
+#pragma unroll
+          for (int a = 0; a < GV_ROWS_PER_WARP; ++a)
+#pragma unroll
+            for (int e = 0; e < 8; ++e) acc[a][r] = fmaf(w[a][e], xv[e], acc[a][r]);
+        }
+      }
+    }
+  }
+  const T* bias = reinterpret_cast<const T*>(P.b);
+#pragma unroll
+  for (int a = 0; a < GV_ROWS_PER_WARP; ++a) {
+    const int j = jbase + a;
+#pragma unroll
+    for (int r = 0; r < GV_MAXN; ++r) {
+      if (r < n) {
+        float s = warp_sum(acc[a][r]);
+        if (lane == 0 && j < P.N) {
+          if (bias) s += to_f<T>(bias[j]);
+          if (P.addv) s += P.addv[(long long)r * P.ldadd + j];
+          if (P.act_out == 1) s = silu(s);
+          P.y[(long long)r * P.ldy + j] = s;
+        }
+      }
+    }
+  }
+}
+
+template <typename T>
+void launch_gemv(const GemvProb* probs_dev, int nprob, int total_groups, int n, int maxK,
+                 cudaStream_t st) {
+  (void)maxK;
+  if (total_groups <= 0) return;
+  gemv_kernel<T><<<total_groups, GV_WARPS * 32, 0, st>>>(probs_dev, nprob, n);
+}
+template void launch_gemv<float>(const GemvProb*, int, int, int, int, cudaStream_t);
+template void launch_gemv<bf16>(const GemvProb*, int, int, int, int, cudaStream_t);
+
+// ======================================================================================
+// a5: h = LN(X)(1 + scale_req) + shift_req, LN without affine, eps (C-AMB 6).  One CTA
+// (128 threads) per row; two-pass mean/variance over the L1-resident fp32 row.
+// ======================================================================================
+template <typename T>
+__global__ void __launch_bounds__(128) ln_mod_kernel(const float* __restrict__ X, int H, int r0,
+                                                     const RowInfo* __restrict__ ri,
+                                                     const float* __restrict__ mod, int mod_ld,
+                                                     int shift_off, int scale_off, float eps,
+                                                     T* __restrict__ h, int ldh) {
+  __shared__ float red[4];
+  const int r = r0 + blockIdx.x;
+  const float* x = X + (long long)r * H;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  float s = 0.f;
+  for (int c = tid * 4; c < H; c += 512) {
+    float4 v = *reinterpret_cast<const float4*>(x + c);
+    s += (v.x + v.y) + (v.z + v.w);
+  }
+  s = warp_sum(s);
+  if (lane == 0) red[wid] = s;
+  __syncthreads();
+  const float mean = (red[0] + red[1] + red[2] + red[3]) / H;
+  __syncthreads();
+  float q = 0.f;
+  for (int c = tid * 4; c < H; c += 512) {
+    float4 v = *reinterpret_cast<const float4*>(x + c);
+    float a = v.x - mean, b = v.y - mean, cc = v.z - mean, d = v.w - mean;
+    q += (a * a + b * b) + (cc * cc + d * d);
+  }
+  q = warp_sum(q);
+  if (lane == 0) red[wid] = q;
+  __syncthreads();
+  const float rstd = 1.0f / sqrtf((red[0] + red[1] + red[2] + red[3]) / H + eps);
+  const float* m = mod + (long long)ri[r].req * mod_ld;
+  T* out = h + (long long)r * ldh;
+  for (int c = tid * 4; c < H; c += 512) {
+    float4 v = *reinterpret_cast<const float4*>(x + c);
+    float4 sc = *reinterpret_cast<const float4*>(m + scale_off + c);
+    float4 sh = *reinterpret_cast<const float4*>(m + shift_off + c);
+    out[c + 0] = from_f<T>((v.x - mean) * rstd * (1.f + sc.x) + sh.x);
+    out[c + 1] = from_f<T>((v.y - mean) * rstd * (1.f + sc.y) + sh.y);
+    out[c + 2] = from_f<T>((v.z - mean) * rstd * (1.f + sc.z) + sh.z);
+    out[c + 3] = from_f<T>((v.w - mean) * rstd * (1.f + sc.w) + sh.w);
+  }
+}
+
+template <typename T>
+void launch_ln_mod(const float* X, int H, int r0, int r1, const RowInfo* ri, const float* mod,
+                   int mod_ld, int shift_off, int scale_off, float eps, T* h, int ldh,
+                   cudaStream_t st) {
+  if (r1 <= r0) return;
+  ln_mod_kernel<T><<<r1 - r0, 128, 0, st>>>(X, H, r0, ri, mod, mod_ld, shift_off, scale_off, eps, h, ldh);
+}
+template void launch_ln_mod<float>(const float*, int, int, int, const RowInfo*, const float*, int, int, int, float, float*, int, cudaStream_t);
+template void launch_ln_mod<bf16>(const float*, int, int, int, const RowInfo*, const float*, int, int, int, float, bf16*, int, cudaStream_t);
+
+}  // namespace ig

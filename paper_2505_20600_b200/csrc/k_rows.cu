@@ -1,0 +1,258 @@
+// k_rows.cu — kernels (a) index build and (b) row gather / positional K/V merge / scatter.
+// All of these are exact copies or integer work (bit-exact, SURVEY §8(c) C-PIN) except the
+// QK-norm/RoPE epilogue, which is token-wise fp arithmetic.
+#include "kernels.h"
+
+namespace ig {
+
+// ======================================================================================
+// (a) mask -> ascending idx_m / idx_u ("extract the matrix of masked tokens";
+//     C-AMB 13-16).  One CTA of 1024 threads; thread t owns a contiguous chunk of tokens;
+//     block-wide exclusive scan of the per-thread masked counts gives each thread its
+//     output base, so both lists come out ascending.  Bit-exact by construction.
+// ======================================================================================
+__global__ void __launch_bounds__(1024) mask_index_kernel(const uint8_t* __restrict__ mask, int L,
+                                                          int32_t* __restrict__ idx_m,
+                                                          int32_t* __restrict__ idx_u,
+                                                          int32_t* __restrict__ n_m_out) {
+  __shared__ int warp_tot[32];
+  __shared__ int carry;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  if (tid == 0) carry = 0;
+  __syncthreads();
+  // process in rounds of 1024 * CH tokens
+  constexpr int CH = 8;
+  for (int base = 0; base < L; base += 1024 * CH) {
+    int beg = base + tid * CH;
+    int cnt = 0;
+    uint8_t mv[CH];
+#pragma unroll
+    for (int j = 0; j < CH; ++j) {
+      int i = beg + j;
+      mv[j] = (i < L) ? (mask[i] != 0) : 0;
+      cnt += mv[j];
+    }
+    // inclusive warp scan
+    int incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    if (lane == 31) warp_tot[wid] = incl;
+    __syncthreads();
+    if (wid == 0) {
+      int t = warp_tot[lane];
+      int ti = t;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        int v = __shfl_up_sync(0xffffffffu, ti, o);
+        if (lane >= o) ti += v;
+      }
+      warp_tot[lane] = ti - t;  // exclusive over warps
+    }
+    __syncthreads();
+    int m_before = carry + warp_tot[wid] + incl - cnt;  // masked tokens before `beg`
+#pragma unroll
+    for (int j = 0; j < CH; ++j) {
+      int i = beg + j;
+      if (i < L) {
+        if (mv[j]) idx_m[m_before++] = i;
+        else idx_u[i - m_before] = i;
+      }
+    }
+    __syncthreads();
+    if (tid == 1023) carry = m_before;  // last thread's running count = carry for next round
+    __syncthreads();
+  }
+  if (tid == 0) *n_m_out = carry;
+}
+
+void launch_mask_index(const uint8_t* mask, int L, int32_t* idx_m, int32_t* idx_u,
+                       int32_t* n_m_dev, cudaStream_t st) {
+  mask_index_kernel<<<1, 1024, 0, st>>>(mask, L, idx_m, idx_u, n_m_dev);
+}
+
+// ======================================================================================
+// a2/a4 batch assembly + entry gather.  Row order (C-AMB 15): all requests'
+// text rows first (request-major), then all masked image rows (request-major, ascending
+// token index).  One warp per packed row.
+// ======================================================================================
+template <typename T>
+__global__ void build_rows_kernel(const ReqDev* __restrict__ reqs, int n, int L_txt, int C,
+                                  int H, int M_txt, int M, RowInfo* __restrict__ ri,
+                                  float* __restrict__ X, T* __restrict__ Ain) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= M) return;
+  const int r = warp;
+  RowInfo info;
+  if (r < M_txt) {
+    const int q = r / L_txt, t = r - q * L_txt;
+    const ReqDev& R = reqs[q];
+    info.req = q; info.slot = R.slot; info.kvpos = t; info.tok = -1;
+    const T* src = reinterpret_cast<const T*>(R.txt) + (long long)t * H;
+    float* dst = X + (long long)r * H;
+    for (int c = lane; c < H; c += 32) dst[c] = to_f<T>(src[c]);
+  } else {
+    int q = 0;
+    while (q + 1 < n && reqs[q + 1].img_row0 <= r) ++q;  // n <= max_batch: linear search
+    const ReqDev& R = reqs[q];
+    const int j = r - R.img_row0;
+    const int tok = R.idx_m[j];
+    info.req = q; info.slot = R.slot; info.kvpos = L_txt + tok; info.tok = tok;
+    const float* src = R.latent + (long long)tok * C;
+    T* dst = Ain + (long long)(r - M_txt) * C;
+    for (int c = lane; c < C; c += 32) dst[c] = from_f<T>(src[c]);
+  }
+  if (lane == 0) ri[r] = info;
+}
+
+template <typename T>
+void launch_build_rows(const ReqDev* reqs, int n, int L_txt, int C, int H, int M_txt, int M,
+                       RowInfo* ri, float* X, T* Ain, cudaStream_t st) {
+  if (M <= 0) return;
+  const int threads = 256;
+  const int blocks = (M * 32 + threads - 1) / threads;
+  build_rows_kernel<T><<<blocks, threads, 0, st>>>(reqs, n, L_txt, C, H, M_txt, M, ri, X, Ain);
+}
+template void launch_build_rows<float>(const ReqDev*, int, int, int, int, int, int, RowInfo*, float*, float*, cudaStream_t);
+template void launch_build_rows<bf16>(const ReqDev*, int, int, int, int, int, int, RowInfo*, float*, bf16*, cudaStream_t);
+
+// ======================================================================================
+// a6 epilogue: per-head RMSNorm (q, k) + RoPE at the ORIGINAL token position (C-AMB 7),
+// q -> packed Q, k/v -> the request's positional K/V buffer row kvpos: the "merge by mask
+// index", fresh half (fig:transformer_alter; C-AMB 8).  One warp per (row, head).
+// ======================================================================================
+template <typename T>
+__global__ void qkv_post_kernel(QkvPost p, const RowInfo* __restrict__ ri) {
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int rows = p.r1 - p.r0;
+  if (gw >= rows * p.heads) return;
+  const int r = p.r0 + gw / p.heads;
+  const int h = gw % p.heads;
+  const int d = p.head_dim;
+  const RowInfo info = ri[r];
+  const T* src = reinterpret_cast<const T*>(p.qkv) + (long long)r * p.ld_qkv;
+  T* Q = reinterpret_cast<T*>(p.Q) + (long long)r * p.H + h * d;
+  T* arena = reinterpret_cast<T*>(p.kv_arena);
+  T* Kdst = arena + info.slot * p.slot_stride + p.buf_off + (long long)info.kvpos * p.H + h * d;
+  T* Vdst = Kdst + p.L * p.H;
+  // positions (C-AMB 7): image token i -> (0, i / W, i % W); text -> (0, 0, 0)
+  int pos1 = 0, pos2 = 0;
+  if (info.tok >= 0) { pos1 = info.tok / p.grid_w; pos2 = info.tok % p.grid_w; }
+  const T* qg = reinterpret_cast<const T*>(p.qg);
+  const T* kg = reinterpret_cast<const T*>(p.kg);
+  // each lane handles pairs (2e, 2e+1) for e = lane, lane+32, ... < d/2
+  for (int which = 0; which < 2; ++which) {  // 0 = q, 1 = k
+    const T* s = src + (long long)which * p.H + h * d;
+    float ss = 0.f;
+    for (int e = lane; e < d / 2; e += 32) {
+      float x0 = to_f<T>(s[2 * e]), x1 = to_f<T>(s[2 * e + 1]);
+      ss += x0 * x0 + x1 * x1;
+    }
+    ss = warp_sum(ss);
+    const float rinv = p.qk_norm ? rsqrtf(ss / d + 1e-6f) : 1.f;
+    const T* g = which == 0 ? qg : kg;
+    T* dst = which == 0 ? Q : Kdst;
+    for (int e = lane; e < d / 2; e += 32) {
+      float x0 = to_f<T>(s[2 * e]), x1 = to_f<T>(s[2 * e + 1]);
+      if (p.qk_norm) {
+        x0 = x0 * rinv * to_f<T>(g[2 * e]);
+        x1 = x1 * rinv * to_f<T>(g[2 * e + 1]);
+      }
+      if (p.rope) {
+        // rope_tab[e][pos] = (cos, sin)(pos * theta^(-2j/d_a)) for pair e = (2e, 2e+1),
+        // j its index inside axis a (host-built in double precision).
+        const int pos = e < p.ax1_pair ? 0 : (e < p.ax2_pair ? pos1 : pos2);
+        const float2 cs = p.rope_tab[(long long)e * p.rope_maxpos + pos];
+        const float y0 = x0 * cs.x - x1 * cs.y;
+        const float y1 = x0 * cs.y + x1 * cs.x;
+        x0 = y0; x1 = y1;
+      }
+      dst[2 * e] = from_f<T>(x0);
+      dst[2 * e + 1] = from_f<T>(x1);
+    }
+  }
+  // v: plain copy
+  const T* sv = src + 2LL * p.H + h * d;
+  for (int c = lane; c < d; c += 32) Vdst[c] = sv[c];
+}
+
+template <typename T>
+void launch_qkv_post(const QkvPost& p, const RowInfo* ri, cudaStream_t st) {
+  const long long warps = (long long)(p.r1 - p.r0) * p.heads;
+  if (warps <= 0) return;
+  const int threads = 256;
+  const long long blocks = (warps * 32 + threads - 1) / threads;
+  qkv_post_kernel<T><<<(unsigned)blocks, threads, 0, st>>>(p, ri);
+}
+template void launch_qkv_post<float>(const QkvPost&, const RowInfo*, cudaStream_t);
+template void launch_qkv_post<bf16>(const QkvPost&, const RowInfo*, cudaStream_t);
+
+// ======================================================================================
+// a7 compacted cache merge, cached half (kernel e, copy lane): rows idx_u of the template's
+// K and V -> ring rows L_txt + idx_u.  The source may be pinned host memory read over the
+// host link (zero-copy, UVA pointer) or HBM.  One warp per (request, unmasked row, K|V);
+// 16-byte vector loads, 4 in flight per lane.
+// ======================================================================================
+__global__ void kv_gather_kernel(const KvGatherReq* __restrict__ reqs, int n, int max_nu,
+                                 int L_txt, int row_bytes) {
+  const long long gw = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const long long per_req = 2LL * max_nu;
+  const int q = (int)(gw / per_req);
+  if (q >= n) return;
+  const int rem = (int)(gw % per_req);
+  const int which = rem & 1, j = rem >> 1;
+  const KvGatherReq& R = reqs[q];
+  if (j >= R.n_u) return;
+  const int tok = R.idx_u[j];
+  const char* src = (const char*)(which ? R.srcV : R.srcK) + (long long)tok * row_bytes;
+  char* dst = (char*)(which ? R.dstV : R.dstK) + (long long)(L_txt + tok) * row_bytes;
+  const int nvec = row_bytes >> 4;
+  const int4* s4 = reinterpret_cast<const int4*>(src);
+  int4* d4 = reinterpret_cast<int4*>(dst);
+  int v = lane;
+  for (; v + 96 < nvec; v += 128) {
+    int4 a = s4[v], b = s4[v + 32], c = s4[v + 64], d = s4[v + 96];
+    d4[v] = a; d4[v + 32] = b; d4[v + 64] = c; d4[v + 96] = d;
+  }
+  for (; v < nvec; v += 32) d4[v] = s4[v];
+}
+
+void launch_kv_gather(const KvGatherReq* reqs_dev, int n, int max_nu, int L_txt, int H,
+                      int elem_bytes, cudaStream_t st) {
+  const long long warps = 2LL * max_nu * n;
+  if (warps <= 0) return;
+  const int threads = 256;
+  const long long blocks = (warps * 32 + threads - 1) / threads;
+  kv_gather_kernel<<<(unsigned)blocks, threads, 0, st>>>(reqs_dev, n, max_nu, L_txt, H * elem_bytes);
+}
+
+// ======================================================================================
+// a11 exit: flow-matching Euler update scattered into the masked latent rows only
+// (C-AMB 11, 12): latent[idx_m[j]] += (sigma_next - sigma) v[j].  Unmasked rows untouched.
+// ======================================================================================
+__global__ void scatter_euler_kernel(const ReqDev* __restrict__ reqs, int M_img,
+                                     const RowInfo* __restrict__ ri, int M_txt, int C,
+                                     const float* __restrict__ v) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (long long)M_img * C) return;
+  const int r = (int)(i / C), c = (int)(i % C);
+  const RowInfo info = ri[M_txt + r];
+  const ReqDev& R = reqs[info.req];
+  float* dst = R.latent + (long long)info.tok * C + c;
+  *dst = *dst + R.dsig * v[i];
+}
+
+void launch_scatter_euler(const ReqDev* reqs, int n, int M_img, const RowInfo* ri, int M_txt,
+                          int C, const float* v, cudaStream_t st) {
+  (void)n;
+  const long long total = (long long)M_img * C;
+  if (total <= 0) return;
+  scatter_euler_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(reqs, M_img, ri, M_txt, C, v);
+}
+
+}  // namespace ig

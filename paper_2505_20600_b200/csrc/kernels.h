@@ -1,0 +1,131 @@
+// kernels.h — host-side launchers of libig's CUDA kernels (internal; not part of the ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include "common.cuh"
+
+namespace ig {
+
+// ---- a1 index build (k_rows.cu) --------------------------------------------------------
+void launch_mask_index(const uint8_t* mask, int L, int32_t* idx_m, int32_t* idx_u,
+                       int32_t* n_m_dev, cudaStream_t st);
+
+// ---- a2/a4 batch assembly + entry gather (k_rows.cu) -------------------------------------
+struct ReqDev {
+  int slot, n_m, txt_row0, img_row0;  // packed-row offsets of this request's segments
+  const int32_t* idx_m;
+  const int32_t* idx_u;
+  float* latent;
+  const void* txt;
+  const float* cond;
+  float sigma, dsig;                  // dsig = sigma_next - sigma
+  int has_cache;
+  int pad;
+};
+// Fills row_info[M] and gathers: X[txt rows] = txt (fp32), Ain[img rows - M_txt] = latent
+// rows at idx_m (as T).  M_txt = n * L_txt.
+template <typename T>
+void launch_build_rows(const ReqDev* reqs, int n, int L_txt, int C, int H, int M_txt, int M,
+                       RowInfo* row_info, float* X, T* Ain, cudaStream_t st);
+
+// ---- a3 conditioning (k_norm.cu) --------------------------------------------------------
+// temb[r][0:256] = [cos(1000 sigma_r f_k) | sin(...)], computed in double, stored as float.
+void launch_timestep_embed(const ReqDev* reqs, int n, float* temb, cudaStream_t st);
+
+struct GemvProb {
+  const void* W;      // [N, K] row-major (T)
+  const void* b;      // [N] (T) or null
+  const float* x;     // [n, K] fp32 input rows (already activated)
+  float* y;           // [n, ldy] fp32 output
+  const float* addv;  // optional [n, ldadd] added after bias (cond_vec)
+  int N, K, ldx, ldy, ldadd, act_out;  // act_out: 0 none, 1 silu
+  int row_group0;     // prefix of row groups (filled by the launcher)
+};
+template <typename T>
+void launch_gemv(const GemvProb* probs_dev, int nprob, int total_groups, int n, int maxK,
+                 cudaStream_t st);
+// y = silu(x) elementwise (fp32), n*H elements
+void launch_silu(const float* x, float* y, long long count, cudaStream_t st);
+// vec[r] += addv per request pointer (cond vectors live in caller buffers)
+void launch_add_cond(const ReqDev* reqs, int n, int H, float* vec, cudaStream_t st);
+
+// ---- a5 LN + modulate (k_norm.cu) -------------------------------------------------------
+// h[r] = LN(X[r]) * (1 + mod[req][scale_off + c]) + mod[req][shift_off + c], rows [r0, r1)
+template <typename T>
+void launch_ln_mod(const float* X, int H, int r0, int r1, const RowInfo* ri, const float* mod,
+                   int mod_ld, int shift_off, int scale_off, float eps, T* h, int ldh,
+                   cudaStream_t st);
+
+// ---- a6 epilogue: QK-norm, RoPE, Q pack, positional K/V merge (k_rows.cu) ---------------
+struct QkvPost {
+  const void* qkv;  int ld_qkv;     // [M, >=3H] rows r0..r1 (T)
+  void* Q;                          // [M, H] packed (T)
+  void* kv_arena;                   // ring arena (T)
+  long long slot_stride, buf_off;   // elements
+  long long L, H;                   // merged length, hidden
+  const void* qg; const void* kg;   // [d] gains (T) or null
+  const float2* rope_tab;           // [d/2 pairs][max_pos] (cos, sin), or null
+  int rope_maxpos, ax1_pair, ax2_pair;  // pair index where axis 1 / axis 2 start
+  int heads, head_dim, grid_w, qk_norm, rope;
+  int r0, r1;
+};
+template <typename T>
+void launch_qkv_post(const QkvPost& p, const RowInfo* ri, cudaStream_t st);
+
+// ---- a7 compacted cache gather (zero-copy, copy lane) (k_rows.cu) -----------------------
+// for each of n requests with cache: rows idx_u of src K and V (host-mapped or device)
+// -> ring rows L_txt + idx_u.
+struct KvGatherReq {
+  const void* srcK; const void* srcV;  // [L_img, H]
+  const int32_t* idx_u; int n_u;
+  void* dstK; void* dstV;              // [L, H] positional ring buffer
+  int pad[2];
+};
+void launch_kv_gather(const KvGatherReq* reqs_dev, int n, int max_nu, int L_txt, int H,
+                      int elem_bytes, cudaStream_t st);
+
+// ---- a11 exit: Euler scatter (k_rows.cu) ------------------------------------------------
+// latent_req[idx_m[j]][c] += dsig_req * v[img_row][c]
+void launch_scatter_euler(const ReqDev* reqs, int n, int M_img, const RowInfo* ri, int M_txt,
+                          int C, const float* v, cudaStream_t st);
+
+// ---- GEMM (k_gemm_simt.cu / k_gemm_tc.cu) -----------------------------------------------
+enum Epi : int {
+  EPI_STORE = 0,      // C = acc + b (TOut)
+  EPI_GELU = 1,       // C = gelu_tanh(acc + b) (TOut)
+  EPI_GATED_RES = 2,  // X[r, c] += gate[req(r)][c] * (acc + b)  (C is fp32 X)
+  EPI_POS = 3,        // X[r, c] = acc + b + pos[tok(r)][c]      (C is fp32 X)
+};
+struct GemmArgs {
+  const void* A; long long lda;   // [M, K] row-major
+  const void* B; long long ldb;   // [N, K] row-major (weights [out, in])
+  const void* bias;               // [N] (same dtype as B) or null
+  void* C; long long ldc;         // output (TOut) or fp32 residual
+  int M, N, K;
+  int epi;
+  const float* gate; long long gate_ld;  // EPI_GATED_RES: mod + gate offset, row stride
+  const RowInfo* ri;                     // row metadata (rows are A-rows offset by ri_off)
+  int ri_off;
+  const void* pos; long long pos_ld;     // EPI_POS table (T)
+  int out_f32;                           // EPI_STORE/GELU: 1 => C is fp32
+};
+template <typename T>
+void launch_gemm_simt(const GemmArgs& g, cudaStream_t st);
+// tcgen05/TMEM/TMA bf16 GEMM (returns false if the shape is unsupported)
+bool gemm_tc_supported(const GemmArgs& g);
+void launch_gemm_tc(const GemmArgs& g, cudaStream_t st);
+
+// ---- a8 attention (k_attn_simt.cu / k_attn_tc.cu) ---------------------------------------
+struct AttnArgs {
+  const void* Q; long long ldq;   // packed [M, H]
+  void* O; long long ldo;         // packed [M, H] (may alias a column block of a wider buf)
+  const void* kv_arena; long long kv_off;  // K at kv_base + kv_off, V at + L*H
+  const AttnSeg* segs; int nseg; int max_qlen;
+  int L, heads, head_dim;
+  float scale;                    // 1/sqrt(d)
+};
+template <typename T>
+void launch_attn_simt(const AttnArgs& a, cudaStream_t st);
+void launch_attn_tc(const AttnArgs& a, cudaStream_t st);
+
+}  // namespace ig

@@ -1,0 +1,216 @@
+"""Thin ctypes binding of libig (include/ig.h, include/ig_ops.h) — argument marshalling only.
+
+Every function has the C name and forwards to libig.so; every step of the hot path runs in
+the library's CUDA kernels.  There is no fallback: if libig.so is missing or fails to load,
+`lib()` raises.  Pointers are plain integers (e.g. torch `tensor.data_ptr()`), streams are
+`torch.cuda.Stream.cuda_stream` integers (0 = legacy default stream).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import List, Optional, Sequence
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libig.so")
+_lib = None
+
+IG_F32, IG_BF16 = 0, 1
+IG_CACHE_HOST, IG_CACHE_DEVICE = 0, 1
+STATUS = {0: "IG_OK", 1: "IG_EINVAL", 2: "IG_ECACHE_INCOMPAT", 3: "IG_ECACHE_MISS",
+          4: "IG_ENUMERIC", 5: "IG_ENOMEM", 6: "IG_ECUDA", 7: "IG_EUNSUPPORTED"}
+
+EXPORTS = ["ig_weight_count", "ig_ctx_create", "ig_ctx_destroy", "ig_cache_create",
+           "ig_cache_template", "ig_cache_storage", "ig_cache_free", "ig_mask_build",
+           "ig_mask_indices", "ig_mask_free", "ig_edit_step", "ig_prefetch_layer",
+           "ig_last_error", "ig_last_stats", "ig_op_gemm", "ig_op_attention", "ig_copy"]
+
+
+class IgError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+        self.name = STATUS.get(status, str(status))
+
+
+class ig_model_desc(ctypes.Structure):
+    _fields_ = [("n_double", ctypes.c_int), ("n_single", ctypes.c_int),
+                ("hidden", ctypes.c_int), ("heads", ctypes.c_int), ("head_dim", ctypes.c_int),
+                ("mlp_hidden", ctypes.c_int), ("lat_ch", ctypes.c_int), ("grid_h", ctypes.c_int),
+                ("grid_w", ctypes.c_int), ("txt_len", ctypes.c_int), ("qk_norm", ctypes.c_int),
+                ("rope", ctypes.c_int), ("rope_axes", ctypes.c_int * 3),
+                ("rope_theta", ctypes.c_float), ("ln_eps", ctypes.c_float),
+                ("pos_embed_2d", ctypes.c_int), ("context_pre_only_last", ctypes.c_int),
+                ("dtype", ctypes.c_int)]
+
+
+class ig_ctx_opts(ctypes.Structure):
+    _fields_ = [("max_batch", ctypes.c_int), ("max_rows", ctypes.c_int),
+                ("prefetch_depth", ctypes.c_int), ("copy_mode", ctypes.c_int),
+                ("debug_checks", ctypes.c_int)]
+
+
+class ig_edit_req(ctypes.Structure):
+    _fields_ = [("slot", ctypes.c_int), ("latent", ctypes.c_void_p), ("mask", ctypes.c_void_p),
+                ("cache", ctypes.c_void_p), ("step", ctypes.c_int), ("sigma", ctypes.c_float),
+                ("sigma_next", ctypes.c_float), ("txt", ctypes.c_void_p),
+                ("cond_vec", ctypes.c_void_p)]
+
+
+class ig_stats(ctypes.Structure):
+    _fields_ = [("kernel_launches", ctypes.c_longlong), ("h2d_bytes", ctypes.c_longlong),
+                ("d2d_bytes", ctypes.c_longlong), ("d2h_bytes", ctypes.c_longlong),
+                ("rows", ctypes.c_longlong)]
+
+
+def lib():
+    """Load libig.so (in-tree).  Raises if it is missing: there is no other path."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"libig.so not built at {LIB_PATH}; run __graft_entry__.build()")
+        L = ctypes.CDLL(LIB_PATH)
+        vp, i, ll = ctypes.c_void_p, ctypes.c_int, ctypes.c_longlong
+        P = ctypes.POINTER
+        L.ig_weight_count.argtypes = [P(ig_model_desc)]
+        L.ig_weight_count.restype = i
+        L.ig_ctx_create.argtypes = [P(ig_model_desc), P(vp), i, i, P(ig_ctx_opts), P(vp)]
+        L.ig_ctx_destroy.argtypes = [vp]
+        L.ig_ctx_destroy.restype = None
+        L.ig_cache_create.argtypes = [vp, i, i, P(vp)]
+        L.ig_cache_template.argtypes = [vp, vp, vp, vp, P(ctypes.c_float), i, i, vp, P(vp)]
+        L.ig_cache_storage.argtypes = [vp, P(vp), P(ctypes.c_size_t), P(i)]
+        L.ig_cache_free.argtypes = [vp]
+        L.ig_cache_free.restype = None
+        L.ig_mask_build.argtypes = [vp, vp, vp, P(vp), P(i)]
+        L.ig_mask_indices.argtypes = [vp, P(vp), P(vp), P(i)]
+        L.ig_mask_free.argtypes = [vp]
+        L.ig_mask_free.restype = None
+        L.ig_edit_step.argtypes = [vp, P(ig_edit_req), i, vp]
+        L.ig_prefetch_layer.argtypes = [vp, P(ig_edit_req), i]
+        L.ig_last_error.restype = ctypes.c_char_p
+        L.ig_last_stats.argtypes = [vp, P(ig_stats)]
+        L.ig_op_gemm.argtypes = [i, vp, ll, vp, ll, vp, vp, ll, i, i, i, i, i, vp]
+        L.ig_op_attention.argtypes = [i, vp, ll, vp, ll, vp, P(ctypes.c_int32), i, i, i, i, vp]
+        L.ig_copy.argtypes = [vp, vp, ctypes.c_size_t, vp]
+        for name in EXPORTS:
+            if name not in ("ig_ctx_destroy", "ig_cache_free", "ig_mask_free", "ig_last_error",
+                            "ig_weight_count"):
+                getattr(L, name).restype = ctypes.c_int
+        _lib = L
+    return _lib
+
+
+def _check(status: int):
+    if status != 0:
+        raise IgError(status, lib().ig_last_error().decode())
+
+
+def make_desc(m, dtype: int) -> ig_model_desc:
+    """Fill ig_model_desc from any object with the ig.h field names as attributes."""
+    d = ig_model_desc()
+    for f, _ in ig_model_desc._fields_:
+        if f == "rope_axes":
+            d.rope_axes = (ctypes.c_int * 3)(*m.rope_axes)
+        elif f == "dtype":
+            d.dtype = dtype
+        else:
+            setattr(d, f, getattr(m, f))
+    return d
+
+
+def ig_weight_count(desc: ig_model_desc) -> int:
+    return lib().ig_weight_count(ctypes.byref(desc))
+
+
+def ig_ctx_create(desc: ig_model_desc, weight_ptrs: Sequence[int], device: int = 0,
+                  opts: Optional[ig_ctx_opts] = None) -> int:
+    arr = (ctypes.c_void_p * len(weight_ptrs))(*weight_ptrs)
+    out = ctypes.c_void_p()
+    _check(lib().ig_ctx_create(ctypes.byref(desc), arr, len(weight_ptrs), device,
+                               ctypes.byref(opts) if opts is not None else None, ctypes.byref(out)))
+    return out.value
+
+
+def ig_ctx_destroy(ctx: int):
+    lib().ig_ctx_destroy(ctx)
+
+
+def ig_mask_build(ctx: int, mask_ptr: int, stream: int = 0):
+    out, n = ctypes.c_void_p(), ctypes.c_int()
+    _check(lib().ig_mask_build(ctx, mask_ptr, stream, ctypes.byref(out), ctypes.byref(n)))
+    return out.value, n.value
+
+
+def ig_mask_indices(mask: int):
+    pm, pu, n = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_int()
+    _check(lib().ig_mask_indices(mask, ctypes.byref(pm), ctypes.byref(pu), ctypes.byref(n)))
+    return pm.value, pu.value, n.value
+
+
+def ig_mask_free(mask: int):
+    lib().ig_mask_free(mask)
+
+
+def ig_cache_create(ctx: int, n_steps: int, tier: int = IG_CACHE_HOST) -> int:
+    out = ctypes.c_void_p()
+    _check(lib().ig_cache_create(ctx, n_steps, tier, ctypes.byref(out)))
+    return out.value
+
+
+def ig_cache_template(ctx: int, latent_ptr: int, txt_ptr: int, cond_ptr: int,
+                      sigmas: Sequence[float], tier: int = IG_CACHE_HOST, stream: int = 0) -> int:
+    s = (ctypes.c_float * len(sigmas))(*[float(x) for x in sigmas])
+    out = ctypes.c_void_p()
+    _check(lib().ig_cache_template(ctx, latent_ptr, txt_ptr, cond_ptr, s, len(sigmas) - 1, tier,
+                                   stream, ctypes.byref(out)))
+    return out.value
+
+
+def ig_cache_storage(cache: int):
+    p, b, t = ctypes.c_void_p(), ctypes.c_size_t(), ctypes.c_int()
+    _check(lib().ig_cache_storage(cache, ctypes.byref(p), ctypes.byref(b), ctypes.byref(t)))
+    return p.value, b.value, t.value
+
+
+def ig_cache_free(cache: int):
+    lib().ig_cache_free(cache)
+
+
+def make_req(slot, latent, mask, cache, step, sigma, sigma_next, txt, cond) -> ig_edit_req:
+    return ig_edit_req(slot, latent, mask, cache or None, step, sigma, sigma_next, txt or None, cond)
+
+
+def ig_edit_step(ctx: int, reqs: List[ig_edit_req], stream: int = 0):
+    arr = (ig_edit_req * max(1, len(reqs)))(*reqs)
+    _check(lib().ig_edit_step(ctx, arr, len(reqs), stream))
+
+
+def ig_prefetch_layer(ctx: int, req: ig_edit_req, layer: int):
+    _check(lib().ig_prefetch_layer(ctx, ctypes.byref(req), layer))
+
+
+def ig_last_error() -> str:
+    return lib().ig_last_error().decode()
+
+
+def ig_last_stats(ctx: int) -> dict:
+    s = ig_stats()
+    _check(lib().ig_last_stats(ctx, ctypes.byref(s)))
+    return {f: getattr(s, f) for f, _ in ig_stats._fields_}
+
+
+def ig_op_gemm(dtype, A, lda, B, ldb, bias, C, ldc, M, N, K, epi=0, out_f32=0, stream=0):
+    _check(lib().ig_op_gemm(dtype, A, lda, B, ldb, bias or None, C, ldc, M, N, K, epi, out_f32,
+                            stream))
+
+
+def ig_op_attention(dtype, Q, ldq, O, ldo, kv, segs, L, heads, head_dim, stream=0):
+    flat = [int(x) for s in segs for x in s]
+    arr = (ctypes.c_int32 * len(flat))(*flat)
+    _check(lib().ig_op_attention(dtype, Q, ldq, O, ldo, kv, arr, len(segs), L, heads, head_dim,
+                                 stream))
+
+
+def ig_copy(dst: int, src: int, nbytes: int, stream: int = 0):
+    _check(lib().ig_copy(dst, src, nbytes, stream))

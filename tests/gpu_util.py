@@ -1,0 +1,89 @@
+"""Helpers for the -m gpu parity tests: build a context from synth weights, run steps
+through the C ABI, and compare with the oracle using C-TOL."""
+import numpy as np
+import torch
+
+import synth
+from paper_2505_20600_b200 import ig
+
+TDT = {ig.IG_F32: torch.float32, ig.IG_BF16: torch.bfloat16}
+
+
+def ctol(g, o, rtol):
+    """C-TOL (SURVEY 8(c) C-AMB 22): |g - o| <= rtol |o| + rtol RMS(o), elementwise."""
+    g = np.asarray(g, np.float64)
+    o = np.asarray(o, np.float64)
+    atol = rtol * np.sqrt(np.mean(o * o)) if o.size else 0.0
+    err = np.abs(g - o)
+    ok = err <= rtol * np.abs(o) + atol
+    worst = float(np.max(err / (rtol * np.abs(o) + atol + 1e-300))) if o.size else 0.0
+    return bool(ok.all()), worst
+
+
+class Model:
+    """Synthetic weights on the device + an ig context."""
+
+    def __init__(self, d, dtype, seed=0, opts=None, device="cuda"):
+        self.d, self.dtype = d, dtype
+        tdt = TDT[dtype]
+        self.W = {}
+        ptrs = []
+        for name, shape, fan_in in synth.weight_table(d):
+            t = synth.make_weight(d, name, shape, fan_in, seed, device, tdt).contiguous()
+            self.W[name] = t
+            ptrs.append(t.data_ptr())
+        self.desc = ig.make_desc(d, dtype)
+        self.ctx = ig.ig_ctx_create(self.desc, ptrs, 0, opts)
+
+    def host_weights(self):
+        return {k: v.double().cpu().numpy() for k, v in self.W.items()}
+
+    def close(self):
+        if self.ctx:
+            ig.ig_ctx_destroy(self.ctx)
+            self.ctx = None
+
+
+class Request:
+    def __init__(self, m, rid, mask_np, device="cuda"):
+        d = m.d
+        self.latent = synth.make_latent(d, rid, device).contiguous()
+        self.latent0 = self.latent.clone()
+        self.txt = synth.make_txt(d, rid, device, TDT[m.dtype]).contiguous()
+        self.cond = synth.make_cond(d, rid, device).contiguous()
+        self.mask_np = mask_np.astype(np.uint8)
+        self.mask_dev = torch.from_numpy(self.mask_np).to(device)
+        self.mask, self.n_m = ig.ig_mask_build(m.ctx, self.mask_dev.data_ptr(), 0)
+
+    def req(self, slot, cache, step, sigma, sigma_next):
+        return ig.make_req(slot, self.latent.data_ptr(), self.mask, cache, step, sigma, sigma_next,
+                           self.txt.data_ptr() if self.txt.numel() else None, self.cond.data_ptr())
+
+    def host_inputs(self):
+        return (self.latent0.double().cpu().numpy(), self.txt.double().cpu().numpy(),
+                self.cond.double().cpu().numpy())
+
+    def free(self):
+        ig.ig_mask_free(self.mask)
+
+
+def cache_to_numpy(cache, d, n_steps, dtype):
+    ptr, nbytes, tier = ig.ig_cache_storage(cache)
+    shape = (n_steps, d.n_blocks, 2, d.L_img, d.hidden)
+    assert tier == ig.IG_CACHE_HOST, 'host-tier readback only'
+    import ctypes
+    buf = (ctypes.c_char * nbytes).from_address(ptr)
+    raw = np.frombuffer(buf, dtype=np.uint8).copy()
+    if dtype == ig.IG_F32:
+        return raw.view(np.float32).reshape(shape).astype(np.float64)
+    u16 = raw.view(np.uint16).astype(np.uint32) << 16
+    return u16.view(np.float32).reshape(shape).astype(np.float64)
+
+
+def fill_cache(cache, kv: torch.Tensor):
+    """Copy a synthetic cache tensor [steps, blocks, 2, L_img, H] into library storage."""
+    ptr, nbytes, tier = ig.ig_cache_storage(cache)
+    src = kv.contiguous().cpu()
+    assert src.numel() * src.element_size() == nbytes
+    import ctypes
+    ctypes.memmove(ptr, src.data_ptr(), nbytes)

@@ -1,0 +1,202 @@
+"""GPU parity tests (B200): the CUDA path through the C ABI vs the float64 oracle on the
+same seeded inputs.  Tolerances: bit-exact for indices/copies; C-TOL rtol 1e-4 (fp32 parity
+mode) and 2e-2 (bf16) (BASELINE.json north_star; DESIGN.md C-TOL)."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from paper_2505_20600_b200 import ig
+from gpu_util import Model, Request, cache_to_numpy, ctol, fill_cache
+
+pytestmark = pytest.mark.gpu
+
+RTOL = {ig.IG_F32: 1e-4, ig.IG_BF16: 2e-2}
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    ig.lib()
+
+
+# ------------------------------------------------------------------ a1 index build
+@pytest.mark.parametrize("L", [256, 1024, 4096, 9000])
+def test_mask_index_bit_exact(L):
+    d = synth.ModelDesc("m", 0, 1, 64, 4, 16, 256, 16, 1, L, 0, rope_axes=(4, 6, 6))
+    m = Model(d, ig.IG_F32)
+    rng = np.random.default_rng(L)
+    masks = [np.zeros(L, np.uint8), np.ones(L, np.uint8)]
+    one = np.zeros(L, np.uint8); one[0] = 1; masks.append(one)
+    last = np.zeros(L, np.uint8); last[-1] = 7; masks.append(last)
+    for _ in range(6):
+        masks.append((rng.random(L) < rng.random()).astype(np.uint8) * rng.integers(1, 256, L).astype(np.uint8))
+    for mk in masks:
+        dev = torch.from_numpy(mk).cuda()
+        h, n = ig.ig_mask_build(m.ctx, dev.data_ptr(), 0)
+        pm, pu, n2 = ig.ig_mask_indices(h)
+        ref_m, ref_u, ref_n = oracle.index_build(mk)
+        assert n == n2 == ref_n
+        got = torch.empty(2 * L, dtype=torch.int32, device="cuda")
+        ig.ig_copy(got.data_ptr(), pm, 2 * L * 4)
+        g = got.cpu().numpy()
+        assert np.array_equal(g[:n], ref_m) and np.array_equal(g[L:L + L - n], ref_u)
+        ig.ig_mask_free(h)
+    m.close()
+
+
+# ------------------------------------------------------------------ kernel (c) GEMM
+@pytest.mark.parametrize("dtype", [ig.IG_F32, ig.IG_BF16])
+@pytest.mark.parametrize("M,N,K", [(1, 64, 64), (127, 128, 128), (129, 256, 192), (300, 576, 320),
+                                   (1331, 384, 256)])
+@pytest.mark.parametrize("epi", [0, 1])
+def test_gemm_vs_oracle(dtype, M, N, K, epi):
+    tdt = torch.float32 if dtype == ig.IG_F32 else torch.bfloat16
+    A = (synth.uniform(1, "A", (M, K), "cuda")).float().to(tdt)
+    B = (synth.uniform(2, "B", (N, K), "cuda") / K ** 0.5).float().to(tdt)
+    bias = synth.uniform(3, "b", (N,), "cuda").float().to(tdt)
+    C = torch.full((M, N), float("nan"), dtype=torch.float32, device="cuda")
+    ig.ig_op_gemm(dtype, A.data_ptr(), K, B.data_ptr(), K, bias.data_ptr(), C.data_ptr(), N,
+                  M, N, K, epi, 1, 0)
+    torch.cuda.synchronize()
+    ref = oracle.linear(A.double().cpu().numpy(), B.double().cpu().numpy(), bias.double().cpu().numpy())
+    if epi == 1:
+        ref = oracle.gelu_tanh(ref)
+    ok, worst = ctol(C.cpu().numpy(), ref, 1e-4 if dtype == ig.IG_F32 else 2e-3)
+    assert ok, worst
+
+
+# ------------------------------------------------------------------ kernel (d) attention
+@pytest.mark.parametrize("dtype", [ig.IG_F32, ig.IG_BF16])
+@pytest.mark.parametrize("heads,dh,L,qlens", [(4, 16, 256, [64]), (2, 128, 300, [0, 1, 127, 128, 129]),
+                                              (3, 64, 1357, [333, 200]), (2, 128, 4608, [512, 819])])
+def test_attention_vs_oracle(dtype, heads, dh, L, qlens):
+    tdt = torch.float32 if dtype == ig.IG_F32 else torch.bfloat16
+    H = heads * dh
+    nseg = len(qlens)
+    M = sum(qlens)
+    Q = synth.normal(5, "Q", (max(M, 1), H), "cuda").float().to(tdt)
+    kv = synth.normal(6, "KV", (nseg, 2, L, H), "cuda").float().to(tdt)
+    O = torch.full((max(M, 1), H), float("nan"), dtype=tdt, device="cuda")
+    segs, s = [], 0
+    for i, q in enumerate(qlens):
+        segs.append((s, q, i))
+        s += q
+    ig.ig_op_attention(dtype, Q.data_ptr(), H, O.data_ptr(), H, kv.data_ptr(), segs, L, heads, dh, 0)
+    torch.cuda.synchronize()
+    Qh, KVh, Oh = Q.double().cpu().numpy(), kv.double().cpu().numpy(), O.double().cpu().numpy()
+    for (q0, ql, i) in segs:
+        if ql == 0:
+            continue
+        ref = oracle.attention(Qh[q0:q0 + ql], KVh[i, 0], KVh[i, 1], heads)
+        ok, worst = ctol(Oh[q0:q0 + ql], ref, 1e-4 if dtype == ig.IG_F32 else 2e-2)
+        assert ok, (i, worst)
+
+
+# ------------------------------------------------------------------ end to end
+def _run_edit(m, reqs_objs, masks_cache, n_steps, sig):
+    for s in range(n_steps):
+        rr = [r.req(i, masks_cache, s, sig[s], sig[s + 1]) for i, r in enumerate(reqs_objs)]
+        ig.ig_edit_step(m.ctx, rr, 0)
+    torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("dtype", [ig.IG_F32, ig.IG_BF16])
+def test_tiny_config_end_to_end(dtype):
+    """Config 1: tiny single block, 25% rectangle, 2 steps.  GPU cache_template vs the
+    oracle's recorded cache, then the edit steps with a synthetic cache shared by both."""
+    d = synth.TINY
+    sig = [1.0, 0.5, 0.0]
+    m = Model(d, dtype)
+    W = m.host_weights()
+    rq = Request(m, 0, synth.tiny_rect_mask())
+    lat0, txt, cond = rq.host_inputs()
+    # cache recording (dense trajectory)
+    lat_t = rq.latent.clone()
+    cache = ig.ig_cache_template(m.ctx, lat_t.data_ptr(), 0, rq.cond.data_ptr(), sig)
+    _, ocache, traj = oracle.cache_template(d, W, lat0, txt, cond, sig)
+    g = cache_to_numpy(cache, d, 2, dtype)
+    ok, worst = ctol(g, ocache, RTOL[dtype])
+    assert ok, ("cache", worst)
+    ok, worst = ctol(lat_t.double().cpu().numpy(), traj[-1], RTOL[dtype])
+    assert ok, ("dense trajectory", worst)
+    # edit steps with a synthetic cache (same bytes for both sides)
+    kv = synth.make_cache_kv(d, 0, 2, dtype=torch.float32 if dtype == ig.IG_F32 else torch.bfloat16)
+    syn = ig.ig_cache_create(m.ctx, 2, ig.IG_CACHE_HOST)
+    fill_cache(syn, kv)
+    kvh = kv.double().numpy()
+    _run_edit(m, [rq], syn, 2, sig)
+    x = lat0
+    for s in range(2):
+        x = oracle.edit_step(d, W, x, rq.mask_np, kvh[s], sig[s], sig[s + 1], txt, cond)
+    got = rq.latent.double().cpu().numpy()
+    ok, worst = ctol(got, x, RTOL[dtype])
+    assert ok, ("edit", worst)
+    assert np.array_equal(got[rq.mask_np == 0], lat0[rq.mask_np == 0])  # untouched rows
+    ig.ig_cache_free(cache)
+    ig.ig_cache_free(syn)
+    rq.free()
+    m.close()
+
+
+@pytest.mark.parametrize("dtype", [ig.IG_F32, ig.IG_BF16])
+@pytest.mark.parametrize("copy_mode", [0, 1])
+def test_flux_small_batch_end_to_end(dtype, copy_mode):
+    """Flux-structured small model (2 double + 2 single blocks, text tokens): a continuous
+    batch of 3 requests with different masks (rectangle, blob, all-ones) and a synthetic
+    cache, 2 steps, against the oracle request by request."""
+    d = synth.FLUX_SMALL
+    sig = [1.0, 0.7, 0.4]
+    opts = ig.ig_ctx_opts(4, 0, 2, copy_mode, 0)
+    m = Model(d, dtype, opts=opts)
+    W = m.host_weights()
+    rng = np.random.default_rng(0)
+    masks = [synth.rect_mask_count(d, 50, rng), synth.blob_mask_count(d, 120, rng),
+             np.ones(d.L_img, np.uint8)]
+    reqs = [Request(m, 10 + i, mk) for i, mk in enumerate(masks)]
+    tdt = torch.float32 if dtype == ig.IG_F32 else torch.bfloat16
+    kv = synth.make_cache_kv(d, 3, 2, dtype=tdt)
+    cache = ig.ig_cache_create(m.ctx, 2, ig.IG_CACHE_HOST)
+    fill_cache(cache, kv)
+    kvh = kv.double().numpy()
+    _run_edit(m, reqs, cache, 2, sig)
+    for r in reqs:
+        lat0, txt, cond = r.host_inputs()
+        x = lat0
+        for s in range(2):
+            x = oracle.edit_step(d, W, x, r.mask_np, kvh[s], sig[s], sig[s + 1], txt, cond)
+        got = r.latent.double().cpu().numpy()
+        ok, worst = ctol(got, x, RTOL[dtype])
+        assert ok, worst
+        assert np.array_equal(got[r.mask_np == 0], lat0[r.mask_np == 0])
+    ig.ig_cache_free(cache)
+    for r in reqs:
+        r.free()
+    m.close()
+
+
+def test_degenerate_and_errors():
+    d = synth.FLUX_SMALL
+    m = Model(d, ig.IG_BF16)
+    empty = Request(m, 1, np.zeros(d.L_img, np.uint8))
+    ig.ig_edit_step(m.ctx, [empty.req(0, None, 0, 1.0, 0.9)], 0)
+    torch.cuda.synchronize()
+    assert torch.equal(empty.latent, empty.latent0)
+    st = ig.ig_last_stats(m.ctx)
+    assert st["h2d_bytes"] == 0 and st["kernel_launches"] == 0
+    part = Request(m, 2, synth.rect_mask(d, 0, 4, 0, 4))
+    with pytest.raises(ig.IgError) as e:
+        ig.ig_edit_step(m.ctx, [part.req(0, None, 0, 1.0, 0.9)], 0)
+    assert e.value.name == "IG_ECACHE_MISS"
+    cache = ig.ig_cache_create(m.ctx, 2, ig.IG_CACHE_HOST)
+    with pytest.raises(ig.IgError) as e:
+        ig.ig_edit_step(m.ctx, [part.req(0, cache, 5, 1.0, 0.9)], 0)
+    assert e.value.name == "IG_ECACHE_INCOMPAT"
+    with pytest.raises(ig.IgError) as e:
+        ig.ig_edit_step(m.ctx, [part.req(0, cache, 0, 1.0, 0.9), part.req(0, cache, 0, 1.0, 0.9)], 0)
+    assert e.value.name == "IG_EINVAL"
+    ig.ig_cache_free(cache)
+    empty.free(); part.free()
+    m.close()
