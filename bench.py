@@ -1,0 +1,415 @@
+"""bench.py — edited images/s of the mask-aware denoising step on a Flux.1-dev-shaped DiT.
+
+Metric (BASELINE.json): "edited images/s (Flux-shape 1024^2, mixed masks) at 1/2/4/8 B200;
+vs dense step".  One bench *step* = one ig_edit_step over the running continuous batch
+(max_batch 8 requests at staggered denoising steps; a request that finishes its 28th step
+leaves and a new one joins at the next step boundary).  Requests carry masks with
+m ~ U[0.05, 0.60] (half rectangles, half blobs) and reference one template whose 28-step
+K/V cache (80.3 GB bf16) lives in pinned host memory and is prefetched layer by layer
+(P:541-560).  value = request-steps completed in the timed window / 28 / window seconds.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Under torchrun each rank runs an independent replica (request-wise partition, no collective
+on the step path; weak scaling) and rank 0 prints one JSON line.
+"""
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import synth  # noqa: E402
+
+N_STEPS = 28
+METRIC = "edited images/s (Flux-shape 1024^2, mixed masks) at 1/2/4/8 B200; vs dense step"
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d["hbm_gbs"], d["bf16_tflops"], d["bf16_tflops_sustained"], "measured"
+    return 6650.0, 1590.0, 1400.0, "fallback"
+
+
+# ------------------------------------------------------------------------------- clocks
+class Clocks:
+    """Samples nvidia-smi clocks and throttle reasons during the timed region."""
+
+    def __init__(self, gpu):
+        self.gpu, self.rows, self.proc = gpu, [], None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), "--query-gpu=clocks.sm,clocks.max.sm,power.draw,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm = [float(r[0]) for r in self.rows if r and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) > 1 and r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 3 + i and r[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(sm)}
+
+
+# ------------------------------------------------------------------------------- model
+def build_model(d, dev):
+    from paper_2505_20600_b200 import ig
+    W, ptrs = {}, []
+    for name, shape, fan_in in synth.weight_table(d):
+        t = synth.make_weight(d, name, shape, fan_in, 0, dev, torch.bfloat16).contiguous()
+        W[name] = t
+        ptrs.append(t.data_ptr())
+    return W, ptrs
+
+
+class Req:
+    def __init__(self, ig, ctx, d, rid, dev, dense=False):
+        self.rid = rid
+        self.latent = synth.make_latent(d, rid, dev).contiguous()
+        self.txt = synth.make_txt(d, rid, dev, torch.bfloat16).contiguous()
+        self.cond = synth.make_cond(d, rid, dev).contiguous()
+        mk = np.ones(d.L_img, np.uint8) if dense else synth.mixed_mask(d, rid)
+        self.mask_np = mk
+        self.mask_dev = torch.from_numpy(mk).to(dev)
+        self.mask, self.n_m = ig.ig_mask_build(ctx, self.mask_dev.data_ptr(), 0)  # admission
+        self.step = 0
+
+
+class Batch:
+    """Continuous batching at saturation: max_batch slots, staggered start steps."""
+
+    def __init__(self, ig, ctx, d, dev, max_batch, pool_size, rid0, dense=False):
+        self.ig, self.ctx, self.d = ig, ctx, d
+        self.pool = [Req(ig, ctx, d, rid0 + i, dev, dense) for i in range(pool_size)]
+        self.next = 0
+        self.slots = []
+        for s in range(max_batch):
+            r = self._admit()
+            r.step = (s * N_STEPS) // max_batch
+            self.slots.append(r)
+        self.completed = 0
+
+    def _admit(self):
+        r = self.pool[self.next % len(self.pool)]
+        self.next += 1
+        r.step = 0
+        return r
+
+    def reqs(self, cache, sig):
+        return [self.ig.make_req(i, r.latent.data_ptr(), r.mask, cache, r.step, float(sig[r.step]),
+                                 float(sig[r.step + 1]), r.txt.data_ptr(), r.cond.data_ptr())
+                for i, r in enumerate(self.slots)]
+
+    def advance(self):
+        done = 0
+        for i, r in enumerate(self.slots):
+            r.step += 1
+            if r.step == N_STEPS:
+                done += 1
+                self.slots[i] = self._admit()
+        self.completed += done
+        return len(self.slots)  # request-steps done this step
+
+
+def run_loop(ig, ctx, batch, cache, sig, steps, stream, profile=False, e2e=None):
+    """Runs `steps` batch steps on `stream`; returns (ms, request_steps, launches, stats)."""
+    launches, rsteps = 0, 0
+    h2d = d2h = 0
+    evs = []
+    start = torch.cuda.Event(enable_timing=True)
+    end = torch.cuda.Event(enable_timing=True)
+    if profile:
+        ig.ig_profile_enable(ctx, True)
+    start.record(stream)
+    for _ in range(steps):
+        e0 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        if e2e is not None:  # public-API end to end: host latents in, results out
+            for r in batch.slots:
+                hb = e2e[r.rid]
+                r.latent.copy_(hb, non_blocking=True)
+                h2d += hb.numel() * 4
+        ig.ig_edit_step(ctx, batch.reqs(cache, sig), stream.cuda_stream)
+        st = ig.ig_last_stats(ctx)
+        launches += st["kernel_launches"]
+        h2d += st["h2d_bytes"]
+        if e2e is not None:
+            for r in batch.slots:
+                hb = e2e[r.rid]
+                hb.copy_(r.latent, non_blocking=True)
+                d2h += hb.numel() * 4
+        e1 = torch.cuda.Event(enable_timing=True)
+        e1.record(stream)
+        evs.append((e0, e1))
+        rsteps += batch.advance()
+    end.record(stream)
+    end.synchronize()
+    prof = ig.ig_profile_read(ctx) if profile else None
+    if profile:
+        ig.ig_profile_enable(ctx, False)
+    per_step = [a.elapsed_time(b) for a, b in evs]
+    return start.elapsed_time(end), rsteps, launches, per_step, prof, h2d, d2h
+
+
+# ------------------------------------------------------------------------------- oracle leg
+def oracle_sample(d, m_ratio=0.2, seed=0):
+    """Time the oracle (as it stands) on one Flux double block and one single block for one
+    request at mask ratio m (teacher-forced random inputs); returns (t_double, t_single, n)."""
+    import oracle
+    H = d.hidden
+    names_d = {n for n, _, _ in synth.weight_table(d) if n.startswith("double.0.")}
+    names_s = {n for n, _, _ in synth.weight_table(d) if n.startswith("single.0.")}
+    W = {k: v.double().numpy() for k, v in synth.make_weights(d, 0, "cpu", torch.bfloat16,
+                                                              names=names_d | names_s).items()}
+    n_m = int(round(m_ratio * d.L_img))
+    mask = synth.rect_mask_count(d, n_m, np.random.default_rng(seed))
+    idx_m, idx_u, _ = oracle.index_build(mask)
+    rng = np.random.default_rng(seed)
+    vec = rng.standard_normal(H)
+    kv = rng.standard_normal((2, d.L_img, H))
+    xt, xi = rng.standard_normal((d.txt_len, H)), rng.standard_normal((n_m, H))
+    t0 = time.perf_counter()
+    oracle.double_block_masked(d, W, 0, xt, xi, vec, idx_m, idx_u, kv)
+    t1 = time.perf_counter()
+    oracle.single_block_masked(d, W, 0, np.concatenate([xt, xi]), vec, idx_m, idx_u, kv)
+    t2 = time.perf_counter()
+    return t1 - t0, t2 - t1, n_m
+
+
+def cpu_cores():
+    try:
+        from threadpoolctl import threadpool_info
+        return max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
+    except Exception:
+        return len(os.sched_getaffinity(0))
+
+
+def cpu_baseline(d):
+    td, ts, n_m = oracle_sample(d, 0.2)
+    step_s = d.n_double * td + d.n_single * ts
+    return {"value": 1.0 / (N_STEPS * step_s), "unit": "images/s", "cores": cpu_cores(), "kind": "oracle",
+            "sample": f"float64 NumPy oracle: one Flux double block ({td:.2f} s) + one single block "
+                      f"({ts:.2f} s), 1 request, m=0.2 (n_m={n_m}); extrapolated x(19 double + 38 single) "
+                      f"x 28 steps per image"}
+
+
+def run_reference(args, rank):
+    if rank != 0:
+        return
+    d = synth.FLUX
+    per = []
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        td, ts, n_m = oracle_sample(d, 0.325, seed=i)
+        el = time.perf_counter() - t0
+        if i >= args.warmup:
+            per.append((td, ts))
+    td = float(np.mean([p[0] for p in per]))
+    ts = float(np.mean([p[1] for p in per]))
+    img_s = 1.0 / (N_STEPS * (d.n_double * td + d.n_single * ts))
+    cb = {"value": img_s, "unit": "images/s", "cores": cpu_cores(), "kind": "oracle",
+          "sample": "per step: one Flux double + one single block, 1 request at m=0.325, float64 "
+                    "oracle; extrapolated x(19+38) blocks x 28 steps"}
+    print(json.dumps({"impl": "reference", "metric": METRIC, "value": img_s, "unit": "images/s",
+                      "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+                      "ms_per_step": 1e3 * (td + ts), "higher_is_better": True, "scaling": "weak",
+                      "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                      "config": {"workload": "flux1_dev 1024^2 mask-aware step (oracle sample)"},
+                      "cpu_baseline": cb,
+                      "e2e": {"value": img_s, "unit": "images/s", "h2d_bytes_per_step": 0,
+                              "d2h_bytes_per_step": 0}}))
+
+
+# ------------------------------------------------------------------------------- main
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=12)
+    ap.add_argument("--warmup", type=int, default=4)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--max-batch", type=int, default=8)
+    ap.add_argument("--tier", default=None, choices=["host", "device"])
+    ap.add_argument("--copy-mode", type=int, default=0)
+    ap.add_argument("--depth", type=int, default=2)
+    ap.add_argument("--dense-steps", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--model", default="flux1_dev")
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl" if args.impl == "ours" else "gloo")
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+    assert args.warmup >= 3 or os.environ.get("IG_BENCH_QUICK"), "W >= 3 warm-up steps"
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    from paper_2505_20600_b200 import ig
+    ig.lib()
+    d = synth.MODELS[args.model]
+    tier = args.tier or ("host" if world == 1 else "device")
+    hbm, pk_burst, pk_sus, pk_src = peaks()
+
+    t_setup = time.time()
+    W, ptrs = build_model(d, dev)
+    opts = ig.ig_ctx_opts(args.max_batch, args.max_batch * d.L, args.depth, args.copy_mode, 0)
+    ctx = ig.ig_ctx_create(ig.make_desc(d, ig.IG_BF16), ptrs, local, opts)
+    sig = synth.flow_sigmas(N_STEPS)
+    # the template: dense 28-step sampler recording every (step, block) K/V (ig_cache_template)
+    tl = synth.make_latent(d, 10 ** 6, dev)
+    tt = synth.make_txt(d, 10 ** 6, dev, torch.bfloat16)
+    tc = synth.make_cond(d, 10 ** 6, dev)
+    t0 = time.time()
+    cache = ig.ig_cache_template(ctx, tl.data_ptr(), tt.data_ptr(), tc.data_ptr(), sig,
+                                 ig.IG_CACHE_HOST if tier == "host" else ig.IG_CACHE_DEVICE, 0)
+    t_template = time.time() - t0
+    stream = torch.cuda.Stream(device=dev)
+    pool = args.max_batch + math.ceil(args.max_batch * (2 * args.warmup + 2 * args.steps) / N_STEPS) + 2
+    batch = Batch(ig, ctx, d, dev, args.max_batch, pool, rid0=rank * 100000)
+    torch.cuda.synchronize()
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+
+    # warm-up, then the timed window (profiling events on the launching stream)
+    run_loop(ig, ctx, batch, cache, sig, args.warmup, stream)
+    clocks = Clocks(local)
+    barrier()
+    clocks.start()
+    ms, rsteps, launches, per_step, prof, h2d, _ = run_loop(ig, ctx, batch, cache, sig, args.steps, stream,
+                                                            profile=True)
+    barrier()
+    clk = clocks.stop()
+    t = torch.tensor([ms, float(rsteps)], dtype=torch.float64, device=dev)
+    if world > 1:
+        mx = t.clone()
+        torch.distributed.all_reduce(mx, op=torch.distributed.ReduceOp.MAX)
+        sm = t.clone()
+        torch.distributed.all_reduce(sm, op=torch.distributed.ReduceOp.SUM)
+        ms_max, rsteps_all = float(mx[0]), float(sm[1])
+    else:
+        ms_max, rsteps_all = ms, float(rsteps)
+    value = rsteps_all / N_STEPS / (ms_max / 1e3)
+
+    # end to end through the public API with host buffers (latent H2D + D2H every step)
+    e2e = None
+    if not args.no_e2e:
+        hbufs = {r.rid: r.latent.detach().cpu().pin_memory() for r in batch.pool}
+        barrier()
+        ms_e, rs_e, _, _, _, h2d_e, d2h_e = run_loop(ig, ctx, batch, cache, sig, args.steps, stream, e2e=hbufs)
+        barrier()
+        te = torch.tensor([ms_e, float(rs_e)], dtype=torch.float64, device=dev)
+        if world > 1:
+            mx = te.clone()
+            torch.distributed.all_reduce(mx, op=torch.distributed.ReduceOp.MAX)
+            sm = te.clone()
+            torch.distributed.all_reduce(sm, op=torch.distributed.ReduceOp.SUM)
+            ms_e, rs_e = float(mx[0]), float(sm[1])
+        e2e = {"value": rs_e / N_STEPS / (ms_e / 1e3), "unit": "images/s",
+               "h2d_bytes_per_step": int(h2d_e / args.steps), "d2h_bytes_per_step": int(d2h_e / args.steps)}
+
+    # dense comparison step (all-ones masks, no cache) on the same GPUs and kernels
+    dense = None
+    if args.dense_steps > 0:
+        dbatch = Batch(ig, ctx, d, dev, args.max_batch, args.max_batch + 2, rid0=rank * 100000 + 50000, dense=True)
+        run_loop(ig, ctx, dbatch, None, sig, 1, stream)
+        barrier()
+        ms_d, rs_d, _, _, _, _, _ = run_loop(ig, ctx, dbatch, None, sig, args.dense_steps, stream)
+        barrier()
+        td = torch.tensor([ms_d, float(rs_d)], dtype=torch.float64, device=dev)
+        if world > 1:
+            mx = td.clone()
+            torch.distributed.all_reduce(mx, op=torch.distributed.ReduceOp.MAX)
+            sm = td.clone()
+            torch.distributed.all_reduce(sm, op=torch.distributed.ReduceOp.SUM)
+            ms_d, rs_d = float(mx[0]), float(sm[1])
+        dense = rs_d / N_STEPS / (ms_d / 1e3)
+
+    if rank != 0:
+        if world > 1:
+            torch.distributed.barrier()
+        return
+    g = prof["gemm"]
+    gemm_tf = g["flops"] / (g["ms"] * 1e-3) / 1e12 if g["ms"] else 0.0
+    a = prof["attn"]
+    attn_tf = a["flops"] / (a["ms"] * 1e-3) / 1e12 if a["ms"] else 0.0
+    step_ms = ms / args.steps
+    shares = {k: round(v["ms"] / args.steps / step_ms, 4) for k, v in prof.items()}
+    out = {
+        "metric": METRIC, "value": round(value, 4), "unit": "images/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic",
+        "config": {"workload": f"{d.name} 1024^2 (4096 img + 512 txt tokens), 28-step flow schedule, "
+                               f"continuous batching max_batch {args.max_batch}, masks m~U[0.05,0.60] "
+                               f"(rect/blob), K/V cache tier={tier} copy_mode={args.copy_mode} depth={args.depth}",
+                   "global_batch": args.max_batch * world, "seq_len": d.L, "parallelism": f"replica{world}",
+                   "l2": "inputs larger than L2 (23.7 GB weights + 2.9 GB K/V per request-step streamed)"},
+        "roofline": {"bound": "tensor", "kernel": "gemm_tc (tcgen05 bf16)", "achieved": round(gemm_tf, 1),
+                     "peak": pk_sus, "unit": "TFLOP/s", "frac": round(gemm_tf / pk_sus, 4),
+                     "traffic": None, "peak_kind": f"bf16 sustained ({pk_src})",
+                     "frac_of_burst": round(gemm_tf / pk_burst, 4)},
+        "attn_roofline": {"achieved": round(attn_tf, 1), "unit": "TFLOP/s", "frac": round(attn_tf / pk_sus, 4)},
+        "kernel_share_of_step": shares,
+        "per_step_ms": {"median": round(statistics.median(per_step), 3),
+                        "p10": round(float(np.percentile(per_step, 10)), 3),
+                        "p90": round(float(np.percentile(per_step, 90)), 3)},
+        "dense_images_per_s": round(dense, 4) if dense else None,
+        "speedup_vs_dense": round(value / dense, 3) if dense else None,
+        "host_link_GBps": round(h2d / (ms * 1e-3) / 1e9, 2),
+        "gpu_launches": int(launches),
+        "clocks": clk,
+        "e2e": e2e,
+        "setup_s": {"total": round(time.time() - t_setup, 1), "template": round(t_template, 1)},
+        "paper_context": "InstGenIE m=0.2 speedups 1.3x SD2.1 (A10), 2.2x SDXL / 1.9x Flux (H800) (P:1003)",
+    }
+    if not args.no_cpu_baseline and world == 1:
+        out["cpu_baseline"] = cpu_baseline(d)
+    print(json.dumps(out))
+    if world > 1:
+        torch.distributed.barrier()
+
+
+if __name__ == "__main__":
+    main()

@@ -178,6 +178,24 @@ typedef struct {
 } ig_stats;
 ig_status ig_last_stats(const ig_ctx* ctx, ig_stats* out);
 
+/* Live per-kernel-class timing for the roofline report: while enabled, every libig launch
+ * on the compute stream is bracketed by CUDA events (recorded on the launching stream) and
+ * tagged with its ALGORITHMIC work (flops for GEMM/attention = 2*M*N*K and 4*sum(q)*L*H;
+ * bytes for the HBM-bound kernels).  ig_profile_read synchronises those events, returns the
+ * per-class totals accumulated since the last read, and resets them. */
+typedef enum {
+  IG_K_GEMM = 0, IG_K_ATTN = 1, IG_K_LNMOD = 2, IG_K_QKVPOST = 3, IG_K_COND = 4,
+  IG_K_ROWS = 5, IG_K_NCLASS = 6
+} ig_kernel_class;
+typedef struct {
+  long long launches;
+  double ms;     /* sum of event-timed launch durations                       */
+  double flops;  /* algorithmic flops of those launches (GEMM, attention)      */
+  double bytes;  /* algorithmic HBM bytes of those launches (other classes)    */
+} ig_prof_entry;
+ig_status ig_profile_enable(ig_ctx* ctx, int enable);
+ig_status ig_profile_read(ig_ctx* ctx, ig_prof_entry out[IG_K_NCLASS]);
+
 #ifdef __cplusplus
 }
 #endif

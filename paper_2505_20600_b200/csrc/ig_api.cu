@@ -136,6 +136,37 @@ struct ig_ctx {
   ig_mask* ones_mask = nullptr;
   ig_stats stats{};
   std::vector<ig_cache*> zombies;
+  // live profiling (ig_profile_enable)
+  bool prof = false;
+  struct ProfRec { int kind; cudaEvent_t a, b; double flops, bytes; };
+  std::vector<ProfRec> prof_recs;
+  std::vector<cudaEvent_t> ev_pool;
+  ig_prof_entry prof_acc[IG_K_NCLASS] = {};
+};
+
+static cudaEvent_t pool_event(ig_ctx* ctx) {
+  if (!ctx->ev_pool.empty()) {
+    cudaEvent_t e = ctx->ev_pool.back();
+    ctx->ev_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+
+// RAII bracket around one launch when profiling is enabled
+struct ProfScope {
+  ig_ctx* ctx; cudaStream_t st; int kind; double flops, bytes; cudaEvent_t a = nullptr;
+  ProfScope(ig_ctx* c, cudaStream_t s, int k, double f, double b) : ctx(c), st(s), kind(k), flops(f), bytes(b) {
+    if (ctx->prof) { a = pool_event(ctx); cudaEventRecord(a, st); }
+  }
+  ~ProfScope() {
+    if (!a) return;
+    cudaEvent_t b = pool_event(ctx);
+    cudaEventRecord(b, st);
+    ctx->prof_recs.push_back({kind, a, b, flops, bytes});
+  }
 };
 
 // ----------------------------------------------------------------------------------------
@@ -192,13 +223,15 @@ static bool g_tc_attn = true;
 static void gemm(ig_ctx* ctx, const GemmArgs& g, cudaStream_t st) {
   if (g.M <= 0 || g.N <= 0) return;
   ctx->stats.kernel_launches++;
+  ProfScope ps(ctx, st, IG_K_GEMM, 2.0 * g.M * g.N * g.K, 0.0);
   if (ctx->d.dtype == IG_F32) launch_gemm_simt<float>(g, st);
   else if (g_tc_gemm && gemm_tc_supported(g)) launch_gemm_tc(g, st);
   else launch_gemm_simt<bf16>(g, st);
 }
 
-static void attention(ig_ctx* ctx, const AttnArgs& a, cudaStream_t st) {
+static void attention(ig_ctx* ctx, const AttnArgs& a, cudaStream_t st, double flops) {
   ctx->stats.kernel_launches++;
+  ProfScope ps(ctx, st, IG_K_ATTN, flops, 0.0);
   if (ctx->d.dtype == IG_F32) launch_attn_simt<float>(a, st);
   else if (g_tc_attn && a.head_dim == 128) launch_attn_tc(a, st);
   else launch_attn_simt<bf16>(a, st);
@@ -420,9 +453,38 @@ extern "C" void ig_ctx_destroy(ig_ctx* ctx) {
     if (ctx->ev_comp[i]) cudaEventDestroy(ctx->ev_comp[i]);
   }
   if (ctx->ev_desc) cudaEventDestroy(ctx->ev_desc);
+  for (auto& r : ctx->prof_recs) { ctx->ev_pool.push_back(r.a); ctx->ev_pool.push_back(r.b); }
+  for (auto e : ctx->ev_pool) cudaEventDestroy(e);
   if (ctx->copy_st) cudaStreamDestroy(ctx->copy_st);
   if (ctx->ones_mask) { cudaFree(ctx->ones_mask->idx); delete ctx->ones_mask; }
   delete ctx;
+}
+
+extern "C" ig_status ig_profile_enable(ig_ctx* ctx, int enable) {
+  if (!ctx) return set_err(IG_EINVAL, "ctx is NULL");
+  ctx->prof = enable != 0;
+  return IG_OK;
+}
+
+extern "C" ig_status ig_profile_read(ig_ctx* ctx, ig_prof_entry out[IG_K_NCLASS]) {
+  if (!ctx || !out) return set_err(IG_EINVAL, "NULL argument");
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  for (auto& r : ctx->prof_recs) {
+    CUDA_TRY(cudaEventSynchronize(r.b));
+    float ms = 0.f;
+    CUDA_TRY(cudaEventElapsedTime(&ms, r.a, r.b));
+    ig_prof_entry& e = ctx->prof_acc[r.kind];
+    e.launches++;
+    e.ms += ms;
+    e.flops += r.flops;
+    e.bytes += r.bytes;
+    ctx->ev_pool.push_back(r.a);
+    ctx->ev_pool.push_back(r.b);
+  }
+  ctx->prof_recs.clear();
+  for (int k = 0; k < IG_K_NCLASS; ++k) out[k] = ctx->prof_acc[k];
+  for (int k = 0; k < IG_K_NCLASS; ++k) ctx->prof_acc[k] = ig_prof_entry{};
+  return IG_OK;
 }
 
 extern "C" ig_status ig_last_stats(const ig_ctx* ctx, ig_stats* out) {
@@ -717,13 +779,19 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
   auto& stats = ctx->stats;
 
   // ---- a2/a4: rows + gather; a3: conditioning ----
-  launch_build_rows<T>(dreq, na, Lt, C, H, M_txt, M, ctx->ri, ctx->X, (T*)ctx->Ain, st);
+  {
+    ProfScope ps(ctx, st, IG_K_ROWS, 0.0, (double)M_txt * H * (4 + es) + (double)M_img * C * (4 + es));
+    launch_build_rows<T>(dreq, na, Lt, C, H, M_txt, M, ctx->ri, ctx->X, (T*)ctx->Ain, st);
+  }
+  {
+  ProfScope ps_cond(ctx, st, IG_K_COND, 0.0, (double)ctx->mod_ld * H * es);
   launch_timestep_embed(dreq, na, ctx->temb, st);
   launch_gemv<T>(ctx->gv_t1, 1, (H + 31) / 32, na, 256, st);
   launch_gemv<T>(ctx->gv_t2, 1, (H + 31) / 32, na, H, st);
   launch_add_cond(dreq, na, H, ctx->vec, st);
   launch_silu(ctx->vec, ctx->svec, (long long)na * H, st);
   launch_gemv<T>(ctx->gv_mod, (int)ctx->gv_mod_host.size(), ctx->gv_mod_groups, na, H, st);
+  }
   stats.kernel_launches += 7;
   {  // img_in (+ SD3 pos_embed) into the fp32 residual X
     GemmArgs g{};
@@ -737,6 +805,7 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
   auto ln_mod = [&](int r0, int r1, int mod_t, int shift_c, int scale_c) {
     if (r1 <= r0) return;
     const long long off = ctx->mods[mod_t].off;
+    ProfScope ps(ctx, st, IG_K_LNMOD, 0.0, (double)(r1 - r0) * H * (4 + es));
     launch_ln_mod<T>(ctx->X, H, r0, r1, ctx->ri, mod + off, (int)mld, shift_c * H, scale_c * H,
                      ctx->d.ln_eps, h, H, st);
     stats.kernel_launches++;
@@ -767,6 +836,7 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
     p.ax1_pair = ctx->d.rope_axes[0] / 2; p.ax2_pair = (ctx->d.rope_axes[0] + ctx->d.rope_axes[1]) / 2;
     p.heads = ctx->d.heads; p.head_dim = ctx->d.head_dim; p.grid_w = ctx->d.grid_w;
     p.qk_norm = ctx->d.qk_norm; p.rope = ctx->d.rope; p.r0 = r0; p.r1 = r1;
+    ProfScope ps(ctx, st, IG_K_QKVPOST, 0.0, (double)(r1 - r0) * 6.0 * H * es);
     launch_qkv_post<T>(p, ctx->ri, st);
     stats.kernel_launches++;
   };
@@ -776,7 +846,7 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
     a.kv_off = (long long)buf * ctx->buf_elems; a.segs = dseg; a.nseg = nseg; a.max_qlen = max_q;
     a.L = ctx->L; a.heads = ctx->d.heads; a.head_dim = ctx->d.head_dim;
     a.scale = 1.0f / sqrtf((float)ctx->d.head_dim);
-    attention(ctx, a, st);
+    attention(ctx, a, st, 4.0 * (double)M * ctx->L * H);
   };
   // cache recording (template mode): image-token K/V of ring buffer -> cache[s][b]
   auto record_kv = [&](int b, int buf) {

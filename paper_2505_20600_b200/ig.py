@@ -23,7 +23,9 @@ STATUS = {0: "IG_OK", 1: "IG_EINVAL", 2: "IG_ECACHE_INCOMPAT", 3: "IG_ECACHE_MIS
 EXPORTS = ["ig_weight_count", "ig_ctx_create", "ig_ctx_destroy", "ig_cache_create",
            "ig_cache_template", "ig_cache_storage", "ig_cache_free", "ig_mask_build",
            "ig_mask_indices", "ig_mask_free", "ig_edit_step", "ig_prefetch_layer",
-           "ig_last_error", "ig_last_stats", "ig_op_gemm", "ig_op_attention", "ig_copy"]
+           "ig_last_error", "ig_last_stats", "ig_op_gemm", "ig_op_attention", "ig_copy",
+           "ig_profile_enable", "ig_profile_read"]
+KCLASS = ["gemm", "attn", "lnmod", "qkvpost", "cond", "rows"]
 
 
 class IgError(RuntimeError):
@@ -63,6 +65,11 @@ class ig_stats(ctypes.Structure):
                 ("rows", ctypes.c_longlong)]
 
 
+class ig_prof_entry(ctypes.Structure):
+    _fields_ = [("launches", ctypes.c_longlong), ("ms", ctypes.c_double),
+                ("flops", ctypes.c_double), ("bytes", ctypes.c_double)]
+
+
 def lib():
     """Load libig.so (in-tree).  Raises if it is missing: there is no other path."""
     global _lib
@@ -93,6 +100,8 @@ def lib():
         L.ig_op_gemm.argtypes = [i, vp, ll, vp, ll, vp, vp, ll, i, i, i, i, i, vp]
         L.ig_op_attention.argtypes = [i, vp, ll, vp, ll, vp, P(ctypes.c_int32), i, i, i, i, vp]
         L.ig_copy.argtypes = [vp, vp, ctypes.c_size_t, vp]
+        L.ig_profile_enable.argtypes = [vp, i]
+        L.ig_profile_read.argtypes = [vp, P(ig_prof_entry)]
         for name in EXPORTS:
             if name not in ("ig_ctx_destroy", "ig_cache_free", "ig_mask_free", "ig_last_error",
                             "ig_weight_count"):
@@ -214,3 +223,13 @@ def ig_op_attention(dtype, Q, ldq, O, ldo, kv, segs, L, heads, head_dim, stream=
 
 def ig_copy(dst: int, src: int, nbytes: int, stream: int = 0):
     _check(lib().ig_copy(dst, src, nbytes, stream))
+
+
+def ig_profile_enable(ctx: int, enable: bool = True):
+    _check(lib().ig_profile_enable(ctx, int(enable)))
+
+
+def ig_profile_read(ctx: int) -> dict:
+    arr = (ig_prof_entry * len(KCLASS))()
+    _check(lib().ig_profile_read(ctx, arr))
+    return {k: {f: getattr(arr[i], f) for f, _ in ig_prof_entry._fields_} for i, k in enumerate(KCLASS)}
