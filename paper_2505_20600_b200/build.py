@@ -54,4 +54,9 @@ def build(verbose=False, extra=()):
 
 
 if __name__ == "__main__":
-    print(build(verbose="-v" in sys.argv, extra=["-G"] if "--debug" in sys.argv else []))
+    ex = []
+    if "--debug" in sys.argv:
+        ex.append("-G")
+    if "--hang-check" in sys.argv:
+        ex.append("-DIG_HANG_CHECK")
+    print(build(verbose="-v" in sys.argv, extra=ex))

@@ -233,7 +233,7 @@ static void attention(ig_ctx* ctx, const AttnArgs& a, cudaStream_t st, double fl
   ctx->stats.kernel_launches++;
   ProfScope ps(ctx, st, IG_K_ATTN, flops, 0.0);
   if (ctx->d.dtype == IG_F32) launch_attn_simt<float>(a, st);
-  else if (g_tc_attn && a.head_dim == 128) launch_attn_tc(a, st);
+  else if (g_tc_attn && attn_tc_supported(a)) launch_attn_tc(a, st);
   else launch_attn_simt<bf16>(a, st);
 }
 
@@ -844,6 +844,7 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
     AttnArgs a{};
     a.Q = ctx->Q; a.ldq = H; a.O = cat; a.ldo = ldcat; a.kv_arena = ctx->kv_arena;
     a.kv_off = (long long)buf * ctx->buf_elems; a.segs = dseg; a.nseg = nseg; a.max_qlen = max_q;
+    a.q_rows = M;
     a.L = ctx->L; a.heads = ctx->d.heads; a.head_dim = ctx->d.head_dim;
     a.scale = 1.0f / sqrtf((float)ctx->d.head_dim);
     attention(ctx, a, st, 4.0 * (double)M * ctx->L * H);
@@ -1051,10 +1052,13 @@ extern "C" ig_status ig_op_attention(int dtype, const void* Q, long long ldq, vo
   AttnArgs a{};
   a.Q = Q; a.ldq = ldq; a.O = O; a.ldo = ldo; a.kv_arena = kv; a.kv_off = 0; a.segs = dsegs;
   a.nseg = nseg; a.max_qlen = maxq; a.L = L; a.heads = heads; a.head_dim = head_dim;
+  int qrows = 1;
+  for (auto& s : hs) qrows = std::max(qrows, s.q_start + s.q_len);
+  a.q_rows = qrows;
   a.scale = 1.0f / sqrtf((float)head_dim);
   if (dtype == IG_F32) launch_attn_simt<float>(a, st);
   else if (dtype == IG_BF16) {
-    if (g_tc_attn && head_dim == 128) launch_attn_tc(a, st);
+    if (g_tc_attn && attn_tc_supported(a)) launch_attn_tc(a, st);
     else launch_attn_simt<bf16>(a, st);
   } else return set_err(IG_EINVAL, "bad dtype");
   CUDA_TRY(cudaFreeAsync(dsegs, st));

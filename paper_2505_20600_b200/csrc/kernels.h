@@ -121,11 +121,13 @@ struct AttnArgs {
   void* O; long long ldo;         // packed [M, H] (may alias a column block of a wider buf)
   const void* kv_arena; long long kv_off;  // K at kv_base + kv_off, V at + L*H
   const AttnSeg* segs; int nseg; int max_qlen;
+  int q_rows;                     // rows of Q / O (bounds for the TMA tensor map)
   int L, heads, head_dim;
   float scale;                    // 1/sqrt(d)
 };
 template <typename T>
 void launch_attn_simt(const AttnArgs& a, cudaStream_t st);
+bool attn_tc_supported(const AttnArgs& a);
 void launch_attn_tc(const AttnArgs& a, cudaStream_t st);
 
 }  // namespace ig

@@ -5,6 +5,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <cstdio>
 
 namespace ig {
 namespace tc {
@@ -39,8 +40,19 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
   return ok != 0;
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+#ifdef IG_HANG_CHECK
+  long long n = 0;
+  while (!mbar_try_wait(bar, parity)) {
+    if (++n == (1ll << 26)) {
+      printf("IG_HANG_CHECK: block (%d,%d,%d) thread %d stuck on mbarrier smem+%u parity %u\n", blockIdx.x,
+             blockIdx.y, blockIdx.z, threadIdx.x, smem_u32(bar), parity);
+      __trap();
+    }
+  }
+#else
   while (!mbar_try_wait(bar, parity)) {
   }
+#endif
 }
 
 // ---- TMA ---------------------------------------------------------------------------------
