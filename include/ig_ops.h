@@ -20,6 +20,12 @@ ig_status ig_op_gemm(int dtype, const void* A, long long lda, const void* B, lon
                      const void* bias, void* C, long long ldc, int M, int N, int K, int epi,
                      int out_f32, void* stream);
 
+/* a9/a10 gated-residual epilogue variant (kernel c): X[M,N] (fp32, leading dimension ldx) +=
+ * gate[N] (fp32, one request) * (A B^T + bias).  Same dtype rules as ig_op_gemm. */
+ig_status ig_op_gemm_gated(int dtype, const void* A, long long lda, const void* B, long long ldb,
+                           const void* bias, float* X, long long ldx, const float* gate, int M, int N,
+                           int K, void* stream);
+
 /* a8 — ragged attention (kernel d): for each segment s (host array
  * segs[s] = {q_start, q_len, kv_index}) and head j: O[q rows, j] = softmax(Q K^T * scale) V
  * where K = kv + kv_index*2*L*H ([L, H]) and V = K + L*H.  Q, O: [M, H] packed rows with

@@ -13,6 +13,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -138,7 +139,7 @@ struct ig_ctx {
   std::vector<ig_cache*> zombies;
   // live profiling (ig_profile_enable)
   bool prof = false;
-  struct ProfRec { int kind; cudaEvent_t a, b; double flops, bytes; };
+  struct ProfRec { int kind; cudaEvent_t a, b; double flops, bytes; int M, N, K, epi; };
   std::vector<ProfRec> prof_recs;
   std::vector<cudaEvent_t> ev_pool;
   ig_prof_entry prof_acc[IG_K_NCLASS] = {};
@@ -158,14 +159,16 @@ static cudaEvent_t pool_event(ig_ctx* ctx) {
 // RAII bracket around one launch when profiling is enabled
 struct ProfScope {
   ig_ctx* ctx; cudaStream_t st; int kind; double flops, bytes; cudaEvent_t a = nullptr;
-  ProfScope(ig_ctx* c, cudaStream_t s, int k, double f, double b) : ctx(c), st(s), kind(k), flops(f), bytes(b) {
+  int M = 0, N = 0, K = 0, epi = -1;
+  ProfScope(ig_ctx* c, cudaStream_t s, int k, double f, double b, int m = 0, int n = 0, int kk = 0, int e = -1)
+      : ctx(c), st(s), kind(k), flops(f), bytes(b), M(m), N(n), K(kk), epi(e) {
     if (ctx->prof) { a = pool_event(ctx); cudaEventRecord(a, st); }
   }
   ~ProfScope() {
     if (!a) return;
     cudaEvent_t b = pool_event(ctx);
     cudaEventRecord(b, st);
-    ctx->prof_recs.push_back({kind, a, b, flops, bytes});
+    ctx->prof_recs.push_back({kind, a, b, flops, bytes, M, N, K, epi});
   }
 };
 
@@ -223,7 +226,7 @@ static bool g_tc_attn = true;
 static void gemm(ig_ctx* ctx, const GemmArgs& g, cudaStream_t st) {
   if (g.M <= 0 || g.N <= 0) return;
   ctx->stats.kernel_launches++;
-  ProfScope ps(ctx, st, IG_K_GEMM, 2.0 * g.M * g.N * g.K, 0.0);
+  ProfScope ps(ctx, st, IG_K_GEMM, 2.0 * g.M * g.N * g.K, 0.0, g.M, g.N, g.K, g.epi);
   if (ctx->d.dtype == IG_F32) launch_gemm_simt<float>(g, st);
   else if (g_tc_gemm && gemm_tc_supported(g)) launch_gemm_tc(g, st);
   else launch_gemm_simt<bf16>(g, st);
@@ -469,10 +472,13 @@ extern "C" ig_status ig_profile_enable(ig_ctx* ctx, int enable) {
 extern "C" ig_status ig_profile_read(ig_ctx* ctx, ig_prof_entry out[IG_K_NCLASS]) {
   if (!ctx || !out) return set_err(IG_EINVAL, "NULL argument");
   CUDA_TRY(cudaSetDevice(ctx->device));
+  const char* dump = getenv("IG_PROFILE_DUMP");
+  FILE* fd = dump ? fopen(dump, "a") : nullptr;
   for (auto& r : ctx->prof_recs) {
     CUDA_TRY(cudaEventSynchronize(r.b));
     float ms = 0.f;
     CUDA_TRY(cudaEventElapsedTime(&ms, r.a, r.b));
+    if (fd) fprintf(fd, "%d,%d,%d,%d,%d,%.6f,%.6g,%.6g\n", r.kind, r.M, r.N, r.K, r.epi, ms, r.flops, r.bytes);
     ig_prof_entry& e = ctx->prof_acc[r.kind];
     e.launches++;
     e.ms += ms;
@@ -481,6 +487,7 @@ extern "C" ig_status ig_profile_read(ig_ctx* ctx, ig_prof_entry out[IG_K_NCLASS]
     ctx->ev_pool.push_back(r.a);
     ctx->ev_pool.push_back(r.b);
   }
+  if (fd) fclose(fd);
   ctx->prof_recs.clear();
   for (int k = 0; k < IG_K_NCLASS; ++k) out[k] = ctx->prof_acc[k];
   for (int k = 0; k < IG_K_NCLASS; ++k) ctx->prof_acc[k] = ig_prof_entry{};
@@ -1028,6 +1035,30 @@ extern "C" ig_status ig_op_gemm(int dtype, const void* A, long long lda, const v
     if (!gemm_tc_supported(g)) return set_err(IG_EUNSUPPORTED, "shape not supported by the tcgen05 GEMM");
     launch_gemm_tc(g, st);
   } else return set_err(IG_EINVAL, "bad dtype");
+  CUDA_TRY(cudaGetLastError());
+  return IG_OK;
+}
+
+extern "C" ig_status ig_op_gemm_gated(int dtype, const void* A, long long lda, const void* B, long long ldb,
+                                      const void* bias, float* X, long long ldx, const float* gate, int M, int N,
+                                      int K, void* stream) {
+  if (!A || !B || !X || !gate) return set_err(IG_EINVAL, "NULL argument");
+  if (M < 0 || N <= 0 || K <= 0) return set_err(IG_EINVAL, "bad shape");
+  cudaStream_t st = (cudaStream_t)stream;
+  RowInfo* ri = nullptr;  // every row belongs to request 0
+  if (M > 0) {
+    CUDA_TRY(cudaMallocAsync((void**)&ri, (size_t)M * sizeof(RowInfo), st));
+    CUDA_TRY(cudaMemsetAsync(ri, 0, (size_t)M * sizeof(RowInfo), st));
+  }
+  GemmArgs g{};
+  g.A = A; g.lda = lda; g.B = B; g.ldb = ldb; g.bias = bias; g.C = X; g.ldc = ldx;
+  g.M = M; g.N = N; g.K = K; g.epi = EPI_GATED_RES; g.gate = gate; g.gate_ld = 0; g.ri = ri; g.ri_off = 0;
+  if (dtype == IG_F32) launch_gemm_simt<float>(g, st);
+  else if (dtype == IG_BF16) {
+    if (!gemm_tc_supported(g)) { if (ri) cudaFreeAsync(ri, st); return set_err(IG_EUNSUPPORTED, "shape not supported by the tcgen05 GEMM"); }
+    launch_gemm_tc(g, st);
+  } else return set_err(IG_EINVAL, "bad dtype");
+  if (ri) CUDA_TRY(cudaFreeAsync(ri, st));
   CUDA_TRY(cudaGetLastError());
   return IG_OK;
 }

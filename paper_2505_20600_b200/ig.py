@@ -23,7 +23,7 @@ STATUS = {0: "IG_OK", 1: "IG_EINVAL", 2: "IG_ECACHE_INCOMPAT", 3: "IG_ECACHE_MIS
 EXPORTS = ["ig_weight_count", "ig_ctx_create", "ig_ctx_destroy", "ig_cache_create",
            "ig_cache_template", "ig_cache_storage", "ig_cache_free", "ig_mask_build",
            "ig_mask_indices", "ig_mask_free", "ig_edit_step", "ig_prefetch_layer",
-           "ig_last_error", "ig_last_stats", "ig_op_gemm", "ig_op_attention", "ig_copy",
+           "ig_last_error", "ig_last_stats", "ig_op_gemm", "ig_op_gemm_gated", "ig_op_attention", "ig_copy",
            "ig_profile_enable", "ig_profile_read"]
 KCLASS = ["gemm", "attn", "lnmod", "qkvpost", "cond", "rows"]
 
@@ -100,6 +100,7 @@ def lib():
         L.ig_op_gemm.argtypes = [i, vp, ll, vp, ll, vp, vp, ll, i, i, i, i, i, vp]
         L.ig_op_attention.argtypes = [i, vp, ll, vp, ll, vp, P(ctypes.c_int32), i, i, i, i, vp]
         L.ig_copy.argtypes = [vp, vp, ctypes.c_size_t, vp]
+        L.ig_op_gemm_gated.argtypes = [i, vp, ll, vp, ll, vp, vp, ll, vp, i, i, i, vp]
         L.ig_profile_enable.argtypes = [vp, i]
         L.ig_profile_read.argtypes = [vp, P(ig_prof_entry)]
         for name in EXPORTS:
@@ -212,6 +213,10 @@ def ig_last_stats(ctx: int) -> dict:
 def ig_op_gemm(dtype, A, lda, B, ldb, bias, C, ldc, M, N, K, epi=0, out_f32=0, stream=0):
     _check(lib().ig_op_gemm(dtype, A, lda, B, ldb, bias or None, C, ldc, M, N, K, epi, out_f32,
                             stream))
+
+
+def ig_op_gemm_gated(dtype, A, lda, B, ldb, bias, X, ldx, gate, M, N, K, stream=0):
+    _check(lib().ig_op_gemm_gated(dtype, A, lda, B, ldb, bias or None, X, ldx, gate, M, N, K, stream))
 
 
 def ig_op_attention(dtype, Q, ldq, O, ldo, kv, segs, L, heads, head_dim, stream=0):

@@ -200,3 +200,22 @@ def test_degenerate_and_errors():
     ig.ig_cache_free(cache)
     empty.free(); part.free()
     m.close()
+
+
+@pytest.mark.parametrize("dtype", [ig.IG_F32, ig.IG_BF16])
+@pytest.mark.parametrize("M,N,K", [(129, 256, 192), (300, 3072, 320)])
+def test_gemm_gated_residual_vs_oracle(dtype, M, N, K):
+    tdt = torch.float32 if dtype == ig.IG_F32 else torch.bfloat16
+    A = synth.uniform(1, "A", (M, K), "cuda").float().to(tdt)
+    B = (synth.uniform(2, "B", (N, K), "cuda") / K ** 0.5).float().to(tdt)
+    bias = synth.uniform(3, "b", (N,), "cuda").float().to(tdt)
+    X0 = synth.normal(4, "X", (M, N), "cuda").float()
+    gate = synth.uniform(5, "g", (N,), "cuda").float()
+    X = X0.clone()
+    ig.ig_op_gemm_gated(dtype, A.data_ptr(), K, B.data_ptr(), K, bias.data_ptr(), X.data_ptr(), N,
+                        gate.data_ptr(), M, N, K, 0)
+    torch.cuda.synchronize()
+    y = oracle.linear(A.double().cpu().numpy(), B.double().cpu().numpy(), bias.double().cpu().numpy())
+    ref = X0.double().cpu().numpy() + gate.double().cpu().numpy() * y
+    ok, worst = ctol(X.cpu().numpy(), ref, 1e-4 if dtype == ig.IG_F32 else 2e-3)
+    assert ok, worst

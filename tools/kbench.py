@@ -1,0 +1,49 @@
+"""Kernel micro-bench for the two tensor-core kernels at Flux step shapes (through ig_ops)."""
+import sys, os, json, argparse
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+import synth
+from paper_2505_20600_b200 import ig
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--which", default="gemm,attn")
+ap.add_argument("--M", type=int, default=14720)
+ap.add_argument("--N", type=int, default=3072)
+ap.add_argument("--K", type=int, default=3072)
+ap.add_argument("--iters", type=int, default=10)
+args = ap.parse_args()
+res = {}
+def timeit(fn, iters):
+    for _ in range(2): fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+    e0.record()
+    for _ in range(iters): fn()
+    e1.record(); torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / iters
+if "gemm" in args.which:
+    M, N, K = args.M, args.N, args.K
+    A = torch.randn(M, K, device="cuda", dtype=torch.bfloat16)
+    B = torch.randn(N, K, device="cuda", dtype=torch.bfloat16) / K ** 0.5
+    C = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    ms = timeit(lambda: ig.ig_op_gemm(ig.IG_BF16, A.data_ptr(), K, B.data_ptr(), K, 0, C.data_ptr(), N, M, N, K, 0, 0, 0), args.iters)
+    ref = timeit(lambda: torch.matmul(A, B.t(), out=C), args.iters)
+    X = torch.zeros(M, N, device="cuda", dtype=torch.float32)
+    gate = torch.rand(N, device="cuda", dtype=torch.float32)
+    msg = timeit(lambda: ig.ig_op_gemm_gated(ig.IG_BF16, A.data_ptr(), K, B.data_ptr(), K, 0, X.data_ptr(), N, gate.data_ptr(), M, N, K, 0), args.iters)
+    res["gemm_gated_tflops"] = 2 * M * N * K / msg / 1e9
+    res["gemm"] = {"M": M, "N": N, "K": K, "ms": ms, "tflops": 2 * M * N * K / ms / 1e9, "cublas_tflops": 2 * M * N * K / ref / 1e9}
+if "attn" in args.which:
+    heads, dh, L = 24, 128, 4608
+    qlens = [512, 1843] * 8
+    H = heads * dh
+    M = sum(qlens)
+    Q = torch.randn(M, H, device="cuda", dtype=torch.bfloat16)
+    kv = torch.randn(8, 2, L, H, device="cuda", dtype=torch.bfloat16)
+    O = torch.empty(M, H, device="cuda", dtype=torch.bfloat16)
+    segs, s = [], 0
+    for i, q in enumerate(qlens):
+        segs.append((s, q, i // 2)); s += q
+    ms = timeit(lambda: ig.ig_op_attention(ig.IG_BF16, Q.data_ptr(), H, O.data_ptr(), H, kv.data_ptr(), segs, L, heads, dh, 0), args.iters)
+    res["attn"] = {"M": M, "ms": ms, "tflops": 4 * M * L * H / ms / 1e9}
+print(json.dumps(res))
