@@ -262,7 +262,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--max-batch", type=int, default=8)
     ap.add_argument("--tier", default=None, choices=["host", "device"])
-    ap.add_argument("--copy-mode", type=int, default=0)
+    ap.add_argument("--copy-mode", type=int, default=1)
     ap.add_argument("--depth", type=int, default=2)
     ap.add_argument("--dense-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")

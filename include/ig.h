@@ -82,8 +82,11 @@ typedef struct {
   int max_rows;        /* max packed query rows per step, sum_r (L_txt + n_m,r) (default  */
                        /* max_batch * L)                                                  */
   int prefetch_depth;  /* D: layers the copy lane runs ahead of compute (default 2)       */
-  int copy_mode;       /* 0 = full-L per-layer cudaMemcpyAsync (v1), 1 = compacted:       */
-                       /*     unmasked rows only, zero-copy gather kernel on the copy lane */
+  int copy_mode;       /* 0 = full-L per-layer cudaMemcpyAsync (all L_img rows),          */
+                       /* 1 = compacted: only unmasked rows, as contiguous runs of the     */
+                       /*     unmasked index list in one cudaMemcpyBatchAsync per layer    */
+                       /*     (copy engines),                                              */
+                       /* 2 = compacted: zero-copy SM gather kernel on the copy stream     */
   int debug_checks;    /* 1 = check the latent for non-finite values after each step     */
 } ig_ctx_opts;
 

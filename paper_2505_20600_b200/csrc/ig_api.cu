@@ -82,6 +82,7 @@ constexpr int MAXR = 8;  // max ring depth R = D + 1
 
 struct ig_mask {
   int L_img = 0, n_m = 0;
+  std::vector<std::pair<int, int>> runs;  // host: maximal runs (start, len) of unmasked tokens
   int32_t* idx = nullptr;  // device: idx_m at [0, L_img), idx_u at [L_img, 2 L_img), n_m at [2 L_img]
 };
 
@@ -135,6 +136,8 @@ struct ig_ctx {
   struct Pref { const ig_cache* c = nullptr; int step = -1; };
   std::vector<Pref> pref;  // [max_batch * R]
   ig_mask* ones_mask = nullptr;
+  std::vector<void*> b_dst, b_src;  // batched-copy scratch (copy_mode 1)
+  std::vector<size_t> b_size;
   ig_stats stats{};
   std::vector<ig_cache*> zombies;
   // live profiling (ig_profile_enable)
@@ -309,7 +312,7 @@ extern "C" ig_status ig_ctx_create(const ig_model_desc* desc, const void* const*
   if (o.max_batch > 16) return set_err(IG_EUNSUPPORTED, "max_batch > 16");
   if (o.prefetch_depth <= 0) o.prefetch_depth = 2;
   if (o.prefetch_depth + 1 > MAXR) return set_err(IG_EUNSUPPORTED, "prefetch_depth > %d", MAXR - 1);
-  if (o.copy_mode != 0 && o.copy_mode != 1) return set_err(IG_EINVAL, "copy_mode must be 0 or 1");
+  if (o.copy_mode < 0 || o.copy_mode > 2) return set_err(IG_EINVAL, "copy_mode must be 0, 1 or 2");
   const int Lall = desc->txt_len + desc->grid_h * desc->grid_w;
   if (o.max_rows <= 0) o.max_rows = o.max_batch * Lall;
 
@@ -518,8 +521,17 @@ extern "C" ig_status ig_mask_build(ig_ctx* ctx, const uint8_t* mask, void* strea
   }
   launch_mask_index(mask, ctx->Limg, m->idx, m->idx + ctx->Limg, m->idx + 2 * ctx->Limg, st);
   int32_t n = 0;
+  std::vector<uint8_t> hm(ctx->Limg);
   cudaError_t e = cudaMemcpyAsync(&n, m->idx + 2 * ctx->Limg, sizeof(int32_t), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(hm.data(), mask, ctx->Limg, cudaMemcpyDeviceToHost, st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  for (int i = 0; i < ctx->Limg;) {  // unmasked runs for the compacted DMA copy (copy_mode 1)
+    if (hm[i]) { ++i; continue; }
+    int j = i;
+    while (j < ctx->Limg && !hm[j]) ++j;
+    m->runs.push_back({i, j - i});
+    i = j;
+  }
   if (e != cudaSuccess) {
     cudaFree(m->idx);
     delete m;
@@ -637,7 +649,7 @@ static void issue_copy(ig_ctx* ctx, const std::vector<StepReq>& sr, const KvGath
   const int buf = b % ctx->R;
   cudaStreamWaitEvent(ctx->copy_st, ctx->ev_comp[buf], 0);
   const int n = (int)sr.size();
-  if (ctx->o.copy_mode == 1) {
+  if (ctx->o.copy_mode == 2) {
     ctx->stats.kernel_launches++;
     launch_kv_gather(kvg_dev + (size_t)b * n, n, max_nu, ctx->Lt, ctx->H, (int)ctx->esz, ctx->copy_st);
     for (int q = 0; q < n; ++q)
@@ -645,6 +657,39 @@ static void issue_copy(ig_ctx* ctx, const std::vector<StepReq>& sr, const KvGath
         const long long by = 2LL * kvg_host[(size_t)b * n + q].n_u * ctx->H * ctx->esz;
         if (sr[q].r->cache->tier == IG_CACHE_HOST) ctx->stats.h2d_bytes += by; else ctx->stats.d2d_bytes += by;
       }
+  } else if (ctx->o.copy_mode == 1) {
+    // compacted: only the unmasked rows, as runs of consecutive tokens, one batched DMA call
+    const size_t row = (size_t)ctx->H * ctx->esz;
+    const size_t plane = (size_t)ctx->Limg * row;
+    const size_t txt_off = (size_t)ctx->Lt * row, vplane = (size_t)ctx->L * row;
+    std::vector<void*>& dsts = ctx->b_dst;
+    std::vector<void*>& srcs = ctx->b_src;
+    std::vector<size_t>& sizes = ctx->b_size;
+    dsts.clear(); srcs.clear(); sizes.clear();
+    long long by = 0;
+    bool host = false;
+    for (int q = 0; q < n; ++q) {
+      if (!sr[q].use_cache) continue;
+      const ig_edit_req* r = sr[q].r;
+      host |= r->cache->tier == IG_CACHE_HOST;
+      const char* src = (const char*)r->cache->ptr + ((size_t)r->step * ctx->nb + b) * 2 * plane;
+      char* dst = (char*)ctx->kv_arena + ((size_t)r->slot * ctx->slot_stride + (size_t)buf * ctx->buf_elems) * ctx->esz;
+      for (auto& run : sr[q].m->runs) {
+        const size_t off = (size_t)run.first * row, len = (size_t)run.second * row;
+        dsts.push_back(dst + txt_off + off); srcs.push_back((void*)(src + off)); sizes.push_back(len);
+        dsts.push_back(dst + vplane + txt_off + off); srcs.push_back((void*)(src + plane + off)); sizes.push_back(len);
+        by += 2 * (long long)len;
+      }
+    }
+    if (!sizes.empty()) {
+      cudaMemcpyAttributes attr{};
+      attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
+      attr.flags = cudaMemcpyFlagPreferOverlapWithCompute;
+      size_t attr_idx = 0, fail = 0;
+      cudaMemcpyBatchAsync(dsts.data(), srcs.data(), sizes.data(), sizes.size(), &attr, &attr_idx, 1, &fail,
+                           ctx->copy_st);
+    }
+    if (host) ctx->stats.h2d_bytes += by; else ctx->stats.d2d_bytes += by;
   } else {
     const size_t plane = (size_t)ctx->Limg * ctx->H * ctx->esz;
     for (int q = 0; q < n; ++q) {
@@ -749,7 +794,7 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
     img_row += d.n_m;
   }
   std::vector<KvGatherReq> kvg_host;
-  if (any_cache && ctx->o.copy_mode == 1) {
+  if (any_cache && ctx->o.copy_mode == 2) {
     kvg_host.resize((size_t)nb * na);
     const size_t plane = (size_t)ctx->Limg * H;
     for (int b = 0; b < nb; ++b)
@@ -770,7 +815,7 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
         hkvg[(size_t)b * na + q] = g;
       }
   }
-  const size_t desc_bytes = (char*)(hkvg + (any_cache && ctx->o.copy_mode == 1 ? (size_t)nb * na : 0)) - hs;
+  const size_t desc_bytes = (char*)(hkvg + (any_cache && ctx->o.copy_mode == 2 ? (size_t)nb * na : 0)) - hs;
   CUDA_TRY(cudaMemcpyAsync(ds, hs, desc_bytes, cudaMemcpyHostToDevice, st));
   CUDA_TRY(cudaEventRecord(ctx->ev_desc, st));
   if (any_cache) CUDA_TRY(cudaStreamWaitEvent(ctx->copy_st, ctx->ev_desc, 0));
@@ -871,8 +916,14 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
     if (record->tier == IG_CACHE_HOST) stats.d2h_bytes += 2 * plane; else stats.d2d_bytes += 2 * plane;
     cudaEventRecord(ctx->ev_copy[buf], ctx->copy_st);
   };
+  // full-L copies also write the masked rows, so they must land before the fresh K/V
+  // scatter; compacted copies touch only unmasked rows and are awaited right before attention
+  const bool late_wait = ctx->o.copy_mode != 0 && !record;
   auto wait_copy = [&](int buf) {
-    if (any_cache || record) cudaStreamWaitEvent(st, ctx->ev_copy[buf], 0);
+    if ((any_cache || record) && !late_wait) cudaStreamWaitEvent(st, ctx->ev_copy[buf], 0);
+  };
+  auto wait_copy_late = [&](int buf) {
+    if (any_cache && late_wait) cudaStreamWaitEvent(st, ctx->ev_copy[buf], 0);
   };
 
   // ---- blocks ----
@@ -888,6 +939,7 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
       wait_copy(buf);
       qkv_post(M_txt, M, wi.qg, wi.kg, buf);
       if (Lt) qkv_post(0, M_txt, wt.qg, wt.kg, buf);
+      wait_copy_late(buf);
       attn(buf);
       record_kv(b, buf);
       cudaEventRecord(ctx->ev_comp[buf], st);
@@ -913,6 +965,7 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
       gemm_rows(0, M, h, H, w_u, b_u, F, H, cat + H, ldcat, EPI_GELU, nullptr, 0);
       wait_copy(buf);
       qkv_post(0, M, ws.qg, ws.kg, buf);
+      wait_copy_late(buf);
       attn(buf);
       record_kv(b, buf);
       cudaEventRecord(ctx->ev_comp[buf], st);

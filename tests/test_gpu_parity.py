@@ -142,7 +142,7 @@ def test_tiny_config_end_to_end(dtype):
 
 
 @pytest.mark.parametrize("dtype", [ig.IG_F32, ig.IG_BF16])
-@pytest.mark.parametrize("copy_mode", [0, 1])
+@pytest.mark.parametrize("copy_mode", [0, 1, 2])
 def test_flux_small_batch_end_to_end(dtype, copy_mode):
     """Flux-structured small model (2 double + 2 single blocks, text tokens): a continuous
     batch of 3 requests with different masks (rectangle, blob, all-ones) and a synthetic
