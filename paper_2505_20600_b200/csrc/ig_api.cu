@@ -24,6 +24,20 @@
 
 using namespace ig;
 
+#include <execinfo.h>
+#include <signal.h>
+#include <unistd.h>
+// IG_SEGV_TRACE=1: print a native backtrace of libig on SIGSEGV (debug aid)
+static void ig_segv_handler(int sig) {
+  void* buf[64];
+  int n = backtrace(buf, 64);
+  backtrace_symbols_fd(buf, n, 2);
+  _exit(128 + sig);
+}
+__attribute__((constructor)) static void ig_install_trace() {
+  if (getenv("IG_SEGV_TRACE")) signal(SIGSEGV, ig_segv_handler);
+}
+
 // ----------------------------------------------------------------------------------------
 // errors
 // ----------------------------------------------------------------------------------------
@@ -686,8 +700,12 @@ static void issue_copy(ig_ctx* ctx, const std::vector<StepReq>& sr, const KvGath
       attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
       attr.flags = cudaMemcpyFlagPreferOverlapWithCompute;
       size_t attr_idx = 0, fail = 0;
-      cudaMemcpyBatchAsync(dsts.data(), srcs.data(), sizes.data(), sizes.size(), &attr, &attr_idx, 1, &fail,
-                           ctx->copy_st);
+      constexpr size_t CHUNKC = 128;  // bounded batches (very large batches crash driver 580)
+      for (size_t i = 0; i < sizes.size(); i += CHUNKC) {
+        const size_t c = std::min(CHUNKC, sizes.size() - i);
+        cudaMemcpyBatchAsync(dsts.data() + i, srcs.data() + i, sizes.data() + i, c, &attr, &attr_idx, 1, &fail,
+                             ctx->copy_st);
+      }
     }
     if (host) ctx->stats.h2d_bytes += by; else ctx->stats.d2d_bytes += by;
   } else {
