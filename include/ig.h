@@ -199,6 +199,15 @@ typedef struct {
 ig_status ig_profile_enable(ig_ctx* ctx, int enable);
 ig_status ig_profile_read(ig_ctx* ctx, ig_prof_entry out[IG_K_NCLASS]);
 
+/* Teacher-forced single block (debug/parity export): runs block `block` of the
+ * step for ONE request on caller-given packed input rows and writes the packed output rows.
+ * X_in, X_out: dev fp32 [txt_len + n_m, H], rows ordered [text 0..L_txt-1 | masked image
+ * tokens ascending] (C-AMB 15).  The block's cached K/V come from (req->cache, req->step) and
+ * the modulation from (req->sigma, req->cond_vec) exactly as in ig_edit_step.  The latent is
+ * not touched.  Synchronous on `stream`. */
+ig_status ig_debug_block(ig_ctx* ctx, const ig_edit_req* req, int block, const float* X_in,
+                         float* X_out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

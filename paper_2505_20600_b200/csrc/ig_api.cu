@@ -730,10 +730,19 @@ static void issue_copy(ig_ctx* ctx, const std::vector<StepReq>& sr, const KvGath
   cudaEventRecord(ctx->ev_copy[buf], ctx->copy_st);
 }
 
+// Optional restriction of a step to blocks [b0, b1) on caller-given residual rows (the
+// teacher-forced debug hook); defaults run the whole step.
+struct StepRange {
+  int b0 = 0, b1 = -1;
+  const float* X_in = nullptr;
+  float* X_out = nullptr;
+};
+
 template <typename T>
 static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStream_t st,
-                          ig_cache* record, int record_step) {
+                          ig_cache* record, int record_step, const StepRange& rng = StepRange()) {
   const int H = ctx->H, F = ctx->F, C = ctx->C, Lt = ctx->Lt, nb = ctx->nb, R = ctx->R;
+  const int b0 = rng.b0, b1 = rng.b1 < 0 ? nb : rng.b1;
   const long long es = (long long)ctx->esz;
   ctx->stats = ig_stats{};
   // ---- host validation (nothing enqueued before this passes) ----
@@ -840,7 +849,7 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
   for (auto& s : sr) if (s.use_cache) { s.r->cache->pins.fetch_add(1); }
 
   // ---- prefetch the first R blocks (copy lane) ----
-  for (int b = 0; b < std::min(R, nb); ++b) issue_copy(ctx, sr, dkvg, kvg_host, b, any_cache, max_nu);
+  for (int b = b0; b < std::min(b0 + R, b1); ++b) issue_copy(ctx, sr, dkvg, kvg_host, b, any_cache, max_nu);
 
   T* h = (T*)ctx->h;
   T* qkv = (T*)ctx->qkv;
@@ -863,7 +872,9 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
   launch_gemv<T>(ctx->gv_mod, (int)ctx->gv_mod_host.size(), ctx->gv_mod_groups, na, H, st);
   }
   stats.kernel_launches += 7;
-  {  // img_in (+ SD3 pos_embed) into the fp32 residual X
+  if (rng.X_in) {  // teacher-forced residual rows
+    CUDA_TRY(cudaMemcpyAsync(ctx->X, rng.X_in, (size_t)M * H * 4, cudaMemcpyDeviceToDevice, st));
+  } else {  // img_in (+ SD3 pos_embed) into the fp32 residual X
     GemmArgs g{};
     g.A = ctx->Ain; g.lda = C; g.B = ctx->img_in.w; g.ldb = C; g.bias = ctx->img_in.b;
     g.C = ctx->X + (long long)M_txt * H; g.ldc = H; g.M = M_img; g.N = H; g.K = C;
@@ -945,7 +956,7 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
   };
 
   // ---- blocks ----
-  for (int b = 0; b < nb; ++b) {
+  for (int b = b0; b < b1; ++b) {
     const int buf = b % R;
     if (b < ctx->d.n_double) {
       const StreamW& wi = ctx->dimg[b];
@@ -961,7 +972,7 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
       attn(buf);
       record_kv(b, buf);
       cudaEventRecord(ctx->ev_comp[buf], st);
-      if (b + R < nb) issue_copy(ctx, sr, dkvg, kvg_host, b + R, any_cache, max_nu);
+      if (b + R < b1) issue_copy(ctx, sr, dkvg, kvg_host, b + R, any_cache, max_nu);
       const long long gi = ctx->mods[wi.mod_t].off;
       gemm_rows(M_txt, M, cat, ldcat, wi.proj.w, wi.proj.b, H, H, ctx->X, H, EPI_GATED_RES, mod + gi + 2 * H, 0);
       ln_mod(M_txt, M, wi.mod_t, 3, 4);
@@ -987,30 +998,49 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
       attn(buf);
       record_kv(b, buf);
       cudaEventRecord(ctx->ev_comp[buf], st);
-      if (b + R < nb) issue_copy(ctx, sr, dkvg, kvg_host, b + R, any_cache, max_nu);
+      if (b + R < b1) issue_copy(ctx, sr, dkvg, kvg_host, b + R, any_cache, max_nu);
       const long long gs = ctx->mods[ws.mod_t].off;
       gemm_rows(0, M, cat, ldcat, ws.lin2.w, ws.lin2.b, H, H + F, ctx->X, H, EPI_GATED_RES, mod + gs + 2 * H, 0);
     }
   }
-  // ---- a11: final layer + Euler scatter ----
-  ln_mod(M_txt, M, ctx->fmod_t, 1, 0);  // final chunk order (scale, shift)
-  gemm_rows(M_txt, M, h, H, ctx->pout.w, ctx->pout.b, C, H, ctx->vel - (long long)M_txt * C, C, EPI_STORE, nullptr, 1);
-  launch_scatter_euler(dreq, na, M_img, ctx->ri, M_txt, C, ctx->vel, st);
-  stats.kernel_launches++;
+  if (rng.X_out) {
+    CUDA_TRY(cudaMemcpyAsync(rng.X_out, ctx->X, (size_t)M * H * 4, cudaMemcpyDeviceToDevice, st));
+  } else {
+    // ---- a11: final layer + Euler scatter ----
+    ln_mod(M_txt, M, ctx->fmod_t, 1, 0);  // final chunk order (scale, shift)
+    gemm_rows(M_txt, M, h, H, ctx->pout.w, ctx->pout.b, C, H, ctx->vel - (long long)M_txt * C, C, EPI_STORE, nullptr, 1);
+    launch_scatter_euler(dreq, na, M_img, ctx->ri, M_txt, C, ctx->vel, st);
+    stats.kernel_launches++;
+  }
   // the copy lane must not run ahead into the next step's buffers before compute is done
   CUDA_TRY(cudaEventRecord(ctx->ev_stage[si], st));
   for (auto& s : sr)
     if (s.use_cache) CUDA_TRY(cudaLaunchHostFunc(st, unpin_cb, (void*)s.r->cache));
-  if (record) CUDA_TRY(cudaStreamWaitEvent(st, ctx->ev_copy[(nb - 1) % R], 0));
+  if (record) CUDA_TRY(cudaStreamWaitEvent(st, ctx->ev_copy[(b1 - 1) % R], 0));
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_err(IG_ECUDA, "step enqueue: %s", cudaGetErrorString(e));
   return IG_OK;
 }
 
 static ig_status step_dispatch(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStream_t st,
-                               ig_cache* record, int record_step) {
-  if (ctx->d.dtype == IG_F32) return run_step<float>(ctx, reqs, n, st, record, record_step);
-  return run_step<bf16>(ctx, reqs, n, st, record, record_step);
+                               ig_cache* record, int record_step, const StepRange& rng = StepRange()) {
+  if (ctx->d.dtype == IG_F32) return run_step<float>(ctx, reqs, n, st, record, record_step, rng);
+  return run_step<bf16>(ctx, reqs, n, st, record, record_step, rng);
+}
+
+extern "C" ig_status ig_debug_block(ig_ctx* ctx, const ig_edit_req* req, int block, const float* X_in,
+                                    float* X_out, void* stream) {
+  if (!ctx || !req || !X_in || !X_out) return set_err(IG_EINVAL, "NULL argument");
+  if (block < 0 || block >= ctx->nb) return set_err(IG_EINVAL, "block %d out of range", block);
+  if (!req->mask || req->mask->n_m == 0) return set_err(IG_EINVAL, "debug block needs n_m > 0");
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  StepRange rng;
+  rng.b0 = block; rng.b1 = block + 1; rng.X_in = X_in; rng.X_out = X_out;
+  cudaStream_t st = (cudaStream_t)stream;
+  ig_status s = step_dispatch(ctx, req, 1, st, nullptr, 0, rng);
+  if (s != IG_OK) return s;
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return IG_OK;
 }
 
 extern "C" ig_status ig_edit_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, void* stream) {

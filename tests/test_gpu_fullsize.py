@@ -1,0 +1,113 @@
+"""Full-size (Flux.1-dev-shaped, BASELINE configs[2]) GPU checks in the launch configuration
+bench.py times (bf16, tcgen05 kernels, max_batch 8 context):
+
+* teacher-forced blocks: one double and one single block at full width
+  (H = 3072, L = 4608) through ig_debug_block vs the oracle's block functions on the same
+  inputs, m in {0.05, 0.2, 0.6}; compared on the block's update (X_out - X_in) with C-TOL 2e-2;
+* exactness invariants at full scale: with a cache recorded from the same
+  trajectory, the edited masked rows equal the dense step's rows bitwise; unmasked rows are
+  untouched; a request alone equals the same request inside a batch, bitwise.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from paper_2505_20600_b200 import ig
+from gpu_util import Model, Request, ctol
+
+pytestmark = pytest.mark.gpu
+
+D = synth.FLUX
+
+
+@pytest.fixture(scope="module")
+def flux():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    m = Model(D, ig.IG_BF16, opts=ig.ig_ctx_opts(8, 8 * D.L, 2, 1, 0))
+    yield m
+    m.close()
+
+
+def _host_block_weights(names):
+    return {k: v.double().numpy() for k, v in synth.make_weights(D, 0, "cpu", torch.bfloat16, names=names).items()}
+
+
+def _fill_cache_block(cache, block, step_count, kv):
+    """Write kv [2, L_img, H] (bf16) into (step 0, block) of a device-tier cache."""
+    ptr, nbytes, tier = ig.ig_cache_storage(cache)
+    plane = D.L_img * D.hidden * 2
+    off = (0 * D.n_blocks + block) * 2 * plane
+    src = kv.contiguous()
+    ig.ig_copy(ptr + off, src.data_ptr(), 2 * plane)
+
+
+@pytest.mark.parametrize("block,m_ratio,kind", [(3, 0.05, "rect"), (3, 0.6, "blob"), (19 + 7, 0.2, "rect")])
+def test_flux_teacher_forced_block(flux, block, m_ratio, kind):
+    rng = np.random.default_rng(block)
+    n = int(round(m_ratio * D.L_img))
+    mask = synth.rect_mask_count(D, n, rng) if kind == "rect" else synth.blob_mask_count(D, n, rng)
+    rq = Request(flux, 77 + block, mask)
+    cache = ig.ig_cache_create(flux.ctx, 1, ig.IG_CACHE_DEVICE)
+    kv = synth.normal(500 + block, "kv_blk", (2, D.L_img, D.hidden), "cuda").float().bfloat16()
+    _fill_cache_block(cache, block, 1, kv)
+    rows = D.txt_len + rq.n_m
+    X_in = synth.normal(900 + block, "X_in", (rows, D.hidden), "cuda").float()
+    X_out = torch.full_like(X_in, float("nan"))
+    sigma, sigma_next = 0.7, 0.65
+    ig.ig_debug_block(flux.ctx, rq.req(0, cache, 0, sigma, sigma_next), block, X_in.data_ptr(), X_out.data_ptr())
+    # oracle on the same inputs
+    if block < D.n_double:
+        names = {nm for nm, _, _ in synth.weight_table(D) if nm.startswith(f"double.{block}.")}
+    else:
+        names = {nm for nm, _, _ in synth.weight_table(D) if nm.startswith(f"single.{block - D.n_double}.")}
+    names |= {"t_mlp1.w", "t_mlp1.b", "t_mlp2.w", "t_mlp2.b"}
+    W = _host_block_weights(names)
+    _, _, cond = rq.host_inputs()
+    vec = oracle.conditioning(W, sigma, cond)
+    idx_m, idx_u, _ = oracle.index_build(mask)
+    Xh = X_in.double().cpu().numpy()
+    kvh = kv.double().cpu().numpy()
+    if block < D.n_double:
+        xt, xi = oracle.double_block_masked(D, W, block, Xh[:D.txt_len], Xh[D.txt_len:], vec, idx_m, idx_u, kvh)
+        ref = np.concatenate([xt, xi])
+    else:
+        ref = oracle.single_block_masked(D, W, block - D.n_double, Xh, vec, idx_m, idx_u, kvh)
+    got = X_out.double().cpu().numpy()
+    assert np.isfinite(got).all()
+    ok, worst = ctol(got - Xh, ref - Xh, 2e-2)
+    assert ok, ("update", worst)
+    ig.ig_cache_free(cache)
+    rq.free()
+
+
+def test_flux_same_trajectory_bitwise_and_batch_invariance(flux):
+    sig = (1.0, 0.96)
+    rng = np.random.default_rng(5)
+    mask = synth.blob_mask_count(D, 1400, rng)
+    a = Request(flux, 31, mask)
+    # dense step of the same request = the template's own first step, recording its K/V
+    lat_dense = a.latent.clone()
+    cache = ig.ig_cache_template(flux.ctx, lat_dense.data_ptr(), a.txt.data_ptr(), a.cond.data_ptr(), sig,
+                                 ig.IG_CACHE_DEVICE, 0)
+    # edit alone
+    ig.ig_edit_step(flux.ctx, [a.req(0, cache, 0, *sig)], 0)
+    torch.cuda.synchronize()
+    idx = torch.from_numpy(np.flatnonzero(mask)).cuda()
+    un = torch.from_numpy(np.flatnonzero(mask == 0)).cuda()
+    assert torch.equal(a.latent[idx], lat_dense[idx]), \
+        float((a.latent[idx] - lat_dense[idx]).abs().max())
+    assert torch.equal(a.latent[un], a.latent0[un])
+    alone = a.latent.clone()
+    # the same request inside a batch of three (other masks, other slots, other order)
+    a.latent.copy_(a.latent0)
+    b = Request(flux, 32, synth.rect_mask_count(D, 700, rng))
+    c = Request(flux, 33, np.ones(D.L_img, np.uint8))
+    ig.ig_edit_step(flux.ctx, [b.req(0, cache, 0, *sig), c.req(1, None, 0, *sig), a.req(5, cache, 0, *sig)], 0)
+    torch.cuda.synchronize()
+    assert torch.equal(a.latent, alone)
+    ig.ig_cache_free(cache)
+    for r in (a, b, c):
+        r.free()
