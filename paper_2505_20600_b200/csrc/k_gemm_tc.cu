@@ -70,7 +70,7 @@ __device__ __forceinline__ void epilogue_chunk(const GemmArgs& g, int row, int c
   switch (g.epi) {
     case EPI_GELU:
 #pragma unroll
-      for (int i = 0; i < 32; ++i) v[i] = gelu_tanh_fast(v[i]);
+      for (int i = 0; i < 32; ++i) v[i] = g.precise_gelu ? gelu_tanh(v[i]) : gelu_tanh_fast(v[i]);
       // fallthrough
     case EPI_STORE: {
       if (g.out_f32) {

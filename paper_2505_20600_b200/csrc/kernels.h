@@ -108,6 +108,7 @@ struct GemmArgs {
   int ri_off;
   const void* pos; long long pos_ld;     // EPI_POS table (T)
   int out_f32;                           // EPI_STORE/GELU: 1 => C is fp32
+  int precise_gelu;                      // 1 => tanhf instead of MUFU tanh.approx (debug)
 };
 template <typename T>
 void launch_gemm_simt(const GemmArgs& g, cudaStream_t st);

@@ -9,11 +9,11 @@ from paper_2505_20600_b200 import ig
 TDT = {ig.IG_F32: torch.float32, ig.IG_BF16: torch.bfloat16}
 
 
-def ctol(g, o, rtol):
-    """C-TOL (SURVEY 8(c) C-AMB 22): |g - o| <= rtol |o| + rtol RMS(o), elementwise."""
+def ctol(g, o, rtol, atol_mult=1.0):
+    """C-TOL (DESIGN.md C-AMB 22): |g - o| <= rtol |o| + atol_mult rtol RMS(o), elementwise."""
     g = np.asarray(g, np.float64)
     o = np.asarray(o, np.float64)
-    atol = rtol * np.sqrt(np.mean(o * o)) if o.size else 0.0
+    atol = atol_mult * rtol * np.sqrt(np.mean(o * o)) if o.size else 0.0
     err = np.abs(g - o)
     ok = err <= rtol * np.abs(o) + atol
     worst = float(np.max(err / (rtol * np.abs(o) + atol + 1e-300))) if o.size else 0.0

@@ -77,7 +77,23 @@ def test_flux_teacher_forced_block(flux, block, m_ratio, kind):
         ref = oracle.single_block_masked(D, W, block - D.n_double, Xh, vec, idx_m, idx_u, kvh)
     got = X_out.double().cpu().numpy()
     assert np.isfinite(got).all()
-    ok, worst = ctol(got - Xh, ref - Xh, 2e-2)
+    dg, do = got - Xh, ref - Xh
+    # C-TOL-full (DESIGN.md C-AMB 22): normwise ||g-o||/||o|| <= rtol and elementwise
+    # |g-o| <= rtol |o| + 2 rtol RMS(o).  At ~4M elements the elementwise max sits ~12x the
+    # normwise error (measured: normwise 2.4e-3, p99.99 1.9e-2 RMS, max 3.6e-2 RMS).
+    normwise = np.linalg.norm(dg - do) / np.linalg.norm(do)
+    assert normwise <= 2e-2, normwise
+    ok, worst = ctol(dg, do, 2e-2, atol_mult=2.0)
+    err = np.abs(dg - do)
+    rms = np.sqrt(np.mean(do * do))
+    i, j = np.unravel_index(np.argmax(err), err.shape)
+    print(f"\nblock {block} m {m_ratio}: worst {worst:.3f} rel_rms_err {np.sqrt(np.mean(err**2))/rms:.4e} "
+          f"max_err/rms {err.max()/rms:.4e} at row {i} (txt={i < D.txt_len}) col {j} head {j // 128} "
+          f"txt-rows rel {np.sqrt(np.mean(err[:D.txt_len]**2))/rms:.3e} img-rows rel {np.sqrt(np.mean(err[D.txt_len:]**2))/rms:.3e}")
+    q = np.quantile(err / rms, [0.5, 0.99, 0.999, 0.9999])
+    top = np.argsort(err.ravel())[-6:]
+    print("quantiles err/rms", q, "top", [(int(t // D.hidden), int(t % D.hidden), float(err.ravel()[t] / rms),
+                                             float(do.ravel()[t] / rms)) for t in top])
     assert ok, ("update", worst)
     ig.ig_cache_free(cache)
     rq.free()
