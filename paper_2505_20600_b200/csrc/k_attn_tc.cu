@@ -3,16 +3,24 @@
 // along with the K and V matrices of all present tokens"): each ragged query segment of the
 // packed continuous batch attends to its own request's positional K/V buffer of L rows.
 //
-// One CTA per (query tile of 128 rows, head, segment):
-//   warp 0      TMA producer: Q tile once, then K/V tiles of 128 keys into a 2-stage ring
-//   warp 1      TMEM allocator + single-thread MMA issuer:
-//                 S_j = Q K_j^T   (SS, M=128 N=128 K=128, fp32 in TMEM, double-buffered)
-//                 O  += P_j V_j   (SS, P from shared memory, V MN-major, fp32 O in TMEM)
-//               S_{j+1} is issued before waiting for softmax j, so QK^T overlaps softmax.
-//   warps 4..7  softmax, thread = query row (TMEM lane): row max / exp2 / row sum in fp32,
-//               P (bf16) written to shared memory in the SW128 K-major layout; the O row is
-//               rescaled in TMEM only when that row's running max grows — a per-row decision,
-//               so a row's result never depends on its tile-mates (batch invariance).
+// One CTA per (pair of 128-row query tiles A/B, head, segment); 384 threads:
+//   warp 0       TMA producer: Q_A, Q_B once, then K/V tiles of 128 keys (2-stage ring,
+//                shared by both query tiles)
+//   warp 1       TMEM allocator + single-thread MMA issuer, ping-pong over the two tiles:
+//                  S_t = Q_t K_j^T      (SS, M=128 N=128 K=128, fp32 in TMEM)
+//                  O_t += P_t V_j       (TS: P read from TMEM where it overwrote S_t, V an
+//                                        MN-major smem operand; fp32 O_t in TMEM)
+//                while softmax group A works on S_A(j) the tensor core runs S_B(j) / PV_B(j-1)
+//   warps 4..7   softmax of tile A, warps 8..11 softmax of tile B; thread = query row (TMEM
+//                lane): row max, exp2, row sum in fp32, P packed to bf16 and stored back to
+//                TMEM (tcgen05.st).  Lazy O correction with a threshold: a row keeps its stale
+//                max unless the new max exceeds it by more than 8 (log2 units, P <= 2^8), and
+//                only rescales O then — decisions per row, so a row's result never depends on
+//                its tile-mates (batch invariance).
+// TMEM (512 columns): [S_A|P_A 128][O_A 128][S_B|P_B 128][O_B 128].
+// Ordering: tcgen05.mma execute in issue order, and S_t(j+1) is issued after PV_t(j), so when
+// softmax t sees S_t(j+1) complete (its commit covers every earlier MMA) PV_t(j) has finished
+// reading P_t(j) and writing O_t: O_t is stable for the correction, the P region is free.
 // Keys >= L (ragged last tile) are zero-filled by TMA and masked to -inf.
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -25,17 +33,17 @@ namespace {
 
 constexpr int BQ = 128, BKV = 128, D = 128;
 constexpr int CHUNK = 128 * 64 * 2;             // one [128 rows x 64 cols] bf16 SW128 box
-constexpr int Q_BYTES = 2 * CHUNK;              // 32 KB
+constexpr int Q_BYTES = 2 * CHUNK;              // 32 KB per query tile
 constexpr int KV_BYTES = 2 * CHUNK;             // 32 KB each for K and V
 constexpr int STAGES = 2;
-constexpr int SMEM_BYTES = Q_BYTES + STAGES * 2 * KV_BYTES + 2 * CHUNK /*P*/ + 1024 + 256;
-constexpr int NTHREADS = 256;
+constexpr int SMEM_BYTES = 2 * Q_BYTES + STAGES * 2 * KV_BYTES + 1024 + 256;
+constexpr int NTHREADS = 384;
+constexpr float RESCALE_THRESHOLD = 8.0f;       // log2 units
 
 struct Bars {
   uint64_t q_full;
   uint64_t kv_full[STAGES], kv_empty[STAGES];
-  uint64_t s_full[2], s_empty[2];
-  uint64_t p_full, pv_done;
+  uint64_t s_full[2], p_full[2], o_done[2];
   uint32_t tmem;
 };
 
@@ -44,26 +52,32 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   return *reinterpret_cast<uint32_t*>(&p);
 }
 
+__device__ __forceinline__ void tma_load_3d(void* smem, const CUtensorMap* m, uint64_t* bar, int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];"
+      ::"r"(tc::smem_u32(smem)), "l"(reinterpret_cast<uint64_t>(m)), "r"(tc::smem_u32(bar)), "r"(c0), "r"(c1),
+      "r"(c2) : "memory");
+}
+
 __global__ void __launch_bounds__(NTHREADS, 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmKV,
                    const AttnArgs a, float scale_log2) {
   const AttnSeg seg = a.segs[blockIdx.z];
   const int h = blockIdx.y;
-  const int q0 = blockIdx.x * BQ;
+  const int q0 = blockIdx.x * 2 * BQ;
   if (q0 >= seg.q_len) return;
+  const bool has_b = q0 + BQ < seg.q_len;
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sQ = smem;
-  uint8_t* sK = sQ + Q_BYTES;                      // [STAGES][KV_BYTES]
+  uint8_t* sQ = smem;                              // [2 tiles][Q_BYTES]
+  uint8_t* sK = sQ + 2 * Q_BYTES;                  // [STAGES][KV_BYTES]
   uint8_t* sV = sK + STAGES * KV_BYTES;            // [STAGES][KV_BYTES]
-  uint8_t* sP = sV + STAGES * KV_BYTES;            // [2 chunks][128 rows][128 B]
-  Bars* bar = reinterpret_cast<Bars*>(sP + 2 * CHUNK);
+  Bars* bar = reinterpret_cast<Bars*>(sV + STAGES * KV_BYTES);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nkv = (a.L + BKV - 1) / BKV;
   const long long H = (long long)a.heads * D;
-  // plane index of this segment's K (and V = K + 1) in the 3-D K/V tensor map
   const long long plane_elems = (long long)a.L * H;
   const int planeK = (int)((seg.kv_base + a.kv_off) / plane_elems);
 
@@ -72,9 +86,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     tc::tma_prefetch_desc(&tmKV);
     tc::mbar_init(&bar->q_full, 1);
     for (int s = 0; s < STAGES; ++s) { tc::mbar_init(&bar->kv_full[s], 1); tc::mbar_init(&bar->kv_empty[s], 1); }
-    for (int s = 0; s < 2; ++s) { tc::mbar_init(&bar->s_full[s], 1); tc::mbar_init(&bar->s_empty[s], 4); }
-    tc::mbar_init(&bar->p_full, 4);
-    tc::mbar_init(&bar->pv_done, 1);
+    for (int t = 0; t < 2; ++t) {
+      tc::mbar_init(&bar->s_full[t], 1);
+      tc::mbar_init(&bar->p_full[t], 4);
+      tc::mbar_init(&bar->o_done[t], 1);
+    }
     tc::fence_barrier_init();
   }
   if (warp == 1) tc::tmem_alloc<512>(&bar->tmem);
@@ -82,15 +98,17 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   __syncthreads();
   tc::tc_fence_after();
   const uint32_t tmem = bar->tmem;
-  const uint32_t tS[2] = {tmem, tmem + 128};
-  const uint32_t tO = tmem + 256;
 
   if (warp == 0) {
     if (lane == 0) {  // ===== TMA producer =====
       const int qrow = seg.q_start + q0;
-      tc::mbar_arrive_expect_tx(&bar->q_full, Q_BYTES);
+      tc::mbar_arrive_expect_tx(&bar->q_full, (has_b ? 2 : 1) * Q_BYTES);
       tc::tma_load_2d(sQ, &tmQ, &bar->q_full, h * D, qrow);
       tc::tma_load_2d(sQ + CHUNK, &tmQ, &bar->q_full, h * D + 64, qrow);
+      if (has_b) {
+        tc::tma_load_2d(sQ + Q_BYTES, &tmQ, &bar->q_full, h * D, qrow + BQ);
+        tc::tma_load_2d(sQ + Q_BYTES + CHUNK, &tmQ, &bar->q_full, h * D + 64, qrow + BQ);
+      }
       for (int j = 0; j < nkv; ++j) {
         const int s = j % STAGES;
         tc::mbar_wait(&bar->kv_empty[s], ((j / STAGES) & 1) ^ 1);
@@ -98,173 +116,133 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         uint8_t* k = sK + s * KV_BYTES;
         uint8_t* v = sV + s * KV_BYTES;
         const int kvrow = j * BKV;
-        asm volatile(
-            "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];"
-            ::"r"(tc::smem_u32(k)), "l"(reinterpret_cast<uint64_t>(&tmKV)), "r"(tc::smem_u32(&bar->kv_full[s])),
-            "r"(h * D), "r"(kvrow), "r"(planeK) : "memory");
-        asm volatile(
-            "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];"
-            ::"r"(tc::smem_u32(k + CHUNK)), "l"(reinterpret_cast<uint64_t>(&tmKV)), "r"(tc::smem_u32(&bar->kv_full[s])),
-            "r"(h * D + 64), "r"(kvrow), "r"(planeK) : "memory");
-        asm volatile(
-            "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];"
-            ::"r"(tc::smem_u32(v)), "l"(reinterpret_cast<uint64_t>(&tmKV)), "r"(tc::smem_u32(&bar->kv_full[s])),
-            "r"(h * D), "r"(kvrow), "r"(planeK + 1) : "memory");
-        asm volatile(
-            "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];"
-            ::"r"(tc::smem_u32(v + CHUNK)), "l"(reinterpret_cast<uint64_t>(&tmKV)), "r"(tc::smem_u32(&bar->kv_full[s])),
-            "r"(h * D + 64), "r"(kvrow), "r"(planeK + 1) : "memory");
+        tma_load_3d(k, &tmKV, &bar->kv_full[s], h * D, kvrow, planeK);
+        tma_load_3d(k + CHUNK, &tmKV, &bar->kv_full[s], h * D + 64, kvrow, planeK);
+        tma_load_3d(v, &tmKV, &bar->kv_full[s], h * D, kvrow, planeK + 1);
+        tma_load_3d(v + CHUNK, &tmKV, &bar->kv_full[s], h * D + 64, kvrow, planeK + 1);
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {  // ===== MMA issuer =====
       constexpr uint32_t idS = tc::idesc_bf16(BQ, BKV, 0);
       constexpr uint32_t idO = tc::idesc_bf16(BQ, D, 1);  // B = V is MN-major
-      const uint32_t q_addr = tc::smem_u32(sQ);
-      const uint32_t p_addr = tc::smem_u32(sP);
+      const int ntiles = has_b ? 2 : 1;
       tc::mbar_wait(&bar->q_full, 0);
-      auto issue_S = [&](int j) {
-        const int s = j % STAGES, b = j & 1;
-        tc::mbar_wait(&bar->kv_full[s], (j / STAGES) & 1);
-        tc::mbar_wait(&bar->s_empty[b], ((j >> 1) & 1) ^ 1);
-        tc::tc_fence_after();
-        const uint32_t k_addr = tc::smem_u32(sK + s * KV_BYTES);
+      auto issue_S = [&](int t, int j) {
+        const uint32_t q_addr = tc::smem_u32(sQ + t * Q_BYTES);
+        const uint32_t k_addr = tc::smem_u32(sK + (j % STAGES) * KV_BYTES);
 #pragma unroll
         for (int k = 0; k < D / 16; ++k) {
           const uint32_t off = (k >> 2) * CHUNK + (k & 3) * 32;
-          tc::mma_bf16_ss(tS[b], tc::sdesc_sw128(q_addr + off, 16, 1024), tc::sdesc_sw128(k_addr + off, 16, 1024),
-                          idS, k != 0);
+          tc::mma_bf16_ss(tmem + t * 256, tc::sdesc_sw128(q_addr + off, 16, 1024),
+                          tc::sdesc_sw128(k_addr + off, 16, 1024), idS, k != 0);
         }
-        tc::mma_commit(&bar->s_full[b]);
+        tc::mma_commit(&bar->s_full[t]);
       };
-      auto issue_PV = [&](int j) {
-        const int s = j % STAGES;
-        tc::mbar_wait(&bar->p_full, j & 1);
+      auto issue_PV = [&](int t, int j) {
+        tc::mbar_wait(&bar->p_full[t], j & 1);
         tc::tc_fence_after();
-        const uint32_t v_addr = tc::smem_u32(sV + s * KV_BYTES);
+        const uint32_t v_addr = tc::smem_u32(sV + (j % STAGES) * KV_BYTES);
 #pragma unroll
-        for (int k = 0; k < BKV / 16; ++k) {
-          const uint32_t poff = (k >> 2) * CHUNK + (k & 3) * 32;
-          tc::mma_bf16_ss(tO, tc::sdesc_sw128(p_addr + poff, 16, 1024),
+        for (int k = 0; k < BKV / 16; ++k)
+          tc::mma_bf16_ts(tmem + t * 256 + 128, tmem + t * 256 + k * 8,
                           tc::sdesc_sw128(v_addr + k * 2048, CHUNK, 1024), idO, (j | k) != 0);
-        }
-        tc::mma_commit(&bar->pv_done);
-        tc::mma_commit(&bar->kv_empty[s]);
       };
-      issue_S(0);
-      for (int j = 1; j < nkv; ++j) {
-        issue_S(j);
-        issue_PV(j - 1);
-      }
-      issue_PV(nkv - 1);
-    }
-  } else if (warp >= 4) {  // ===== softmax / correction / epilogue =====
-    const int quad = warp & 3;
-    const int row = quad * 32 + lane;  // query row inside the tile == TMEM lane
-    const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
-    float m = -INFINITY, l = 0.f;
-    uint8_t* prow = sP + row * 128;
-    const int swz = row & 7;
-    for (int j = 0; j < nkv; ++j) {
-      const int b = j & 1;
-#ifdef IG_HANG_CHECK
-      if (threadIdx.x == 128 && blockIdx.x == 0 && blockIdx.y == 0) printf("sm j=%d wait s_full\n", j);
-#endif
-      tc::mbar_wait(&bar->s_full[b], (j >> 1) & 1);
+      tc::mbar_wait(&bar->kv_full[0], 0);
       tc::tc_fence_after();
-      uint32_t r[128];
-      tc::tmem_ld32(tS[b] + lane_off + 0, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
-      tc::tmem_ld32(tS[b] + lane_off + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
-      tc::tmem_ld32(tS[b] + lane_off + 64, *reinterpret_cast<uint32_t(*)[32]>(&r[64]));
-      tc::tmem_ld32(tS[b] + lane_off + 96, *reinterpret_cast<uint32_t(*)[32]>(&r[96]));
-      tc::tmem_ld_wait();
-      tc::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) tc::mbar_arrive(&bar->s_empty[b]);  // S buffer may be overwritten by S_{j+2}
-      const int valid = a.L - j * BKV;                    // keys >= L are masked
-      float mx = -INFINITY;
-#pragma unroll
-      for (int i = 0; i < 128; ++i) {
-        float s = __uint_as_float(r[i]) * scale_log2;
-        if (i >= valid) s = -INFINITY;
-        r[i] = __float_as_uint(s);
-        mx = fmaxf(mx, s);
-      }
-      const float m_new = fmaxf(m, mx);
-      const float alpha = exp2f(m - m_new);  // 0 on the first tile
-      float sum = 0.f;
-      uint32_t pk[64];
-#pragma unroll
-      for (int i = 0; i < 64; ++i) {
-        const float p0 = exp2f(__uint_as_float(r[2 * i]) - m_new);
-        const float p1 = exp2f(__uint_as_float(r[2 * i + 1]) - m_new);
-        sum += p0 + p1;
-        pk[i] = pack_bf16(p0, p1);
-      }
-      l = l * alpha + sum;
-      // P_j may only overwrite shared memory / O may only be rescaled once PV_{j-1} is done
-#ifdef IG_HANG_CHECK
-      if (threadIdx.x == 128 && blockIdx.x == 0 && blockIdx.y == 0) printf("sm j=%d m=%f mnew=%f l=%f wait pv\n", j, m, m_new, l);
-#endif
-      if (j > 0) {
-        tc::mbar_wait(&bar->pv_done, (j - 1) & 1);
-        tc::tc_fence_after();
-      }
-#ifdef IG_HANG_CHECK
-      if (threadIdx.x == 128 && blockIdx.x == 0 && blockIdx.y == 0) printf("sm j=%d pv ok\n", j);
-#endif
-#pragma unroll
-      for (int c = 0; c < 2; ++c)
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const int base = c * 32 + u * 4;
-          uint4 v = make_uint4(pk[base], pk[base + 1], pk[base + 2], pk[base + 3]);
-          *reinterpret_cast<uint4*>(prow + c * CHUNK + ((u ^ swz) << 4)) = v;
+      for (int t = 0; t < ntiles; ++t) issue_S(t, 0);
+      for (int j = 0; j < nkv; ++j) {
+        const bool more = j + 1 < nkv;
+        if (more) {
+          tc::mbar_wait(&bar->kv_full[(j + 1) % STAGES], ((j + 1) / STAGES) & 1);
+          tc::tc_fence_after();
         }
-      // Lazy correction of the O accumulator.  tcgen05.ld/st are warp-collective, so the warp
-      // runs the pass if any of its rows needs it; rows whose max did not grow use alpha = 1
-      // (an exact multiply), keeping each row's result independent of its tile-mates.
-      if (j > 0 && __any_sync(0xffffffffu, m_new > m)) {
-#pragma unroll 1
-        for (int c = 0; c < D; c += 16) {
-          uint32_t o[16];
-          tc::tmem_ld16(tO + lane_off + c, o);
-          tc::tmem_ld_wait();
-#pragma unroll
-          for (int i = 0; i < 16; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
-          tc::tmem_st16(tO + lane_off + c, o);
+        for (int t = 0; t < ntiles; ++t) {
+          issue_PV(t, j);
+          if (more) issue_S(t, j + 1);
+          else tc::mma_commit(&bar->o_done[t]);
         }
-        tc::tmem_st_wait();
+        tc::mma_commit(&bar->kv_empty[j % STAGES]);
       }
-#ifdef IG_HANG_CHECK
-      if (threadIdx.x == 128 && blockIdx.x == 0 && blockIdx.y == 0) printf("sm j=%d rescale done\n", j);
-#endif
-      m = m_new;
-      tc::fence_proxy_async_smem();
-      tc::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) tc::mbar_arrive(&bar->p_full);
     }
-    // epilogue: O / l -> bf16 -> global
-    tc::mbar_wait(&bar->pv_done, (nkv - 1) & 1);
-    tc::tc_fence_after();
-    const int qi = q0 + row;
-    const float inv = 1.0f / l;
-    bf16* out = reinterpret_cast<bf16*>(a.O) + (long long)(seg.q_start + qi) * a.ldo + h * D;
-#pragma unroll 1
-    for (int c = 0; c < D; c += 32) {
-      uint32_t o[32];
-      tc::tmem_ld32(tO + lane_off + c, o);
-      tc::tmem_ld_wait();
-      if (qi < seg.q_len) {
+  } else if (warp >= 4) {  // ===== softmax / correction / epilogue, tile t =====
+    const int t = (warp - 4) >> 2;
+    if (t == 0 || has_b) {
+      const int quad = warp & 3;
+      const int row = quad * 32 + lane;  // query row inside the tile == TMEM lane
+      const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
+      const uint32_t tS = tmem + t * 256 + lane_off, tO = tS + 128;
+      float m = -INFINITY, l = 0.f;
+      for (int j = 0; j < nkv; ++j) {
+        tc::mbar_wait(&bar->s_full[t], j & 1);
+        tc::tc_fence_after();
+        uint32_t r[128];
+        tc::tmem_ld32(tS + 0, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
+        tc::tmem_ld32(tS + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
+        tc::tmem_ld32(tS + 64, *reinterpret_cast<uint32_t(*)[32]>(&r[64]));
+        tc::tmem_ld32(tS + 96, *reinterpret_cast<uint32_t(*)[32]>(&r[96]));
+        tc::tmem_ld_wait();
+        const int valid = a.L - j * BKV;  // keys >= L are masked
+        float mx = -INFINITY;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          uint4 v;
-          v.x = pack_bf16(__uint_as_float(o[8 * q + 0]) * inv, __uint_as_float(o[8 * q + 1]) * inv);
-          v.y = pack_bf16(__uint_as_float(o[8 * q + 2]) * inv, __uint_as_float(o[8 * q + 3]) * inv);
-          v.z = pack_bf16(__uint_as_float(o[8 * q + 4]) * inv, __uint_as_float(o[8 * q + 5]) * inv);
-          v.w = pack_bf16(__uint_as_float(o[8 * q + 6]) * inv, __uint_as_float(o[8 * q + 7]) * inv);
-          *reinterpret_cast<uint4*>(out + c + 8 * q) = v;
+        for (int i = 0; i < 128; ++i) {
+          float s = __uint_as_float(r[i]) * scale_log2;
+          if (i >= valid) s = -INFINITY;
+          r[i] = __float_as_uint(s);
+          mx = fmaxf(mx, s);
+        }
+        // keep the stale max unless it grew by more than the threshold (per row)
+        const float m_use = (mx > m + RESCALE_THRESHOLD) ? mx : m;
+        const float alpha = exp2f(m - m_use);  // 1 when kept, 0 on the first tile
+        float sum = 0.f;
+#pragma unroll
+        for (int i = 0; i < 64; ++i) {  // in-place pack: r[i] <- bf16x2(p[2i], p[2i+1])
+          const float p0 = exp2f(__uint_as_float(r[2 * i]) - m_use);
+          const float p1 = exp2f(__uint_as_float(r[2 * i + 1]) - m_use);
+          sum += p0 + p1;
+          r[i] = pack_bf16(p0, p1);
+        }
+        tc::tmem_st32(tS + 0, &r[0]);
+        tc::tmem_st32(tS + 32, &r[32]);
+        if (j > 0 && __any_sync(0xffffffffu, m_use > m)) {
+#pragma unroll 1
+          for (int c = 0; c < D; c += 32) {
+            uint32_t o[32];
+            tc::tmem_ld32(tO + c, o);
+            tc::tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+            tc::tmem_st32(tO + c, o);
+          }
+        }
+        l = l * alpha + sum;
+        m = m_use;
+        tc::tmem_st_wait();
+        tc::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&bar->p_full[t]);
+      }
+      // epilogue: O / l -> bf16 -> global
+      tc::mbar_wait(&bar->o_done[t], 0);
+      tc::tc_fence_after();
+      const int qi = q0 + t * BQ + row;
+      const float inv = 1.0f / l;
+      bf16* out = reinterpret_cast<bf16*>(a.O) + (long long)(seg.q_start + qi) * a.ldo + h * D;
+#pragma unroll 1
+      for (int c = 0; c < D; c += 32) {
+        uint32_t o[32];
+        tc::tmem_ld32(tO + c, o);
+        tc::tmem_ld_wait();
+        if (qi < seg.q_len) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            uint4 v;
+            v.x = pack_bf16(__uint_as_float(o[8 * q + 0]) * inv, __uint_as_float(o[8 * q + 1]) * inv);
+            v.y = pack_bf16(__uint_as_float(o[8 * q + 2]) * inv, __uint_as_float(o[8 * q + 3]) * inv);
+            v.z = pack_bf16(__uint_as_float(o[8 * q + 4]) * inv, __uint_as_float(o[8 * q + 5]) * inv);
+            v.w = pack_bf16(__uint_as_float(o[8 * q + 6]) * inv, __uint_as_float(o[8 * q + 7]) * inv);
+            *reinterpret_cast<uint4*>(out + c + 8 * q) = v;
+          }
         }
       }
     }
@@ -299,7 +277,6 @@ void launch_attn_tc(const AttnArgs& a, cudaStream_t st) {
   if (a.nseg <= 0 || a.max_qlen <= 0) return;
   init_attn();
   const long long H = (long long)a.heads * a.head_dim;
-  // Q: 2-D [rows, H] with leading dimension ldq.  Rows: enough to cover every segment.
   CUtensorMap tq, tkv;
   {
     cuuint64_t dims[2] = {(cuuint64_t)H, (cuuint64_t)a.q_rows};
@@ -321,7 +298,7 @@ void launch_attn_tc(const AttnArgs& a, cudaStream_t st) {
           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   }
-  dim3 grid((a.max_qlen + BQ - 1) / BQ, a.heads, a.nseg);
+  dim3 grid((a.max_qlen + 2 * BQ - 1) / (2 * BQ), a.heads, a.nseg);
   const float scale_log2 = a.scale * 1.4426950408889634f;
   attn_tc_kernel<<<grid, NTHREADS, SMEM_BYTES, st>>>(tq, tkv, a, scale_log2);
 }
