@@ -922,6 +922,31 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
     launch_qkv_post<T>(p, ctx->ri, st);
     stats.kernel_launches++;
   };
+  // a6: QKV projection + norm/RoPE/Q-pack/positional K/V merge.  bf16 mode fuses the whole
+  // epilogue into the tensor-core GEMM; fp32 parity mode runs the GEMM then qkv_post.
+  const bool fused_qkv = ctx->d.dtype == IG_BF16 && g_tc_gemm && (H % 256) == 0 &&
+                         (ctx->d.head_dim == 128 || ctx->d.head_dim == 64);
+  auto qkv_proj = [&](int r0, int r1, const void* W, const void* bias, const void* qg, const void* kg, int buf) {
+    if (r1 <= r0) return;
+    if (!fused_qkv) {
+      gemm_rows(r0, r1, h, H, W, bias, 3 * H, H, qkv, 3 * H, EPI_STORE, nullptr, 0);
+      qkv_post(r0, r1, qg, kg, buf);
+      return;
+    }
+    GemmArgs g{};
+    g.A = (const char*)h + (long long)r0 * H * es; g.lda = H;
+    g.B = W; g.ldb = H; g.bias = bias;
+    g.C = ctx->Q; g.ldc = H;
+    g.M = r1 - r0; g.N = 3 * H; g.K = H; g.epi = EPI_QKV;
+    g.ri = ctx->ri; g.ri_off = r0;
+    QkvEpi& e = g.qkv;
+    e.Q = ctx->Q; e.kv_arena = ctx->kv_arena; e.slot_stride = ctx->slot_stride;
+    e.buf_off = (long long)buf * ctx->buf_elems; e.L = ctx->L; e.H = H; e.qg = qg; e.kg = kg;
+    e.rope_tab = ctx->rope_tab; e.rope_maxpos = ctx->rope_maxpos;
+    e.ax1_pair = ctx->d.rope_axes[0] / 2; e.ax2_pair = (ctx->d.rope_axes[0] + ctx->d.rope_axes[1]) / 2;
+    e.head_dim = ctx->d.head_dim; e.grid_w = ctx->d.grid_w; e.qk_norm = ctx->d.qk_norm; e.rope = ctx->d.rope;
+    gemm(ctx, g, st);
+  };
   auto attn = [&](int buf) {
     AttnArgs a{};
     a.Q = ctx->Q; a.ldq = H; a.O = cat; a.ldo = ldcat; a.kv_arena = ctx->kv_arena;
@@ -964,11 +989,9 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
       const StreamW& wt = ctx->dtxt[b];
       ln_mod(M_txt, M, wi.mod_t, 0, 1);
       if (Lt) ln_mod(0, M_txt, wt.mod_t, wt.pre_only ? 1 : 0, wt.pre_only ? 0 : 1);
-      gemm_rows(M_txt, M, h, H, wi.qkv.w, wi.qkv.b, 3 * H, H, qkv, 3 * H, EPI_STORE, nullptr, 0);
-      if (Lt) gemm_rows(0, M_txt, h, H, wt.qkv.w, wt.qkv.b, 3 * H, H, qkv, 3 * H, EPI_STORE, nullptr, 0);
       wait_copy(buf);
-      qkv_post(M_txt, M, wi.qg, wi.kg, buf);
-      if (Lt) qkv_post(0, M_txt, wt.qg, wt.kg, buf);
+      qkv_proj(M_txt, M, wi.qkv.w, wi.qkv.b, wi.qg, wi.kg, buf);
+      if (Lt) qkv_proj(0, M_txt, wt.qkv.w, wt.qkv.b, wt.qg, wt.kg, buf);
       wait_copy_late(buf);
       attn(buf);
       record_kv(b, buf);
@@ -989,12 +1012,11 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
     } else {
       const SingleW& ws = ctx->sgl[b - ctx->d.n_double];
       ln_mod(0, M, ws.mod_t, 0, 1);
-      gemm_rows(0, M, h, H, ws.lin1.w, ws.lin1.b, 3 * H, H, qkv, 3 * H, EPI_STORE, nullptr, 0);
       const char* w_u = (const char*)ws.lin1.w + 3LL * H * H * es;
       const char* b_u = (const char*)ws.lin1.b + 3LL * H * es;
       gemm_rows(0, M, h, H, w_u, b_u, F, H, cat + H, ldcat, EPI_GELU, nullptr, 0);
       wait_copy(buf);
-      qkv_post(0, M, ws.qg, ws.kg, buf);
+      qkv_proj(0, M, ws.lin1.w, ws.lin1.b, ws.qg, ws.kg, buf);
       wait_copy_late(buf);
       attn(buf);
       record_kv(b, buf);

@@ -141,6 +141,77 @@ __device__ __forceinline__ void epilogue_chunk(const GemmArgs& g, int row, int c
   }
 }
 
+// Fused a6 epilogue for one head (d columns starting at absolute column col0 of the [q|k|v]
+// output) of one row: bias, per-head RMSNorm with gain (q, k), RoPE at the row's ORIGINAL
+// token position (C-AMB 7), then q -> packed Q row, k/v -> the request's positional K/V
+// buffer row (the fresh half of the merge by mask index, C-AMB 8).
+template <int DH>
+__device__ __forceinline__ void epilogue_qkv_head(const GemmArgs& g, int row, int col0, const uint32_t (&r)[DH],
+                                                  const RowInfo& info) {
+  const QkvEpi& e = g.qkv;
+  float v[DH];
+#pragma unroll
+  for (int i = 0; i < DH; ++i) v[i] = __uint_as_float(r[i]);
+  const bf16* bias = reinterpret_cast<const bf16*>(g.bias);
+  if (bias) {
+#pragma unroll
+    for (int q = 0; q < DH / 8; ++q) {
+      uint4 u = reinterpret_cast<const uint4*>(bias + col0)[q];
+      const bf16* hb = reinterpret_cast<const bf16*>(&u);
+#pragma unroll
+      for (int t = 0; t < 8; ++t) v[q * 8 + t] += __bfloat162float(hb[t]);
+    }
+  }
+  const int which = (int)(col0 / e.H);          // 0 q, 1 k, 2 v
+  const int hcol = (int)(col0 - which * e.H);   // column inside the hidden dim
+  bf16* dst;
+  if (which == 0) {
+    dst = reinterpret_cast<bf16*>(e.Q) + (long long)(g.ri_off + row) * e.H + hcol;
+  } else {
+    dst = reinterpret_cast<bf16*>(e.kv_arena) + info.slot * e.slot_stride + e.buf_off +
+          (which == 2 ? e.L * e.H : 0) + (long long)info.kvpos * e.H + hcol;
+  }
+  if (which < 2) {
+    if (e.qk_norm) {
+      float ss = 0.f;
+#pragma unroll
+      for (int i = 0; i < DH; ++i) ss = fmaf(v[i], v[i], ss);
+      const float rinv = rsqrtf(ss / DH + 1e-6f);
+      const bf16* gn = reinterpret_cast<const bf16*>(which == 0 ? e.qg : e.kg);
+#pragma unroll
+      for (int q = 0; q < DH / 8; ++q) {
+        uint4 u = reinterpret_cast<const uint4*>(gn)[q];
+        const bf16* hg = reinterpret_cast<const bf16*>(&u);
+#pragma unroll
+        for (int t = 0; t < 8; ++t) v[q * 8 + t] *= rinv * __bfloat162float(hg[t]);
+      }
+    }
+    if (e.rope) {
+      int p1 = 0, p2 = 0;
+      if (info.tok >= 0) { p1 = info.tok / e.grid_w; p2 = info.tok - p1 * e.grid_w; }
+#pragma unroll
+      for (int j = 0; j < DH / 2; ++j) {
+        const int pos = j < e.ax1_pair ? 0 : (j < e.ax2_pair ? p1 : p2);
+        const float2 cs = __ldg(e.rope_tab + (long long)j * e.rope_maxpos + pos);
+        const float x0 = v[2 * j], x1 = v[2 * j + 1];
+        v[2 * j] = x0 * cs.x - x1 * cs.y;
+        v[2 * j + 1] = x0 * cs.y + x1 * cs.x;
+      }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < DH / 8; ++q) {
+    uint4 u;
+    uint32_t* w = reinterpret_cast<uint32_t*>(&u);
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      __nv_bfloat162 p = __floats2bfloat162_rn(v[q * 8 + 2 * t], v[q * 8 + 2 * t + 1]);
+      w[t] = *reinterpret_cast<uint32_t*>(&p);
+    }
+    reinterpret_cast<uint4*>(dst)[q] = u;
+  }
+}
+
 template <int BN>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -233,13 +304,37 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       tc::tc_fence_after();
       const int row = m0 + quad * 32 + lane;
       RowInfo info{0, 0, 0, 0};
-      if (row < g.M && g.ri && (g.epi == EPI_GATED_RES || g.epi == EPI_POS)) info = g.ri[g.ri_off + row];
+      if (row < g.M && g.ri && (g.epi == EPI_GATED_RES || g.epi == EPI_POS || g.epi == EPI_QKV))
+        info = g.ri[g.ri_off + row];
+      const uint32_t tbase = tmem_base + ((uint32_t)(quad * 32) << 16) + acc * BN;
+      if (g.epi == EPI_QKV) {
+        if (g.qkv.head_dim == 128) {
 #pragma unroll 1
-      for (int c = 0; c < BN; c += 32) {
-        uint32_t r[32];
-        tc::tmem_ld32(tmem_base + ((uint32_t)(quad * 32) << 16) + acc * BN + c, r);
-        tc::tmem_ld_wait();
-        if (row < g.M && n0 + c < g.N) epilogue_chunk<BN>(g, row, n0 + c, r, &info);
+          for (int c = 0; c < BN; c += 128) {
+            uint32_t v[128];
+#pragma unroll
+            for (int s = 0; s < 4; ++s) tc::tmem_ld32(tbase + c + 32 * s, *reinterpret_cast<uint32_t(*)[32]>(&v[32 * s]));
+            tc::tmem_ld_wait();
+            if (row < g.M && n0 + c < g.N) epilogue_qkv_head<128>(g, row, n0 + c, v, info);
+          }
+        } else {
+#pragma unroll 1
+          for (int c = 0; c < BN; c += 64) {
+            uint32_t v[64];
+#pragma unroll
+            for (int s = 0; s < 2; ++s) tc::tmem_ld32(tbase + c + 32 * s, *reinterpret_cast<uint32_t(*)[32]>(&v[32 * s]));
+            tc::tmem_ld_wait();
+            if (row < g.M && n0 + c < g.N) epilogue_qkv_head<64>(g, row, n0 + c, v, info);
+          }
+        }
+      } else {
+#pragma unroll 1
+        for (int c = 0; c < BN; c += 32) {
+          uint32_t r[32];
+          tc::tmem_ld32(tbase + c, r);
+          tc::tmem_ld_wait();
+          if (row < g.M && n0 + c < g.N) epilogue_chunk<BN>(g, row, n0 + c, r, &info);
+        }
       }
       tc::tc_fence_before();
       __syncwarp();
@@ -290,18 +385,20 @@ bool gemm_tc_supported(const GemmArgs& g) {
   if (!al16(g.A) || !al16(g.B) || (g.lda & 7) || (g.ldb & 7) || (g.K & 7)) return false;
   if (g.epi == EPI_STORE || g.epi == EPI_GELU) {
     if (!al16(g.C) || (g.ldc & (g.out_f32 ? 3 : 7))) return false;
-  } else {
+  } else if (g.epi != EPI_QKV) {
     if (!al16(g.C) || (g.ldc & 3)) return false;
     if (g.epi == EPI_GATED_RES && (!al16(g.gate) || (g.gate_ld & 3))) return false;
   }
   if (g.bias && !al16(g.bias)) return false;
+  if (g.epi == EPI_QKV && ((g.qkv.head_dim != 128 && g.qkv.head_dim != 64) || (g.qkv.H % 256) || g.N != 3 * g.qkv.H))
+    return false;
   return true;
 }
 
 void launch_gemm_tc(const GemmArgs& g, cudaStream_t st) {
   if (g.M <= 0 || g.N <= 0) return;
   init_driver();
-  const bool wide = g.N > 128;
+  const bool wide = g.N > 128 || g.epi == EPI_QKV;
   const int BN = wide ? 256 : 128;
   CUtensorMap ta, tb;
   make_tmap(&ta, g.A, g.M, g.K, g.lda, BM);

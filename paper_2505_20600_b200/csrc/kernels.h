@@ -95,6 +95,19 @@ enum Epi : int {
   EPI_GELU = 1,       // C = gelu_tanh(acc + b) (TOut)
   EPI_GATED_RES = 2,  // X[r, c] += gate[req(r)][c] * (acc + b)  (C is fp32 X)
   EPI_POS = 3,        // X[r, c] = acc + b + pos[tok(r)][c]      (C is fp32 X)
+  EPI_QKV = 4,        // q,k: per-head RMSNorm + RoPE; q -> packed Q, k,v -> positional K/V
+};
+// Extra arguments of the fused QKV epilogue (a6: norm, RoPE and the positional merge done
+// on the fp32 accumulators, one bf16 rounding per output).
+struct QkvEpi {
+  void* Q;                          // [M, H] packed (bf16)
+  void* kv_arena;                   // ring arena (bf16)
+  long long slot_stride, buf_off;   // elements
+  long long L, H;
+  const void* qg; const void* kg;   // [d] gains (bf16) or null
+  const float2* rope_tab;           // [d/2][rope_maxpos] (cos, sin) or null
+  int rope_maxpos, ax1_pair, ax2_pair;
+  int head_dim, grid_w, qk_norm, rope;
 };
 struct GemmArgs {
   const void* A; long long lda;   // [M, K] row-major
@@ -109,6 +122,7 @@ struct GemmArgs {
   const void* pos; long long pos_ld;     // EPI_POS table (T)
   int out_f32;                           // EPI_STORE/GELU: 1 => C is fp32
   int precise_gelu;                      // 1 => tanhf instead of MUFU tanh.approx (debug)
+  QkvEpi qkv;                            // EPI_QKV only
 };
 template <typename T>
 void launch_gemm_simt(const GemmArgs& g, cudaStream_t st);
