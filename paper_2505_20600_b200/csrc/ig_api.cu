@@ -1211,11 +1211,15 @@ extern "C" ig_status ig_op_attention(int dtype, const void* Q, long long ldq, vo
   for (auto& s : hs) qrows = std::max(qrows, s.q_start + s.q_len);
   a.q_rows = qrows;
   a.scale = 1.0f / sqrtf((float)head_dim);
-  if (dtype == IG_F32) launch_attn_simt<float>(a, st);
-  else if (dtype == IG_BF16) {
-    if (g_tc_attn && attn_tc_supported(a)) launch_attn_tc(a, st);
-    else launch_attn_simt<bf16>(a, st);
-  } else return set_err(IG_EINVAL, "bad dtype");
+  const char* rep_env = getenv("IG_OP_REPEAT");  // benchmarking aid: launch the kernel N times
+  const int rep = rep_env ? std::max(1, atoi(rep_env)) : 1;
+  for (int it = 0; it < rep; ++it) {
+    if (dtype == IG_F32) launch_attn_simt<float>(a, st);
+    else if (dtype == IG_BF16) {
+      if (g_tc_attn && attn_tc_supported(a)) launch_attn_tc(a, st);
+      else launch_attn_simt<bf16>(a, st);
+    } else return set_err(IG_EINVAL, "bad dtype");
+  }
   CUDA_TRY(cudaFreeAsync(dsegs, st));
   CUDA_TRY(cudaStreamSynchronize(st));  // host segment vector lifetime
   CUDA_TRY(cudaGetLastError());

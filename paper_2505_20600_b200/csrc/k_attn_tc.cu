@@ -52,6 +52,12 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   return *reinterpret_cast<uint32_t*>(&p);
 }
 
+__device__ __forceinline__ float ex2_fast(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 __device__ __forceinline__ void tma_load_3d(void* smem, const CUtensorMap* m, uint64_t* bar, int c0, int c1, int c2) {
   asm volatile(
       "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];"
@@ -182,26 +188,34 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         tc::tmem_ld32(tS + 64, *reinterpret_cast<uint32_t(*)[32]>(&r[64]));
         tc::tmem_ld32(tS + 96, *reinterpret_cast<uint32_t(*)[32]>(&r[96]));
         tc::tmem_ld_wait();
-        const int valid = a.L - j * BKV;  // keys >= L are masked
+        const int valid = a.L - j * BKV;  // keys >= L are masked (ragged last tile only)
         float mx = -INFINITY;
+        if (valid >= BKV) {
 #pragma unroll
-        for (int i = 0; i < 128; ++i) {
-          float s = __uint_as_float(r[i]) * scale_log2;
-          if (i >= valid) s = -INFINITY;
-          r[i] = __float_as_uint(s);
-          mx = fmaxf(mx, s);
+          for (int i = 0; i < 128; i += 2) mx = fmaxf(mx, fmaxf(__uint_as_float(r[i]), __uint_as_float(r[i + 1])));
+        } else {
+#pragma unroll
+          for (int i = 0; i < 128; ++i) {
+            if (i >= valid) r[i] = __float_as_uint(-INFINITY);
+            mx = fmaxf(mx, __uint_as_float(r[i]));
+          }
         }
-        // keep the stale max unless it grew by more than the threshold (per row)
-        const float m_use = (mx > m + RESCALE_THRESHOLD) ? mx : m;
+        // scores in log2 units: s * scale * log2(e).  Keep the stale max unless it grew by
+        // more than the threshold (per row).
+        const float mxs = mx * scale_log2;
+        const float m_use = (mxs > m + RESCALE_THRESHOLD) ? mxs : m;
         const float alpha = exp2f(m - m_use);  // 1 when kept, 0 on the first tile
-        float sum = 0.f;
+        const float2 sc2 = make_float2(scale_log2, scale_log2);
+        const float2 nm2 = make_float2(-m_use, -m_use);
+        float2 acc2 = make_float2(0.f, 0.f);
 #pragma unroll
         for (int i = 0; i < 64; ++i) {  // in-place pack: r[i] <- bf16x2(p[2i], p[2i+1])
-          const float p0 = exp2f(__uint_as_float(r[2 * i]) - m_use);
-          const float p1 = exp2f(__uint_as_float(r[2 * i + 1]) - m_use);
-          sum += p0 + p1;
-          r[i] = pack_bf16(p0, p1);
+          const float2 x = __ffma2_rn(make_float2(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1])), sc2, nm2);
+          const float2 pp = make_float2(ex2_fast(x.x), ex2_fast(x.y));
+          acc2 = __fadd2_rn(acc2, pp);
+          r[i] = pack_bf16(pp.x, pp.y);
         }
+        const float sum = acc2.x + acc2.y;
         tc::tmem_st32(tS + 0, &r[0]);
         tc::tmem_st32(tS + 32, &r[32]);
         if (j > 0 && __any_sync(0xffffffffu, m_use > m)) {
