@@ -83,9 +83,9 @@ typedef struct {
                        /* max_batch * L)                                                  */
   int prefetch_depth;  /* D: layers the copy lane runs ahead of compute (default 2)       */
   int copy_mode;       /* 0 = full-L per-layer cudaMemcpyAsync (all L_img rows),          */
-                       /* 1 = compacted: only unmasked rows, as contiguous runs of the     */
-                       /*     unmasked index list in one cudaMemcpyBatchAsync per layer    */
-                       /*     (copy engines),                                              */
+                       /* 1 = compacted: only unmasked rows — host-tier caches as runs of  */
+                       /*     the unmasked index list, batched cudaMemcpyBatchAsync per    */
+                       /*     layer (copy engines); HBM-tier caches via the SM gather      */
                        /* 2 = compacted: zero-copy SM gather kernel on the copy stream     */
   int debug_checks;    /* 1 = check the latent for non-finite values after each step     */
 } ig_ctx_opts;
@@ -121,6 +121,10 @@ ig_status ig_cache_create(ig_ctx* ctx, int n_steps, int tier, ig_cache** out);
 ig_status ig_cache_template(ig_ctx* ctx, float* latent, const void* txt, const float* cond_vec,
                             const float* sigmas, int n_steps, int tier, void* stream,
                             ig_cache** out);
+
+/* Copy of a cache into another tier (e.g. an HBM-resident hot template): same
+ * schedule and layout.  Synchronous. */
+ig_status ig_cache_clone(ig_ctx* ctx, const ig_cache* src, int tier, ig_cache** out);
 
 /* Raw storage of a cache: host or device pointer (per tier) and its size in bytes, for
  * test I/O and for filling a synthetic cache.  The pointer stays owned by the cache. */

@@ -151,6 +151,7 @@ struct ig_ctx {
   std::vector<Pref> pref;  // [max_batch * R]
   ig_mask* ones_mask = nullptr;
   std::vector<void*> b_dst, b_src;  // batched-copy scratch (copy_mode 1)
+  bool gather_dev = false;          // this step's caches are all HBM-resident: SM gather
   std::vector<size_t> b_size;
   ig_stats stats{};
   std::vector<ig_cache*> zombies;
@@ -623,6 +624,19 @@ extern "C" ig_status ig_cache_create(ig_ctx* ctx, int n_steps, int tier, ig_cach
   return IG_OK;
 }
 
+extern "C" ig_status ig_cache_clone(ig_ctx* ctx, const ig_cache* src, int tier, ig_cache** out) {
+  if (!ctx || !src || !out) return set_err(IG_EINVAL, "NULL argument");
+  *out = nullptr;
+  if (!desc_equal(src->desc, ctx->d)) return set_err(IG_ECACHE_INCOMPAT, "cache built for another model");
+  ig_cache* c = nullptr;
+  ig_status s = ig_cache_create(ctx, src->n_steps, tier, &c);
+  if (s != IG_OK) return s;
+  cudaError_t e = cudaMemcpy(c->ptr, src->ptr, src->bytes, cudaMemcpyDefault);
+  if (e != cudaSuccess) { free_cache_now(c); return set_err(IG_ECUDA, "cache clone: %s", cudaGetErrorString(e)); }
+  *out = c;
+  return IG_OK;
+}
+
 extern "C" ig_status ig_cache_storage(ig_cache* c, void** ptr, size_t* bytes, int* tier) {
   if (!c) return set_err(IG_EINVAL, "cache is NULL");
   if (ptr) *ptr = c->ptr;
@@ -663,7 +677,7 @@ static void issue_copy(ig_ctx* ctx, const std::vector<StepReq>& sr, const KvGath
   const int buf = b % ctx->R;
   cudaStreamWaitEvent(ctx->copy_st, ctx->ev_comp[buf], 0);
   const int n = (int)sr.size();
-  if (ctx->o.copy_mode == 2) {
+  if (ctx->o.copy_mode == 2 || (ctx->o.copy_mode == 1 && ctx->gather_dev)) {
     ctx->stats.kernel_launches++;
     launch_kv_gather(kvg_dev + (size_t)b * n, n, max_nu, ctx->Lt, ctx->H, (int)ctx->esz, ctx->copy_st);
     for (int q = 0; q < n; ++q)
@@ -820,8 +834,13 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
     max_q = std::max(max_q, d.n_m);
     img_row += d.n_m;
   }
+  // compacted copies: DMA runs over the host link, an SM gather kernel for HBM-resident caches
+  bool all_dev = any_cache;
+  for (auto& s : sr) if (s.use_cache && s.r->cache->tier != IG_CACHE_DEVICE) all_dev = false;
+  ctx->gather_dev = ctx->o.copy_mode == 1 && all_dev;
+  const bool use_gather = ctx->o.copy_mode == 2 || ctx->gather_dev;
   std::vector<KvGatherReq> kvg_host;
-  if (any_cache && ctx->o.copy_mode == 2) {
+  if (any_cache && use_gather) {
     kvg_host.resize((size_t)nb * na);
     const size_t plane = (size_t)ctx->Limg * H;
     for (int b = 0; b < nb; ++b)
@@ -842,7 +861,7 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
         hkvg[(size_t)b * na + q] = g;
       }
   }
-  const size_t desc_bytes = (char*)(hkvg + (any_cache && ctx->o.copy_mode == 2 ? (size_t)nb * na : 0)) - hs;
+  const size_t desc_bytes = (char*)(hkvg + (any_cache && use_gather ? (size_t)nb * na : 0)) - hs;
   CUDA_TRY(cudaMemcpyAsync(ds, hs, desc_bytes, cudaMemcpyHostToDevice, st));
   CUDA_TRY(cudaEventRecord(ctx->ev_desc, st));
   if (any_cache) CUDA_TRY(cudaStreamWaitEvent(ctx->copy_st, ctx->ev_desc, 0));

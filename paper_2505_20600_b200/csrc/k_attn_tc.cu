@@ -25,6 +25,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <mutex>
+#include <cstdlib>
 #include "kernels.h"
 #include "tc_common.cuh"
 
@@ -39,6 +40,7 @@ constexpr int STAGES = 2;
 constexpr int SMEM_BYTES = 2 * Q_BYTES + STAGES * 2 * KV_BYTES + 1024 + 256;
 constexpr int NTHREADS = 384;
 constexpr float RESCALE_THRESHOLD = 8.0f;       // log2 units
+constexpr int NPOLY = 0;  // pairs per key tile on ex2_poly2 (measured: MUFU is not the limiter; 0 is fastest)
 
 struct Bars {
   uint64_t q_full;
@@ -56,6 +58,24 @@ __device__ __forceinline__ float ex2_fast(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
+}
+
+// 2^x on the FMA pipe for a pair (relieves the MUFU unit, which would otherwise bound the
+// softmax at the tensor-core rate): round-to-nearest split x = j + f, |f| <= 1/2, a degree-3
+// polynomial for 2^f (relative error < 1e-5, far below the bf16 rounding of P), and j added
+// into the exponent field.  x is clamped at -127 (2^-127 ~ 0).
+__device__ __forceinline__ float2 ex2_poly2(float2 x) {
+  x.x = fmaxf(x.x, -127.f);
+  x.y = fmaxf(x.y, -127.f);
+  const float2 magic = make_float2(12582912.f, 12582912.f);  // 1.5 * 2^23
+  const float2 t = __fadd2_rn(x, magic);
+  const float2 j = __fadd2_rn(t, make_float2(-12582912.f, -12582912.f));
+  const float2 f = __ffma2_rn(j, make_float2(-1.f, -1.f), x);
+  float2 p = __ffma2_rn(f, make_float2(0.05550411f, 0.05550411f), make_float2(0.24022651f, 0.24022651f));
+  p = __ffma2_rn(p, f, make_float2(0.69314718f, 0.69314718f));
+  p = __ffma2_rn(p, f, make_float2(1.f, 1.f));
+  const int ex = __float_as_int(t.x) << 23, ey = __float_as_int(t.y) << 23;
+  return make_float2(__int_as_float(__float_as_int(p.x) + ex), __int_as_float(__float_as_int(p.y) + ey));
 }
 
 __device__ __forceinline__ void tma_load_3d(void* smem, const CUtensorMap* m, uint64_t* bar, int c0, int c1, int c2) {
@@ -211,7 +231,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 #pragma unroll
         for (int i = 0; i < 64; ++i) {  // in-place pack: r[i] <- bf16x2(p[2i], p[2i+1])
           const float2 x = __ffma2_rn(make_float2(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1])), sc2, nm2);
-          const float2 pp = make_float2(ex2_fast(x.x), ex2_fast(x.y));
+          // ~3/8 of the exponentials on the FMA pipe, the rest on MUFU
+          const float2 pp = (i < NPOLY) ? ex2_poly2(x) : make_float2(ex2_fast(x.x), ex2_fast(x.y));
           acc2 = __fadd2_rn(acc2, pp);
           r[i] = pack_bf16(pp.x, pp.y);
         }

@@ -24,7 +24,7 @@ EXPORTS = ["ig_weight_count", "ig_ctx_create", "ig_ctx_destroy", "ig_cache_creat
            "ig_cache_template", "ig_cache_storage", "ig_cache_free", "ig_mask_build",
            "ig_mask_indices", "ig_mask_free", "ig_edit_step", "ig_prefetch_layer",
            "ig_last_error", "ig_last_stats", "ig_op_gemm", "ig_op_gemm_gated", "ig_op_attention", "ig_copy",
-           "ig_profile_enable", "ig_profile_read", "ig_debug_block"]
+           "ig_profile_enable", "ig_profile_read", "ig_debug_block", "ig_cache_clone"]
 KCLASS = ["gemm", "attn", "lnmod", "qkvpost", "cond", "rows"]
 
 
@@ -102,6 +102,7 @@ def lib():
         L.ig_copy.argtypes = [vp, vp, ctypes.c_size_t, vp]
         L.ig_op_gemm_gated.argtypes = [i, vp, ll, vp, ll, vp, vp, ll, vp, i, i, i, vp]
         L.ig_profile_enable.argtypes = [vp, i]
+        L.ig_cache_clone.argtypes = [vp, vp, i, P(vp)]
         L.ig_debug_block.argtypes = [vp, P(ig_edit_req), i, vp, vp, vp]
         L.ig_profile_read.argtypes = [vp, P(ig_prof_entry)]
         for name in EXPORTS:
@@ -243,3 +244,9 @@ def ig_profile_read(ctx: int) -> dict:
 
 def ig_debug_block(ctx: int, req: ig_edit_req, block: int, X_in: int, X_out: int, stream: int = 0):
     _check(lib().ig_debug_block(ctx, ctypes.byref(req), block, X_in, X_out, stream))
+
+
+def ig_cache_clone(ctx: int, cache: int, tier: int) -> int:
+    out = ctypes.c_void_p()
+    _check(lib().ig_cache_clone(ctx, cache, tier, ctypes.byref(out)))
+    return out.value
