@@ -134,6 +134,12 @@ struct ig_ctx {
   float2* rope_tab = nullptr;
   int rope_maxpos = 1;
   GemvProb *gv_t1 = nullptr, *gv_t2 = nullptr, *gv_mod = nullptr;
+  // bf16 mode: every block's modulation weight packed into one [mod_ld, H] matrix (+ bias) so
+  // the whole a3 modulation is ONE tensor-core GEMM [n, H] x [mod_ld, H]^T (HBM-bound on the
+  // 6.5 GB of weights) instead of a CUDA-core GEMV
+  void* modw = nullptr;
+  void* modb = nullptr;
+  bf16* svec_bf = nullptr;
   int gv_mod_groups = 0;
   std::vector<GemvProb> gv_mod_host;
   // per-step descriptors: device ring + pinned host staging
@@ -274,6 +280,7 @@ static ig_status validate_desc(const ig_model_desc* d) {
     return set_err(IG_EUNSUPPORTED, "head_dim %d not in {16, 64, 128}", d->head_dim);
   if (d->hidden % 64 || d->mlp_hidden % 64 || d->lat_ch % 4)
     return set_err(IG_EUNSUPPORTED, "hidden and mlp_hidden must be multiples of 64, lat_ch of 4");
+  if (d->hidden > 4096) return set_err(IG_EUNSUPPORTED, "hidden > 4096");
   if (d->rope && d->rope_axes[0] + d->rope_axes[1] + d->rope_axes[2] != d->head_dim)
     return set_err(IG_EINVAL, "rope axes must sum to head_dim");
   if (d->rope && ((d->rope_axes[0] | d->rope_axes[1] | d->rope_axes[2]) & 1))
@@ -423,6 +430,16 @@ extern "C" ig_status ig_ctx_create(const ig_model_desc* desc, const void* const*
     ctx->gv_mod_host.push_back(g);
   }
   ctx->gv_mod_groups = groups;
+  if (desc->dtype == IG_BF16) {
+    okm &= dmalloc(&ctx->modw, (size_t)ctx->mod_ld * H * 2);
+    okm &= dmalloc(&ctx->modb, (size_t)ctx->mod_ld * 2);
+    okm &= dmalloc((void**)&ctx->svec_bf, (size_t)B * H * 2);
+    if (!okm) { ig_ctx_destroy(ctx); return set_err(IG_ENOMEM, "modulation pack allocation failed"); }
+    for (auto& m : ctx->mods) {
+      cudaMemcpy((char*)ctx->modw + (size_t)m.off * H * 2, m.w->w, (size_t)m.k * H * H * 2, cudaMemcpyDeviceToDevice);
+      cudaMemcpy((char*)ctx->modb + (size_t)m.off * 2, m.w->b, (size_t)m.k * H * 2, cudaMemcpyDeviceToDevice);
+    }
+  }
   okm &= dmalloc((void**)&ctx->gv_t1, sizeof(GemvProb));
   okm &= dmalloc((void**)&ctx->gv_t2, sizeof(GemvProb));
   okm &= dmalloc((void**)&ctx->gv_mod, ctx->gv_mod_host.size() * sizeof(GemvProb));
@@ -462,7 +479,7 @@ extern "C" void ig_ctx_destroy(ig_ctx* ctx) {
   for (auto* z : ctx->zombies) free_cache_now(z);
   void* bufs[] = {ctx->X, ctx->vel, ctx->temb, ctx->tmp, ctx->vec, ctx->svec, ctx->modbuf, ctx->h,
                   ctx->qkv, ctx->Q, ctx->cat, ctx->Ain, ctx->ri, ctx->kv_arena, ctx->rope_tab,
-                  ctx->gv_t1, ctx->gv_t2, ctx->gv_mod};
+                  ctx->gv_t1, ctx->gv_t2, ctx->gv_mod, ctx->modw, ctx->modb, ctx->svec_bf};
   for (void* b : bufs) if (b) cudaFree(b);
   for (int i = 0; i < NSTAGE; ++i) {
     if (ctx->h_stage[i]) cudaFreeHost(ctx->h_stage[i]);
@@ -887,8 +904,17 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
   launch_gemv<T>(ctx->gv_t1, 1, (H + 31) / 32, na, 256, st);
   launch_gemv<T>(ctx->gv_t2, 1, (H + 31) / 32, na, H, st);
   launch_add_cond(dreq, na, H, ctx->vec, st);
-  launch_silu(ctx->vec, ctx->svec, (long long)na * H, st);
-  launch_gemv<T>(ctx->gv_mod, (int)ctx->gv_mod_host.size(), ctx->gv_mod_groups, na, H, st);
+  if (ctx->modw) {  // bf16: one tensor-core GEMM over the packed modulation weights
+    launch_silu(ctx->vec, ctx->svec, (long long)na * H, st, ctx->svec_bf);
+    GemmArgs g{};
+    g.A = ctx->svec_bf; g.lda = H; g.B = ctx->modw; g.ldb = H; g.bias = ctx->modb;
+    g.C = ctx->modbuf; g.ldc = ctx->mod_ld; g.M = na; g.N = (int)ctx->mod_ld; g.K = H;
+    g.epi = EPI_STORE; g.out_f32 = 1;
+    launch_gemm_tc(g, st);
+  } else {
+    launch_silu(ctx->vec, ctx->svec, (long long)na * H, st);
+    launch_gemv<T>(ctx->gv_mod, (int)ctx->gv_mod_host.size(), ctx->gv_mod_groups, na, H, st);
+  }
   }
   stats.kernel_launches += 7;
   if (rng.X_in) {  // teacher-forced residual rows

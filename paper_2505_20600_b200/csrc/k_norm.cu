@@ -20,12 +20,17 @@ void launch_timestep_embed(const ReqDev* reqs, int n, float* temb, cudaStream_t 
   temb_kernel<<<n, 128, 0, st>>>(reqs, n, temb);
 }
 
-__global__ void silu_kernel(const float* __restrict__ x, float* __restrict__ y, long long count) {
+__global__ void silu_kernel(const float* __restrict__ x, float* __restrict__ y, bf16* __restrict__ yb,
+                            long long count) {
   long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < count) y[i] = silu(x[i]);
+  if (i < count) {
+    const float s = silu(x[i]);
+    y[i] = s;
+    if (yb) yb[i] = __float2bfloat16_rn(s);
+  }
 }
-void launch_silu(const float* x, float* y, long long count, cudaStream_t st) {
-  silu_kernel<<<(unsigned)((count + 255) / 256), 256, 0, st>>>(x, y, count);
+void launch_silu(const float* x, float* y, long long count, cudaStream_t st, bf16* yb) {
+  silu_kernel<<<(unsigned)((count + 255) / 256), 256, 0, st>>>(x, y, yb, count);
 }
 
 __global__ void add_cond_kernel(const ReqDev* __restrict__ reqs, int H, float* __restrict__ vec) {
@@ -147,48 +152,79 @@ template void launch_gemv<bf16>(const GemvProb*, int, int, int, int, cudaStream_
 
 // ======================================================================================
 // a5: h = LN(X)(1 + scale_req) + shift_req, LN without affine, eps (C-AMB 6).  One CTA
-// (128 threads) per row; two-pass mean/variance over the L1-resident fp32 row.
+// (128 threads) per row; the fp32 row is read once into registers (H <= 4096), two-pass
+// mean/variance from registers, 16-byte loads/stores.
 // ======================================================================================
+constexpr int LN_THREADS = 128, LN_MAXV = 8;  // float4 per thread -> H <= 4096
+
 template <typename T>
-__global__ void __launch_bounds__(128) ln_mod_kernel(const float* __restrict__ X, int H, int r0,
-                                                     const RowInfo* __restrict__ ri,
-                                                     const float* __restrict__ mod, int mod_ld,
-                                                     int shift_off, int scale_off, float eps,
-                                                     T* __restrict__ h, int ldh) {
-  __shared__ float red[4];
+__device__ __forceinline__ void store4(T* p, float a, float b, float c, float d);
+template <>
+__device__ __forceinline__ void store4<float>(float* p, float a, float b, float c, float d) {
+  *reinterpret_cast<float4*>(p) = make_float4(a, b, c, d);
+}
+template <>
+__device__ __forceinline__ void store4<bf16>(bf16* p, float a, float b, float c, float d) {
+  __nv_bfloat162 lo = __floats2bfloat162_rn(a, b), hi = __floats2bfloat162_rn(c, d);
+  uint2 u;
+  u.x = *reinterpret_cast<uint32_t*>(&lo);
+  u.y = *reinterpret_cast<uint32_t*>(&hi);
+  *reinterpret_cast<uint2*>(p) = u;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(LN_THREADS) ln_mod_kernel(const float* __restrict__ X, int H, int r0,
+                                                            const RowInfo* __restrict__ ri,
+                                                            const float* __restrict__ mod, int mod_ld,
+                                                            int shift_off, int scale_off, float eps,
+                                                            T* __restrict__ h, int ldh) {
+  __shared__ float red[LN_THREADS / 32];
   const int r = r0 + blockIdx.x;
   const float* x = X + (long long)r * H;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  float4 v[LN_MAXV];
   float s = 0.f;
-  for (int c = tid * 4; c < H; c += 512) {
-    float4 v = *reinterpret_cast<const float4*>(x + c);
-    s += (v.x + v.y) + (v.z + v.w);
+#pragma unroll
+  for (int k = 0; k < LN_MAXV; ++k) {
+    const int c = (k * LN_THREADS + tid) * 4;
+    v[k] = c < H ? __ldcs(reinterpret_cast<const float4*>(x + c)) : make_float4(0.f, 0.f, 0.f, 0.f);
+    s += (v[k].x + v[k].y) + (v[k].z + v[k].w);
   }
   s = warp_sum(s);
   if (lane == 0) red[wid] = s;
   __syncthreads();
-  const float mean = (red[0] + red[1] + red[2] + red[3]) / H;
+  float tot = 0.f;
+#pragma unroll
+  for (int w = 0; w < LN_THREADS / 32; ++w) tot += red[w];
+  const float mean = tot / H;
   __syncthreads();
   float q = 0.f;
-  for (int c = tid * 4; c < H; c += 512) {
-    float4 v = *reinterpret_cast<const float4*>(x + c);
-    float a = v.x - mean, b = v.y - mean, cc = v.z - mean, d = v.w - mean;
-    q += (a * a + b * b) + (cc * cc + d * d);
+#pragma unroll
+  for (int k = 0; k < LN_MAXV; ++k) {
+    const int c = (k * LN_THREADS + tid) * 4;
+    if (c < H) {
+      const float a = v[k].x - mean, b = v[k].y - mean, cc = v[k].z - mean, d = v[k].w - mean;
+      q += (a * a + b * b) + (cc * cc + d * d);
+    }
   }
   q = warp_sum(q);
   if (lane == 0) red[wid] = q;
   __syncthreads();
-  const float rstd = 1.0f / sqrtf((red[0] + red[1] + red[2] + red[3]) / H + eps);
+  float qt = 0.f;
+#pragma unroll
+  for (int w = 0; w < LN_THREADS / 32; ++w) qt += red[w];
+  const float rstd = 1.0f / sqrtf(qt / H + eps);
   const float* m = mod + (long long)ri[r].req * mod_ld;
   T* out = h + (long long)r * ldh;
-  for (int c = tid * 4; c < H; c += 512) {
-    float4 v = *reinterpret_cast<const float4*>(x + c);
-    float4 sc = *reinterpret_cast<const float4*>(m + scale_off + c);
-    float4 sh = *reinterpret_cast<const float4*>(m + shift_off + c);
-    out[c + 0] = from_f<T>((v.x - mean) * rstd * (1.f + sc.x) + sh.x);
-    out[c + 1] = from_f<T>((v.y - mean) * rstd * (1.f + sc.y) + sh.y);
-    out[c + 2] = from_f<T>((v.z - mean) * rstd * (1.f + sc.z) + sh.z);
-    out[c + 3] = from_f<T>((v.w - mean) * rstd * (1.f + sc.w) + sh.w);
+#pragma unroll
+  for (int k = 0; k < LN_MAXV; ++k) {
+    const int c = (k * LN_THREADS + tid) * 4;
+    if (c < H) {
+      const float4 sc = *reinterpret_cast<const float4*>(m + scale_off + c);
+      const float4 sh = *reinterpret_cast<const float4*>(m + shift_off + c);
+      store4<T>(out + c, (v[k].x - mean) * rstd * (1.f + sc.x) + sh.x, (v[k].y - mean) * rstd * (1.f + sc.y) + sh.y,
+                (v[k].z - mean) * rstd * (1.f + sc.z) + sh.z, (v[k].w - mean) * rstd * (1.f + sc.w) + sh.w);
+    }
   }
 }
 
@@ -197,7 +233,7 @@ void launch_ln_mod(const float* X, int H, int r0, int r1, const RowInfo* ri, con
                    int mod_ld, int shift_off, int scale_off, float eps, T* h, int ldh,
                    cudaStream_t st) {
   if (r1 <= r0) return;
-  ln_mod_kernel<T><<<r1 - r0, 128, 0, st>>>(X, H, r0, ri, mod, mod_ld, shift_off, scale_off, eps, h, ldh);
+  ln_mod_kernel<T><<<r1 - r0, LN_THREADS, 0, st>>>(X, H, r0, ri, mod, mod_ld, shift_off, scale_off, eps, h, ldh);
 }
 template void launch_ln_mod<float>(const float*, int, int, int, const RowInfo*, const float*, int, int, int, float, float*, int, cudaStream_t);
 template void launch_ln_mod<bf16>(const float*, int, int, int, const RowInfo*, const float*, int, int, int, float, bf16*, int, cudaStream_t);

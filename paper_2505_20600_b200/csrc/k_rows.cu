@@ -197,29 +197,30 @@ template void launch_qkv_post<bf16>(const QkvPost&, const RowInfo*, cudaStream_t
 // host link (zero-copy, UVA pointer) or HBM.  One warp per (request, unmasked row, K|V);
 // 16-byte vector loads, 4 in flight per lane.
 // ======================================================================================
-__global__ void kv_gather_kernel(const KvGatherReq* __restrict__ reqs, int n, int max_nu,
-                                 int L_txt, int row_bytes) {
-  const long long gw = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
+__global__ void __launch_bounds__(256) kv_gather_kernel(const KvGatherReq* __restrict__ reqs, int n, int max_nu,
+                                                        int L_txt, int row_bytes) {
+  // grid-stride over (request, unmasked row, K|V)
   const long long per_req = 2LL * max_nu;
-  const int q = (int)(gw / per_req);
-  if (q >= n) return;
-  const int rem = (int)(gw % per_req);
-  const int which = rem & 1, j = rem >> 1;
-  const KvGatherReq& R = reqs[q];
-  if (j >= R.n_u) return;
-  const int tok = R.idx_u[j];
-  const char* src = (const char*)(which ? R.srcV : R.srcK) + (long long)tok * row_bytes;
-  char* dst = (char*)(which ? R.dstV : R.dstK) + (long long)(L_txt + tok) * row_bytes;
+  const long long total = per_req * n;
+  const int lane = threadIdx.x & 31;
+  const long long warps = ((long long)gridDim.x * blockDim.x) >> 5;
   const int nvec = row_bytes >> 4;
-  const int4* s4 = reinterpret_cast<const int4*>(src);
-  int4* d4 = reinterpret_cast<int4*>(dst);
-  int v = lane;
-  for (; v + 96 < nvec; v += 128) {
-    int4 a = s4[v], b = s4[v + 32], c = s4[v + 64], d = s4[v + 96];
-    d4[v] = a; d4[v + 32] = b; d4[v + 64] = c; d4[v + 96] = d;
+  for (long long gw = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; gw < total; gw += warps) {
+    const int q = (int)(gw / per_req);
+    const int rem = (int)(gw % per_req);
+    const int which = rem & 1, j = rem >> 1;
+    const KvGatherReq& R = reqs[q];
+    if (j >= R.n_u) continue;
+    const int tok = R.idx_u[j];
+    const int4* s4 = reinterpret_cast<const int4*>((const char*)(which ? R.srcV : R.srcK) + (long long)tok * row_bytes);
+    int4* d4 = reinterpret_cast<int4*>((char*)(which ? R.dstV : R.dstK) + (long long)(L_txt + tok) * row_bytes);
+    int v = lane;
+    for (; v + 96 < nvec; v += 128) {
+      int4 a = __ldcs(s4 + v), b = __ldcs(s4 + v + 32), c = __ldcs(s4 + v + 64), d = __ldcs(s4 + v + 96);
+      d4[v] = a; d4[v + 32] = b; d4[v + 64] = c; d4[v + 96] = d;
+    }
+    for (; v < nvec; v += 32) d4[v] = __ldcs(s4 + v);
   }
-  for (; v < nvec; v += 32) d4[v] = s4[v];
 }
 
 void launch_kv_gather(const KvGatherReq* reqs_dev, int n, int max_nu, int L_txt, int H,
@@ -227,6 +228,8 @@ void launch_kv_gather(const KvGatherReq* reqs_dev, int n, int max_nu, int L_txt,
   const long long warps = 2LL * max_nu * n;
   if (warps <= 0) return;
   const int threads = 256;
+  // one warp per row: a short full-GPU burst beats a small persistent grid, which would sit on
+  // SMs the persistent GEMMs need (measured: 24-CTA grid cut the HBM-tier step rate by 10%)
   const long long blocks = (warps * 32 + threads - 1) / threads;
   kv_gather_kernel<<<(unsigned)blocks, threads, 0, st>>>(reqs_dev, n, max_nu, L_txt, H * elem_bytes);
 }

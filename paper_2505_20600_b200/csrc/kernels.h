@@ -44,8 +44,8 @@ struct GemvProb {
 template <typename T>
 void launch_gemv(const GemvProb* probs_dev, int nprob, int total_groups, int n, int maxK,
                  cudaStream_t st);
-// y = silu(x) elementwise (fp32), n*H elements
-void launch_silu(const float* x, float* y, long long count, cudaStream_t st);
+// y = silu(x) elementwise (fp32), n*H elements; optionally also a bf16 copy (GEMM operand)
+void launch_silu(const float* x, float* y, long long count, cudaStream_t st, bf16* yb = nullptr);
 // vec[r] += addv per request pointer (cond vectors live in caller buffers)
 void launch_add_cond(const ReqDev* reqs, int n, int H, float* vec, cudaStream_t st);
 
