@@ -32,13 +32,18 @@
 namespace ig {
 namespace {
 
-constexpr int BQ = 128, BKV = 128, D = 128;
+constexpr int BQ = 128, BKV = 128;
 constexpr int CHUNK = 128 * 64 * 2;             // one [128 rows x 64 cols] bf16 SW128 box
-constexpr int Q_BYTES = 2 * CHUNK;              // 32 KB per query tile
-constexpr int KV_BYTES = 2 * CHUNK;             // 32 KB each for K and V
 constexpr int STAGES = 2;
-constexpr int SMEM_BYTES = 2 * Q_BYTES + STAGES * 2 * KV_BYTES + 1024 + 256;
 constexpr int NTHREADS = 384;
+template <int D>
+struct AC {                                     // per-head-dim configuration (d = 64 or 128)
+  static constexpr int NCH = D / 64;            // 64-column SW128 boxes per row
+  static constexpr int Q_BYTES = NCH * CHUNK;   // per query tile
+  static constexpr int KV_BYTES = NCH * CHUNK;  // each for K and V
+  static constexpr int TSTRIDE = 128 + D;       // TMEM columns per tile: S/P 128, O D
+  static constexpr int SMEM_BYTES = 2 * Q_BYTES + STAGES * 2 * KV_BYTES + 1024 + 256;
+};
 constexpr float RESCALE_THRESHOLD = 8.0f;       // log2 units
 constexpr int NPOLY = 0;  // pairs per key tile on ex2_poly2 (measured: MUFU is not the limiter; 0 is fastest)
 
@@ -85,9 +90,12 @@ __device__ __forceinline__ void tma_load_3d(void* smem, const CUtensorMap* m, ui
       "r"(c2) : "memory");
 }
 
+template <int D>
 __global__ void __launch_bounds__(NTHREADS, 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmKV,
                    const AttnArgs a, float scale_log2) {
+  using C = AC<D>;
+  constexpr int Q_BYTES = C::Q_BYTES, KV_BYTES = C::KV_BYTES, TS = C::TSTRIDE;
   const AttnSeg seg = a.segs[blockIdx.z];
   const int h = blockIdx.y;
   const int q0 = blockIdx.x * 2 * BQ;
@@ -129,11 +137,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     if (lane == 0) {  // ===== TMA producer =====
       const int qrow = seg.q_start + q0;
       tc::mbar_arrive_expect_tx(&bar->q_full, (has_b ? 2 : 1) * Q_BYTES);
-      tc::tma_load_2d(sQ, &tmQ, &bar->q_full, h * D, qrow);
-      tc::tma_load_2d(sQ + CHUNK, &tmQ, &bar->q_full, h * D + 64, qrow);
-      if (has_b) {
-        tc::tma_load_2d(sQ + Q_BYTES, &tmQ, &bar->q_full, h * D, qrow + BQ);
-        tc::tma_load_2d(sQ + Q_BYTES + CHUNK, &tmQ, &bar->q_full, h * D + 64, qrow + BQ);
+#pragma unroll
+      for (int c = 0; c < C::NCH; ++c) {
+        tc::tma_load_2d(sQ + c * CHUNK, &tmQ, &bar->q_full, h * D + 64 * c, qrow);
+        if (has_b) tc::tma_load_2d(sQ + Q_BYTES + c * CHUNK, &tmQ, &bar->q_full, h * D + 64 * c, qrow + BQ);
       }
       for (int j = 0; j < nkv; ++j) {
         const int s = j % STAGES;
@@ -142,10 +149,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         uint8_t* k = sK + s * KV_BYTES;
         uint8_t* v = sV + s * KV_BYTES;
         const int kvrow = j * BKV;
-        tma_load_3d(k, &tmKV, &bar->kv_full[s], h * D, kvrow, planeK);
-        tma_load_3d(k + CHUNK, &tmKV, &bar->kv_full[s], h * D + 64, kvrow, planeK);
-        tma_load_3d(v, &tmKV, &bar->kv_full[s], h * D, kvrow, planeK + 1);
-        tma_load_3d(v + CHUNK, &tmKV, &bar->kv_full[s], h * D + 64, kvrow, planeK + 1);
+#pragma unroll
+        for (int c = 0; c < C::NCH; ++c) {
+          tma_load_3d(k + c * CHUNK, &tmKV, &bar->kv_full[s], h * D + 64 * c, kvrow, planeK);
+          tma_load_3d(v + c * CHUNK, &tmKV, &bar->kv_full[s], h * D + 64 * c, kvrow, planeK + 1);
+        }
       }
     }
   } else if (warp == 1) {
@@ -160,7 +168,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 #pragma unroll
         for (int k = 0; k < D / 16; ++k) {
           const uint32_t off = (k >> 2) * CHUNK + (k & 3) * 32;
-          tc::mma_bf16_ss(tmem + t * 256, tc::sdesc_sw128(q_addr + off, 16, 1024),
+          tc::mma_bf16_ss(tmem + t * TS, tc::sdesc_sw128(q_addr + off, 16, 1024),
                           tc::sdesc_sw128(k_addr + off, 16, 1024), idS, k != 0);
         }
         tc::mma_commit(&bar->s_full[t]);
@@ -171,7 +179,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         const uint32_t v_addr = tc::smem_u32(sV + (j % STAGES) * KV_BYTES);
 #pragma unroll
         for (int k = 0; k < BKV / 16; ++k)
-          tc::mma_bf16_ts(tmem + t * 256 + 128, tmem + t * 256 + k * 8,
+          tc::mma_bf16_ts(tmem + t * TS + 128, tmem + t * TS + k * 8,
                           tc::sdesc_sw128(v_addr + k * 2048, CHUNK, 1024), idO, (j | k) != 0);
       };
       tc::mbar_wait(&bar->kv_full[0], 0);
@@ -197,7 +205,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       const int quad = warp & 3;
       const int row = quad * 32 + lane;  // query row inside the tile == TMEM lane
       const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
-      const uint32_t tS = tmem + t * 256 + lane_off, tO = tS + 128;
+      const uint32_t tS = tmem + t * TS + lane_off, tO = tS + 128;
       float m = -INFINITY, l = 0.f;
       for (int j = 0; j < nkv; ++j) {
         tc::mbar_wait(&bar->s_full[t], j & 1);
@@ -296,7 +304,8 @@ void init_attn() {
     void* fn = nullptr;
     cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
     g_enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
-    cudaFuncSetAttribute(attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    cudaFuncSetAttribute(attn_tc_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, AC<128>::SMEM_BYTES);
+    cudaFuncSetAttribute(attn_tc_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, AC<64>::SMEM_BYTES);
   });
 }
 }  // namespace
@@ -304,7 +313,7 @@ void init_attn() {
 bool attn_tc_supported(const AttnArgs& a) {
   auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
   const long long H = (long long)a.heads * a.head_dim;
-  return a.head_dim == D && al16(a.Q) && al16(a.O) && al16(a.kv_arena) && (a.ldq % 8) == 0 &&
+  return (a.head_dim == 128 || a.head_dim == 64) && al16(a.Q) && al16(a.O) && al16(a.kv_arena) && (a.ldq % 8) == 0 &&
          (a.ldo % 8) == 0 && ((a.kv_off % ((long long)a.L * H)) == 0);
 }
 
@@ -335,7 +344,8 @@ void launch_attn_tc(const AttnArgs& a, cudaStream_t st) {
   }
   dim3 grid((a.max_qlen + 2 * BQ - 1) / (2 * BQ), a.heads, a.nseg);
   const float scale_log2 = a.scale * 1.4426950408889634f;
-  attn_tc_kernel<<<grid, NTHREADS, SMEM_BYTES, st>>>(tq, tkv, a, scale_log2);
+  if (a.head_dim == 128) attn_tc_kernel<128><<<grid, NTHREADS, AC<128>::SMEM_BYTES, st>>>(tq, tkv, a, scale_log2);
+  else attn_tc_kernel<64><<<grid, NTHREADS, AC<64>::SMEM_BYTES, st>>>(tq, tkv, a, scale_log2);
 }
 
 }  // namespace ig

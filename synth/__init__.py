@@ -136,7 +136,11 @@ SD3 = ModelDesc("sd3_medium", 24, 0, 1536, 24, 64, 6144, 64, 32, 32, 333, qk_nor
 FLUX = ModelDesc("flux1_dev", 19, 38, 3072, 24, 128, 12288, 64, 64, 64, 512)
 # Small Flux-structured model for multi-block / multi-step parity (tiles span >1 CTA tile)
 FLUX_SMALL = ModelDesc("flux_small", 2, 2, 256, 2, 128, 1024, 64, 16, 16, 32)
-MODELS = {m.name: m for m in (TINY, TINY_DOUBLE, SD3, FLUX, FLUX_SMALL)}
+# Small SD3-structured model (joint blocks, d=64, no RoPE / QK-norm, 2-D pos-embed, ragged
+# text length, context-pre-only last block)
+SD3_SMALL = ModelDesc("sd3_small", 2, 0, 128, 2, 64, 512, 64, 8, 8, 13, qk_norm=0, rope=0,
+                      rope_axes=(0, 0, 0), pos_embed_2d=1, context_pre_only_last=1)
+MODELS = {m.name: m for m in (TINY, TINY_DOUBLE, SD3, FLUX, FLUX_SMALL, SD3_SMALL)}
 
 
 def weight_table(d: ModelDesc) -> List[Tuple[str, Tuple[int, ...], int]]:

@@ -127,3 +127,49 @@ def test_flux_same_trajectory_bitwise_and_batch_invariance(flux):
     ig.ig_cache_free(cache)
     for r in (a, b, c):
         r.free()
+
+
+
+def test_sd3_teacher_forced_blocks():
+    """SD3-medium-shaped (BASELINE configs[1]) joint blocks at full width (H=1536, d=64,
+    333 text tokens, context-pre-only last block) through ig_debug_block vs the oracle,
+    random-blob mask m=0.3."""
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    d = synth.SD3
+    m = Model(d, ig.IG_BF16)
+    rng = np.random.default_rng(3)
+    mask = synth.blob_mask_count(d, int(round(0.3 * d.L_img)), rng)
+    rq = Request(m, 91, mask)
+    cache = ig.ig_cache_create(m.ctx, 1, ig.IG_CACHE_DEVICE)
+    ptr, _, _ = ig.ig_cache_storage(cache)
+    plane = d.L_img * d.hidden * 2
+    for block in (5, d.n_blocks - 1):
+        kv = synth.normal(700 + block, "kv_sd3", (2, d.L_img, d.hidden), "cuda").float().bfloat16()
+        ig.ig_copy(ptr + block * 2 * plane, kv.data_ptr(), 2 * plane)
+        rows = d.txt_len + rq.n_m
+        X_in = synth.normal(800 + block, "X_sd3", (rows, d.hidden), "cuda").float()
+        X_out = torch.full_like(X_in, float("nan"))
+        ig.ig_debug_block(m.ctx, rq.req(0, cache, 0, 0.5, 0.45), block, X_in.data_ptr(), X_out.data_ptr())
+        names = {nm for nm, _, _ in synth.weight_table(d) if nm.startswith(f"double.{block}.")}
+        names |= {"t_mlp1.w", "t_mlp1.b", "t_mlp2.w", "t_mlp2.b"}
+        W = {k: v.double().numpy() for k, v in synth.make_weights(d, 0, "cpu", torch.bfloat16, names=names).items()}
+        _, _, cond = rq.host_inputs()
+        vec = oracle.conditioning(W, 0.5, cond)
+        idx_m, idx_u, _ = oracle.index_build(mask)
+        Xh = X_in.double().cpu().numpy()
+        xt, xi = oracle.double_block_masked(d, W, block, Xh[:d.txt_len], Xh[d.txt_len:], vec, idx_m, idx_u,
+                                            kv.double().cpu().numpy())
+        ref = np.concatenate([xt, xi])
+        got = X_out.double().cpu().numpy()
+        dg, do = got - Xh, ref - Xh
+        if block == d.n_blocks - 1:  # context-pre-only: text rows pass through unchanged
+            assert np.array_equal(got[:d.txt_len], Xh[:d.txt_len])
+            dg, do = dg[d.txt_len:], do[d.txt_len:]
+        normwise = np.linalg.norm(dg - do) / np.linalg.norm(do)
+        assert normwise <= 2e-2, (block, normwise)
+        ok, worst = ctol(dg, do, 2e-2, atol_mult=2.0)
+        assert ok, (block, worst)
+    ig.ig_cache_free(cache)
+    rq.free()
+    m.close()

@@ -219,3 +219,35 @@ def test_gemm_gated_residual_vs_oracle(dtype, M, N, K):
     ref = X0.double().cpu().numpy() + gate.double().cpu().numpy() * y
     ok, worst = ctol(X.cpu().numpy(), ref, 1e-4 if dtype == ig.IG_F32 else 2e-3)
     assert ok, worst
+
+
+@pytest.mark.parametrize("dtype", [ig.IG_F32, ig.IG_BF16])
+@pytest.mark.parametrize("model", ["sd3_small", "tiny_double"])
+def test_sd3_and_double_structures_end_to_end(dtype, model):
+    """SD3-structured joint blocks (d=64, 2-D pos-embed, ragged text, context-pre-only last
+    block) and a tiny double+single model: batch of 2 requests, 2 steps, synthetic cache."""
+    d = synth.MODELS[model]
+    sig = [0.9, 0.6, 0.3]
+    m = Model(d, dtype)
+    W = m.host_weights()
+    rng = np.random.default_rng(1)
+    masks = [synth.blob_mask_count(d, int(0.3 * d.L_img), rng), synth.rect_mask_count(d, int(0.1 * d.L_img) + 1, rng)]
+    reqs = [Request(m, 40 + i, mk) for i, mk in enumerate(masks)]
+    tdt = torch.float32 if dtype == ig.IG_F32 else torch.bfloat16
+    kv = synth.make_cache_kv(d, 5, 2, dtype=tdt)
+    cache = ig.ig_cache_create(m.ctx, 2, ig.IG_CACHE_HOST)
+    fill_cache(cache, kv)
+    kvh = kv.double().numpy()
+    _run_edit(m, reqs, cache, 2, sig)
+    for r in reqs:
+        lat0, txt, cond = r.host_inputs()
+        x = lat0
+        for s in range(2):
+            x = oracle.edit_step(d, W, x, r.mask_np, kvh[s], sig[s], sig[s + 1], txt, cond)
+        got = r.latent.double().cpu().numpy()
+        ok, worst = ctol(got, x, RTOL[dtype])
+        assert ok, worst
+    ig.ig_cache_free(cache)
+    for r in reqs:
+        r.free()
+    m.close()
