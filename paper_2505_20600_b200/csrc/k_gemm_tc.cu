@@ -15,6 +15,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <mutex>
+#include <cstdlib>
 #include "kernels.h"
 #include "tc_common.cuh"
 
@@ -347,10 +348,165 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   if (warp == 1) tc::tmem_dealloc<C::TMEM_COLS>(tmem_base);
 }
 
+
+// ---- 2-CTA variant: a cluster of two CTAs (one TPC) computes a 256 x 256 tile with
+// tcgen05.mma.cta_group::2 (M = 256, N = 256, K = 16).  Each CTA loads its own 128 rows of A
+// and 128 rows (half) of B; both halves of B feed the pair's MMA, halving per-SM operand
+// traffic versus the 1-CTA 128 x 256 tile.  Only the leader CTA issues MMAs; commits are
+// multicast to both CTAs; each CTA's epilogue warps drain their own TMEM (rows 128r..128r+127)
+// and release the accumulator to the leader with a cluster-scope mbarrier arrive.
+struct Cfg2 {
+  static constexpr int STAGES = 6;
+  static constexpr int A_BYTES = 128 * BK * 2;
+  static constexpr int B_BYTES = 128 * BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int TMEM_COLS = 512;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+};
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
+    gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                    const GemmArgs g, int num_m, int num_n) {
+  using C = Cfg2;
+  constexpr int BN = 256;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + C::STAGES * C::A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
+  uint64_t* empty = full + C::STAGES;
+  uint64_t* tfull = empty + C::STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = tc::cluster_ctarank();
+  const int cluster = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
+  const int num_tiles = num_m * num_n;
+  const int num_k = (g.K + BK - 1) / BK;
+
+  if (warp == 0 && lane == 0) {
+    tc::tma_prefetch_desc(&tmA);
+    tc::tma_prefetch_desc(&tmB);
+    for (int s = 0; s < C::STAGES; ++s) {
+      tc::mbar_init(&full[s], 1);
+      tc::mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      tc::mbar_init(&tfull[a], 1);
+      tc::mbar_init(&tempty[a], 8);  // 4 epilogue warps x 2 CTAs (leader's copy is used)
+    }
+    tc::fence_barrier_init();
+  }
+  if (warp == 1) tc::tmem_alloc2<C::TMEM_COLS>(tmem_slot);
+  tc::tc_fence_before();
+  tc::cluster_sync();
+  tc::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ===== TMA producer (both CTAs) =====
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = cluster; t < num_tiles; t += nclusters) {
+        const int m0 = (t / num_n) * 256 + rank * 128, n0 = (t % num_n) * BN + rank * 128;
+        for (int kb = 0; kb < num_k; ++kb) {
+          tc::mbar_wait(&empty[stage], phase ^ 1);
+          if (rank == 0) tc::mbar_arrive_expect_tx(&full[stage], 2 * C::STAGE_BYTES);
+          tc::tma_load_2d_2sm(sA + stage * C::A_BYTES, &tmA, &full[stage], kb * BK, m0);
+          tc::tma_load_2d_2sm(sB + stage * C::B_BYTES, &tmB, &full[stage], kb * BK, n0);
+          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {  // ===== MMA issuer (leader CTA) =====
+      constexpr uint32_t idesc = tc::idesc_bf16(256, BN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int t = cluster; t < num_tiles; t += nclusters) {
+        tc::mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc::tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < num_k; ++kb) {
+          tc::mbar_wait(&full[stage], phase);
+          tc::tc_fence_after();
+          const uint32_t a_addr = tc::smem_u32(sA + stage * C::A_BYTES);
+          const uint32_t b_addr = tc::smem_u32(sB + stage * C::B_BYTES);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k)
+            tc::mma2_bf16_ss(d_tmem, tc::sdesc_sw128(a_addr + k * 32, 16, 1024),
+                             tc::sdesc_sw128(b_addr + k * 32, 16, 1024), idesc, (kb | k) != 0);
+          tc::mma2_commit_mc(&empty[stage], 0x3);
+          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+        }
+        tc::mma2_commit_mc(&tfull[acc], 0x3);
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      }
+    }
+  } else if (warp >= 4) {  // ===== epilogue (both CTAs, own TMEM rows) =====
+    const int quad = warp & 3;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int t = cluster; t < num_tiles; t += nclusters) {
+      const int m0 = (t / num_n) * 256 + rank * 128, n0 = (t % num_n) * BN;
+      tc::mbar_wait(&tfull[acc], acc_phase);
+      tc::tc_fence_after();
+      const int row = m0 + quad * 32 + lane;
+      RowInfo info{0, 0, 0, 0};
+      if (row < g.M && g.ri && (g.epi == EPI_GATED_RES || g.epi == EPI_POS || g.epi == EPI_QKV))
+        info = g.ri[g.ri_off + row];
+      const uint32_t tbase = tmem_base + ((uint32_t)(quad * 32) << 16) + acc * BN;
+      if (g.epi == EPI_QKV) {
+        if (g.qkv.head_dim == 128) {
+#pragma unroll 1
+          for (int c = 0; c < BN; c += 128) {
+            uint32_t v[128];
+#pragma unroll
+            for (int s = 0; s < 4; ++s) tc::tmem_ld32(tbase + c + 32 * s, *reinterpret_cast<uint32_t(*)[32]>(&v[32 * s]));
+            tc::tmem_ld_wait();
+            if (row < g.M && n0 + c < g.N) epilogue_qkv_head<128>(g, row, n0 + c, v, info);
+          }
+        } else {
+#pragma unroll 1
+          for (int c = 0; c < BN; c += 64) {
+            uint32_t v[64];
+#pragma unroll
+            for (int s = 0; s < 2; ++s) tc::tmem_ld32(tbase + c + 32 * s, *reinterpret_cast<uint32_t(*)[32]>(&v[32 * s]));
+            tc::tmem_ld_wait();
+            if (row < g.M && n0 + c < g.N) epilogue_qkv_head<64>(g, row, n0 + c, v, info);
+          }
+        }
+      } else {
+#pragma unroll 1
+        for (int c = 0; c < BN; c += 32) {
+          uint32_t r[32];
+          tc::tmem_ld32(tbase + c, r);
+          tc::tmem_ld_wait();
+          if (row < g.M && n0 + c < g.N) epilogue_chunk<BN>(g, row, n0 + c, r, &info);
+        }
+      }
+      tc::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        if (rank == 0) tc::mbar_arrive(&tempty[acc]);
+        else tc::mbar_arrive_cluster(&tempty[acc], 0);
+      }
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+    }
+  }
+  tc::tc_fence_before();
+  tc::cluster_sync();
+  if (warp == 1) tc::tmem_dealloc2<C::TMEM_COLS>(tmem_base);
+}
+
 // ---- host side -----------------------------------------------------------------------------
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 std::once_flag g_encode_once;
 int g_num_sms = 0;
+bool g_two_cta = true;
 
 void init_driver() {
   std::call_once(g_encode_once, [] {
@@ -363,6 +519,8 @@ void init_driver() {
     cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
     cudaFuncSetAttribute(gemm_tc_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<256>::SMEM);
     cudaFuncSetAttribute(gemm_tc_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<128>::SMEM);
+    cudaFuncSetAttribute(gemm_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg2::SMEM);
+    g_two_cta = getenv("IG_GEMM_1CTA") == nullptr;
   });
 }
 
@@ -399,6 +557,16 @@ void launch_gemm_tc(const GemmArgs& g, cudaStream_t st) {
   if (g.M <= 0 || g.N <= 0) return;
   init_driver();
   const bool wide = g.N > 128 || g.epi == EPI_QKV;
+  if (wide && g_two_cta && g.M > 128) {  // 2-CTA 256 x 256 tiles
+    CUtensorMap ta, tb;
+    make_tmap(&ta, g.A, g.M, g.K, g.lda, 128);
+    make_tmap(&tb, g.B, g.N, g.K, g.ldb, 128);
+    const int num_m = (g.M + 255) / 256, num_n = (g.N + 255) / 256;
+    const int tiles = num_m * num_n;
+    const int clusters = tiles < g_num_sms / 2 ? tiles : g_num_sms / 2;
+    gemm_tc2_kernel<<<2 * clusters, NUM_THREADS, Cfg2::SMEM, st>>>(ta, tb, g, num_m, num_n);
+    return;
+  }
   const int BN = wide ? 256 : 128;
   CUtensorMap ta, tb;
   make_tmap(&ta, g.A, g.M, g.K, g.lda, BM);
