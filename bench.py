@@ -352,9 +352,12 @@ def main():
         ms_max, rsteps_all = ms, float(rsteps)
     value = rsteps_all / N_STEPS / (ms_max / 1e3)
 
-    # end to end through the public API with host buffers (latent H2D + D2H every step)
+    # end to end through the public API with host buffers (latent H2D + D2H every step); each
+    # measured leg replays the same request sequence (fresh batch, same request ids)
     e2e = None
     if not args.no_e2e:
+        batch = Batch(ig, ctx, d, dev, args.max_batch, pool, rid0=rank * 100000)
+        run_loop(ig, ctx, batch, cache, sig, args.warmup, stream)
         hbufs = {r.rid: r.latent.detach().cpu().pin_memory() for r in batch.pool}
         barrier()
         ms_e, rs_e, _, _, _, h2d_e, d2h_e = run_loop(ig, ctx, batch, cache, sig, args.steps, stream, e2e=hbufs)
@@ -373,7 +376,8 @@ def main():
     hbm = None
     if tier == "host" and not args.no_hbm_tier and world == 1:
         dcache = ig.ig_cache_clone(ctx, cache, ig.IG_CACHE_DEVICE)
-        run_loop(ig, ctx, batch, dcache, sig, 2, stream)
+        batch = Batch(ig, ctx, d, dev, args.max_batch, pool, rid0=rank * 100000)
+        run_loop(ig, ctx, batch, dcache, sig, args.warmup, stream)
         barrier()
         ms_h, rs_h, _, per_h, prof_h, _, _ = run_loop(ig, ctx, batch, dcache, sig, args.steps, stream, profile=True)
         barrier()
@@ -406,6 +410,10 @@ def main():
         if world > 1:
             torch.distributed.barrier()
         return
+    traffic = {}
+    tp = os.path.join(ROOT, "profiles", "gemm_traffic.json")
+    if os.path.exists(tp):
+        traffic = json.load(open(tp))
     g = prof["gemm"]
     gemm_tf = g["flops"] / (g["ms"] * 1e-3) / 1e12 if g["ms"] else 0.0
     a = prof["attn"]
@@ -424,7 +432,9 @@ def main():
                    "l2": "inputs larger than L2 (23.7 GB weights + 2.9 GB K/V per request-step streamed)"},
         "roofline": {"bound": "tensor", "kernel": "gemm_tc (tcgen05 bf16)", "achieved": round(gemm_tf, 1),
                      "peak": pk_sus, "unit": "TFLOP/s", "frac": round(gemm_tf / pk_sus, 4),
-                     "traffic": None, "peak_kind": f"bf16 sustained ({pk_src})",
+                     "traffic": traffic.get("dram_bytes_per_launch"),
+                     "traffic_note": traffic.get("note"),
+                     "peak_kind": f"bf16 sustained ({pk_src})",
                      "frac_of_burst": round(gemm_tf / pk_burst, 4)},
         "attn_roofline": {"achieved": round(attn_tf, 1), "unit": "TFLOP/s", "frac": round(attn_tf / pk_sus, 4)},
         "kernel_share_of_step": shares,
