@@ -43,6 +43,19 @@ __device__ __forceinline__ float gelu_tanh_fast(float x) {
   return 0.5f * x * (1.0f + t);
 }
 
+// Grouped raster (L2 reuse): consecutive tiles walk G m-blocks first, then n, so the tiles in
+// flight share a small band of A rows (G blocks) and of B rows; G is sized on the host so the
+// A band stays well inside L2 (measured: n-fastest order re-read B up to 6.5x).
+__device__ __forceinline__ void tile_coords(int t, int num_m, int num_n, int G, int& mb, int& nb) {
+  const int group_size = G * num_n;
+  const int group = t / group_size;
+  const int first_m = group * G;
+  const int gm = min(G, num_m - first_m);
+  const int local = t - group * group_size;
+  mb = first_m + local % gm;
+  nb = local / gm;
+}
+
 // epilogue for one 32-column chunk of one row held in registers
 template <int BN>
 __device__ __forceinline__ void epilogue_chunk(const GemmArgs& g, int row, int col0, const uint32_t (&r)[32],
@@ -216,7 +229,7 @@ __device__ __forceinline__ void epilogue_qkv_head(const GemmArgs& g, int row, in
 template <int BN>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                   const GemmArgs g, int num_m, int num_n) {
+                   const GemmArgs g, int num_m, int num_n, int G) {
   using C = Cfg<BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -256,7 +269,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
-        const int m0 = (t / num_n) * BM, n0 = (t % num_n) * BN;
+        int mb, nb;
+        tile_coords(t, num_m, num_n, G, mb, nb);
+        const int m0 = mb * BM, n0 = nb * BN;
         for (int kb = 0; kb < num_k; ++kb) {
           tc::mbar_wait(&empty[stage], phase ^ 1);
           tc::mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
@@ -300,7 +315,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
-      const int m0 = (t / num_n) * BM, n0 = (t % num_n) * BN;
+      int mb, nb;
+      tile_coords(t, num_m, num_n, G, mb, nb);
+      const int m0 = mb * BM, n0 = nb * BN;
       tc::mbar_wait(&tfull[acc], acc_phase);
       tc::tc_fence_after();
       const int row = m0 + quad * 32 + lane;
@@ -366,7 +383,7 @@ struct Cfg2 {
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                    const GemmArgs g, int num_m, int num_n) {
+                    const GemmArgs g, int num_m, int num_n, int G) {
   using C = Cfg2;
   constexpr int BN = 256;
   extern __shared__ uint8_t smem_raw[];
@@ -409,7 +426,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int t = cluster; t < num_tiles; t += nclusters) {
-        const int m0 = (t / num_n) * 256 + rank * 128, n0 = (t % num_n) * BN + rank * 128;
+        int mb, nb;
+        tile_coords(t, num_m, num_n, G, mb, nb);
+        const int m0 = mb * 256 + rank * 128, n0 = nb * BN + rank * 128;
         for (int kb = 0; kb < num_k; ++kb) {
           tc::mbar_wait(&empty[stage], phase ^ 1);
           if (rank == 0) tc::mbar_arrive_expect_tx(&full[stage], 2 * C::STAGE_BYTES);
@@ -451,7 +470,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int t = cluster; t < num_tiles; t += nclusters) {
-      const int m0 = (t / num_n) * 256 + rank * 128, n0 = (t % num_n) * BN;
+      int mb, nb;
+      tile_coords(t, num_m, num_n, G, mb, nb);
+      const int m0 = mb * 256 + rank * 128, n0 = nb * BN;
       tc::mbar_wait(&tfull[acc], acc_phase);
       tc::tc_fence_after();
       const int row = m0 + quad * 32 + lane;
@@ -538,6 +559,15 @@ bool make_tmap(CUtensorMap* m, const void* ptr, long long rows, long long cols, 
 }
 }  // namespace
 
+// m-blocks per raster group: keep the group's A band (G * rows * K * 2 bytes) around 32 MB
+int raster_group(int num_m, int rows, int K) {
+  const long long band = 32ll << 20;
+  long long G = band / ((long long)rows * K * 2);
+  if (G < 1) G = 1;
+  if (G > num_m) G = num_m;
+  return (int)G;
+}
+
 bool gemm_tc_supported(const GemmArgs& g) {
   auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
   if (!al16(g.A) || !al16(g.B) || (g.lda & 7) || (g.ldb & 7) || (g.K & 7)) return false;
@@ -564,7 +594,8 @@ void launch_gemm_tc(const GemmArgs& g, cudaStream_t st) {
     const int num_m = (g.M + 255) / 256, num_n = (g.N + 255) / 256;
     const int tiles = num_m * num_n;
     const int clusters = tiles < g_num_sms / 2 ? tiles : g_num_sms / 2;
-    gemm_tc2_kernel<<<2 * clusters, NUM_THREADS, Cfg2::SMEM, st>>>(ta, tb, g, num_m, num_n);
+    gemm_tc2_kernel<<<2 * clusters, NUM_THREADS, Cfg2::SMEM, st>>>(ta, tb, g, num_m, num_n,
+                                                                   raster_group(num_m, 256, g.K));
     return;
   }
   const int BN = wide ? 256 : 128;
@@ -574,8 +605,9 @@ void launch_gemm_tc(const GemmArgs& g, cudaStream_t st) {
   const int num_m = (g.M + BM - 1) / BM, num_n = (g.N + BN - 1) / BN;
   const int tiles = num_m * num_n;
   const int grid = tiles < g_num_sms ? tiles : g_num_sms;
-  if (wide) gemm_tc_kernel<256><<<grid, NUM_THREADS, Cfg<256>::SMEM, st>>>(ta, tb, g, num_m, num_n);
-  else gemm_tc_kernel<128><<<grid, NUM_THREADS, Cfg<128>::SMEM, st>>>(ta, tb, g, num_m, num_n);
+  const int G = raster_group(num_m, BM, g.K);
+  if (wide) gemm_tc_kernel<256><<<grid, NUM_THREADS, Cfg<256>::SMEM, st>>>(ta, tb, g, num_m, num_n, G);
+  else gemm_tc_kernel<128><<<grid, NUM_THREADS, Cfg<128>::SMEM, st>>>(ta, tb, g, num_m, num_n, G);
 }
 
 }  // namespace ig
