@@ -291,6 +291,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--model", default="flux1_dev")
     ap.add_argument("--no-hbm-tier", action="store_true", help="skip the HBM-resident template run")
+    ap.add_argument("--no-fp8", action="store_true", help="skip the FP8-cache run")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -314,7 +315,7 @@ def main():
     t_setup = time.time()
     link_peak = measure_h2d(dev)
     W, ptrs = build_model(d, dev)
-    opts = ig.ig_ctx_opts(args.max_batch, args.max_batch * d.L, args.depth, args.copy_mode, 0)
+    opts = ig.ig_ctx_opts(args.max_batch, args.max_batch * d.L, args.depth, args.copy_mode, 0, 0)
     ctx = ig.ig_ctx_create(ig.make_desc(d, ig.IG_BF16), ptrs, local, opts)
     sig = synth.flow_sigmas(N_STEPS)
     # the template: dense 28-step sampler recording every (step, block) K/V (ig_cache_template)
@@ -393,6 +394,28 @@ def main():
                "attn_tflops": round(ah["flops"] / (ah["ms"] * 1e-3) / 1e12, 1) if ah["ms"] else None,
                "kernel_share_of_step": {k: round(v["ms"] / ms_h, 4) for k, v in prof_h.items()}}
 
+    # FP8 (e4m3) cache in pinned host memory (SURVEY N4 byte reducer): a second context on the
+    # same weights whose caches are e4m3 + per-(token, head) scales; same request sequence
+    fp8 = None
+    if tier == "host" and not args.no_fp8 and world == 1:
+        opts8 = ig.ig_ctx_opts(args.max_batch, args.max_batch * d.L, args.depth, args.copy_mode, 0, 1)
+        ctx8 = ig.ig_ctx_create(ig.make_desc(d, ig.IG_BF16), ptrs, local, opts8)
+        cache8 = ig.ig_cache_clone(ctx8, cache, ig.IG_CACHE_HOST)
+        batch = Batch(ig, ctx8, d, dev, args.max_batch, pool, rid0=rank * 100000)
+        run_loop(ig, ctx8, batch, cache8, sig, args.warmup, stream)
+        barrier()
+        ms_8, rs_8, _, _, prof_8, h2d_8, _ = run_loop(ig, ctx8, batch, cache8, sig, args.steps, stream, profile=True)
+        barrier()
+        g8 = prof_8["gemm"]
+        fp8 = {"value": round(rs_8 / N_STEPS / (ms_8 / 1e3), 4), "unit": "images/s",
+               "ms_per_step": round(ms_8 / args.steps, 3),
+               "host_link_GBps": round(h2d_8 / (ms_8 * 1e-3) / 1e9, 2),
+               "gemm_tflops": round(g8["flops"] / (g8["ms"] * 1e-3) / 1e12, 1) if g8["ms"] else None,
+               "kernel_share_of_step": {k: round(v["ms"] / ms_8, 4) for k, v in prof_8.items()},
+               "note": "same workload, K/V cache stored as e4m3 + fp32 scale per (token, head): half the host-link bytes"}
+        ig.ig_cache_free(cache8)
+        ig.ig_ctx_destroy(ctx8)
+
     # dense comparison step (all-ones masks, no cache) on the same GPUs and kernels
     dense = None
     if args.dense_steps > 0:
@@ -451,6 +474,7 @@ def main():
                       "frac": round(h2d / (ms * 1e-3) / 1e9 / link_peak, 4) if link_peak else None,
                       "peak_kind": "pinned H2D cudaMemcpyAsync 512 MiB x8, measured in this run"},
         "hbm_tier": hbm,
+        "fp8_cache_host_tier": fp8,
         "speedup_hbm_tier_vs_dense": round(hbm["value"] / dense, 3) if (hbm and dense) else None,
         "gpu_launches": int(launches),
         "clocks": clk,

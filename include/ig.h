@@ -88,6 +88,9 @@ typedef struct {
                        /*     layer (copy engines); HBM-tier caches via the SM gather      */
                        /* 2 = compacted: zero-copy SM gather kernel on the copy stream     */
   int debug_checks;    /* 1 = check the latent for non-finite values after each step     */
+  int cache_fp8;       /* 1 = caches created by this ctx store K/V as e4m3 with a fp32   */
+                       /*     scale per (token, head): scale = amax/448, x' = bf16(q*scale)*/
+                       /*     (halves host-link bytes; bf16 mode only)          */
 } ig_ctx_opts;
 
 typedef struct ig_ctx ig_ctx;
@@ -122,9 +125,15 @@ ig_status ig_cache_template(ig_ctx* ctx, float* latent, const void* txt, const f
                             const float* sigmas, int n_steps, int tier, void* stream,
                             ig_cache** out);
 
-/* Copy of a cache into another tier (e.g. an HBM-resident hot template): same
- * schedule and layout.  Synchronous. */
+/* Copy of a cache into another tier (e.g. an HBM-resident hot template) in the
+ * cache format of `ctx` (a bf16 cache cloned by a cache_fp8 ctx is quantized per (token,
+ * head) on the device).  Same schedule.  Synchronous. */
 ig_status ig_cache_clone(ig_ctx* ctx, const ig_cache* src, int tier, ig_cache** out);
+
+/* Write a whole cache from caller K/V in the compute dtype (dev or host pointer,
+ * [n_steps][n_blocks][2][L_img][H]); FP8 caches are quantized on the device (per (token, head)
+ * scale = amax/448, e4m3 round-to-nearest-even, saturating).  Synchronous on `stream`. */
+ig_status ig_cache_write(ig_ctx* ctx, ig_cache* cache, const void* kv, void* stream);
 
 /* Raw storage of a cache: host or device pointer (per tier) and its size in bytes, for
  * test I/O and for filling a synthetic cache.  The pointer stays owned by the cache. */

@@ -427,6 +427,47 @@ def reduced_forward_masked_kvcache(x, mask, K_cache, V_cache, Wq, Wk, Wv, Wo, W1
 
 
 # --------------------------------------------------------------------------------------
+# FP8 (e4m3) K/V cache, SURVEY N4 (a byte reducer for the cache, not in the paper): the
+# quantize-dequantize round trip the attention then consumes, mirrored in float32 exactly:
+# per (token, head) scale = amax / 448, q = e4m3 round-to-nearest-even of x / scale
+# (saturating at 448; subnormal quantum 2^-9), x' = bf16(q * scale).
+# --------------------------------------------------------------------------------------
+def e4m3_round(y: np.ndarray) -> np.ndarray:
+    """Nearest e4m3 (fn) value, ties to even, saturating at +-448 (float32 in/out)."""
+    y = np.asarray(y, np.float32)
+    a = np.minimum(np.abs(y).astype(np.float64), 448.0)
+    e = np.floor(np.log2(np.where(a > 0, a, 1.0)))
+    e = np.clip(e, -6, 8)                     # normal exponents; below 2^-6 the quantum is 2^-9
+    quantum = 2.0 ** (e - 3)                  # 3 mantissa bits
+    q = a / quantum
+    r = np.floor(q + 0.5)
+    tie = (q + 0.5) == r                      # exact .5 -> round to even
+    r = np.where(tie & (r % 2 == 1), r - 1, r)
+    out = np.minimum(r * quantum, 448.0)
+    return (np.sign(y) * out).astype(np.float32)
+
+
+def bf16_round(x: np.ndarray) -> np.ndarray:
+    """float32 -> bfloat16 (round to nearest even) -> float32."""
+    x = np.ascontiguousarray(x, np.float32)
+    u = x.view(np.uint32).astype(np.uint64)
+    u = (u + 0x7FFF + ((u >> 16) & 1)) & 0xFFFF0000
+    return u.astype(np.uint32).view(np.float32)
+
+
+def fp8_kv_roundtrip(kv: np.ndarray, heads: int) -> np.ndarray:
+    """kv [..., L, H] (bf16 values) -> the bf16 values attention reads from an FP8 cache."""
+    x = np.asarray(kv, np.float32)
+    shp = x.shape
+    xh = x.reshape(shp[:-1] + (heads, shp[-1] // heads))
+    amax = np.abs(xh).max(axis=-1, keepdims=True).astype(np.float32)
+    scale = np.where(amax > 0, amax / np.float32(448.0), np.float32(1.0)).astype(np.float32)
+    q = e4m3_round((xh / scale).astype(np.float32))
+    deq = (q * scale).astype(np.float32)
+    return bf16_round(deq).reshape(shp).astype(np.float64)
+
+
+# --------------------------------------------------------------------------------------
 # Table 1 closed forms (P:461-482) for the Flux-shaped model, per query row per step
 # --------------------------------------------------------------------------------------
 def macs_per_row_linear(d) -> int:

@@ -103,6 +103,8 @@ struct ig_mask {
 struct ig_cache {
   ig_model_desc desc{};
   int n_steps = 0, tier = 0;
+  int fp8 = 0;              // 1: e4m3 data [steps][blocks][2][L_img][H] + fp32 scales [..][heads]
+  size_t scale_off = 0;     // byte offset of the scale region (fp8 only)
   void* ptr = nullptr;     // pinned host (mapped) or device
   void* dptr = nullptr;    // device-visible pointer (== ptr with UVA)
   size_t bytes = 0;
@@ -157,7 +159,11 @@ struct ig_ctx {
   std::vector<Pref> pref;  // [max_batch * R]
   ig_mask* ones_mask = nullptr;
   std::vector<void*> b_dst, b_src;  // batched-copy scratch (copy_mode 1)
-  bool gather_dev = false;          // this step's caches are all HBM-resident: SM gather
+  bool gather_dev = false;          // unused (kept for layout)
+  // FP8 cache staging (cache_fp8): per (slot, ring buffer) e4m3 rows + scales landed by the DMA
+  // lane before the dequantizing gather into the bf16 ring; per ring buffer for recording
+  uint8_t* q8in = nullptr;  float* q8in_scl = nullptr;
+  uint8_t* q8rec = nullptr; float* q8rec_scl = nullptr;
   std::vector<size_t> b_size;
   ig_stats stats{};
   std::vector<ig_cache*> zombies;
@@ -328,13 +334,14 @@ extern "C" ig_status ig_ctx_create(const ig_model_desc* desc, const void* const*
     return set_err(IG_EINVAL, "expected %d weight pointers, got %d", nw, n_weights);
   for (int i = 0; i < nw; ++i)
     if (!weights[i]) return set_err(IG_EINVAL, "weight %d is NULL", i);
-  ig_ctx_opts o{8, 0, 2, 0, 0};
+  ig_ctx_opts o{8, 0, 2, 0, 0, 0};
   if (opts) o = *opts;
   if (o.max_batch <= 0) o.max_batch = 8;
   if (o.max_batch > 16) return set_err(IG_EUNSUPPORTED, "max_batch > 16");
   if (o.prefetch_depth <= 0) o.prefetch_depth = 2;
   if (o.prefetch_depth + 1 > MAXR) return set_err(IG_EUNSUPPORTED, "prefetch_depth > %d", MAXR - 1);
   if (o.copy_mode < 0 || o.copy_mode > 2) return set_err(IG_EINVAL, "copy_mode must be 0, 1 or 2");
+  if (o.cache_fp8 && desc->dtype != IG_BF16) return set_err(IG_EUNSUPPORTED, "FP8 caches need the bf16 mode");
   const int Lall = desc->txt_len + desc->grid_h * desc->grid_w;
   if (o.max_rows <= 0) o.max_rows = o.max_batch * Lall;
 
@@ -449,8 +456,16 @@ extern "C" ig_status ig_ctx_create(const ig_model_desc* desc, const void* const*
   cudaMemcpy(ctx->gv_mod, ctx->gv_mod_host.data(), ctx->gv_mod_host.size() * sizeof(GemvProb),
              cudaMemcpyHostToDevice);
 
-  // per-step descriptor staging: ReqDev[B] + AttnSeg[2B] + KvGatherReq[nb * B]
-  ctx->stage_bytes = B * sizeof(ReqDev) + 2 * B * sizeof(AttnSeg) + (size_t)ctx->nb * B * sizeof(KvGatherReq) + 1024;
+  if (o.cache_fp8) {
+    const size_t pl = (size_t)ctx->Limg * H, spl = (size_t)ctx->Limg * desc->heads;
+    okm &= dmalloc((void**)&ctx->q8in, (size_t)B * ctx->R * 2 * pl);
+    okm &= dmalloc((void**)&ctx->q8in_scl, (size_t)B * ctx->R * 2 * spl * 4);
+    okm &= dmalloc((void**)&ctx->q8rec, (size_t)ctx->R * 2 * pl);
+    okm &= dmalloc((void**)&ctx->q8rec_scl, (size_t)ctx->R * 2 * spl * 4);
+    if (!okm) { ig_ctx_destroy(ctx); return set_err(IG_ENOMEM, "fp8 staging allocation failed"); }
+  }
+  // per-step descriptor staging: ReqDev[B] + AttnSeg[2B] + 2 x KvGatherReq[nb * B]
+  ctx->stage_bytes = B * sizeof(ReqDev) + 2 * B * sizeof(AttnSeg) + 2 * (size_t)ctx->nb * B * sizeof(KvGatherReq) + 1024;
   for (int i = 0; i < NSTAGE; ++i) {
     if (cudaHostAlloc((void**)&ctx->h_stage[i], ctx->stage_bytes, cudaHostAllocDefault) != cudaSuccess ||
         cudaMalloc((void**)&ctx->d_stage[i], ctx->stage_bytes) != cudaSuccess) {
@@ -479,7 +494,8 @@ extern "C" void ig_ctx_destroy(ig_ctx* ctx) {
   for (auto* z : ctx->zombies) free_cache_now(z);
   void* bufs[] = {ctx->X, ctx->vel, ctx->temb, ctx->tmp, ctx->vec, ctx->svec, ctx->modbuf, ctx->h,
                   ctx->qkv, ctx->Q, ctx->cat, ctx->Ain, ctx->ri, ctx->kv_arena, ctx->rope_tab,
-                  ctx->gv_t1, ctx->gv_t2, ctx->gv_mod, ctx->modw, ctx->modb, ctx->svec_bf};
+                  ctx->gv_t1, ctx->gv_t2, ctx->gv_mod, ctx->modw, ctx->modb, ctx->svec_bf,
+                  ctx->q8in, ctx->q8in_scl, ctx->q8rec, ctx->q8rec_scl};
   for (void* b : bufs) if (b) cudaFree(b);
   for (int i = 0; i < NSTAGE; ++i) {
     if (ctx->h_stage[i]) cudaFreeHost(ctx->h_stage[i]);
@@ -606,8 +622,24 @@ static ig_status get_ones_mask(ig_ctx* ctx, ig_mask** out) {
 // ----------------------------------------------------------------------------------------
 // caches
 // ----------------------------------------------------------------------------------------
-static size_t cache_bytes(const ig_ctx* ctx, int n_steps) {
+static size_t cache_bytes(const ig_ctx* ctx, int n_steps, int fp8 = 0) {
+  if (fp8) return (size_t)n_steps * ctx->nb * 2 * ctx->Limg * ((size_t)ctx->H + 4 * ctx->d.heads);
   return (size_t)n_steps * ctx->nb * 2 * ctx->Limg * ctx->H * ctx->esz;
+}
+// data plane (which = 0 K, 1 V) of (step, block) and its scale plane (fp8 caches)
+static char* cache_plane(const ig_ctx* ctx, const ig_cache* c, int step, int b, int which) {
+  const size_t row = c->fp8 ? (size_t)ctx->H : (size_t)ctx->H * ctx->esz;
+  return (char*)c->ptr + (((size_t)step * ctx->nb + b) * 2 + which) * ctx->Limg * row;
+}
+static float* cache_scales(const ig_ctx* ctx, const ig_cache* c, int step, int b, int which) {
+  return (float*)((char*)c->ptr + c->scale_off +
+                  (((size_t)step * ctx->nb + b) * 2 + which) * ctx->Limg * ctx->d.heads * 4);
+}
+static const char* cache_plane_dev(const ig_ctx* ctx, const ig_cache* c, int step, int b, int which) {
+  return (const char*)c->dptr + (cache_plane(ctx, c, step, b, which) - (char*)c->ptr);
+}
+static const float* cache_scales_dev(const ig_ctx* ctx, const ig_cache* c, int step, int b, int which) {
+  return (const float*)((const char*)c->dptr + ((char*)cache_scales(ctx, c, step, b, which) - (char*)c->ptr));
 }
 
 extern "C" ig_status ig_cache_create(ig_ctx* ctx, int n_steps, int tier, ig_cache** out) {
@@ -621,7 +653,9 @@ extern "C" ig_status ig_cache_create(ig_ctx* ctx, int n_steps, int tier, ig_cach
   c->n_steps = n_steps;
   c->tier = tier;
   c->device = ctx->device;
-  c->bytes = cache_bytes(ctx, n_steps);
+  c->fp8 = ctx->o.cache_fp8;
+  c->bytes = cache_bytes(ctx, n_steps, c->fp8);
+  if (c->fp8) c->scale_off = (size_t)n_steps * ctx->nb * 2 * ctx->Limg * ctx->H;
   cudaError_t e;
   if (tier == IG_CACHE_HOST) {
     e = cudaHostAlloc(&c->ptr, c->bytes, cudaHostAllocMapped | cudaHostAllocPortable);
@@ -634,7 +668,7 @@ extern "C" ig_status ig_cache_create(ig_ctx* ctx, int n_steps, int tier, ig_cach
     cudaGetLastError();
     if (c->ptr) { if (tier == IG_CACHE_HOST) cudaFreeHost(c->ptr); else cudaFree(c->ptr); }
     delete c;
-    return set_err(IG_ENOMEM, "cache allocation of %zu bytes failed: %s", cache_bytes(ctx, n_steps),
+    return set_err(IG_ENOMEM, "cache allocation of %zu bytes failed: %s", cache_bytes(ctx, n_steps, ctx->o.cache_fp8),
                    cudaGetErrorString(e));
   }
   *out = c;
@@ -645,12 +679,61 @@ extern "C" ig_status ig_cache_clone(ig_ctx* ctx, const ig_cache* src, int tier, 
   if (!ctx || !src || !out) return set_err(IG_EINVAL, "NULL argument");
   *out = nullptr;
   if (!desc_equal(src->desc, ctx->d)) return set_err(IG_ECACHE_INCOMPAT, "cache built for another model");
+  const bool quantize = ctx->o.cache_fp8 && !src->fp8;  // bf16 -> fp8 conversion
+  if (!ctx->o.cache_fp8 && src->fp8) return set_err(IG_EUNSUPPORTED, "cannot clone an fp8 cache into bf16");
+  CUDA_TRY(cudaSetDevice(ctx->device));
   ig_cache* c = nullptr;
   ig_status s = ig_cache_create(ctx, src->n_steps, tier, &c);
   if (s != IG_OK) return s;
-  cudaError_t e = cudaMemcpy(c->ptr, src->ptr, src->bytes, cudaMemcpyDefault);
+  cudaError_t e = cudaSuccess;
+  if (!quantize) {
+    e = cudaMemcpy(c->ptr, src->ptr, src->bytes, cudaMemcpyDefault);
+  } else {  // per (step, block): bf16 planes -> device temp -> quantize -> destination
+    const size_t pl = (size_t)ctx->Limg * ctx->H, spl = (size_t)ctx->Limg * ctx->d.heads;
+    void* tmp = nullptr;
+    e = cudaMalloc(&tmp, 2 * pl * 2);
+    for (int st = 0; st < src->n_steps && e == cudaSuccess; ++st)
+      for (int b = 0; b < ctx->nb && e == cudaSuccess; ++b) {
+        e = cudaMemcpy(tmp, cache_plane(ctx, src, st, b, 0), 2 * pl * 2, cudaMemcpyDefault);
+        if (e != cudaSuccess) break;
+        launch_kv_quant((const bf16*)tmp, (const bf16*)tmp + pl, ctx->Limg, ctx->H, ctx->d.heads, ctx->q8rec,
+                        ctx->q8rec + pl, ctx->q8rec_scl, ctx->q8rec_scl + spl, 0);
+        for (int w = 0; w < 2 && e == cudaSuccess; ++w) {
+          e = cudaMemcpy(cache_plane(ctx, c, st, b, w), ctx->q8rec + w * pl, pl, cudaMemcpyDefault);
+          if (e == cudaSuccess)
+            e = cudaMemcpy(cache_scales(ctx, c, st, b, w), ctx->q8rec_scl + w * spl, spl * 4, cudaMemcpyDefault);
+        }
+      }
+    if (tmp) cudaFree(tmp);
+  }
   if (e != cudaSuccess) { free_cache_now(c); return set_err(IG_ECUDA, "cache clone: %s", cudaGetErrorString(e)); }
   *out = c;
+  return IG_OK;
+}
+
+extern "C" ig_status ig_cache_write(ig_ctx* ctx, ig_cache* c, const void* kv, void* stream) {
+  if (!ctx || !c || !kv) return set_err(IG_EINVAL, "NULL argument");
+  if (!desc_equal(c->desc, ctx->d)) return set_err(IG_ECACHE_INCOMPAT, "cache built for another model");
+  if (c->fp8 && !ctx->q8rec) return set_err(IG_EUNSUPPORTED, "fp8 cache needs a ctx created with cache_fp8");
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t pl = (size_t)ctx->Limg * ctx->H, spl = (size_t)ctx->Limg * ctx->d.heads;
+  for (int s = 0; s < c->n_steps; ++s)
+    for (int b = 0; b < ctx->nb; ++b) {
+      const char* src = (const char*)kv + (((size_t)s * ctx->nb + b) * 2) * pl * ctx->esz;
+      if (c->fp8) {
+        launch_kv_quant((const bf16*)src, (const bf16*)(src + pl * ctx->esz), ctx->Limg, ctx->H, ctx->d.heads,
+                        ctx->q8rec, ctx->q8rec + pl, ctx->q8rec_scl, ctx->q8rec_scl + spl, st);
+        for (int w = 0; w < 2; ++w) {
+          CUDA_TRY(cudaMemcpyAsync(cache_plane(ctx, c, s, b, w), ctx->q8rec + w * pl, pl, cudaMemcpyDefault, st));
+          CUDA_TRY(cudaMemcpyAsync(cache_scales(ctx, c, s, b, w), ctx->q8rec_scl + w * spl, spl * 4, cudaMemcpyDefault, st));
+        }
+        CUDA_TRY(cudaStreamSynchronize(st));
+      } else {
+        CUDA_TRY(cudaMemcpyAsync(cache_plane(ctx, c, s, b, 0), src, 2 * pl * ctx->esz, cudaMemcpyDefault, st));
+      }
+    }
+  CUDA_TRY(cudaStreamSynchronize(st));
   return IG_OK;
 }
 
@@ -687,76 +770,104 @@ struct StepReq {
 };
 
 // Enqueue the cached K/V of block b for every cache-using request into ring buffer b % R.
+// Per request, by cache kind:
+//   bf16, host tier : copy_mode 0 -> two full-L memcpys; else DMA runs of unmasked rows
+//   bf16, HBM tier  : copy_mode 0 -> two full-L memcpys; else the SM gather kernel
+//   fp8 (any tier)  : host tier first lands e4m3 runs + scale planes in a staging buffer by DMA;
+//                     then the dequantizing gather writes bf16 unmasked rows into the ring
+// kvg_dev/kvq_dev: per (block, request) gather descriptors (n_u = 0 when not applicable).
+struct CopyPlan {
+  bool any = false, gather = false, gather_q8 = false;
+  int max_nu = 0;
+};
+
 static void issue_copy(ig_ctx* ctx, const std::vector<StepReq>& sr, const KvGatherReq* kvg_dev,
-                       const std::vector<KvGatherReq>& kvg_host, int b, bool any_cache,
-                       int max_nu) {
-  if (!any_cache) return;
+                       const KvGatherReq* kvq_dev, int b, const CopyPlan& plan) {
+  if (!plan.any) return;
   const int buf = b % ctx->R;
   cudaStreamWaitEvent(ctx->copy_st, ctx->ev_comp[buf], 0);
   const int n = (int)sr.size();
-  if (ctx->o.copy_mode == 2 || (ctx->o.copy_mode == 1 && ctx->gather_dev)) {
-    ctx->stats.kernel_launches++;
-    launch_kv_gather(kvg_dev + (size_t)b * n, n, max_nu, ctx->Lt, ctx->H, (int)ctx->esz, ctx->copy_st);
-    for (int q = 0; q < n; ++q)
-      if (sr[q].use_cache) {
-        const long long by = 2LL * kvg_host[(size_t)b * n + q].n_u * ctx->H * ctx->esz;
-        if (sr[q].r->cache->tier == IG_CACHE_HOST) ctx->stats.h2d_bytes += by; else ctx->stats.d2d_bytes += by;
-      }
-  } else if (ctx->o.copy_mode == 1) {
-    // compacted: only the unmasked rows, as runs of consecutive tokens, one batched DMA call
-    const size_t row = (size_t)ctx->H * ctx->esz;
-    const size_t plane = (size_t)ctx->Limg * row;
-    const size_t txt_off = (size_t)ctx->Lt * row, vplane = (size_t)ctx->L * row;
-    std::vector<void*>& dsts = ctx->b_dst;
-    std::vector<void*>& srcs = ctx->b_src;
-    std::vector<size_t>& sizes = ctx->b_size;
-    dsts.clear(); srcs.clear(); sizes.clear();
+  const size_t row = (size_t)ctx->H * ctx->esz;
+  const size_t txt_off = (size_t)ctx->Lt * row, vplane = (size_t)ctx->L * row;
+  std::vector<void*>& dsts = ctx->b_dst;
+  std::vector<void*>& srcs = ctx->b_src;
+  std::vector<size_t>& sizes = ctx->b_size;
+  dsts.clear(); srcs.clear(); sizes.clear();
+  for (int q = 0; q < n; ++q) {
+    if (!sr[q].use_cache) continue;
+    const ig_edit_req* r = sr[q].r;
+    const ig_cache* c = r->cache;
+    const bool host = c->tier == IG_CACHE_HOST;
+    const int slot = r->slot;
+    const int n_u = ctx->Limg - sr[q].m->n_m;
     long long by = 0;
-    bool host = false;
-    for (int q = 0; q < n; ++q) {
-      if (!sr[q].use_cache) continue;
-      const ig_edit_req* r = sr[q].r;
-      host |= r->cache->tier == IG_CACHE_HOST;
-      const char* src = (const char*)r->cache->ptr + ((size_t)r->step * ctx->nb + b) * 2 * plane;
-      char* dst = (char*)ctx->kv_arena + ((size_t)r->slot * ctx->slot_stride + (size_t)buf * ctx->buf_elems) * ctx->esz;
-      for (auto& run : sr[q].m->runs) {
-        const size_t off = (size_t)run.first * row, len = (size_t)run.second * row;
-        dsts.push_back(dst + txt_off + off); srcs.push_back((void*)(src + off)); sizes.push_back(len);
-        dsts.push_back(dst + vplane + txt_off + off); srcs.push_back((void*)(src + plane + off)); sizes.push_back(len);
-        by += 2 * (long long)len;
+    if (c->fp8) {
+      by = 2LL * n_u * (ctx->H + 4 * ctx->d.heads);
+      if (host) {  // e4m3 runs + whole scale planes -> staging (slot, buf)
+        const size_t pl = (size_t)ctx->Limg * ctx->H, spl = (size_t)ctx->Limg * ctx->d.heads * 4;
+        uint8_t* sd = ctx->q8in + ((size_t)slot * ctx->R + buf) * 2 * pl;
+        char* ss = (char*)ctx->q8in_scl + ((size_t)slot * ctx->R + buf) * 2 * spl;
+        for (int w = 0; w < 2; ++w) {
+          const char* src = cache_plane(ctx, c, r->step, b, w);
+          for (auto& run : sr[q].m->runs) {
+            dsts.push_back(sd + w * pl + (size_t)run.first * ctx->H);
+            srcs.push_back((void*)(src + (size_t)run.first * ctx->H));
+            sizes.push_back((size_t)run.second * ctx->H);
+          }
+          dsts.push_back(ss + w * spl);
+          srcs.push_back((void*)cache_scales(ctx, c, r->step, b, w));
+          sizes.push_back(spl);
+        }
+        by = 2LL * n_u * ctx->H + 2LL * ctx->Limg * ctx->d.heads * 4;
       }
-    }
-    if (!sizes.empty()) {
-      cudaMemcpyAttributes attr{};
-      attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-      attr.flags = cudaMemcpyFlagPreferOverlapWithCompute;
-      size_t attr_idx = 0, fail = 0;
-      constexpr size_t CHUNKC = 128;  // bounded batches (very large batches crash driver 580)
-      for (size_t i = 0; i < sizes.size(); i += CHUNKC) {
-        const size_t c = std::min(CHUNKC, sizes.size() - i);
-        cudaMemcpyBatchAsync(dsts.data() + i, srcs.data() + i, sizes.data() + i, c, &attr, &attr_idx, 1, &fail,
-                             ctx->copy_st);
+    } else if (ctx->o.copy_mode == 0) {
+      const size_t plane = (size_t)ctx->Limg * row;
+      auto& pf = ctx->pref[(size_t)slot * ctx->R + buf];
+      const bool prefetched = (pf.c == c && pf.step == r->step && b < ctx->R);
+      pf = ig_ctx::Pref{};
+      if (!prefetched) {
+        char* dst = (char*)ctx->kv_arena + ((size_t)slot * ctx->slot_stride + (size_t)buf * ctx->buf_elems) * ctx->esz;
+        cudaMemcpyAsync(dst + txt_off, cache_plane(ctx, c, r->step, b, 0), plane, cudaMemcpyDefault, ctx->copy_st);
+        cudaMemcpyAsync(dst + vplane + txt_off, cache_plane(ctx, c, r->step, b, 1), plane, cudaMemcpyDefault,
+                        ctx->copy_st);
+        by = 2 * (long long)plane;
       }
+    } else if (host && ctx->o.copy_mode == 1) {  // DMA runs straight into the ring
+      char* dst = (char*)ctx->kv_arena + ((size_t)slot * ctx->slot_stride + (size_t)buf * ctx->buf_elems) * ctx->esz;
+      for (int w = 0; w < 2; ++w) {
+        const char* src = cache_plane(ctx, c, r->step, b, w);
+        for (auto& run : sr[q].m->runs) {
+          const size_t off = (size_t)run.first * row;
+          dsts.push_back(dst + w * vplane + txt_off + off);
+          srcs.push_back((void*)(src + off));
+          sizes.push_back((size_t)run.second * row);
+        }
+      }
+      by = 2LL * n_u * row;
+    } else {
+      by = 2LL * n_u * row;  // SM gather kernel below
     }
     if (host) ctx->stats.h2d_bytes += by; else ctx->stats.d2d_bytes += by;
-  } else {
-    const size_t plane = (size_t)ctx->Limg * ctx->H * ctx->esz;
-    for (int q = 0; q < n; ++q) {
-      if (!sr[q].use_cache) continue;
-      const ig_edit_req* r = sr[q].r;
-      const int slot = r->slot;
-      auto& pf = ctx->pref[(size_t)slot * ctx->R + buf];
-      const bool prefetched = (pf.c == r->cache && pf.step == r->step && b < ctx->R);
-      pf = ig_ctx::Pref{};
-      if (prefetched) continue;
-      const char* src = (const char*)r->cache->ptr + ((size_t)r->step * ctx->nb + b) * 2 * plane;
-      char* dst = (char*)ctx->kv_arena + ((size_t)slot * ctx->slot_stride + (size_t)buf * ctx->buf_elems) * ctx->esz;
-      const size_t txt_off = (size_t)ctx->Lt * ctx->H * ctx->esz;
-      const size_t vplane = (size_t)ctx->L * ctx->H * ctx->esz;
-      cudaMemcpyAsync(dst + txt_off, src, plane, cudaMemcpyDefault, ctx->copy_st);
-      cudaMemcpyAsync(dst + vplane + txt_off, src + plane, plane, cudaMemcpyDefault, ctx->copy_st);
-      if (r->cache->tier == IG_CACHE_HOST) ctx->stats.h2d_bytes += 2 * plane; else ctx->stats.d2d_bytes += 2 * plane;
+  }
+  if (!sizes.empty()) {
+    cudaMemcpyAttributes attr{};
+    attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
+    attr.flags = cudaMemcpyFlagPreferOverlapWithCompute;
+    size_t attr_idx = 0, fail = 0;
+    constexpr size_t CHUNKC = 128;  // bounded batches (very large batches crash driver 580)
+    for (size_t i = 0; i < sizes.size(); i += CHUNKC) {
+      const size_t cnt = std::min(CHUNKC, sizes.size() - i);
+      cudaMemcpyBatchAsync(dsts.data() + i, srcs.data() + i, sizes.data() + i, cnt, &attr, &attr_idx, 1, &fail,
+                           ctx->copy_st);
     }
+  }
+  if (plan.gather) {
+    ctx->stats.kernel_launches++;
+    launch_kv_gather(kvg_dev + (size_t)b * n, n, plan.max_nu, ctx->Lt, ctx->H, (int)ctx->esz, ctx->copy_st);
+  }
+  if (plan.gather_q8) {
+    ctx->stats.kernel_launches++;
+    launch_kv_gather_q8(kvq_dev + (size_t)b * n, n, plan.max_nu, ctx->Lt, ctx->H, ctx->d.heads, ctx->copy_st);
   }
   cudaEventRecord(ctx->ev_copy[buf], ctx->copy_st);
 }
@@ -851,41 +962,66 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
     max_q = std::max(max_q, d.n_m);
     img_row += d.n_m;
   }
-  // compacted copies: DMA runs over the host link, an SM gather kernel for HBM-resident caches
-  bool all_dev = any_cache;
-  for (auto& s : sr) if (s.use_cache && s.r->cache->tier != IG_CACHE_DEVICE) all_dev = false;
-  ctx->gather_dev = ctx->o.copy_mode == 1 && all_dev;
-  const bool use_gather = ctx->o.copy_mode == 2 || ctx->gather_dev;
-  std::vector<KvGatherReq> kvg_host;
-  if (any_cache && use_gather) {
-    kvg_host.resize((size_t)nb * na);
-    const size_t plane = (size_t)ctx->Limg * H;
+  // copy-lane plan and per-(block, request) gather descriptors (see issue_copy)
+  CopyPlan plan;
+  plan.any = any_cache;
+  plan.max_nu = max_nu;
+  KvGatherReq* hkvq = hkvg + (size_t)nb * ctx->o.max_batch;
+  KvGatherReq* dkvq = dkvg + (size_t)nb * ctx->o.max_batch;
+  if (any_cache) {
+    for (int q = 0; q < na; ++q) {
+      if (!sr[q].use_cache) continue;
+      const ig_cache* c = sr[q].r->cache;
+      if (c->fp8) plan.gather_q8 = true;
+      else if (c->tier == IG_CACHE_DEVICE ? ctx->o.copy_mode != 0 : ctx->o.copy_mode == 2) plan.gather = true;
+    }
     for (int b = 0; b < nb; ++b)
       for (int q = 0; q < na; ++q) {
-        KvGatherReq g{};
+        KvGatherReq g{}, gq{};
         const ig_edit_req* r = sr[q].r;
         if (sr[q].use_cache) {
-          const char* base = (const char*)r->cache->dptr + (((size_t)r->step * nb + b) * 2 * plane) * es;
-          g.srcK = base;
-          g.srcV = base + plane * es;
-          g.idx_u = sr[q].m->idx + ctx->Limg;
-          g.n_u = ctx->Limg - sr[q].m->n_m;
+          const ig_cache* c = r->cache;
           char* dst = (char*)ctx->kv_arena + ((size_t)r->slot * ctx->slot_stride + (size_t)(b % R) * ctx->buf_elems) * es;
-          g.dstK = dst;
-          g.dstV = dst + (size_t)ctx->L * H * es;
+          const int n_u = ctx->Limg - sr[q].m->n_m;
+          if (c->fp8) {
+            gq.idx_u = sr[q].m->idx + ctx->Limg;
+            gq.n_u = n_u;
+            gq.dstK = dst;
+            gq.dstV = dst + (size_t)ctx->L * H * es;
+            if (c->tier == IG_CACHE_HOST) {  // dequantize from the staging the DMA lands in
+              const size_t pl = (size_t)ctx->Limg * H, spl = (size_t)ctx->Limg * ctx->d.heads;
+              const size_t sb = (size_t)r->slot * R + (b % R);
+              gq.srcK = ctx->q8in + sb * 2 * pl;
+              gq.srcV = ctx->q8in + sb * 2 * pl + pl;
+              gq.sclK = ctx->q8in_scl + sb * 2 * spl;
+              gq.sclV = ctx->q8in_scl + sb * 2 * spl + spl;
+            } else {
+              gq.srcK = cache_plane_dev(ctx, c, r->step, b, 0);
+              gq.srcV = cache_plane_dev(ctx, c, r->step, b, 1);
+              gq.sclK = cache_scales_dev(ctx, c, r->step, b, 0);
+              gq.sclV = cache_scales_dev(ctx, c, r->step, b, 1);
+            }
+          } else if (c->tier == IG_CACHE_DEVICE ? ctx->o.copy_mode != 0 : ctx->o.copy_mode == 2) {
+            g.srcK = cache_plane_dev(ctx, c, r->step, b, 0);
+            g.srcV = cache_plane_dev(ctx, c, r->step, b, 1);
+            g.idx_u = sr[q].m->idx + ctx->Limg;
+            g.n_u = n_u;
+            g.dstK = dst;
+            g.dstV = dst + (size_t)ctx->L * H * es;
+          }
         }
-        kvg_host[(size_t)b * na + q] = g;
         hkvg[(size_t)b * na + q] = g;
+        hkvq[(size_t)b * na + q] = gq;
       }
   }
-  const size_t desc_bytes = (char*)(hkvg + (any_cache && use_gather ? (size_t)nb * na : 0)) - hs;
+  const size_t desc_bytes = (char*)(hkvq + (any_cache ? (size_t)nb * na : 0)) - hs;
   CUDA_TRY(cudaMemcpyAsync(ds, hs, desc_bytes, cudaMemcpyHostToDevice, st));
   CUDA_TRY(cudaEventRecord(ctx->ev_desc, st));
   if (any_cache) CUDA_TRY(cudaStreamWaitEvent(ctx->copy_st, ctx->ev_desc, 0));
   for (auto& s : sr) if (s.use_cache) { s.r->cache->pins.fetch_add(1); }
 
   // ---- prefetch the first R blocks (copy lane) ----
-  for (int b = b0; b < std::min(b0 + R, b1); ++b) issue_copy(ctx, sr, dkvg, kvg_host, b, any_cache, max_nu);
+  for (int b = b0; b < std::min(b0 + R, b1); ++b) issue_copy(ctx, sr, dkvg, dkvq, b, plan);
 
   T* h = (T*)ctx->h;
   T* qkv = (T*)ctx->qkv;
@@ -1007,13 +1143,30 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
     cudaEventRecord(ctx->ev_comp[buf], st);
     cudaStreamWaitEvent(ctx->copy_st, ctx->ev_comp[buf], 0);
     const size_t plane = (size_t)ctx->Limg * H * es;
-    char* dst = (char*)record->ptr + ((size_t)record_step * nb + b) * 2 * plane;
     const char* src = (const char*)ctx->kv_arena + ((size_t)sr[0].r->slot * ctx->slot_stride + (size_t)buf * ctx->buf_elems) * es;
     const size_t txt_off = (size_t)Lt * H * es;
     const size_t vplane = (size_t)ctx->L * H * es;
-    cudaMemcpyAsync(dst, src + txt_off, plane, cudaMemcpyDefault, ctx->copy_st);
-    cudaMemcpyAsync(dst + plane, src + vplane + txt_off, plane, cudaMemcpyDefault, ctx->copy_st);
-    if (record->tier == IG_CACHE_HOST) stats.d2h_bytes += 2 * plane; else stats.d2d_bytes += 2 * plane;
+    if (record->fp8) {  // quantize on the compute stream into the recording staging, then D2H
+      const size_t pl = (size_t)ctx->Limg * H, spl = (size_t)ctx->Limg * ctx->d.heads;
+      uint8_t* qd = ctx->q8rec + (size_t)buf * 2 * pl;
+      float* qs = ctx->q8rec_scl + (size_t)buf * 2 * spl;
+      launch_kv_quant((const bf16*)(src + txt_off), (const bf16*)(src + vplane + txt_off), ctx->Limg, H,
+                      ctx->d.heads, qd, qd + pl, qs, qs + spl, st);
+      cudaEventRecord(ctx->ev_comp[buf], st);
+      cudaStreamWaitEvent(ctx->copy_st, ctx->ev_comp[buf], 0);
+      for (int w = 0; w < 2; ++w) {
+        cudaMemcpyAsync(cache_plane(ctx, record, record_step, b, w), qd + w * pl, pl, cudaMemcpyDefault, ctx->copy_st);
+        cudaMemcpyAsync(cache_scales(ctx, record, record_step, b, w), qs + w * spl, spl * 4, cudaMemcpyDefault,
+                        ctx->copy_st);
+      }
+      const long long by = 2LL * (pl + spl * 4);
+      if (record->tier == IG_CACHE_HOST) stats.d2h_bytes += by; else stats.d2d_bytes += by;
+    } else {
+      cudaMemcpyAsync(cache_plane(ctx, record, record_step, b, 0), src + txt_off, plane, cudaMemcpyDefault, ctx->copy_st);
+      cudaMemcpyAsync(cache_plane(ctx, record, record_step, b, 1), src + vplane + txt_off, plane, cudaMemcpyDefault,
+                      ctx->copy_st);
+      if (record->tier == IG_CACHE_HOST) stats.d2h_bytes += 2 * plane; else stats.d2d_bytes += 2 * plane;
+    }
     cudaEventRecord(ctx->ev_copy[buf], ctx->copy_st);
   };
   // full-L copies also write the masked rows, so they must land before the fresh K/V
@@ -1041,7 +1194,7 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
       attn(buf);
       record_kv(b, buf);
       cudaEventRecord(ctx->ev_comp[buf], st);
-      if (b + R < b1) issue_copy(ctx, sr, dkvg, kvg_host, b + R, any_cache, max_nu);
+      if (b + R < b1) issue_copy(ctx, sr, dkvg, dkvq, b + R, plan);
       const long long gi = ctx->mods[wi.mod_t].off;
       gemm_rows(M_txt, M, cat, ldcat, wi.proj.w, wi.proj.b, H, H, ctx->X, H, EPI_GATED_RES, mod + gi + 2 * H, 0);
       ln_mod(M_txt, M, wi.mod_t, 3, 4);
@@ -1066,7 +1219,7 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
       attn(buf);
       record_kv(b, buf);
       cudaEventRecord(ctx->ev_comp[buf], st);
-      if (b + R < b1) issue_copy(ctx, sr, dkvg, kvg_host, b + R, any_cache, max_nu);
+      if (b + R < b1) issue_copy(ctx, sr, dkvg, dkvq, b + R, plan);
       const long long gs = ctx->mods[ws.mod_t].off;
       gemm_rows(0, M, cat, ldcat, ws.lin2.w, ws.lin2.b, H, H + F, ctx->X, H, EPI_GATED_RES, mod + gs + 2 * H, 0);
     }
@@ -1170,13 +1323,13 @@ extern "C" ig_status ig_prefetch_layer(ig_ctx* ctx, const ig_edit_req* r, int la
   if (!r->cache) return set_err(IG_ECACHE_MISS, "no cache");
   if (!desc_equal(r->cache->desc, ctx->d)) return set_err(IG_ECACHE_INCOMPAT, "cache built for another model");
   if (r->step < 0 || r->step >= r->cache->n_steps) return set_err(IG_ECACHE_INCOMPAT, "step out of range");
-  if (ctx->o.copy_mode != 0) return set_err(IG_EUNSUPPORTED, "explicit prefetch needs copy_mode 0");
+  if (ctx->o.copy_mode != 0 || r->cache->fp8) return set_err(IG_EUNSUPPORTED, "explicit prefetch needs copy_mode 0 and a bf16 cache");
   CUDA_TRY(cudaSetDevice(ctx->device));
   const int buf = layer % ctx->R;
   const size_t es = ctx->esz, H = ctx->H;
   const size_t plane = (size_t)ctx->Limg * H * es;
   CUDA_TRY(cudaStreamWaitEvent(ctx->copy_st, ctx->ev_comp[buf], 0));
-  const char* src = (const char*)r->cache->ptr + ((size_t)r->step * ctx->nb + layer) * 2 * plane;
+  const char* src = cache_plane(ctx, r->cache, r->step, layer, 0);
   char* dst = (char*)ctx->kv_arena + ((size_t)r->slot * ctx->slot_stride + (size_t)buf * ctx->buf_elems) * es;
   const size_t txt_off = (size_t)ctx->Lt * H * es, vplane = (size_t)ctx->L * H * es;
   CUDA_TRY(cudaMemcpyAsync(dst + txt_off, src, plane, cudaMemcpyDefault, ctx->copy_st));

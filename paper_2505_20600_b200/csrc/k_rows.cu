@@ -1,6 +1,7 @@
 // k_rows.cu — kernels (a) index build and (b) row gather / positional K/V merge / scatter.
 // All of these are exact copies or integer work (bit-exact, SURVEY §8(c) C-PIN) except the
 // QK-norm/RoPE epilogue, which is token-wise fp arithmetic.
+#include <cuda_fp8.h>
 #include "kernels.h"
 
 namespace ig {
@@ -232,6 +233,92 @@ void launch_kv_gather(const KvGatherReq* reqs_dev, int n, int max_nu, int L_txt,
   // SMs the persistent GEMMs need (measured: 24-CTA grid cut the HBM-tier step rate by 10%)
   const long long blocks = (warps * 32 + threads - 1) / threads;
   kv_gather_kernel<<<(unsigned)blocks, threads, 0, st>>>(reqs_dev, n, max_nu, L_txt, H * elem_bytes);
+}
+
+// ======================================================================================
+// FP8 (e4m3) K/V cache.  Quantize: per (token, head) scale = amax / 448 (fp32),
+// q = e4m3 round-to-nearest-even of x / scale (saturating); amax = 0 -> scale 1.
+// ======================================================================================
+__global__ void __launch_bounds__(256) kv_quant_kernel(const bf16* __restrict__ srcK, const bf16* __restrict__ srcV,
+                                                       long long rows, int H, int heads, uint8_t* __restrict__ dstK,
+                                                       uint8_t* __restrict__ dstV, float* __restrict__ sclK,
+                                                       float* __restrict__ sclV) {
+  const long long gw = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (gw >= 2 * rows) return;
+  const int which = (int)(gw & 1);
+  const long long r = gw >> 1;
+  const bf16* s = (which ? srcV : srcK) + r * H;
+  uint8_t* d = (which ? dstV : dstK) + r * H;
+  float* sc = (which ? sclV : sclK) + r * heads;
+  const int dh = H / heads;
+  for (int h = 0; h < heads; ++h) {
+    float amax = 0.f;
+    for (int c = lane; c < dh; c += 32) amax = fmaxf(amax, fabsf(__bfloat162float(s[h * dh + c])));
+    amax = warp_max(amax);
+    const float scale = amax > 0.f ? amax / 448.0f : 1.0f;
+    for (int c = lane; c < dh; c += 32) {
+      const float y = __bfloat162float(s[h * dh + c]) / scale;
+      d[h * dh + c] = (uint8_t)__nv_cvt_float_to_fp8(y, __NV_SATFINITE, __NV_E4M3);
+    }
+    if (lane == 0) sc[h] = scale;
+  }
+}
+
+void launch_kv_quant(const bf16* srcK, const bf16* srcV, long long rows, int H, int heads, uint8_t* dstK,
+                     uint8_t* dstV, float* sclK, float* sclV, cudaStream_t st) {
+  if (rows <= 0) return;
+  const long long warps = 2 * rows;
+  kv_quant_kernel<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, st>>>(srcK, srcV, rows, H, heads, dstK, dstV,
+                                                                          sclK, sclV);
+}
+
+__device__ __forceinline__ float e4m3_to_float(uint8_t b) {
+  __half_raw hr = __nv_cvt_fp8_to_halfraw((__nv_fp8_storage_t)b, __NV_E4M3);
+  return __half2float(__half(hr));
+}
+
+// gather + dequantize: ring[L_txt + tok] = bf16(e4m3(src[tok]) * scale[tok][head]) for tok in idx_u
+__global__ void __launch_bounds__(256) kv_gather_q8_kernel(const KvGatherReq* __restrict__ reqs, int n, int max_nu,
+                                                           int L_txt, int H, int heads) {
+  const long long per_req = 2LL * max_nu;
+  const long long total = per_req * n;
+  const int lane = threadIdx.x & 31;
+  const long long warps = ((long long)gridDim.x * blockDim.x) >> 5;
+  const int dh = H / heads;
+  for (long long gw = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; gw < total; gw += warps) {
+    const int q = (int)(gw / per_req);
+    const int rem = (int)(gw % per_req);
+    const int which = rem & 1, j = rem >> 1;
+    const KvGatherReq& R = reqs[q];
+    if (j >= R.n_u) continue;
+    const int tok = R.idx_u[j];
+    const uint8_t* s = (const uint8_t*)(which ? R.srcV : R.srcK) + (long long)tok * H;
+    const float* sc = (which ? R.sclV : R.sclK) + (long long)tok * heads;
+    bf16* d = (bf16*)(which ? R.dstV : R.dstK) + (long long)(L_txt + tok) * H;
+    for (int c = lane * 16; c < H; c += 512) {  // 16 e4m3 values (one head) per lane-iteration
+      const uint4 raw = __ldcs(reinterpret_cast<const uint4*>(s + c));
+      const float scale = __ldg(sc + c / dh);
+      const uint8_t* b = reinterpret_cast<const uint8_t*>(&raw);
+      uint4 o[2];
+      uint32_t* w = reinterpret_cast<uint32_t*>(o);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        __nv_bfloat162 p = __floats2bfloat162_rn(e4m3_to_float(b[2 * e]) * scale, e4m3_to_float(b[2 * e + 1]) * scale);
+        w[e] = *reinterpret_cast<uint32_t*>(&p);
+      }
+      reinterpret_cast<uint4*>(d + c)[0] = o[0];
+      reinterpret_cast<uint4*>(d + c)[1] = o[1];
+    }
+  }
+}
+
+void launch_kv_gather_q8(const KvGatherReq* reqs_dev, int n, int max_nu, int L_txt, int H, int heads,
+                         cudaStream_t st) {
+  const long long warps = 2LL * max_nu * n;
+  if (warps <= 0) return;
+  const long long blocks = (warps * 32 + 255) / 256;
+  kv_gather_q8_kernel<<<(unsigned)blocks, 256, 0, st>>>(reqs_dev, n, max_nu, L_txt, H, heads);
 }
 
 // ======================================================================================

@@ -76,11 +76,19 @@ void launch_qkv_post(const QkvPost& p, const RowInfo* ri, cudaStream_t st);
 // for each of n requests with cache: rows idx_u of src K and V (host-mapped or device)
 // -> ring rows L_txt + idx_u.
 struct KvGatherReq {
-  const void* srcK; const void* srcV;  // [L_img, H]
+  const void* srcK; const void* srcV;  // [L_img, H] (compute dtype, or e4m3 bytes for q8)
   const int32_t* idx_u; int n_u;
   void* dstK; void* dstV;              // [L, H] positional ring buffer
-  int pad[2];
+  const float* sclK; const float* sclV;  // q8 only: [L_img, heads] dequantization scales
 };
+// FP8 (e4m3) K/V cache: per (token, head) scale = amax / 448, q = e4m3_rn(x / scale)
+// (saturating), x' = bf16(q * scale).  Quantize rows [0, rows) of src (bf16 [rows, H]) to
+// dst (u8 [rows, H]) + scl ([rows, heads]); one warp per (row, K|V plane).
+void launch_kv_quant(const bf16* srcK, const bf16* srcV, long long rows, int H, int heads, uint8_t* dstK,
+                     uint8_t* dstV, float* sclK, float* sclV, cudaStream_t st);
+// gather + dequantize unmasked rows of an e4m3 source into the bf16 ring buffer
+void launch_kv_gather_q8(const KvGatherReq* reqs_dev, int n, int max_nu, int L_txt, int H, int heads,
+                         cudaStream_t st);
 void launch_kv_gather(const KvGatherReq* reqs_dev, int n, int max_nu, int L_txt, int H,
                       int elem_bytes, cudaStream_t st);
 

@@ -24,7 +24,7 @@ EXPORTS = ["ig_weight_count", "ig_ctx_create", "ig_ctx_destroy", "ig_cache_creat
            "ig_cache_template", "ig_cache_storage", "ig_cache_free", "ig_mask_build",
            "ig_mask_indices", "ig_mask_free", "ig_edit_step", "ig_prefetch_layer",
            "ig_last_error", "ig_last_stats", "ig_op_gemm", "ig_op_gemm_gated", "ig_op_attention", "ig_copy",
-           "ig_profile_enable", "ig_profile_read", "ig_debug_block", "ig_cache_clone"]
+           "ig_profile_enable", "ig_profile_read", "ig_debug_block", "ig_cache_clone", "ig_cache_write"]
 KCLASS = ["gemm", "attn", "lnmod", "qkvpost", "cond", "rows"]
 
 
@@ -49,7 +49,7 @@ class ig_model_desc(ctypes.Structure):
 class ig_ctx_opts(ctypes.Structure):
     _fields_ = [("max_batch", ctypes.c_int), ("max_rows", ctypes.c_int),
                 ("prefetch_depth", ctypes.c_int), ("copy_mode", ctypes.c_int),
-                ("debug_checks", ctypes.c_int)]
+                ("debug_checks", ctypes.c_int), ("cache_fp8", ctypes.c_int)]
 
 
 class ig_edit_req(ctypes.Structure):
@@ -103,6 +103,7 @@ def lib():
         L.ig_op_gemm_gated.argtypes = [i, vp, ll, vp, ll, vp, vp, ll, vp, i, i, i, vp]
         L.ig_profile_enable.argtypes = [vp, i]
         L.ig_cache_clone.argtypes = [vp, vp, i, P(vp)]
+        L.ig_cache_write.argtypes = [vp, vp, vp, vp]
         L.ig_debug_block.argtypes = [vp, P(ig_edit_req), i, vp, vp, vp]
         L.ig_profile_read.argtypes = [vp, P(ig_prof_entry)]
         for name in EXPORTS:
@@ -250,3 +251,7 @@ def ig_cache_clone(ctx: int, cache: int, tier: int) -> int:
     out = ctypes.c_void_p()
     _check(lib().ig_cache_clone(ctx, cache, tier, ctypes.byref(out)))
     return out.value
+
+
+def ig_cache_write(ctx: int, cache: int, kv_ptr: int, stream: int = 0):
+    _check(lib().ig_cache_write(ctx, cache, kv_ptr, stream))

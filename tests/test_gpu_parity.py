@@ -149,7 +149,7 @@ def test_flux_small_batch_end_to_end(dtype, copy_mode):
     cache, 2 steps, against the oracle request by request."""
     d = synth.FLUX_SMALL
     sig = [1.0, 0.7, 0.4]
-    opts = ig.ig_ctx_opts(4, 0, 2, copy_mode, 0)
+    opts = ig.ig_ctx_opts(4, 0, 2, copy_mode, 0, 0)
     m = Model(d, dtype, opts=opts)
     W = m.host_weights()
     rng = np.random.default_rng(0)
@@ -247,6 +247,43 @@ def test_sd3_and_double_structures_end_to_end(dtype, model):
         got = r.latent.double().cpu().numpy()
         ok, worst = ctol(got, x, RTOL[dtype])
         assert ok, worst
+    ig.ig_cache_free(cache)
+    for r in reqs:
+        r.free()
+    m.close()
+
+
+
+@pytest.mark.parametrize("tier", [ig.IG_CACHE_HOST, ig.IG_CACHE_DEVICE])
+def test_fp8_cache_end_to_end(tier):
+    """FP8 (e4m3) K/V cache: the oracle mirrors the quantize/dequantize round trip
+    of the same synthetic bf16 cache; batch of 2 requests, 2 steps, host and HBM tiers."""
+    d = synth.FLUX_SMALL
+    sig = [1.0, 0.7, 0.4]
+    m = Model(d, ig.IG_BF16, opts=ig.ig_ctx_opts(4, 0, 2, 1, 0, 1))
+    W = m.host_weights()
+    rng = np.random.default_rng(2)
+    masks = [synth.blob_mask_count(d, 70, rng), synth.rect_mask_count(d, 30, rng)]
+    reqs = [Request(m, 60 + i, mk) for i, mk in enumerate(masks)]
+    kv = synth.make_cache_kv(d, 9, 2, dtype=torch.bfloat16, device="cuda")
+    cache = ig.ig_cache_create(m.ctx, 2, ig.IG_CACHE_HOST)
+    ig.ig_cache_write(m.ctx, cache, kv.data_ptr())
+    if tier == ig.IG_CACHE_DEVICE:
+        dc = ig.ig_cache_clone(m.ctx, cache, ig.IG_CACHE_DEVICE)
+        ig.ig_cache_free(cache)
+        cache = dc
+    kvh = oracle.fp8_kv_roundtrip(kv.float().cpu().numpy(), d.heads)
+    _run_edit(m, reqs, cache, 2, sig)
+    for r in reqs:
+        lat0, txt, cond = r.host_inputs()
+        x = lat0
+        for s in range(2):
+            x = oracle.edit_step(d, W, x, r.mask_np, kvh[s], sig[s], sig[s + 1], txt, cond)
+        got = r.latent.double().cpu().numpy()
+        ok, worst = ctol(got, x, 2e-2)
+        assert ok, worst
+    st = ig.ig_last_stats(m.ctx)
+    assert st["h2d_bytes"] + st["d2d_bytes"] > 0
     ig.ig_cache_free(cache)
     for r in reqs:
         r.free()

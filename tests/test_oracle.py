@@ -321,3 +321,33 @@ def test_table1_flux_per_row_closed_form():
     assert abs(lin / 1e9 - 12.910) < 1e-3 and abs(att / 1e9 - 3.2275) < 1e-4
     F = lambda m: (lin + att) * (512 + 4096 * m) / 1e12
     assert abs(F(0) - 8.262) < 1e-3 and abs(F(1) - 74.36) < 1e-2
+
+
+
+# ---------------------------------------------------------------- FP8 cache round trip (N4)
+def test_e4m3_round_matches_torch_float8():
+    # library routine: torch float8_e4m3fn conversion (RNE) on in-range values
+    g = torch.Generator().manual_seed(0)
+    y = torch.cat([torch.randn(20000, generator=g) * 50, torch.randn(20000, generator=g) * 1e-3,
+                   torch.tensor([0.0, 448.0, -448.0, 2 ** -9, 2 ** -10, 3 * 2 ** -10, 0.0625 + 2 ** -8])])
+    y = y.clamp(-448, 448).float()
+    ref = y.to(torch.float8_e4m3fn).float().numpy()
+    assert np.array_equal(oracle.e4m3_round(y.numpy()), ref)
+
+
+def test_bf16_round_matches_torch():
+    x = torch.randn(50000, generator=torch.Generator().manual_seed(1)) * 3
+    assert np.array_equal(oracle.bf16_round(x.numpy()), x.bfloat16().float().numpy())
+
+
+def test_fp8_roundtrip_error_bound_and_scale_invariance():
+    rng = np.random.default_rng(0)
+    kv = oracle.bf16_round(rng.standard_normal((2, 64, 256)).astype(np.float32)).astype(np.float64)
+    r = oracle.fp8_kv_roundtrip(kv, 2)
+    # e4m3: 3 mantissa bits -> relative error <= 2^-4 (+ bf16 rounding) for normal values
+    rel = np.abs(r - kv) / np.maximum(np.abs(kv), 1e-3)
+    assert np.quantile(rel, 0.99) < 2 ** -4 + 2 ** -8
+    # per-(token, head) amax is represented exactly (q = 448 -> x' = amax up to bf16)
+    amax = np.abs(kv.reshape(2, 64, 2, 128)).max(-1)
+    ramax = np.abs(r.reshape(2, 64, 2, 128)).max(-1)
+    assert np.allclose(ramax, amax, rtol=2 ** -8)
