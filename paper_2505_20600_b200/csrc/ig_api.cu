@@ -1014,10 +1014,15 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
         hkvq[(size_t)b * na + q] = gq;
       }
   }
-  const size_t desc_bytes = (char*)(hkvq + (any_cache ? (size_t)nb * na : 0)) - hs;
+  // the compute stream's descriptors go up on the compute stream; the copy lane's gather
+  // descriptors on the copy stream, so the copy lane never waits for the previous step's
+  // compute tail before it starts this step's prefetch (no bubble at step boundaries)
+  const size_t desc_bytes = (char*)hkvg - hs;
   CUDA_TRY(cudaMemcpyAsync(ds, hs, desc_bytes, cudaMemcpyHostToDevice, st));
-  CUDA_TRY(cudaEventRecord(ctx->ev_desc, st));
-  if (any_cache) CUDA_TRY(cudaStreamWaitEvent(ctx->copy_st, ctx->ev_desc, 0));
+  if (plan.gather || plan.gather_q8) {
+    const size_t off = (char*)hkvg - hs, bytes = (char*)(hkvq + (size_t)nb * na) - (char*)hkvg;
+    CUDA_TRY(cudaMemcpyAsync(ds + off, hs + off, bytes, cudaMemcpyHostToDevice, ctx->copy_st));
+  }
   for (auto& s : sr) if (s.use_cache) { s.r->cache->pins.fetch_add(1); }
 
   // ---- prefetch the first R blocks (copy lane) ----
