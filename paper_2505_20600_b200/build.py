@@ -29,7 +29,7 @@ def _compile(src, extra):
     return src, obj, p.returncode, p.stdout + p.stderr
 
 
-def build(verbose=False, extra=()):
+def build(verbose=False, extra=(), out=None):
     os.makedirs(OBJ, exist_ok=True)
     os.makedirs(os.path.dirname(LIB), exist_ok=True)
     extra = list(extra)
@@ -40,7 +40,8 @@ def build(verbose=False, extra=()):
             if rc != 0:
                 raise RuntimeError(f"nvcc failed on {src}:\n{log}")
             objs.append(obj)
-    link = [NVCC] + ARCH + ["-shared", "--cudart", "static", "-o", LIB] + objs
+    lib = out or LIB
+    link = [NVCC] + ARCH + ["-shared", "--cudart", "static", "-o", lib] + objs
     p = subprocess.run(link, capture_output=True, text=True)
     if p.returncode != 0:
         raise RuntimeError("link failed:\n" + p.stdout + p.stderr)
@@ -50,7 +51,7 @@ def build(verbose=False, extra=()):
     if verbose:
         for k, v in logs.items():
             print(f"==== {k}\n{v}")
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":
@@ -59,4 +60,7 @@ if __name__ == "__main__":
         ex.append("-G")
     if "--hang-check" in sys.argv:
         ex.append("-DIG_HANG_CHECK")
-    print(build(verbose="-v" in sys.argv, extra=ex))
+    out = None
+    if "--out" in sys.argv:
+        out = sys.argv[sys.argv.index("--out") + 1]
+    print(build(verbose="-v" in sys.argv, extra=ex, out=out))

@@ -217,17 +217,21 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         tc::tmem_ld32(tS + 96, *reinterpret_cast<uint32_t(*)[32]>(&r[96]));
         tc::tmem_ld_wait();
         const int valid = a.L - j * BKV;  // keys >= L are masked (ragged last tile only)
-        float mx = -INFINITY;
-        if (valid >= BKV) {
+        // row max as 8 independent partial chains (latency, one warp per SMSP in this phase)
+        float pm[8];
 #pragma unroll
-          for (int i = 0; i < 128; i += 2) mx = fmaxf(mx, fmaxf(__uint_as_float(r[i]), __uint_as_float(r[i + 1])));
-        } else {
+        for (int u = 0; u < 8; ++u) pm[u] = -INFINITY;
+        if (valid < BKV) {
 #pragma unroll
-          for (int i = 0; i < 128; ++i) {
+          for (int i = 0; i < 128; ++i)
             if (i >= valid) r[i] = __float_as_uint(-INFINITY);
-            mx = fmaxf(mx, __uint_as_float(r[i]));
-          }
         }
+#pragma unroll
+        for (int i = 0; i < 128; i += 8)
+#pragma unroll
+          for (int u = 0; u < 8; ++u) pm[u] = fmaxf(pm[u], __uint_as_float(r[i + u]));
+        const float mx = fmaxf(fmaxf(fmaxf(pm[0], pm[1]), fmaxf(pm[2], pm[3])),
+                               fmaxf(fmaxf(pm[4], pm[5]), fmaxf(pm[6], pm[7])));
         // scores in log2 units: s * scale * log2(e).  Keep the stale max unless it grew by
         // more than the threshold (per row).
         const float mxs = mx * scale_log2;
@@ -235,16 +239,19 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         const float alpha = exp2f(m - m_use);  // 1 when kept, 0 on the first tile
         const float2 sc2 = make_float2(scale_log2, scale_log2);
         const float2 nm2 = make_float2(-m_use, -m_use);
-        float2 acc2 = make_float2(0.f, 0.f);
+        float2 acc[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) acc[u] = make_float2(0.f, 0.f);
 #pragma unroll
         for (int i = 0; i < 64; ++i) {  // in-place pack: r[i] <- bf16x2(p[2i], p[2i+1])
           const float2 x = __ffma2_rn(make_float2(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1])), sc2, nm2);
-          // ~3/8 of the exponentials on the FMA pipe, the rest on MUFU
           const float2 pp = (i < NPOLY) ? ex2_poly2(x) : make_float2(ex2_fast(x.x), ex2_fast(x.y));
-          acc2 = __fadd2_rn(acc2, pp);
+          acc[i & 3] = __fadd2_rn(acc[i & 3], pp);
           r[i] = pack_bf16(pp.x, pp.y);
         }
-        const float sum = acc2.x + acc2.y;
+        const float2 s01 = __fadd2_rn(acc[0], acc[1]), s23 = __fadd2_rn(acc[2], acc[3]);
+        const float2 s4 = __fadd2_rn(s01, s23);
+        const float sum = s4.x + s4.y;
         tc::tmem_st32(tS + 0, &r[0]);
         tc::tmem_st32(tS + 32, &r[32]);
         if (j > 0 && __any_sync(0xffffffffu, m_use > m)) {

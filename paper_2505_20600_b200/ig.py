@@ -12,7 +12,7 @@ import os
 from typing import List, Optional, Sequence
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libig.so")
+LIB_PATH = os.environ.get("IG_LIB_OVERRIDE") or os.path.join(_HERE, "lib", "libig.so")  # override: A/B benchmarking only
 _lib = None
 
 IG_F32, IG_BF16 = 0, 1
