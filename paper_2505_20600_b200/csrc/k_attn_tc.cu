@@ -34,7 +34,8 @@ namespace {
 
 constexpr int BQ = 128, BKV = 128;
 constexpr int CHUNK = 128 * 64 * 2;             // one [128 rows x 64 cols] bf16 SW128 box
-constexpr int STAGES = 2;
+constexpr int KSTAGES = 3;   // K ring (needed first: S = Q K^T), fetched two tiles ahead
+constexpr int VSTAGES = 2;   // V ring (needed one softmax later: O += P V)
 constexpr int NTHREADS = 384;
 template <int D>
 struct AC {                                     // per-head-dim configuration (d = 64 or 128)
@@ -42,14 +43,14 @@ struct AC {                                     // per-head-dim configuration (d
   static constexpr int Q_BYTES = NCH * CHUNK;   // per query tile
   static constexpr int KV_BYTES = NCH * CHUNK;  // each for K and V
   static constexpr int TSTRIDE = 128 + D;       // TMEM columns per tile: S/P 128, O D
-  static constexpr int SMEM_BYTES = 2 * Q_BYTES + STAGES * 2 * KV_BYTES + 1024 + 256;
+  static constexpr int SMEM_BYTES = 2 * Q_BYTES + (KSTAGES + VSTAGES) * KV_BYTES + 1024 + 256;
 };
 constexpr float RESCALE_THRESHOLD = 8.0f;       // log2 units
 constexpr int NPOLY = 0;  // pairs per key tile on ex2_poly2 (measured: MUFU is not the limiter; 0 is fastest)
 
 struct Bars {
   uint64_t q_full;
-  uint64_t kv_full[STAGES], kv_empty[STAGES];
+  uint64_t k_full[KSTAGES], k_empty[KSTAGES], v_full[VSTAGES], v_empty[VSTAGES];
   uint64_t s_full[2], p_full[2], o_done[2];
   uint32_t tmem;
 };
@@ -58,6 +59,17 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   __nv_bfloat162 p = __floats2bfloat162_rn(a, b);
   return *reinterpret_cast<uint32_t*>(&p);
 }
+
+#ifdef IG_ATTN_TRACE
+__device__ long long g_trace[5][2][40];
+#define TRACE(ev, t, j)                                                                              \
+  do {                                                                                               \
+    if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && (j) < 40)                           \
+      g_trace[ev][t][j] = (long long)clock64();                                                      \
+  } while (0)
+#else
+#define TRACE(ev, t, j) do { } while (0)
+#endif
 
 __device__ __forceinline__ float ex2_fast(float x) {
   float y;
@@ -105,9 +117,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = smem;                              // [2 tiles][Q_BYTES]
-  uint8_t* sK = sQ + 2 * Q_BYTES;                  // [STAGES][KV_BYTES]
-  uint8_t* sV = sK + STAGES * KV_BYTES;            // [STAGES][KV_BYTES]
-  Bars* bar = reinterpret_cast<Bars*>(sV + STAGES * KV_BYTES);
+  uint8_t* sK = sQ + 2 * Q_BYTES;                  // [KSTAGES][KV_BYTES]
+  uint8_t* sV = sK + KSTAGES * KV_BYTES;           // [VSTAGES][KV_BYTES]
+  Bars* bar = reinterpret_cast<Bars*>(sV + VSTAGES * KV_BYTES);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nkv = (a.L + BKV - 1) / BKV;
@@ -119,7 +131,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     tc::tma_prefetch_desc(&tmQ);
     tc::tma_prefetch_desc(&tmKV);
     tc::mbar_init(&bar->q_full, 1);
-    for (int s = 0; s < STAGES; ++s) { tc::mbar_init(&bar->kv_full[s], 1); tc::mbar_init(&bar->kv_empty[s], 1); }
+    for (int s = 0; s < KSTAGES; ++s) { tc::mbar_init(&bar->k_full[s], 1); tc::mbar_init(&bar->k_empty[s], 1); }
+    for (int s = 0; s < VSTAGES; ++s) { tc::mbar_init(&bar->v_full[s], 1); tc::mbar_init(&bar->v_empty[s], 1); }
     for (int t = 0; t < 2; ++t) {
       tc::mbar_init(&bar->s_full[t], 1);
       tc::mbar_init(&bar->p_full[t], 4);
@@ -142,18 +155,24 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         tc::tma_load_2d(sQ + c * CHUNK, &tmQ, &bar->q_full, h * D + 64 * c, qrow);
         if (has_b) tc::tma_load_2d(sQ + Q_BYTES + c * CHUNK, &tmQ, &bar->q_full, h * D + 64 * c, qrow + BQ);
       }
-      for (int j = 0; j < nkv; ++j) {
-        const int s = j % STAGES;
-        tc::mbar_wait(&bar->kv_empty[s], ((j / STAGES) & 1) ^ 1);
-        tc::mbar_arrive_expect_tx(&bar->kv_full[s], 2 * KV_BYTES);
-        uint8_t* k = sK + s * KV_BYTES;
-        uint8_t* v = sV + s * KV_BYTES;
-        const int kvrow = j * BKV;
+      for (int j = 0; j < nkv; ++j) {  // K ring
+        const int s = j % KSTAGES;
+        tc::mbar_wait(&bar->k_empty[s], ((j / KSTAGES) & 1) ^ 1);
+        tc::mbar_arrive_expect_tx(&bar->k_full[s], KV_BYTES);
 #pragma unroll
-        for (int c = 0; c < C::NCH; ++c) {
-          tma_load_3d(k + c * CHUNK, &tmKV, &bar->kv_full[s], h * D + 64 * c, kvrow, planeK);
-          tma_load_3d(v + c * CHUNK, &tmKV, &bar->kv_full[s], h * D + 64 * c, kvrow, planeK + 1);
-        }
+        for (int c = 0; c < C::NCH; ++c)
+          tma_load_3d(sK + s * KV_BYTES + c * CHUNK, &tmKV, &bar->k_full[s], h * D + 64 * c, j * BKV, planeK);
+      }
+    }
+  } else if (warp == 2) {
+    if (lane == 0) {  // ===== TMA producer, V ring =====
+      for (int j = 0; j < nkv; ++j) {
+        const int s = j % VSTAGES;
+        tc::mbar_wait(&bar->v_empty[s], ((j / VSTAGES) & 1) ^ 1);
+        tc::mbar_arrive_expect_tx(&bar->v_full[s], KV_BYTES);
+#pragma unroll
+        for (int c = 0; c < C::NCH; ++c)
+          tma_load_3d(sV + s * KV_BYTES + c * CHUNK, &tmKV, &bar->v_full[s], h * D + 64 * c, j * BKV, planeK + 1);
       }
     }
   } else if (warp == 1) {
@@ -164,7 +183,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       tc::mbar_wait(&bar->q_full, 0);
       auto issue_S = [&](int t, int j) {
         const uint32_t q_addr = tc::smem_u32(sQ + t * Q_BYTES);
-        const uint32_t k_addr = tc::smem_u32(sK + (j % STAGES) * KV_BYTES);
+        const uint32_t k_addr = tc::smem_u32(sK + (j % KSTAGES) * KV_BYTES);
 #pragma unroll
         for (int k = 0; k < D / 16; ++k) {
           const uint32_t off = (k >> 2) * CHUNK + (k & 3) * 32;
@@ -174,29 +193,38 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         tc::mma_commit(&bar->s_full[t]);
       };
       auto issue_PV = [&](int t, int j) {
+        TRACE(0, t, j);  // MMA warp starts waiting for P_t(j)
         tc::mbar_wait(&bar->p_full[t], j & 1);
+        TRACE(1, t, j);  // P_t(j) ready
         tc::tc_fence_after();
-        const uint32_t v_addr = tc::smem_u32(sV + (j % STAGES) * KV_BYTES);
+        const uint32_t v_addr = tc::smem_u32(sV + (j % VSTAGES) * KV_BYTES);
 #pragma unroll
         for (int k = 0; k < BKV / 16; ++k)
           tc::mma_bf16_ts(tmem + t * TS + 128, tmem + t * TS + k * 8,
                           tc::sdesc_sw128(v_addr + k * 2048, CHUNK, 1024), idO, (j | k) != 0);
       };
-      tc::mbar_wait(&bar->kv_full[0], 0);
+      tc::mbar_wait(&bar->k_full[0], 0);
       tc::tc_fence_after();
       for (int t = 0; t < ntiles; ++t) issue_S(t, 0);
+      tc::mma_commit(&bar->k_empty[0]);
       for (int j = 0; j < nkv; ++j) {
         const bool more = j + 1 < nkv;
-        if (more) {
-          tc::mbar_wait(&bar->kv_full[(j + 1) % STAGES], ((j + 1) / STAGES) & 1);
-          tc::tc_fence_after();
-        }
+        tc::mbar_wait(&bar->v_full[j % VSTAGES], (j / VSTAGES) & 1);
+        tc::tc_fence_after();
         for (int t = 0; t < ntiles; ++t) {
           issue_PV(t, j);
-          if (more) issue_S(t, j + 1);
-          else tc::mma_commit(&bar->o_done[t]);
+          if (more) {
+            if (t == 0) {
+              tc::mbar_wait(&bar->k_full[(j + 1) % KSTAGES], ((j + 1) / KSTAGES) & 1);
+              tc::tc_fence_after();
+            }
+            issue_S(t, j + 1);
+          } else {
+            tc::mma_commit(&bar->o_done[t]);
+          }
         }
-        tc::mma_commit(&bar->kv_empty[j % STAGES]);
+        tc::mma_commit(&bar->v_empty[j % VSTAGES]);
+        if (more) tc::mma_commit(&bar->k_empty[(j + 1) % KSTAGES]);
       }
     }
   } else if (warp >= 4) {  // ===== softmax / correction / epilogue, tile t =====
@@ -208,7 +236,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       const uint32_t tS = tmem + t * TS + lane_off, tO = tS + 128;
       float m = -INFINITY, l = 0.f;
       for (int j = 0; j < nkv; ++j) {
+        if (lane == 0 && quad == 0) TRACE(2, t, j);  // softmax starts waiting for S_t(j)
         tc::mbar_wait(&bar->s_full[t], j & 1);
+        if (lane == 0 && quad == 0) TRACE(3, t, j);  // S_t(j) seen
         tc::tc_fence_after();
         uint32_t r[128];
         tc::tmem_ld32(tS + 0, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
@@ -271,6 +301,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         tc::tc_fence_before();
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(&bar->p_full[t]);
+        if (lane == 0 && quad == 0) TRACE(4, t, j);  // softmax done
       }
       // epilogue: O / l -> bf16 -> global
       tc::mbar_wait(&bar->o_done[t], 0);
@@ -300,6 +331,15 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   tc::tc_fence_before();
   __syncthreads();
   if (warp == 1) tc::tmem_dealloc<512>(tmem);
+#ifdef IG_ATTN_TRACE
+  if (threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) {
+    __threadfence();
+    for (int j = 0; j < 40 && j < nkv; ++j)
+      for (int t = 0; t < 2; ++t)
+        printf("TR %d %d %lld %lld %lld %lld %lld\n", t, j, g_trace[0][t][j], g_trace[1][t][j], g_trace[2][t][j],
+               g_trace[3][t][j], g_trace[4][t][j]);
+  }
+#endif
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 g_enc = nullptr;

@@ -14,8 +14,11 @@ ap.add_argument("--iters", type=int, default=10)
 args = ap.parse_args()
 res = {}
 def timeit(fn, iters):
-    for _ in range(2): fn()
-    torch.cuda.synchronize()
+    import time
+    t0 = time.time()
+    while time.time() - t0 < float(os.environ.get("KB_WARM", "1.0")):  # ramp the SM clock up from idle
+        fn()
+        torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
     e0.record()
     for _ in range(iters): fn()
@@ -44,8 +47,8 @@ if "attn" in args.which:
     segs, s = [], 0
     for i, q in enumerate(qlens):
         segs.append((s, q, i // 2)); s += q
-    os.environ["IG_OP_REPEAT"] = "20"
-    ms = timeit(lambda: ig.ig_op_attention(ig.IG_BF16, Q.data_ptr(), H, O.data_ptr(), H, kv.data_ptr(), segs, L, heads, dh, 0), args.iters) / 20
-    os.environ.pop("IG_OP_REPEAT")
+    rep = int(os.environ.get("IG_OP_REPEAT", "20"))
+    os.environ["IG_OP_REPEAT"] = str(rep)
+    ms = timeit(lambda: ig.ig_op_attention(ig.IG_BF16, Q.data_ptr(), H, O.data_ptr(), H, kv.data_ptr(), segs, L, heads, dh, 0), args.iters) / rep
     res["attn"] = {"M": M, "ms": ms, "tflops": 4 * M * L * H / ms / 1e9}
 print(json.dumps(res))
