@@ -338,6 +338,58 @@ def edit_step(d, W, latent, mask, kv_cache_step, sigma, sigma_next, txt, cond_ve
     return out
 
 
+def edit_step_planned(d, W, latent, mask, kv_cache_step, tlatent, k, sigma, sigma_next, txt, cond_vec):
+    """Algorithm 1 plan under the K/V variant (C-AMB 23): blocks [0, k) use no
+    cached activations ("computes all tokens — both masked and unmasked — without
+    distinguishing between them"), blocks [k, N) use the cache.  Under K/V caching
+    the dense blocks must form a prefix (a cached block does not produce the unmasked rows'
+    hidden states), and the unmasked image tokens enter the prefix from the TEMPLATE's input
+    latent at this step (`tlatent`), the trajectory the cache was recorded on.  After block
+    k-1 the unmasked rows are dropped; their K/V come from the cache from block k on."""
+    latent = np.asarray(latent, np.float64)
+    idx_m, idx_u, n_m = index_build(mask)
+    if n_m == 0:
+        return latent.copy()
+    if k <= 0 or len(idx_u) == 0:
+        return edit_step(d, W, latent, mask, kv_cache_step, sigma, sigma_next, txt, cond_vec)
+    k = min(k, d.n_blocks)
+    vec = conditioning(W, sigma, np.asarray(cond_vec, np.float64))
+    full = latent.copy()
+    full[idx_u] = np.asarray(tlatent, np.float64)[idx_u]
+    all_idx = np.arange(d.L_img)
+    none = np.zeros(0, np.int64)
+    x_img = img_in(d, W, full, all_idx)
+    x_txt = np.asarray(txt, np.float64).copy()
+    x = None
+    for b in range(d.n_blocks):
+        dense = b < k
+        if dense:  # the all-tokens block = the masked block with every token masked
+            if b < d.n_double:
+                x_txt, x_img = double_block_masked(d, W, b, x_txt, x_img, vec, all_idx, none, None)
+            else:
+                if x is None:
+                    x = np.concatenate([x_txt, x_img])
+                x = single_block_masked(d, W, b - d.n_double, x, vec, all_idx, none, None)
+            if b == k - 1:  # switch: keep only the masked image rows
+                if x is None:
+                    x_img = x_img[idx_m]
+                else:
+                    x = np.concatenate([x[:d.txt_len], x[d.txt_len:][idx_m]])
+        else:
+            if b < d.n_double:
+                x_txt, x_img = double_block_masked(d, W, b, x_txt, x_img, vec, idx_m, idx_u, kv_cache_step[b])
+            else:
+                if x is None:
+                    x = np.concatenate([x_txt, x_img])
+                x = single_block_masked(d, W, b - d.n_double, x, vec, idx_m, idx_u, kv_cache_step[b])
+    if x is None:
+        x = np.concatenate([x_txt, x_img])
+    v = final_velocity(d, W, x[d.txt_len:], vec)
+    out = latent.copy()
+    out[idx_m] = latent[idx_m] + (float(sigma_next) - float(sigma)) * v
+    return out
+
+
 # --------------------------------------------------------------------------------------
 # Dense step (independent code path: all L tokens, no index lists, no cache) + recording
 # --------------------------------------------------------------------------------------

@@ -351,3 +351,41 @@ def test_fp8_roundtrip_error_bound_and_scale_invariance():
     amax = np.abs(kv.reshape(2, 64, 2, 128)).max(-1)
     ramax = np.abs(r.reshape(2, 64, 2, 128)).max(-1)
     assert np.allclose(ramax, amax, rtol=2 ** -8)
+
+
+
+# ---------------------------------------------------------------- Algorithm 1 plan (N1)
+def test_planned_step_k0_is_edit_step_and_kN_is_dense(small_model):
+    d, W = small_model
+    lat, txt, cond = _inputs(d, 11)
+    tl, _, _ = _inputs(d, 12)
+    mask = np.zeros(d.L_img, np.uint8)
+    mask[5:40] = 1
+    _, kv = oracle.dense_step(d, W, tl, 0.9, 0.8, txt, cond, record=True)
+    a = oracle.edit_step(d, W, lat, mask, kv, 0.9, 0.8, txt, cond)
+    b = oracle.edit_step_planned(d, W, lat, mask, kv, tl, 0, 0.9, 0.8, txt, cond)
+    assert np.array_equal(a, b)
+    # all blocks dense: the masked rows equal a dense step on [request masked | template unmasked]
+    full = lat.copy()
+    full[mask == 0] = tl[mask == 0]
+    dn, _ = oracle.dense_step(d, W, full, 0.9, 0.8, txt, cond)
+    c = oracle.edit_step_planned(d, W, lat, mask, kv, tl, d.n_blocks, 0.9, 0.8, txt, cond)
+    idx = mask != 0
+    assert np.max(np.abs(c[idx] - dn[idx])) <= 1e-12 * np.abs(dn).max()
+    assert np.array_equal(c[~idx], lat[~idx])
+
+
+@pytest.mark.parametrize("k", [1, 2])
+def test_planned_step_exact_with_same_trajectory_cache(small_model, k):
+    # cache recorded on the same combined input -> every prefix length gives the dense rows
+    d, W = small_model
+    lat, txt, cond = _inputs(d, 13)
+    tl, _, _ = _inputs(d, 14)
+    mask = np.zeros(d.L_img, np.uint8)
+    mask[20:50] = 1
+    full = lat.copy()
+    full[mask == 0] = tl[mask == 0]
+    dn, kv = oracle.dense_step(d, W, full, 0.7, 0.5, txt, cond, record=True)
+    c = oracle.edit_step_planned(d, W, lat, mask, kv, tl, k, 0.7, 0.5, txt, cond)
+    idx = mask != 0
+    assert np.max(np.abs(c[idx] - dn[idx])) <= 1e-12 * np.abs(dn).max()
