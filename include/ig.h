@@ -111,7 +111,8 @@ typedef enum { IG_CACHE_HOST = 0, IG_CACHE_DEVICE = 1 } ig_cache_tier;
  * by attention (post-bias, post-RMSNorm, post-RoPE; C-AMB 2), layout
  * [n_steps][n_blocks][2 (K,V)][L_img][H], dtype = desc.dtype, in pinned host memory
  * (IG_CACHE_HOST, "host memory ... for cached activations") or in HBM
- * (IG_CACHE_DEVICE).  Bytes = n_steps*n_blocks*2*L_img*H*sizeof(dtype): twice the
+ * (IG_CACHE_DEVICE), followed by the template's input latent of every step
+ * [n_steps][L_img][lat_ch] fp32 (used by the Algorithm-1 dense prefix, ig_set_plan).  Bytes = n_steps*n_blocks*2*L_img*H*sizeof(dtype): twice the
  * Y-cache size ("doubles the sizes of the cached activations"). */
 ig_status ig_cache_create(ig_ctx* ctx, int n_steps, int tier, ig_cache** out);
 
@@ -132,8 +133,10 @@ ig_status ig_cache_clone(ig_ctx* ctx, const ig_cache* src, int tier, ig_cache** 
 
 /* Write a whole cache from caller K/V in the compute dtype (dev or host pointer,
  * [n_steps][n_blocks][2][L_img][H]); FP8 caches are quantized on the device (per (token, head)
- * scale = amax/448, e4m3 round-to-nearest-even, saturating).  Synchronous on `stream`. */
-ig_status ig_cache_write(ig_ctx* ctx, ig_cache* cache, const void* kv, void* stream);
+ * scale = amax/448, e4m3 round-to-nearest-even, saturating).  latents (optional, fp32
+ * [n_steps][L_img][lat_ch]): the template's input latent of every step (Algorithm-1 dense
+ * prefix).  Synchronous on `stream`. */
+ig_status ig_cache_write(ig_ctx* ctx, ig_cache* cache, const void* kv, const float* latents, void* stream);
 
 /* Raw storage of a cache: host or device pointer (per tier) and its size in bytes, for
  * test I/O and for filling a synthetic cache.  The pointer stays owned by the cache. */
@@ -183,6 +186,20 @@ ig_status ig_edit_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, void* stream
 ig_status ig_prefetch_layer(ig_ctx* ctx, const ig_edit_req* req, int layer);
 
 const char* ig_last_error(void);
+
+/* Algorithm 1 block plan ("bubble-free pipeline"): the first k blocks of
+ * a step run without cached activations over ALL tokens of each cache-using request (the
+ * unmasked image tokens entering from the template's input latent of that step, recorded in
+ * the cache), the remaining blocks use the cache (C-AMB 23: dense blocks must form a prefix
+ * under K/V caching).  mode 0: k = 0 (always cache); mode 1: fixed k; mode 2: k chosen per
+ * step by minimising the two-lane pipeline latency of the batch under the linear latency
+ * models comp = comp_s_per_flop * FLOPs + comp_s and load = load_s_per_byte * bytes + load_s
+ * (P:701-726), with the ring depth as the copy lane's look-ahead.  Use a prefetch_depth at
+ * least as large as the expected prefix. */
+ig_status ig_set_plan(ig_ctx* ctx, int mode, int k, double comp_s_per_flop, double comp_s,
+                      double load_s_per_byte, double load_s);
+/* Prefix length chosen by the last ig_edit_step. */
+int ig_last_plan(const ig_ctx* ctx);
 
 /* Counters of the last ig_edit_step / ig_cache_template call on this ctx. */
 typedef struct {

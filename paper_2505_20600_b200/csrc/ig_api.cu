@@ -91,7 +91,7 @@ struct ModT {
   long long off;  // float offset inside one request's modulation row
 };
 constexpr int NSTAGE = 4;
-constexpr int MAXR = 8;  // max ring depth R = D + 1
+constexpr int MAXR = 32;  // max ring depth R = D + 1
 }  // namespace
 
 struct ig_mask {
@@ -105,6 +105,8 @@ struct ig_cache {
   int n_steps = 0, tier = 0;
   int fp8 = 0;              // 1: e4m3 data [steps][blocks][2][L_img][H] + fp32 scales [..][heads]
   size_t scale_off = 0;     // byte offset of the scale region (fp8 only)
+  size_t lat_off = 0;       // template input latent per step [steps][L_img][C] fp32 (Algorithm-1
+                            // dense prefix: unmasked rows enter from the template's trajectory)
   void* ptr = nullptr;     // pinned host (mapped) or device
   void* dptr = nullptr;    // device-visible pointer (== ptr with UVA)
   size_t bytes = 0;
@@ -167,6 +169,9 @@ struct ig_ctx {
   std::vector<size_t> b_size;
   ig_stats stats{};
   std::vector<ig_cache*> zombies;
+  // Algorithm-1 block plan (ig_set_plan): 0 off, 1 forced dense-prefix length, 2 model
+  int plan_mode = 0, plan_k = 0, last_plan_k = 0;
+  double pm_cs = 0, pm_cb = 0, pm_ls = 0, pm_lb = 0;  // s/FLOP, s, s/byte, s
   // live profiling (ig_profile_enable)
   bool prof = false;
   struct ProfRec { int kind; cudaEvent_t a, b; double flops, bytes; int M, N, K, epi; };
@@ -417,7 +422,7 @@ extern "C" ig_status ig_ctx_create(const ig_model_desc* desc, const void* const*
   okm &= dmalloc(&ctx->Ain, Mx * C * es);
   okm &= dmalloc((void**)&ctx->ri, Mx * sizeof(RowInfo));
   ctx->buf_elems = 2LL * ctx->L * H;
-  ctx->slot_stride = ctx->buf_elems * ctx->R;
+  ctx->slot_stride = ctx->buf_elems * (ctx->R + 1);  // R ring buffers + 1 for dense-prefix blocks
   okm &= dmalloc(&ctx->kv_arena, (size_t)(B * ctx->slot_stride * es));
   if (!okm) { ig_ctx_destroy(ctx); return set_err(IG_ENOMEM, "workspace allocation failed"); }
   cudaMemset(ctx->kv_arena, 0, (size_t)(B * ctx->slot_stride * es));
@@ -465,7 +470,7 @@ extern "C" ig_status ig_ctx_create(const ig_model_desc* desc, const void* const*
     if (!okm) { ig_ctx_destroy(ctx); return set_err(IG_ENOMEM, "fp8 staging allocation failed"); }
   }
   // per-step descriptor staging: ReqDev[B] + AttnSeg[2B] + 2 x KvGatherReq[nb * B]
-  ctx->stage_bytes = B * sizeof(ReqDev) + 2 * B * sizeof(AttnSeg) + 2 * (size_t)ctx->nb * B * sizeof(KvGatherReq) + 1024;
+  ctx->stage_bytes = B * sizeof(ReqDev) + 5 * B * sizeof(AttnSeg) + 2 * (size_t)ctx->nb * B * sizeof(KvGatherReq) + 1024;
   for (int i = 0; i < NSTAGE; ++i) {
     if (cudaHostAlloc((void**)&ctx->h_stage[i], ctx->stage_bytes, cudaHostAllocDefault) != cudaSuccess ||
         cudaMalloc((void**)&ctx->d_stage[i], ctx->stage_bytes) != cudaSuccess) {
@@ -622,9 +627,18 @@ static ig_status get_ones_mask(ig_ctx* ctx, ig_mask** out) {
 // ----------------------------------------------------------------------------------------
 // caches
 // ----------------------------------------------------------------------------------------
-static size_t cache_bytes(const ig_ctx* ctx, int n_steps, int fp8 = 0) {
+static size_t cache_kv_bytes(const ig_ctx* ctx, int n_steps, int fp8) {
   if (fp8) return (size_t)n_steps * ctx->nb * 2 * ctx->Limg * ((size_t)ctx->H + 4 * ctx->d.heads);
   return (size_t)n_steps * ctx->nb * 2 * ctx->Limg * ctx->H * ctx->esz;
+}
+static size_t cache_bytes(const ig_ctx* ctx, int n_steps, int fp8 = 0) {
+  return cache_kv_bytes(ctx, n_steps, fp8) + (size_t)n_steps * ctx->Limg * ctx->C * 4;
+}
+static float* cache_latent(const ig_ctx* ctx, const ig_cache* c, int step) {
+  return (float*)((char*)c->ptr + c->lat_off + (size_t)step * ctx->Limg * ctx->C * 4);
+}
+static const float* cache_latent_dev(const ig_ctx* ctx, const ig_cache* c, int step) {
+  return (const float*)((const char*)c->dptr + ((char*)cache_latent(ctx, c, step) - (char*)c->ptr));
 }
 // data plane (which = 0 K, 1 V) of (step, block) and its scale plane (fp8 caches)
 static char* cache_plane(const ig_ctx* ctx, const ig_cache* c, int step, int b, int which) {
@@ -656,6 +670,7 @@ extern "C" ig_status ig_cache_create(ig_ctx* ctx, int n_steps, int tier, ig_cach
   c->fp8 = ctx->o.cache_fp8;
   c->bytes = cache_bytes(ctx, n_steps, c->fp8);
   if (c->fp8) c->scale_off = (size_t)n_steps * ctx->nb * 2 * ctx->Limg * ctx->H;
+  c->lat_off = cache_kv_bytes(ctx, n_steps, c->fp8);
   cudaError_t e;
   if (tier == IG_CACHE_HOST) {
     e = cudaHostAlloc(&c->ptr, c->bytes, cudaHostAllocMapped | cudaHostAllocPortable);
@@ -705,13 +720,16 @@ extern "C" ig_status ig_cache_clone(ig_ctx* ctx, const ig_cache* src, int tier, 
         }
       }
     if (tmp) cudaFree(tmp);
+    if (e == cudaSuccess)
+      e = cudaMemcpy(cache_latent(ctx, c, 0), cache_latent(ctx, src, 0), (size_t)src->n_steps * ctx->Limg * ctx->C * 4,
+                     cudaMemcpyDefault);
   }
   if (e != cudaSuccess) { free_cache_now(c); return set_err(IG_ECUDA, "cache clone: %s", cudaGetErrorString(e)); }
   *out = c;
   return IG_OK;
 }
 
-extern "C" ig_status ig_cache_write(ig_ctx* ctx, ig_cache* c, const void* kv, void* stream) {
+extern "C" ig_status ig_cache_write(ig_ctx* ctx, ig_cache* c, const void* kv, const float* latents, void* stream) {
   if (!ctx || !c || !kv) return set_err(IG_EINVAL, "NULL argument");
   if (!desc_equal(c->desc, ctx->d)) return set_err(IG_ECACHE_INCOMPAT, "cache built for another model");
   if (c->fp8 && !ctx->q8rec) return set_err(IG_EUNSUPPORTED, "fp8 cache needs a ctx created with cache_fp8");
@@ -733,6 +751,9 @@ extern "C" ig_status ig_cache_write(ig_ctx* ctx, ig_cache* c, const void* kv, vo
         CUDA_TRY(cudaMemcpyAsync(cache_plane(ctx, c, s, b, 0), src, 2 * pl * ctx->esz, cudaMemcpyDefault, st));
       }
     }
+  if (latents)
+    CUDA_TRY(cudaMemcpyAsync(cache_latent(ctx, c, 0), latents, (size_t)c->n_steps * ctx->Limg * ctx->C * 4,
+                             cudaMemcpyDefault, st));
   CUDA_TRY(cudaStreamSynchronize(st));
   return IG_OK;
 }
@@ -872,6 +893,64 @@ static void issue_copy(ig_ctx* ctx, const std::vector<StepReq>& sr, const KvGath
   cudaEventRecord(ctx->ev_copy[buf], ctx->copy_st);
 }
 
+// ---- Algorithm 1 planner on B200 ----------------------------------------------
+// Per-block latencies of the batch from the linear models: C_w = comp(masked-rows
+// FLOPs), C_w/o = comp(all-rows FLOPs), L = load(cached bytes).  Under the K/V variant the
+// dense blocks form a prefix (C-AMB 23), so the exact optimum is a scan over the prefix length
+// k of the two-lane pipeline: the copy lane loads cached blocks in order, at most R ahead of
+// the compute lane (ring depth); the compute lane runs dense blocks, then each cached block
+// once its load landed.  (Algorithm 1's greedy per-block rule, placement.py algorithm1, never
+// picks a dense block when C_w/o > L + C_w, which is the B200 + PCIe regime.)
+static double block_flops_rows(const ig_ctx* ctx, long long rows) {
+  const double H = ctx->H, F = ctx->F;
+  return 2.0 * rows * (3 * H * H + H * H + 2 * H * F) + 4.0 * rows * ctx->L * H;
+}
+
+static int plan_prefix(ig_ctx* ctx, const std::vector<StepReq>& sr) {
+  long long rows_m = 0, rows_all = 0, bytes = 0;
+  for (auto& s : sr) {
+    rows_m += ctx->Lt + s.m->n_m;
+    rows_all += ctx->Lt + (s.use_cache ? ctx->Limg : s.m->n_m);
+    if (s.use_cache) {
+      const int n_u = ctx->Limg - s.m->n_m;
+      bytes += s.r->cache->fp8 ? 2LL * n_u * (ctx->H + 4 * ctx->d.heads)
+                               : 2LL * n_u * ctx->H * (long long)ctx->esz;
+    }
+  }
+  const double cw = ctx->pm_cs * block_flops_rows(ctx, rows_m) + ctx->pm_cb;
+  const double cwo = ctx->pm_cs * block_flops_rows(ctx, rows_all) + ctx->pm_cb;
+  const double lt = ctx->pm_ls * (double)bytes + ctx->pm_lb;
+  const int N = ctx->nb, R = ctx->R;
+  int best_k = 0;
+  double best = 1e300;
+  std::vector<double> comp_end(N + 1);
+  for (int k = 0; k <= N; ++k) {
+    double comp = 0, load = 0;
+    for (int b = 0; b < N; ++b) {
+      if (b < k) { comp += cwo; comp_end[b] = comp; continue; }
+      // ring slot of block b is free once cached block b - R finished computing
+      const double slot_free = (b - R >= k) ? comp_end[b - R] : 0.0;
+      load = std::max(load, slot_free) + lt;
+      comp = std::max(comp, load) + cw;
+      comp_end[b] = comp;
+    }
+    if (comp < best - 1e-12) { best = comp; best_k = k; }
+  }
+  return best_k;
+}
+
+extern "C" ig_status ig_set_plan(ig_ctx* ctx, int mode, int k, double comp_s_per_flop, double comp_s,
+                                 double load_s_per_byte, double load_s) {
+  if (!ctx) return set_err(IG_EINVAL, "ctx is NULL");
+  if (mode < 0 || mode > 2 || k < 0) return set_err(IG_EINVAL, "bad plan mode/k");
+  ctx->plan_mode = mode;
+  ctx->plan_k = k;
+  ctx->pm_cs = comp_s_per_flop; ctx->pm_cb = comp_s; ctx->pm_ls = load_s_per_byte; ctx->pm_lb = load_s;
+  return IG_OK;
+}
+
+extern "C" int ig_last_plan(const ig_ctx* ctx) { return ctx ? ctx->last_plan_k : -1; }
+
 // Optional restriction of a step to blocks [b0, b1) on caller-given residual rows (the
 // teacher-forced debug hook); defaults run the whole step.
 struct StepRange {
@@ -923,7 +1002,17 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
     any_cache |= s.use_cache;
     if (s.use_cache) max_nu = std::max(max_nu, ctx->Limg - s.m->n_m);
   }
-  if (M > ctx->o.max_rows) return set_err(IG_ENOMEM, "step needs %d rows > max_rows %d", M, ctx->o.max_rows);
+  // ---- Algorithm-1 block plan (C-AMB 23): a dense prefix of k blocks ----
+  int kplan = 0;
+  if (any_cache && !record && b0 == 0 && b1 == nb) {
+    if (ctx->plan_mode == 1) kplan = std::min(ctx->plan_k, nb);
+    else if (ctx->plan_mode == 2) kplan = plan_prefix(ctx, sr);
+  }
+  ctx->last_plan_k = kplan;
+  int M_full = M;
+  if (kplan > 0)
+    for (auto& s : sr) if (s.use_cache) M_full += ctx->Limg - s.m->n_m;
+  if (M_full > ctx->o.max_rows) return set_err(IG_ENOMEM, "step needs %d rows > max_rows %d", M_full, ctx->o.max_rows);
   const int M_img = M - M_txt;
   ctx->stats.rows = M;
 
@@ -934,13 +1023,16 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
   char* hs = ctx->h_stage[si];
   char* ds = ctx->d_stage[si];
   ReqDev* hreq = (ReqDev*)hs;
+  // attention segments: [0, 2B) the masked-rows step, [2B, 5B) the dense prefix (+ unmasked)
   AttnSeg* hseg = (AttnSeg*)(hs + ctx->o.max_batch * sizeof(ReqDev));
-  KvGatherReq* hkvg = (KvGatherReq*)((char*)hseg + 2 * ctx->o.max_batch * sizeof(AttnSeg));
+  AttnSeg* hsegf = hseg + 2 * ctx->o.max_batch;
+  KvGatherReq* hkvg = (KvGatherReq*)((char*)hseg + 5 * ctx->o.max_batch * sizeof(AttnSeg));
   ReqDev* dreq = (ReqDev*)ds;
   AttnSeg* dseg = (AttnSeg*)(ds + ctx->o.max_batch * sizeof(ReqDev));
-  KvGatherReq* dkvg = (KvGatherReq*)((char*)dseg + 2 * ctx->o.max_batch * sizeof(AttnSeg));
-  int nseg = 0, max_q = 0;
-  int img_row = M_txt;
+  AttnSeg* dsegf = dseg + 2 * ctx->o.max_batch;
+  KvGatherReq* dkvg = (KvGatherReq*)((char*)dseg + 5 * ctx->o.max_batch * sizeof(AttnSeg));
+  int nseg = 0, max_q = 0, nsegf = 0, max_qf = 0;
+  int img_row = M_txt, uimg_row = M;
   for (int q = 0; q < na; ++q) {
     const ig_edit_req* r = sr[q].r;
     ReqDev& d = hreq[q];
@@ -956,11 +1048,21 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
     d.sigma = r->sigma;
     d.dsig = r->sigma_next - r->sigma;
     d.has_cache = sr[q].use_cache;
+    d.n_ui = (kplan > 0 && sr[q].use_cache) ? ctx->Limg - d.n_m : 0;
+    d.uimg_row0 = uimg_row;
+    d.tlatent = sr[q].use_cache ? cache_latent_dev(ctx, r->cache, r->step) : nullptr;
     const long long kvb = (long long)r->slot * ctx->slot_stride;
     if (Lt > 0) { hseg[nseg++] = AttnSeg{q * Lt, Lt, kvb}; max_q = std::max(max_q, Lt); }
     hseg[nseg++] = AttnSeg{img_row, d.n_m, kvb};
     max_q = std::max(max_q, d.n_m);
+    if (kplan > 0) {
+      if (Lt > 0) hsegf[nsegf++] = AttnSeg{q * Lt, Lt, kvb};
+      hsegf[nsegf++] = AttnSeg{img_row, d.n_m, kvb};
+      if (d.n_ui > 0) hsegf[nsegf++] = AttnSeg{uimg_row, d.n_ui, kvb};
+      max_qf = std::max(max_qf, std::max(Lt, std::max(d.n_m, d.n_ui)));
+    }
     img_row += d.n_m;
+    uimg_row += d.n_ui;
   }
   // copy-lane plan and per-(block, request) gather descriptors (see issue_copy)
   CopyPlan plan;
@@ -1025,8 +1127,9 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
   }
   for (auto& s : sr) if (s.use_cache) { s.r->cache->pins.fetch_add(1); }
 
-  // ---- prefetch the first R blocks (copy lane) ----
-  for (int b = b0; b < std::min(b0 + R, b1); ++b) issue_copy(ctx, sr, dkvg, dkvq, b, plan);
+  // ---- prefetch the first R cached blocks (copy lane); dense-prefix blocks need no cache ----
+  const int bc0 = std::max(b0, kplan);
+  for (int b = bc0; b < std::min(bc0 + R, b1); ++b) issue_copy(ctx, sr, dkvg, dkvq, b, plan);
 
   T* h = (T*)ctx->h;
   T* qkv = (T*)ctx->qkv;
@@ -1037,7 +1140,7 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
   // ---- a2/a4: rows + gather; a3: conditioning ----
   {
     ProfScope ps(ctx, st, IG_K_ROWS, 0.0, (double)M_txt * H * (4 + es) + (double)M_img * C * (4 + es));
-    launch_build_rows<T>(dreq, na, Lt, C, H, M_txt, M, ctx->ri, ctx->X, (T*)ctx->Ain, st);
+    launch_build_rows<T>(dreq, na, Lt, C, H, M_txt, M, ctx->ri, ctx->X, (T*)ctx->Ain, st, M_full);
   }
   {
   ProfScope ps_cond(ctx, st, IG_K_COND, 0.0, (double)ctx->mod_ld * H * es);
@@ -1063,7 +1166,7 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
   } else {  // img_in (+ SD3 pos_embed) into the fp32 residual X
     GemmArgs g{};
     g.A = ctx->Ain; g.lda = C; g.B = ctx->img_in.w; g.ldb = C; g.bias = ctx->img_in.b;
-    g.C = ctx->X + (long long)M_txt * H; g.ldc = H; g.M = M_img; g.N = H; g.K = C;
+    g.C = ctx->X + (long long)M_txt * H; g.ldc = H; g.M = M_full - M_txt; g.N = H; g.K = C;
     g.epi = EPI_POS; g.ri = ctx->ri; g.ri_off = M_txt; g.pos = ctx->pos_embed; g.pos_ld = H;
     gemm(ctx, g, st);
   }
@@ -1133,14 +1236,15 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
     e.head_dim = ctx->d.head_dim; e.grid_w = ctx->d.grid_w; e.qk_norm = ctx->d.qk_norm; e.rope = ctx->d.rope;
     gemm(ctx, g, st);
   };
-  auto attn = [&](int buf) {
+  auto attn = [&](int buf, bool dense) {
     AttnArgs a{};
     a.Q = ctx->Q; a.ldq = H; a.O = cat; a.ldo = ldcat; a.kv_arena = ctx->kv_arena;
-    a.kv_off = (long long)buf * ctx->buf_elems; a.segs = dseg; a.nseg = nseg; a.max_qlen = max_q;
-    a.q_rows = M;
+    a.kv_off = (long long)buf * ctx->buf_elems;
+    a.segs = dense ? dsegf : dseg; a.nseg = dense ? nsegf : nseg; a.max_qlen = dense ? max_qf : max_q;
+    a.q_rows = dense ? M_full : M;
     a.L = ctx->L; a.heads = ctx->d.heads; a.head_dim = ctx->d.head_dim;
     a.scale = 1.0f / sqrtf((float)ctx->d.head_dim);
-    attention(ctx, a, st, 4.0 * (double)M * ctx->L * H);
+    attention(ctx, a, st, 4.0 * (double)(dense ? M_full : M) * ctx->L * H);
   };
   // cache recording (template mode): image-token K/V of ring buffer -> cache[s][b]
   auto record_kv = [&](int b, int buf) {
@@ -1185,26 +1289,32 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
   };
 
   // ---- blocks ----
+  // Dense-prefix blocks (b < kplan) run every row [0, M_full) with their own K/V buffer (index
+  // R, no cache); cached blocks run the masked rows [0, M) with ring buffer b % R.
   for (int b = b0; b < b1; ++b) {
-    const int buf = b % R;
+    const bool dense = b < kplan;
+    const int Mc = dense ? M_full : M;
+    const int buf = dense ? R : b % R;
     if (b < ctx->d.n_double) {
       const StreamW& wi = ctx->dimg[b];
       const StreamW& wt = ctx->dtxt[b];
-      ln_mod(M_txt, M, wi.mod_t, 0, 1);
+      ln_mod(M_txt, Mc, wi.mod_t, 0, 1);
       if (Lt) ln_mod(0, M_txt, wt.mod_t, wt.pre_only ? 1 : 0, wt.pre_only ? 0 : 1);
-      wait_copy(buf);
-      qkv_proj(M_txt, M, wi.qkv.w, wi.qkv.b, wi.qg, wi.kg, buf);
+      if (!dense) wait_copy(buf);
+      qkv_proj(M_txt, Mc, wi.qkv.w, wi.qkv.b, wi.qg, wi.kg, buf);
       if (Lt) qkv_proj(0, M_txt, wt.qkv.w, wt.qkv.b, wt.qg, wt.kg, buf);
-      wait_copy_late(buf);
-      attn(buf);
+      if (!dense) wait_copy_late(buf);
+      attn(buf, dense);
       record_kv(b, buf);
-      cudaEventRecord(ctx->ev_comp[buf], st);
-      if (b + R < b1) issue_copy(ctx, sr, dkvg, dkvq, b + R, plan);
+      if (!dense) {
+        cudaEventRecord(ctx->ev_comp[buf], st);
+        if (b + R < b1) issue_copy(ctx, sr, dkvg, dkvq, b + R, plan);
+      }
       const long long gi = ctx->mods[wi.mod_t].off;
-      gemm_rows(M_txt, M, cat, ldcat, wi.proj.w, wi.proj.b, H, H, ctx->X, H, EPI_GATED_RES, mod + gi + 2 * H, 0);
-      ln_mod(M_txt, M, wi.mod_t, 3, 4);
-      gemm_rows(M_txt, M, h, H, wi.fc1.w, wi.fc1.b, F, H, cat + H, ldcat, EPI_GELU, nullptr, 0);
-      gemm_rows(M_txt, M, cat + H, ldcat, wi.fc2.w, wi.fc2.b, H, F, ctx->X, H, EPI_GATED_RES, mod + gi + 5 * H, 0);
+      gemm_rows(M_txt, Mc, cat, ldcat, wi.proj.w, wi.proj.b, H, H, ctx->X, H, EPI_GATED_RES, mod + gi + 2 * H, 0);
+      ln_mod(M_txt, Mc, wi.mod_t, 3, 4);
+      gemm_rows(M_txt, Mc, h, H, wi.fc1.w, wi.fc1.b, F, H, cat + H, ldcat, EPI_GELU, nullptr, 0);
+      gemm_rows(M_txt, Mc, cat + H, ldcat, wi.fc2.w, wi.fc2.b, H, F, ctx->X, H, EPI_GATED_RES, mod + gi + 5 * H, 0);
       if (Lt && !wt.pre_only) {
         const long long gt = ctx->mods[wt.mod_t].off;
         gemm_rows(0, M_txt, cat, ldcat, wt.proj.w, wt.proj.b, H, H, ctx->X, H, EPI_GATED_RES, mod + gt + 2 * H, 0);
@@ -1214,19 +1324,21 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
       }
     } else {
       const SingleW& ws = ctx->sgl[b - ctx->d.n_double];
-      ln_mod(0, M, ws.mod_t, 0, 1);
+      ln_mod(0, Mc, ws.mod_t, 0, 1);
       const char* w_u = (const char*)ws.lin1.w + 3LL * H * H * es;
       const char* b_u = (const char*)ws.lin1.b + 3LL * H * es;
-      gemm_rows(0, M, h, H, w_u, b_u, F, H, cat + H, ldcat, EPI_GELU, nullptr, 0);
-      wait_copy(buf);
-      qkv_proj(0, M, ws.lin1.w, ws.lin1.b, ws.qg, ws.kg, buf);
-      wait_copy_late(buf);
-      attn(buf);
+      gemm_rows(0, Mc, h, H, w_u, b_u, F, H, cat + H, ldcat, EPI_GELU, nullptr, 0);
+      if (!dense) wait_copy(buf);
+      qkv_proj(0, Mc, ws.lin1.w, ws.lin1.b, ws.qg, ws.kg, buf);
+      if (!dense) wait_copy_late(buf);
+      attn(buf, dense);
       record_kv(b, buf);
-      cudaEventRecord(ctx->ev_comp[buf], st);
-      if (b + R < b1) issue_copy(ctx, sr, dkvg, dkvq, b + R, plan);
+      if (!dense) {
+        cudaEventRecord(ctx->ev_comp[buf], st);
+        if (b + R < b1) issue_copy(ctx, sr, dkvg, dkvq, b + R, plan);
+      }
       const long long gs = ctx->mods[ws.mod_t].off;
-      gemm_rows(0, M, cat, ldcat, ws.lin2.w, ws.lin2.b, H, H + F, ctx->X, H, EPI_GATED_RES, mod + gs + 2 * H, 0);
+      gemm_rows(0, Mc, cat, ldcat, ws.lin2.w, ws.lin2.b, H, H + F, ctx->X, H, EPI_GATED_RES, mod + gs + 2 * H, 0);
     }
   }
   if (rng.X_out) {
@@ -1305,6 +1417,9 @@ extern "C" ig_status ig_cache_template(ig_ctx* ctx, float* latent, const void* t
     ig_edit_req r{};
     r.slot = 0; r.latent = latent; r.mask = ones; r.cache = nullptr; r.step = k;
     r.sigma = sigmas[k]; r.sigma_next = sigmas[k + 1]; r.txt = txt; r.cond_vec = cond_vec;
+    cudaError_t el = cudaMemcpyAsync(cache_latent(ctx, c, k), latent, (size_t)ctx->Limg * ctx->C * 4,
+                                     cudaMemcpyDefault, st);  // the template's input latent of step k
+    if (el != cudaSuccess) { free_cache_now(c); return set_err(IG_ECUDA, "cache_template: %s", cudaGetErrorString(el)); }
     s = step_dispatch(ctx, &r, 1, st, c, k);
     if (s != IG_OK) { free_cache_now(c); return s; }
     total.kernel_launches += ctx->stats.kernel_launches;

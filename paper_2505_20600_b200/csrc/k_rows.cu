@@ -82,10 +82,10 @@ void launch_mask_index(const uint8_t* mask, int L, int32_t* idx_m, int32_t* idx_
 template <typename T>
 __global__ void build_rows_kernel(const ReqDev* __restrict__ reqs, int n, int L_txt, int C,
                                   int H, int M_txt, int M, RowInfo* __restrict__ ri,
-                                  float* __restrict__ X, T* __restrict__ Ain) {
+                                  float* __restrict__ X, T* __restrict__ Ain, int M_full) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  if (warp >= M) return;
+  if (warp >= M_full) return;
   const int r = warp;
   RowInfo info;
   if (r < M_txt) {
@@ -95,6 +95,17 @@ __global__ void build_rows_kernel(const ReqDev* __restrict__ reqs, int n, int L_
     const T* src = reinterpret_cast<const T*>(R.txt) + (long long)t * H;
     float* dst = X + (long long)r * H;
     for (int c = lane; c < H; c += 32) dst[c] = to_f<T>(src[c]);
+  } else if (r >= M) {  // included unmasked rows (dense prefix) from the template latent
+    int q = 0;
+    for (int i = 0; i < n; ++i)
+      if (reqs[i].n_ui > 0 && reqs[i].uimg_row0 <= r) q = i;  // request-major, n <= 16
+    const ReqDev& R = reqs[q];
+    const int j = r - R.uimg_row0;
+    const int tok = R.idx_u[j];
+    info.req = q; info.slot = R.slot; info.kvpos = L_txt + tok; info.tok = tok;
+    const float* src = R.tlatent + (long long)tok * C;
+    T* dst = Ain + (long long)(r - M_txt) * C;
+    for (int c = lane; c < C; c += 32) dst[c] = from_f<T>(src[c]);
   } else {
     int q = 0;
     while (q + 1 < n && reqs[q + 1].img_row0 <= r) ++q;  // n <= max_batch: linear search
@@ -111,14 +122,15 @@ __global__ void build_rows_kernel(const ReqDev* __restrict__ reqs, int n, int L_
 
 template <typename T>
 void launch_build_rows(const ReqDev* reqs, int n, int L_txt, int C, int H, int M_txt, int M,
-                       RowInfo* ri, float* X, T* Ain, cudaStream_t st) {
-  if (M <= 0) return;
+                       RowInfo* ri, float* X, T* Ain, cudaStream_t st, int M_full) {
+  if (M_full < M) M_full = M;
+  if (M_full <= 0) return;
   const int threads = 256;
-  const int blocks = (M * 32 + threads - 1) / threads;
-  build_rows_kernel<T><<<blocks, threads, 0, st>>>(reqs, n, L_txt, C, H, M_txt, M, ri, X, Ain);
+  const int blocks = (M_full * 32 + threads - 1) / threads;
+  build_rows_kernel<T><<<blocks, threads, 0, st>>>(reqs, n, L_txt, C, H, M_txt, M, ri, X, Ain, M_full);
 }
-template void launch_build_rows<float>(const ReqDev*, int, int, int, int, int, int, RowInfo*, float*, float*, cudaStream_t);
-template void launch_build_rows<bf16>(const ReqDev*, int, int, int, int, int, int, RowInfo*, float*, bf16*, cudaStream_t);
+template void launch_build_rows<float>(const ReqDev*, int, int, int, int, int, int, RowInfo*, float*, float*, cudaStream_t, int);
+template void launch_build_rows<bf16>(const ReqDev*, int, int, int, int, int, int, RowInfo*, float*, bf16*, cudaStream_t, int);
 
 // ======================================================================================
 // a6 epilogue: per-head RMSNorm (q, k) + RoPE at the ORIGINAL token position (C-AMB 7),

@@ -20,13 +20,18 @@ struct ReqDev {
   const float* cond;
   float sigma, dsig;                  // dsig = sigma_next - sigma
   int has_cache;
+  int n_ui;                           // unmasked rows included (Algorithm-1 dense prefix)
+  int uimg_row0;                      // packed row of the first included unmasked row
   int pad;
+  const float* tlatent;               // template input latent of this step [L_img, C]
 };
 // Fills row_info[M] and gathers: X[txt rows] = txt (fp32), Ain[img rows - M_txt] = latent
 // rows at idx_m (as T).  M_txt = n * L_txt.
+// Rows [M, M_full) are the included unmasked image rows (dense prefix): latent rows of the
+// template's input latent at idx_u.
 template <typename T>
 void launch_build_rows(const ReqDev* reqs, int n, int L_txt, int C, int H, int M_txt, int M,
-                       RowInfo* row_info, float* X, T* Ain, cudaStream_t st);
+                       RowInfo* row_info, float* X, T* Ain, cudaStream_t st, int M_full = -1);
 
 // ---- a3 conditioning (k_norm.cu) --------------------------------------------------------
 // temb[r][0:256] = [cos(1000 sigma_r f_k) | sin(...)], computed in double, stored as float.

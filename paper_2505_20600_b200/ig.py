@@ -24,7 +24,8 @@ EXPORTS = ["ig_weight_count", "ig_ctx_create", "ig_ctx_destroy", "ig_cache_creat
            "ig_cache_template", "ig_cache_storage", "ig_cache_free", "ig_mask_build",
            "ig_mask_indices", "ig_mask_free", "ig_edit_step", "ig_prefetch_layer",
            "ig_last_error", "ig_last_stats", "ig_op_gemm", "ig_op_gemm_gated", "ig_op_attention", "ig_copy",
-           "ig_profile_enable", "ig_profile_read", "ig_debug_block", "ig_cache_clone", "ig_cache_write"]
+           "ig_profile_enable", "ig_profile_read", "ig_debug_block", "ig_cache_clone", "ig_cache_write",
+           "ig_set_plan", "ig_last_plan"]
 KCLASS = ["gemm", "attn", "lnmod", "qkvpost", "cond", "rows"]
 
 
@@ -96,6 +97,7 @@ def lib():
         L.ig_edit_step.argtypes = [vp, P(ig_edit_req), i, vp]
         L.ig_prefetch_layer.argtypes = [vp, P(ig_edit_req), i]
         L.ig_last_error.restype = ctypes.c_char_p
+        L.ig_last_plan.restype = ctypes.c_int
         L.ig_last_stats.argtypes = [vp, P(ig_stats)]
         L.ig_op_gemm.argtypes = [i, vp, ll, vp, ll, vp, vp, ll, i, i, i, i, i, vp]
         L.ig_op_attention.argtypes = [i, vp, ll, vp, ll, vp, P(ctypes.c_int32), i, i, i, i, vp]
@@ -103,12 +105,15 @@ def lib():
         L.ig_op_gemm_gated.argtypes = [i, vp, ll, vp, ll, vp, vp, ll, vp, i, i, i, vp]
         L.ig_profile_enable.argtypes = [vp, i]
         L.ig_cache_clone.argtypes = [vp, vp, i, P(vp)]
-        L.ig_cache_write.argtypes = [vp, vp, vp, vp]
+        L.ig_cache_write.argtypes = [vp, vp, vp, vp, vp]
+        d_ = ctypes.c_double
+        L.ig_set_plan.argtypes = [vp, i, i, d_, d_, d_, d_]
+        L.ig_last_plan.argtypes = [vp]
         L.ig_debug_block.argtypes = [vp, P(ig_edit_req), i, vp, vp, vp]
         L.ig_profile_read.argtypes = [vp, P(ig_prof_entry)]
         for name in EXPORTS:
             if name not in ("ig_ctx_destroy", "ig_cache_free", "ig_mask_free", "ig_last_error",
-                            "ig_weight_count"):
+                            "ig_weight_count", "ig_last_plan"):
                 getattr(L, name).restype = ctypes.c_int
         _lib = L
     return _lib
@@ -253,5 +258,14 @@ def ig_cache_clone(ctx: int, cache: int, tier: int) -> int:
     return out.value
 
 
-def ig_cache_write(ctx: int, cache: int, kv_ptr: int, stream: int = 0):
-    _check(lib().ig_cache_write(ctx, cache, kv_ptr, stream))
+def ig_cache_write(ctx: int, cache: int, kv_ptr: int, latents_ptr: int = 0, stream: int = 0):
+    _check(lib().ig_cache_write(ctx, cache, kv_ptr, latents_ptr or None, stream))
+
+
+def ig_set_plan(ctx: int, mode: int, k: int = 0, comp_s_per_flop: float = 0.0, comp_s: float = 0.0,
+                load_s_per_byte: float = 0.0, load_s: float = 0.0):
+    _check(lib().ig_set_plan(ctx, mode, k, comp_s_per_flop, comp_s, load_s_per_byte, load_s))
+
+
+def ig_last_plan(ctx: int) -> int:
+    return lib().ig_last_plan(ctx)

@@ -69,6 +69,7 @@ class Request:
 
 def cache_to_numpy(cache, d, n_steps, dtype):
     ptr, nbytes, tier = ig.ig_cache_storage(cache)
+    nbytes = n_steps * d.n_blocks * 2 * d.L_img * d.hidden * (4 if dtype == ig.IG_F32 else 2)  # K/V region
     shape = (n_steps, d.n_blocks, 2, d.L_img, d.hidden)
     assert tier == ig.IG_CACHE_HOST, 'host-tier readback only'
     import ctypes
@@ -80,10 +81,9 @@ def cache_to_numpy(cache, d, n_steps, dtype):
     return u16.view(np.float32).reshape(shape).astype(np.float64)
 
 
-def fill_cache(cache, kv: torch.Tensor):
-    """Copy a synthetic cache tensor [steps, blocks, 2, L_img, H] into library storage."""
-    ptr, nbytes, tier = ig.ig_cache_storage(cache)
-    src = kv.contiguous().cpu()
-    assert src.numel() * src.element_size() == nbytes
-    import ctypes
-    ctypes.memmove(ptr, src.data_ptr(), nbytes)
+def fill_cache(m, cache, kv: torch.Tensor, latents: torch.Tensor = None):
+    """Write a synthetic cache [steps, blocks, 2, L_img, H] (+ optional template latents
+    [steps, L_img, C]) through ig_cache_write."""
+    src = kv.contiguous().cuda()
+    lat = latents.contiguous().cuda().float() if latents is not None else None
+    ig.ig_cache_write(m.ctx, cache, src.data_ptr(), lat.data_ptr() if lat is not None else 0)

@@ -125,7 +125,7 @@ def test_tiny_config_end_to_end(dtype):
     # edit steps with a synthetic cache (same bytes for both sides)
     kv = synth.make_cache_kv(d, 0, 2, dtype=torch.float32 if dtype == ig.IG_F32 else torch.bfloat16)
     syn = ig.ig_cache_create(m.ctx, 2, ig.IG_CACHE_HOST)
-    fill_cache(syn, kv)
+    fill_cache(m, syn, kv)
     kvh = kv.double().numpy()
     _run_edit(m, [rq], syn, 2, sig)
     x = lat0
@@ -159,7 +159,7 @@ def test_flux_small_batch_end_to_end(dtype, copy_mode):
     tdt = torch.float32 if dtype == ig.IG_F32 else torch.bfloat16
     kv = synth.make_cache_kv(d, 3, 2, dtype=tdt)
     cache = ig.ig_cache_create(m.ctx, 2, ig.IG_CACHE_HOST)
-    fill_cache(cache, kv)
+    fill_cache(m, cache, kv)
     kvh = kv.double().numpy()
     _run_edit(m, reqs, cache, 2, sig)
     for r in reqs:
@@ -236,7 +236,7 @@ def test_sd3_and_double_structures_end_to_end(dtype, model):
     tdt = torch.float32 if dtype == ig.IG_F32 else torch.bfloat16
     kv = synth.make_cache_kv(d, 5, 2, dtype=tdt)
     cache = ig.ig_cache_create(m.ctx, 2, ig.IG_CACHE_HOST)
-    fill_cache(cache, kv)
+    fill_cache(m, cache, kv)
     kvh = kv.double().numpy()
     _run_edit(m, reqs, cache, 2, sig)
     for r in reqs:
@@ -287,4 +287,58 @@ def test_fp8_cache_end_to_end(tier):
     ig.ig_cache_free(cache)
     for r in reqs:
         r.free()
+    m.close()
+
+
+
+@pytest.mark.parametrize("k", [1, 2, 4])
+def test_algorithm1_dense_prefix_end_to_end(k):
+    """Algorithm-1 plan (N1) executed: the first k blocks run every token of each request (the
+    unmasked ones from the template's input latent of the step), the rest use the cache; vs
+    the oracle's planned step (C-AMB 23).  Batch of 3 (one all-ones request), 2 steps."""
+    d = synth.FLUX_SMALL
+    sig = [1.0, 0.7, 0.4]
+    m = Model(d, ig.IG_BF16, opts=ig.ig_ctx_opts(4, 0, 4, 1, 0, 0))
+    ig.ig_set_plan(m.ctx, 1, k)
+    W = m.host_weights()
+    rng = np.random.default_rng(4)
+    masks = [synth.blob_mask_count(d, 80, rng), synth.rect_mask_count(d, 25, rng), np.ones(d.L_img, np.uint8)]
+    reqs = [Request(m, 70 + i, mk) for i, mk in enumerate(masks)]
+    kv = synth.make_cache_kv(d, 4, 2, dtype=torch.bfloat16)
+    tlat = torch.stack([synth.make_latent(d, 900 + s) for s in range(2)])
+    cache = ig.ig_cache_create(m.ctx, 2, ig.IG_CACHE_HOST)
+    fill_cache(m, cache, kv, tlat)
+    kvh, tlh = kv.double().numpy(), tlat.double().numpy()
+    _run_edit(m, reqs, cache, 2, sig)
+    assert ig.ig_last_plan(m.ctx) == min(k, d.n_blocks)
+    for r in reqs:
+        lat0, txt, cond = r.host_inputs()
+        x = lat0
+        for s in range(2):
+            x = oracle.edit_step_planned(d, W, x, r.mask_np, kvh[s], tlh[s], k, sig[s], sig[s + 1], txt, cond)
+        got = r.latent.double().cpu().numpy()
+        ok, worst = ctol(got, x, 2e-2)
+        assert ok, worst
+        assert np.array_equal(got[r.mask_np == 0], lat0[r.mask_np == 0])
+    ig.ig_cache_free(cache)
+    for r in reqs:
+        r.free()
+    m.close()
+
+
+def test_algorithm1_model_plan_extremes():
+    d = synth.FLUX_SMALL
+    m = Model(d, ig.IG_BF16, opts=ig.ig_ctx_opts(2, 0, 4, 1, 0, 0))
+    r = Request(m, 80, synth.rect_mask_count(d, 40, np.random.default_rng(0)))
+    kv = synth.make_cache_kv(d, 4, 1, dtype=torch.bfloat16)
+    cache = ig.ig_cache_create(m.ctx, 1, ig.IG_CACHE_HOST)
+    fill_cache(m, cache, kv, torch.stack([synth.make_latent(d, 1)]))
+    # free loads -> never dense; very slow loads -> every block dense
+    for load_s_per_byte, expect in ((0.0, 0), (1.0, d.n_blocks)):
+        ig.ig_set_plan(m.ctx, 2, 0, 1e-15, 1e-6, load_s_per_byte, 0.0)
+        ig.ig_edit_step(m.ctx, [r.req(0, cache, 0, 1.0, 0.9)], 0)
+        torch.cuda.synchronize()
+        assert ig.ig_last_plan(m.ctx) == expect
+    ig.ig_cache_free(cache)
+    r.free()
     m.close()
