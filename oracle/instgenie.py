@@ -18,6 +18,10 @@ What it computes, and where the paper says so
 * Dense step (no cache, all L tokens; fig:transformer-Top P:387-402) with K/V recording
   = the template cache ("pre-computed activations from previous requests").
                                                                      dense_step(record=)
+* Y-caching variant (fig:transformer-Bottom): the cache holds the
+  template's block outputs Y of the image tokens; unmasked rows of each block's input are
+  replenished from it and only feed K/V.        kv_from_y, edit_step_y, cache_template_y
+* Algorithm 1 dense prefix (C-AMB 23).            edit_step_planned, edit_step_y(k=)
 Readings where the paper is silent (Flux-shaped blocks, adaLN, QK-RMSNorm, RoPE,
 GELU-tanh, flow-matching Euler, row order) are the numbered C-AMB readings in DESIGN.md
 (SURVEY §8(c)).  Everything is float64; inputs are the exact fp32/bf16 values.
@@ -391,12 +395,103 @@ def edit_step_planned(d, W, latent, mask, kv_cache_step, tlatent, k, sigma, sigm
 
 
 # --------------------------------------------------------------------------------------
+# Y-caching variant (fig:transformer-Bottom; SPEC forward_masked_ycache S:113-121;
+# SURVEY N2).  The cache holds Y_b = the template's block-b OUTPUT rows of the image tokens.
+# Block b's input X holds every token: the masked rows computed by this request, the unmasked
+# rows "replenished" from the cache (Y_{b-1}; for b = 0 the template's block input
+# img_in(template latent) — C-AMB 23's reading of the unmasked tokens' trajectory).  K and V
+# come from the full X ("K and V computed from full x"); Q, the attention output and
+# every later token-wise op only from the masked rows ("project it into Q, and compute an Y
+# matrix exclusively for the masked tokens").
+# --------------------------------------------------------------------------------------
+def kv_from_y(d, W, b, x_u, vec, idx_u):
+    """K, V of the unmasked tokens recomputed from their block input rows x_u [n_u, H] with
+    THIS request's modulation and block-b weights; returned positionally as a [2, L_img, H]
+    array (rows idx_u filled), i.e. the K/V variant's cache slice that the Y variant implies."""
+    kv = np.zeros((2, d.L_img, d.hidden))
+    if len(idx_u) == 0:
+        return kv
+    pos = image_positions(d, idx_u)
+    if b < d.n_double:
+        p = f"double.{b}.img"
+        _, k, v = _qkv_stream(d, W, p, x_u, modulation(W, p, vec, 6), pos, FLUX_FLAGS)
+    else:
+        p = f"single.{b - d.n_double}"
+        _, k, v, _ = _single_pre(d, W, p, x_u, modulation(W, p, vec, 3), pos)
+    kv[0][idx_u], kv[1][idx_u] = k, v
+    return kv
+
+
+def edit_step_y(d, W, latent, mask, y_cache_step, tlatent, sigma, sigma_next, txt, cond_vec, k=0):
+    """One mask-aware step under the Y variant, with an optional Algorithm-1 dense prefix of k
+    blocks (P:563-605).  y_cache_step: [blocks, L_img, H] = Y_b of the template at this step;
+    tlatent: the template's input latent of this step [L_img, C].  A block whose predecessor
+    ran densely takes its unmasked input rows from that computation; otherwise from Y_{b-1}
+    (block 0: img_in(tlatent)).  Latent update and untouched rows as in edit_step."""
+    latent = np.asarray(latent, np.float64)
+    idx_m, idx_u, n_m = index_build(mask)
+    if n_m == 0:
+        return latent.copy()
+    if len(idx_u) == 0:
+        return edit_step(d, W, latent, mask, None, sigma, sigma_next, txt, cond_vec)
+    if y_cache_step is None:
+        raise KeyError("cache-miss: 0 < n_m < L_img needs a cache entry (S:134)")
+    k = max(0, min(k, d.n_blocks))
+    vec = conditioning(W, sigma, np.asarray(cond_vec, np.float64))
+    full = latent.copy()
+    full[idx_u] = np.asarray(tlatent, np.float64)[idx_u]
+    all_idx = np.arange(d.L_img)
+    none = np.zeros(0, np.int64)
+    Lt = d.txt_len
+    x_txt = np.asarray(txt, np.float64).copy()
+    x = None  # single-stream rows [txt | img]
+    if k > 0:
+        x_img = img_in(d, W, full, all_idx)
+    else:
+        x_img = img_in(d, W, latent, idx_m)
+    x_u = img_in(d, W, full, idx_u)  # block-0 input of the unmasked tokens
+    for b in range(d.n_blocks):
+        if b < k:  # dense block: every token, no cache
+            if b < d.n_double:
+                x_txt, x_img = double_block_masked(d, W, b, x_txt, x_img, vec, all_idx, none, None)
+            else:
+                if x is None:
+                    x = np.concatenate([x_txt, x_img])
+                x = single_block_masked(d, W, b - d.n_double, x, vec, all_idx, none, None)
+            if b == k - 1:  # unmasked rows leave the row set; their output feeds block k
+                rows = x_img if x is None else x[Lt:]
+                x_u = rows[idx_u]
+                if x is None:
+                    x_img = x_img[idx_m]
+                else:
+                    x = np.concatenate([x[:Lt], x[Lt:][idx_m]])
+            continue
+        if b > k:  # predecessor used the cache: replenish from Y_{b-1}
+            x_u = np.asarray(y_cache_step[b - 1], np.float64)[idx_u]
+        kv = kv_from_y(d, W, b, x_u, vec, idx_u)
+        if b < d.n_double:
+            x_txt, x_img = double_block_masked(d, W, b, x_txt, x_img, vec, idx_m, idx_u, kv)
+        else:
+            if x is None:
+                x = np.concatenate([x_txt, x_img])
+            x = single_block_masked(d, W, b - d.n_double, x, vec, idx_m, idx_u, kv)
+    if x is None:
+        x = np.concatenate([x_txt, x_img])
+    v = final_velocity(d, W, x[Lt:], vec)
+    out = latent.copy()
+    out[idx_m] = latent[idx_m] + (float(sigma_next) - float(sigma)) * v
+    return out
+
+
+# --------------------------------------------------------------------------------------
 # Dense step (independent code path: all L tokens, no index lists, no cache) + recording
 # --------------------------------------------------------------------------------------
-def dense_step(d, W, latent, sigma, sigma_next, txt, cond_vec, record: bool = False):
+def dense_step(d, W, latent, sigma, sigma_next, txt, cond_vec, record: bool = False,
+               record_y: bool = False):
     """Textbook full-token step (fig:transformer-Top).  Returns (new_latent, kv) where
     kv[b] = (K_img, V_img) [2, L_img, H] exactly as consumed by attention (post-norm,
-    post-RoPE; C-AMB 2) when record=True."""
+    post-RoPE; C-AMB 2) when record=True.  With record_y, returns (new_latent, kv, y) where
+    y[b] = the image tokens' rows of block b's output (the Y matrix of fig:transformer)."""
     latent = np.asarray(latent, np.float64)
     L_img, Lt, H = d.L_img, d.txt_len, d.hidden
     vec = conditioning(W, sigma, np.asarray(cond_vec, np.float64))
@@ -408,6 +503,7 @@ def dense_step(d, W, latent, sigma, sigma_next, txt, cond_vec, record: bool = Fa
     pos_img = image_positions(d, all_idx)
     pos_all = np.concatenate([np.zeros((Lt, 3), np.int64), pos_img])
     kv = np.zeros((d.n_blocks, 2, L_img, H)) if record else None
+    y = np.zeros((d.n_blocks, L_img, H)) if record_y else None
     for i in range(d.n_double):
         pi, pt = f"double.{i}.img", f"double.{i}.txt"
         mi = modulation(W, pi, vec, 6)
@@ -428,6 +524,8 @@ def dense_step(d, W, latent, sigma, sigma_next, txt, cond_vec, record: bool = Fa
         x_img = _double_out(d, W, pi, x_img, o[Lt:], mi, FLUX_FLAGS)
         if Lt and not pre_only:
             x_txt = _double_out(d, W, pt, x_txt, o[:Lt], mt, FLUX_FLAGS)
+        if record_y:
+            y[i] = x_img
     x = np.concatenate([x_txt, x_img])
     for i in range(d.n_single):
         p = f"single.{i}"
@@ -437,7 +535,11 @@ def dense_step(d, W, latent, sigma, sigma_next, txt, cond_vec, record: bool = Fa
             kv[d.n_double + i, 0], kv[d.n_double + i, 1] = k[Lt:], v[Lt:]
         o = attention(q, k, v, d.heads)
         x = _single_out(d, W, p, x, o, u, m)
+        if record_y:
+            y[d.n_double + i] = x[Lt:]
     vel = final_velocity(d, W, x[Lt:], vec)
+    if record_y:
+        return latent + (float(sigma_next) - float(sigma)) * vel, kv, y
     return latent + (float(sigma_next) - float(sigma)) * vel, kv
 
 
@@ -451,6 +553,20 @@ def cache_template(d, W, latent, txt, cond_vec, sigmas):
     for s in range(n):
         x, kv = dense_step(d, W, x, sigmas[s], sigmas[s + 1], txt, cond_vec, record=True)
         cache[s] = kv
+        traj.append(x.copy())
+    return x, cache, traj
+
+
+def cache_template_y(d, W, latent, txt, cond_vec, sigmas):
+    """Y-variant recording over the template's own schedule: returns (final_latent,
+    ycache[steps, blocks, L_img, H], trajectory)."""
+    n = len(sigmas) - 1
+    cache = np.zeros((n, d.n_blocks, d.L_img, d.hidden))
+    traj = [np.asarray(latent, np.float64).copy()]
+    x = traj[0]
+    for s in range(n):
+        x, _, y = dense_step(d, W, x, sigmas[s], sigmas[s + 1], txt, cond_vec, record_y=True)
+        cache[s] = y
         traj.append(x.copy())
     return x, cache, traj
 

@@ -389,3 +389,98 @@ def test_planned_step_exact_with_same_trajectory_cache(small_model, k):
     c = oracle.edit_step_planned(d, W, lat, mask, kv, tl, k, 0.7, 0.5, txt, cond)
     idx = mask != 0
     assert np.max(np.abs(c[idx] - dn[idx])) <= 1e-12 * np.abs(dn).max()
+
+
+# ---------------------------------------------------------------- Y variant (N2)
+def test_y_variant_masked_rows_equal_dense_grid(small_model):
+    # Y cache recorded from the same input -> masked rows equal the dense rows (S:141 grid;
+    # SPEC forward_masked_ycache post-condition), every bitmap-integral m, k = 0 and 1
+    d, W = small_model
+    sig = (0.8, 0.6)
+    cases = 0
+    for rid in range(2):
+        lat, txt, cond = _inputs(d, rid)
+        x1, _, y = oracle.dense_step(d, W, lat, sig[0], sig[1], txt, cond, record_y=True)
+        rng = np.random.default_rng(100 + rid)
+        for n in range(1, d.L_img + 1):
+            mask = np.zeros(d.L_img, np.uint8)
+            mask[rng.permutation(d.L_img)[:n]] = 1
+            idx = np.flatnonzero(mask)
+            for k in (0, 1) if n % 8 == 0 else (0,):
+                out = oracle.edit_step_y(d, W, lat, mask, y, lat, sig[0], sig[1], txt, cond, k=k)
+                assert np.max(np.abs(out[idx] - x1[idx])) <= 1e-12 * np.abs(x1[idx]).max(), (n, k)
+                assert np.array_equal(out[mask == 0], lat[mask == 0])
+                cases += 1
+    assert cases >= 128
+
+
+def test_y_variant_degenerate_masks(small_model):
+    d, W = small_model
+    lat, txt, cond = _inputs(d, 8)
+    x1, _ = oracle.dense_step(d, W, lat, 1.0, 0.9, txt, cond)
+    ones = np.ones(d.L_img, np.uint8)
+    assert np.array_equal(oracle.edit_step_y(d, W, lat, ones, None, lat, 1.0, 0.9, txt, cond), x1)
+    zero = np.zeros(d.L_img, np.uint8)
+    assert np.array_equal(oracle.edit_step_y(d, W, lat, zero, None, lat, 1.0, 0.9, txt, cond), lat)
+    m = np.zeros(d.L_img, np.uint8)
+    m[3] = 1
+    with pytest.raises(KeyError):
+        oracle.edit_step_y(d, W, lat, m, None, lat, 1.0, 0.9, txt, cond)
+
+
+def test_y_variant_equals_kv_variant_under_template_conditioning(small_model):
+    # Template and request share text, conditioning and sigma but not the latent: the K/V the
+    # Y variant recomputes for the unmasked tokens (from the template's block inputs, with the
+    # same modulation) are exactly the template's recorded K/V, so both variants agree to
+    # rounding for ANY masked content.  With other conditioning they differ (the Y variant
+    # really recomputes K/V with the request's modulation).
+    d, W = small_model
+    lat, txt, cond = _inputs(d, 21)
+    tl, _, cond_o = _inputs(d, 22)
+    _, kv, y = oracle.dense_step(d, W, tl, 0.9, 0.7, txt, cond, record=True, record_y=True)
+    mask = np.zeros(d.L_img, np.uint8)
+    mask[7:29] = 1
+    a = oracle.edit_step(d, W, lat, mask, kv, 0.9, 0.7, txt, cond)
+    b = oracle.edit_step_y(d, W, lat, mask, y, tl, 0.9, 0.7, txt, cond)
+    assert np.max(np.abs(a - b)) <= 1e-12 * np.abs(a).max()
+    c = oracle.edit_step(d, W, lat, mask, kv, 0.9, 0.7, txt, cond_o)
+    e = oracle.edit_step_y(d, W, lat, mask, y, tl, 0.9, 0.7, txt, cond_o)
+    assert np.max(np.abs(c - e)) > 1e-6
+
+
+def test_y_variant_multistep_trajectory_and_cache_bytes():
+    # 2-step tiny (config 1) along the recorded trajectory; Y cache = half the K/V cache
+    # ("doubles the sizes of the cached activations")
+    d = synth.TINY
+    W = _weights(d)
+    lat, txt, cond = _inputs(d, 0)
+    sig = [1.0, 0.5, 0.0]
+    _, ycache, traj = oracle.cache_template_y(d, W, lat, txt, cond, sig)
+    _, kvcache, _ = oracle.cache_template(d, W, lat, txt, cond, sig)
+    assert kvcache.size == 2 * ycache.size
+    mask = synth.tiny_rect_mask()
+    idx = np.flatnonzero(mask)
+    x = lat
+    for s in range(2):
+        x = oracle.edit_step_y(d, W, x, mask, ycache[s], traj[s], sig[s], sig[s + 1], txt, cond)
+        assert np.max(np.abs(x[idx] - traj[s + 1][idx])) <= 1e-12 * np.abs(traj[s + 1]).max()
+
+
+def test_y_variant_dense_prefix_all_blocks_is_dense_on_combined_input(small_model):
+    d, W = small_model
+    lat, txt, cond = _inputs(d, 31)
+    tl, _, _ = _inputs(d, 32)
+    mask = np.zeros(d.L_img, np.uint8)
+    mask[12:44] = 1
+    _, _, y = oracle.dense_step(d, W, tl, 0.9, 0.8, txt, cond, record_y=True)
+    full = lat.copy()
+    full[mask == 0] = tl[mask == 0]
+    dn, _ = oracle.dense_step(d, W, full, 0.9, 0.8, txt, cond)
+    c = oracle.edit_step_y(d, W, lat, mask, y, tl, 0.9, 0.8, txt, cond, k=d.n_blocks)
+    idx = mask != 0
+    assert np.max(np.abs(c[idx] - dn[idx])) <= 1e-12 * np.abs(dn).max()
+    # k = 1 under the Y variant: block 1 takes the COMPUTED unmasked rows of block 0 (their
+    # input was the template's), so with a template-identical request it is exact as well
+    _, _, y_same = oracle.dense_step(d, W, full, 0.9, 0.8, txt, cond, record_y=True)
+    c1 = oracle.edit_step_y(d, W, lat, mask, y_same, full, 0.9, 0.8, txt, cond, k=1)
+    assert np.max(np.abs(c1[idx] - dn[idx])) <= 1e-12 * np.abs(dn).max()
