@@ -166,7 +166,8 @@ def run_loop(ig, ctx, batch, cache, sig, steps, stream, profile=False, e2e=None)
     """Runs `steps` batch steps on `stream`; returns (ms, request_steps, launches, stats)."""
     launches, rsteps = 0, 0
     h2d = d2h = 0
-    evs = []
+    evs, plans = [], []
+    alg_flops = 0.0
     start = torch.cuda.Event(enable_timing=True)
     end = torch.cuda.Event(enable_timing=True)
     if profile:
@@ -181,6 +182,8 @@ def run_loop(ig, ctx, batch, cache, sig, steps, stream, profile=False, e2e=None)
                 r.latent.copy_(hb, non_blocking=True)
                 h2d += hb.numel() * 4
         ig.ig_edit_step(ctx, batch.reqs(cache, sig), stream.cuda_stream)
+        plans.append(ig.ig_last_plan(ctx))
+        alg_flops += sum(N_BLOCKS_FLOPS(batch.d, r.n_m) for r in batch.slots)
         st = ig.ig_last_stats(ctx)
         launches += st["kernel_launches"]
         h2d += st["h2d_bytes"]
@@ -199,7 +202,47 @@ def run_loop(ig, ctx, batch, cache, sig, steps, stream, profile=False, e2e=None)
     if profile:
         ig.ig_profile_enable(ctx, False)
     per_step = [a.elapsed_time(b) for a, b in evs]
-    return start.elapsed_time(end), rsteps, launches, per_step, prof, h2d, d2h
+    return Leg(start.elapsed_time(end), rsteps, launches, per_step, prof, h2d, d2h, plans, alg_flops)
+
+
+class Leg:
+    """Result of one timed run_loop window."""
+
+    def __init__(self, ms, rsteps, launches, per_step, prof, h2d, d2h, plans, alg_flops):
+        self.ms, self.rsteps, self.launches, self.per_step = ms, rsteps, launches, per_step
+        self.prof, self.h2d, self.d2h, self.plans, self.alg_flops = prof, h2d, d2h, plans, alg_flops
+
+    def tflops(self, cls):
+        e = self.prof[cls]
+        return e["flops"] / (e["ms"] * 1e-3) / 1e12 if e["ms"] else 0.0
+
+
+def N_BLOCKS_FLOPS(d, n_m):
+    """All-cache algorithmic FLOPs of one request-step (Table 1 scaling; SURVEY
+    §8(d) F(m) = 16.138 GFLOP x (L_txt + n_m) for Flux): every block's projections/MLP over the
+    request's query rows plus masked-Q x full-KV attention."""
+    from paper_2505_20600_b200.placement import block_flops
+    if n_m == 0:
+        return 0.0
+    return d.n_blocks * block_flops(d, n_m)
+
+
+def fit_latency(ig, ctx, d, dev, stream, link_gbs):
+    """Linear latency models of Algorithm 1/2: per-block compute time vs FLOPs
+    from dense steps (all-ones masks, no cache) at two batch sizes, and per-block load time
+    vs bytes from the measured host link.  Returns (a_c, b_c, a_l, b_l, r2 info)."""
+    from paper_2505_20600_b200.placement import block_flops, fit_ols
+    pts = []
+    for nb_ in (2, 4):
+        bt = Batch(ig, ctx, d, dev, nb_, nb_, rid0=900000 + nb_, dense=True)
+        run_loop(ig, ctx, bt, None, synth.flow_sigmas(N_STEPS), 1, stream)
+        lg = run_loop(ig, ctx, bt, None, synth.flow_sigmas(N_STEPS), 2, stream)
+        per_block_ms = statistics.median(lg.per_step) / d.n_blocks
+        pts.append((nb_ * block_flops(d, d.L_img), per_block_ms * 1e-3))
+        for r in bt.pool:
+            ig.ig_mask_free(r.mask)
+    a_c, b_c, _ = fit_ols([p[0] for p in pts], [p[1] for p in pts])
+    return a_c, max(b_c, 0.0), 1.0 / (link_gbs * 1e9), 0.0
 
 
 # ------------------------------------------------------------------------------- oracle leg
@@ -285,7 +328,8 @@ def main():
     ap.add_argument("--max-batch", type=int, default=8)
     ap.add_argument("--tier", default=None, choices=["host", "device"])
     ap.add_argument("--copy-mode", type=int, default=1)
-    ap.add_argument("--depth", type=int, default=2)
+    ap.add_argument("--depth", type=int, default=8)
+    ap.add_argument("--plan", default="model", help="Algorithm-1 dense prefix: model | none | <k>")
     ap.add_argument("--dense-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -328,7 +372,6 @@ def main():
     t_template = time.time() - t0
     stream = torch.cuda.Stream(device=dev)
     pool = args.max_batch + math.ceil(args.max_batch * (2 * args.warmup + 2 * args.steps) / N_STEPS) + 2
-    batch = Batch(ig, ctx, d, dev, args.max_batch, pool, rid0=rank * 100000)
     torch.cuda.synchronize()
 
     def barrier():
@@ -337,62 +380,74 @@ def main():
             torch.distributed.barrier()
         torch.cuda.synchronize()
 
-    # warm-up, then the timed window (profiling events on the launching stream)
-    run_loop(ig, ctx, batch, cache, sig, args.warmup, stream)
-    clocks = Clocks(local)
-    barrier()
-    clocks.start()
-    ms, rsteps, launches, per_step, prof, h2d, _ = run_loop(ig, ctx, batch, cache, sig, args.steps, stream,
-                                                            profile=True)
-    barrier()
-    clk = clocks.stop()
-    t = torch.tensor([ms, float(rsteps)], dtype=torch.float64, device=dev)
-    if world > 1:
-        mx = t.clone()
-        torch.distributed.all_reduce(mx, op=torch.distributed.ReduceOp.MAX)
-        sm = t.clone()
-        torch.distributed.all_reduce(sm, op=torch.distributed.ReduceOp.SUM)
-        ms_max, rsteps_all = float(mx[0]), float(sm[1])
-    else:
-        ms_max, rsteps_all = ms, float(rsteps)
-    value = rsteps_all / N_STEPS / (ms_max / 1e3)
+    def reduce_max_sum(ms_, rs_):
+        t = torch.tensor([ms_, float(rs_)], dtype=torch.float64, device=dev)
+        if world > 1:
+            mx = t.clone()
+            torch.distributed.all_reduce(mx, op=torch.distributed.ReduceOp.MAX)
+            sm = t.clone()
+            torch.distributed.all_reduce(sm, op=torch.distributed.ReduceOp.SUM)
+            return float(mx[0]), float(sm[1])
+        return ms_, float(rs_)
 
-    # end to end through the public API with host buffers (latent H2D + D2H every step); each
-    # measured leg replays the same request sequence (fresh batch, same request ids)
+    def leg(c, cch, profile=True, e2e=False, clk=None):
+        """One measured configuration: a fresh batch replaying the same request sequence,
+        W warm-up steps, then K timed steps between barriers."""
+        bt = Batch(ig, c, d, dev, args.max_batch, pool, rid0=rank * 100000)
+        run_loop(ig, c, bt, cch, sig, args.warmup, stream)
+        hb = {r.rid: r.latent.detach().cpu().pin_memory() for r in bt.pool} if e2e else None
+        barrier()
+        if clk:
+            clk.start()
+        lg = run_loop(ig, c, bt, cch, sig, args.steps, stream, profile=profile, e2e=hb)
+        barrier()
+        lg.clk = clk.stop() if clk else None
+        lg.ms_max, lg.rs_all = reduce_max_sum(lg.ms, lg.rsteps)
+        lg.value = lg.rs_all / N_STEPS / (lg.ms_max / 1e3)
+        for r in bt.pool:
+            ig.ig_mask_free(r.mask)
+        return lg
+
+    def summary(lg):
+        return {"value": round(lg.value, 4), "unit": "images/s", "ms_per_step": round(lg.ms / args.steps, 3),
+                "gemm_tflops": round(lg.tflops("gemm"), 1), "attn_tflops": round(lg.tflops("attn"), 1),
+                "host_link_GBps": round(lg.h2d / (lg.ms * 1e-3) / 1e9, 2),
+                "plan_k": {"min": min(lg.plans), "max": max(lg.plans),
+                           "mean": round(float(np.mean(lg.plans)), 2)},
+                "alg_tensor_frac": round(lg.alg_flops / (lg.ms * 1e-3) / 1e12 / pk_sus, 4),
+                "kernel_share_of_step": {k: round(v["ms"] / lg.ms, 4) for k, v in lg.prof.items()}}
+
+    # Algorithm-1 latency models (P:701-726) fitted on this GPU, then the headline: the
+    # mask-aware step with the per-step dense-prefix plan (N1), cache in pinned host memory
+    a_c, b_c, a_l, b_l = fit_latency(ig, ctx, d, dev, stream, link_peak)
+    plan_mode = {"model": 2, "none": 0}.get(args.plan, 1)
+    ig.ig_set_plan(ctx, plan_mode, 0 if plan_mode != 1 else int(args.plan), a_c, b_c, a_l, b_l)
+    main_leg = leg(ctx, cache, clk=Clocks(local))
+    ms, ms_max, value, prof, per_step = main_leg.ms, main_leg.ms_max, main_leg.value, main_leg.prof, main_leg.per_step
+    launches, h2d, clk = main_leg.launches, main_leg.h2d, main_leg.clk
+
+    # end to end through the public API with host buffers (latent H2D + D2H every step)
     e2e = None
     if not args.no_e2e:
-        batch = Batch(ig, ctx, d, dev, args.max_batch, pool, rid0=rank * 100000)
-        run_loop(ig, ctx, batch, cache, sig, args.warmup, stream)
-        hbufs = {r.rid: r.latent.detach().cpu().pin_memory() for r in batch.pool}
-        barrier()
-        ms_e, rs_e, _, _, _, h2d_e, d2h_e = run_loop(ig, ctx, batch, cache, sig, args.steps, stream, e2e=hbufs)
-        barrier()
-        te = torch.tensor([ms_e, float(rs_e)], dtype=torch.float64, device=dev)
-        if world > 1:
-            mx = te.clone()
-            torch.distributed.all_reduce(mx, op=torch.distributed.ReduceOp.MAX)
-            sm = te.clone()
-            torch.distributed.all_reduce(sm, op=torch.distributed.ReduceOp.SUM)
-            ms_e, rs_e = float(mx[0]), float(sm[1])
-        e2e = {"value": rs_e / N_STEPS / (ms_e / 1e3), "unit": "images/s",
-               "h2d_bytes_per_step": int(h2d_e / args.steps), "d2h_bytes_per_step": int(d2h_e / args.steps)}
+        le = leg(ctx, cache, profile=False, e2e=True)
+        e2e = {"value": le.value, "unit": "images/s",
+               "h2d_bytes_per_step": int(le.h2d / args.steps), "d2h_bytes_per_step": int(le.d2h / args.steps)}
+
+    # the same workload without the plan (every block uses the cache: the K/V variant alone)
+    noplan = None
+    if plan_mode != 0 and tier == "host" and world == 1:
+        ig.ig_set_plan(ctx, 0, 0, 0.0, 0.0, 0.0, 0.0)
+        noplan = summary(leg(ctx, cache))
+        ig.ig_set_plan(ctx, plan_mode, 0 if plan_mode != 1 else int(args.plan), a_c, b_c, a_l, b_l)
 
     # the same workload with the template cache resident in HBM (hot-template tier, SURVEY N4)
     hbm = None
     if tier == "host" and not args.no_hbm_tier and world == 1:
         dcache = ig.ig_cache_clone(ctx, cache, ig.IG_CACHE_DEVICE)
-        batch = Batch(ig, ctx, d, dev, args.max_batch, pool, rid0=rank * 100000)
-        run_loop(ig, ctx, batch, dcache, sig, args.warmup, stream)
-        barrier()
-        ms_h, rs_h, _, per_h, prof_h, _, _ = run_loop(ig, ctx, batch, dcache, sig, args.steps, stream, profile=True)
-        barrier()
+        ig.ig_set_plan(ctx, 0, 0, 0.0, 0.0, 0.0, 0.0)  # nothing to balance: no host link
+        hbm = summary(leg(ctx, dcache))
+        ig.ig_set_plan(ctx, plan_mode, 0 if plan_mode != 1 else int(args.plan), a_c, b_c, a_l, b_l)
         ig.ig_cache_free(dcache)
-        gh, ah = prof_h["gemm"], prof_h["attn"]
-        hbm = {"value": round(rs_h / N_STEPS / (ms_h / 1e3), 4), "unit": "images/s",
-               "ms_per_step": round(ms_h / args.steps, 3),
-               "gemm_tflops": round(gh["flops"] / (gh["ms"] * 1e-3) / 1e12, 1) if gh["ms"] else None,
-               "attn_tflops": round(ah["flops"] / (ah["ms"] * 1e-3) / 1e12, 1) if ah["ms"] else None,
-               "kernel_share_of_step": {k: round(v["ms"] / ms_h, 4) for k, v in prof_h.items()}}
 
     # FP8 (e4m3) cache in pinned host memory (SURVEY N4 byte reducer): a second context on the
     # same weights whose caches are e4m3 + per-(token, head) scales; same request sequence
@@ -401,18 +456,10 @@ def main():
         opts8 = ig.ig_ctx_opts(args.max_batch, args.max_batch * d.L, args.depth, args.copy_mode, 0, 1)
         ctx8 = ig.ig_ctx_create(ig.make_desc(d, ig.IG_BF16), ptrs, local, opts8)
         cache8 = ig.ig_cache_clone(ctx8, cache, ig.IG_CACHE_HOST)
-        batch = Batch(ig, ctx8, d, dev, args.max_batch, pool, rid0=rank * 100000)
-        run_loop(ig, ctx8, batch, cache8, sig, args.warmup, stream)
-        barrier()
-        ms_8, rs_8, _, _, prof_8, h2d_8, _ = run_loop(ig, ctx8, batch, cache8, sig, args.steps, stream, profile=True)
-        barrier()
-        g8 = prof_8["gemm"]
-        fp8 = {"value": round(rs_8 / N_STEPS / (ms_8 / 1e3), 4), "unit": "images/s",
-               "ms_per_step": round(ms_8 / args.steps, 3),
-               "host_link_GBps": round(h2d_8 / (ms_8 * 1e-3) / 1e9, 2),
-               "gemm_tflops": round(g8["flops"] / (g8["ms"] * 1e-3) / 1e12, 1) if g8["ms"] else None,
-               "kernel_share_of_step": {k: round(v["ms"] / ms_8, 4) for k, v in prof_8.items()},
-               "note": "same workload, K/V cache stored as e4m3 + fp32 scale per (token, head): half the host-link bytes"}
+        ig.ig_set_plan(ctx8, plan_mode, 0 if plan_mode != 1 else int(args.plan), a_c, b_c, a_l / 1.0, b_l)
+        fp8 = summary(leg(ctx8, cache8))
+        fp8["note"] = ("same workload, K/V cache stored as e4m3 + fp32 scale per (token, head): "
+                       "half the host-link bytes")
         ig.ig_cache_free(cache8)
         ig.ig_ctx_destroy(ctx8)
 
@@ -422,15 +469,9 @@ def main():
         dbatch = Batch(ig, ctx, d, dev, args.max_batch, args.max_batch + 2, rid0=rank * 100000 + 50000, dense=True)
         run_loop(ig, ctx, dbatch, None, sig, 1, stream)
         barrier()
-        ms_d, rs_d, _, _, _, _, _ = run_loop(ig, ctx, dbatch, None, sig, args.dense_steps, stream)
+        ld = run_loop(ig, ctx, dbatch, None, sig, args.dense_steps, stream)
         barrier()
-        td = torch.tensor([ms_d, float(rs_d)], dtype=torch.float64, device=dev)
-        if world > 1:
-            mx = td.clone()
-            torch.distributed.all_reduce(mx, op=torch.distributed.ReduceOp.MAX)
-            sm = td.clone()
-            torch.distributed.all_reduce(sm, op=torch.distributed.ReduceOp.SUM)
-            ms_d, rs_d = float(mx[0]), float(sm[1])
+        ms_d, rs_d = reduce_max_sum(ld.ms, ld.rsteps)
         dense = rs_d / N_STEPS / (ms_d / 1e3)
 
     if rank != 0:
@@ -441,10 +482,9 @@ def main():
     tp = os.path.join(ROOT, "profiles", "gemm_traffic.json")
     if os.path.exists(tp):
         traffic = json.load(open(tp))
-    g = prof["gemm"]
-    gemm_tf = g["flops"] / (g["ms"] * 1e-3) / 1e12 if g["ms"] else 0.0
-    a = prof["attn"]
-    attn_tf = a["flops"] / (a["ms"] * 1e-3) / 1e12 if a["ms"] else 0.0
+    gemm_tf = main_leg.tflops("gemm")
+    attn_tf = main_leg.tflops("attn")
+    exec_flops = prof["gemm"]["flops"] + prof["attn"]["flops"]
     step_ms = ms / args.steps
     shares = {k: round(v["ms"] / args.steps / step_ms, 4) for k, v in prof.items()}
     out = {
@@ -454,7 +494,8 @@ def main():
         "data": "synthetic",
         "config": {"workload": f"{d.name} 1024^2 (4096 img + 512 txt tokens), 28-step flow schedule, "
                                f"continuous batching max_batch {args.max_batch}, masks m~U[0.05,0.60] "
-                               f"(rect/blob), K/V cache tier={tier} copy_mode={args.copy_mode} depth={args.depth}",
+                               f"(rect/blob), K/V cache tier={tier} copy_mode={args.copy_mode} depth={args.depth} "
+                               f"plan={args.plan}",
                    "global_batch": args.max_batch * world, "seq_len": d.L, "parallelism": f"replica{world}",
                    "l2": "inputs larger than L2 (23.7 GB weights + 2.9 GB K/V per request-step streamed)"},
         "roofline": {"bound": "tensor", "kernel": "gemm_tc (tcgen05 bf16)", "achieved": round(gemm_tf, 1),
@@ -465,6 +506,19 @@ def main():
                      "frac_of_burst": round(gemm_tf / pk_burst, 4)},
         "attn_roofline": {"achieved": round(attn_tf, 1), "unit": "TFLOP/s", "frac": round(attn_tf / pk_sus, 4)},
         "kernel_share_of_step": shares,
+        "step_roofline": {"bound": "tensor", "unit": "TFLOP/s", "peak": pk_sus,
+                          "alg_tflop_per_step": round(main_leg.alg_flops / args.steps / 1e12, 2),
+                          "achieved": round(main_leg.alg_flops / (ms * 1e-3) / 1e12, 1),
+                          "frac": round(main_leg.alg_flops / (ms * 1e-3) / 1e12 / pk_sus, 4),
+                          "executed_frac": round(exec_flops / (ms * 1e-3) / 1e12 / pk_sus, 4),
+                          "note": "all-cache algorithmic FLOPs (Table 1 scaling, SURVEY 8(d) F(m)) of the "
+                                  "request-steps in the window / window time; executed_frac counts the "
+                                  "FLOPs actually run (dense-prefix blocks included)"},
+        "plan": {"mode": args.plan, "k": {"min": min(main_leg.plans), "max": max(main_leg.plans),
+                                          "mean": round(float(np.mean(main_leg.plans)), 2)},
+                 "latency_model": {"comp_s_per_tflop": round(a_c * 1e12, 6), "comp_s": round(b_c, 6),
+                                   "load_s_per_GB": round(a_l * 1e9, 6), "load_s": b_l}},
+        "no_plan_host_tier": noplan,
         "per_step_ms": {"median": round(statistics.median(per_step), 3),
                         "p10": round(float(np.percentile(per_step, 10)), 3),
                         "p90": round(float(np.percentile(per_step, 90)), 3)},

@@ -91,6 +91,11 @@ typedef struct {
   int cache_fp8;       /* 1 = caches created by this ctx store K/V as e4m3 with a fp32   */
                        /*     scale per (token, head): scale = amax/448, x' = bf16(q*scale)*/
                        /*     (halves host-link bytes; bf16 mode only)          */
+  int cache_y;         /* 1 = caches created by this ctx hold Y, the template's block     */
+                       /*     OUTPUT rows of the image tokens [steps][blocks][L_img][H]    */
+                       /*     (fig:transformer-Bottom): half the     */
+                       /*     bytes of K/V; a step recomputes the unmasked tokens' K/V     */
+                       /*     from them (LN-mod + K/V projection).  Not with cache_fp8.    */
 } ig_ctx_opts;
 
 typedef struct ig_ctx ig_ctx;
@@ -109,7 +114,8 @@ typedef enum { IG_CACHE_HOST = 0, IG_CACHE_DEVICE = 1 } ig_cache_tier;
 
 /* Template cache: for every (step s, block b) the image-token K and V exactly as consumed
  * by attention (post-bias, post-RMSNorm, post-RoPE; C-AMB 2), layout
- * [n_steps][n_blocks][2 (K,V)][L_img][H], dtype = desc.dtype, in pinned host memory
+ * [n_steps][n_blocks][2 (K,V)][L_img][H] — or, for a ctx created with cache_y, the block
+ * output Y [n_steps][n_blocks][L_img][H] — dtype = desc.dtype, in pinned host memory
  * (IG_CACHE_HOST, "host memory ... for cached activations") or in HBM
  * (IG_CACHE_DEVICE), followed by the template's input latent of every step
  * [n_steps][L_img][lat_ch] fp32 (used by the Algorithm-1 dense prefix, ig_set_plan).  Bytes = n_steps*n_blocks*2*L_img*H*sizeof(dtype): twice the
@@ -168,7 +174,13 @@ typedef struct {
   const float* cond_vec;   /* dev [H] fp32                                                   */
 } ig_edit_req;
 
-/* One mask-aware denoising step for a ragged continuous batch (P:642-659 step-level
+/* Y-cache requests (cache created by a cache_y ctx; any ctx can consume them, and a batch may
+ * mix both kinds): block b's unmasked input rows are the template's Y_{b-1} rows (block 0:
+ * img_in of the template's input latent; a block after a dense-prefix block: the computed
+ * rows), they go through LN-modulation and the K/V projection only (Q, attention output and
+ * the MLP stay on the masked rows), and the copy lane moves one plane per block instead of two.
+ *
+ * One mask-aware denoising step for a ragged continuous batch (P:642-659 step-level
  * continuous batching): for every block, only the [txt | masked image] rows of each
  * request go through the GEMMs, their fresh K/V are merged by mask index
  * with the template's cached unmasked-token K/V (fig:transformer_alter), masked-Q x full-KV

@@ -104,6 +104,7 @@ struct ig_cache {
   ig_model_desc desc{};
   int n_steps = 0, tier = 0;
   int fp8 = 0;              // 1: e4m3 data [steps][blocks][2][L_img][H] + fp32 scales [..][heads]
+  int y = 0;                // 1: Y variant, block outputs [steps][blocks][L_img][H] (one plane)
   size_t scale_off = 0;     // byte offset of the scale region (fp8 only)
   size_t lat_off = 0;       // template input latent per step [steps][L_img][C] fp32 (Algorithm-1
                             // dense prefix: unmasked rows enter from the template's trajectory)
@@ -167,6 +168,10 @@ struct ig_ctx {
   uint8_t* q8in = nullptr;  float* q8in_scl = nullptr;
   uint8_t* q8rec = nullptr; float* q8rec_scl = nullptr;
   std::vector<size_t> b_size;
+  // Y recording staging (cache_y): per ring buffer the block output's image rows in the
+  // compute dtype, read by the D2H on the copy stream; ev_yrec guards its reuse (WAR)
+  void* yrec = nullptr;
+  cudaEvent_t ev_yrec[MAXR] = {};
   ig_stats stats{};
   std::vector<ig_cache*> zombies;
   // Algorithm-1 block plan (ig_set_plan): 0 off, 1 forced dense-prefix length, 2 model
@@ -339,7 +344,7 @@ extern "C" ig_status ig_ctx_create(const ig_model_desc* desc, const void* const*
     return set_err(IG_EINVAL, "expected %d weight pointers, got %d", nw, n_weights);
   for (int i = 0; i < nw; ++i)
     if (!weights[i]) return set_err(IG_EINVAL, "weight %d is NULL", i);
-  ig_ctx_opts o{8, 0, 2, 0, 0, 0};
+  ig_ctx_opts o{8, 0, 2, 0, 0, 0, 0};
   if (opts) o = *opts;
   if (o.max_batch <= 0) o.max_batch = 8;
   if (o.max_batch > 16) return set_err(IG_EUNSUPPORTED, "max_batch > 16");
@@ -347,6 +352,7 @@ extern "C" ig_status ig_ctx_create(const ig_model_desc* desc, const void* const*
   if (o.prefetch_depth + 1 > MAXR) return set_err(IG_EUNSUPPORTED, "prefetch_depth > %d", MAXR - 1);
   if (o.copy_mode < 0 || o.copy_mode > 2) return set_err(IG_EINVAL, "copy_mode must be 0, 1 or 2");
   if (o.cache_fp8 && desc->dtype != IG_BF16) return set_err(IG_EUNSUPPORTED, "FP8 caches need the bf16 mode");
+  if (o.cache_fp8 && o.cache_y) return set_err(IG_EUNSUPPORTED, "cache_y with cache_fp8 is not supported");
   const int Lall = desc->txt_len + desc->grid_h * desc->grid_w;
   if (o.max_rows <= 0) o.max_rows = o.max_batch * Lall;
 
@@ -469,6 +475,10 @@ extern "C" ig_status ig_ctx_create(const ig_model_desc* desc, const void* const*
     okm &= dmalloc((void**)&ctx->q8rec_scl, (size_t)ctx->R * 2 * spl * 4);
     if (!okm) { ig_ctx_destroy(ctx); return set_err(IG_ENOMEM, "fp8 staging allocation failed"); }
   }
+  if (o.cache_y) {
+    okm &= dmalloc(&ctx->yrec, (size_t)ctx->R * ctx->Limg * H * es);
+    if (!okm) { ig_ctx_destroy(ctx); return set_err(IG_ENOMEM, "Y recording staging allocation failed"); }
+  }
   // per-step descriptor staging: ReqDev[B] + AttnSeg[2B] + 2 x KvGatherReq[nb * B]
   ctx->stage_bytes = B * sizeof(ReqDev) + 5 * B * sizeof(AttnSeg) + 2 * (size_t)ctx->nb * B * sizeof(KvGatherReq) + 1024;
   for (int i = 0; i < NSTAGE; ++i) {
@@ -483,6 +493,7 @@ extern "C" ig_status ig_ctx_create(const ig_model_desc* desc, const void* const*
   for (int i = 0; i < MAXR; ++i) {
     cudaEventCreateWithFlags(&ctx->ev_copy[i], cudaEventDisableTiming);
     cudaEventCreateWithFlags(&ctx->ev_comp[i], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&ctx->ev_yrec[i], cudaEventDisableTiming);
   }
   cudaEventCreateWithFlags(&ctx->ev_desc, cudaEventDisableTiming);
   ctx->pref.assign((size_t)B * ctx->R, ig_ctx::Pref{});
@@ -500,7 +511,7 @@ extern "C" void ig_ctx_destroy(ig_ctx* ctx) {
   void* bufs[] = {ctx->X, ctx->vel, ctx->temb, ctx->tmp, ctx->vec, ctx->svec, ctx->modbuf, ctx->h,
                   ctx->qkv, ctx->Q, ctx->cat, ctx->Ain, ctx->ri, ctx->kv_arena, ctx->rope_tab,
                   ctx->gv_t1, ctx->gv_t2, ctx->gv_mod, ctx->modw, ctx->modb, ctx->svec_bf,
-                  ctx->q8in, ctx->q8in_scl, ctx->q8rec, ctx->q8rec_scl};
+                  ctx->q8in, ctx->q8in_scl, ctx->q8rec, ctx->q8rec_scl, ctx->yrec};
   for (void* b : bufs) if (b) cudaFree(b);
   for (int i = 0; i < NSTAGE; ++i) {
     if (ctx->h_stage[i]) cudaFreeHost(ctx->h_stage[i]);
@@ -510,6 +521,7 @@ extern "C" void ig_ctx_destroy(ig_ctx* ctx) {
   for (int i = 0; i < MAXR; ++i) {
     if (ctx->ev_copy[i]) cudaEventDestroy(ctx->ev_copy[i]);
     if (ctx->ev_comp[i]) cudaEventDestroy(ctx->ev_comp[i]);
+    if (ctx->ev_yrec[i]) cudaEventDestroy(ctx->ev_yrec[i]);
   }
   if (ctx->ev_desc) cudaEventDestroy(ctx->ev_desc);
   for (auto& r : ctx->prof_recs) { ctx->ev_pool.push_back(r.a); ctx->ev_pool.push_back(r.b); }
@@ -627,12 +639,12 @@ static ig_status get_ones_mask(ig_ctx* ctx, ig_mask** out) {
 // ----------------------------------------------------------------------------------------
 // caches
 // ----------------------------------------------------------------------------------------
-static size_t cache_kv_bytes(const ig_ctx* ctx, int n_steps, int fp8) {
+static size_t cache_kv_bytes(const ig_ctx* ctx, int n_steps, int fp8, int y = 0) {
   if (fp8) return (size_t)n_steps * ctx->nb * 2 * ctx->Limg * ((size_t)ctx->H + 4 * ctx->d.heads);
-  return (size_t)n_steps * ctx->nb * 2 * ctx->Limg * ctx->H * ctx->esz;
+  return (size_t)n_steps * ctx->nb * (y ? 1 : 2) * ctx->Limg * ctx->H * ctx->esz;
 }
-static size_t cache_bytes(const ig_ctx* ctx, int n_steps, int fp8 = 0) {
-  return cache_kv_bytes(ctx, n_steps, fp8) + (size_t)n_steps * ctx->Limg * ctx->C * 4;
+static size_t cache_bytes(const ig_ctx* ctx, int n_steps, int fp8 = 0, int y = 0) {
+  return cache_kv_bytes(ctx, n_steps, fp8, y) + (size_t)n_steps * ctx->Limg * ctx->C * 4;
 }
 static float* cache_latent(const ig_ctx* ctx, const ig_cache* c, int step) {
   return (float*)((char*)c->ptr + c->lat_off + (size_t)step * ctx->Limg * ctx->C * 4);
@@ -640,9 +652,11 @@ static float* cache_latent(const ig_ctx* ctx, const ig_cache* c, int step) {
 static const float* cache_latent_dev(const ig_ctx* ctx, const ig_cache* c, int step) {
   return (const float*)((const char*)c->dptr + ((char*)cache_latent(ctx, c, step) - (char*)c->ptr));
 }
-// data plane (which = 0 K, 1 V) of (step, block) and its scale plane (fp8 caches)
+// data plane (which = 0 K, 1 V) of (step, block) and its scale plane (fp8 caches); a Y cache
+// has one plane per (step, block) (which is ignored)
 static char* cache_plane(const ig_ctx* ctx, const ig_cache* c, int step, int b, int which) {
   const size_t row = c->fp8 ? (size_t)ctx->H : (size_t)ctx->H * ctx->esz;
+  if (c->y) return (char*)c->ptr + ((size_t)step * ctx->nb + b) * ctx->Limg * row;
   return (char*)c->ptr + (((size_t)step * ctx->nb + b) * 2 + which) * ctx->Limg * row;
 }
 static float* cache_scales(const ig_ctx* ctx, const ig_cache* c, int step, int b, int which) {
@@ -656,8 +670,13 @@ static const float* cache_scales_dev(const ig_ctx* ctx, const ig_cache* c, int s
   return (const float*)((const char*)c->dptr + ((char*)cache_scales(ctx, c, step, b, which) - (char*)c->ptr));
 }
 
+static ig_status cache_create_kind(ig_ctx* ctx, int n_steps, int tier, int fp8, int y, ig_cache** out);
 extern "C" ig_status ig_cache_create(ig_ctx* ctx, int n_steps, int tier, ig_cache** out) {
   if (!ctx || !out) return set_err(IG_EINVAL, "NULL argument");
+  return cache_create_kind(ctx, n_steps, tier, ctx->o.cache_fp8, ctx->o.cache_y, out);
+}
+
+static ig_status cache_create_kind(ig_ctx* ctx, int n_steps, int tier, int fp8, int y, ig_cache** out) {
   *out = nullptr;
   if (n_steps <= 0) return set_err(IG_EINVAL, "n_steps must be positive");
   if (tier != IG_CACHE_HOST && tier != IG_CACHE_DEVICE) return set_err(IG_EINVAL, "bad tier");
@@ -667,10 +686,11 @@ extern "C" ig_status ig_cache_create(ig_ctx* ctx, int n_steps, int tier, ig_cach
   c->n_steps = n_steps;
   c->tier = tier;
   c->device = ctx->device;
-  c->fp8 = ctx->o.cache_fp8;
-  c->bytes = cache_bytes(ctx, n_steps, c->fp8);
+  c->fp8 = fp8;
+  c->y = y;
+  c->bytes = cache_bytes(ctx, n_steps, c->fp8, c->y);
   if (c->fp8) c->scale_off = (size_t)n_steps * ctx->nb * 2 * ctx->Limg * ctx->H;
-  c->lat_off = cache_kv_bytes(ctx, n_steps, c->fp8);
+  c->lat_off = cache_kv_bytes(ctx, n_steps, c->fp8, c->y);
   cudaError_t e;
   if (tier == IG_CACHE_HOST) {
     e = cudaHostAlloc(&c->ptr, c->bytes, cudaHostAllocMapped | cudaHostAllocPortable);
@@ -683,7 +703,7 @@ extern "C" ig_status ig_cache_create(ig_ctx* ctx, int n_steps, int tier, ig_cach
     cudaGetLastError();
     if (c->ptr) { if (tier == IG_CACHE_HOST) cudaFreeHost(c->ptr); else cudaFree(c->ptr); }
     delete c;
-    return set_err(IG_ENOMEM, "cache allocation of %zu bytes failed: %s", cache_bytes(ctx, n_steps, ctx->o.cache_fp8),
+    return set_err(IG_ENOMEM, "cache allocation of %zu bytes failed: %s", cache_bytes(ctx, n_steps, fp8, y),
                    cudaGetErrorString(e));
   }
   *out = c;
@@ -696,9 +716,10 @@ extern "C" ig_status ig_cache_clone(ig_ctx* ctx, const ig_cache* src, int tier, 
   if (!desc_equal(src->desc, ctx->d)) return set_err(IG_ECACHE_INCOMPAT, "cache built for another model");
   const bool quantize = ctx->o.cache_fp8 && !src->fp8;  // bf16 -> fp8 conversion
   if (!ctx->o.cache_fp8 && src->fp8) return set_err(IG_EUNSUPPORTED, "cannot clone an fp8 cache into bf16");
+  if (quantize && src->y) return set_err(IG_EUNSUPPORTED, "FP8 Y caches are not supported");
   CUDA_TRY(cudaSetDevice(ctx->device));
   ig_cache* c = nullptr;
-  ig_status s = ig_cache_create(ctx, src->n_steps, tier, &c);
+  ig_status s = cache_create_kind(ctx, src->n_steps, tier, quantize ? 1 : src->fp8, src->y, &c);
   if (s != IG_OK) return s;
   cudaError_t e = cudaSuccess;
   if (!quantize) {
@@ -738,7 +759,8 @@ extern "C" ig_status ig_cache_write(ig_ctx* ctx, ig_cache* c, const void* kv, co
   const size_t pl = (size_t)ctx->Limg * ctx->H, spl = (size_t)ctx->Limg * ctx->d.heads;
   for (int s = 0; s < c->n_steps; ++s)
     for (int b = 0; b < ctx->nb; ++b) {
-      const char* src = (const char*)kv + (((size_t)s * ctx->nb + b) * 2) * pl * ctx->esz;
+      const int planes = c->y ? 1 : 2;
+      const char* src = (const char*)kv + (((size_t)s * ctx->nb + b) * planes) * pl * ctx->esz;
       if (c->fp8) {
         launch_kv_quant((const bf16*)src, (const bf16*)(src + pl * ctx->esz), ctx->Limg, ctx->H, ctx->d.heads,
                         ctx->q8rec, ctx->q8rec + pl, ctx->q8rec_scl, ctx->q8rec_scl + spl, st);
@@ -748,7 +770,7 @@ extern "C" ig_status ig_cache_write(ig_ctx* ctx, ig_cache* c, const void* kv, co
         }
         CUDA_TRY(cudaStreamSynchronize(st));
       } else {
-        CUDA_TRY(cudaMemcpyAsync(cache_plane(ctx, c, s, b, 0), src, 2 * pl * ctx->esz, cudaMemcpyDefault, st));
+        CUDA_TRY(cudaMemcpyAsync(cache_plane(ctx, c, s, b, 0), src, planes * pl * ctx->esz, cudaMemcpyDefault, st));
       }
     }
   if (latents)
@@ -800,6 +822,7 @@ struct StepReq {
 struct CopyPlan {
   bool any = false, gather = false, gather_q8 = false;
   int max_nu = 0;
+  int kplan = 0;  // Algorithm-1 dense prefix: Y caches load Y_{b-1} for blocks b > kplan only
 };
 
 static void issue_copy(ig_ctx* ctx, const std::vector<StepReq>& sr, const KvGatherReq* kvg_dev,
@@ -822,6 +845,29 @@ static void issue_copy(ig_ctx* ctx, const std::vector<StepReq>& sr, const KvGath
     const int slot = r->slot;
     const int n_u = ctx->Limg - sr[q].m->n_m;
     long long by = 0;
+    if (c->y) {  // Y variant: the template's Y_{b-1} rows of the unmasked tokens -> V plane rows
+      if (b <= plan.kplan) continue;  // block 0 / first block after the prefix: computed rows
+      const char* src = cache_plane(ctx, c, r->step, b - 1, 0);
+      char* dst = (char*)ctx->kv_arena + ((size_t)slot * ctx->slot_stride + (size_t)buf * ctx->buf_elems) * ctx->esz +
+                  vplane + txt_off;
+      const bool gathered = host ? ctx->o.copy_mode == 2 : ctx->o.copy_mode != 0;
+      if (gathered) {
+        by = (long long)n_u * row;  // SM gather kernel below
+      } else if (ctx->o.copy_mode == 0) {
+        cudaMemcpyAsync(dst, src, (size_t)ctx->Limg * row, cudaMemcpyDefault, ctx->copy_st);
+        by = (long long)ctx->Limg * row;
+      } else {
+        for (auto& run : sr[q].m->runs) {
+          const size_t off = (size_t)run.first * row;
+          dsts.push_back(dst + off);
+          srcs.push_back((void*)(src + off));
+          sizes.push_back((size_t)run.second * row);
+        }
+        by = (long long)n_u * row;
+      }
+      if (host) ctx->stats.h2d_bytes += by; else ctx->stats.d2d_bytes += by;
+      continue;
+    }
     if (c->fp8) {
       by = 2LL * n_u * (ctx->H + 4 * ctx->d.heads);
       if (host) {  // e4m3 runs + whole scale planes -> staging (slot, buf)
@@ -907,34 +953,45 @@ static double block_flops_rows(const ig_ctx* ctx, long long rows) {
 }
 
 static int plan_prefix(ig_ctx* ctx, const std::vector<StepReq>& sr) {
-  long long rows_m = 0, rows_all = 0, bytes = 0;
+  long long rows_m = 0, rows_all = 0, bytes = 0, rows_y = 0;
   for (auto& s : sr) {
     rows_m += ctx->Lt + s.m->n_m;
     rows_all += ctx->Lt + (s.use_cache ? ctx->Limg : s.m->n_m);
     if (s.use_cache) {
       const int n_u = ctx->Limg - s.m->n_m;
-      bytes += s.r->cache->fp8 ? 2LL * n_u * (ctx->H + 4 * ctx->d.heads)
-                               : 2LL * n_u * ctx->H * (long long)ctx->esz;
+      if (s.r->cache->y) {  // one plane; the K/V projection of the unmasked rows is recomputed
+        bytes += (long long)n_u * ctx->H * (long long)ctx->esz;
+        rows_y += n_u;
+      } else {
+        bytes += s.r->cache->fp8 ? 2LL * n_u * (ctx->H + 4 * ctx->d.heads)
+                                 : 2LL * n_u * ctx->H * (long long)ctx->esz;
+      }
     }
   }
-  const double cw = ctx->pm_cs * block_flops_rows(ctx, rows_m) + ctx->pm_cb;
+  const double cw = ctx->pm_cs * (block_flops_rows(ctx, rows_m) + 4.0 * rows_y * ctx->H * ctx->H) + ctx->pm_cb;
   const double cwo = ctx->pm_cs * block_flops_rows(ctx, rows_all) + ctx->pm_cb;
   const double lt = ctx->pm_ls * (double)bytes + ctx->pm_lb;
   const int N = ctx->nb, R = ctx->R;
   int best_k = 0;
   double best = 1e300;
-  std::vector<double> comp_end(N + 1);
+  // Steady state of continuous batching: the copy lane is in order and runs into the next
+  // step as soon as ring buffers free up (buffer b % R is free once the last cached block
+  // that used it finished computing), so the step period is measured over repeated steps.
+  std::vector<double> free_at(R);
   for (int k = 0; k <= N; ++k) {
-    double comp = 0, load = 0;
-    for (int b = 0; b < N; ++b) {
-      if (b < k) { comp += cwo; comp_end[b] = comp; continue; }
-      // ring slot of block b is free once cached block b - R finished computing
-      const double slot_free = (b - R >= k) ? comp_end[b - R] : 0.0;
-      load = std::max(load, slot_free) + lt;
-      comp = std::max(comp, load) + cw;
-      comp_end[b] = comp;
+    std::fill(free_at.begin(), free_at.end(), 0.0);
+    double comp = 0, load = 0, start = 0;
+    for (int rep = 0; rep < 3; ++rep) {
+      start = comp;
+      for (int b = 0; b < N; ++b) {
+        if (b < k) { comp += cwo; continue; }
+        load = std::max(load, free_at[b % R]) + lt;
+        comp = std::max(comp, load) + cw;
+        free_at[b % R] = comp;
+      }
     }
-    if (comp < best - 1e-12) { best = comp; best_k = k; }
+    const double period = comp - start;
+    if (period < best - 1e-12) { best = period; best_k = k; }
   }
   return best_k;
 }
@@ -1009,9 +1066,17 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
     else if (ctx->plan_mode == 2) kplan = plan_prefix(ctx, sr);
   }
   ctx->last_plan_k = kplan;
-  int M_full = M;
-  if (kplan > 0)
-    for (auto& s : sr) if (s.use_cache) M_full += ctx->Limg - s.m->n_m;
+  // unmasked image rows in the row set: Y-cache requests always (their K/V are recomputed from
+  // the replenished block inputs), K/V-cache requests only under a dense prefix.  Y requests'
+  // rows come first, so a cached block's K/V-recompute rows are the one range [M, M_y).
+  int U_y = 0, U_kv = 0;
+  for (auto& s : sr)
+    if (s.use_cache) {
+      if (s.r->cache->y) U_y += ctx->Limg - s.m->n_m;
+      else if (kplan > 0) U_kv += ctx->Limg - s.m->n_m;
+    }
+  const int M_y = M + U_y;
+  const int M_full = M_y + U_kv;
   if (M_full > ctx->o.max_rows) return set_err(IG_ENOMEM, "step needs %d rows > max_rows %d", M_full, ctx->o.max_rows);
   const int M_img = M - M_txt;
   ctx->stats.rows = M;
@@ -1032,7 +1097,7 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
   AttnSeg* dsegf = dseg + 2 * ctx->o.max_batch;
   KvGatherReq* dkvg = (KvGatherReq*)((char*)dseg + 5 * ctx->o.max_batch * sizeof(AttnSeg));
   int nseg = 0, max_q = 0, nsegf = 0, max_qf = 0;
-  int img_row = M_txt, uimg_row = M;
+  int img_row = M_txt, yrow = M, kvrow = M_y;
   for (int q = 0; q < na; ++q) {
     const ig_edit_req* r = sr[q].r;
     ReqDev& d = hreq[q];
@@ -1048,8 +1113,9 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
     d.sigma = r->sigma;
     d.dsig = r->sigma_next - r->sigma;
     d.has_cache = sr[q].use_cache;
-    d.n_ui = (kplan > 0 && sr[q].use_cache) ? ctx->Limg - d.n_m : 0;
-    d.uimg_row0 = uimg_row;
+    const bool ycache = sr[q].use_cache && r->cache->y;
+    d.n_ui = (sr[q].use_cache && (ycache || kplan > 0)) ? ctx->Limg - d.n_m : 0;
+    d.uimg_row0 = ycache ? yrow : kvrow;
     d.tlatent = sr[q].use_cache ? cache_latent_dev(ctx, r->cache, r->step) : nullptr;
     const long long kvb = (long long)r->slot * ctx->slot_stride;
     if (Lt > 0) { hseg[nseg++] = AttnSeg{q * Lt, Lt, kvb}; max_q = std::max(max_q, Lt); }
@@ -1058,16 +1124,17 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
     if (kplan > 0) {
       if (Lt > 0) hsegf[nsegf++] = AttnSeg{q * Lt, Lt, kvb};
       hsegf[nsegf++] = AttnSeg{img_row, d.n_m, kvb};
-      if (d.n_ui > 0) hsegf[nsegf++] = AttnSeg{uimg_row, d.n_ui, kvb};
+      if (d.n_ui > 0) hsegf[nsegf++] = AttnSeg{d.uimg_row0, d.n_ui, kvb};
       max_qf = std::max(max_qf, std::max(Lt, std::max(d.n_m, d.n_ui)));
     }
     img_row += d.n_m;
-    uimg_row += d.n_ui;
+    (ycache ? yrow : kvrow) += d.n_ui;
   }
   // copy-lane plan and per-(block, request) gather descriptors (see issue_copy)
   CopyPlan plan;
   plan.any = any_cache;
   plan.max_nu = max_nu;
+  plan.kplan = kplan;
   KvGatherReq* hkvq = hkvg + (size_t)nb * ctx->o.max_batch;
   KvGatherReq* dkvq = dkvg + (size_t)nb * ctx->o.max_batch;
   if (any_cache) {
@@ -1102,6 +1169,15 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
               gq.srcV = cache_plane_dev(ctx, c, r->step, b, 1);
               gq.sclK = cache_scales_dev(ctx, c, r->step, b, 0);
               gq.sclV = cache_scales_dev(ctx, c, r->step, b, 1);
+            }
+          } else if (c->y) {  // one plane: Y_{b-1} -> V plane (blocks after the first cached one)
+            if ((c->tier == IG_CACHE_DEVICE ? ctx->o.copy_mode != 0 : ctx->o.copy_mode == 2) && b > kplan) {
+              g.srcK = nullptr;
+              g.srcV = cache_plane_dev(ctx, c, r->step, b - 1, 0);
+              g.idx_u = sr[q].m->idx + ctx->Limg;
+              g.n_u = n_u;
+              g.dstK = dst;
+              g.dstV = dst + (size_t)ctx->L * H * es;
             }
           } else if (c->tier == IG_CACHE_DEVICE ? ctx->o.copy_mode != 0 : ctx->o.copy_mode == 2) {
             g.srcK = cache_plane_dev(ctx, c, r->step, b, 0);
@@ -1161,8 +1237,15 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
   }
   }
   stats.kernel_launches += 7;
-  if (rng.X_in) {  // teacher-forced residual rows
+  if (rng.X_in) {  // teacher-forced residual rows (+ img_in of the template rows, if any)
     CUDA_TRY(cudaMemcpyAsync(ctx->X, rng.X_in, (size_t)M * H * 4, cudaMemcpyDeviceToDevice, st));
+    if (M_full > M) {
+      GemmArgs g{};
+      g.A = (const char*)ctx->Ain + (long long)(M - M_txt) * C * es; g.lda = C; g.B = ctx->img_in.w; g.ldb = C;
+      g.bias = ctx->img_in.b; g.C = ctx->X + (long long)M * H; g.ldc = H; g.M = M_full - M; g.N = H; g.K = C;
+      g.epi = EPI_POS; g.ri = ctx->ri; g.ri_off = M; g.pos = ctx->pos_embed; g.pos_ld = H;
+      gemm(ctx, g, st);
+    }
   } else {  // img_in (+ SD3 pos_embed) into the fp32 residual X
     GemmArgs g{};
     g.A = ctx->Ain; g.lda = C; g.B = ctx->img_in.w; g.ldb = C; g.bias = ctx->img_in.b;
@@ -1236,6 +1319,53 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
     e.head_dim = ctx->d.head_dim; e.grid_w = ctx->d.grid_w; e.qk_norm = ctx->d.qk_norm; e.rope = ctx->d.rope;
     gemm(ctx, g, st);
   };
+  // Y variant: K/V of the replenished unmasked rows only (B = rows [H, 3H) of W_qkv / lin1)
+  auto kv_proj = [&](int r0, int r1, const void* W, const void* bias, const void* kg, int buf) {
+    if (r1 <= r0) return;
+    if (!fused_qkv) {  // parity mode: full [q|k|v] GEMM, the Q rows >= M are never read
+      gemm_rows(r0, r1, h, H, W, bias, 3 * H, H, qkv, 3 * H, EPI_STORE, nullptr, 0);
+      qkv_post(r0, r1, kg, kg, buf);
+      return;
+    }
+    GemmArgs g{};
+    g.A = (const char*)h + (long long)r0 * H * es; g.lda = H;
+    g.B = (const char*)W + (long long)H * H * es; g.ldb = H; g.bias = (const char*)bias + (long long)H * es;
+    g.C = ctx->Q; g.ldc = H;
+    g.M = r1 - r0; g.N = 2 * H; g.K = H; g.epi = EPI_QKV;
+    g.ri = ctx->ri; g.ri_off = r0;
+    QkvEpi& e = g.qkv;
+    e.Q = ctx->Q; e.kv_arena = ctx->kv_arena; e.slot_stride = ctx->slot_stride;
+    e.buf_off = (long long)buf * ctx->buf_elems; e.L = ctx->L; e.H = H; e.qg = nullptr; e.kg = kg;
+    e.rope_tab = ctx->rope_tab; e.rope_maxpos = ctx->rope_maxpos;
+    e.ax1_pair = ctx->d.rope_axes[0] / 2; e.ax2_pair = (ctx->d.rope_axes[0] + ctx->d.rope_axes[1]) / 2;
+    e.head_dim = ctx->d.head_dim; e.grid_w = ctx->d.grid_w; e.qk_norm = ctx->d.qk_norm; e.rope = ctx->d.rope;
+    e.col_base = H;
+    gemm(ctx, g, st);
+  };
+  // Y variant: replenish the unmasked rows' block input from the staged Y_{b-1} (V plane)
+  auto y_load = [&](int b, int buf) {
+    if (U_y == 0 || b <= kplan) return;
+    cudaStreamWaitEvent(st, ctx->ev_copy[buf], 0);
+    ProfScope ps(ctx, st, IG_K_ROWS, 0.0, (double)U_y * H * (es + 4));
+    launch_y_load<T>(ctx->kv_arena, ctx->slot_stride, (long long)buf * ctx->buf_elems, ctx->L, H, ctx->ri, ctx->X, M,
+                     M_y, st);
+    stats.kernel_launches++;
+  };
+  // Y recording (template pass): the block output's image rows -> compute dtype -> D2H
+  auto record_y = [&](int b) {
+    if (!record || !record->y) return;
+    const int yb = b % R;
+    const size_t plane = (size_t)ctx->Limg * H * es;
+    char* ys = (char*)ctx->yrec + (size_t)yb * plane;
+    cudaStreamWaitEvent(st, ctx->ev_yrec[yb], 0);  // the D2H of block b - R is done
+    launch_rows_to<T>(ctx->X + (long long)M_txt * H, ys, (long long)ctx->Limg * H, st);
+    stats.kernel_launches++;
+    cudaEventRecord(ctx->ev_comp[yb], st);
+    cudaStreamWaitEvent(ctx->copy_st, ctx->ev_comp[yb], 0);
+    cudaMemcpyAsync(cache_plane(ctx, record, record_step, b, 0), ys, plane, cudaMemcpyDefault, ctx->copy_st);
+    if (record->tier == IG_CACHE_HOST) stats.d2h_bytes += plane; else stats.d2d_bytes += plane;
+    cudaEventRecord(ctx->ev_yrec[yb], ctx->copy_st);
+  };
   auto attn = [&](int buf, bool dense) {
     AttnArgs a{};
     a.Q = ctx->Q; a.ldq = H; a.O = cat; a.ldo = ldcat; a.kv_arena = ctx->kv_arena;
@@ -1248,7 +1378,7 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
   };
   // cache recording (template mode): image-token K/V of ring buffer -> cache[s][b]
   auto record_kv = [&](int b, int buf) {
-    if (!record) return;
+    if (!record || record->y) return;
     cudaEventRecord(ctx->ev_comp[buf], st);
     cudaStreamWaitEvent(ctx->copy_st, ctx->ev_comp[buf], 0);
     const size_t plane = (size_t)ctx->Limg * H * es;
@@ -1293,15 +1423,18 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
   // R, no cache); cached blocks run the masked rows [0, M) with ring buffer b % R.
   for (int b = b0; b < b1; ++b) {
     const bool dense = b < kplan;
-    const int Mc = dense ? M_full : M;
+    const int Mc = dense ? M_full : M;    // rows through every op of the block
+    const int Mk = dense ? M_full : M_y;  // rows through LN-mod and the K/V projection
     const int buf = dense ? R : b % R;
+    if (!dense) y_load(b, buf);
     if (b < ctx->d.n_double) {
       const StreamW& wi = ctx->dimg[b];
       const StreamW& wt = ctx->dtxt[b];
-      ln_mod(M_txt, Mc, wi.mod_t, 0, 1);
+      ln_mod(M_txt, Mk, wi.mod_t, 0, 1);
       if (Lt) ln_mod(0, M_txt, wt.mod_t, wt.pre_only ? 1 : 0, wt.pre_only ? 0 : 1);
       if (!dense) wait_copy(buf);
       qkv_proj(M_txt, Mc, wi.qkv.w, wi.qkv.b, wi.qg, wi.kg, buf);
+      if (!dense) kv_proj(M, M_y, wi.qkv.w, wi.qkv.b, wi.kg, buf);
       if (Lt) qkv_proj(0, M_txt, wt.qkv.w, wt.qkv.b, wt.qg, wt.kg, buf);
       if (!dense) wait_copy_late(buf);
       attn(buf, dense);
@@ -1324,12 +1457,13 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
       }
     } else {
       const SingleW& ws = ctx->sgl[b - ctx->d.n_double];
-      ln_mod(0, Mc, ws.mod_t, 0, 1);
+      ln_mod(0, Mk, ws.mod_t, 0, 1);
       const char* w_u = (const char*)ws.lin1.w + 3LL * H * H * es;
       const char* b_u = (const char*)ws.lin1.b + 3LL * H * es;
       gemm_rows(0, Mc, h, H, w_u, b_u, F, H, cat + H, ldcat, EPI_GELU, nullptr, 0);
       if (!dense) wait_copy(buf);
       qkv_proj(0, Mc, ws.lin1.w, ws.lin1.b, ws.qg, ws.kg, buf);
+      if (!dense) kv_proj(M, M_y, ws.lin1.w, ws.lin1.b, ws.kg, buf);
       if (!dense) wait_copy_late(buf);
       attn(buf, dense);
       record_kv(b, buf);
@@ -1340,6 +1474,7 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
       const long long gs = ctx->mods[ws.mod_t].off;
       gemm_rows(0, Mc, cat, ldcat, ws.lin2.w, ws.lin2.b, H, H + F, ctx->X, H, EPI_GATED_RES, mod + gs + 2 * H, 0);
     }
+    record_y(b);
   }
   if (rng.X_out) {
     CUDA_TRY(cudaMemcpyAsync(rng.X_out, ctx->X, (size_t)M * H * 4, cudaMemcpyDeviceToDevice, st));
@@ -1354,7 +1489,7 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
   CUDA_TRY(cudaEventRecord(ctx->ev_stage[si], st));
   for (auto& s : sr)
     if (s.use_cache) CUDA_TRY(cudaLaunchHostFunc(st, unpin_cb, (void*)s.r->cache));
-  if (record) CUDA_TRY(cudaStreamWaitEvent(st, ctx->ev_copy[(b1 - 1) % R], 0));
+  if (record) CUDA_TRY(cudaStreamWaitEvent(st, record->y ? ctx->ev_yrec[(b1 - 1) % R] : ctx->ev_copy[(b1 - 1) % R], 0));
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_err(IG_ECUDA, "step enqueue: %s", cudaGetErrorString(e));
   return IG_OK;
@@ -1443,7 +1578,8 @@ extern "C" ig_status ig_prefetch_layer(ig_ctx* ctx, const ig_edit_req* r, int la
   if (!r->cache) return set_err(IG_ECACHE_MISS, "no cache");
   if (!desc_equal(r->cache->desc, ctx->d)) return set_err(IG_ECACHE_INCOMPAT, "cache built for another model");
   if (r->step < 0 || r->step >= r->cache->n_steps) return set_err(IG_ECACHE_INCOMPAT, "step out of range");
-  if (ctx->o.copy_mode != 0 || r->cache->fp8) return set_err(IG_EUNSUPPORTED, "explicit prefetch needs copy_mode 0 and a bf16 cache");
+  if (ctx->o.copy_mode != 0 || r->cache->fp8 || r->cache->y)
+    return set_err(IG_EUNSUPPORTED, "explicit prefetch needs copy_mode 0 and a bf16 K/V cache");
   CUDA_TRY(cudaSetDevice(ctx->device));
   const int buf = layer % ctx->R;
   const size_t es = ctx->esz, H = ctx->H;

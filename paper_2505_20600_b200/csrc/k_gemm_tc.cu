@@ -176,8 +176,9 @@ __device__ __forceinline__ void epilogue_qkv_head(const GemmArgs& g, int row, in
       for (int t = 0; t < 8; ++t) v[q * 8 + t] += __bfloat162float(hb[t]);
     }
   }
-  const int which = (int)(col0 / e.H);          // 0 q, 1 k, 2 v
-  const int hcol = (int)(col0 - which * e.H);   // column inside the hidden dim
+  const int cq = col0 + e.col_base;             // column in [q|k|v] (col_base = H: K/V only)
+  const int which = (int)(cq / e.H);            // 0 q, 1 k, 2 v
+  const int hcol = (int)(cq - which * e.H);     // column inside the hidden dim
   bf16* dst;
   if (which == 0) {
     dst = reinterpret_cast<bf16*>(e.Q) + (long long)(g.ri_off + row) * e.H + hcol;
@@ -578,7 +579,7 @@ bool gemm_tc_supported(const GemmArgs& g) {
     if (g.epi == EPI_GATED_RES && (!al16(g.gate) || (g.gate_ld & 3))) return false;
   }
   if (g.bias && !al16(g.bias)) return false;
-  if (g.epi == EPI_QKV && ((g.qkv.head_dim != 128 && g.qkv.head_dim != 64) || (g.qkv.H % 256) || g.N != 3 * g.qkv.H))
+  if (g.epi == EPI_QKV && ((g.qkv.head_dim != 128 && g.qkv.head_dim != 64) || (g.qkv.H % 256) || g.N + g.qkv.col_base != 3 * g.qkv.H))
     return false;
   return true;
 }

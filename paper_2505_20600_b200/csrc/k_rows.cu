@@ -95,10 +95,10 @@ __global__ void build_rows_kernel(const ReqDev* __restrict__ reqs, int n, int L_
     const T* src = reinterpret_cast<const T*>(R.txt) + (long long)t * H;
     float* dst = X + (long long)r * H;
     for (int c = lane; c < H; c += 32) dst[c] = to_f<T>(src[c]);
-  } else if (r >= M) {  // included unmasked rows (dense prefix) from the template latent
+  } else if (r >= M) {  // included unmasked rows (dense prefix / Y variant): template latent
     int q = 0;
-    for (int i = 0; i < n; ++i)
-      if (reqs[i].n_ui > 0 && reqs[i].uimg_row0 <= r) q = i;  // request-major, n <= 16
+    for (int i = 0; i < n; ++i)  // n <= max_batch; regions are disjoint but not request-ordered
+      if (reqs[i].n_ui > 0 && reqs[i].uimg_row0 <= r && r < reqs[i].uimg_row0 + reqs[i].n_ui) q = i;
     const ReqDev& R = reqs[q];
     const int j = r - R.uimg_row0;
     const int tok = R.idx_u[j];
@@ -225,7 +225,9 @@ __global__ void __launch_bounds__(256) kv_gather_kernel(const KvGatherReq* __res
     const KvGatherReq& R = reqs[q];
     if (j >= R.n_u) continue;
     const int tok = R.idx_u[j];
-    const int4* s4 = reinterpret_cast<const int4*>((const char*)(which ? R.srcV : R.srcK) + (long long)tok * row_bytes);
+    const char* src = (const char*)(which ? R.srcV : R.srcK);
+    if (!src) continue;  // Y-variant caches fill one plane only
+    const int4* s4 = reinterpret_cast<const int4*>(src + (long long)tok * row_bytes);
     int4* d4 = reinterpret_cast<int4*>((char*)(which ? R.dstV : R.dstK) + (long long)(L_txt + tok) * row_bytes);
     int v = lane;
     for (; v + 96 < nvec; v += 128) {
@@ -246,6 +248,67 @@ void launch_kv_gather(const KvGatherReq* reqs_dev, int n, int max_nu, int L_txt,
   const long long blocks = (warps * 32 + threads - 1) / threads;
   kv_gather_kernel<<<(unsigned)blocks, threads, 0, st>>>(reqs_dev, n, max_nu, L_txt, H * elem_bytes);
 }
+
+// ======================================================================================
+// Y variant (fig:transformer-Bottom): the unmasked rows of a block's
+// input are replenished from the staged cache rows.  The copy lane lands the template's
+// Y_{b-1} rows of the unmasked tokens positionally in the V plane of the ring buffer (it is
+// overwritten by this block's fresh V only after this kernel ran, stream order); this kernel
+// widens them into the fp32 residual rows [r0, r1).  One warp per row, 16-byte loads.
+// ======================================================================================
+template <typename T>
+__global__ void __launch_bounds__(256) y_load_kernel(const T* __restrict__ arena, long long slot_stride,
+                                                     long long buf_off, long long L, int H,
+                                                     const RowInfo* __restrict__ ri, float* __restrict__ X,
+                                                     int r0, int r1) {
+  const int r = r0 + (int)(((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
+  if (r >= r1) return;
+  const RowInfo info = ri[r];
+  const T* src = arena + info.slot * slot_stride + buf_off + L * H + (long long)info.kvpos * H;
+  float* dst = X + (long long)r * H;
+  constexpr int V = 16 / sizeof(T);
+  for (int c = lane * V; c < H; c += 32 * V) {
+    const uint4 raw = __ldcs(reinterpret_cast<const uint4*>(src + c));
+    const T* e = reinterpret_cast<const T*>(&raw);
+#pragma unroll
+    for (int t = 0; t < V; t += 4)
+      *reinterpret_cast<float4*>(dst + c + t) = make_float4(to_f<T>(e[t]), to_f<T>(e[t + 1]), to_f<T>(e[t + 2]),
+                                                            to_f<T>(e[t + 3]));
+  }
+}
+
+template <typename T>
+void launch_y_load(const void* arena, long long slot_stride, long long buf_off, long long L, int H, const RowInfo* ri,
+                   float* X, int r0, int r1, cudaStream_t st) {
+  if (r1 <= r0) return;
+  const long long threads = (long long)(r1 - r0) * 32;
+  y_load_kernel<T><<<(unsigned)((threads + 255) / 256), 256, 0, st>>>((const T*)arena, slot_stride, buf_off, L, H, ri,
+                                                                      X, r0, r1);
+}
+template void launch_y_load<float>(const void*, long long, long long, long long, int, const RowInfo*, float*, int, int,
+                                   cudaStream_t);
+template void launch_y_load<bf16>(const void*, long long, long long, long long, int, const RowInfo*, float*, int, int,
+                                  cudaStream_t);
+
+// Y recording: fp32 residual rows -> cache dtype (round-to-nearest-even for bf16, C-AMB 18)
+template <typename T>
+__global__ void rows_to_kernel(const float* __restrict__ src, T* __restrict__ dst, long long n4) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n4) return;
+  const float4 v = reinterpret_cast<const float4*>(src)[i];
+  T* d = dst + 4 * i;
+  d[0] = from_f<T>(v.x); d[1] = from_f<T>(v.y); d[2] = from_f<T>(v.z); d[3] = from_f<T>(v.w);
+}
+
+template <typename T>
+void launch_rows_to(const float* src, void* dst, long long n, cudaStream_t st) {
+  const long long n4 = n / 4;
+  if (n4 <= 0) return;
+  rows_to_kernel<T><<<(unsigned)((n4 + 255) / 256), 256, 0, st>>>(src, (T*)dst, n4);
+}
+template void launch_rows_to<float>(const float*, void*, long long, cudaStream_t);
+template void launch_rows_to<bf16>(const float*, void*, long long, cudaStream_t);
 
 // ======================================================================================
 // FP8 (e4m3) K/V cache.  Quantize: per (token, head) scale = amax / 448 (fp32),

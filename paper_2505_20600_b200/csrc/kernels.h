@@ -97,6 +97,16 @@ void launch_kv_gather_q8(const KvGatherReq* reqs_dev, int n, int max_nu, int L_t
 void launch_kv_gather(const KvGatherReq* reqs_dev, int n, int max_nu, int L_txt, int H,
                       int elem_bytes, cudaStream_t st);
 
+// ---- Y variant (k_rows.cu) ------------------------------------------------------
+// X[r] (fp32) = staged Y row of (ri[r].slot, ring buffer at buf_off, position ri[r].kvpos) in
+// the V plane, rows [r0, r1)
+template <typename T>
+void launch_y_load(const void* arena, long long slot_stride, long long buf_off, long long L, int H, const RowInfo* ri,
+                   float* X, int r0, int r1, cudaStream_t st);
+// dst[i] = T(src[i]), n a multiple of 4
+template <typename T>
+void launch_rows_to(const float* src, void* dst, long long n, cudaStream_t st);
+
 // ---- a11 exit: Euler scatter (k_rows.cu) ------------------------------------------------
 // latent_req[idx_m[j]][c] += dsig_req * v[img_row][c]
 void launch_scatter_euler(const ReqDev* reqs, int n, int M_img, const RowInfo* ri, int M_txt,
@@ -121,6 +131,7 @@ struct QkvEpi {
   const float2* rope_tab;           // [d/2][rope_maxpos] (cos, sin) or null
   int rope_maxpos, ax1_pair, ax2_pair;
   int head_dim, grid_w, qk_norm, rope;
+  int col_base;                     // first output column's offset in [q|k|v] (H: K/V only)
 };
 struct GemmArgs {
   const void* A; long long lda;   // [M, K] row-major

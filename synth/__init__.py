@@ -232,6 +232,13 @@ def make_cache_kv(d: ModelDesc, template: int, n_steps: int, dtype=torch.float32
     return normal(1000 + template, "cache_kv", shape, device).to(torch.float32).to(dtype)
 
 
+def make_cache_y(d: ModelDesc, template: int, n_steps: int, dtype=torch.float32, device="cpu"):
+    """A synthetic Y-variant template cache [steps][blocks][L_img][H] (block outputs of the
+    image tokens), for testing the edit step independently of cache recording."""
+    shape = (n_steps, d.n_blocks, d.L_img, d.hidden)
+    return normal(2000 + template, "cache_y", shape, device).to(torch.float32).to(dtype)
+
+
 def flow_sigmas(n_steps: int, shift: float = 3.0) -> np.ndarray:
     """Shift-3 flow schedule on linspace(1, 0, n+1) [proposal, SURVEY §8(d) config 3]."""
     s = np.linspace(1.0, 0.0, n_steps + 1)

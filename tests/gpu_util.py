@@ -67,10 +67,11 @@ class Request:
         ig.ig_mask_free(self.mask)
 
 
-def cache_to_numpy(cache, d, n_steps, dtype):
+def cache_to_numpy(cache, d, n_steps, dtype, y=False):
+    """Host-tier cache readback: K/V [steps, blocks, 2, L_img, H] (or Y [steps, blocks, L_img, H])."""
     ptr, nbytes, tier = ig.ig_cache_storage(cache)
-    nbytes = n_steps * d.n_blocks * 2 * d.L_img * d.hidden * (4 if dtype == ig.IG_F32 else 2)  # K/V region
-    shape = (n_steps, d.n_blocks, 2, d.L_img, d.hidden)
+    shape = (n_steps, d.n_blocks) + (() if y else (2,)) + (d.L_img, d.hidden)
+    nbytes = int(np.prod(shape)) * (4 if dtype == ig.IG_F32 else 2)  # K/V (Y) region
     assert tier == ig.IG_CACHE_HOST, 'host-tier readback only'
     import ctypes
     buf = (ctypes.c_char * nbytes).from_address(ptr)

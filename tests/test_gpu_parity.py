@@ -342,3 +342,126 @@ def test_algorithm1_model_plan_extremes():
     ig.ig_cache_free(cache)
     r.free()
     m.close()
+
+
+# ------------------------------------------------------------------ Y variant (N2)
+@pytest.mark.parametrize("dtype", [ig.IG_F32, ig.IG_BF16])
+@pytest.mark.parametrize("copy_mode,tier", [(0, ig.IG_CACHE_HOST), (1, ig.IG_CACHE_HOST), (2, ig.IG_CACHE_HOST),
+                                            (1, ig.IG_CACHE_DEVICE)])
+def test_y_cache_mixed_batch_end_to_end(dtype, copy_mode, tier):
+    """Y-caching variant (fig:transformer-Bottom): a continuous batch mixing two
+    Y-cache requests, one K/V-cache request and an all-ones request, 2 steps, vs the oracle's
+    edit_step_y / edit_step request by request (synthetic caches shared by both sides)."""
+    d = synth.FLUX_SMALL
+    sig = [1.0, 0.7, 0.4]
+    tdt = torch.float32 if dtype == ig.IG_F32 else torch.bfloat16
+    m = Model(d, dtype, opts=ig.ig_ctx_opts(4, 0, 2, copy_mode, 0, 0, 1))
+    W = m.host_weights()
+    rng = np.random.default_rng(11)
+    masks = [synth.blob_mask_count(d, 90, rng), synth.rect_mask_count(d, 40, rng),
+             synth.blob_mask_count(d, 60, rng), np.ones(d.L_img, np.uint8)]
+    reqs = [Request(m, 110 + i, mk) for i, mk in enumerate(masks)]
+    yv = synth.make_cache_y(d, 5, 2, dtype=tdt)
+    tlat = torch.stack([synth.make_latent(d, 950 + s) for s in range(2)])
+    ycache = ig.ig_cache_create(m.ctx, 2, ig.IG_CACHE_HOST)  # cache_y ctx -> Y cache
+    fill_cache(m, ycache, yv, tlat)
+    if tier == ig.IG_CACHE_DEVICE:
+        dc = ig.ig_cache_clone(m.ctx, ycache, ig.IG_CACHE_DEVICE)
+        ig.ig_cache_free(ycache)
+        ycache = dc
+    mk = Model(d, dtype, opts=ig.ig_ctx_opts(4, 0, 2, copy_mode, 0, 0, 0))  # same weights, K/V caches
+    kv = synth.make_cache_kv(d, 6, 2, dtype=tdt)
+    kvcache = ig.ig_cache_create(mk.ctx, 2, tier)
+    fill_cache(mk, kvcache, kv)
+    caches = [ycache, ycache, kvcache, None]
+    for s in range(2):
+        rr = [r.req(i, caches[i], s, sig[s], sig[s + 1]) for i, r in enumerate(reqs)]
+        ig.ig_edit_step(m.ctx, rr, 0)
+    torch.cuda.synchronize()
+    st = ig.ig_last_stats(m.ctx)
+    n_u = [d.L_img - int(mk_.sum()) for mk_ in masks]
+    es = 4 if dtype == ig.IG_F32 else 2
+    if copy_mode != 0:  # compacted: one plane per Y request (blocks 1..N-1), two per K/V request
+        exp = ((d.n_blocks - 1) * (n_u[0] + n_u[1]) + 2 * d.n_blocks * n_u[2]) * d.hidden * es
+        assert st["h2d_bytes"] + st["d2d_bytes"] == exp
+    yh, kvh, tlh = yv.double().numpy(), kv.double().numpy(), tlat.double().numpy()
+    for i, r in enumerate(reqs):
+        lat0, txt, cond = r.host_inputs()
+        x = lat0
+        for s in range(2):
+            if i < 2:
+                x = oracle.edit_step_y(d, W, x, r.mask_np, yh[s], tlh[s], sig[s], sig[s + 1], txt, cond)
+            else:
+                x = oracle.edit_step(d, W, x, r.mask_np, kvh[s] if i == 2 else None, sig[s], sig[s + 1], txt, cond)
+        got = r.latent.double().cpu().numpy()
+        ok, worst = ctol(got, x, RTOL[dtype])
+        assert ok, (i, worst)
+        assert np.array_equal(got[r.mask_np == 0], lat0[r.mask_np == 0])
+    ig.ig_cache_free(ycache)
+    ig.ig_cache_free(kvcache)
+    for r in reqs:
+        r.free()
+    mk.close()
+    m.close()
+
+
+@pytest.mark.parametrize("dtype", [ig.IG_F32, ig.IG_BF16])
+@pytest.mark.parametrize("model", ["tiny", "flux_small"])
+def test_y_cache_template_recording(dtype, model):
+    """ig_cache_template on a cache_y ctx records every (step, block) image-token block output
+    (the Y of fig:transformer): vs the oracle's dense pass (cache_template_y), 2 steps; then a
+    2-step edit on that recorded cache along the template trajectory stays on it."""
+    d = synth.TINY if model == "tiny" else synth.FLUX_SMALL
+    sig = [1.0, 0.5, 0.0]
+    m = Model(d, dtype, opts=ig.ig_ctx_opts(2, 0, 2, 1, 0, 0, 1))
+    W = m.host_weights()
+    rq = Request(m, 3, synth.tiny_rect_mask() if model == "tiny" else synth.blob_mask_count(d, 64, np.random.default_rng(3)))
+    lat0, txt, cond = rq.host_inputs()
+    lat_t = rq.latent.clone()
+    cache = ig.ig_cache_template(m.ctx, lat_t.data_ptr(), rq.txt.data_ptr() if d.txt_len else 0,
+                                 rq.cond.data_ptr(), sig)
+    _, oy, traj = oracle.cache_template_y(d, W, lat0, txt, cond, sig)
+    g = cache_to_numpy(cache, d, 2, dtype, y=True)
+    ok, worst = ctol(g, oy, RTOL[dtype])
+    assert ok, ("Y cache", worst)
+    _run_edit(m, [rq], cache, 2, sig)
+    got = rq.latent.double().cpu().numpy()
+    idx = rq.mask_np != 0
+    ok, worst = ctol(got[idx], traj[-1][idx], RTOL[dtype])
+    assert ok, ("edit on the recorded Y cache", worst)
+    ig.ig_cache_free(cache)
+    rq.free()
+    m.close()
+
+
+@pytest.mark.parametrize("k", [1, 3])
+def test_y_cache_dense_prefix_end_to_end(k):
+    """Algorithm-1 prefix under the Y variant: block k takes the prefix's computed unmasked
+    rows, later blocks replenish from Y_{b-1}; vs oracle edit_step_y(k=)."""
+    d = synth.FLUX_SMALL
+    sig = [1.0, 0.7, 0.4]
+    m = Model(d, ig.IG_BF16, opts=ig.ig_ctx_opts(4, 0, 4, 1, 0, 0, 1))
+    ig.ig_set_plan(m.ctx, 1, k)
+    W = m.host_weights()
+    rng = np.random.default_rng(12)
+    masks = [synth.blob_mask_count(d, 70, rng), synth.rect_mask_count(d, 35, rng)]
+    reqs = [Request(m, 130 + i, mk) for i, mk in enumerate(masks)]
+    yv = synth.make_cache_y(d, 7, 2, dtype=torch.bfloat16)
+    tlat = torch.stack([synth.make_latent(d, 960 + s) for s in range(2)])
+    cache = ig.ig_cache_create(m.ctx, 2, ig.IG_CACHE_HOST)
+    fill_cache(m, cache, yv, tlat)
+    _run_edit(m, reqs, cache, 2, sig)
+    assert ig.ig_last_plan(m.ctx) == k
+    yh, tlh = yv.double().numpy(), tlat.double().numpy()
+    for r in reqs:
+        lat0, txt, cond = r.host_inputs()
+        x = lat0
+        for s in range(2):
+            x = oracle.edit_step_y(d, W, x, r.mask_np, yh[s], tlh[s], sig[s], sig[s + 1], txt, cond, k=k)
+        got = r.latent.double().cpu().numpy()
+        ok, worst = ctol(got, x, 2e-2)
+        assert ok, worst
+    ig.ig_cache_free(cache)
+    for r in reqs:
+        r.free()
+    m.close()
