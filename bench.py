@@ -176,11 +176,12 @@ def run_loop(ig, ctx, batch, cache, sig, steps, stream, profile=False, e2e=None)
     for _ in range(steps):
         e0 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        if e2e is not None:  # public-API end to end: host latents in, results out
-            for r in batch.slots:
-                hb = e2e[r.rid]
-                r.latent.copy_(hb, non_blocking=True)
-                h2d += hb.numel() * 4
+        if e2e is not None:  # public-API end to end: host latents in, results out (on `stream`)
+            with torch.cuda.stream(stream):
+                for r in batch.slots:
+                    hb = e2e[r.rid]
+                    r.latent.copy_(hb, non_blocking=True)
+                    h2d += hb.numel() * 4
         ig.ig_edit_step(ctx, batch.reqs(cache, sig), stream.cuda_stream)
         plans.append(ig.ig_last_plan(ctx))
         alg_flops += sum(N_BLOCKS_FLOPS(batch.d, r.n_m) for r in batch.slots)
@@ -188,10 +189,11 @@ def run_loop(ig, ctx, batch, cache, sig, steps, stream, profile=False, e2e=None)
         launches += st["kernel_launches"]
         h2d += st["h2d_bytes"]
         if e2e is not None:
-            for r in batch.slots:
-                hb = e2e[r.rid]
-                hb.copy_(r.latent, non_blocking=True)
-                d2h += hb.numel() * 4
+            with torch.cuda.stream(stream):
+                for r in batch.slots:
+                    hb = e2e[r.rid]
+                    hb.copy_(r.latent, non_blocking=True)
+                    d2h += hb.numel() * 4
         e1 = torch.cuda.Event(enable_timing=True)
         e1.record(stream)
         evs.append((e0, e1))
@@ -336,6 +338,7 @@ def main():
     ap.add_argument("--model", default="flux1_dev")
     ap.add_argument("--no-hbm-tier", action="store_true", help="skip the HBM-resident template run")
     ap.add_argument("--no-fp8", action="store_true", help="skip the FP8-cache run")
+    ap.add_argument("--no-y", action="store_true", help="skip the Y-cache run")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -415,7 +418,8 @@ def main():
                 "plan_k": {"min": min(lg.plans), "max": max(lg.plans),
                            "mean": round(float(np.mean(lg.plans)), 2)},
                 "alg_tensor_frac": round(lg.alg_flops / (lg.ms * 1e-3) / 1e12 / pk_sus, 4),
-                "kernel_share_of_step": {k: round(v["ms"] / lg.ms, 4) for k, v in lg.prof.items()}}
+                "copy_lane_busy": round(lg.prof["copy"]["ms"] / lg.ms, 4),
+                "kernel_share_of_step": {k: round(v["ms"] / lg.ms, 4) for k, v in lg.prof.items() if k != "copy"}}
 
     # Algorithm-1 latency models fitted on this GPU, then the headline: the
     # mask-aware step with the per-step dense-prefix plan (N1), cache in pinned host memory
@@ -463,6 +467,21 @@ def main():
         ig.ig_cache_free(cache8)
         ig.ig_ctx_destroy(ctx8)
 
+    # Y-caching variant (the paper's primary form, fig:transformer-Bottom): a context
+    # whose template cache holds block outputs (half the bytes); same request sequence, host tier
+    ycache_leg = None
+    if tier == "host" and not args.no_y and world == 1:
+        optsy = ig.ig_ctx_opts(args.max_batch, args.max_batch * d.L, args.depth, args.copy_mode, 0, 0, 1)
+        ctxy = ig.ig_ctx_create(ig.make_desc(d, ig.IG_BF16), ptrs, local, optsy)
+        tl = synth.make_latent(d, 10 ** 6, dev)
+        cachey = ig.ig_cache_template(ctxy, tl.data_ptr(), tt.data_ptr(), tc.data_ptr(), sig, ig.IG_CACHE_HOST, 0)
+        ig.ig_set_plan(ctxy, plan_mode, 0 if plan_mode != 1 else int(args.plan), a_c, b_c, a_l, b_l)
+        ycache_leg = summary(leg(ctxy, cachey))
+        ycache_leg["note"] = ("same workload, Y cache (block outputs of the unmasked tokens, one plane per block; "
+                              "their K/V recomputed on the GPU)")
+        ig.ig_cache_free(cachey)
+        ig.ig_ctx_destroy(ctxy)
+
     # dense comparison step (all-ones masks, no cache) on the same GPUs and kernels
     dense = None
     if args.dense_steps > 0:
@@ -486,7 +505,7 @@ def main():
     attn_tf = main_leg.tflops("attn")
     exec_flops = prof["gemm"]["flops"] + prof["attn"]["flops"]
     step_ms = ms / args.steps
-    shares = {k: round(v["ms"] / args.steps / step_ms, 4) for k, v in prof.items()}
+    shares = {k: round(v["ms"] / args.steps / step_ms, 4) for k, v in prof.items() if k != "copy"}
     out = {
         "metric": METRIC, "value": round(value, 4), "unit": "images/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 3),
@@ -526,9 +545,13 @@ def main():
         "speedup_vs_dense": round(value / dense, 3) if dense else None,
         "host_link": {"achieved_GBps": round(h2d / (ms * 1e-3) / 1e9, 2), "peak_GBps": link_peak,
                       "frac": round(h2d / (ms * 1e-3) / 1e9 / link_peak, 4) if link_peak else None,
-                      "peak_kind": "pinned H2D cudaMemcpyAsync 512 MiB x8, measured in this run"},
+                      "peak_kind": "pinned H2D cudaMemcpyAsync 512 MiB x8, measured in this run",
+                      "copy_lane_busy": round(prof["copy"]["ms"] / ms, 4),
+                      "GBps_while_busy": round(prof["copy"]["bytes"] / (prof["copy"]["ms"] * 1e-3) / 1e9, 2)
+                      if prof["copy"]["ms"] else None},
         "hbm_tier": hbm,
         "fp8_cache_host_tier": fp8,
+        "y_cache_host_tier": ycache_leg,
         "speedup_hbm_tier_vs_dense": round(hbm["value"] / dense, 3) if (hbm and dense) else None,
         "gpu_launches": int(launches),
         "clocks": clk,

@@ -230,7 +230,9 @@ ig_status ig_last_stats(const ig_ctx* ctx, ig_stats* out);
  * per-class totals accumulated since the last read, and resets them. */
 typedef enum {
   IG_K_GEMM = 0, IG_K_ATTN = 1, IG_K_LNMOD = 2, IG_K_QKVPOST = 3, IG_K_COND = 4,
-  IG_K_ROWS = 5, IG_K_NCLASS = 6
+  IG_K_ROWS = 5,
+  IG_K_COPY = 6,  /* copy lane (a7): one entry per block's cache copy, timed on the copy stream */
+  IG_K_NCLASS = 7
 } ig_kernel_class;
 typedef struct {
   long long launches;

@@ -1,6 +1,7 @@
 // k_rows.cu — kernels (a) index build and (b) row gather / positional K/V merge / scatter.
 // All of these are exact copies or integer work (bit-exact, SURVEY §8(c) C-PIN) except the
 // QK-norm/RoPE epilogue, which is token-wise fp arithmetic.
+#include <algorithm>
 #include <cuda_fp8.h>
 #include "kernels.h"
 
@@ -247,6 +248,25 @@ void launch_kv_gather(const KvGatherReq* reqs_dev, int n, int max_nu, int L_txt,
   // SMs the persistent GEMMs need (measured: 24-CTA grid cut the HBM-tier step rate by 10%)
   const long long blocks = (warps * 32 + threads - 1) / threads;
   kv_gather_kernel<<<(unsigned)blocks, threads, 0, st>>>(reqs_dev, n, max_nu, L_txt, H * elem_bytes);
+}
+
+// ======================================================================================
+// Small host->device transfers by SM loads from mapped pinned memory (per-step descriptors):
+// never queued behind the copy engines' cache prefetch.  bytes % 16 == 0 not required.
+// ======================================================================================
+__global__ void copy_bytes_kernel(char* __restrict__ dst, const char* __restrict__ src, size_t n) {
+  const size_t n16 = n / 16;
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n16; i += stride)
+    reinterpret_cast<uint4*>(dst)[i] = reinterpret_cast<const uint4*>(src)[i];
+  for (size_t i = n16 * 16 + (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) dst[i] = src[i];
+}
+
+void launch_copy_bytes(void* dst, const void* src, size_t n, cudaStream_t st) {
+  if (n == 0) return;
+  const size_t n16 = (n + 15) / 16;
+  const unsigned blocks = (unsigned)std::min<size_t>((n16 + 255) / 256, 16);
+  copy_bytes_kernel<<<blocks, 256, 0, st>>>((char*)dst, (const char*)src, n);
 }
 
 // ======================================================================================

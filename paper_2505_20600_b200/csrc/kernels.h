@@ -97,6 +97,9 @@ void launch_kv_gather_q8(const KvGatherReq* reqs_dev, int n, int max_nu, int L_t
 void launch_kv_gather(const KvGatherReq* reqs_dev, int n, int max_nu, int L_txt, int H,
                       int elem_bytes, cudaStream_t st);
 
+// dst[0, n) = src[0, n) by SM loads (src may be mapped pinned host memory), 16-byte vectors
+void launch_copy_bytes(void* dst, const void* src, size_t n, cudaStream_t st);
+
 // ---- Y variant (k_rows.cu) ------------------------------------------------------
 // X[r] (fp32) = staged Y row of (ri[r].slot, ring buffer at buf_off, position ri[r].kvpos) in
 // the V plane, rows [r0, r1)

@@ -26,7 +26,7 @@ EXPORTS = ["ig_weight_count", "ig_ctx_create", "ig_ctx_destroy", "ig_cache_creat
            "ig_last_error", "ig_last_stats", "ig_op_gemm", "ig_op_gemm_gated", "ig_op_attention", "ig_copy",
            "ig_profile_enable", "ig_profile_read", "ig_debug_block", "ig_cache_clone", "ig_cache_write",
            "ig_set_plan", "ig_last_plan"]
-KCLASS = ["gemm", "attn", "lnmod", "qkvpost", "cond", "rows"]
+KCLASS = ["gemm", "attn", "lnmod", "qkvpost", "cond", "rows", "copy"]
 
 
 class IgError(RuntimeError):
