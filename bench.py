@@ -113,13 +113,26 @@ def measure_h2d(dev):
     return round(bw, 2)
 
 
+MASKS = {"lo": 0.05, "hi": 0.60, "kind": "mixed"}
+
+
+def make_mask(d, rid):
+    """Per-request token mask: m ~ U[lo, hi], n_m = round(m L_img); the headline mix alternates
+    rectangles and blobs (synth.mixed_mask); 'blob' = random-blob masks only (SD3 config 2)."""
+    if MASKS["kind"] == "blob":
+        rng = np.random.default_rng(7919 * rid + 17)
+        n = int(round(rng.uniform(MASKS["lo"], MASKS["hi"]) * d.L_img))
+        return synth.blob_mask_count(d, n, rng)
+    return synth.mixed_mask(d, rid, MASKS["lo"], MASKS["hi"])
+
+
 class Req:
     def __init__(self, ig, ctx, d, rid, dev, dense=False):
         self.rid = rid
         self.latent = synth.make_latent(d, rid, dev).contiguous()
         self.txt = synth.make_txt(d, rid, dev, torch.bfloat16).contiguous()
         self.cond = synth.make_cond(d, rid, dev).contiguous()
-        mk = np.ones(d.L_img, np.uint8) if dense else synth.mixed_mask(d, rid)
+        mk = np.ones(d.L_img, np.uint8) if dense else make_mask(d, rid)
         self.mask_np = mk
         self.mask_dev = torch.from_numpy(mk).to(dev)
         self.mask, self.n_m = ig.ig_mask_build(ctx, self.mask_dev.data_ptr(), 0)  # admission
@@ -146,8 +159,9 @@ class Batch:
         r.step = 0
         return r
 
-    def reqs(self, cache, sig):
-        return [self.ig.make_req(i, r.latent.data_ptr(), r.mask, cache, r.step, float(sig[r.step]),
+    def reqs(self, cache, sig, host=None):
+        return [self.ig.make_req(i, (host[r.rid] if host else r.latent).data_ptr(), r.mask, cache, r.step,
+                                 float(sig[r.step]),
                                  float(sig[r.step + 1]), r.txt.data_ptr(), r.cond.data_ptr())
                 for i, r in enumerate(self.slots)]
 
@@ -176,24 +190,19 @@ def run_loop(ig, ctx, batch, cache, sig, steps, stream, profile=False, e2e=None)
     for _ in range(steps):
         e0 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        if e2e is not None:  # public-API end to end: host latents in, results out (on `stream`)
-            with torch.cuda.stream(stream):
-                for r in batch.slots:
-                    hb = e2e[r.rid]
-                    r.latent.copy_(hb, non_blocking=True)
-                    h2d += hb.numel() * 4
-        ig.ig_edit_step(ctx, batch.reqs(cache, sig), stream.cuda_stream)
+        # e2e: the public API on HOST buffers — each request's latent lives in pinned host memory
+        # and the step's gather/scatter kernels read its masked rows and write the updated rows
+        # in place over the host link (no device copy of the latent exists)
+        ig.ig_edit_step(ctx, batch.reqs(cache, sig, e2e), stream.cuda_stream)
         plans.append(ig.ig_last_plan(ctx))
         alg_flops += sum(N_BLOCKS_FLOPS(batch.d, r.n_m) for r in batch.slots)
         st = ig.ig_last_stats(ctx)
         launches += st["kernel_launches"]
         h2d += st["h2d_bytes"]
         if e2e is not None:
-            with torch.cuda.stream(stream):
-                for r in batch.slots:
-                    hb = e2e[r.rid]
-                    hb.copy_(r.latent, non_blocking=True)
-                    d2h += hb.numel() * 4
+            rows = sum(r.n_m for r in batch.slots) * batch.d.lat_ch * 4
+            h2d += 2 * rows  # masked latent rows read by the gather and by the Euler update
+            d2h += rows      # updated masked rows written back
         e1 = torch.cuda.Event(enable_timing=True)
         e1.record(stream)
         evs.append((e0, e1))
@@ -339,7 +348,11 @@ def main():
     ap.add_argument("--no-hbm-tier", action="store_true", help="skip the HBM-resident template run")
     ap.add_argument("--no-fp8", action="store_true", help="skip the FP8-cache run")
     ap.add_argument("--no-y", action="store_true", help="skip the Y-cache run")
+    ap.add_argument("--mask-lo", type=float, default=0.05)
+    ap.add_argument("--mask-hi", type=float, default=0.60)
+    ap.add_argument("--mask-kind", default="mixed", choices=["mixed", "blob"])
     args = ap.parse_args()
+    MASKS.update(lo=args.mask_lo, hi=args.mask_hi, kind=args.mask_kind)
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -511,10 +524,10 @@ def main():
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic",
-        "config": {"workload": f"{d.name} 1024^2 (4096 img + 512 txt tokens), 28-step flow schedule, "
-                               f"continuous batching max_batch {args.max_batch}, masks m~U[0.05,0.60] "
-                               f"(rect/blob), K/V cache tier={tier} copy_mode={args.copy_mode} depth={args.depth} "
-                               f"plan={args.plan}",
+        "config": {"workload": f"{d.name} ({d.L_img} img + {d.txt_len} txt tokens), 28-step flow schedule, "
+                               f"continuous batching max_batch {args.max_batch}, masks m~U[{args.mask_lo},{args.mask_hi}] "
+                               f"({'rect/blob' if args.mask_kind == 'mixed' else 'blob'}), K/V cache tier={tier} "
+                               f"copy_mode={args.copy_mode} depth={args.depth} plan={args.plan}",
                    "global_batch": args.max_batch * world, "seq_len": d.L, "parallelism": f"replica{world}",
                    "l2": "inputs larger than L2 (23.7 GB weights + 2.9 GB K/V per request-step streamed)"},
         "roofline": {"bound": "tensor", "kernel": "gemm_tc (tcgen05 bf16)", "achieved": round(gemm_tf, 1),

@@ -164,8 +164,11 @@ void ig_mask_free(ig_mask* mask);
 typedef struct {
   int slot;                /* continuous-batching slot 0..max_batch-1, stable for the       */
                            /* request's life; distinct within one call                      */
-  float* latent;           /* dev [L_img, lat_ch] fp32, in/out: masked rows updated,         */
-                           /* unmasked rows untouched (C-AMB 11)                             */
+  float* latent;           /* [L_img, lat_ch] fp32, in/out: masked rows updated, unmasked    */
+                           /* rows untouched (C-AMB 11).  Device memory, or pinned host memory */
+                           /* (cudaHostAlloc / cudaHostRegister; the host-buffer path of the   */
+                           /* public API): the gather and Euler-scatter kernels then read and  */
+                           /* write only the masked rows in place over the host link           */
   const ig_mask* mask;
   const ig_cache* cache;   /* NULL allowed only when n_m == L_img (ignored then, C-AMB 27)   */
   int step;                /* index into the cache's schedule (C-AMB 9)                      */

@@ -1544,7 +1544,7 @@ extern "C" ig_status ig_edit_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, v
     CUDA_TRY(cudaStreamSynchronize((cudaStream_t)stream));
     for (int i = 0; i < n; ++i) {
       std::vector<float> lat((size_t)ctx->Limg * ctx->C);
-      CUDA_TRY(cudaMemcpy(lat.data(), reqs[i].latent, lat.size() * 4, cudaMemcpyDeviceToHost));
+      CUDA_TRY(cudaMemcpy(lat.data(), reqs[i].latent, lat.size() * 4, cudaMemcpyDefault));
       for (float v : lat)
         if (!std::isfinite(v)) return set_err(IG_ENUMERIC, "req %d: non-finite latent after step", i);
     }

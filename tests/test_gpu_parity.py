@@ -465,3 +465,26 @@ def test_y_cache_dense_prefix_end_to_end(k):
     for r in reqs:
         r.free()
     m.close()
+
+
+def test_host_pinned_latent_bitwise_equals_device_latent():
+    """The public API's host-buffer path: a latent in pinned host memory is gathered and
+    updated in place by the kernels over the host link; same bits as a device latent."""
+    d = synth.FLUX_SMALL
+    m = Model(d, ig.IG_BF16, opts=ig.ig_ctx_opts(2, 0, 2, 1, 0, 0))
+    r = Request(m, 140, synth.blob_mask_count(d, 77, np.random.default_rng(14)))
+    kv = synth.make_cache_kv(d, 8, 2, dtype=torch.bfloat16)
+    cache = ig.ig_cache_create(m.ctx, 2, ig.IG_CACHE_HOST)
+    fill_cache(m, cache, kv)
+    host = r.latent0.cpu().pin_memory()
+    sig = [1.0, 0.7, 0.4]
+    for s in range(2):
+        ig.ig_edit_step(m.ctx, [r.req(0, cache, s, sig[s], sig[s + 1])], 0)
+        q = ig.make_req(0, host.data_ptr(), r.mask, cache, s, sig[s], sig[s + 1], r.txt.data_ptr(), r.cond.data_ptr())
+        ig.ig_edit_step(m.ctx, [q], 0)
+    torch.cuda.synchronize()
+    assert torch.equal(host, r.latent.cpu())
+    assert not torch.equal(host, r.latent0.cpu())
+    ig.ig_cache_free(cache)
+    r.free()
+    m.close()
