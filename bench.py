@@ -5,8 +5,11 @@ vs dense step".  One bench *step* = one ig_edit_step over the running continuous
 (max_batch 8 requests at staggered denoising steps; a request that finishes its 28th step
 leaves and a new one joins at the next step boundary).  Requests carry masks with
 m ~ U[0.05, 0.60] (half rectangles, half blobs) and reference one template whose 28-step
-K/V cache (80.3 GB bf16) lives in pinned host memory and is prefetched layer by layer
-(P:541-560).  value = request-steps completed in the timed window / 28 / window seconds.
+cache lives in pinned host memory and is prefetched layer by layer: by default a
+hybrid cache — K/V (fig:transformer_alter) for the first blocks, Y (fig:transformer-Bottom,
+half the bytes, K/V recomputed) for the rest, the split chosen by the fitted latency models
+to balance the copy lane against compute — with the Algorithm-1 dense prefix per step.
+value = request-steps completed in the timed window / 28 / window seconds.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
@@ -238,6 +241,22 @@ def N_BLOCKS_FLOPS(d, n_m):
     return d.n_blocks * block_flops(d, n_m)
 
 
+def choose_kv_blocks(d, a_c, b_c, a_l, max_batch, mean_m):
+    """Hybrid split: s blocks move K/V (two planes), the other N - s (interleaved) move Y (one
+    plane) and recompute the unmasked rows' K/V (4 n_u H^2 flops, x1.3 for the LN-modulation
+    and the row widening around it).  Under the fitted linear models pick the s that balances
+    the two lanes of a full batch at the mean mask ratio: argmin_s max(sum compute, sum load)."""
+    from paper_2505_20600_b200.placement import block_flops
+    N, H = d.n_blocks, d.hidden
+    n_m = int(round(mean_m * d.L_img))
+    n_u = max_batch * (d.L_img - n_m)
+    cw = a_c * max_batch * block_flops(d, n_m) + b_c
+    cw_y = cw + 1.3 * a_c * 4.0 * n_u * H * H
+    lt, lt_y = a_l * 2 * n_u * H * 2, a_l * n_u * H * 2
+    best = min(range(N + 1), key=lambda s_: (max(s_ * cw + (N - s_) * cw_y, s_ * lt + max(0, N - s_ - (s_ == 0)) * lt_y), -s_))
+    return best
+
+
 def fit_latency(ig, ctx, d, dev, stream, link_gbs):
     """Linear latency models of Algorithm 1/2: per-block compute time vs FLOPs
     from dense steps (all-ones masks, no cache) at two batch sizes, and per-block load time
@@ -347,7 +366,10 @@ def main():
     ap.add_argument("--model", default="flux1_dev")
     ap.add_argument("--no-hbm-tier", action="store_true", help="skip the HBM-resident template run")
     ap.add_argument("--no-fp8", action="store_true", help="skip the FP8-cache run")
-    ap.add_argument("--no-y", action="store_true", help="skip the Y-cache run")
+    ap.add_argument("--no-y", action="store_true", help="skip the other-cache-kind runs")
+    ap.add_argument("--cache", default="hybrid", choices=["kv", "hybrid", "y"],
+                    help="headline cache kind: K/V, hybrid K/V + Y (interleaved Y blocks), Y")
+    ap.add_argument("--kv-blocks", type=int, default=-1, help="hybrid: blocks keeping K/V (-1: latency-model choice)")
     ap.add_argument("--mask-lo", type=float, default=0.05)
     ap.add_argument("--mask-hi", type=float, default=0.60)
     ap.add_argument("--mask-kind", default="mixed", choices=["mixed", "blob"])
@@ -375,19 +397,34 @@ def main():
     t_setup = time.time()
     link_peak = measure_h2d(dev)
     W, ptrs = build_model(d, dev)
-    opts = ig.ig_ctx_opts(args.max_batch, args.max_batch * d.L, args.depth, args.copy_mode, 0, 0)
-    ctx = ig.ig_ctx_create(ig.make_desc(d, ig.IG_BF16), ptrs, local, opts)
+    mb_kv = max(args.max_batch, 4)  # the latency fit runs dense batches of 2 and 4
+    opts = ig.ig_ctx_opts(mb_kv, mb_kv * d.L, args.depth, args.copy_mode, 0, 0)
+    ctx_kv = ig.ig_ctx_create(ig.make_desc(d, ig.IG_BF16), ptrs, local, opts)
     sig = synth.flow_sigmas(N_STEPS)
-    # the template: dense 28-step sampler recording every (step, block) K/V (ig_cache_template)
-    tl = synth.make_latent(d, 10 ** 6, dev)
-    tt = synth.make_txt(d, 10 ** 6, dev, torch.bfloat16)
-    tc = synth.make_cond(d, 10 ** 6, dev)
-    t0 = time.time()
-    cache = ig.ig_cache_template(ctx, tl.data_ptr(), tt.data_ptr(), tc.data_ptr(), sig,
-                                 ig.IG_CACHE_HOST if tier == "host" else ig.IG_CACHE_DEVICE, 0)
-    t_template = time.time() - t0
     stream = torch.cuda.Stream(device=dev)
     pool = args.max_batch + math.ceil(args.max_batch * (2 * args.warmup + 2 * args.steps) / N_STEPS) + 2
+    tt = synth.make_txt(d, 10 ** 6, dev, torch.bfloat16)
+    tc = synth.make_cond(d, 10 ** 6, dev)
+
+    def record(c, tier_):
+        """The template: the dense 28-step sampler recording every (step, block) entry of the
+        ctx's cache kind (ig_cache_template), from the same template inputs every time."""
+        tl = synth.make_latent(d, 10 ** 6, dev)
+        return ig.ig_cache_template(c, tl.data_ptr(), tt.data_ptr(), tc.data_ptr(), sig,
+                                    ig.IG_CACHE_HOST if tier_ == "host" else ig.IG_CACHE_DEVICE, 0)
+
+    def make_y_ctx(kv_blocks):
+        o = ig.ig_ctx_opts(args.max_batch, args.max_batch * d.L, args.depth, args.copy_mode, 0, 0, 1, kv_blocks)
+        return ig.ig_ctx_create(ig.make_desc(d, ig.IG_BF16), ptrs, local, o)
+
+    # Algorithm-1/2 latency models (P:701-726) fitted on this GPU; the hybrid split point
+    a_c, b_c, a_l, b_l = fit_latency(ig, ctx_kv, d, dev, stream, link_peak)
+    kv_auto = choose_kv_blocks(d, a_c, b_c, a_l, args.max_batch, 0.5 * (args.mask_lo + args.mask_hi))
+    kv_blocks = {"kv": None, "y": 0}.get(args.cache, kv_auto if args.kv_blocks < 0 else args.kv_blocks)
+    ctx = ctx_kv if kv_blocks is None else make_y_ctx(kv_blocks)
+    t0 = time.time()
+    cache = record(ctx, tier)
+    t_template = time.time() - t0
     torch.cuda.synchronize()
 
     def barrier():
@@ -434,9 +471,8 @@ def main():
                 "copy_lane_busy": round(lg.prof["copy"]["ms"] / lg.ms, 4),
                 "kernel_share_of_step": {k: round(v["ms"] / lg.ms, 4) for k, v in lg.prof.items() if k != "copy"}}
 
-    # Algorithm-1 latency models fitted on this GPU, then the headline: the
-    # mask-aware step with the per-step dense-prefix plan (N1), cache in pinned host memory
-    a_c, b_c, a_l, b_l = fit_latency(ig, ctx, d, dev, stream, link_peak)
+    # the headline: the mask-aware step with the per-step dense-prefix plan (N1), cache in
+    # pinned host memory
     plan_mode = {"model": 2, "none": 0}.get(args.plan, 1)
     ig.ig_set_plan(ctx, plan_mode, 0 if plan_mode != 1 else int(args.plan), a_c, b_c, a_l, b_l)
     main_leg = leg(ctx, cache, clk=Clocks(local))
@@ -466,42 +502,47 @@ def main():
         ig.ig_set_plan(ctx, plan_mode, 0 if plan_mode != 1 else int(args.plan), a_c, b_c, a_l, b_l)
         ig.ig_cache_free(dcache)
 
-    # FP8 (e4m3) cache in pinned host memory (SURVEY N4 byte reducer): a second context on the
-    # same weights whose caches are e4m3 + per-(token, head) scales; same request sequence
+    ig.ig_cache_free(cache)  # host memory for the next legs' templates
+
+    # FP8 (e4m3) K/V cache in pinned host memory (SURVEY N4 byte reducer): a context whose
+    # caches are e4m3 + per-(token, head) scales, recorded directly; same request sequence
     fp8 = None
     if tier == "host" and not args.no_fp8 and world == 1:
         opts8 = ig.ig_ctx_opts(args.max_batch, args.max_batch * d.L, args.depth, args.copy_mode, 0, 1)
         ctx8 = ig.ig_ctx_create(ig.make_desc(d, ig.IG_BF16), ptrs, local, opts8)
-        cache8 = ig.ig_cache_clone(ctx8, cache, ig.IG_CACHE_HOST)
-        ig.ig_set_plan(ctx8, plan_mode, 0 if plan_mode != 1 else int(args.plan), a_c, b_c, a_l / 1.0, b_l)
+        cache8 = record(ctx8, "host")
+        ig.ig_set_plan(ctx8, plan_mode, 0 if plan_mode != 1 else int(args.plan), a_c, b_c, a_l, b_l)
         fp8 = summary(leg(ctx8, cache8))
         fp8["note"] = ("same workload, K/V cache stored as e4m3 + fp32 scale per (token, head): "
                        "half the host-link bytes")
         ig.ig_cache_free(cache8)
         ig.ig_ctx_destroy(ctx8)
 
-    # Y-caching variant (the paper's primary form, fig:transformer-Bottom): a context
-    # whose template cache holds block outputs (half the bytes); same request sequence, host tier
-    ycache_leg = None
+    # the other cache kinds on the same workload: K/V only (fig:transformer_alter) when the
+    # headline uses a Y/hybrid cache, the hybrid K/V + Y cache otherwise
+    alt = {}
     if tier == "host" and not args.no_y and world == 1:
-        optsy = ig.ig_ctx_opts(args.max_batch, args.max_batch * d.L, args.depth, args.copy_mode, 0, 0, 1)
-        ctxy = ig.ig_ctx_create(ig.make_desc(d, ig.IG_BF16), ptrs, local, optsy)
-        tl = synth.make_latent(d, 10 ** 6, dev)
-        cachey = ig.ig_cache_template(ctxy, tl.data_ptr(), tt.data_ptr(), tc.data_ptr(), sig, ig.IG_CACHE_HOST, 0)
-        ig.ig_set_plan(ctxy, plan_mode, 0 if plan_mode != 1 else int(args.plan), a_c, b_c, a_l, b_l)
-        ycache_leg = summary(leg(ctxy, cachey))
-        ycache_leg["note"] = ("same workload, Y cache (block outputs of the unmasked tokens, one plane per block; "
-                              "their K/V recomputed on the GPU)")
-        ig.ig_cache_free(cachey)
-        ig.ig_ctx_destroy(ctxy)
+        kinds = [("kv_cache_host_tier", None)] if kv_blocks is not None else [("hybrid_cache_host_tier", kv_auto)]
+        if kv_blocks != 0:
+            kinds.append(("y_cache_host_tier", 0))
+        for name, yf in kinds:
+            cx = ctx_kv if yf is None else make_y_ctx(yf)
+            ca = record(cx, "host")
+            ig.ig_set_plan(cx, plan_mode, 0 if plan_mode != 1 else int(args.plan), a_c, b_c, a_l, b_l)
+            alt[name] = summary(leg(cx, ca))
+            alt[name]["kv_blocks"] = yf
+            ig.ig_cache_free(ca)
+            if cx is not ctx_kv:
+                ig.ig_set_plan(cx, 0, 0, 0.0, 0.0, 0.0, 0.0)
+                ig.ig_ctx_destroy(cx)
 
     # dense comparison step (all-ones masks, no cache) on the same GPUs and kernels
     dense = None
     if args.dense_steps > 0:
-        dbatch = Batch(ig, ctx, d, dev, args.max_batch, args.max_batch + 2, rid0=rank * 100000 + 50000, dense=True)
-        run_loop(ig, ctx, dbatch, None, sig, 1, stream)
+        dbatch = Batch(ig, ctx_kv, d, dev, args.max_batch, args.max_batch + 2, rid0=rank * 100000 + 50000, dense=True)
+        run_loop(ig, ctx_kv, dbatch, None, sig, 1, stream)
         barrier()
-        ld = run_loop(ig, ctx, dbatch, None, sig, args.dense_steps, stream)
+        ld = run_loop(ig, ctx_kv, dbatch, None, sig, args.dense_steps, stream)
         barrier()
         ms_d, rs_d = reduce_max_sum(ld.ms, ld.rsteps)
         dense = rs_d / N_STEPS / (ms_d / 1e3)
@@ -526,8 +567,9 @@ def main():
         "data": "synthetic",
         "config": {"workload": f"{d.name} ({d.L_img} img + {d.txt_len} txt tokens), 28-step flow schedule, "
                                f"continuous batching max_batch {args.max_batch}, masks m~U[{args.mask_lo},{args.mask_hi}] "
-                               f"({'rect/blob' if args.mask_kind == 'mixed' else 'blob'}), K/V cache tier={tier} "
-                               f"copy_mode={args.copy_mode} depth={args.depth} plan={args.plan}",
+                               f"({'rect/blob' if args.mask_kind == 'mixed' else 'blob'}), "
+                               f"{'K/V' if kv_blocks is None else ('Y' if kv_blocks == 0 else f'hybrid K/V+Y ({kv_blocks} K/V blocks, {d.n_blocks - kv_blocks} Y blocks interleaved)')} "
+                               f"cache tier={tier} copy_mode={args.copy_mode} depth={args.depth} plan={args.plan}",
                    "global_batch": args.max_batch * world, "seq_len": d.L, "parallelism": f"replica{world}",
                    "l2": "inputs larger than L2 (23.7 GB weights + 2.9 GB K/V per request-step streamed)"},
         "roofline": {"bound": "tensor", "kernel": "gemm_tc (tcgen05 bf16)", "achieved": round(gemm_tf, 1),
@@ -564,7 +606,7 @@ def main():
                       if prof["copy"]["ms"] else None},
         "hbm_tier": hbm,
         "fp8_cache_host_tier": fp8,
-        "y_cache_host_tier": ycache_leg,
+        **alt,
         "speedup_hbm_tier_vs_dense": round(hbm["value"] / dense, 3) if (hbm and dense) else None,
         "gpu_launches": int(launches),
         "clocks": clk,

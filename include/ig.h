@@ -96,6 +96,13 @@ typedef struct {
                        /*     (fig:transformer-Bottom): half the     */
                        /*     bytes of K/V; a step recomputes the unmasked tokens' K/V     */
                        /*     from them (LN-mod + K/V projection).  Not with cache_fp8.    */
+  int cache_kv_blocks; /* with cache_y: hybrid cache — this many blocks keep K/V, the     */
+                       /*     other N - cache_kv_blocks are Y blocks (0 = pure Y): the     */
+                       /*     first N - kv_blocks entries of the bit-reversal order over   */
+                       /*     the next power of two >= N (entries >= N skipped), i.e. Y    */
+                       /*     blocks spread evenly over the step.  Per step, block b       */
+                       /*     stores [K_b, V_b] if it is a K/V block, then [Y_b] if block  */
+                       /*     b or b + 1 is a Y block (ig_cache_write takes that order)    */
 } ig_ctx_opts;
 
 typedef struct ig_ctx ig_ctx;

@@ -21,7 +21,7 @@ What it computes, and where the paper says so
 * Y-caching variant (fig:transformer-Bottom): the cache holds the
   template's block outputs Y of the image tokens; unmasked rows of each block's input are
   replenished from it and only feed K/V.        kv_from_y, edit_step_y, cache_template_y
-  A hybrid cache keeps K/V for the blocks before y_from and Y after it.   edit_step_y(y_from=)
+  A hybrid cache keeps K/V for some blocks and Y for the others.     edit_step_y(y_blocks=)
 * Algorithm 1 dense prefix (C-AMB 23).            edit_step_planned, edit_step_y(k=)
 Readings where the paper is silent (Flux-shaped blocks, adaLN, QK-RMSNorm, RoPE,
 GELU-tanh, flow-matching Euler, row order) are the numbered C-AMB readings in DESIGN.md
@@ -424,14 +424,14 @@ def kv_from_y(d, W, b, x_u, vec, idx_u):
 
 
 def edit_step_y(d, W, latent, mask, y_cache_step, tlatent, sigma, sigma_next, txt, cond_vec, k=0,
-                y_from=0, kv_cache_step=None):
+                y_blocks=None, kv_cache_step=None):
     """One mask-aware step under the Y variant, with an optional Algorithm-1 dense prefix of k
     blocks (P:563-605).  y_cache_step: [blocks, L_img, H] = Y_b of the template at this step;
     tlatent: the template's input latent of this step [L_img, C].  A block whose predecessor
     ran densely takes its unmasked input rows from that computation; otherwise from Y_{b-1}
     (block 0: img_in(tlatent)).  Latent update and untouched rows as in edit_step.
-    Hybrid cache (DESIGN reading 30): blocks b < y_from are K/V-variant blocks on
-    kv_cache_step[b]; blocks b >= y_from are Y-variant blocks."""
+    Hybrid cache (DESIGN reading 30): only the blocks in y_blocks (None = all) are Y-variant
+    blocks; the others are K/V-variant blocks on kv_cache_step[b]."""
     latent = np.asarray(latent, np.float64)
     idx_m, idx_u, n_m = index_build(mask)
     if n_m == 0:
@@ -470,7 +470,7 @@ def edit_step_y(d, W, latent, mask, y_cache_step, tlatent, sigma, sigma_next, tx
                 else:
                     x = np.concatenate([x[:Lt], x[Lt:][idx_m]])
             continue
-        if b < y_from:  # K/V-variant block of a hybrid cache
+        if y_blocks is not None and b not in y_blocks:  # K/V-variant block of a hybrid cache
             kv = kv_cache_step[b]
         else:
             if b > k:  # predecessor used the cache: replenish from Y_{b-1}

@@ -104,7 +104,11 @@ struct ig_cache {
   ig_model_desc desc{};
   int n_steps = 0, tier = 0;
   int fp8 = 0;              // 1: e4m3 data [steps][blocks][2][L_img][H] + fp32 scales [..][heads]
-  int y = 0;                // 1: Y variant, block outputs [steps][blocks][L_img][H] (one plane)
+  int y = 0;                // 1: Y variant (block outputs of the image tokens), see ymode
+  int kv_blocks = 0;        // hybrid: number of blocks that keep K/V (0 = pure Y)
+  std::vector<uint8_t> ymode;  // per block: 1 = Y block (interleaved order, ig.h cache_kv_blocks)
+  int step_planes = 0;      // planes per step: [K_b, V_b] for K/V blocks, then [Y_b] when block b
+                            // or b + 1 is a Y block (Y_b feeds block b + 1)
   size_t scale_off = 0;     // byte offset of the scale region (fp8 only)
   size_t lat_off = 0;       // template input latent per step [steps][L_img][C] fp32 (Algorithm-1
                             // dense prefix: unmasked rows enter from the template's trajectory)
@@ -346,7 +350,7 @@ extern "C" ig_status ig_ctx_create(const ig_model_desc* desc, const void* const*
     return set_err(IG_EINVAL, "expected %d weight pointers, got %d", nw, n_weights);
   for (int i = 0; i < nw; ++i)
     if (!weights[i]) return set_err(IG_EINVAL, "weight %d is NULL", i);
-  ig_ctx_opts o{8, 0, 2, 0, 0, 0, 0};
+  ig_ctx_opts o{8, 0, 2, 0, 0, 0, 0, 0};
   if (opts) o = *opts;
   if (o.max_batch <= 0) o.max_batch = 8;
   if (o.max_batch > 16) return set_err(IG_EUNSUPPORTED, "max_batch > 16");
@@ -651,12 +655,40 @@ static ig_status get_ones_mask(ig_ctx* ctx, ig_mask** out) {
 // ----------------------------------------------------------------------------------------
 // caches
 // ----------------------------------------------------------------------------------------
-static size_t cache_kv_bytes(const ig_ctx* ctx, int n_steps, int fp8, int y = 0) {
-  if (fp8) return (size_t)n_steps * ctx->nb * 2 * ctx->Limg * ((size_t)ctx->H + 4 * ctx->d.heads);
-  return (size_t)n_steps * ctx->nb * (y ? 1 : 2) * ctx->Limg * ctx->H * ctx->esz;
+// Which blocks of a hybrid cache are Y blocks (ig.h cache_kv_blocks): the first N - kv_blocks
+// blocks of the bit-reversal order over the next power of two >= N (values >= N skipped), so
+// Y blocks are spread evenly over the step (the copy lane sees a locally balanced mix) and the
+// Y-block sets of different splits are nested.
+static std::vector<uint8_t> y_modes(int N, int y, int kv_blocks) {
+  std::vector<uint8_t> m(N, 0);
+  if (!y) return m;
+  int bits = 0;
+  while ((1 << bits) < N) ++bits;
+  int taken = 0;
+  const int ny = N - std::max(0, std::min(kv_blocks, N));
+  for (int k = 0; k < (1 << bits) && taken < ny; ++k) {
+    int v = 0;
+    for (int i = 0; i < bits; ++i) v |= ((k >> i) & 1) << (bits - 1 - i);
+    if (v < N) { m[v] = 1; ++taken; }
+  }
+  return m;
 }
-static size_t cache_bytes(const ig_ctx* ctx, int n_steps, int fp8 = 0, int y = 0) {
-  return cache_kv_bytes(ctx, n_steps, fp8, y) + (size_t)n_steps * ctx->Limg * ctx->C * 4;
+static inline bool blk_kv(const std::vector<uint8_t>& m, int b) { return !m[b]; }
+static inline bool blk_yrec(const std::vector<uint8_t>& m, int b) {
+  return m[b] || (b + 1 < (int)m.size() && m[b + 1]);
+}
+static int planes_of(const std::vector<uint8_t>& m, int b) { return (blk_kv(m, b) ? 2 : 0) + (blk_yrec(m, b) ? 1 : 0); }
+static int step_planes(const std::vector<uint8_t>& m) {
+  int n = 0;
+  for (int b = 0; b < (int)m.size(); ++b) n += planes_of(m, b);
+  return n;
+}
+static size_t cache_kv_bytes(const ig_ctx* ctx, int n_steps, int fp8, const std::vector<uint8_t>& m) {
+  if (fp8) return (size_t)n_steps * ctx->nb * 2 * ctx->Limg * ((size_t)ctx->H + 4 * ctx->d.heads);
+  return (size_t)n_steps * step_planes(m) * ctx->Limg * ctx->H * ctx->esz;
+}
+static size_t cache_bytes(const ig_ctx* ctx, int n_steps, int fp8, const std::vector<uint8_t>& m) {
+  return cache_kv_bytes(ctx, n_steps, fp8, m) + (size_t)n_steps * ctx->Limg * ctx->C * 4;
 }
 static float* cache_latent(const ig_ctx* ctx, const ig_cache* c, int step) {
   return (float*)((char*)c->ptr + c->lat_off + (size_t)step * ctx->Limg * ctx->C * 4);
@@ -664,13 +696,18 @@ static float* cache_latent(const ig_ctx* ctx, const ig_cache* c, int step) {
 static const float* cache_latent_dev(const ig_ctx* ctx, const ig_cache* c, int step) {
   return (const float*)((const char*)c->dptr + ((char*)cache_latent(ctx, c, step) - (char*)c->ptr));
 }
-// data plane (which = 0 K, 1 V) of (step, block) and its scale plane (fp8 caches); a Y cache
-// has one plane per (step, block) (which is ignored)
+// data plane (which = 0 K, 1 V, 2 Y) of (step, block) and its scale plane (fp8 caches)
 static char* cache_plane(const ig_ctx* ctx, const ig_cache* c, int step, int b, int which) {
   const size_t row = c->fp8 ? (size_t)ctx->H : (size_t)ctx->H * ctx->esz;
-  if (c->y) return (char*)c->ptr + ((size_t)step * ctx->nb + b) * ctx->Limg * row;
-  return (char*)c->ptr + (((size_t)step * ctx->nb + b) * 2 + which) * ctx->Limg * row;
+  if (!c->y) return (char*)c->ptr + (((size_t)step * ctx->nb + b) * 2 + which) * ctx->Limg * row;
+  size_t idx = (size_t)step * c->step_planes;
+  for (int bb = 0; bb < b; ++bb) idx += planes_of(c->ymode, bb);
+  if (which == 2) idx += blk_kv(c->ymode, b) ? 2 : 0;
+  else idx += which;
+  return (char*)c->ptr + idx * ctx->Limg * row;
 }
+// block b of a request on cache c runs as a Y block (unmasked rows replenished, K/V recomputed)
+static inline bool y_block(const ig_cache* c, int b) { return c && c->y && c->ymode[b]; }
 static float* cache_scales(const ig_ctx* ctx, const ig_cache* c, int step, int b, int which) {
   return (float*)((char*)c->ptr + c->scale_off +
                   (((size_t)step * ctx->nb + b) * 2 + which) * ctx->Limg * ctx->d.heads * 4);
@@ -682,13 +719,13 @@ static const float* cache_scales_dev(const ig_ctx* ctx, const ig_cache* c, int s
   return (const float*)((const char*)c->dptr + ((char*)cache_scales(ctx, c, step, b, which) - (char*)c->ptr));
 }
 
-static ig_status cache_create_kind(ig_ctx* ctx, int n_steps, int tier, int fp8, int y, ig_cache** out);
+static ig_status cache_create_kind(ig_ctx* ctx, int n_steps, int tier, int fp8, int y, int kv_blocks, ig_cache** out);
 extern "C" ig_status ig_cache_create(ig_ctx* ctx, int n_steps, int tier, ig_cache** out) {
   if (!ctx || !out) return set_err(IG_EINVAL, "NULL argument");
-  return cache_create_kind(ctx, n_steps, tier, ctx->o.cache_fp8, ctx->o.cache_y, out);
+  return cache_create_kind(ctx, n_steps, tier, ctx->o.cache_fp8, ctx->o.cache_y, ctx->o.cache_kv_blocks, out);
 }
 
-static ig_status cache_create_kind(ig_ctx* ctx, int n_steps, int tier, int fp8, int y, ig_cache** out) {
+static ig_status cache_create_kind(ig_ctx* ctx, int n_steps, int tier, int fp8, int y, int kv_blocks, ig_cache** out) {
   *out = nullptr;
   if (n_steps <= 0) return set_err(IG_EINVAL, "n_steps must be positive");
   if (tier != IG_CACHE_HOST && tier != IG_CACHE_DEVICE) return set_err(IG_EINVAL, "bad tier");
@@ -700,9 +737,12 @@ static ig_status cache_create_kind(ig_ctx* ctx, int n_steps, int tier, int fp8, 
   c->device = ctx->device;
   c->fp8 = fp8;
   c->y = y;
-  c->bytes = cache_bytes(ctx, n_steps, c->fp8, c->y);
+  c->kv_blocks = y ? std::max(0, std::min(kv_blocks, ctx->nb)) : ctx->nb;
+  c->ymode = y_modes(ctx->nb, y, c->kv_blocks);
+  c->step_planes = step_planes(c->ymode);
+  c->bytes = cache_bytes(ctx, n_steps, c->fp8, c->ymode);
   if (c->fp8) c->scale_off = (size_t)n_steps * ctx->nb * 2 * ctx->Limg * ctx->H;
-  c->lat_off = cache_kv_bytes(ctx, n_steps, c->fp8, c->y);
+  c->lat_off = cache_kv_bytes(ctx, n_steps, c->fp8, c->ymode);
   cudaError_t e;
   if (tier == IG_CACHE_HOST) {
     e = cudaHostAlloc(&c->ptr, c->bytes, cudaHostAllocMapped | cudaHostAllocPortable);
@@ -715,7 +755,7 @@ static ig_status cache_create_kind(ig_ctx* ctx, int n_steps, int tier, int fp8, 
     cudaGetLastError();
     if (c->ptr) { if (tier == IG_CACHE_HOST) cudaFreeHost(c->ptr); else cudaFree(c->ptr); }
     delete c;
-    return set_err(IG_ENOMEM, "cache allocation of %zu bytes failed: %s", cache_bytes(ctx, n_steps, fp8, y),
+    return set_err(IG_ENOMEM, "cache allocation of %zu bytes failed: %s", c->bytes,
                    cudaGetErrorString(e));
   }
   *out = c;
@@ -731,7 +771,7 @@ extern "C" ig_status ig_cache_clone(ig_ctx* ctx, const ig_cache* src, int tier, 
   if (quantize && src->y) return set_err(IG_EUNSUPPORTED, "FP8 Y caches are not supported");
   CUDA_TRY(cudaSetDevice(ctx->device));
   ig_cache* c = nullptr;
-  ig_status s = cache_create_kind(ctx, src->n_steps, tier, quantize ? 1 : src->fp8, src->y, &c);
+  ig_status s = cache_create_kind(ctx, src->n_steps, tier, quantize ? 1 : src->fp8, src->y, src->kv_blocks, &c);
   if (s != IG_OK) return s;
   cudaError_t e = cudaSuccess;
   if (!quantize) {
@@ -769,11 +809,13 @@ extern "C" ig_status ig_cache_write(ig_ctx* ctx, ig_cache* c, const void* kv, co
   CUDA_TRY(cudaSetDevice(ctx->device));
   cudaStream_t st = (cudaStream_t)stream;
   const size_t pl = (size_t)ctx->Limg * ctx->H, spl = (size_t)ctx->Limg * ctx->d.heads;
-  for (int s = 0; s < c->n_steps; ++s)
+  if (!c->fp8) {  // the caller's buffer is the storage layout of every step: one copy
+    CUDA_TRY(cudaMemcpyAsync(c->ptr, kv, c->lat_off, cudaMemcpyDefault, st));
+  }
+  for (int s = 0; s < c->n_steps && c->fp8; ++s)
     for (int b = 0; b < ctx->nb; ++b) {
-      const int planes = c->y ? 1 : 2;
-      const char* src = (const char*)kv + (((size_t)s * ctx->nb + b) * planes) * pl * ctx->esz;
-      if (c->fp8) {
+      const char* src = (const char*)kv + (((size_t)s * ctx->nb + b) * 2) * pl * ctx->esz;
+      {
         launch_kv_quant((const bf16*)src, (const bf16*)(src + pl * ctx->esz), ctx->Limg, ctx->H, ctx->d.heads,
                         ctx->q8rec, ctx->q8rec + pl, ctx->q8rec_scl, ctx->q8rec_scl + spl, st);
         for (int w = 0; w < 2; ++w) {
@@ -781,8 +823,6 @@ extern "C" ig_status ig_cache_write(ig_ctx* ctx, ig_cache* c, const void* kv, co
           CUDA_TRY(cudaMemcpyAsync(cache_scales(ctx, c, s, b, w), ctx->q8rec_scl + w * spl, spl * 4, cudaMemcpyDefault, st));
         }
         CUDA_TRY(cudaStreamSynchronize(st));
-      } else {
-        CUDA_TRY(cudaMemcpyAsync(cache_plane(ctx, c, s, b, 0), src, planes * pl * ctx->esz, cudaMemcpyDefault, st));
       }
     }
   if (latents)
@@ -859,9 +899,9 @@ static void issue_copy(ig_ctx* ctx, const std::vector<StepReq>& sr, const KvGath
     const int slot = r->slot;
     const int n_u = ctx->Limg - sr[q].m->n_m;
     long long by = 0;
-    if (c->y) {  // Y variant: the template's Y_{b-1} rows of the unmasked tokens -> V plane rows
+    if (y_block(c, b)) {  // Y block: the template's Y_{b-1} rows of the unmasked tokens -> V plane
       if (b <= plan.kplan) continue;  // block 0 / first block after the prefix: computed rows
-      const char* src = cache_plane(ctx, c, r->step, b - 1, 0);
+      const char* src = cache_plane(ctx, c, r->step, b - 1, 2);
       char* dst = (char*)ctx->kv_arena + ((size_t)slot * ctx->slot_stride + (size_t)buf * ctx->buf_elems) * ctx->esz +
                   vplane + txt_off;
       const bool gathered = host ? ctx->o.copy_mode == 2 : ctx->o.copy_mode != 0;
@@ -968,25 +1008,31 @@ static double block_flops_rows(const ig_ctx* ctx, long long rows) {
 }
 
 static int plan_prefix(ig_ctx* ctx, const std::vector<StepReq>& sr) {
-  long long rows_m = 0, rows_all = 0, bytes = 0, rows_y = 0;
+  const int N = ctx->nb;
+  long long rows_m = 0, rows_all = 0;
+  std::vector<long long> bytes(N, 0), rows_y(N, 0);
   for (auto& s : sr) {
     rows_m += ctx->Lt + s.m->n_m;
     rows_all += ctx->Lt + (s.use_cache ? ctx->Limg : s.m->n_m);
-    if (s.use_cache) {
-      const int n_u = ctx->Limg - s.m->n_m;
-      if (s.r->cache->y) {  // one plane; the K/V projection of the unmasked rows is recomputed
-        bytes += (long long)n_u * ctx->H * (long long)ctx->esz;
-        rows_y += n_u;
+    if (!s.use_cache) continue;
+    const ig_cache* c = s.r->cache;
+    const long long n_u = ctx->Limg - s.m->n_m;
+    for (int b = 0; b < N; ++b) {
+      if (y_block(c, b)) {  // one plane; the K/V projection of the unmasked rows is recomputed
+        if (b > 0) bytes[b] += n_u * ctx->H * (long long)ctx->esz;
+        rows_y[b] += n_u;
       } else {
-        bytes += s.r->cache->fp8 ? 2LL * n_u * (ctx->H + 4 * ctx->d.heads)
-                                 : 2LL * n_u * ctx->H * (long long)ctx->esz;
+        bytes[b] += c->fp8 ? 2LL * n_u * (ctx->H + 4 * ctx->d.heads) : 2LL * n_u * ctx->H * (long long)ctx->esz;
       }
     }
   }
-  const double cw = ctx->pm_cs * (block_flops_rows(ctx, rows_m) + 4.0 * rows_y * ctx->H * ctx->H) + ctx->pm_cb;
+  std::vector<double> cw(N), lt(N);
+  for (int b = 0; b < N; ++b) {
+    cw[b] = ctx->pm_cs * (block_flops_rows(ctx, rows_m) + 4.0 * rows_y[b] * ctx->H * ctx->H) + ctx->pm_cb;
+    lt[b] = bytes[b] > 0 ? ctx->pm_ls * (double)bytes[b] + ctx->pm_lb : 0.0;
+  }
   const double cwo = ctx->pm_cs * block_flops_rows(ctx, rows_all) + ctx->pm_cb;
-  const double lt = ctx->pm_ls * (double)bytes + ctx->pm_lb;
-  const int N = ctx->nb, R = ctx->R;
+  const int R = ctx->R;
   int best_k = 0;
   double best = 1e300;
   // Steady state of continuous batching: the copy lane is in order and runs into the next
@@ -1000,8 +1046,8 @@ static int plan_prefix(ig_ctx* ctx, const std::vector<StepReq>& sr) {
       start = comp;
       for (int b = 0; b < N; ++b) {
         if (b < k) { comp += cwo; continue; }
-        load = std::max(load, free_at[b % R]) + lt;
-        comp = std::max(comp, load) + cw;
+        load = std::max(load, free_at[b % R]) + lt[b];
+        comp = std::max(comp, load) + cw[b];
         free_at[b % R] = comp;
       }
     }
@@ -1084,12 +1130,24 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
   // unmasked image rows in the row set: Y-cache requests always (their K/V are recomputed from
   // the replenished block inputs), K/V-cache requests only under a dense prefix.  Y requests'
   // rows come first, so a cached block's K/V-recompute rows are the one range [M, M_y).
+  // Y requests are ordered by their cache's number of Y blocks (descending); the Y-block sets
+  // are nested (y_modes), so block b's Y rows are the one range [M, M + uy[b]).
   int U_y = 0, U_kv = 0;
-  for (auto& s : sr)
-    if (s.use_cache) {
-      if (s.r->cache->y) U_y += ctx->Limg - s.m->n_m;
-      else if (kplan > 0) U_kv += ctx->Limg - s.m->n_m;
+  std::vector<int> yord;
+  for (int q = 0; q < (int)sr.size(); ++q)
+    if (sr[q].use_cache) {
+      if (sr[q].r->cache->y) { U_y += ctx->Limg - sr[q].m->n_m; yord.push_back(q); }
+      else if (kplan > 0) U_kv += ctx->Limg - sr[q].m->n_m;
     }
+  std::stable_sort(yord.begin(), yord.end(),
+                   [&](int a, int b) { return sr[a].r->cache->kv_blocks < sr[b].r->cache->kv_blocks; });
+  std::vector<int> urow0(sr.size(), 0), uy(nb, 0);
+  {
+    int row = M;
+    for (int q : yord) { urow0[q] = row; row += ctx->Limg - sr[q].m->n_m; }
+    for (int b = 0; b < nb; ++b)
+      for (int q : yord) if (y_block(sr[q].r->cache, b)) uy[b] += ctx->Limg - sr[q].m->n_m;
+  }
   const int M_y = M + U_y;
   const int M_full = M_y + U_kv;
   if (M_full > ctx->o.max_rows) return set_err(IG_ENOMEM, "step needs %d rows > max_rows %d", M_full, ctx->o.max_rows);
@@ -1112,7 +1170,7 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
   AttnSeg* dsegf = dseg + 2 * ctx->o.max_batch;
   KvGatherReq* dkvg = (KvGatherReq*)((char*)dseg + 5 * ctx->o.max_batch * sizeof(AttnSeg));
   int nseg = 0, max_q = 0, nsegf = 0, max_qf = 0;
-  int img_row = M_txt, yrow = M, kvrow = M_y;
+  int img_row = M_txt, kvrow = M_y;
   for (int q = 0; q < na; ++q) {
     const ig_edit_req* r = sr[q].r;
     ReqDev& d = hreq[q];
@@ -1130,7 +1188,7 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
     d.has_cache = sr[q].use_cache;
     const bool ycache = sr[q].use_cache && r->cache->y;
     d.n_ui = (sr[q].use_cache && (ycache || kplan > 0)) ? ctx->Limg - d.n_m : 0;
-    d.uimg_row0 = ycache ? yrow : kvrow;
+    d.uimg_row0 = ycache ? urow0[q] : kvrow;
     d.tlatent = sr[q].use_cache ? cache_latent_dev(ctx, r->cache, r->step) : nullptr;
     const long long kvb = (long long)r->slot * ctx->slot_stride;
     if (Lt > 0) { hseg[nseg++] = AttnSeg{q * Lt, Lt, kvb}; max_q = std::max(max_q, Lt); }
@@ -1143,7 +1201,7 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
       max_qf = std::max(max_qf, std::max(Lt, std::max(d.n_m, d.n_ui)));
     }
     img_row += d.n_m;
-    (ycache ? yrow : kvrow) += d.n_ui;
+    if (!ycache) kvrow += d.n_ui;
   }
   // copy-lane plan and per-(block, request) gather descriptors (see issue_copy)
   CopyPlan plan;
@@ -1185,10 +1243,10 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
               gq.sclK = cache_scales_dev(ctx, c, r->step, b, 0);
               gq.sclV = cache_scales_dev(ctx, c, r->step, b, 1);
             }
-          } else if (c->y) {  // one plane: Y_{b-1} -> V plane (blocks after the first cached one)
+          } else if (y_block(c, b)) {  // one plane: Y_{b-1} -> V plane (blocks after the first cached one)
             if ((c->tier == IG_CACHE_DEVICE ? ctx->o.copy_mode != 0 : ctx->o.copy_mode == 2) && b > kplan) {
               g.srcK = nullptr;
-              g.srcV = cache_plane_dev(ctx, c, r->step, b - 1, 0);
+              g.srcV = cache_plane_dev(ctx, c, r->step, b - 1, 2);
               g.idx_u = sr[q].m->idx + ctx->Limg;
               g.n_u = n_u;
               g.dstK = dst;
@@ -1363,16 +1421,16 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
   };
   // Y variant: replenish the unmasked rows' block input from the staged Y_{b-1} (V plane)
   auto y_load = [&](int b, int buf) {
-    if (U_y == 0 || b <= kplan) return;
+    if (uy[b] == 0 || b <= kplan) return;
     cudaStreamWaitEvent(st, ctx->ev_copy[buf], 0);
-    ProfScope ps(ctx, st, IG_K_ROWS, 0.0, (double)U_y * H * (es + 4));
+    ProfScope ps(ctx, st, IG_K_ROWS, 0.0, (double)uy[b] * H * (es + 4));
     launch_y_load<T>(ctx->kv_arena, ctx->slot_stride, (long long)buf * ctx->buf_elems, ctx->L, H, ctx->ri, ctx->X, M,
-                     M_y, st);
+                     M + uy[b], st);
     stats.kernel_launches++;
   };
   // Y recording (template pass): the block output's image rows -> compute dtype -> D2H
   auto record_y = [&](int b) {
-    if (!record || !record->y) return;
+    if (!record || !record->y || !blk_yrec(record->ymode, b)) return;
     const int yb = b % R;
     const size_t plane = (size_t)ctx->Limg * H * es;
     char* ys = (char*)ctx->yrec + (size_t)yb * plane;
@@ -1381,7 +1439,7 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
     stats.kernel_launches++;
     cudaEventRecord(ctx->ev_comp[yb], st);
     cudaStreamWaitEvent(ctx->copy_st, ctx->ev_comp[yb], 0);
-    cudaMemcpyAsync(cache_plane(ctx, record, record_step, b, 0), ys, plane, cudaMemcpyDefault, ctx->copy_st);
+    cudaMemcpyAsync(cache_plane(ctx, record, record_step, b, 2), ys, plane, cudaMemcpyDefault, ctx->copy_st);
     if (record->tier == IG_CACHE_HOST) stats.d2h_bytes += plane; else stats.d2d_bytes += plane;
     cudaEventRecord(ctx->ev_yrec[yb], ctx->copy_st);
   };
@@ -1397,7 +1455,7 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
   };
   // cache recording (template mode): image-token K/V of ring buffer -> cache[s][b]
   auto record_kv = [&](int b, int buf) {
-    if (!record || record->y) return;
+    if (!record || (record->y && !blk_kv(record->ymode, b))) return;
     cudaEventRecord(ctx->ev_comp[buf], st);
     cudaStreamWaitEvent(ctx->copy_st, ctx->ev_comp[buf], 0);
     const size_t plane = (size_t)ctx->Limg * H * es;
@@ -1443,7 +1501,7 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
   for (int b = b0; b < b1; ++b) {
     const bool dense = b < kplan;
     const int Mc = dense ? M_full : M;    // rows through every op of the block
-    const int Mk = dense ? M_full : M_y;  // rows through LN-mod and the K/V projection
+    const int Mk = dense ? M_full : M + uy[b];  // rows through LN-mod and the K/V projection
     const int buf = dense ? R : b % R;
     if (!dense) y_load(b, buf);
     if (b < ctx->d.n_double) {
@@ -1453,7 +1511,7 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
       if (Lt) ln_mod(0, M_txt, wt.mod_t, wt.pre_only ? 1 : 0, wt.pre_only ? 0 : 1);
       if (!dense) wait_copy(buf);
       qkv_proj(M_txt, Mc, wi.qkv.w, wi.qkv.b, wi.qg, wi.kg, buf);
-      if (!dense) kv_proj(M, M_y, wi.qkv.w, wi.qkv.b, wi.kg, buf);
+      if (!dense) kv_proj(M, M + uy[b], wi.qkv.w, wi.qkv.b, wi.kg, buf);
       if (Lt) qkv_proj(0, M_txt, wt.qkv.w, wt.qkv.b, wt.qg, wt.kg, buf);
       if (!dense) wait_copy_late(buf);
       attn(buf, dense);
@@ -1482,7 +1540,7 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
       gemm_rows(0, Mc, h, H, w_u, b_u, F, H, cat + H, ldcat, EPI_GELU, nullptr, 0);
       if (!dense) wait_copy(buf);
       qkv_proj(0, Mc, ws.lin1.w, ws.lin1.b, ws.qg, ws.kg, buf);
-      if (!dense) kv_proj(M, M_y, ws.lin1.w, ws.lin1.b, ws.kg, buf);
+      if (!dense) kv_proj(M, M + uy[b], ws.lin1.w, ws.lin1.b, ws.kg, buf);
       if (!dense) wait_copy_late(buf);
       attn(buf, dense);
       record_kv(b, buf);
@@ -1508,7 +1566,9 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
   CUDA_TRY(cudaEventRecord(ctx->ev_stage[si], st));
   for (auto& s : sr)
     if (s.use_cache) CUDA_TRY(cudaLaunchHostFunc(st, unpin_cb, (void*)s.r->cache));
-  if (record) CUDA_TRY(cudaStreamWaitEvent(st, record->y ? ctx->ev_yrec[(b1 - 1) % R] : ctx->ev_copy[(b1 - 1) % R], 0));
+  if (record)
+    CUDA_TRY(cudaStreamWaitEvent(st, record->y && blk_yrec(record->ymode, b1 - 1) ? ctx->ev_yrec[(b1 - 1) % R]
+                                                                                 : ctx->ev_copy[(b1 - 1) % R], 0));
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_err(IG_ECUDA, "step enqueue: %s", cudaGetErrorString(e));
   return IG_OK;

@@ -50,7 +50,8 @@ class ig_model_desc(ctypes.Structure):
 class ig_ctx_opts(ctypes.Structure):
     _fields_ = [("max_batch", ctypes.c_int), ("max_rows", ctypes.c_int),
                 ("prefetch_depth", ctypes.c_int), ("copy_mode", ctypes.c_int),
-                ("debug_checks", ctypes.c_int), ("cache_fp8", ctypes.c_int), ("cache_y", ctypes.c_int)]
+                ("debug_checks", ctypes.c_int), ("cache_fp8", ctypes.c_int), ("cache_y", ctypes.c_int),
+                ("cache_kv_blocks", ctypes.c_int)]
 
 
 class ig_edit_req(ctypes.Structure):
@@ -269,3 +270,17 @@ def ig_set_plan(ctx: int, mode: int, k: int = 0, comp_s_per_flop: float = 0.0, c
 
 def ig_last_plan(ctx: int) -> int:
     return lib().ig_last_plan(ctx)
+
+
+def y_block_modes(n_blocks: int, kv_blocks: int):
+    """The Y blocks of a hybrid cache (ig.h cache_kv_blocks): the first n_blocks - kv_blocks
+    entries of the bit-reversal order over the next power of two >= n_blocks."""
+    bits = max(0, (n_blocks - 1).bit_length())
+    ny = n_blocks - max(0, min(kv_blocks, n_blocks))
+    out, k = [], 0
+    while len(out) < ny:
+        v = int(format(k, f"0{bits}b")[::-1], 2) if bits else 0
+        if v < n_blocks:
+            out.append(v)
+        k += 1
+    return sorted(out)

@@ -88,3 +88,57 @@ def fill_cache(m, cache, kv: torch.Tensor, latents: torch.Tensor = None):
     src = kv.contiguous().cuda()
     lat = latents.contiguous().cuda().float() if latents is not None else None
     ig.ig_cache_write(m.ctx, cache, src.data_ptr(), lat.data_ptr() if lat is not None else 0)
+
+
+def hybrid_planes(kv, y, ymodes):
+    """Storage order of a hybrid cache step by step (ig.h cache_kv_blocks): block b contributes
+    [K_b, V_b] if it is a K/V block, then [Y_b] if block b or b + 1 is a Y block.
+    kv: [steps, blocks, 2, L_img, H], y: [steps, blocks, L_img, H], ymodes: set of Y blocks
+    -> [steps, planes, L_img, H]."""
+    import torch as _t
+    steps, nb = kv.shape[0], kv.shape[1]
+    out = []
+    for s in range(steps):
+        pl = []
+        for b in range(nb):
+            if b not in ymodes:
+                pl += [kv[s, b, 0], kv[s, b, 1]]
+            if b in ymodes or (b + 1) in ymodes:
+                pl.append(y[s, b])
+        out.append(_t.stack(pl))
+    return _t.stack(out)
+
+
+def split_hybrid(raw, nb, ymodes):
+    """Inverse of hybrid_planes on a numpy [steps, planes, L_img, H] array -> (kv, y) with
+    zeros where a block stores nothing."""
+    steps = raw.shape[0]
+    kv = np.zeros((steps, nb, 2) + raw.shape[2:])
+    y = np.zeros((steps, nb) + raw.shape[2:])
+    for s in range(steps):
+        i = 0
+        for b in range(nb):
+            if b not in ymodes:
+                kv[s, b, 0], kv[s, b, 1] = raw[s, i], raw[s, i + 1]
+                i += 2
+            if b in ymodes or (b + 1) in ymodes:
+                y[s, b] = raw[s, i]
+                i += 1
+    return kv, y
+
+
+def n_planes(nb, ymodes):
+    return sum((0 if b in ymodes else 2) + (1 if (b in ymodes or (b + 1) in ymodes) else 0) for b in range(nb))
+
+
+def cache_raw_numpy(cache, d, n_steps, n_planes, dtype):
+    """Host-tier cache readback of the plane region [steps, planes, L_img, H]."""
+    import ctypes
+    ptr, nbytes, tier = ig.ig_cache_storage(cache)
+    assert tier == ig.IG_CACHE_HOST
+    shape = (n_steps, n_planes, d.L_img, d.hidden)
+    nbytes = int(np.prod(shape)) * (4 if dtype == ig.IG_F32 else 2)
+    raw = np.frombuffer((ctypes.c_char * nbytes).from_address(ptr), dtype=np.uint8).copy()
+    if dtype == ig.IG_F32:
+        return raw.view(np.float32).reshape(shape).astype(np.float64)
+    return (raw.view(np.uint16).astype(np.uint32) << 16).view(np.float32).reshape(shape).astype(np.float64)

@@ -488,3 +488,100 @@ def test_host_pinned_latent_bitwise_equals_device_latent():
     ig.ig_cache_free(cache)
     r.free()
     m.close()
+
+
+# ------------------------------------------------------------------ hybrid K/V + Y cache
+@pytest.mark.parametrize("dtype", [ig.IG_F32, ig.IG_BF16])
+@pytest.mark.parametrize("tier", [ig.IG_CACHE_HOST, ig.IG_CACHE_DEVICE])
+def test_hybrid_cache_batch_end_to_end(dtype, tier):
+    """Hybrid caches (DESIGN reading 30: kv_blocks blocks keep K/V, the others — interleaved in
+    bit-reversal order — are Y blocks) with different splits in one continuous batch, plus a
+    pure K/V cache and an all-ones request; 2 steps vs the oracle's edit_step_y(y_blocks=)."""
+    from gpu_util import hybrid_planes
+    d = synth.FLUX_SMALL
+    sig = [1.0, 0.7, 0.4]
+    tdt = torch.float32 if dtype == ig.IG_F32 else torch.bfloat16
+    rng = np.random.default_rng(21)
+    masks = [synth.blob_mask_count(d, 85, rng), synth.rect_mask_count(d, 45, rng),
+             synth.blob_mask_count(d, 66, rng), np.ones(d.L_img, np.uint8)]
+    splits = [2, 3, None, None]  # kv_blocks per request (None: pure K/V cache / no cache)
+    ms, caches, refs = [], [], []
+    base = Model(d, dtype, opts=ig.ig_ctx_opts(4, 0, 2, 1, 0, 0, 0))
+    reqs = [Request(base, 150 + i, mk) for i, mk in enumerate(masks)]
+    tlat = torch.stack([synth.make_latent(d, 970 + s) for s in range(2)])
+    for i, kvb in enumerate(splits[:3]):
+        kv = synth.make_cache_kv(d, 20 + i, 2, dtype=tdt)
+        yv = synth.make_cache_y(d, 20 + i, 2, dtype=tdt)
+        if kvb is None:
+            c = ig.ig_cache_create(base.ctx, 2, tier)
+            fill_cache(base, c, kv, tlat)
+            refs.append((kv.double().numpy(), None, None))
+        else:
+            m = Model(d, dtype, opts=ig.ig_ctx_opts(4, 0, 2, 1, 0, 0, 1, kvb))
+            ms.append(m)
+            ym = set(ig.y_block_modes(d.n_blocks, kvb))
+            c = ig.ig_cache_create(m.ctx, 2, tier)
+            fill_cache(m, c, hybrid_planes(kv, yv, ym), tlat)
+            refs.append((kv.double().numpy(), yv.double().numpy(), ym))
+        caches.append(c)
+    caches.append(None)
+    for s in range(2):
+        rr = [r.req(i, caches[i], s, sig[s], sig[s + 1]) for i, r in enumerate(reqs)]
+        ig.ig_edit_step(base.ctx, rr, 0)
+    torch.cuda.synchronize()
+    W = base.host_weights()
+    tlh = tlat.double().numpy()
+    for i, r in enumerate(reqs):
+        lat0, txt, cond = r.host_inputs()
+        x = lat0
+        for s in range(2):
+            if i < 3 and refs[i][2] is not None:
+                kvh, yh, ym = refs[i]
+                x = oracle.edit_step_y(d, W, x, r.mask_np, yh[s], tlh[s], sig[s], sig[s + 1], txt, cond,
+                                       y_blocks=ym, kv_cache_step=kvh[s])
+            else:
+                x = oracle.edit_step(d, W, x, r.mask_np, refs[i][0][s] if i < 3 else None, sig[s], sig[s + 1], txt, cond)
+        got = r.latent.double().cpu().numpy()
+        ok, worst = ctol(got, x, RTOL[dtype])
+        assert ok, (i, worst)
+    for c in caches[:3]:
+        ig.ig_cache_free(c)
+    for r in reqs:
+        r.free()
+    for m in ms:
+        m.close()
+    base.close()
+
+
+@pytest.mark.parametrize("kv_blocks", [1, 3])
+def test_hybrid_cache_template_recording_and_plan(kv_blocks):
+    """ig_cache_template on a hybrid ctx records K/V for the K/V blocks and Y_b where block b or
+    b + 1 is a Y block (vs the oracle's dense pass); then an edit with a dense prefix k = 1 on
+    that cache stays on the template trajectory (same inputs)."""
+    from gpu_util import cache_raw_numpy, n_planes, split_hybrid
+    d = synth.FLUX_SMALL
+    sig = [1.0, 0.5, 0.0]
+    m = Model(d, ig.IG_BF16, opts=ig.ig_ctx_opts(2, 0, 4, 1, 0, 0, 1, kv_blocks))
+    W = m.host_weights()
+    ym = set(ig.y_block_modes(d.n_blocks, kv_blocks))
+    rq = Request(m, 160, synth.rect_mask_count(d, 70, np.random.default_rng(16)))
+    lat0, txt, cond = rq.host_inputs()
+    lat_t = rq.latent.clone()
+    cache = ig.ig_cache_template(m.ctx, lat_t.data_ptr(), rq.txt.data_ptr(), rq.cond.data_ptr(), sig)
+    _, okv, _ = oracle.cache_template(d, W, lat0, txt, cond, sig)
+    _, oy, traj = oracle.cache_template_y(d, W, lat0, txt, cond, sig)
+    gkv, gy = split_hybrid(cache_raw_numpy(cache, d, 2, n_planes(d.n_blocks, ym), ig.IG_BF16), d.n_blocks, ym)
+    kvb = [b for b in range(d.n_blocks) if b not in ym]
+    yb = [b for b in range(d.n_blocks) if b in ym or (b + 1) in ym]
+    ok, worst = ctol(gkv[:, kvb], okv[:, kvb], 2e-2)
+    assert ok, ("K/V part", worst)
+    ok, worst = ctol(gy[:, yb], oy[:, yb], 2e-2)
+    assert ok, ("Y part", worst)
+    ig.ig_set_plan(m.ctx, 1, 1)
+    _run_edit(m, [rq], cache, 2, sig)
+    idx = rq.mask_np != 0
+    ok, worst = ctol(rq.latent.double().cpu().numpy()[idx], traj[-1][idx], 2e-2)
+    assert ok, ("edit on the recorded hybrid cache", worst)
+    ig.ig_cache_free(cache)
+    rq.free()
+    m.close()

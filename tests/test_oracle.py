@@ -487,8 +487,8 @@ def test_y_variant_dense_prefix_all_blocks_is_dense_on_combined_input(small_mode
 
 
 def test_hybrid_cache_reduces_to_both_variants_and_is_exact(small_model):
-    # blocks < y_from use K/V, blocks >= y_from use Y (DESIGN reading 30): y_from = N is the
-    # K/V variant, y_from = 0 the Y variant, and any split is exact with same-input caches
+    # a per-block choice of K/V or Y blocks (DESIGN reading 30): no Y block is the K/V variant,
+    # all Y blocks the Y variant (bitwise), and any choice is exact with same-input caches
     d, W = small_model
     lat, txt, cond = _inputs(d, 41)
     tl, _, cond_o = _inputs(d, 42)
@@ -497,16 +497,16 @@ def test_hybrid_cache_reduces_to_both_variants_and_is_exact(small_model):
     _, kv, y = oracle.dense_step(d, W, tl, 0.9, 0.7, txt, cond, record=True, record_y=True)
     kvv = oracle.edit_step(d, W, lat, mask, kv, 0.9, 0.7, txt, cond_o)
     yv = oracle.edit_step_y(d, W, lat, mask, y, tl, 0.9, 0.7, txt, cond_o)
-    hN = oracle.edit_step_y(d, W, lat, mask, y, tl, 0.9, 0.7, txt, cond_o, y_from=d.n_blocks, kv_cache_step=kv)
-    h0 = oracle.edit_step_y(d, W, lat, mask, y, tl, 0.9, 0.7, txt, cond_o, y_from=0, kv_cache_step=kv)
+    hN = oracle.edit_step_y(d, W, lat, mask, y, tl, 0.9, 0.7, txt, cond_o, y_blocks=set(), kv_cache_step=kv)
+    h0 = oracle.edit_step_y(d, W, lat, mask, y, tl, 0.9, 0.7, txt, cond_o, y_blocks={0, 1}, kv_cache_step=kv)
     assert np.array_equal(hN, kvv) and np.array_equal(h0, yv)
-    h1 = oracle.edit_step_y(d, W, lat, mask, y, tl, 0.9, 0.7, txt, cond_o, y_from=1, kv_cache_step=kv)
+    h1 = oracle.edit_step_y(d, W, lat, mask, y, tl, 0.9, 0.7, txt, cond_o, y_blocks={1}, kv_cache_step=kv)
     assert np.max(np.abs(h1 - kvv)) > 1e-6 and np.max(np.abs(h1 - yv)) > 1e-6  # a real mix
     full = lat.copy()
     full[mask == 0] = tl[mask == 0]
     dn, kv_s, y_s = oracle.dense_step(d, W, full, 0.9, 0.7, txt, cond, record=True, record_y=True)
     idx = mask != 0
-    for yf in range(d.n_blocks + 1):
+    for yb in (set(), {0}, {1}, {0, 1}):
         for k in (0, 1):
-            h = oracle.edit_step_y(d, W, lat, mask, y_s, full, 0.9, 0.7, txt, cond, k=k, y_from=yf, kv_cache_step=kv_s)
-            assert np.max(np.abs(h[idx] - dn[idx])) <= 1e-12 * np.abs(dn).max(), (yf, k)
+            h = oracle.edit_step_y(d, W, lat, mask, y_s, full, 0.9, 0.7, txt, cond, k=k, y_blocks=yb, kv_cache_step=kv_s)
+            assert np.max(np.abs(h[idx] - dn[idx])) <= 1e-12 * np.abs(dn).max(), (yb, k)
