@@ -367,7 +367,7 @@ def main():
     ap.add_argument("--no-hbm-tier", action="store_true", help="skip the HBM-resident template run")
     ap.add_argument("--no-fp8", action="store_true", help="skip the FP8-cache run")
     ap.add_argument("--no-y", action="store_true", help="skip the other-cache-kind runs")
-    ap.add_argument("--cache", default="hybrid", choices=["kv", "hybrid", "y"],
+    ap.add_argument("--cache", default=None, choices=["kv", "hybrid", "y"],
                     help="headline cache kind: K/V, hybrid K/V + Y (interleaved Y blocks), Y")
     ap.add_argument("--kv-blocks", type=int, default=-1, help="hybrid: blocks keeping K/V (-1: latency-model choice)")
     ap.add_argument("--mask-lo", type=float, default=0.05)
@@ -420,7 +420,10 @@ def main():
     # Algorithm-1/2 latency models fitted on this GPU; the hybrid split point
     a_c, b_c, a_l, b_l = fit_latency(ig, ctx_kv, d, dev, stream, link_peak)
     kv_auto = choose_kv_blocks(d, a_c, b_c, a_l, args.max_batch, 0.5 * (args.mask_lo + args.mask_hi))
-    kv_blocks = {"kv": None, "y": 0}.get(args.cache, kv_auto if args.kv_blocks < 0 else args.kv_blocks)
+    # default: the hybrid split for a host-tier cache (the link is the other lane); plain K/V
+    # when the cache is HBM-resident (the loads are on-chip gathers, Y would only add compute)
+    cache_kind = args.cache or ("hybrid" if tier == "host" else "kv")
+    kv_blocks = {"kv": None, "y": 0}.get(cache_kind, kv_auto if args.kv_blocks < 0 else args.kv_blocks)
     ctx = ctx_kv if kv_blocks is None else make_y_ctx(kv_blocks)
     t0 = time.time()
     cache = record(ctx, tier)

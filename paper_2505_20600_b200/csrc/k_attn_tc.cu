@@ -71,12 +71,6 @@ __device__ long long g_trace[5][2][40];
 #define TRACE(ev, t, j) do { } while (0)
 #endif
 
-__device__ __forceinline__ float fmax3(float a, float b, float c) {  // FMNMX3 (sm_100)
-  float r;
-  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
-  return r;
-}
-
 __device__ __forceinline__ float ex2_fast(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -247,38 +241,27 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         if (lane == 0 && quad == 0) TRACE(3, t, j);  // S_t(j) seen
         tc::tc_fence_after();
         uint32_t r[128];
+        tc::tmem_ld32(tS + 0, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
+        tc::tmem_ld32(tS + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
+        tc::tmem_ld32(tS + 64, *reinterpret_cast<uint32_t(*)[32]>(&r[64]));
+        tc::tmem_ld32(tS + 96, *reinterpret_cast<uint32_t(*)[32]>(&r[96]));
+        tc::tmem_ld_wait();
         const int valid = a.L - j * BKV;  // keys >= L are masked (ragged last tile only)
-        // row max as 8 independent 3-input chains; the second half of S is loaded from TMEM
-        // while the first half is reduced
+        // row max as 8 independent partial chains (latency, one warp per SMSP in this phase)
         float pm[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u) pm[u] = -INFINITY;
-        tc::tmem_ld32(tS + 0, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
-        tc::tmem_ld32(tS + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
-        tc::tmem_ld_wait();
-        tc::tmem_ld32(tS + 64, *reinterpret_cast<uint32_t(*)[32]>(&r[64]));
-        tc::tmem_ld32(tS + 96, *reinterpret_cast<uint32_t(*)[32]>(&r[96]));
-        if (valid >= BKV) {
-#pragma unroll
-          for (int i = 0; i < 64; i += 16)
-#pragma unroll
-            for (int u = 0; u < 8; ++u) pm[u] = fmax3(pm[u], __uint_as_float(r[i + u]), __uint_as_float(r[i + 8 + u]));
-        }
-        tc::tmem_ld_wait();
         if (valid < BKV) {
 #pragma unroll
           for (int i = 0; i < 128; ++i)
             if (i >= valid) r[i] = __float_as_uint(-INFINITY);
-#pragma unroll
-          for (int i = 0; i < 64; i += 16)
-#pragma unroll
-            for (int u = 0; u < 8; ++u) pm[u] = fmax3(pm[u], __uint_as_float(r[i + u]), __uint_as_float(r[i + 8 + u]));
         }
 #pragma unroll
-        for (int i = 64; i < 128; i += 16)
+        for (int i = 0; i < 128; i += 8)
 #pragma unroll
-          for (int u = 0; u < 8; ++u) pm[u] = fmax3(pm[u], __uint_as_float(r[i + u]), __uint_as_float(r[i + 8 + u]));
-        const float mx = fmaxf(fmax3(pm[0], pm[1], pm[2]), fmax3(fmax3(pm[3], pm[4], pm[5]), pm[6], pm[7]));
+          for (int u = 0; u < 8; ++u) pm[u] = fmaxf(pm[u], __uint_as_float(r[i + u]));
+        const float mx = fmaxf(fmaxf(fmaxf(pm[0], pm[1]), fmaxf(pm[2], pm[3])),
+                               fmaxf(fmaxf(pm[4], pm[5]), fmaxf(pm[6], pm[7])));
         // scores in log2 units: s * scale * log2(e).  Keep the stale max unless it grew by
         // more than the threshold (per row).
         const float mxs = mx * scale_log2;
@@ -295,11 +278,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           const float2 pp = (i < NPOLY) ? ex2_poly2(x) : make_float2(ex2_fast(x.x), ex2_fast(x.y));
           acc[i & 3] = __fadd2_rn(acc[i & 3], pp);
           r[i] = pack_bf16(pp.x, pp.y);
-          if (i == 31) tc::tmem_st32(tS + 0, &r[0]);  // first half of P goes out while the rest computes
         }
         const float2 s01 = __fadd2_rn(acc[0], acc[1]), s23 = __fadd2_rn(acc[2], acc[3]);
         const float2 s4 = __fadd2_rn(s01, s23);
         const float sum = s4.x + s4.y;
+        tc::tmem_st32(tS + 0, &r[0]);
         tc::tmem_st32(tS + 32, &r[32]);
         if (j > 0 && __any_sync(0xffffffffu, m_use > m)) {
 #pragma unroll 1
