@@ -46,7 +46,11 @@ struct AC {                                     // per-head-dim configuration (d
   static constexpr int SMEM_BYTES = 2 * Q_BYTES + (KSTAGES + VSTAGES) * KV_BYTES + 1024 + 256;
 };
 constexpr float RESCALE_THRESHOLD = 8.0f;       // log2 units
-constexpr int NPOLY = 0;  // pairs per key tile on ex2_poly2 (measured: MUFU is not the limiter; 0 is fastest)
+// exp2 on the FMA pipe (ex2_poly2) for one pair in 16, interleaved with the MUFU pairs
+// (ncu A/B, batch-8 shape: 0.939 vs 0.954 ms; 8 or 16 pairs in 64 are slower)
+#ifndef POLY_AT
+#define POLY_AT(i) (((i) & 15) == 15)
+#endif  // pairs per key tile on ex2_poly2 (measured: MUFU is not the limiter; 0 is fastest)
 
 struct Bars {
   uint64_t q_full;
@@ -275,7 +279,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 #pragma unroll
         for (int i = 0; i < 64; ++i) {  // in-place pack: r[i] <- bf16x2(p[2i], p[2i+1])
           const float2 x = __ffma2_rn(make_float2(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1])), sc2, nm2);
-          const float2 pp = (i < NPOLY) ? ex2_poly2(x) : make_float2(ex2_fast(x.x), ex2_fast(x.y));
+          const float2 pp = POLY_AT(i) ? ex2_poly2(x) : make_float2(ex2_fast(x.x), ex2_fast(x.y));
           acc[i & 3] = __fadd2_rn(acc[i & 3], pp);
           r[i] = pack_bf16(pp.x, pp.y);
         }
