@@ -130,6 +130,44 @@ def test_flux_same_trajectory_bitwise_and_batch_invariance(flux):
 
 
 
+def test_flux_hybrid_cache_same_trajectory_and_batch_invariance(flux):
+    """Full Flux shape, the bench's hybrid cache (37 K/V blocks, 20 interleaved Y blocks,
+    DESIGN reading 30) recorded by ig_cache_template from the request's own inputs: the edited
+    masked rows match the dense step (C-TOL: Y blocks recompute K/V from the bf16 Y cache, so
+    not bitwise), unmasked rows are untouched, and the request alone equals the request inside
+    a mixed batch (hybrid + K/V + all-ones) bitwise."""
+    ptrs = [flux.W[n].data_ptr() for n, _, _ in synth.weight_table(D)]
+    ctx = ig.ig_ctx_create(flux.desc, ptrs, 0, ig.ig_ctx_opts(8, 8 * D.L, 2, 1, 0, 0, 1, 37))
+    sig = (1.0, 0.96)
+    rng = np.random.default_rng(6)
+    mask = synth.blob_mask_count(D, 1100, rng)
+    a = Request(flux, 34, mask)
+    lat_dense = a.latent.clone()
+    cache = ig.ig_cache_template(ctx, lat_dense.data_ptr(), a.txt.data_ptr(), a.cond.data_ptr(), sig,
+                                 ig.IG_CACHE_DEVICE, 0)
+    ig.ig_edit_step(ctx, [a.req(0, cache, 0, *sig)], 0)
+    torch.cuda.synchronize()
+    idx = np.flatnonzero(mask)
+    ok, worst = ctol(a.latent.double().cpu().numpy()[idx], lat_dense.double().cpu().numpy()[idx], 2e-2)
+    assert ok, worst
+    un = torch.from_numpy(np.flatnonzero(mask == 0)).cuda()
+    assert torch.equal(a.latent[un], a.latent0[un])
+    alone = a.latent.clone()
+    kvcache = ig.ig_cache_template(flux.ctx, a.latent0.clone().data_ptr(), a.txt.data_ptr(), a.cond.data_ptr(), sig,
+                                   ig.IG_CACHE_DEVICE, 0)
+    a.latent.copy_(a.latent0)
+    b = Request(flux, 35, synth.rect_mask_count(D, 900, rng))
+    c = Request(flux, 36, np.ones(D.L_img, np.uint8))
+    ig.ig_edit_step(ctx, [b.req(0, kvcache, 0, *sig), c.req(1, None, 0, *sig), a.req(6, cache, 0, *sig)], 0)
+    torch.cuda.synchronize()
+    assert torch.equal(a.latent, alone)
+    ig.ig_cache_free(cache)
+    ig.ig_cache_free(kvcache)
+    for r in (a, b, c):
+        r.free()
+    ig.ig_ctx_destroy(ctx)
+
+
 def test_sd3_teacher_forced_blocks():
     """SD3-medium-shaped (BASELINE configs[1]) joint blocks at full width (H=1536, d=64,
     333 text tokens, context-pre-only last block) through ig_debug_block vs the oracle,
