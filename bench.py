@@ -185,6 +185,7 @@ def run_loop(ig, ctx, batch, cache, sig, steps, stream, profile=False, e2e=None)
     h2d = d2h = 0
     evs, plans = [], []
     alg_flops = 0.0
+    host_s = 0.0
     start = torch.cuda.Event(enable_timing=True)
     end = torch.cuda.Event(enable_timing=True)
     if profile:
@@ -196,7 +197,9 @@ def run_loop(ig, ctx, batch, cache, sig, steps, stream, profile=False, e2e=None)
         # e2e: the public API on HOST buffers — each request's latent lives in pinned host memory
         # and the step's gather/scatter kernels read its masked rows and write the updated rows
         # in place over the host link (no device copy of the latent exists)
+        th = time.perf_counter()
         ig.ig_edit_step(ctx, batch.reqs(cache, sig, e2e), stream.cuda_stream)
+        host_s += time.perf_counter() - th
         plans.append(ig.ig_last_plan(ctx))
         alg_flops += sum(N_BLOCKS_FLOPS(batch.d, r.n_m) for r in batch.slots)
         st = ig.ig_last_stats(ctx)
@@ -216,7 +219,9 @@ def run_loop(ig, ctx, batch, cache, sig, steps, stream, profile=False, e2e=None)
     if profile:
         ig.ig_profile_enable(ctx, False)
     per_step = [a.elapsed_time(b) for a, b in evs]
-    return Leg(start.elapsed_time(end), rsteps, launches, per_step, prof, h2d, d2h, plans, alg_flops)
+    lg = Leg(start.elapsed_time(end), rsteps, launches, per_step, prof, h2d, d2h, plans, alg_flops)
+    lg.host_ms_per_step = 1e3 * host_s / max(steps, 1)
+    return lg
 
 
 class Leg:
@@ -367,6 +372,7 @@ def main():
     ap.add_argument("--no-hbm-tier", action="store_true", help="skip the HBM-resident template run")
     ap.add_argument("--no-fp8", action="store_true", help="skip the FP8-cache run")
     ap.add_argument("--no-y", action="store_true", help="skip the other-cache-kind runs")
+    ap.add_argument("--no-profile", action="store_true", help="no per-launch event timing in the timed window")
     ap.add_argument("--cache", default=None, choices=["kv", "hybrid", "y"],
                     help="headline cache kind: K/V, hybrid K/V + Y (interleaved Y blocks), Y")
     ap.add_argument("--kv-blocks", type=int, default=-1, help="hybrid: blocks keeping K/V (-1: latency-model choice)")
@@ -478,7 +484,9 @@ def main():
     # pinned host memory
     plan_mode = {"model": 2, "none": 0}.get(args.plan, 1)
     ig.ig_set_plan(ctx, plan_mode, 0 if plan_mode != 1 else int(args.plan), a_c, b_c, a_l, b_l)
-    main_leg = leg(ctx, cache, clk=Clocks(local))
+    main_leg = leg(ctx, cache, clk=Clocks(local), profile=not args.no_profile)
+    if main_leg.prof is None:  # --no-profile (diagnostic): no per-kernel numbers
+        main_leg.prof = {k: {"ms": 0.0, "flops": 0.0, "bytes": 0.0, "launches": 0} for k in ig.KCLASS}
     ms, ms_max, value, prof, per_step = main_leg.ms, main_leg.ms_max, main_leg.value, main_leg.prof, main_leg.per_step
     launches, h2d, clk = main_leg.launches, main_leg.h2d, main_leg.clk
 
@@ -604,7 +612,7 @@ def main():
         "host_link": {"achieved_GBps": round(h2d / (ms * 1e-3) / 1e9, 2), "peak_GBps": link_peak,
                       "frac": round(h2d / (ms * 1e-3) / 1e9 / link_peak, 4) if link_peak else None,
                       "peak_kind": "pinned H2D cudaMemcpyAsync 512 MiB x8, measured in this run",
-                      "copy_lane_busy": round(prof["copy"]["ms"] / ms, 4),
+                      "copy_lane_busy": round(prof["copy"]["ms"] / ms, 4) if prof["copy"]["ms"] else None,
                       "GBps_while_busy": round(prof["copy"]["bytes"] / (prof["copy"]["ms"] * 1e-3) / 1e9, 2)
                       if prof["copy"]["ms"] else None},
         "hbm_tier": hbm,
@@ -612,6 +620,7 @@ def main():
         **alt,
         "speedup_hbm_tier_vs_dense": round(hbm["value"] / dense, 3) if (hbm and dense) else None,
         "gpu_launches": int(launches),
+        "host_enqueue_ms_per_step": round(main_leg.host_ms_per_step, 3),
         "clocks": clk,
         "e2e": e2e,
         "setup_s": {"total": round(time.time() - t_setup, 1), "template": round(t_template, 1)},

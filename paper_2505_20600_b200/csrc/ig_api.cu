@@ -1348,7 +1348,8 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
     g.B = B; g.ldb = K; g.bias = bias;
     g.M = r1 - r0; g.N = N; g.K = K; g.epi = epi; g.out_f32 = out_f32;
     g.ri = ctx->ri; g.ri_off = r0;
-    g.precise_gelu = getenv("IG_PRECISE_GELU") != nullptr;
+    static const bool precise_gelu = getenv("IG_PRECISE_GELU") != nullptr;  // debug switch, read once
+    g.precise_gelu = precise_gelu;
     if (epi == EPI_GATED_RES) {
       g.C = (float*)Cp + (long long)r0 * ldc; g.gate = gate; g.gate_ld = mld;
     } else {

@@ -25,6 +25,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <mutex>
+#include <vector>
 #include <cstdlib>
 #include "kernels.h"
 #include "tc_common.cuh"
@@ -373,7 +374,19 @@ void launch_attn_tc(const AttnArgs& a, cudaStream_t st) {
   init_attn();
   const long long H = (long long)a.heads * a.head_dim;
   CUtensorMap tq, tkv;
-  {
+  // encoded maps cached per (pointer, shape) like the GEMM's (host enqueue cost)
+  struct Ent { const void* p; long long x, y, z; CUtensorMap m; };
+  thread_local std::vector<Ent> cache;
+  auto lookup = [&](const void* p, long long x, long long y, long long z, CUtensorMap* out) {
+    for (auto& e : cache)
+      if (e.p == p && e.x == x && e.y == y && e.z == z) { *out = e.m; return true; }
+    return false;
+  };
+  auto remember = [&](const void* p, long long x, long long y, long long z, const CUtensorMap& m) {
+    if (cache.size() > 256) cache.clear();
+    cache.push_back(Ent{p, x, y, z, m});
+  };
+  if (!lookup(a.Q, H, a.q_rows, a.ldq, &tq)) {
     cuuint64_t dims[2] = {(cuuint64_t)H, (cuuint64_t)a.q_rows};
     cuuint64_t strides[1] = {(cuuint64_t)(a.ldq * 2)};
     cuuint32_t box[2] = {64, 128};
@@ -381,8 +394,9 @@ void launch_attn_tc(const AttnArgs& a, cudaStream_t st) {
     g_enc(&tq, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(a.Q), dims, strides, box, es,
           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    remember(a.Q, H, a.q_rows, a.ldq, tq);
   }
-  {
+  if (!lookup(a.kv_arena, H, a.L, -1, &tkv)) {
     // K/V arena as 3-D [planes][L][H]: plane p = K or V of one (slot, ring buffer); rows >= L
     // are out of bounds (zero fill) for the ragged last key tile.
     cuuint64_t dims[3] = {(cuuint64_t)H, (cuuint64_t)a.L, (cuuint64_t)(1u << 20)};
@@ -392,6 +406,7 @@ void launch_attn_tc(const AttnArgs& a, cudaStream_t st) {
     g_enc(&tkv, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(a.kv_arena), dims, strides, box, es,
           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    remember(a.kv_arena, H, a.L, -1, tkv);
   }
   dim3 grid((a.max_qlen + 2 * BQ - 1) / (2 * BQ), a.heads, a.nseg);
   const float scale_log2 = a.scale * 1.4426950408889634f;

@@ -15,6 +15,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <mutex>
+#include <unordered_map>
 #include <cstdlib>
 #include "kernels.h"
 #include "tc_common.cuh"
@@ -548,7 +549,34 @@ void init_driver() {
 
 // 2-D bf16 tensor map over a row-major [rows, cols] matrix with leading dimension ld, box
 // [box_rows, 64 cols], 128-byte swizzle; out-of-bounds reads fill zeros.
+// Encoded maps are cached per (pointer, shape, box): the weights' maps never change and the
+// workspaces' recur every step, so the driver encode runs once instead of twice per launch
+// (host enqueue cost matters for small single-request steps).
+struct TmapKey {
+  const void* ptr; long long rows, cols, ld; int box;
+  bool operator==(const TmapKey& o) const {
+    return ptr == o.ptr && rows == o.rows && cols == o.cols && ld == o.ld && box == o.box;
+  }
+};
+struct TmapHash {
+  size_t operator()(const TmapKey& k) const {
+    size_t h = std::hash<const void*>()(k.ptr);
+    for (long long v : {k.rows, k.cols, k.ld, (long long)k.box}) h = h * 1000003u ^ std::hash<long long>()(v);
+    return h;
+  }
+};
+bool encode_tmap(CUtensorMap* m, const void* ptr, long long rows, long long cols, long long ld, int box_rows);
 bool make_tmap(CUtensorMap* m, const void* ptr, long long rows, long long cols, long long ld, int box_rows) {
+  thread_local std::unordered_map<TmapKey, CUtensorMap, TmapHash> cache;
+  const TmapKey k{ptr, rows, cols, ld, box_rows};
+  auto it = cache.find(k);
+  if (it != cache.end()) { *m = it->second; return true; }
+  if (!encode_tmap(m, ptr, rows, cols, ld, box_rows)) return false;
+  if (cache.size() > 8192) cache.clear();
+  cache.emplace(k, *m);
+  return true;
+}
+bool encode_tmap(CUtensorMap* m, const void* ptr, long long rows, long long cols, long long ld, int box_rows) {
   cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
   cuuint64_t strides[1] = {(cuuint64_t)(ld * 2)};
   cuuint32_t box[2] = {64, (cuuint32_t)box_rows};

@@ -585,3 +585,36 @@ def test_hybrid_cache_template_recording_and_plan(kv_blocks):
     ig.ig_cache_free(cache)
     rq.free()
     m.close()
+
+
+@pytest.mark.parametrize("k", [2])
+def test_fp8_cache_with_dense_prefix(k):
+    """FP8 K/V cache (N4) under the Algorithm-1 dense prefix (N1): the oracle's planned step
+    on the fp8-round-tripped cache; batch of 2, 2 steps."""
+    d = synth.FLUX_SMALL
+    sig = [1.0, 0.7, 0.4]
+    m = Model(d, ig.IG_BF16, opts=ig.ig_ctx_opts(4, 0, 4, 1, 0, 1))
+    ig.ig_set_plan(m.ctx, 1, k)
+    W = m.host_weights()
+    rng = np.random.default_rng(31)
+    masks = [synth.blob_mask_count(d, 75, rng), synth.rect_mask_count(d, 33, rng)]
+    reqs = [Request(m, 170 + i, mk) for i, mk in enumerate(masks)]
+    kv = synth.make_cache_kv(d, 11, 2, dtype=torch.bfloat16, device="cuda")
+    tlat = torch.stack([synth.make_latent(d, 980 + s) for s in range(2)]).cuda()
+    cache = ig.ig_cache_create(m.ctx, 2, ig.IG_CACHE_HOST)
+    ig.ig_cache_write(m.ctx, cache, kv.data_ptr(), tlat.data_ptr())
+    kvh = oracle.fp8_kv_roundtrip(kv.float().cpu().numpy(), d.heads)
+    tlh = tlat.double().cpu().numpy()
+    _run_edit(m, reqs, cache, 2, sig)
+    assert ig.ig_last_plan(m.ctx) == k
+    for r in reqs:
+        lat0, txt, cond = r.host_inputs()
+        x = lat0
+        for s in range(2):
+            x = oracle.edit_step_planned(d, W, x, r.mask_np, kvh[s], tlh[s], k, sig[s], sig[s + 1], txt, cond)
+        ok, worst = ctol(r.latent.double().cpu().numpy(), x, 2e-2)
+        assert ok, worst
+    ig.ig_cache_free(cache)
+    for r in reqs:
+        r.free()
+    m.close()
