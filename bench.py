@@ -387,6 +387,8 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
         import torch.distributed as dist
+        if args.impl == "ours":
+            torch.cuda.set_device(local)  # the NCCL communicator binds to this rank's GPU
         dist.init_process_group("nccl" if args.impl == "ours" else "gloo")
     if args.impl == "reference":
         run_reference(args, rank)
