@@ -38,6 +38,9 @@ def main():
     ap.add_argument("--depth", type=int, default=8)
     ap.add_argument("--tier", default=None, choices=["host", "device"])
     ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--cache", default="hybrid", choices=["kv", "hybrid"])
+    ap.add_argument("--simulate-gpus", type=int, default=0,
+                    help="also print the latency model's prediction of every policy on this many GPUs")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -52,16 +55,22 @@ def main():
     tier = args.tier or ("host" if world == 1 else "device")
     link = bench.measure_h2d(dev)
     W, ptrs = bench.build_model(d, dev)
-    opts = ig.ig_ctx_opts(args.max_batch, args.max_batch * d.L, args.depth, 1, 0, 0)
-    ctx = ig.ig_ctx_create(ig.make_desc(d, ig.IG_BF16), ptrs, local, opts)
+    opts = ig.ig_ctx_opts(max(args.max_batch, 4), max(args.max_batch, 4) * d.L, args.depth, 1, 0, 0)
+    ctx_kv = ig.ig_ctx_create(ig.make_desc(d, ig.IG_BF16), ptrs, local, opts)
     sig = synth.flow_sigmas(bench.N_STEPS)
     tl = synth.make_latent(d, 10 ** 6, dev)
     tt = synth.make_txt(d, 10 ** 6, dev, torch.bfloat16)
     tc = synth.make_cond(d, 10 ** 6, dev)
+    stream = torch.cuda.Stream(device=dev)
+    a_c, b_c, a_l, b_l = bench.fit_latency(ig, ctx_kv, d, dev, stream, link if tier == "host" else 1e6)
+    kv_blocks = None
+    ctx = ctx_kv
+    if args.cache == "hybrid" and tier == "host":  # the bench's hybrid K/V + Y cache (DESIGN reading 30)
+        kv_blocks = bench.choose_kv_blocks(d, a_c, b_c, a_l, args.max_batch, 0.325)
+        ctx = ig.ig_ctx_create(ig.make_desc(d, ig.IG_BF16), ptrs, local,
+                               ig.ig_ctx_opts(args.max_batch, args.max_batch * d.L, args.depth, 1, 0, 0, 1, kv_blocks))
     cache = ig.ig_cache_template(ctx, tl.data_ptr(), tt.data_ptr(), tc.data_ptr(), sig,
                                  ig.IG_CACHE_HOST if tier == "host" else ig.IG_CACHE_DEVICE, 0)
-    stream = torch.cuda.Stream(device=dev)
-    a_c, b_c, a_l, b_l = bench.fit_latency(ig, ctx, d, dev, stream, link if tier == "host" else 1e6)
     sm = S.StepModel(d, LatencyModel(a_c, b_c, a_l, b_l))
     # predicted per-GPU capacity at a full batch of the mean mask, and the offered rate
     n_mean = int(round(0.325 * d.L_img)) if args.skew is None else int(round((0.05 + 0.55 * (0.25 if args.skew == "public" else 1 / 9)) * d.L_img))
@@ -107,8 +116,18 @@ def main():
                "requests": len(rows), "denoise_steps_run": steps,
                "throughput_images_per_s": round(len(rows) / makespan, 4),
                "measured": S.summarize(lat, que), "predicted_by_latency_model": S.summarize(plat, pque),
+               "cache": args.cache if kv_blocks is not None else "kv", "kv_blocks": kv_blocks,
                "latency_model": {"comp_s_per_tflop": a_c * 1e12, "comp_s": b_c, "load_s_per_GB": a_l * 1e9},
                "data": "synthetic", "dtype": "bf16"}
+        if args.simulate_gpus:  # the model's view of the routing policies at cluster scale
+            big = S.poisson_trace(args.load * cap * args.simulate_gpus, 8 * args.requests, d.L_img,
+                                  seed=args.seed + 1, skew=args.skew)
+            sim = {}
+            for pol in S.POLICIES:
+                _, rec_p = S.simulate_cluster(big, args.simulate_gpus, pol, sm, args.max_batch, bench.N_STEPS)
+                sim[pol] = S.summarize([v[2] - v[0] for v in rec_p.values()], [v[1] - v[0] for v in rec_p.values()])
+            out["simulated_policies"] = {"n_gpus": args.simulate_gpus, "requests": len(big),
+                                         "note": "latency-model simulation (not measured)", **sim}
         print(json.dumps(out))
     if world > 1:
         torch.distributed.barrier()
