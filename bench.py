@@ -316,6 +316,40 @@ def cpu_cores():
         return len(os.sched_getaffinity(0))
 
 
+def torch_dense_block_ms(d, dev, rows, iters=5):
+    """Context only: one Flux single-stream block in plain PyTorch (cuBLAS GEMMs,
+    SDPA flash attention, eager LN/modulation/GELU; no RoPE/QK-norm) over `rows` query rows of a
+    dense batch of rows // L requests.  Never called by libig; shows whether the library's
+    kernels are at least library-class on the same shapes."""
+    import torch.nn.functional as F
+    H, Fh, L = d.hidden, d.mlp_hidden, d.L
+    nb = rows // L
+    g = torch.Generator(device=dev).manual_seed(0)
+    w1 = torch.randn(3 * H + Fh, H, device=dev, dtype=torch.bfloat16, generator=g) / H ** 0.5
+    w2 = torch.randn(H, H + Fh, device=dev, dtype=torch.bfloat16, generator=g) / (H + Fh) ** 0.5
+    x = torch.randn(rows, H, device=dev, dtype=torch.float32, generator=g)
+    mod = torch.randn(3, H, device=dev, dtype=torch.float32, generator=g) * 0.1
+
+    def block(x):
+        h = (F.layer_norm(x, (H,)) * (1 + mod[1]) + mod[0]).bfloat16()
+        y = h @ w1.t()
+        q, k, v = (y[:, i * H:(i + 1) * H].view(nb, L, d.heads, H // d.heads).transpose(1, 2) for i in range(3))
+        o = F.scaled_dot_product_attention(q, k, v).transpose(1, 2).reshape(rows, H)
+        u = F.gelu(y[:, 3 * H:], approximate="tanh")
+        return x + mod[2] * (torch.cat([o, u], 1) @ w2.t()).float()
+
+    for _ in range(2):
+        block(x)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+    e0.record()
+    for _ in range(iters):
+        block(x)
+    e1.record()
+    e1.synchronize()
+    return e0.elapsed_time(e1) / iters
+
+
 def cpu_baseline(d):
     td, ts, n_m = oracle_sample(d, 0.2)
     step_s = d.n_double * td + d.n_single * ts
@@ -551,6 +585,7 @@ def main():
 
     # dense comparison step (all-ones masks, no cache) on the same GPUs and kernels
     dense = None
+    torch_ctx = None
     if args.dense_steps > 0:
         dbatch = Batch(ig, ctx_kv, d, dev, args.max_batch, args.max_batch + 2, rid0=rank * 100000 + 50000, dense=True)
         run_loop(ig, ctx_kv, dbatch, None, sig, 1, stream)
@@ -559,6 +594,13 @@ def main():
         barrier()
         ms_d, rs_d = reduce_max_sum(ld.ms, ld.rsteps)
         dense = rs_d / N_STEPS / (ms_d / 1e3)
+        dense_block_ms = ld.ms / args.dense_steps / d.n_blocks
+        torch_ctx = None
+        if world == 1 and d.n_single > 0:
+            torch_ctx = {"torch_single_block_ms": round(torch_dense_block_ms(d, dev, args.max_batch * d.L), 3),
+                         "ours_dense_step_ms_per_block": round(dense_block_ms, 3),
+                         "note": "context only: plain PyTorch (cuBLAS + SDPA) Flux single block over the dense "
+                                 "batch; ours = whole dense step / blocks (includes conditioning, RoPE, QK-norm)"}
 
     if rank != 0:
         if world > 1:
@@ -593,6 +635,7 @@ def main():
                      "frac_of_burst": round(gemm_tf / pk_burst, 4)},
         "attn_roofline": {"achieved": round(attn_tf, 1), "unit": "TFLOP/s", "frac": round(attn_tf / pk_sus, 4)},
         "kernel_share_of_step": shares,
+        "compute_lane_busy": round(sum(v["ms"] for k, v in prof.items() if k != "copy") / ms, 4),
         "step_roofline": {"bound": "tensor", "unit": "TFLOP/s", "peak": pk_sus,
                           "alg_tflop_per_step": round(main_leg.alg_flops / args.steps / 1e12, 2),
                           "achieved": round(main_leg.alg_flops / (ms * 1e-3) / 1e12, 1),
@@ -610,6 +653,7 @@ def main():
                         "p10": round(float(np.percentile(per_step, 10)), 3),
                         "p90": round(float(np.percentile(per_step, 90)), 3)},
         "dense_images_per_s": round(dense, 4) if dense else None,
+        "dense_vs_torch_context": torch_ctx,
         "speedup_vs_dense": round(value / dense, 3) if dense else None,
         "host_link": {"achieved_GBps": round(h2d / (ms * 1e-3) / 1e9, 2), "peak_GBps": link_peak,
                       "frac": round(h2d / (ms * 1e-3) / 1e9 / link_peak, 4) if link_peak else None,

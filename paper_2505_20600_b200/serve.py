@@ -82,8 +82,10 @@ class StepModel:
     over the blocks with C_w = Comp(sum of masked FLOPs), C_w/o = Comp(dense FLOPs),
     L = Load(sum of cached bytes)."""
 
-    def __init__(self, desc, model: LatencyModel, elem_bytes: int = 2):
-        self.desc, self.model, self.eb = desc, model, elem_bytes
+    def __init__(self, desc, model: LatencyModel, elem_bytes: int = 2, y_frac: float = 0.0):
+        """y_frac: fraction of Y blocks of a hybrid cache (DESIGN reading 30): they move one
+        plane instead of two and recompute the unmasked rows' K/V (4 n_u H^2 flops)."""
+        self.desc, self.model, self.eb, self.y_frac = desc, model, elem_bytes, y_frac
         self.N = desc.n_double + desc.n_single
         self.L_img = desc.grid_h * desc.grid_w
         self._memo: Dict[tuple, float] = {}
@@ -94,9 +96,10 @@ class StepModel:
         key = tuple(sorted(batch))
         v = self._memo.get(key)
         if v is None:
-            f_w = sum(block_flops(self.desc, n) for n in batch)
+            H = self.desc.hidden
+            f_w = sum(block_flops(self.desc, n) + self.y_frac * 4.0 * (self.L_img - n) * H * H for n in batch)
             f_wo = len(batch) * block_flops(self.desc, self.L_img)
-            b = sum(block_load_bytes(self.desc, n, self.eb) for n in batch)
+            b = (1.0 - 0.5 * self.y_frac) * sum(block_load_bytes(self.desc, n, self.eb) for n in batch)
             v = algorithm1(self.N, self.model.comp(f_w), self.model.comp(f_wo), self.model.load(b))[3]
             self._memo[key] = v
         return v

@@ -71,7 +71,8 @@ def main():
                                ig.ig_ctx_opts(args.max_batch, args.max_batch * d.L, args.depth, 1, 0, 0, 1, kv_blocks))
     cache = ig.ig_cache_template(ctx, tl.data_ptr(), tt.data_ptr(), tc.data_ptr(), sig,
                                  ig.IG_CACHE_HOST if tier == "host" else ig.IG_CACHE_DEVICE, 0)
-    sm = S.StepModel(d, LatencyModel(a_c, b_c, a_l, b_l))
+    y_frac = 0.0 if kv_blocks is None else (d.n_blocks - kv_blocks) / d.n_blocks
+    sm = S.StepModel(d, LatencyModel(a_c, b_c, a_l, b_l), y_frac=y_frac)
     # predicted per-GPU capacity at a full batch of the mean mask, and the offered rate
     n_mean = int(round(0.325 * d.L_img)) if args.skew is None else int(round((0.05 + 0.55 * (0.25 if args.skew == "public" else 1 / 9)) * d.L_img))
     cap = args.max_batch / (bench.N_STEPS * sm.step([n_mean] * args.max_batch))
