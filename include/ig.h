@@ -230,6 +230,8 @@ typedef struct {
   long long d2d_bytes;        /* cache bytes copied device->device          */
   long long d2h_bytes;        /* cache bytes recorded device->host          */
   long long rows;             /* packed query rows M                         */
+  long long host_ns;          /* host time spent enqueueing the call, not counting the wait for
+                                 a free descriptor slot (back-pressure from the GPU)            */
 } ig_stats;
 ig_status ig_last_stats(const ig_ctx* ctx, ig_stats* out);
 

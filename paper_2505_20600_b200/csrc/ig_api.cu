@@ -15,6 +15,7 @@
 #include <cstring>
 #include <cstdlib>
 #include <mutex>
+#include <chrono>
 #include <string>
 #include <vector>
 
@@ -1084,6 +1085,7 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
   const int b0 = rng.b0, b1 = rng.b1 < 0 ? nb : rng.b1;
   const long long es = (long long)ctx->esz;
   ctx->stats = ig_stats{};
+  auto t_host0 = std::chrono::steady_clock::now();
   // ---- host validation (nothing enqueued before this passes) ----
   if (n < 0 || n > ctx->o.max_batch) return set_err(IG_EINVAL, "n=%d outside [0, max_batch=%d]", n, ctx->o.max_batch);
   if (n > 0 && !reqs) return set_err(IG_EINVAL, "reqs is NULL");
@@ -1157,7 +1159,11 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
   // ---- descriptors -> pinned staging -> device (one small H2D) ----
   const int si = ctx->stage_i;
   ctx->stage_i = (si + 1) % NSTAGE;
-  CUDA_TRY(cudaEventSynchronize(ctx->ev_stage[si]));  // the step that used this slot is done
+  {
+    const auto w0 = std::chrono::steady_clock::now();
+    CUDA_TRY(cudaEventSynchronize(ctx->ev_stage[si]));  // the step that used this slot is done
+    t_host0 += std::chrono::steady_clock::now() - w0;  // back-pressure is not enqueue time
+  }
   char* hs = ctx->h_stage[si];
   char* ds = ctx->d_stage[si];
   ReqDev* hreq = (ReqDev*)hs;
@@ -1572,6 +1578,7 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
                                                                                  : ctx->ev_copy[(b1 - 1) % R], 0));
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_err(IG_ECUDA, "step enqueue: %s", cudaGetErrorString(e));
+  stats.host_ns = std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - t_host0).count();
   return IG_OK;
 }
 

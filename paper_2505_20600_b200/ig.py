@@ -64,7 +64,7 @@ class ig_edit_req(ctypes.Structure):
 class ig_stats(ctypes.Structure):
     _fields_ = [("kernel_launches", ctypes.c_longlong), ("h2d_bytes", ctypes.c_longlong),
                 ("d2d_bytes", ctypes.c_longlong), ("d2h_bytes", ctypes.c_longlong),
-                ("rows", ctypes.c_longlong)]
+                ("rows", ctypes.c_longlong), ("host_ns", ctypes.c_longlong)]
 
 
 class ig_prof_entry(ctypes.Structure):
