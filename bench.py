@@ -406,6 +406,8 @@ def main():
     ap.add_argument("--no-fp8", action="store_true", help="skip the FP8-cache run")
     ap.add_argument("--no-y", action="store_true", help="skip the other-cache-kind runs")
     ap.add_argument("--no-profile", action="store_true", help="no per-launch event timing in the timed window")
+    ap.add_argument("--graphs", action="store_true",
+                    help="replay steps as CUDA graphs (HBM-resident caches; needs --no-profile to take effect)")
     ap.add_argument("--cache", default=None, choices=["kv", "hybrid", "y"],
                     help="headline cache kind: K/V, hybrid K/V + Y (interleaved Y blocks), Y")
     ap.add_argument("--kv-blocks", type=int, default=-1, help="hybrid: blocks keeping K/V (-1: latency-model choice)")
@@ -439,7 +441,7 @@ def main():
     link_peak = measure_h2d(dev)
     W, ptrs = build_model(d, dev)
     mb_kv = max(args.max_batch, 4)  # the latency fit runs dense batches of 2 and 4
-    opts = ig.ig_ctx_opts(mb_kv, mb_kv * d.L, args.depth, args.copy_mode, 0, 0)
+    opts = ig.ig_ctx_opts(mb_kv, mb_kv * d.L, args.depth, args.copy_mode, 0, 0, 0, 0, int(args.graphs))
     ctx_kv = ig.ig_ctx_create(ig.make_desc(d, ig.IG_BF16), ptrs, local, opts)
     sig = synth.flow_sigmas(N_STEPS)
     stream = torch.cuda.Stream(device=dev)

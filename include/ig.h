@@ -103,6 +103,11 @@ typedef struct {
                        /*     blocks spread evenly over the step.  Per step, block b       */
                        /*     stores [K_b, V_b] if it is a K/V block, then [Y_b] if block  */
                        /*     b or b + 1 is a Y block (ig_cache_write takes that order)    */
+  int use_graphs;      /* 1 = capture each distinct step shape (row counts, plan, cache    */
+                       /*     kinds, descriptor slot) as a CUDA graph and replay it: one   */
+                       /*     launch per step instead of ~10 per block.  Applies to steps  */
+                       /*     whose caches are HBM-resident (or absent) with copy_mode != 0,*/
+                       /*     on a non-default stream, profiling off; others run eagerly   */
 } ig_ctx_opts;
 
 typedef struct ig_ctx ig_ctx;

@@ -17,6 +17,7 @@
 #include <mutex>
 #include <chrono>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "../../include/ig.h"
@@ -180,6 +181,15 @@ struct ig_ctx {
   cudaEvent_t ev_yrec[MAXR] = {};
   ig_stats stats{};
   std::vector<ig_cache*> zombies;
+  // CUDA graphs of whole steps (ig_ctx_opts.use_graphs): keyed by everything that shapes the
+  // launches (row counts, plan, staging slot, cache kinds); the per-step data (sigmas, step
+  // indices, cache plane pointers, latents) live in the descriptors the graph itself pulls
+  // from the staging slot, so a replay needs no re-enqueue
+  struct GraphEnt { cudaGraphExec_t exec; ig_stats stats; };
+  std::unordered_map<std::string, GraphEnt> graphs;
+  bool capturing = false;
+  unsigned cap_mask = 0;  // ring buffers whose ev_comp was recorded inside the capture
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   // Algorithm-1 block plan (ig_set_plan): 0 off, 1 forced dense-prefix length, 2 model
   int plan_mode = 0, plan_k = 0, last_plan_k = 0;
   double pm_cs = 0, pm_cb = 0, pm_ls = 0, pm_lb = 0;  // s/FLOP, s, s/byte, s
@@ -351,7 +361,7 @@ extern "C" ig_status ig_ctx_create(const ig_model_desc* desc, const void* const*
     return set_err(IG_EINVAL, "expected %d weight pointers, got %d", nw, n_weights);
   for (int i = 0; i < nw; ++i)
     if (!weights[i]) return set_err(IG_EINVAL, "weight %d is NULL", i);
-  ig_ctx_opts o{8, 0, 2, 0, 0, 0, 0, 0};
+  ig_ctx_opts o{8, 0, 2, 0, 0, 0, 0, 0, 0};
   if (opts) o = *opts;
   if (o.max_batch <= 0) o.max_batch = 8;
   if (o.max_batch > 16) return set_err(IG_EUNSUPPORTED, "max_batch > 16");
@@ -505,7 +515,10 @@ extern "C" ig_status ig_ctx_create(const ig_model_desc* desc, const void* const*
     cudaEventCreateWithFlags(&ctx->ev_yrec[i], cudaEventDisableTiming);
   }
   cudaEventCreateWithFlags(&ctx->ev_desc, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming);
   ctx->pref.assign((size_t)B * ctx->R, ig_ctx::Pref{});
+  if (desc->dtype == IG_BF16) { gemm_tc_init(); attn_tc_init(); }  // before any graph capture
   cudaError_t e = cudaDeviceSynchronize();
   if (e != cudaSuccess) { ig_ctx_destroy(ctx); return set_err(IG_ECUDA, "ctx init: %s", cudaGetErrorString(e)); }
   *out = ctx;
@@ -533,6 +546,9 @@ extern "C" void ig_ctx_destroy(ig_ctx* ctx) {
     if (ctx->ev_yrec[i]) cudaEventDestroy(ctx->ev_yrec[i]);
   }
   if (ctx->ev_desc) cudaEventDestroy(ctx->ev_desc);
+  if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
+  if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
+  for (auto& g : ctx->graphs) cudaGraphExecDestroy(g.second.exec);
   for (auto& r : ctx->prof_recs) { ctx->ev_pool.push_back(r.a); ctx->ev_pool.push_back(r.b); }
   for (auto e : ctx->ev_pool) cudaEventDestroy(e);
   if (ctx->copy_st) cudaStreamDestroy(ctx->copy_st);
@@ -882,7 +898,9 @@ static void issue_copy(ig_ctx* ctx, const std::vector<StepReq>& sr, const KvGath
                        const KvGatherReq* kvq_dev, int b, const CopyPlan& plan) {
   if (!plan.any) return;
   const int buf = b % ctx->R;
-  cudaStreamWaitEvent(ctx->copy_st, ctx->ev_comp[buf], 0);
+  // inside a graph capture only this step's records are visible; earlier steps completed
+  // before the graph starts (same stream)
+  if (!ctx->capturing || (ctx->cap_mask >> buf & 1u)) cudaStreamWaitEvent(ctx->copy_st, ctx->ev_comp[buf], 0);
   const long long by0 = ctx->stats.h2d_bytes + ctx->stats.d2d_bytes;
   ProfScope ps(ctx, ctx->copy_st, IG_K_COPY, 0.0, 0.0, b);
   const int n = (int)sr.size();
@@ -1279,6 +1297,40 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
   // cache prefetch (up to R blocks of DMA) and stall the step start (measured: ~85 ms per step
   // with a dense prefix).
   const size_t desc_bytes = (char*)hkvg - hs;
+  // ---- CUDA graph of the step (device-tier caches / no cache only: host-tier DMA sources
+  // change every step) ----
+  // (the legacy default stream cannot be captured)
+  bool graph_ok = ctx->o.use_graphs && st != nullptr && !record && !rng.X_in && !rng.X_out && !ctx->prof &&
+                  b0 == 0 && b1 == nb;
+  for (auto& s2 : sr)
+    if (s2.use_cache && (s2.r->cache->tier != IG_CACHE_DEVICE || ctx->o.copy_mode == 0)) graph_ok = false;
+  std::string gkey;
+  if (graph_ok) {
+    std::vector<long long> k = {si, kplan, na, M, M_txt, M_full, nseg, max_q, nsegf, max_qf, max_nu,
+                                plan.gather, plan.gather_q8, any_cache, (long long)desc_bytes};
+    for (int v : uy) k.push_back(v);
+    for (auto& s2 : sr) {
+      k.push_back(s2.r->slot); k.push_back(s2.m->n_m); k.push_back(s2.use_cache);
+      if (s2.use_cache) { k.push_back(s2.r->cache->y); k.push_back(s2.r->cache->fp8); k.push_back(s2.r->cache->kv_blocks); }
+    }
+    gkey.assign(reinterpret_cast<const char*>(k.data()), k.size() * sizeof(long long));
+    auto it = ctx->graphs.find(gkey);
+    if (it != ctx->graphs.end()) {  // replay: the graph pulls this step's descriptors itself
+      for (auto& s2 : sr) if (s2.use_cache) s2.r->cache->pins.fetch_add(1);
+      CUDA_TRY(cudaGraphLaunch(it->second.exec, st));
+      ctx->stats = it->second.stats;
+      CUDA_TRY(cudaEventRecord(ctx->ev_stage[si], st));
+      for (auto& s2 : sr)
+        if (s2.use_cache) CUDA_TRY(cudaLaunchHostFunc(st, unpin_cb, (void*)s2.r->cache));
+      ctx->stats.host_ns = std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - t_host0).count();
+      return IG_OK;
+    }
+    CUDA_TRY(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    cudaEventRecord(ctx->ev_fork, st);
+    cudaStreamWaitEvent(ctx->copy_st, ctx->ev_fork, 0);  // the copy lane joins the capture
+    ctx->capturing = true;
+    ctx->cap_mask = 0;
+  }
   launch_copy_bytes(ds, ctx->m_stage[si], desc_bytes, st);
   if (plan.gather || plan.gather_q8) {
     const size_t off = (char*)hkvg - hs, bytes = (char*)(hkvq + (size_t)nb * na) - (char*)hkvg;
@@ -1525,6 +1577,7 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
       record_kv(b, buf);
       if (!dense) {
         cudaEventRecord(ctx->ev_comp[buf], st);
+        if (ctx->capturing) ctx->cap_mask |= 1u << buf;
         if (b + R < b1) issue_copy(ctx, sr, dkvg, dkvq, b + R, plan);
       }
       const long long gi = ctx->mods[wi.mod_t].off;
@@ -1553,6 +1606,7 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
       record_kv(b, buf);
       if (!dense) {
         cudaEventRecord(ctx->ev_comp[buf], st);
+        if (ctx->capturing) ctx->cap_mask |= 1u << buf;
         if (b + R < b1) issue_copy(ctx, sr, dkvg, dkvq, b + R, plan);
       }
       const long long gs = ctx->mods[ws.mod_t].off;
@@ -1568,6 +1622,24 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
     gemm_rows(M_txt, M, h, H, ctx->pout.w, ctx->pout.b, C, H, ctx->vel - (long long)M_txt * C, C, EPI_STORE, nullptr, 1);
     launch_scatter_euler(dreq, na, M_img, ctx->ri, M_txt, C, ctx->vel, st);
     stats.kernel_launches++;
+  }
+  if (ctx->capturing) {  // end the capture (copy lane joins back), instantiate, launch
+    cudaEventRecord(ctx->ev_join, ctx->copy_st);
+    cudaStreamWaitEvent(st, ctx->ev_join, 0);
+    cudaGraph_t graph = nullptr;
+    cudaError_t ce = cudaStreamEndCapture(st, &graph);
+    ctx->capturing = false;
+    if (ce != cudaSuccess) return set_err(IG_ECUDA, "step capture: %s", cudaGetErrorString(ce));
+    cudaGraphExec_t exec = nullptr;
+    ce = cudaGraphInstantiate(&exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (ce != cudaSuccess) return set_err(IG_ECUDA, "graph instantiate: %s", cudaGetErrorString(ce));
+    if (ctx->graphs.size() >= 64) {  // bounded: batch compositions change under continuous batching
+      for (auto& g : ctx->graphs) cudaGraphExecDestroy(g.second.exec);
+      ctx->graphs.clear();
+    }
+    ctx->graphs[gkey] = ig_ctx::GraphEnt{exec, stats};
+    CUDA_TRY(cudaGraphLaunch(exec, st));
   }
   // the copy lane must not run ahead into the next step's buffers before compute is done
   CUDA_TRY(cudaEventRecord(ctx->ev_stage[si], st));

@@ -362,6 +362,8 @@ void init_attn() {
 }
 }  // namespace
 
+void attn_tc_init() { init_attn(); }
+
 bool attn_tc_supported(const AttnArgs& a) {
   auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
   const long long H = (long long)a.heads * a.head_dim;

@@ -170,6 +170,9 @@ struct AttnArgs {
 template <typename T>
 void launch_attn_simt(const AttnArgs& a, cudaStream_t st);
 bool attn_tc_supported(const AttnArgs& a);
+// one-time driver setup (function attributes, entry points) outside any stream capture
+void attn_tc_init();
+void gemm_tc_init();
 void launch_attn_tc(const AttnArgs& a, cudaStream_t st);
 
 }  // namespace ig

@@ -51,7 +51,7 @@ class ig_ctx_opts(ctypes.Structure):
     _fields_ = [("max_batch", ctypes.c_int), ("max_rows", ctypes.c_int),
                 ("prefetch_depth", ctypes.c_int), ("copy_mode", ctypes.c_int),
                 ("debug_checks", ctypes.c_int), ("cache_fp8", ctypes.c_int), ("cache_y", ctypes.c_int),
-                ("cache_kv_blocks", ctypes.c_int)]
+                ("cache_kv_blocks", ctypes.c_int), ("use_graphs", ctypes.c_int)]
 
 
 class ig_edit_req(ctypes.Structure):

@@ -618,3 +618,47 @@ def test_fp8_cache_with_dense_prefix(k):
     for r in reqs:
         r.free()
     m.close()
+
+
+def test_cuda_graph_steps_bitwise_equal_eager():
+    """ig_ctx_opts.use_graphs: steps on an HBM-resident cache are captured as CUDA graphs per
+    step shape and replayed; 8 steps (a request leaves after step 4 -> a new shape) must equal
+    the eager path bitwise, including a hybrid cache and an all-ones request."""
+    from gpu_util import hybrid_planes
+    d = synth.FLUX_SMALL
+    sig = synth.flow_sigmas(8)
+    eager = Model(d, ig.IG_BF16, opts=ig.ig_ctx_opts(4, 0, 2, 1, 0, 0))
+    ptrs = [eager.W[n].data_ptr() for n, _, _ in synth.weight_table(d)]
+    gctx = ig.ig_ctx_create(eager.desc, ptrs, 0, ig.ig_ctx_opts(4, 0, 2, 1, 0, 0, 0, 0, 1))
+    rng = np.random.default_rng(41)
+    masks = [synth.blob_mask_count(d, 90, rng), synth.rect_mask_count(d, 40, rng), np.ones(d.L_img, np.uint8)]
+    ra = [Request(eager, 180 + i, mk) for i, mk in enumerate(masks)]
+    rb = [Request(eager, 180 + i, mk) for i, mk in enumerate(masks)]
+    kv = synth.make_cache_kv(d, 12, 8, dtype=torch.bfloat16)
+    tlat = torch.stack([synth.make_latent(d, 990 + s) for s in range(8)])
+    kvc = ig.ig_cache_create(eager.ctx, 8, ig.IG_CACHE_DEVICE)
+    fill_cache(eager, kvc, kv, tlat)
+    m2 = Model(d, ig.IG_BF16, opts=ig.ig_ctx_opts(4, 0, 2, 1, 0, 0, 1, 2))
+    hyc = ig.ig_cache_create(m2.ctx, 8, ig.IG_CACHE_DEVICE)
+    ym = set(ig.y_block_modes(d.n_blocks, 2))
+    fill_cache(m2, hyc, hybrid_planes(kv, synth.make_cache_y(d, 12, 8, dtype=torch.bfloat16), ym), tlat)
+    caches = [kvc, hyc, None]
+    stream = torch.cuda.Stream()  # graphs need a capturable (non-default) stream
+    for s in range(8):
+        live = range(3) if s < 4 else (0, 2)
+        for ctx, rs in ((eager.ctx, ra), (gctx, rb)):
+            ig.ig_edit_step(ctx, [rs[i].req(i, caches[i], s, float(sig[s]), float(sig[s + 1])) for i in live],
+                            stream.cuda_stream)
+    torch.cuda.synchronize()
+    for a, b in zip(ra, rb):
+        assert torch.equal(a.latent, b.latent)
+        assert not torch.equal(a.latent, a.latent0)
+    st = ig.ig_last_stats(gctx)
+    assert st["kernel_launches"] > 0
+    ig.ig_cache_free(kvc)
+    ig.ig_cache_free(hyc)
+    for r in ra + rb:
+        r.free()
+    ig.ig_ctx_destroy(gctx)
+    m2.close()
+    eager.close()
