@@ -420,11 +420,14 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    share = os.environ.get("IG_BENCH_SHARE_GPU") == "1"  # test aid: all ranks on GPU 0, gloo
+    if share:
+        local = 0
     if world > 1:
         import torch.distributed as dist
         if args.impl == "ours":
             torch.cuda.set_device(local)  # the NCCL communicator binds to this rank's GPU
-        dist.init_process_group("nccl" if args.impl == "ours" else "gloo")
+        dist.init_process_group("nccl" if args.impl == "ours" and not share else "gloo")
     if args.impl == "reference":
         run_reference(args, rank)
         return
