@@ -59,16 +59,17 @@ __device__ __forceinline__ void tile_coords(int t, int num_m, int num_n, int G, 
 
 // epilogue for one 32-column chunk of one row held in registers
 template <int BN>
+// bchunk: this chunk's 32 bias values (global memory, or the tile's bias slice staged in shared
+// memory by the 2-CTA kernel), nullptr without bias
 __device__ __forceinline__ void epilogue_chunk(const GemmArgs& g, int row, int col0, const uint32_t (&r)[32],
-                                               const RowInfo* info) {
+                                               const RowInfo* info, const bf16* bchunk) {
   float v[32];
 #pragma unroll
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-  const bf16* bias = reinterpret_cast<const bf16*>(g.bias);
   const bool full = col0 + 32 <= g.N;
-  if (bias) {
+  if (bchunk) {
     if (full) {
-      const uint4* b4 = reinterpret_cast<const uint4*>(bias + col0);
+      const uint4* b4 = reinterpret_cast<const uint4*>(bchunk);
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         uint4 u = b4[q];
@@ -79,7 +80,7 @@ __device__ __forceinline__ void epilogue_chunk(const GemmArgs& g, int row, int c
     } else {
 #pragma unroll
       for (int i = 0; i < 32; ++i)
-        if (col0 + i < g.N) v[i] += __bfloat162float(bias[col0 + i]);
+        if (col0 + i < g.N) v[i] += __bfloat162float(bchunk[i]);
     }
   }
   switch (g.epi) {
@@ -162,16 +163,15 @@ __device__ __forceinline__ void epilogue_chunk(const GemmArgs& g, int row, int c
 // buffer row (the fresh half of the merge by mask index, C-AMB 8).
 template <int DH>
 __device__ __forceinline__ void epilogue_qkv_head(const GemmArgs& g, int row, int col0, const uint32_t (&r)[DH],
-                                                  const RowInfo& info) {
+                                                  const RowInfo& info, const bf16* bchunk) {
   const QkvEpi& e = g.qkv;
   float v[DH];
 #pragma unroll
   for (int i = 0; i < DH; ++i) v[i] = __uint_as_float(r[i]);
-  const bf16* bias = reinterpret_cast<const bf16*>(g.bias);
-  if (bias) {
+  if (bchunk) {
 #pragma unroll
     for (int q = 0; q < DH / 8; ++q) {
-      uint4 u = reinterpret_cast<const uint4*>(bias + col0)[q];
+      uint4 u = reinterpret_cast<const uint4*>(bchunk)[q];
       const bf16* hb = reinterpret_cast<const bf16*>(&u);
 #pragma unroll
       for (int t = 0; t < 8; ++t) v[q * 8 + t] += __bfloat162float(hb[t]);
@@ -327,6 +327,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       if (row < g.M && g.ri && (g.epi == EPI_GATED_RES || g.epi == EPI_POS || g.epi == EPI_QKV))
         info = g.ri[g.ri_off + row];
       const uint32_t tbase = tmem_base + ((uint32_t)(quad * 32) << 16) + acc * BN;
+      const bf16* gbias = reinterpret_cast<const bf16*>(g.bias);
+#define BIAS_AT(c) (gbias ? gbias + n0 + (c) : nullptr)
       if (g.epi == EPI_QKV) {
         if (g.qkv.head_dim == 128) {
 #pragma unroll 1
@@ -335,7 +337,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
             for (int s = 0; s < 4; ++s) tc::tmem_ld32(tbase + c + 32 * s, *reinterpret_cast<uint32_t(*)[32]>(&v[32 * s]));
             tc::tmem_ld_wait();
-            if (row < g.M && n0 + c < g.N) epilogue_qkv_head<128>(g, row, n0 + c, v, info);
+            if (row < g.M && n0 + c < g.N) epilogue_qkv_head<128>(g, row, n0 + c, v, info, BIAS_AT(c));
           }
         } else {
 #pragma unroll 1
@@ -344,7 +346,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
             for (int s = 0; s < 2; ++s) tc::tmem_ld32(tbase + c + 32 * s, *reinterpret_cast<uint32_t(*)[32]>(&v[32 * s]));
             tc::tmem_ld_wait();
-            if (row < g.M && n0 + c < g.N) epilogue_qkv_head<64>(g, row, n0 + c, v, info);
+            if (row < g.M && n0 + c < g.N) epilogue_qkv_head<64>(g, row, n0 + c, v, info, BIAS_AT(c));
           }
         }
       } else {
@@ -353,9 +355,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           uint32_t r[32];
           tc::tmem_ld32(tbase + c, r);
           tc::tmem_ld_wait();
-          if (row < g.M && n0 + c < g.N) epilogue_chunk<BN>(g, row, n0 + c, r, &info);
+          if (row < g.M && n0 + c < g.N) epilogue_chunk<BN>(g, row, n0 + c, r, &info, BIAS_AT(c));
         }
       }
+#undef BIAS_AT
       tc::tc_fence_before();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&tempty[acc]);
@@ -380,7 +383,7 @@ struct Cfg2 {
   static constexpr int B_BYTES = 128 * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int TMEM_COLS = 512;
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256 + 2 * 256 * 2 /*bias slices*/;
 };
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
@@ -397,6 +400,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
   uint64_t* tfull = empty + C::STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  bf16* sbias = reinterpret_cast<bf16*>(smem + C::STAGES * C::STAGE_BYTES + 256);  // [2][BN]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = tc::cluster_ctarank();
@@ -475,6 +479,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       int mb, nb;
       tile_coords(t, num_m, num_n, G, mb, nb);
       const int m0 = mb * 256 + rank * 128, n0 = nb * BN;
+      // the tile's bias slice -> shared memory (one 4-byte load per epilogue thread), so the
+      // chunks below read it at shared-memory latency instead of one global round trip each;
+      // double-buffered by accumulator, and the per-tile barrier keeps warps within one tile
+      bf16* sb = sbias + acc * BN;
+      const bf16* gbias = reinterpret_cast<const bf16*>(g.bias);
+      if (gbias) {
+        const int i = 2 * ((warp - 4) * 32 + lane);
+        sb[i] = n0 + i < g.N ? gbias[n0 + i] : __float2bfloat16_rn(0.f);
+        sb[i + 1] = n0 + i + 1 < g.N ? gbias[n0 + i + 1] : __float2bfloat16_rn(0.f);
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+      }
+#define BIAS_AT(c) (gbias ? sb + (c) : nullptr)
       tc::mbar_wait(&tfull[acc], acc_phase);
       tc::tc_fence_after();
       const int row = m0 + quad * 32 + lane;
@@ -490,7 +506,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
             for (int s = 0; s < 4; ++s) tc::tmem_ld32(tbase + c + 32 * s, *reinterpret_cast<uint32_t(*)[32]>(&v[32 * s]));
             tc::tmem_ld_wait();
-            if (row < g.M && n0 + c < g.N) epilogue_qkv_head<128>(g, row, n0 + c, v, info);
+            if (row < g.M && n0 + c < g.N) epilogue_qkv_head<128>(g, row, n0 + c, v, info, BIAS_AT(c));
           }
         } else {
 #pragma unroll 1
@@ -499,7 +515,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
             for (int s = 0; s < 2; ++s) tc::tmem_ld32(tbase + c + 32 * s, *reinterpret_cast<uint32_t(*)[32]>(&v[32 * s]));
             tc::tmem_ld_wait();
-            if (row < g.M && n0 + c < g.N) epilogue_qkv_head<64>(g, row, n0 + c, v, info);
+            if (row < g.M && n0 + c < g.N) epilogue_qkv_head<64>(g, row, n0 + c, v, info, BIAS_AT(c));
           }
         }
       } else {
@@ -508,9 +524,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
           uint32_t r[32];
           tc::tmem_ld32(tbase + c, r);
           tc::tmem_ld_wait();
-          if (row < g.M && n0 + c < g.N) epilogue_chunk<BN>(g, row, n0 + c, r, &info);
+          if (row < g.M && n0 + c < g.N) epilogue_chunk<BN>(g, row, n0 + c, r, &info, BIAS_AT(c));
         }
       }
+#undef BIAS_AT
       tc::tc_fence_before();
       __syncwarp();
       if (lane == 0) {

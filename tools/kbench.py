@@ -11,6 +11,8 @@ ap.add_argument("--M", type=int, default=14720)
 ap.add_argument("--N", type=int, default=3072)
 ap.add_argument("--K", type=int, default=3072)
 ap.add_argument("--iters", type=int, default=10)
+ap.add_argument("--epi", type=int, default=0, help="0 store, 1 bias+GELU (fc1)")
+ap.add_argument("--bias", action="store_true")
 args = ap.parse_args()
 res = {}
 def timeit(fn, iters):
@@ -29,7 +31,9 @@ if "gemm" in args.which:
     A = torch.randn(M, K, device="cuda", dtype=torch.bfloat16)
     B = torch.randn(N, K, device="cuda", dtype=torch.bfloat16) / K ** 0.5
     C = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
-    ms = timeit(lambda: ig.ig_op_gemm(ig.IG_BF16, A.data_ptr(), K, B.data_ptr(), K, 0, C.data_ptr(), N, M, N, K, 0, 0, 0), args.iters)
+    bias = torch.randn(N, device="cuda", dtype=torch.bfloat16)
+    bp = bias.data_ptr() if args.bias else 0
+    ms = timeit(lambda: ig.ig_op_gemm(ig.IG_BF16, A.data_ptr(), K, B.data_ptr(), K, bp, C.data_ptr(), N, M, N, K, args.epi, 0, 0), args.iters)
     ref = timeit(lambda: torch.matmul(A, B.t(), out=C), args.iters)
     X = torch.zeros(M, N, device="cuda", dtype=torch.float32)
     gate = torch.rand(N, device="cuda", dtype=torch.float32)
