@@ -186,16 +186,17 @@ template <int DH>
 __device__ __forceinline__ void epilogue_qkv_head(const GemmArgs& g, int row, int col0, const uint32_t (&r)[DH],
                                                   const RowInfo& info, const bf16* bchunk) {
   const QkvEpi& e = g.qkv;
-  float v[DH];
+  // packed f32x2 FMA-pipe arithmetic throughout (the epilogue is issue-bound, like GELU's)
+  float2 v[DH / 2];
 #pragma unroll
-  for (int i = 0; i < DH; ++i) v[i] = __uint_as_float(r[i]);
+  for (int i = 0; i < DH / 2; ++i) v[i] = make_float2(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1]));
   if (bchunk) {
 #pragma unroll
     for (int q = 0; q < DH / 8; ++q) {
       uint4 u = reinterpret_cast<const uint4*>(bchunk)[q];
-      const bf16* hb = reinterpret_cast<const bf16*>(&u);
+      const __nv_bfloat162* hb = reinterpret_cast<const __nv_bfloat162*>(&u);
 #pragma unroll
-      for (int t = 0; t < 8; ++t) v[q * 8 + t] += __bfloat162float(hb[t]);
+      for (int t = 0; t < 4; ++t) v[q * 4 + t] = __fadd2_rn(v[q * 4 + t], __bfloat1622float2(hb[t]));
     }
   }
   const int cq = col0 + e.col_base;             // column in [q|k|v] (col_base = H: K/V only)
@@ -210,17 +211,18 @@ __device__ __forceinline__ void epilogue_qkv_head(const GemmArgs& g, int row, in
   }
   if (which < 2) {
     if (e.qk_norm) {
-      float ss = 0.f;
+      float2 ss2 = make_float2(0.f, 0.f);
 #pragma unroll
-      for (int i = 0; i < DH; ++i) ss = fmaf(v[i], v[i], ss);
-      const float rinv = rsqrtf(ss / DH + 1e-6f);
+      for (int i = 0; i < DH / 2; ++i) ss2 = __ffma2_rn(v[i], v[i], ss2);
+      const float rinv = rsqrtf((ss2.x + ss2.y) / DH + 1e-6f);
+      const float2 rinv2 = make_float2(rinv, rinv);
       const bf16* gn = reinterpret_cast<const bf16*>(which == 0 ? e.qg : e.kg);
 #pragma unroll
       for (int q = 0; q < DH / 8; ++q) {
         uint4 u = reinterpret_cast<const uint4*>(gn)[q];
-        const bf16* hg = reinterpret_cast<const bf16*>(&u);
+        const __nv_bfloat162* hg = reinterpret_cast<const __nv_bfloat162*>(&u);
 #pragma unroll
-        for (int t = 0; t < 8; ++t) v[q * 8 + t] *= rinv * __bfloat162float(hg[t]);
+        for (int t = 0; t < 4; ++t) v[q * 4 + t] = __fmul2_rn(v[q * 4 + t], __fmul2_rn(rinv2, __bfloat1622float2(hg[t])));
       }
     }
     if (e.rope) {
@@ -230,9 +232,9 @@ __device__ __forceinline__ void epilogue_qkv_head(const GemmArgs& g, int row, in
       for (int j = 0; j < DH / 2; ++j) {
         const int pos = j < e.ax1_pair ? 0 : (j < e.ax2_pair ? p1 : p2);
         const float2 cs = __ldg(e.rope_tab + (long long)j * e.rope_maxpos + pos);
-        const float x0 = v[2 * j], x1 = v[2 * j + 1];
-        v[2 * j] = x0 * cs.x - x1 * cs.y;
-        v[2 * j + 1] = x0 * cs.y + x1 * cs.x;
+        // (x0, x1) -> (x0 c - x1 s, x0 s + x1 c) as x0 * (c, s) + x1 * (-s, c)
+        const float2 t = __fmul2_rn(make_float2(v[j].y, v[j].y), make_float2(-cs.y, cs.x));
+        v[j] = __ffma2_rn(make_float2(v[j].x, v[j].x), cs, t);
       }
     }
   }
@@ -242,7 +244,7 @@ __device__ __forceinline__ void epilogue_qkv_head(const GemmArgs& g, int row, in
     uint32_t* w = reinterpret_cast<uint32_t*>(&u);
 #pragma unroll
     for (int t = 0; t < 4; ++t) {
-      __nv_bfloat162 p = __floats2bfloat162_rn(v[q * 8 + 2 * t], v[q * 8 + 2 * t + 1]);
+      __nv_bfloat162 p = __float22bfloat162_rn(v[q * 4 + t]);
       w[t] = *reinterpret_cast<uint32_t*>(&p);
     }
     reinterpret_cast<uint4*>(dst)[q] = u;
