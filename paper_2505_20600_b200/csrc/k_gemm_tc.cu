@@ -85,9 +85,13 @@ __device__ __forceinline__ void epilogue_chunk(const GemmArgs& g, int row, int c
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         uint4 u = b4[q];
-        const bf16* hb = reinterpret_cast<const bf16*>(&u);
+        const __nv_bfloat162* hb = reinterpret_cast<const __nv_bfloat162*>(&u);
 #pragma unroll
-        for (int e = 0; e < 8; ++e) v[q * 8 + e] += __bfloat162float(hb[e]);
+        for (int e = 0; e < 4; ++e) {
+          const float2 y = __fadd2_rn(make_float2(v[q * 8 + 2 * e], v[q * 8 + 2 * e + 1]), __bfloat1622float2(hb[e]));
+          v[q * 8 + 2 * e] = y.x;
+          v[q * 8 + 2 * e + 1] = y.y;
+        }
       }
     } else {
 #pragma unroll
@@ -154,11 +158,12 @@ __device__ __forceinline__ void epilogue_chunk(const GemmArgs& g, int row, int c
           gv[q] = __ldg(reinterpret_cast<const float4*>(gt) + q);
         }
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          xv[q].x = fmaf(gv[q].x, v[4 * q], xv[q].x);
-          xv[q].y = fmaf(gv[q].y, v[4 * q + 1], xv[q].y);
-          xv[q].z = fmaf(gv[q].z, v[4 * q + 2], xv[q].z);
-          xv[q].w = fmaf(gv[q].w, v[4 * q + 3], xv[q].w);
+        for (int q = 0; q < 8; ++q) {  // packed f32x2 FMAs (issue-bound epilogue)
+          const float2 lo = __ffma2_rn(make_float2(gv[q].x, gv[q].y), make_float2(v[4 * q], v[4 * q + 1]),
+                                       make_float2(xv[q].x, xv[q].y));
+          const float2 hi = __ffma2_rn(make_float2(gv[q].z, gv[q].w), make_float2(v[4 * q + 2], v[4 * q + 3]),
+                                       make_float2(xv[q].z, xv[q].w));
+          xv[q] = make_float4(lo.x, lo.y, hi.x, hi.y);
         }
 #pragma unroll
         for (int q = 0; q < 8; ++q) __stcs(reinterpret_cast<float4*>(x) + q, xv[q]);

@@ -40,6 +40,15 @@ if "gemm" in args.which:
     msg = timeit(lambda: ig.ig_op_gemm_gated(ig.IG_BF16, A.data_ptr(), K, B.data_ptr(), K, 0, X.data_ptr(), N, gate.data_ptr(), M, N, K, 0), args.iters)
     res["gemm_gated_tflops"] = 2 * M * N * K / msg / 1e9
     res["gemm"] = {"M": M, "N": N, "K": K, "ms": ms, "tflops": 2 * M * N * K / ms / 1e9, "cublas_tflops": 2 * M * N * K / ref / 1e9}
+if "gated" in args.which:  # out-projection shape: fp32 residual += gate * (A B^T + bias)
+    M, N, K = args.M, args.N, args.K
+    A = torch.randn(M, K, device="cuda", dtype=torch.bfloat16)
+    B = torch.randn(N, K, device="cuda", dtype=torch.bfloat16) / K ** 0.5
+    X = torch.zeros(M, N, device="cuda", dtype=torch.float32)
+    gate = torch.rand(N, device="cuda", dtype=torch.float32)
+    ms = timeit(lambda: ig.ig_op_gemm_gated(ig.IG_BF16, A.data_ptr(), K, B.data_ptr(), K, 0, X.data_ptr(), N,
+                                            gate.data_ptr(), M, N, K, 0), args.iters)
+    res["gated"] = {"M": M, "N": N, "K": K, "ms": ms, "tflops": 2 * M * N * K / ms / 1e9}
 if "attn" in args.which:
     heads, dh, L = 24, 128, 4608
     qlens = [512, 1843] * 8
