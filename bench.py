@@ -199,7 +199,7 @@ def run_loop(ig, ctx, batch, cache, sig, steps, stream, profile=False, e2e=None)
         # in place over the host link (no device copy of the latent exists)
         ig.ig_edit_step(ctx, batch.reqs(cache, sig, e2e), stream.cuda_stream)
         plans.append(ig.ig_last_plan(ctx))
-        alg_flops += sum(N_BLOCKS_FLOPS(batch.d, r.n_m) for r in batch.slots)
+        alg_flops += sum(request_step_flops(batch.d, r.n_m) for r in batch.slots)
         st = ig.ig_last_stats(ctx)
         host_s += st["host_ns"] * 1e-9  # library enqueue time, back-pressure waits excluded
         launches += st["kernel_launches"]
@@ -235,7 +235,7 @@ class Leg:
         return e["flops"] / (e["ms"] * 1e-3) / 1e12 if e["ms"] else 0.0
 
 
-def N_BLOCKS_FLOPS(d, n_m):
+def request_step_flops(d, n_m):
     """All-cache algorithmic FLOPs of one request-step (Table 1 scaling; SURVEY
     §8(d) F(m) = 16.138 GFLOP x (L_txt + n_m) for Flux): every block's projections/MLP over the
     request's query rows plus masked-Q x full-KV attention."""

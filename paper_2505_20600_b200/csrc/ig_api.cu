@@ -169,7 +169,6 @@ struct ig_ctx {
   std::vector<Pref> pref;  // [max_batch * R]
   ig_mask* ones_mask = nullptr;
   std::vector<void*> b_dst, b_src;  // batched-copy scratch (copy_mode 1)
-  bool gather_dev = false;          // unused (kept for layout)
   // FP8 cache staging (cache_fp8): per (slot, ring buffer) e4m3 rows + scales landed by the DMA
   // lane before the dequantizing gather into the bf16 ring; per ring buffer for recording
   uint8_t* q8in = nullptr;  float* q8in_scl = nullptr;
