@@ -1481,12 +1481,15 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
     gemm(ctx, g, st);
   };
   // Y variant: replenish the unmasked rows' block input from the staged Y_{b-1} (V plane)
-  auto y_load = [&](int b, int buf) {
-    if (uy[b] == 0 || b <= kplan) return;
+  // Y blocks after the first cached one: LN-modulation of the unmasked rows straight from the
+  // staged Y_{b-1} rows (the copy lane's V-plane landing zone), after waiting for the copy
+  auto y_staged = [&](int b) { return uy[b] > 0 && b > kplan; };
+  auto ln_mod_y = [&](int b, int buf, int mod_t, int shift_c, int scale_c) {
     cudaStreamWaitEvent(st, ctx->ev_copy[buf], 0);
-    ProfScope ps(ctx, st, IG_K_ROWS, 0.0, (double)uy[b] * H * (es + 4));
-    launch_y_load<T>(ctx->kv_arena, ctx->slot_stride, (long long)buf * ctx->buf_elems, ctx->L, H, ctx->ri, ctx->X, M,
-                     M + uy[b], st);
+    const long long off = ctx->mods[mod_t].off;
+    ProfScope ps(ctx, st, IG_K_LNMOD, 0.0, (double)uy[b] * H * (es + es));
+    launch_ln_mod_staged<T>(ctx->kv_arena, ctx->slot_stride, (long long)buf * ctx->buf_elems, ctx->L, H, M, M + uy[b],
+                            ctx->ri, mod + off, (int)mld, shift_c * H, scale_c * H, ctx->d.ln_eps, h, H, st);
     stats.kernel_launches++;
   };
   // Y recording (template pass): the block output's image rows -> compute dtype -> D2H
@@ -1564,11 +1567,12 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
     const int Mc = dense ? M_full : M;    // rows through every op of the block
     const int Mk = dense ? M_full : M + uy[b];  // rows through LN-mod and the K/V projection
     const int buf = dense ? R : b % R;
-    if (!dense) y_load(b, buf);
+    const bool ys = !dense && y_staged(b);
     if (b < ctx->d.n_double) {
       const StreamW& wi = ctx->dimg[b];
       const StreamW& wt = ctx->dtxt[b];
-      ln_mod(M_txt, Mk, wi.mod_t, 0, 1);
+      ln_mod(M_txt, ys ? M : Mk, wi.mod_t, 0, 1);
+      if (ys) ln_mod_y(b, buf, wi.mod_t, 0, 1);
       if (Lt) ln_mod(0, M_txt, wt.mod_t, wt.pre_only ? 1 : 0, wt.pre_only ? 0 : 1);
       if (!dense) wait_copy(buf);
       qkv_proj(M_txt, Mc, wi.qkv.w, wi.qkv.b, wi.qg, wi.kg, buf);
@@ -1596,7 +1600,8 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
       }
     } else {
       const SingleW& ws = ctx->sgl[b - ctx->d.n_double];
-      ln_mod(0, Mk, ws.mod_t, 0, 1);
+      ln_mod(0, ys ? M : Mk, ws.mod_t, 0, 1);
+      if (ys) ln_mod_y(b, buf, ws.mod_t, 0, 1);
       const char* w_u = (const char*)ws.lin1.w + 3LL * H * H * es;
       const char* b_u = (const char*)ws.lin1.b + 3LL * H * es;
       gemm_rows(0, Mc, h, H, w_u, b_u, F, H, cat + H, ldcat, EPI_GELU, nullptr, 0);

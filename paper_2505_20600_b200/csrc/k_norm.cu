@@ -236,6 +236,89 @@ void launch_ln_mod(const float* X, int H, int r0, int r1, const RowInfo* ri, con
   ln_mod_kernel<T><<<r1 - r0, LN_THREADS, 0, st>>>(X, H, r0, ri, mod, mod_ld, shift_off, scale_off, eps, h, ldh);
 }
 template void launch_ln_mod<float>(const float*, int, int, int, const RowInfo*, const float*, int, int, int, float, float*, int, cudaStream_t);
+
+// Y blocks: the same LN-modulation read straight from the staged Y_{b-1} rows (compute dtype,
+// the V plane of the ring buffer at the row's position) instead of the fp32 residual — the
+// widening T -> fp32 is exact, so the result equals widening into the residual + ln_mod bit for bit while the
+// fp32 round trip of the unmasked rows disappears.
+__device__ __forceinline__ float4 load4f(const float* p) { return __ldcs(reinterpret_cast<const float4*>(p)); }
+__device__ __forceinline__ float4 load4f(const bf16* p) {
+  const uint2 u = __ldcs(reinterpret_cast<const uint2*>(p));
+  const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
+  const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
+  return make_float4(a.x, a.y, b.x, b.y);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(LN_THREADS) ln_mod_staged_kernel(const T* __restrict__ arena, long long slot_stride,
+                                                                   long long buf_off, long long L, int H, int r0,
+                                                                   const RowInfo* __restrict__ ri,
+                                                                   const float* __restrict__ mod, int mod_ld,
+                                                                   int shift_off, int scale_off, float eps,
+                                                                   T* __restrict__ h, int ldh) {
+  __shared__ float red[LN_THREADS / 32];
+  const int r = r0 + blockIdx.x;
+  const RowInfo info = ri[r];
+  const T* x = arena + info.slot * slot_stride + buf_off + L * H + (long long)info.kvpos * H;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  float4 v[LN_MAXV];
+  float s = 0.f;
+#pragma unroll
+  for (int k = 0; k < LN_MAXV; ++k) {
+    const int c = (k * LN_THREADS + tid) * 4;
+    v[k] = c < H ? load4f(x + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+    s += (v[k].x + v[k].y) + (v[k].z + v[k].w);
+  }
+  s = warp_sum(s);
+  if (lane == 0) red[wid] = s;
+  __syncthreads();
+  float tot = 0.f;
+#pragma unroll
+  for (int w = 0; w < LN_THREADS / 32; ++w) tot += red[w];
+  const float mean = tot / H;
+  __syncthreads();
+  float q = 0.f;
+#pragma unroll
+  for (int k = 0; k < LN_MAXV; ++k) {
+    const int c = (k * LN_THREADS + tid) * 4;
+    if (c < H) {
+      const float a = v[k].x - mean, b = v[k].y - mean, cc = v[k].z - mean, d = v[k].w - mean;
+      q += (a * a + b * b) + (cc * cc + d * d);
+    }
+  }
+  q = warp_sum(q);
+  if (lane == 0) red[wid] = q;
+  __syncthreads();
+  float qt = 0.f;
+#pragma unroll
+  for (int w = 0; w < LN_THREADS / 32; ++w) qt += red[w];
+  const float rstd = 1.0f / sqrtf(qt / H + eps);
+  const float* m = mod + (long long)info.req * mod_ld;
+  T* out = h + (long long)r * ldh;
+#pragma unroll
+  for (int k = 0; k < LN_MAXV; ++k) {
+    const int c = (k * LN_THREADS + tid) * 4;
+    if (c < H) {
+      const float4 sc = *reinterpret_cast<const float4*>(m + scale_off + c);
+      const float4 sh = *reinterpret_cast<const float4*>(m + shift_off + c);
+      store4<T>(out + c, (v[k].x - mean) * rstd * (1.f + sc.x) + sh.x, (v[k].y - mean) * rstd * (1.f + sc.y) + sh.y,
+                (v[k].z - mean) * rstd * (1.f + sc.z) + sh.z, (v[k].w - mean) * rstd * (1.f + sc.w) + sh.w);
+    }
+  }
+}
+
+template <typename T>
+void launch_ln_mod_staged(const void* arena, long long slot_stride, long long buf_off, long long L, int H, int r0,
+                          int r1, const RowInfo* ri, const float* mod, int mod_ld, int shift_off, int scale_off,
+                          float eps, T* h, int ldh, cudaStream_t st) {
+  if (r1 <= r0) return;
+  ln_mod_staged_kernel<T><<<r1 - r0, LN_THREADS, 0, st>>>((const T*)arena, slot_stride, buf_off, L, H, r0, ri, mod,
+                                                          mod_ld, shift_off, scale_off, eps, h, ldh);
+}
+template void launch_ln_mod_staged<float>(const void*, long long, long long, long long, int, int, int, const RowInfo*,
+                                          const float*, int, int, int, float, float*, int, cudaStream_t);
+template void launch_ln_mod_staged<bf16>(const void*, long long, long long, long long, int, int, int, const RowInfo*,
+                                         const float*, int, int, int, float, bf16*, int, cudaStream_t);
 template void launch_ln_mod<bf16>(const float*, int, int, int, const RowInfo*, const float*, int, int, int, float, bf16*, int, cudaStream_t);
 
 }  // namespace ig

@@ -270,47 +270,10 @@ void launch_copy_bytes(void* dst, const void* src, size_t n, cudaStream_t st) {
 }
 
 // ======================================================================================
-// Y variant (fig:transformer-Bottom): the unmasked rows of a block's
-// input are replenished from the staged cache rows.  The copy lane lands the template's
+// Y variant (fig:transformer-Bottom): the copy lane lands the template's
 // Y_{b-1} rows of the unmasked tokens positionally in the V plane of the ring buffer (it is
-// overwritten by this block's fresh V only after this kernel ran, stream order); this kernel
-// widens them into the fp32 residual rows [r0, r1).  One warp per row, 16-byte loads.
+// overwritten by the block's fresh V only after ln_mod_staged_kernel read them, stream order).
 // ======================================================================================
-template <typename T>
-__global__ void __launch_bounds__(256) y_load_kernel(const T* __restrict__ arena, long long slot_stride,
-                                                     long long buf_off, long long L, int H,
-                                                     const RowInfo* __restrict__ ri, float* __restrict__ X,
-                                                     int r0, int r1) {
-  const int r = r0 + (int)(((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
-  const int lane = threadIdx.x & 31;
-  if (r >= r1) return;
-  const RowInfo info = ri[r];
-  const T* src = arena + info.slot * slot_stride + buf_off + L * H + (long long)info.kvpos * H;
-  float* dst = X + (long long)r * H;
-  constexpr int V = 16 / sizeof(T);
-  for (int c = lane * V; c < H; c += 32 * V) {
-    const uint4 raw = __ldcs(reinterpret_cast<const uint4*>(src + c));
-    const T* e = reinterpret_cast<const T*>(&raw);
-#pragma unroll
-    for (int t = 0; t < V; t += 4)
-      *reinterpret_cast<float4*>(dst + c + t) = make_float4(to_f<T>(e[t]), to_f<T>(e[t + 1]), to_f<T>(e[t + 2]),
-                                                            to_f<T>(e[t + 3]));
-  }
-}
-
-template <typename T>
-void launch_y_load(const void* arena, long long slot_stride, long long buf_off, long long L, int H, const RowInfo* ri,
-                   float* X, int r0, int r1, cudaStream_t st) {
-  if (r1 <= r0) return;
-  const long long threads = (long long)(r1 - r0) * 32;
-  y_load_kernel<T><<<(unsigned)((threads + 255) / 256), 256, 0, st>>>((const T*)arena, slot_stride, buf_off, L, H, ri,
-                                                                      X, r0, r1);
-}
-template void launch_y_load<float>(const void*, long long, long long, long long, int, const RowInfo*, float*, int, int,
-                                   cudaStream_t);
-template void launch_y_load<bf16>(const void*, long long, long long, long long, int, const RowInfo*, float*, int, int,
-                                  cudaStream_t);
-
 // Y recording: fp32 residual rows -> cache dtype (round-to-nearest-even for bf16, C-AMB 18)
 template <typename T>
 __global__ void rows_to_kernel(const float* __restrict__ src, T* __restrict__ dst, long long n4) {

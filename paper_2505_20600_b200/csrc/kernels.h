@@ -101,11 +101,12 @@ void launch_kv_gather(const KvGatherReq* reqs_dev, int n, int max_nu, int L_txt,
 void launch_copy_bytes(void* dst, const void* src, size_t n, cudaStream_t st);
 
 // ---- Y variant (k_rows.cu) ------------------------------------------------------
-// X[r] (fp32) = staged Y row of (ri[r].slot, ring buffer at buf_off, position ri[r].kvpos) in
-// the V plane, rows [r0, r1)
+// LN-modulation of rows [r0, r1) read from the staged Y rows (V plane, position ri[r].kvpos of
+// slot ri[r].slot) instead of the fp32 residual (exact widening: same bits as via the residual)
 template <typename T>
-void launch_y_load(const void* arena, long long slot_stride, long long buf_off, long long L, int H, const RowInfo* ri,
-                   float* X, int r0, int r1, cudaStream_t st);
+void launch_ln_mod_staged(const void* arena, long long slot_stride, long long buf_off, long long L, int H, int r0,
+                          int r1, const RowInfo* ri, const float* mod, int mod_ld, int shift_off, int scale_off,
+                          float eps, T* h, int ldh, cudaStream_t st);
 // dst[i] = T(src[i]), n a multiple of 4
 template <typename T>
 void launch_rows_to(const float* src, void* dst, long long n, cudaStream_t st);
