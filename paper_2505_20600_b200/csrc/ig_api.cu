@@ -1229,6 +1229,9 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
     img_row += d.n_m;
     if (!ycache) kvrow += d.n_ui;
   }
+  int npair = 0, npairf = 0;  // attention work items (segment, 256-row query-tile pair)
+  for (int i = 0; i < nseg; ++i) npair += (hseg[i].q_len + 255) / 256;
+  for (int i = 0; i < nsegf; ++i) npairf += (hsegf[i].q_len + 255) / 256;
   // copy-lane plan and per-(block, request) gather descriptors (see issue_copy)
   CopyPlan plan;
   plan.any = any_cache;
@@ -1512,6 +1515,7 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
     a.Q = ctx->Q; a.ldq = H; a.O = cat; a.ldo = ldcat; a.kv_arena = ctx->kv_arena;
     a.kv_off = (long long)buf * ctx->buf_elems;
     a.segs = dense ? dsegf : dseg; a.nseg = dense ? nsegf : nseg; a.max_qlen = dense ? max_qf : max_q;
+    a.n_pairs = dense ? npairf : npair;
     a.q_rows = dense ? M_full : M;
     a.L = ctx->L; a.heads = ctx->d.heads; a.head_dim = ctx->d.head_dim;
     a.scale = 1.0f / sqrtf((float)ctx->d.head_dim);
@@ -1827,6 +1831,7 @@ extern "C" ig_status ig_op_attention(int dtype, const void* Q, long long ldq, vo
   AttnArgs a{};
   a.Q = Q; a.ldq = ldq; a.O = O; a.ldo = ldo; a.kv_arena = kv; a.kv_off = 0; a.segs = dsegs;
   a.nseg = nseg; a.max_qlen = maxq; a.L = L; a.heads = heads; a.head_dim = head_dim;
+  for (auto& sg : hs) a.n_pairs += (sg.q_len + 255) / 256;
   int qrows = 1;
   for (auto& s : hs) qrows = std::max(qrows, s.q_start + s.q_len);
   a.q_rows = qrows;

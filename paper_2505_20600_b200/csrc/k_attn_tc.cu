@@ -113,9 +113,19 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                    const AttnArgs a, float scale_log2) {
   using C = AC<D>;
   constexpr int Q_BYTES = C::Q_BYTES, KV_BYTES = C::KV_BYTES, TS = C::TSTRIDE;
-  const AttnSeg seg = a.segs[blockIdx.z];
+  // compact grid: blockIdx.x enumerates the (segment, query-tile pair) work items, decoded
+  // from the per-segment pair counts (no idle CTAs for short segments)
+  int z = blockIdx.z, pair = blockIdx.x;
+  if (a.n_pairs > 0) {
+    for (z = 0; z < a.nseg; ++z) {
+      const int np = (a.segs[z].q_len + 2 * BQ - 1) / (2 * BQ);
+      if (pair < np) break;
+      pair -= np;
+    }
+  }
+  const AttnSeg seg = a.segs[z];
   const int h = blockIdx.y;
-  const int q0 = blockIdx.x * 2 * BQ;
+  const int q0 = pair * 2 * BQ;
   if (q0 >= seg.q_len) return;
   const bool has_b = q0 + BQ < seg.q_len;
 
@@ -410,7 +420,8 @@ void launch_attn_tc(const AttnArgs& a, cudaStream_t st) {
           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     remember(a.kv_arena, H, a.L, -1, tkv);
   }
-  dim3 grid((a.max_qlen + 2 * BQ - 1) / (2 * BQ), a.heads, a.nseg);
+  dim3 grid = a.n_pairs > 0 ? dim3(a.n_pairs, a.heads, 1)
+                            : dim3((a.max_qlen + 2 * BQ - 1) / (2 * BQ), a.heads, a.nseg);
   const float scale_log2 = a.scale * 1.4426950408889634f;
   if (a.head_dim == 128) attn_tc_kernel<128><<<grid, NTHREADS, AC<128>::SMEM_BYTES, st>>>(tq, tkv, a, scale_log2);
   else attn_tc_kernel<64><<<grid, NTHREADS, AC<64>::SMEM_BYTES, st>>>(tq, tkv, a, scale_log2);

@@ -164,6 +164,8 @@ struct AttnArgs {
   void* O; long long ldo;         // packed [M, H] (may alias a column block of a wider buf)
   const void* kv_arena; long long kv_off;  // K at kv_base + kv_off, V at + L*H
   const AttnSeg* segs; int nseg; int max_qlen;
+  int n_pairs;                    // sum over segments of ceil(q_len / 256): the tcgen05 grid's x
+                                  // (0: the kernel falls back to max_qlen x nseg with idle CTAs)
   int q_rows;                     // rows of Q / O (bounds for the TMA tensor map)
   int L, heads, head_dim;
   float scale;                    // 1/sqrt(d)
