@@ -247,15 +247,15 @@ def request_step_flops(d, n_m):
 
 def choose_kv_blocks(d, a_c, b_c, a_l, max_batch, mean_m):
     """Hybrid split: s blocks move K/V (two planes), the other N - s (interleaved) move Y (one
-    plane) and recompute the unmasked rows' K/V (4 n_u H^2 flops, x1.3 for the LN-modulation
-    and the row widening around it).  Under the fitted linear models pick the s that balances
+    plane) and recompute the unmasked rows' K/V (4 n_u H^2 flops, x1.1 for the LN-modulation
+    of those rows; measured: 57 Y blocks add ~45 ms to a ~215 ms step = 1.08x the model).  Under the fitted linear models pick the s that balances
     the two lanes of a full batch at the mean mask ratio: argmin_s max(sum compute, sum load)."""
     from paper_2505_20600_b200.placement import block_flops
     N, H = d.n_blocks, d.hidden
     n_m = int(round(mean_m * d.L_img))
     n_u = max_batch * (d.L_img - n_m)
     cw = a_c * max_batch * block_flops(d, n_m) + b_c
-    cw_y = cw + 1.3 * a_c * 4.0 * n_u * H * H
+    cw_y = cw + 1.1 * a_c * 4.0 * n_u * H * H
     lt, lt_y = a_l * 2 * n_u * H * 2, a_l * n_u * H * 2
     best = min(range(N + 1), key=lambda s_: (max(s_ * cw + (N - s_) * cw_y, s_ * lt + max(0, N - s_ - (s_ == 0)) * lt_y), -s_))
     return best
