@@ -145,14 +145,14 @@ class Req:
 class Batch:
     """Continuous batching at saturation: max_batch slots, staggered start steps."""
 
-    def __init__(self, ig, ctx, d, dev, max_batch, pool_size, rid0, dense=False):
+    def __init__(self, ig, ctx, d, dev, max_batch, pool_size, rid0, dense=False, lockstep=False):
         self.ig, self.ctx, self.d = ig, ctx, d
         self.pool = [Req(ig, ctx, d, rid0 + i, dev, dense) for i in range(pool_size)]
         self.next = 0
         self.slots = []
         for s in range(max_batch):
             r = self._admit()
-            r.step = (s * N_STEPS) // max_batch
+            r.step = 0 if lockstep else (s * N_STEPS) // max_batch
             self.slots.append(r)
         self.completed = 0
 
@@ -406,6 +406,7 @@ def main():
     ap.add_argument("--no-fp8", action="store_true", help="skip the FP8-cache run")
     ap.add_argument("--no-y", action="store_true", help="skip the other-cache-kind runs")
     ap.add_argument("--no-profile", action="store_true", help="no per-launch event timing in the timed window")
+    ap.add_argument("--no-lockstep", action="store_true", help="skip the lockstep (deduplicated loads) run")
     ap.add_argument("--graphs", action="store_true",
                     help="replay steps as CUDA graphs (HBM-resident caches; needs --no-profile to take effect)")
     ap.add_argument("--cache", default=None, choices=["kv", "hybrid", "y"],
@@ -492,10 +493,10 @@ def main():
             return float(mx[0]), float(sm[1])
         return ms_, float(rs_)
 
-    def leg(c, cch, profile=True, e2e=False, clk=None):
+    def leg(c, cch, profile=True, e2e=False, clk=None, lockstep=False):
         """One measured configuration: a fresh batch replaying the same request sequence,
         W warm-up steps, then K timed steps between barriers."""
-        bt = Batch(ig, c, d, dev, args.max_batch, pool, rid0=rank * 100000)
+        bt = Batch(ig, c, d, dev, args.max_batch, pool, rid0=rank * 100000, lockstep=lockstep)
         run_loop(ig, c, bt, cch, sig, args.warmup, stream)
         hb = {r.rid: r.latent.detach().cpu().pin_memory() for r in bt.pool} if e2e else None
         barrier()
@@ -552,6 +553,17 @@ def main():
         hbm = summary(leg(ctx, dcache))
         ig.ig_set_plan(ctx, plan_mode, 0 if plan_mode != 1 else int(args.plan), a_c, b_c, a_l, b_l)
         ig.ig_cache_free(dcache)
+
+    # a lockstep batch (all requests on the same template and step, e.g. a burst of edits of one
+    # hot template): requests share their staged rows (load deduplication)
+    lockstep = None
+    if tier == "host" and world == 1 and not args.no_lockstep:
+        ls = leg(ctx, cache, lockstep=True)
+        lockstep = summary(ls)
+        lockstep["h2d_GB_per_step"] = round(ls.h2d / args.steps / 1e9, 3)
+        lockstep["note"] = ("all max_batch requests at the same step of one template (staggered admission "
+                            "replaced by lockstep); rows already staged by an earlier request of the batch are "
+                            "copied HBM->HBM instead of crossing the host link")
 
     ig.ig_cache_free(cache)  # host memory for the next legs' templates
 
@@ -667,6 +679,7 @@ def main():
                       if prof["copy"]["ms"] else None},
         "hbm_tier": hbm,
         "fp8_cache_host_tier": fp8,
+        "lockstep_dedupe_host_tier": lockstep,
         **alt,
         "speedup_hbm_tier_vs_dense": round(hbm["value"] / dense, 3) if (hbm and dense) else None,
         "gpu_launches": int(launches),

@@ -99,6 +99,8 @@ constexpr int MAXR = 32;  // max ring depth R = D + 1
 struct ig_mask {
   int L_img = 0, n_m = 0;
   std::vector<std::pair<int, int>> runs;  // host: maximal runs (start, len) of unmasked tokens
+  std::vector<uint8_t> bits;              // host: 1 = masked (load deduplication)
+  uint8_t* bits_dev = nullptr;            // device copy of bits
   int32_t* idx = nullptr;  // device: idx_m at [0, L_img), idx_u at [L_img, 2 L_img), n_m at [2 L_img]
 };
 
@@ -551,7 +553,7 @@ extern "C" void ig_ctx_destroy(ig_ctx* ctx) {
   for (auto& r : ctx->prof_recs) { ctx->ev_pool.push_back(r.a); ctx->ev_pool.push_back(r.b); }
   for (auto e : ctx->ev_pool) cudaEventDestroy(e);
   if (ctx->copy_st) cudaStreamDestroy(ctx->copy_st);
-  if (ctx->ones_mask) { cudaFree(ctx->ones_mask->idx); delete ctx->ones_mask; }
+  if (ctx->ones_mask) ig_mask_free(ctx->ones_mask);
   delete ctx;
 }
 
@@ -622,6 +624,10 @@ extern "C" ig_status ig_mask_build(ig_ctx* ctx, const uint8_t* mask, void* strea
   cudaError_t e = cudaMemcpyAsync(&n, m->idx + 2 * ctx->Limg, sizeof(int32_t), cudaMemcpyDeviceToHost, st);
   if (e == cudaSuccess) e = cudaMemcpyAsync(hm.data(), mask, ctx->Limg, cudaMemcpyDeviceToHost, st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  for (auto& v : hm) v = v != 0;
+  m->bits = hm;
+  if (e == cudaSuccess) e = cudaMalloc(&m->bits_dev, ctx->Limg);
+  if (e == cudaSuccess) e = cudaMemcpy(m->bits_dev, hm.data(), ctx->Limg, cudaMemcpyHostToDevice);
   for (int i = 0; i < ctx->Limg;) {  // unmasked runs for the compacted DMA copy (copy_mode 1)
     if (hm[i]) { ++i; continue; }
     int j = i;
@@ -631,6 +637,7 @@ extern "C" ig_status ig_mask_build(ig_ctx* ctx, const uint8_t* mask, void* strea
   }
   if (e != cudaSuccess) {
     cudaFree(m->idx);
+    if (m->bits_dev) cudaFree(m->bits_dev);
     delete m;
     return set_err(IG_ECUDA, "mask build: %s", cudaGetErrorString(e));
   }
@@ -652,6 +659,7 @@ extern "C" ig_status ig_mask_indices(const ig_mask* m, const int32_t** idx_m, co
 extern "C" void ig_mask_free(ig_mask* m) {
   if (!m) return;
   cudaFree(m->idx);
+  if (m->bits_dev) cudaFree(m->bits_dev);
   delete m;
 }
 
@@ -891,6 +899,13 @@ struct CopyPlan {
   bool any = false, gather = false, gather_q8 = false;
   int max_nu = 0;
   int kplan = 0;  // Algorithm-1 dense prefix: Y caches load Y_{b-1} for blocks b > kplan only
+  // load deduplication: requests on the same (host-tier cache, step) as an earlier
+  // request of the batch DMA only the rows that request did not load; the rest are copied
+  // HBM -> HBM from its ring buffer (kv_dedupe_kernel)
+  std::vector<int> dsrc;                                // per request: source index or -1
+  std::vector<std::vector<std::pair<int, int>>> druns;  // per member: runs of U_r \ U_src
+  std::vector<int> dshared;                             // per member: |U_r ∩ U_src|
+  DedupeArgs dd{};
 };
 
 static void issue_copy(ig_ctx* ctx, const std::vector<StepReq>& sr, const KvGatherReq* kvg_dev,
@@ -929,13 +944,15 @@ static void issue_copy(ig_ctx* ctx, const std::vector<StepReq>& sr, const KvGath
         cudaMemcpyAsync(dst, src, (size_t)ctx->Limg * row, cudaMemcpyDefault, ctx->copy_st);
         by = (long long)ctx->Limg * row;
       } else {
-        for (auto& run : sr[q].m->runs) {
+        const bool dd = !plan.dsrc.empty() && plan.dsrc[q] >= 0;
+        for (auto& run : dd ? plan.druns[q] : sr[q].m->runs) {
           const size_t off = (size_t)run.first * row;
           dsts.push_back(dst + off);
           srcs.push_back((void*)(src + off));
           sizes.push_back((size_t)run.second * row);
         }
-        by = (long long)n_u * row;
+        by = (long long)(dd ? n_u - plan.dshared[q] : n_u) * row;
+        if (dd) ctx->stats.d2d_bytes += (long long)plan.dshared[q] * row;
       }
       if (host) ctx->stats.h2d_bytes += by; else ctx->stats.d2d_bytes += by;
       continue;
@@ -973,16 +990,18 @@ static void issue_copy(ig_ctx* ctx, const std::vector<StepReq>& sr, const KvGath
       }
     } else if (host && ctx->o.copy_mode == 1) {  // DMA runs straight into the ring
       char* dst = (char*)ctx->kv_arena + ((size_t)slot * ctx->slot_stride + (size_t)buf * ctx->buf_elems) * ctx->esz;
+      const bool dd = !plan.dsrc.empty() && plan.dsrc[q] >= 0;
       for (int w = 0; w < 2; ++w) {
         const char* src = cache_plane(ctx, c, r->step, b, w);
-        for (auto& run : sr[q].m->runs) {
+        for (auto& run : dd ? plan.druns[q] : sr[q].m->runs) {
           const size_t off = (size_t)run.first * row;
           dsts.push_back(dst + w * vplane + txt_off + off);
           srcs.push_back((void*)(src + off));
           sizes.push_back((size_t)run.second * row);
         }
       }
-      by = 2LL * n_u * row;
+      by = 2LL * (dd ? n_u - plan.dshared[q] : n_u) * row;
+      if (dd) ctx->stats.d2d_bytes += 2LL * plan.dshared[q] * row;
     } else {
       by = 2LL * n_u * row;  // SM gather kernel below
     }
@@ -998,6 +1017,17 @@ static void issue_copy(ig_ctx* ctx, const std::vector<StepReq>& sr, const KvGath
       const size_t cnt = std::min(CHUNKC, sizes.size() - i);
       cudaMemcpyBatchAsync(dsts.data() + i, srcs.data() + i, sizes.data() + i, cnt, &attr, &attr_idx, 1, &fail,
                            ctx->copy_st);
+    }
+  }
+  if (plan.dd.n > 0) {  // rows shared with an earlier same-(cache, step) request: HBM -> HBM
+    const ig_cache* c0 = nullptr;
+    for (int q = 0; q < n && !c0; ++q) if (plan.dsrc[q] >= 0) c0 = sr[q].r->cache;
+    if (!(y_block(c0, b) && b <= plan.kplan)) {
+      DedupeArgs dd = plan.dd;
+      dd.buf_off = (long long)buf * ctx->buf_elems;
+      dd.v_only = y_block(c0, b) ? 1 : 0;
+      ctx->stats.kernel_launches++;
+      launch_kv_dedupe(dd, ctx->copy_st);
     }
   }
   if (plan.gather) {
@@ -1025,7 +1055,7 @@ static double block_flops_rows(const ig_ctx* ctx, long long rows) {
   return 2.0 * rows * (3 * H * H + H * H + 2 * H * F) + 4.0 * rows * ctx->L * H;
 }
 
-static int plan_prefix(ig_ctx* ctx, const std::vector<StepReq>& sr) {
+static int plan_prefix(ig_ctx* ctx, const std::vector<StepReq>& sr, const std::vector<int>& dshared) {
   const int N = ctx->nb;
   long long rows_m = 0, rows_all = 0;
   std::vector<long long> bytes(N, 0), rows_y(N, 0);
@@ -1035,12 +1065,13 @@ static int plan_prefix(ig_ctx* ctx, const std::vector<StepReq>& sr) {
     if (!s.use_cache) continue;
     const ig_cache* c = s.r->cache;
     const long long n_u = ctx->Limg - s.m->n_m;
+    const long long n_load = n_u - dshared[&s - &sr[0]];  // deduplicated rows cross the link once
     for (int b = 0; b < N; ++b) {
       if (y_block(c, b)) {  // one plane; the K/V projection of the unmasked rows is recomputed
-        if (b > 0) bytes[b] += n_u * ctx->H * (long long)ctx->esz;
+        if (b > 0) bytes[b] += n_load * ctx->H * (long long)ctx->esz;
         rows_y[b] += n_u;
       } else {
-        bytes[b] += c->fp8 ? 2LL * n_u * (ctx->H + 4 * ctx->d.heads) : 2LL * n_u * ctx->H * (long long)ctx->esz;
+        bytes[b] += c->fp8 ? 2LL * n_u * (ctx->H + 4 * ctx->d.heads) : 2LL * n_load * ctx->H * (long long)ctx->esz;
       }
     }
   }
@@ -1142,11 +1173,56 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
     any_cache |= s.use_cache;
     if (s.use_cache) max_nu = std::max(max_nu, ctx->Limg - s.m->n_m);
   }
+  CopyPlan plan;
+  {
+    static const bool no_dedupe = getenv("IG_NO_DEDUPE") != nullptr;  // A/B switch
+    auto dedupable = [&](int q) {
+      const ig_cache* c = sr[q].use_cache ? sr[q].r->cache : nullptr;
+      return c && c->tier == IG_CACHE_HOST && !c->fp8 && ctx->o.copy_mode == 1;
+    };
+    plan.dsrc.assign(na, -1);
+    plan.druns.assign(na, {});
+    plan.dshared.assign(na, 0);
+    for (int q = 0; q < na && !no_dedupe; ++q) {
+      if (!dedupable(q)) continue;
+      for (int q0 = 0; q0 < q; ++q0)
+        if (plan.dsrc[q0] < 0 && dedupable(q0) && sr[q0].r->cache == sr[q].r->cache && sr[q0].r->step == sr[q].r->step) {
+          if (plan.dd.n >= MAX_DEDUPE) break;
+          const auto& bq = sr[q].m->bits;
+          const auto& b0 = sr[q0].m->bits;
+          int shared = 0;
+          auto& runs = plan.druns[q];
+          for (int i = 0; i < ctx->Limg;) {  // runs of tokens unmasked in q but masked in q0
+            if (bq[i] || !b0[i]) { shared += !bq[i]; ++i; continue; }
+            int j = i;
+            while (j < ctx->Limg && !bq[j] && b0[j]) ++j;
+            runs.push_back({i, j - i});
+            i = j;
+          }
+          plan.dsrc[q] = q0;
+          plan.dshared[q] = shared;
+          DedupeEnt& e = plan.dd.e[plan.dd.n++];
+          e.idx_u = sr[q].m->idx + ctx->Limg;
+          e.n_u = ctx->Limg - sr[q].m->n_m;
+          e.bits0 = sr[q0].m->bits_dev;
+          e.slot0 = sr[q0].r->slot;
+          e.slot = sr[q].r->slot;
+          plan.dd.max_nu = std::max(plan.dd.max_nu, e.n_u);
+          break;
+        }
+    }
+    plan.dd.arena = ctx->kv_arena;
+    plan.dd.slot_stride = ctx->slot_stride;
+    plan.dd.L = ctx->L;
+    plan.dd.Lt = ctx->Lt;
+    plan.dd.H = H;
+    plan.dd.es = (int)es;
+  }
   // ---- Algorithm-1 block plan (C-AMB 23): a dense prefix of k blocks ----
   int kplan = 0;
   if (any_cache && !record && b0 == 0 && b1 == nb) {
     if (ctx->plan_mode == 1) kplan = std::min(ctx->plan_k, nb);
-    else if (ctx->plan_mode == 2) kplan = plan_prefix(ctx, sr);
+    else if (ctx->plan_mode == 2) kplan = plan_prefix(ctx, sr, plan.dshared);
   }
   ctx->last_plan_k = kplan;
   // unmasked image rows in the row set: Y-cache requests always (their K/V are recomputed from
@@ -1233,10 +1309,10 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
   for (int i = 0; i < nseg; ++i) npair += (hseg[i].q_len + 255) / 256;
   for (int i = 0; i < nsegf; ++i) npairf += (hsegf[i].q_len + 255) / 256;
   // copy-lane plan and per-(block, request) gather descriptors (see issue_copy)
-  CopyPlan plan;
   plan.any = any_cache;
   plan.max_nu = max_nu;
   plan.kplan = kplan;
+
   KvGatherReq* hkvq = hkvg + (size_t)nb * ctx->o.max_batch;
   KvGatherReq* dkvq = dkvg + (size_t)nb * ctx->o.max_batch;
   if (any_cache) {

@@ -294,6 +294,36 @@ template void launch_rows_to<float>(const float*, void*, long long, cudaStream_t
 template void launch_rows_to<bf16>(const float*, void*, long long, cudaStream_t);
 
 // ======================================================================================
+// Load deduplication: rows a same-(template, step) source request already staged
+// are copied HBM -> HBM instead of crossing the host link again.  Warp per (member, row).
+// ======================================================================================
+__global__ void __launch_bounds__(256) kv_dedupe_kernel(const DedupeArgs a) {
+  const int ent = blockIdx.y;
+  const DedupeEnt& d = a.e[ent];
+  const int lane = threadIdx.x & 31;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  const long long row_bytes = (long long)a.H * a.es;
+  const int nvec = (int)(row_bytes >> 4);
+  char* arena = reinterpret_cast<char*>(a.arena);
+  for (int j = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; j < d.n_u; j += warps) {
+    const int tok = d.idx_u[j];
+    if (d.bits0[tok]) continue;  // masked in the source: loaded over the link for this member
+    for (int plane = a.v_only; plane < 2; ++plane) {
+      const long long off = (a.buf_off + plane * a.L * a.H + (long long)(a.Lt + tok) * a.H) * a.es;
+      const int4* src = reinterpret_cast<const int4*>(arena + d.slot0 * a.slot_stride * a.es + off);
+      int4* dst = reinterpret_cast<int4*>(arena + d.slot * a.slot_stride * a.es + off);
+      for (int v = lane; v < nvec; v += 32) dst[v] = src[v];
+    }
+  }
+}
+
+void launch_kv_dedupe(const DedupeArgs& a, cudaStream_t st) {
+  if (a.n <= 0 || a.max_nu <= 0) return;
+  const int blocks = std::min((a.max_nu * 32 + 255) / 256, 64);
+  kv_dedupe_kernel<<<dim3(blocks, a.n), 256, 0, st>>>(a);
+}
+
+// ======================================================================================
 // FP8 (e4m3) K/V cache.  Quantize: per (token, head) scale = amax / 448 (fp32),
 // q = e4m3 round-to-nearest-even of x / scale (saturating); amax = 0 -> scale 1.
 // ======================================================================================

@@ -111,6 +111,24 @@ void launch_ln_mod_staged(const void* arena, long long slot_stride, long long bu
 template <typename T>
 void launch_rows_to(const float* src, void* dst, long long n, cudaStream_t st);
 
+// ---- load deduplication (k_rows.cu): requests on the same (template, step) ------
+// Member e of a dedupe group reuses the rows its source request (slot0) already loaded: for
+// every unmasked token of the member that is also unmasked in the source (bits0[tok] == 0),
+// copy the staged K and V rows (V only for Y blocks) of ring buffer buf_off from slot0 to slot.
+struct DedupeEnt {
+  const int32_t* idx_u; int n_u;
+  const uint8_t* bits0;  // source request's mask bitmap (1 = masked)
+  int slot0, slot;
+};
+constexpr int MAX_DEDUPE = 16;
+struct DedupeArgs {
+  DedupeEnt e[MAX_DEDUPE];
+  int n, max_nu;
+  void* arena; long long slot_stride, buf_off, L;
+  int Lt, H, es, v_only;
+};
+void launch_kv_dedupe(const DedupeArgs& a, cudaStream_t st);
+
 // ---- a11 exit: Euler scatter (k_rows.cu) ------------------------------------------------
 // latent_req[idx_m[j]][c] += dsig_req * v[img_row][c]
 void launch_scatter_euler(const ReqDev* reqs, int n, int M_img, const RowInfo* ri, int M_txt,

@@ -662,3 +662,46 @@ def test_cuda_graph_steps_bitwise_equal_eager():
     ig.ig_ctx_destroy(gctx)
     m2.close()
     eager.close()
+
+
+@pytest.mark.parametrize("kind", ["kv", "hybrid"])
+def test_load_dedupe_same_template_and_step(kind):
+    """Requests on the same (host-tier cache, step) share their staged rows (SURVEY N4 load
+    deduplication): a lockstep batch equals each request run alone bit for bit, and moves
+    fewer host-link bytes than the requests alone."""
+    from gpu_util import hybrid_planes
+    d = synth.FLUX_SMALL
+    sig = [1.0, 0.7, 0.4]
+    opts = ig.ig_ctx_opts(4, 0, 2, 1, 0, 0) if kind == "kv" else ig.ig_ctx_opts(4, 0, 2, 1, 0, 0, 1, 2)
+    m = Model(d, ig.IG_BF16, opts=opts)
+    rng = np.random.default_rng(51)
+    masks = [synth.blob_mask_count(d, 90, rng), synth.rect_mask_count(d, 40, rng), synth.blob_mask_count(d, 130, rng)]
+    alone = [Request(m, 190 + i, mk) for i, mk in enumerate(masks)]
+    batch = [Request(m, 190 + i, mk) for i, mk in enumerate(masks)]
+    kv = synth.make_cache_kv(d, 13, 2, dtype=torch.bfloat16)
+    tlat = torch.stack([synth.make_latent(d, 995 + s) for s in range(2)])
+    cache = ig.ig_cache_create(m.ctx, 2, ig.IG_CACHE_HOST)
+    if kind == "kv":
+        fill_cache(m, cache, kv, tlat)
+    else:
+        ym = set(ig.y_block_modes(d.n_blocks, 2))
+        fill_cache(m, cache, hybrid_planes(kv, synth.make_cache_y(d, 13, 2, dtype=torch.bfloat16), ym), tlat)
+    h2d_alone = 0
+    for s in range(2):
+        for i, r in enumerate(alone):
+            ig.ig_edit_step(m.ctx, [r.req(i, cache, s, sig[s], sig[s + 1])], 0)
+            h2d_alone += ig.ig_last_stats(m.ctx)["h2d_bytes"]
+    h2d_batch = 0
+    for s in range(2):
+        ig.ig_edit_step(m.ctx, [r.req(i, cache, s, sig[s], sig[s + 1]) for i, r in enumerate(batch)], 0)
+        st = ig.ig_last_stats(m.ctx)
+        h2d_batch += st["h2d_bytes"]
+        assert st["d2d_bytes"] > 0
+    torch.cuda.synchronize()
+    for a, b in zip(alone, batch):
+        assert torch.equal(a.latent, b.latent)
+    assert h2d_batch < h2d_alone
+    ig.ig_cache_free(cache)
+    for r in alone + batch:
+        r.free()
+    m.close()
