@@ -99,6 +99,50 @@ def test_flux_teacher_forced_block(flux, block, m_ratio, kind):
     rq.free()
 
 
+@pytest.mark.parametrize("block", [5, 19 + 9])
+def test_flux_teacher_forced_y_block(flux, block):
+    """Full-width Y block through ig_debug_block: the unmasked rows' block input is
+    the staged Y_{b-1}, their K/V recomputed with this request's modulation; vs the oracle's
+    kv_from_y + masked block on the same inputs (C-TOL-full)."""
+    ptrs = [flux.W[n].data_ptr() for n, _, _ in synth.weight_table(D)]
+    ctx = ig.ig_ctx_create(flux.desc, ptrs, 0, ig.ig_ctx_opts(8, 8 * D.L, 2, 1, 0, 0, 1, 0))
+    rng = np.random.default_rng(block + 100)
+    mask = synth.blob_mask_count(D, int(round(0.2 * D.L_img)), rng)
+    rq = Request(flux, 88 + block, mask)
+    cache = ig.ig_cache_create(ctx, 1, ig.IG_CACHE_DEVICE)
+    y = synth.normal(600 + block, "y_blk", (D.L_img, D.hidden), "cuda").float().bfloat16()
+    ptr, _, _ = ig.ig_cache_storage(cache)
+    plane = D.L_img * D.hidden * 2
+    ig.ig_copy(ptr + (block - 1) * plane, y.data_ptr(), plane)  # pure Y: plane b holds Y_b
+    rows = D.txt_len + rq.n_m
+    X_in = synth.normal(950 + block, "X_in_y", (rows, D.hidden), "cuda").float()
+    X_out = torch.full_like(X_in, float("nan"))
+    sigma, sigma_next = 0.6, 0.55
+    ig.ig_debug_block(ctx, rq.req(0, cache, 0, sigma, sigma_next), block, X_in.data_ptr(), X_out.data_ptr())
+    pre = f"double.{block}." if block < D.n_double else f"single.{block - D.n_double}."
+    names = {nm for nm, _, _ in synth.weight_table(D) if nm.startswith(pre)} | {"t_mlp1.w", "t_mlp1.b", "t_mlp2.w", "t_mlp2.b"}
+    W = _host_block_weights(names)
+    _, _, cond = rq.host_inputs()
+    vec = oracle.conditioning(W, sigma, cond)
+    idx_m, idx_u, _ = oracle.index_build(mask)
+    kv = oracle.kv_from_y(D, W, block, y.double().cpu().numpy()[idx_u], vec, idx_u)
+    Xh = X_in.double().cpu().numpy()
+    if block < D.n_double:
+        xt, xi = oracle.double_block_masked(D, W, block, Xh[:D.txt_len], Xh[D.txt_len:], vec, idx_m, idx_u, kv)
+        ref = np.concatenate([xt, xi])
+    else:
+        ref = oracle.single_block_masked(D, W, block - D.n_double, Xh, vec, idx_m, idx_u, kv)
+    got = X_out.double().cpu().numpy()
+    dg, do = got - Xh, ref - Xh
+    normwise = np.linalg.norm(dg - do) / np.linalg.norm(do)
+    assert normwise <= 2e-2, normwise
+    ok, worst = ctol(dg, do, 2e-2, atol_mult=2.0)
+    assert ok, ("update", worst)
+    ig.ig_cache_free(cache)
+    rq.free()
+    ig.ig_ctx_destroy(ctx)
+
+
 def test_flux_same_trajectory_bitwise_and_batch_invariance(flux):
     sig = (1.0, 0.96)
     rng = np.random.default_rng(5)
