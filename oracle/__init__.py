@@ -11,3 +11,4 @@ arithmetic.
 Citations: P:n = PAPER.md line n, S:n = SPEC.md line n, C-AMB k = DESIGN.md reading k.
 """
 from .instgenie import *  # noqa: F401,F403
+from .unet import *  # noqa: F401,F403,E402

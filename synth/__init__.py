@@ -115,6 +115,12 @@ class ModelDesc:
     ln_eps: float = 1e-6
     pos_embed_2d: int = 0
     context_pre_only_last: int = 0
+    # SDXL-UNet attention stack (config 5): n_unet BasicTransformerBlocks
+    # (LN -> self-attn -> LN -> cross-attn to a [ctx_len, ctx_dim] context -> LN -> GEGLU FF);
+    # no conditioning, no text rows, lat_ch = hidden (the level's hidden state is the latent)
+    n_unet: int = 0
+    ctx_len: int = 0
+    ctx_dim: int = 0
 
     @property
     def L_img(self) -> int:
@@ -126,7 +132,7 @@ class ModelDesc:
 
     @property
     def n_blocks(self) -> int:
-        return self.n_double + self.n_single
+        return self.n_double + self.n_single + self.n_unet
 
 
 TINY = ModelDesc("tiny", 0, 1, 64, 4, 16, 256, 16, 16, 16, 0, rope_axes=(4, 6, 6))
@@ -140,7 +146,22 @@ FLUX_SMALL = ModelDesc("flux_small", 2, 2, 256, 2, 128, 1024, 64, 16, 16, 32)
 # text length, context-pre-only last block)
 SD3_SMALL = ModelDesc("sd3_small", 2, 0, 128, 2, 64, 512, 64, 8, 8, 13, qk_norm=0, rope=0,
                       rope_axes=(0, 0, 0), pos_embed_2d=1, context_pre_only_last=1)
-MODELS = {m.name: m for m in (TINY, TINY_DOUBLE, SD3, FLUX, FLUX_SMALL, SD3_SMALL)}
+
+
+
+def _unet(name, n, H, heads, grid, ctx_len, ctx_dim):
+    return ModelDesc(name, 0, 0, H, heads, H // heads, 4 * H, H, grid, grid, 0, qk_norm=0, rope=0,
+                     rope_axes=(0, 0, 0), ln_eps=1e-5, n_unet=n, ctx_len=ctx_len, ctx_dim=ctx_dim)
+
+
+# SDXL-UNet attention stacks (config 5): the 64x64 level (10 blocks, C=640, h=10) and the
+# 32x32 level (60 blocks, C=1280, h=20), d = 64, cross-attention to 77 x 2048 text tokens
+UNET_TINY = _unet("unet_tiny", 2, 64, 4, 16, 7, 32)
+UNET_SMALL = _unet("unet_small", 3, 128, 2, 16, 13, 64)
+SDXL_L64 = _unet("sdxl_attn64", 10, 640, 10, 64, 77, 2048)
+SDXL_L32 = _unet("sdxl_attn32", 60, 1280, 20, 32, 77, 2048)
+MODELS = {m.name: m for m in (TINY, TINY_DOUBLE, SD3, FLUX, FLUX_SMALL, SD3_SMALL,
+                              UNET_TINY, UNET_SMALL, SDXL_L64, SDXL_L32)}
 
 
 def weight_table(d: ModelDesc) -> List[Tuple[str, Tuple[int, ...], int]]:
@@ -153,6 +174,21 @@ def weight_table(d: ModelDesc) -> List[Tuple[str, Tuple[int, ...], int]]:
     def lin(name, out, inp):
         t.append((name + ".w", (out, inp), inp))
         t.append((name + ".b", (out,), inp))
+
+    if d.n_unet:
+        for i in range(d.n_unet):
+            p = f"unet.{i}"
+            t += [(p + ".ln1.g", (H,), 0), (p + ".ln1.b", (H,), 0)]
+            t.append((p + ".attn1.qkv.w", (3 * H, H), H))      # to_q|to_k|to_v, no bias
+            lin(p + ".attn1.out", H, H)
+            t += [(p + ".ln2.g", (H,), 0), (p + ".ln2.b", (H,), 0)]
+            t.append((p + ".attn2.q.w", (H, H), H))             # no bias
+            t.append((p + ".attn2.kv.w", (2 * H, d.ctx_dim), d.ctx_dim))  # to_k|to_v, no bias
+            lin(p + ".attn2.out", H, H)
+            t += [(p + ".ln3.g", (H,), 0), (p + ".ln3.b", (H,), 0)]
+            lin(p + ".ff.geglu", 2 * Fm, H)                     # [hidden | gate]
+            lin(p + ".ff.out", H, Fm)
+        return t
 
     lin("img_in", H, C)
     lin("t_mlp1", H, 256)
@@ -190,6 +226,9 @@ def make_weight(d: ModelDesc, name: str, shape, fan_in: int, seed: int = 0, devi
     """One table tensor.  uniform(+-1/sqrt(fan_in)); modulation weights x0.1; norm gains 1."""
     if name.endswith("_norm_g"):
         return torch.ones(shape, dtype=dtype, device=device)
+    if ".ln" in name:  # UNet LayerNorm affine: gain 1 + 0.1 u, bias 0.1 u
+        v = uniform(seed, name, shape, device) * 0.1 + (1.0 if name.endswith(".g") else 0.0)
+        return v.to(torch.float32).to(dtype)
     if name == "pos_embed":
         v = uniform(seed, name, shape, device) * 0.5
     else:
@@ -219,6 +258,11 @@ def make_latent(d: ModelDesc, rid: int, device="cpu") -> torch.Tensor:
 
 def make_txt(d: ModelDesc, rid: int, device="cpu", dtype=torch.float32) -> torch.Tensor:
     return normal(rid, "txt", (d.txt_len, d.hidden), device).to(torch.float32).to(dtype)
+
+
+def make_ctx(d: ModelDesc, rid: int, device="cpu", dtype=torch.float32) -> torch.Tensor:
+    """UNet cross-attention context (encoder hidden states) [ctx_len, ctx_dim]."""
+    return normal(rid, "ctx", (d.ctx_len, d.ctx_dim), device).to(torch.float32).to(dtype)
 
 
 def make_cond(d: ModelDesc, rid: int, device="cpu") -> torch.Tensor:
