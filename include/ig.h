@@ -57,9 +57,24 @@ typedef struct {
   int pos_embed_2d;         /* SD3: add pos_embed[token] at img_in                       */
   int context_pre_only_last;/* SD3: last double block's text stream only feeds K/V      */
   ig_dtype dtype;           /* IG_F32 = parity mode (fp32 SIMT), IG_BF16 = perf mode    */
+  /* SDXL-UNet attention stack (BASELINE config 5; "a latent of shape
+   * (B, C, H, W) is reshaped to (B, H x W, C) to pass through transformer blocks"): n_unet > 0
+   * selects a model of n_unet BasicTransformerBlocks (C-AMB 31-33): x += SelfAttn(LN1(x)),
+   * x += CrossAttn(LN2(x), context [ctx_len, ctx_dim]), x += GEGLU-FF(LN3(x)); LayerNorms with
+   * affine (eps = ln_eps), no conditioning, no text rows.  Requires n_double = n_single = 0,
+   * txt_len = 0, qk_norm = rope = pos_embed_2d = 0, lat_ch = hidden (the request's "latent"
+   * is the level's hidden state [L_img, hidden] fp32; a step runs the stack on its masked rows
+   * and writes the block stack's output rows back in place), mlp_hidden = GEGLU inner width. */
+  int n_unet, ctx_len, ctx_dim;
 } ig_model_desc;
 
-/* Weight table (device pointers, caller-owned, dtype = desc.dtype except where noted),
+/* UNet weight table (n_unet > 0), per block i:
+ *   ln1.g [H], ln1.b [H], attn1.qkv.w [3H,H] (to_q|to_k|to_v, no bias), attn1.out.w [H,H],
+ *   attn1.out.b, ln2.g, ln2.b, attn2.q.w [H,H] (no bias), attn2.kv.w [2H,ctx_dim] (to_k|to_v,
+ *   no bias), attn2.out.w [H,H], attn2.out.b, ln3.g, ln3.b, ff.geglu.w [2F,H] ([hidden|gate]
+ *   rows), ff.geglu.b [2F], ff.out.w [H,F], ff.out.b — 17 entries per block.
+ *
+ * Weight table (device pointers, caller-owned, dtype = desc.dtype except where noted),
  * in this fixed order; matrices are [out, in] row-major (nn.Linear), each followed by its
  * bias [out]:
  *   img_in.w [H,C], img_in.b, t_mlp1.w [H,256], t_mlp1.b, t_mlp2.w [H,H], t_mlp2.b,
@@ -185,8 +200,9 @@ typedef struct {
   const ig_cache* cache;   /* NULL allowed only when n_m == L_img (ignored then, C-AMB 27)   */
   int step;                /* index into the cache's schedule (C-AMB 9)                      */
   float sigma, sigma_next; /* flow-matching Euler step; t = 1000*sigma (C-AMB 12)            */
-  const void* txt;         /* dev [txt_len, H] (desc.dtype)                                  */
-  const float* cond_vec;   /* dev [H] fp32                                                   */
+  const void* txt;         /* dev [txt_len, H] (desc.dtype); UNet models: the cross-attention */
+                           /* context [ctx_len, ctx_dim] (desc.dtype)                        */
+  const float* cond_vec;   /* dev [H] fp32 (unused, may be NULL, for UNet models)            */
 } ig_edit_req;
 
 /* Y-cache requests (cache created by a cache_y ctx; any ctx can consume them, and a batch may

@@ -87,6 +87,14 @@ struct SingleW {
   const void* kg = nullptr;
   int mod_t = -1;
 };
+// UNet BasicTransformerBlock (config 5; ig.h weight table): LayerNorm affines live in
+// ctx->unet_ln as (shift = beta, scale = gamma - 1) rows for the LN-modulation kernel
+struct UnetW {
+  const void* qkv = nullptr;            // [3H, H], no bias
+  LinW out1, q2, kv2, out2, geglu, ff2; // q2 / kv2 without bias
+  const void* geglu_w_tc = nullptr;     // tile-interleaved copy for EPI_GEGLU (bf16 + tcgen05)
+  const void* geglu_b_tc = nullptr;
+};
 struct ModT {
   const LinW* w;
   int k;
@@ -135,6 +143,18 @@ struct ig_ctx {
   const void* pos_embed = nullptr;
   std::vector<StreamW> dimg, dtxt;
   std::vector<SingleW> sgl;
+  std::vector<UnetW> unet;
+  // UNet-only buffers: LN constants fp32 [nb][3][2H]; ones [H] (ungated residual); cross K/V
+  // arena [max_batch][2][ctx_len][H]; packed contexts [max_batch * ctx_len][ctx_dim]; the
+  // context rows' RowInfo (static: slot = request index, kvpos = context token); unfused GEGLU
+  // input [max_rows][2F]; interleaved GEGLU weights (bf16)
+  float* unet_ln = nullptr;
+  float* ones = nullptr;
+  void* xkv = nullptr;
+  void* ctxp = nullptr;
+  RowInfo* ri_c = nullptr;
+  void* u2 = nullptr;
+  void* geglu_tc = nullptr;
   std::vector<ModT> mods;
   long long mod_ld = 0;
   int fmod_t = -1;
@@ -239,6 +259,7 @@ static bool desc_equal(const ig_model_desc& a, const ig_model_desc& b) {
 
 extern "C" int ig_weight_count(const ig_model_desc* d) {
   if (!d) return -1;
+  if (d->n_unet > 0) return 17 * d->n_unet;
   int n = 10 + (d->pos_embed_2d ? 1 : 0);
   for (int i = 0; i < d->n_double; ++i)
     for (int s = 0; s < 2; ++s) {
@@ -306,8 +327,18 @@ static ig_status validate_desc(const ig_model_desc* d) {
   if (d->hidden <= 0 || d->heads <= 0 || d->head_dim <= 0 || d->hidden != d->heads * d->head_dim)
     return set_err(IG_EINVAL, "hidden (%d) must equal heads (%d) * head_dim (%d)", d->hidden,
                    d->heads, d->head_dim);
-  if (d->n_double < 0 || d->n_single < 0 || d->n_double + d->n_single <= 0)
+  if (d->n_double < 0 || d->n_single < 0 || d->n_unet < 0 || d->n_double + d->n_single + d->n_unet <= 0)
     return set_err(IG_EINVAL, "need at least one block");
+  if (d->n_unet > 0) {
+    if (d->n_double || d->n_single || d->txt_len || d->qk_norm || d->rope || d->pos_embed_2d ||
+        d->context_pre_only_last || d->lat_ch != d->hidden)
+      return set_err(IG_EINVAL, "UNet models: no double/single blocks, txt_len = qk_norm = rope = "
+                                "pos_embed_2d = 0 and lat_ch = hidden");
+    if (d->ctx_len <= 0 || d->ctx_dim <= 0 || d->ctx_dim % 8)
+      return set_err(IG_EINVAL, "UNet models need ctx_len > 0 and ctx_dim a positive multiple of 8");
+  } else if (d->ctx_len || d->ctx_dim) {
+    return set_err(IG_EINVAL, "ctx_len / ctx_dim are for UNet models only");
+  }
   if (d->grid_h <= 0 || d->grid_w <= 0 || d->lat_ch <= 0 || d->txt_len < 0 || d->mlp_hidden <= 0)
     return set_err(IG_EINVAL, "bad grid/lat_ch/txt_len/mlp_hidden");
   if (d->head_dim != 16 && d->head_dim != 64 && d->head_dim != 128)
@@ -373,6 +404,10 @@ extern "C" ig_status ig_ctx_create(const ig_model_desc* desc, const void* const*
   if (o.cache_fp8 && o.cache_y) return set_err(IG_EUNSUPPORTED, "cache_y with cache_fp8 is not supported");
   const int Lall = desc->txt_len + desc->grid_h * desc->grid_w;
   if (o.max_rows <= 0) o.max_rows = o.max_batch * Lall;
+  if (desc->n_unet > 0) {
+    if (o.cache_y) return set_err(IG_EUNSUPPORTED, "UNet models: K/V caches only (cache_y)");
+    o.max_rows = std::max(o.max_rows, o.max_batch * desc->ctx_len);  // the context rows' K/V projection
+  }
 
   CUDA_TRY(cudaSetDevice(device));
   ig_ctx* ctx = new ig_ctx();
@@ -382,7 +417,7 @@ extern "C" ig_status ig_ctx_create(const ig_model_desc* desc, const void* const*
   ctx->esz = desc->dtype == IG_F32 ? 4 : 2;
   ctx->H = desc->hidden; ctx->F = desc->mlp_hidden; ctx->C = desc->lat_ch;
   ctx->Limg = desc->grid_h * desc->grid_w; ctx->Lt = desc->txt_len; ctx->L = Lall;
-  ctx->nb = desc->n_double + desc->n_single;
+  ctx->nb = desc->n_double + desc->n_single + desc->n_unet;
   ctx->R = o.prefetch_depth + 1;
   ctx->w.assign(weights, weights + nw);
   const int H = ctx->H, F = ctx->F, C = ctx->C;
@@ -390,6 +425,23 @@ extern "C" ig_status ig_ctx_create(const ig_model_desc* desc, const void* const*
   // resolve the weight table (order documented in ig.h)
   int k = 0;
   auto lin = [&](LinW& l, int outd, int ind) { l.w = weights[k++]; l.b = weights[k++]; l.out = outd; l.in = ind; };
+  std::vector<const void*> ln_ptrs;  // UNet: [nb][3][gamma, beta]
+  ctx->unet.resize(desc->n_unet);
+  for (int i = 0; i < desc->n_unet; ++i) {
+    UnetW& u = ctx->unet[i];
+    auto nobias = [&](LinW& l, int outd, int ind) { l.w = weights[k++]; l.out = outd; l.in = ind; };
+    ln_ptrs.push_back(weights[k++]); ln_ptrs.push_back(weights[k++]);
+    u.qkv = weights[k++];
+    lin(u.out1, H, H);
+    ln_ptrs.push_back(weights[k++]); ln_ptrs.push_back(weights[k++]);
+    nobias(u.q2, H, H);
+    nobias(u.kv2, 2 * H, desc->ctx_dim);
+    lin(u.out2, H, H);
+    ln_ptrs.push_back(weights[k++]); ln_ptrs.push_back(weights[k++]);
+    lin(u.geglu, 2 * F, H);
+    lin(u.ff2, H, F);
+  }
+  if (desc->n_unet == 0) {
   lin(ctx->img_in, H, C);
   lin(ctx->t1, H, 256);
   lin(ctx->t2, H, H);
@@ -415,6 +467,7 @@ extern "C" ig_status ig_ctx_create(const ig_model_desc* desc, const void* const*
     if (desc->qk_norm) { sw.qg = weights[k++]; sw.kg = weights[k++]; }
     lin(sw.lin2, H, H + F);
   }
+  }  // n_unet == 0
   // modulation tensors and their offsets inside one request's modulation row
   auto add_mod = [&](const LinW* l, int kk) {
     ctx->mods.push_back({l, kk, ctx->mod_ld});
@@ -426,7 +479,7 @@ extern "C" ig_status ig_ctx_create(const ig_model_desc* desc, const void* const*
     if (ctx->Lt > 0) ctx->dtxt[i].mod_t = add_mod(&ctx->dtxt[i].mod, ctx->dtxt[i].pre_only ? 2 : 6);
   }
   for (int i = 0; i < desc->n_single; ++i) ctx->sgl[i].mod_t = add_mod(&ctx->sgl[i].mod, 3);
-  ctx->fmod_t = add_mod(&ctx->fmod, 2);
+  if (desc->n_unet == 0) ctx->fmod_t = add_mod(&ctx->fmod, 2);
 
   // workspaces
   const long long Mx = o.max_rows, B = o.max_batch, es = (long long)ctx->esz;
@@ -452,6 +505,49 @@ extern "C" ig_status ig_ctx_create(const ig_model_desc* desc, const void* const*
   cudaMemset(ctx->kv_arena, 0, (size_t)(B * ctx->slot_stride * es));
   cudaMemset(ctx->X, 0, Mx * H * 4);
   if ((s = build_rope_table(ctx)) != IG_OK) { ig_ctx_destroy(ctx); return s; }
+  if (desc->n_unet > 0) {  // UNet constants and buffers
+    const int nbu = desc->n_unet, Lc = desc->ctx_len, Dc = desc->ctx_dim;
+    okm &= dmalloc((void**)&ctx->unet_ln, (size_t)nbu * 3 * 2 * H * 4);
+    okm &= dmalloc((void**)&ctx->ones, (size_t)H * 4);
+    okm &= dmalloc(&ctx->xkv, (size_t)B * 2 * Lc * H * es);
+    okm &= dmalloc(&ctx->ctxp, (size_t)B * Lc * Dc * es);
+    okm &= dmalloc((void**)&ctx->ri_c, (size_t)B * Lc * sizeof(RowInfo));
+    okm &= dmalloc(&ctx->u2, (size_t)Mx * 2 * F * es);
+    const bool tc_geglu = desc->dtype == IG_BF16 && F % 128 == 0;
+    if (tc_geglu) okm &= dmalloc(&ctx->geglu_tc, (size_t)nbu * 2 * F * (H + 1) * 2);
+    if (!okm) { ig_ctx_destroy(ctx); return set_err(IG_ENOMEM, "UNet workspace allocation failed"); }
+    // LN affine -> (shift = beta, scale = gamma - 1): LN(x) * (1 + scale) + shift == LN(x) * gamma + beta
+    // (gamma - 1 is exact in fp32 for gamma in [0.5, 2], and 1 + (gamma - 1) == gamma there)
+    std::vector<float> lnh((size_t)nbu * 3 * 2 * H), ones(H, 1.f);
+    std::vector<char> tmp((size_t)H * es);
+    for (int i = 0; i < nbu * 3; ++i) {
+      for (int w = 0; w < 2; ++w) {
+        CUDA_TRY(cudaMemcpy(tmp.data(), ln_ptrs[2 * i + w], (size_t)H * es, cudaMemcpyDeviceToHost));
+        for (int c = 0; c < H; ++c) {
+          float v;
+          if (es == 4) v = reinterpret_cast<const float*>(tmp.data())[c];
+          else { uint32_t b = (uint32_t)reinterpret_cast<const uint16_t*>(tmp.data())[c] << 16; memcpy(&v, &b, 4); }
+          if (w == 0) lnh[(size_t)i * 2 * H + H + c] = v - 1.f;  // scale
+          else lnh[(size_t)i * 2 * H + c] = v;                   // shift
+        }
+      }
+    }
+    CUDA_TRY(cudaMemcpy(ctx->unet_ln, lnh.data(), lnh.size() * 4, cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(ctx->ones, ones.data(), (size_t)H * 4, cudaMemcpyHostToDevice));
+    std::vector<RowInfo> ric((size_t)B * Lc);
+    for (int q = 0; q < B; ++q)
+      for (int j = 0; j < Lc; ++j) ric[(size_t)q * Lc + j] = RowInfo{q, q, j, -1};
+    CUDA_TRY(cudaMemcpy(ctx->ri_c, ric.data(), ric.size() * sizeof(RowInfo), cudaMemcpyHostToDevice));
+    if (tc_geglu)
+      for (int i = 0; i < nbu; ++i) {
+        bf16* wd = (bf16*)ctx->geglu_tc + (size_t)i * 2 * F * (H + 1);
+        bf16* bd = wd + (size_t)2 * F * H;
+        launch_permute_geglu_rows((const bf16*)ctx->unet[i].geglu.w, wd, F, H, 0);
+        launch_permute_geglu_rows((const bf16*)ctx->unet[i].geglu.b, bd, F, 1, 0);
+        ctx->unet[i].geglu_w_tc = wd;
+        ctx->unet[i].geglu_b_tc = bd;
+      }
+  }
 
   // static GEMV problem lists (a3)
   std::vector<GemvProb> p1(1), p2(1);
@@ -534,7 +630,8 @@ extern "C" void ig_ctx_destroy(ig_ctx* ctx) {
   void* bufs[] = {ctx->X, ctx->vel, ctx->temb, ctx->tmp, ctx->vec, ctx->svec, ctx->modbuf, ctx->h,
                   ctx->qkv, ctx->Q, ctx->cat, ctx->Ain, ctx->ri, ctx->kv_arena, ctx->rope_tab,
                   ctx->gv_t1, ctx->gv_t2, ctx->gv_mod, ctx->modw, ctx->modb, ctx->svec_bf,
-                  ctx->q8in, ctx->q8in_scl, ctx->q8rec, ctx->q8rec_scl, ctx->yrec};
+                  ctx->q8in, ctx->q8in_scl, ctx->q8rec, ctx->q8rec_scl, ctx->yrec, ctx->unet_ln,
+                  ctx->ones, ctx->xkv, ctx->ctxp, ctx->ri_c, ctx->u2, ctx->geglu_tc};
   for (void* b : bufs) if (b) cudaFree(b);
   for (int i = 0; i < NSTAGE; ++i) {
     if (ctx->h_stage[i]) cudaFreeHost(ctx->h_stage[i]);
@@ -1135,6 +1232,7 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
   const int H = ctx->H, F = ctx->F, C = ctx->C, Lt = ctx->Lt, nb = ctx->nb, R = ctx->R;
   const int b0 = rng.b0, b1 = rng.b1 < 0 ? nb : rng.b1;
   const long long es = (long long)ctx->esz;
+  const bool unet = ctx->d.n_unet > 0;
   ctx->stats = ig_stats{};
   auto t_host0 = std::chrono::steady_clock::now();
   // ---- host validation (nothing enqueued before this passes) ----
@@ -1147,7 +1245,7 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
     if (r.slot < 0 || r.slot >= ctx->o.max_batch) return set_err(IG_EINVAL, "req %d: slot %d out of range", i, r.slot);
     if (slots_seen & (1u << r.slot)) return set_err(IG_EINVAL, "req %d: duplicate slot %d", i, r.slot);
     slots_seen |= 1u << r.slot;
-    if (!r.mask || !r.latent || !r.cond_vec || (Lt > 0 && !r.txt))
+    if (!r.mask || !r.latent || (!unet && !r.cond_vec) || ((Lt > 0 || unet) && !r.txt))
       return set_err(IG_EINVAL, "req %d: NULL mask/latent/txt/cond_vec", i);
     if (r.mask->L_img != ctx->Limg) return set_err(IG_EINVAL, "req %d: mask built for another model", i);
     const int nm = r.mask->n_m;
@@ -1220,7 +1318,7 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
   }
   // ---- Algorithm-1 block plan (C-AMB 23): a dense prefix of k blocks ----
   int kplan = 0;
-  if (any_cache && !record && b0 == 0 && b1 == nb) {
+  if (any_cache && !record && b0 == 0 && b1 == nb && !unet) {  // (UNet: no Algorithm-1 plan yet)
     if (ctx->plan_mode == 1) kplan = std::min(ctx->plan_k, nb);
     else if (ctx->plan_mode == 2) kplan = plan_prefix(ctx, sr, plan.dshared);
   }
@@ -1296,6 +1394,10 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
     if (Lt > 0) { hseg[nseg++] = AttnSeg{q * Lt, Lt, kvb}; max_q = std::max(max_q, Lt); }
     hseg[nseg++] = AttnSeg{img_row, d.n_m, kvb};
     max_q = std::max(max_q, d.n_m);
+    if (unet) {  // cross-attention segments (the dense-prefix slots: UNet steps never plan)
+      hsegf[nsegf++] = AttnSeg{img_row, d.n_m, (long long)q * 2 * ctx->d.ctx_len * H};
+      max_qf = std::max(max_qf, d.n_m);
+    }
     if (kplan > 0) {
       if (Lt > 0) hsegf[nsegf++] = AttnSeg{q * Lt, Lt, kvb};
       hsegf[nsegf++] = AttnSeg{img_row, d.n_m, kvb};
@@ -1432,9 +1534,14 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
   // ---- a2/a4: rows + gather; a3: conditioning ----
   {
     ProfScope ps(ctx, st, IG_K_ROWS, 0.0, (double)M_txt * H * (4 + es) + (double)M_img * C * (4 + es));
-    launch_build_rows<T>(dreq, na, Lt, C, H, M_txt, M, ctx->ri, ctx->X, (T*)ctx->Ain, st, M_full);
+    launch_build_rows<T>(dreq, na, Lt, C, H, M_txt, M, ctx->ri, ctx->X, (T*)ctx->Ain, st, M_full, unet ? 1 : 0);
   }
-  {
+  if (unet) {
+    ProfScope ps(ctx, st, IG_K_ROWS, 0.0, 2.0 * na * ctx->d.ctx_len * ctx->d.ctx_dim * es);
+    launch_pack_ctx<T>(dreq, na, ctx->d.ctx_len, ctx->d.ctx_dim, (T*)ctx->ctxp, st);
+    stats.kernel_launches++;
+  }
+  if (!unet) {
   ProfScope ps_cond(ctx, st, IG_K_COND, 0.0, (double)ctx->mod_ld * H * es);
   launch_timestep_embed(dreq, na, ctx->temb, st);
   launch_gemv<T>(ctx->gv_t1, 1, (H + 31) / 32, na, 256, st);
@@ -1452,8 +1559,10 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
     launch_gemv<T>(ctx->gv_mod, (int)ctx->gv_mod_host.size(), ctx->gv_mod_groups, na, H, st);
   }
   }
-  stats.kernel_launches += 7;
-  if (rng.X_in) {  // teacher-forced residual rows (+ img_in of the template rows, if any)
+  if (!unet) stats.kernel_launches += 7;
+  if (unet) {
+    // the masked rows of the level's hidden state are already in X (build_rows)
+  } else if (rng.X_in) {  // teacher-forced residual rows (+ img_in of the template rows, if any)
     CUDA_TRY(cudaMemcpyAsync(ctx->X, rng.X_in, (size_t)M * H * 4, cudaMemcpyDeviceToDevice, st));
     if (M_full > M) {
       GemmArgs g{};
@@ -1513,7 +1622,7 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
   };
   // a6: QKV projection + norm/RoPE/Q-pack/positional K/V merge.  bf16 mode fuses the whole
   // epilogue into the tensor-core GEMM; fp32 parity mode runs the GEMM then qkv_post.
-  const bool fused_qkv = ctx->d.dtype == IG_BF16 && g_tc_gemm && (H % 256) == 0 &&
+  const bool fused_qkv = ctx->d.dtype == IG_BF16 && g_tc_gemm && ((H % 256) == 0 || unet) &&
                          (ctx->d.head_dim == 128 || ctx->d.head_dim == 64);
   auto qkv_proj = [&](int r0, int r1, const void* W, const void* bias, const void* qg, const void* kg, int buf) {
     if (r1 <= r0) return;
@@ -1639,6 +1748,80 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
     if (any_cache && late_wait) cudaStreamWaitEvent(st, ctx->ev_copy[buf], 0);
   };
 
+  // ---- UNet BasicTransformerBlock (config 5; oracle/unet.py unet_block_masked) ----
+  // x += SelfAttn(LN1 x) [masked Q x all L_img K/V: fresh rows merged with the cache by mask
+  // index]; x += CrossAttn(LN2 x, context K/V computed fresh); x += GEGLU-FF(LN3 x).
+  const int Lc = ctx->d.ctx_len, Dc = ctx->d.ctx_dim;
+  auto ln_aff = [&](int b, int which) {  // LayerNorm affine as LN-modulation with (beta, gamma - 1)
+    ProfScope ps(ctx, st, IG_K_LNMOD, 0.0, (double)M * H * (4 + es));
+    launch_ln_mod<T>(ctx->X, H, 0, M, ctx->ri, ctx->unet_ln + ((size_t)b * 3 + which) * 2 * H, 0, 0, H,
+                     ctx->d.ln_eps, h, H, st);
+    stats.kernel_launches++;
+  };
+  auto cross_kv = [&](const UnetW& u) {  // context rows -> K/V planes of the cross arena
+    const int Mc = na * Lc;
+    if (fused_qkv) {
+      GemmArgs g{};
+      g.A = ctx->ctxp; g.lda = Dc; g.B = u.kv2.w; g.ldb = Dc; g.bias = nullptr;
+      g.C = ctx->Q; g.ldc = H; g.M = Mc; g.N = 2 * H; g.K = Dc; g.epi = EPI_QKV;
+      g.ri = ctx->ri_c; g.ri_off = 0;
+      QkvEpi& e = g.qkv;
+      e.Q = ctx->Q; e.kv_arena = ctx->xkv; e.slot_stride = 2LL * Lc * H; e.buf_off = 0; e.L = Lc; e.H = H;
+      e.head_dim = ctx->d.head_dim; e.col_base = H;
+      gemm(ctx, g, st);
+    } else {  // parity mode: K/V GEMM into the [q|k|v] scratch, then the positional write
+      GemmArgs g{};
+      g.A = ctx->ctxp; g.lda = Dc; g.B = u.kv2.w; g.ldb = Dc;
+      g.C = (char*)qkv + (long long)H * es; g.ldc = 3 * H; g.M = Mc; g.N = 2 * H; g.K = Dc; g.epi = EPI_STORE;
+      gemm(ctx, g, st);
+      QkvPost p{};
+      p.qkv = qkv; p.ld_qkv = 3 * H; p.Q = ctx->Q; p.kv_arena = ctx->xkv;
+      p.slot_stride = 2LL * Lc * H; p.buf_off = 0; p.L = Lc; p.H = H;
+      p.heads = ctx->d.heads; p.head_dim = ctx->d.head_dim; p.r0 = 0; p.r1 = Mc;
+      ProfScope ps(ctx, st, IG_K_QKVPOST, 0.0, (double)Mc * 6.0 * H * es);
+      launch_qkv_post<T>(p, ctx->ri_c, st);
+      stats.kernel_launches++;
+    }
+  };
+  auto unet_block = [&](int b, int buf) {
+    const UnetW& u = ctx->unet[b];
+    cross_kv(u);  // first: the parity path's positional write also stores (unused) Q rows
+    ln_aff(b, 0);
+    wait_copy(buf);
+    qkv_proj(0, M, u.qkv, nullptr, nullptr, nullptr, buf);
+    wait_copy_late(buf);
+    attn(buf, false);
+    record_kv(b, buf);
+    cudaEventRecord(ctx->ev_comp[buf], st);
+    if (ctx->capturing) ctx->cap_mask |= 1u << buf;
+    if (b + R < b1) issue_copy(ctx, sr, dkvg, dkvq, b + R, plan);
+    gemm_rows(0, M, cat, ldcat, u.out1.w, u.out1.b, H, H, ctx->X, H, EPI_GATED_RES, ctx->ones, 0);
+    ln_aff(b, 1);
+    gemm_rows(0, M, h, H, u.q2.w, nullptr, H, H, ctx->Q, H, EPI_STORE, nullptr, 0);
+    {
+      AttnArgs a{};
+      a.Q = ctx->Q; a.ldq = H; a.O = cat; a.ldo = ldcat; a.kv_arena = ctx->xkv; a.kv_off = 0;
+      a.segs = dsegf; a.nseg = nsegf; a.max_qlen = max_qf; a.n_pairs = npairf; a.q_rows = M;
+      a.L = Lc; a.heads = ctx->d.heads; a.head_dim = ctx->d.head_dim;
+      a.scale = 1.0f / sqrtf((float)ctx->d.head_dim);
+      attention(ctx, a, st, 4.0 * (double)M * Lc * H);
+    }
+    gemm_rows(0, M, cat, ldcat, u.out2.w, u.out2.b, H, H, ctx->X, H, EPI_GATED_RES, ctx->ones, 0);
+    ln_aff(b, 2);
+    GemmArgs gg{};  // fused: GEGLU in the tcgen05 epilogue (tile-interleaved weight copy)
+    gg.A = h; gg.lda = H; gg.B = u.geglu_w_tc; gg.ldb = H; gg.bias = u.geglu_b_tc;
+    gg.C = cat + H; gg.ldc = ldcat; gg.M = M; gg.N = 2 * F; gg.K = H; gg.epi = EPI_GEGLU;
+    if (u.geglu_w_tc && g_tc_gemm && gemm_tc_supported(gg)) {
+      gemm(ctx, gg, st);
+    } else {
+      gemm_rows(0, M, h, H, u.geglu.w, u.geglu.b, 2 * F, H, ctx->u2, 2 * F, EPI_STORE, nullptr, 0);
+      ProfScope ps(ctx, st, IG_K_LNMOD, 0.0, (double)M * 3 * F * es);
+      launch_geglu<T>((const T*)ctx->u2, 2 * F, M, F, cat + H, ldcat, st);
+      stats.kernel_launches++;
+    }
+    gemm_rows(0, M, cat + H, ldcat, u.ff2.w, u.ff2.b, H, F, ctx->X, H, EPI_GATED_RES, ctx->ones, 0);
+  };
+
   // ---- blocks ----
   // Dense-prefix blocks (b < kplan) run every row [0, M_full) with their own K/V buffer (index
   // R, no cache); cached blocks run the masked rows [0, M) with ring buffer b % R.
@@ -1648,7 +1831,9 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
     const int Mk = dense ? M_full : M + uy[b];  // rows through LN-mod and the K/V projection
     const int buf = dense ? R : b % R;
     const bool ys = !dense && y_staged(b);
-    if (b < ctx->d.n_double) {
+    if (unet) {
+      unet_block(b, buf);
+    } else if (b < ctx->d.n_double) {
       const StreamW& wi = ctx->dimg[b];
       const StreamW& wt = ctx->dtxt[b];
       ln_mod(M_txt, ys ? M : Mk, wi.mod_t, 0, 1);
@@ -1701,7 +1886,11 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
     }
     record_y(b);
   }
-  if (rng.X_out) {
+  if (unet) {  // exit: the stack's output rows back into the level's hidden state
+    ProfScope ps(ctx, st, IG_K_ROWS, 0.0, 2.0 * M * H * 4);
+    launch_scatter_rows(dreq, M, ctx->ri, H, ctx->X, st);
+    stats.kernel_launches++;
+  } else if (rng.X_out) {
     CUDA_TRY(cudaMemcpyAsync(rng.X_out, ctx->X, (size_t)M * H * 4, cudaMemcpyDeviceToDevice, st));
   } else {
     // ---- a11: final layer + Euler scatter ----
@@ -1782,7 +1971,7 @@ extern "C" ig_status ig_edit_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, v
 extern "C" ig_status ig_cache_template(ig_ctx* ctx, float* latent, const void* txt, const float* cond_vec,
                                        const float* sigmas, int n_steps, int tier, void* stream,
                                        ig_cache** out) {
-  if (!ctx || !latent || !cond_vec || !sigmas || !out || (ctx->Lt > 0 && !txt))
+  if (!ctx || !latent || (!cond_vec && ctx->d.n_unet == 0) || !sigmas || !out || ((ctx->Lt > 0 || ctx->d.n_unet > 0) && !txt))
     return set_err(IG_EINVAL, "NULL argument");
   *out = nullptr;
   if (n_steps <= 0) return set_err(IG_EINVAL, "n_steps must be positive");

@@ -69,6 +69,32 @@ __device__ __forceinline__ void tile_coords(int t, int num_m, int num_n, int G, 
   nb = local / gm;
 }
 
+// EPI_GEGLU: 32 hidden columns (ra) and their 32 gate columns (rg, 128 columns later in the
+// interleaved tile) -> 32 outputs at column n0/2 + c: (a + b_a) * gelu_erf(g + b_g)
+__device__ __forceinline__ void epilogue_geglu(const GemmArgs& g, int row, int ocol, const uint32_t (&ra)[32],
+                                               const uint32_t (&rg)[32], const bf16* ba, const bf16* bg) {
+  bf16* c = reinterpret_cast<bf16*>(g.C) + (long long)row * g.ldc + ocol;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    uint4 u;
+    uint32_t* w = reinterpret_cast<uint32_t*>(&u);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      float y[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int i = q * 8 + 2 * e + h;
+        float a = __uint_as_float(ra[i]), gt = __uint_as_float(rg[i]);
+        if (ba) { a += __bfloat162float(ba[i]); gt += __bfloat162float(bg[i]); }
+        y[h] = a * (0.5f * gt * (1.f + erff(gt * 0.70710678118654752f)));
+      }
+      __nv_bfloat162 p = __floats2bfloat162_rn(y[0], y[1]);
+      w[e] = *reinterpret_cast<uint32_t*>(&p);
+    }
+    reinterpret_cast<uint4*>(c)[q] = u;
+  }
+}
+
 // epilogue for one 32-column chunk of one row held in registers
 template <int BN>
 // bchunk: this chunk's 32 bias values (global memory, or the tile's bias slice staged in shared
@@ -377,6 +403,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             if (row < g.M && n0 + c < g.N) epilogue_qkv_head<64>(g, row, n0 + c, v, info, BIAS_AT(c));
           }
         }
+      } else if (BN == 256 && g.epi == EPI_GEGLU) {
+#pragma unroll 1
+        for (int c = 0; c < 128; c += 32) {
+          uint32_t ra[32], rg[32];
+          tc::tmem_ld32(tbase + c, ra);
+          tc::tmem_ld32(tbase + 128 + c, rg);
+          tc::tmem_ld_wait();
+          if (row < g.M && n0 + c < g.N) epilogue_geglu(g, row, n0 / 2 + c, ra, rg, BIAS_AT(c), BIAS_AT(128 + c));
+        }
       } else {
 #pragma unroll 1
         for (int c = 0; c < BN; c += 32) {
@@ -546,6 +581,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
             if (row < g.M && n0 + c < g.N) epilogue_qkv_head<64>(g, row, n0 + c, v, info, BIAS_AT(c));
           }
         }
+      } else if (g.epi == EPI_GEGLU) {
+#pragma unroll 1
+        for (int c = 0; c < 128; c += 32) {
+          uint32_t ra[32], rg[32];
+          tc::tmem_ld32(tbase + c, ra);
+          tc::tmem_ld32(tbase + 128 + c, rg);
+          tc::tmem_ld_wait();
+          if (row < g.M && n0 + c < g.N) epilogue_geglu(g, row, n0 / 2 + c, ra, rg, BIAS_AT(c), BIAS_AT(128 + c));
+        }
       } else {
 #pragma unroll 1
         for (int c = 0; c < BN; c += 32) {
@@ -645,14 +689,16 @@ int raster_group(int num_m, int rows, int K) {
 bool gemm_tc_supported(const GemmArgs& g) {
   auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
   if (!al16(g.A) || !al16(g.B) || (g.lda & 7) || (g.ldb & 7) || (g.K & 7)) return false;
-  if (g.epi == EPI_STORE || g.epi == EPI_GELU) {
+  if (g.epi == EPI_GEGLU) {
+    if (!al16(g.C) || (g.ldc & 7) || g.out_f32 || (g.N % 256)) return false;
+  } else if (g.epi == EPI_STORE || g.epi == EPI_GELU) {
     if (!al16(g.C) || (g.ldc & (g.out_f32 ? 3 : 7))) return false;
   } else if (g.epi != EPI_QKV) {
     if (!al16(g.C) || (g.ldc & 3)) return false;
     if (g.epi == EPI_GATED_RES && (!al16(g.gate) || (g.gate_ld & 3))) return false;
   }
   if (g.bias && !al16(g.bias)) return false;
-  if (g.epi == EPI_QKV && ((g.qkv.head_dim != 128 && g.qkv.head_dim != 64) || (g.qkv.H % 256) || g.N + g.qkv.col_base != 3 * g.qkv.H))
+  if (g.epi == EPI_QKV && ((g.qkv.head_dim != 128 && g.qkv.head_dim != 64) || (g.qkv.H % 64) || g.N + g.qkv.col_base != 3 * g.qkv.H))
     return false;
   return true;
 }
@@ -662,7 +708,7 @@ void gemm_tc_init() { init_driver(); }
 void launch_gemm_tc(const GemmArgs& g, cudaStream_t st) {
   if (g.M <= 0 || g.N <= 0) return;
   init_driver();
-  const bool wide = g.N > 128 || g.epi == EPI_QKV;
+  const bool wide = g.N > 128 || g.epi == EPI_QKV || g.epi == EPI_GEGLU;
   if (wide && g_two_cta && g.M > 128) {  // 2-CTA 256 x 256 tiles
     CUtensorMap ta, tb;
     make_tmap(&ta, g.A, g.M, g.K, g.lda, 128);

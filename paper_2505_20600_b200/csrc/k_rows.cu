@@ -83,7 +83,7 @@ void launch_mask_index(const uint8_t* mask, int L, int32_t* idx_m, int32_t* idx_
 template <typename T>
 __global__ void build_rows_kernel(const ReqDev* __restrict__ reqs, int n, int L_txt, int C,
                                   int H, int M_txt, int M, RowInfo* __restrict__ ri,
-                                  float* __restrict__ X, T* __restrict__ Ain, int M_full) {
+                                  float* __restrict__ X, T* __restrict__ Ain, int M_full, int img_to_x) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (warp >= M_full) return;
@@ -115,23 +115,28 @@ __global__ void build_rows_kernel(const ReqDev* __restrict__ reqs, int n, int L_
     const int tok = R.idx_m[j];
     info.req = q; info.slot = R.slot; info.kvpos = L_txt + tok; info.tok = tok;
     const float* src = R.latent + (long long)tok * C;
-    T* dst = Ain + (long long)(r - M_txt) * C;
-    for (int c = lane; c < C; c += 32) dst[c] = from_f<T>(src[c]);
+    if (img_to_x) {
+      float* dst = X + (long long)r * H;
+      for (int c = lane; c < C; c += 32) dst[c] = src[c];
+    } else {
+      T* dst = Ain + (long long)(r - M_txt) * C;
+      for (int c = lane; c < C; c += 32) dst[c] = from_f<T>(src[c]);
+    }
   }
   if (lane == 0) ri[r] = info;
 }
 
 template <typename T>
 void launch_build_rows(const ReqDev* reqs, int n, int L_txt, int C, int H, int M_txt, int M,
-                       RowInfo* ri, float* X, T* Ain, cudaStream_t st, int M_full) {
+                       RowInfo* ri, float* X, T* Ain, cudaStream_t st, int M_full, int img_to_x) {
   if (M_full < M) M_full = M;
   if (M_full <= 0) return;
   const int threads = 256;
   const int blocks = (M_full * 32 + threads - 1) / threads;
-  build_rows_kernel<T><<<blocks, threads, 0, st>>>(reqs, n, L_txt, C, H, M_txt, M, ri, X, Ain, M_full);
+  build_rows_kernel<T><<<blocks, threads, 0, st>>>(reqs, n, L_txt, C, H, M_txt, M, ri, X, Ain, M_full, img_to_x);
 }
-template void launch_build_rows<float>(const ReqDev*, int, int, int, int, int, int, RowInfo*, float*, float*, cudaStream_t, int);
-template void launch_build_rows<bf16>(const ReqDev*, int, int, int, int, int, int, RowInfo*, float*, bf16*, cudaStream_t, int);
+template void launch_build_rows<float>(const ReqDev*, int, int, int, int, int, int, RowInfo*, float*, float*, cudaStream_t, int, int);
+template void launch_build_rows<bf16>(const ReqDev*, int, int, int, int, int, int, RowInfo*, float*, bf16*, cudaStream_t, int, int);
 
 // ======================================================================================
 // a6 epilogue: per-head RMSNorm (q, k) + RoPE at the ORIGINAL token position (C-AMB 7),
@@ -431,6 +436,72 @@ void launch_scatter_euler(const ReqDev* reqs, int n, int M_img, const RowInfo* r
   const long long total = (long long)M_img * C;
   if (total <= 0) return;
   scatter_euler_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(reqs, M_img, ri, M_txt, C, v);
+}
+
+// ======================================================================================
+// UNet attention stack (config 5): exit scatter, context pack, unfused GEGLU, GEGLU weight
+// interleave.  All HBM-bound copies; float4 where the widths allow (H, Dc, F multiples of 64).
+// ======================================================================================
+__global__ void scatter_rows_kernel(const ReqDev* __restrict__ reqs, int M, const RowInfo* __restrict__ ri, int H,
+                                    const float* __restrict__ X) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (warp >= M) return;
+  const RowInfo info = ri[warp];
+  float4* dst = reinterpret_cast<float4*>(reqs[info.req].latent + (long long)info.tok * H);
+  const float4* src = reinterpret_cast<const float4*>(X + (long long)warp * H);
+  for (int c = lane; c < H / 4; c += 32) dst[c] = src[c];
+}
+
+void launch_scatter_rows(const ReqDev* reqs, int M, const RowInfo* ri, int H, const float* X, cudaStream_t st) {
+  if (M <= 0) return;
+  scatter_rows_kernel<<<(M * 32 + 255) / 256, 256, 0, st>>>(reqs, M, ri, H, X);
+}
+
+template <typename T>
+__global__ void pack_ctx_kernel(const ReqDev* __restrict__ reqs, int Lc, int Dc, T* __restrict__ dst) {
+  const int q = blockIdx.y, j = blockIdx.x;
+  const T* src = reinterpret_cast<const T*>(reqs[q].txt) + (long long)j * Dc;
+  T* d = dst + ((long long)q * Lc + j) * Dc;
+  for (int c = threadIdx.x; c < Dc; c += blockDim.x) d[c] = src[c];
+}
+
+template <typename T>
+void launch_pack_ctx(const ReqDev* reqs, int n, int Lc, int Dc, T* dst, cudaStream_t st) {
+  if (n <= 0 || Lc <= 0) return;
+  pack_ctx_kernel<T><<<dim3(Lc, n), 256, 0, st>>>(reqs, Lc, Dc, dst);
+}
+template void launch_pack_ctx<float>(const ReqDev*, int, int, int, float*, cudaStream_t);
+template void launch_pack_ctx<bf16>(const ReqDev*, int, int, int, bf16*, cudaStream_t);
+
+template <typename T>
+__global__ void geglu_kernel(const T* __restrict__ u, long long ldu, int F, T* __restrict__ out, long long ldo) {
+  const int r = blockIdx.y;
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= F) return;
+  const float a = to_f<T>(u[(long long)r * ldu + j]);
+  const float g = to_f<T>(u[(long long)r * ldu + F + j]);
+  out[(long long)r * ldo + j] = from_f<T>(a * (0.5f * g * (1.f + erff(g * 0.70710678118654752f))));
+}
+
+template <typename T>
+void launch_geglu(const T* u, long long ldu, int M, int F, T* out, long long ldo, cudaStream_t st) {
+  if (M <= 0) return;
+  geglu_kernel<T><<<dim3((F + 255) / 256, M), 256, 0, st>>>(u, ldu, F, out, ldo);
+}
+template void launch_geglu<float>(const float*, long long, int, int, float*, long long, cudaStream_t);
+template void launch_geglu<bf16>(const bf16*, long long, int, int, bf16*, long long, cudaStream_t);
+
+__global__ void permute_geglu_kernel(const bf16* __restrict__ src, bf16* __restrict__ dst, int F, int K) {
+  const int r = blockIdx.x;  // destination row
+  const int t = r >> 8, i = r & 255;
+  const int s = i < 128 ? 128 * t + i : F + 128 * t + (i - 128);
+  const bf16* a = src + (long long)s * K;
+  bf16* b = dst + (long long)r * K;
+  for (int c = threadIdx.x; c < K; c += blockDim.x) b[c] = a[c];
+}
+
+void launch_permute_geglu_rows(const bf16* src, bf16* dst, int F, int K, cudaStream_t st) {
+  permute_geglu_kernel<<<2 * F, 256, 0, st>>>(src, dst, F, K);
 }
 
 }  // namespace ig

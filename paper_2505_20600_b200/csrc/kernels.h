@@ -29,9 +29,23 @@ struct ReqDev {
 // rows at idx_m (as T).  M_txt = n * L_txt.
 // Rows [M, M_full) are the included unmasked image rows (dense prefix): latent rows of the
 // template's input latent at idx_u.
+// img_to_x (UNet models, C == H): the masked image rows are copied into X (fp32, exact)
+// instead of Ain.
 template <typename T>
 void launch_build_rows(const ReqDev* reqs, int n, int L_txt, int C, int H, int M_txt, int M,
-                       RowInfo* row_info, float* X, T* Ain, cudaStream_t st, int M_full = -1);
+                       RowInfo* row_info, float* X, T* Ain, cudaStream_t st, int M_full = -1,
+                       int img_to_x = 0);
+// UNet exit: latent_req[idx_m[j]][:] = X[img_row][:] (fp32 copy of the stack's output rows)
+void launch_scatter_rows(const ReqDev* reqs, int M, const RowInfo* ri, int H, const float* X, cudaStream_t st);
+// UNet cross-attention context: dst[q * Lc + j][:] = reqs[q].txt[j][:] (T, width Dc)
+template <typename T>
+void launch_pack_ctx(const ReqDev* reqs, int n, int Lc, int Dc, T* dst, cudaStream_t st);
+// GEGLU on an unfused projection u [M, 2F] (ld ldu): out[r][j] = u[r][j] * gelu_erf(u[r][F + j])
+template <typename T>
+void launch_geglu(const T* u, long long ldu, int M, int F, T* out, long long ldo, cudaStream_t st);
+// EPI_GEGLU weight layout: dst row (256 t + i) = src row (128 t + i) for i < 128 (hidden) and
+// src row (F + 128 t + i - 128) otherwise (gate); rows of K elements (bf16); F % 128 == 0
+void launch_permute_geglu_rows(const bf16* src, bf16* dst, int F, int K, cudaStream_t st);
 
 // ---- a3 conditioning (k_norm.cu) --------------------------------------------------------
 // temb[r][0:256] = [cos(1000 sigma_r f_k) | sin(...)], computed in double, stored as float.
@@ -141,6 +155,9 @@ enum Epi : int {
   EPI_GATED_RES = 2,  // X[r, c] += gate[req(r)][c] * (acc + b)  (C is fp32 X)
   EPI_POS = 3,        // X[r, c] = acc + b + pos[tok(r)][c]      (C is fp32 X)
   EPI_QKV = 4,        // q,k: per-head RMSNorm + RoPE; q -> packed Q, k,v -> positional K/V
+  EPI_GEGLU = 5,      // tcgen05 only, B/bias rows tile-interleaved (permute_geglu_rows): every
+                      // 256-column tile holds 128 hidden columns then their 128 gate columns;
+                      // C[r, n0/2 + j] = (acc_j + b_j) * gelu_erf(acc_{128+j} + b_{128+j}) (TOut)
 };
 // Extra arguments of the fused QKV epilogue (a6: norm, RoPE and the positional merge done
 // on the fp32 accumulators, one bf16 rounding per output).

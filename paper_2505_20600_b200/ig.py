@@ -44,7 +44,8 @@ class ig_model_desc(ctypes.Structure):
                 ("rope", ctypes.c_int), ("rope_axes", ctypes.c_int * 3),
                 ("rope_theta", ctypes.c_float), ("ln_eps", ctypes.c_float),
                 ("pos_embed_2d", ctypes.c_int), ("context_pre_only_last", ctypes.c_int),
-                ("dtype", ctypes.c_int)]
+                ("dtype", ctypes.c_int), ("n_unet", ctypes.c_int), ("ctx_len", ctypes.c_int),
+                ("ctx_dim", ctypes.c_int)]
 
 
 class ig_ctx_opts(ctypes.Structure):

@@ -49,7 +49,10 @@ class Request:
         d = m.d
         self.latent = synth.make_latent(d, rid, device).contiguous()
         self.latent0 = self.latent.clone()
-        self.txt = synth.make_txt(d, rid, device, TDT[m.dtype]).contiguous()
+        if d.n_unet:  # UNet: the txt slot carries the cross-attention context
+            self.txt = synth.make_ctx(d, rid, device, TDT[m.dtype]).contiguous()
+        else:
+            self.txt = synth.make_txt(d, rid, device, TDT[m.dtype]).contiguous()
         self.cond = synth.make_cond(d, rid, device).contiguous()
         self.mask_np = mask_np.astype(np.uint8)
         self.mask_dev = torch.from_numpy(self.mask_np).to(device)

@@ -38,7 +38,7 @@ def test_library_exports_every_declared_symbol():
         assert callable(getattr(ig, n))
 
 
-@pytest.mark.parametrize("name", [n for n, m in synth.MODELS.items() if not m.n_unet])
+@pytest.mark.parametrize("name", list(synth.MODELS))
 def test_weight_count_matches_table(name):
     m = synth.MODELS[name]
     assert ig.ig_weight_count(ig.make_desc(m, ig.IG_BF16)) == len(synth.weight_table(m))
@@ -56,3 +56,16 @@ def test_ctx_create_rejects_bad_desc_without_gpu():
     with pytest.raises(ig.IgError) as e:
         ig.ig_ctx_create(d, [1] * 3)
     assert e.value.name == "IG_EINVAL"
+
+
+@pytest.mark.parametrize("name", [n for n, m in synth.MODELS.items() if m.n_unet])
+def test_unet_desc_passes_host_validation(name):
+    """Every UNet shape synth describes passes the host-side checks (without a GPU the call
+    then fails at the first CUDA call, never with IG_EINVAL / IG_EUNSUPPORTED)."""
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("fake weight pointers: CPU-only check")
+    m = synth.MODELS[name]
+    with pytest.raises(ig.IgError) as e:
+        ig.ig_ctx_create(ig.make_desc(m, ig.IG_BF16), [1] * len(synth.weight_table(m)))
+    assert e.value.name not in ("IG_EINVAL", "IG_EUNSUPPORTED"), str(e.value)

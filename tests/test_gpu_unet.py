@@ -1,0 +1,174 @@
+"""GPU parity of the SDXL-UNet attention stack (BASELINE config 5) through the C ABI
+against oracle/unet.py on the same seeded inputs: C-TOL rtol 1e-4 (fp32 parity mode) and
+2e-2 (bf16); unmasked rows bit-identical."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from paper_2505_20600_b200 import ig
+from gpu_util import Model, Request, cache_to_numpy, ctol, fill_cache
+
+pytestmark = pytest.mark.gpu
+
+RTOL = {ig.IG_F32: 1e-4, ig.IG_BF16: 2e-2}
+TDT = {ig.IG_F32: torch.float32, ig.IG_BF16: torch.bfloat16}
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    ig.lib()
+
+
+def _steps(m, reqs, cache, n_steps, stream=0):
+    for s in range(n_steps):
+        rr = [r.req(i, cache, s, 0.0, 0.0) for i, r in enumerate(reqs)]
+        ig.ig_edit_step(m.ctx, rr, stream)
+    torch.cuda.synchronize()
+
+
+def _oracle_steps(d, W, r, kvh, n_steps):
+    x, ctx = r.latent0.double().cpu().numpy(), r.txt.double().cpu().numpy()
+    for s in range(n_steps):
+        x = oracle.unet_edit_step(d, W, x, r.mask_np, kvh[s], ctx)
+    return x
+
+
+@pytest.mark.parametrize("dtype", [ig.IG_F32, ig.IG_BF16])
+def test_unet_tiny_template_and_edit(dtype):
+    """Template recording (dense stack, K/V of every block and step) vs the oracle's cache and
+    trajectory; then two edit steps with a synthetic cache shared by both sides."""
+    d = synth.UNET_TINY
+    m = Model(d, dtype)
+    W = m.host_weights()
+    rq = Request(m, 0, synth.rect_mask(d, 4, 12, 4, 12))
+    x0, ctx = rq.latent0.double().cpu().numpy(), rq.txt.double().cpu().numpy()
+    st = rq.latent.clone()
+    cache = ig.ig_cache_template(m.ctx, st.data_ptr(), rq.txt.data_ptr(), 0, [1.0, 0.5, 0.0])
+    states, ocache = oracle.unet_cache_template(d, W, x0, ctx, 2)
+    ok, worst = ctol(cache_to_numpy(cache, d, 2, dtype), ocache, RTOL[dtype])
+    assert ok, ("cache", worst)
+    ok, worst = ctol(st.double().cpu().numpy(), states[-1], RTOL[dtype])
+    assert ok, ("dense trajectory", worst)
+    kv = synth.make_cache_kv(d, 0, 2, dtype=TDT[dtype])
+    syn = ig.ig_cache_create(m.ctx, 2, ig.IG_CACHE_HOST)
+    fill_cache(m, syn, kv)
+    _steps(m, [rq], syn, 2)
+    want = _oracle_steps(d, W, rq, kv.double().numpy(), 2)
+    got = rq.latent.double().cpu().numpy()
+    ok, worst = ctol(got, want, RTOL[dtype])
+    assert ok, ("edit", worst)
+    assert np.array_equal(got[rq.mask_np == 0], x0[rq.mask_np == 0])
+    ig.ig_cache_free(cache)
+    ig.ig_cache_free(syn)
+    rq.free()
+    m.close()
+
+
+@pytest.mark.parametrize("dtype", [ig.IG_F32, ig.IG_BF16])
+@pytest.mark.parametrize("copy_mode,tier", [(0, ig.IG_CACHE_HOST), (1, ig.IG_CACHE_HOST), (1, ig.IG_CACHE_DEVICE)])
+def test_unet_small_batch(dtype, copy_mode, tier):
+    """d = 64 (tcgen05 attention, fused K/V-merge epilogue, fused GEGLU epilogue in bf16): a
+    batch of 3 requests (rectangle, blob, all-ones) over 2 steps of a synthetic cache."""
+    d = synth.UNET_SMALL
+    opts = ig.ig_ctx_opts(4, 0, 2, copy_mode, 0, 0)
+    m = Model(d, dtype, opts=opts)
+    W = m.host_weights()
+    rng = np.random.default_rng(1)
+    masks = [synth.rect_mask_count(d, 40, rng), synth.blob_mask_count(d, 150, rng), np.ones(d.L_img, np.uint8)]
+    reqs = [Request(m, 20 + i, mk) for i, mk in enumerate(masks)]
+    kv = synth.make_cache_kv(d, 4, 2, dtype=TDT[dtype])
+    cache = ig.ig_cache_create(m.ctx, 2, tier)
+    fill_cache(m, cache, kv)
+    _steps(m, reqs, cache, 2)
+    kvh = kv.double().numpy()
+    for r in reqs:
+        want = _oracle_steps(d, W, r, kvh, 2)
+        got = r.latent.double().cpu().numpy()
+        ok, worst = ctol(got, want, RTOL[dtype])
+        assert ok, worst
+        assert np.array_equal(got[r.mask_np == 0], r.latent0.cpu().numpy()[r.mask_np == 0])
+    ig.ig_cache_free(cache)
+    for r in reqs:
+        r.free()
+    m.close()
+
+
+def test_unet_same_inputs_cache_matches_dense_on_gpu():
+    """bf16: a cache recorded on the GPU along the dense trajectory, then an edit step from the
+    template's own state reproduces the GPU dense step on the masked rows (same arithmetic per
+    row: K/V of the unmasked rows are the recorded ones), and is alone == in-batch bitwise."""
+    d = synth.UNET_SMALL
+    m = Model(d, ig.IG_BF16, opts=ig.ig_ctx_opts(4, 0, 2, 1, 0, 0))
+    mask = synth.blob_mask_count(d, 70, np.random.default_rng(2))
+    rq = Request(m, 5, mask)
+    st = rq.latent.clone()
+    cache = ig.ig_cache_template(m.ctx, st.data_ptr(), rq.txt.data_ptr(), 0, [1.0, 0.5])
+    _steps(m, [rq], cache, 1)
+    got = rq.latent.double().cpu().numpy()
+    dense = st.double().cpu().numpy()
+    ok, worst = ctol(got[mask != 0], dense[mask != 0], 2e-2)
+    assert ok, worst
+    # alone == together with another request (batch invariance of the fixed-tile kernels)
+    other = Request(m, 6, synth.rect_mask_count(d, 90, np.random.default_rng(3)))
+    rq2 = Request(m, 5, mask)
+    rr = [rq2.req(0, cache, 0, 0.0, 0.0), other.req(1, cache, 0, 0.0, 0.0)]
+    ig.ig_edit_step(m.ctx, rr, 0)
+    torch.cuda.synchronize()
+    assert torch.equal(rq2.latent, rq.latent)
+    ig.ig_cache_free(cache)
+    for r in (rq, rq2, other):
+        r.free()
+    m.close()
+
+
+def test_unet_cuda_graph_bitwise_equals_eager():
+    d = synth.UNET_SMALL
+    res = []
+    for graphs in (0, 1):
+        m = Model(d, ig.IG_BF16, opts=ig.ig_ctx_opts(4, 0, 2, 1, 0, 0, 0, 0, graphs))
+        rng = np.random.default_rng(4)
+        reqs = [Request(m, 30 + i, synth.blob_mask_count(d, 60 + 40 * i, rng)) for i in range(2)]
+        kv = synth.make_cache_kv(d, 5, 3, dtype=torch.bfloat16)
+        cache = ig.ig_cache_create(m.ctx, 3, ig.IG_CACHE_DEVICE)
+        fill_cache(m, cache, kv)
+        s = torch.cuda.Stream()
+        _steps(m, reqs, cache, 3, s.cuda_stream)
+        res.append([r.latent.clone() for r in reqs])
+        ig.ig_cache_free(cache)
+        for r in reqs:
+            r.free()
+        m.close()
+    for a, b in zip(*res):
+        assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("which", ["sdxl_attn64", "sdxl_attn32_2blocks"])
+def test_sdxl_level_full_width(which):
+    """Full SDXL level widths (64x64 level: all 10 blocks, C=640, 4096 tokens; 32x32 level:
+    C=1280, 1024 tokens, 2 of its 60 blocks), 77 x 2048 context, bf16, a batch of 2 requests
+    (m = 0.1 rectangle, 0.3 blob) over one step of a synthetic cache vs the oracle."""
+    d = synth.SDXL_L64 if which == "sdxl_attn64" else synth._unet("sdxl32_2", 2, 1280, 20, 32, 77, 2048)
+    m = Model(d, ig.IG_BF16, opts=ig.ig_ctx_opts(2, 0, 2, 1, 0, 0))
+    W = m.host_weights()
+    rng = np.random.default_rng(6)
+    masks = [synth.rect_mask_count(d, round(0.1 * d.L_img), rng), synth.blob_mask_count(d, round(0.3 * d.L_img), rng)]
+    reqs = [Request(m, 40 + i, mk) for i, mk in enumerate(masks)]
+    kv = synth.make_cache_kv(d, 6, 1, dtype=torch.bfloat16)
+    cache = ig.ig_cache_create(m.ctx, 1, ig.IG_CACHE_HOST)
+    fill_cache(m, cache, kv)
+    _steps(m, reqs, cache, 1)
+    kvh = kv.double().numpy()
+    for r in reqs:
+        want = _oracle_steps(d, W, r, kvh, 1)
+        got = r.latent.double().cpu().numpy()
+        ok, worst = ctol(got[r.mask_np != 0], want[r.mask_np != 0], 2e-2)
+        assert ok, worst
+        assert np.array_equal(got[r.mask_np == 0], r.latent0.cpu().numpy()[r.mask_np == 0])
+    ig.ig_cache_free(cache)
+    for r in reqs:
+        r.free()
+    m.close()

@@ -219,3 +219,14 @@ def test_macs_per_row_counts_the_block():
     cross = D.n_unet * D.ctx_len * 2 * D.hidden * D.ctx_dim   # the context's K/V, per request
     assert oracle.MACS["linear"] == 40 * D.n_unet * per["linear"] + cross
     assert oracle.MACS["attn"] == 40 * D.n_unet * per["attn"]
+
+
+def test_levels_any_pool2_matches_oracle():
+    """The product's host-side level-mask reduction equals the oracle's loop definition."""
+    from paper_2505_20600_b200 import levels
+    rng = np.random.default_rng(9)
+    for n in (0, 1, 37, 900, 4096):
+        m = synth.blob_mask_count(synth.SDXL_L64, n, rng)
+        assert np.array_equal(levels.any_pool2(m, 64, 64), oracle.any_pool2(m, 64, 64))
+    with pytest.raises(ValueError):
+        levels.any_pool2(np.zeros(15, np.uint8), 3, 5)
