@@ -210,6 +210,10 @@ struct ig_ctx {
   std::unordered_map<std::string, GraphEnt> graphs;
   bool capturing = false;
   unsigned cap_mask = 0;  // ring buffers whose ev_comp was recorded inside the capture
+  // a graph ran last: the ring events' latest records are capture nodes (not waitable
+  // eagerly), so the next eager step first re-records them after the graph on its stream
+  bool graph_tail = false;
+  cudaStream_t graph_st = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   // Algorithm-1 block plan (ig_set_plan): 0 off, 1 forced dense-prefix length, 2 model
   int plan_mode = 0, plan_k = 0, last_plan_k = 0;
@@ -1220,6 +1224,18 @@ extern "C" int ig_last_plan(const ig_ctx* ctx) { return ctx ? ctx->last_plan_k :
 
 // Optional restriction of a step to blocks [b0, b1) on caller-given residual rows (the
 // teacher-forced debug hook); defaults run the whole step.
+// Eager work after a graph launch: the ring events' latest records were capture nodes, which
+// cannot be waited on eagerly; record them again behind the graph on its stream.
+static void flush_graph_tail(ig_ctx* ctx) {
+  if (!ctx->graph_tail) return;
+  for (int i = 0; i < ctx->R; ++i) {
+    cudaEventRecord(ctx->ev_comp[i], ctx->graph_st);
+    cudaEventRecord(ctx->ev_copy[i], ctx->graph_st);
+    cudaEventRecord(ctx->ev_yrec[i], ctx->graph_st);
+  }
+  ctx->graph_tail = false;
+}
+
 struct StepRange {
   int b0 = 0, b1 = -1;
   const float* X_in = nullptr;
@@ -1501,6 +1517,8 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
     if (it != ctx->graphs.end()) {  // replay: the graph pulls this step's descriptors itself
       for (auto& s2 : sr) if (s2.use_cache) s2.r->cache->pins.fetch_add(1);
       CUDA_TRY(cudaGraphLaunch(it->second.exec, st));
+      ctx->graph_tail = true;
+      ctx->graph_st = st;
       ctx->stats = it->second.stats;
       CUDA_TRY(cudaEventRecord(ctx->ev_stage[si], st));
       for (auto& s2 : sr)
@@ -1514,6 +1532,7 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
     ctx->capturing = true;
     ctx->cap_mask = 0;
   }
+  if (!ctx->capturing) flush_graph_tail(ctx);  // eager step after a graph
   launch_copy_bytes(ds, ctx->m_stage[si], desc_bytes, st);
   if (plan.gather || plan.gather_q8) {
     const size_t off = (char*)hkvg - hs, bytes = (char*)(hkvq + (size_t)nb * na) - (char*)hkvg;
@@ -1916,6 +1935,8 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
     }
     ctx->graphs[gkey] = ig_ctx::GraphEnt{exec, stats};
     CUDA_TRY(cudaGraphLaunch(exec, st));
+    ctx->graph_tail = true;
+    ctx->graph_st = st;
   }
   // the copy lane must not run ahead into the next step's buffers before compute is done
   CUDA_TRY(cudaEventRecord(ctx->ev_stage[si], st));
@@ -2019,6 +2040,7 @@ extern "C" ig_status ig_prefetch_layer(ig_ctx* ctx, const ig_edit_req* r, int la
   const int buf = layer % ctx->R;
   const size_t es = ctx->esz, H = ctx->H;
   const size_t plane = (size_t)ctx->Limg * H * es;
+  flush_graph_tail(ctx);
   CUDA_TRY(cudaStreamWaitEvent(ctx->copy_st, ctx->ev_comp[buf], 0));
   const char* src = cache_plane(ctx, r->cache, r->step, layer, 0);
   char* dst = (char*)ctx->kv_arena + ((size_t)r->slot * ctx->slot_stride + (size_t)buf * ctx->buf_elems) * es;

@@ -136,7 +136,14 @@ def test_unet_cuda_graph_bitwise_equals_eager():
         cache = ig.ig_cache_create(m.ctx, 3, ig.IG_CACHE_DEVICE)
         fill_cache(m, cache, kv)
         s = torch.cuda.Stream()
-        _steps(m, reqs, cache, 3, s.cuda_stream)
+        _steps(m, reqs, cache, 2, s.cuda_stream)
+        # a third step eagerly (profiling forces eager launches) after the graph replays:
+        # the ring events recorded inside captures must not be waited on
+        ig.ig_profile_enable(m.ctx, 1)
+        ig.ig_edit_step(m.ctx, [r.req(i, cache, 2, 0.0, 0.0) for i, r in enumerate(reqs)], s.cuda_stream)
+        torch.cuda.synchronize()
+        ig.ig_profile_read(m.ctx)
+        ig.ig_profile_enable(m.ctx, 0)
         res.append([r.latent.clone() for r in reqs])
         ig.ig_cache_free(cache)
         for r in reqs:
