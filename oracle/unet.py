@@ -15,6 +15,9 @@ What it computes, and where the paper says so
   them depends on the image tokens).                              unet_block_masked
 * The dense block (fig:transformer-Top) with K/V recording = the template
   cache (P:157).                                                   unet_dense_step(record=)
+* Y-caching variant and hybrid per-block choice (fig:transformer-Bottom, P:423-426): Y_{b-1}
+  of the unmasked tokens replenishes their block input, which only feeds K/V.
+                                                    unet_kv_from_y, unet_edit_step_y
 * Per-level masks: a 2x2 any-pool of the finer level's token mask (C-AMB 13, SURVEY
   §8(d) config 5).                                                                any_pool2
 * One synthetic step applies the level's stack to its hidden state and feeds the output
@@ -109,30 +112,71 @@ def unet_edit_step(d, W, state: np.ndarray, mask, kv_cache_step: Optional[np.nda
     return out
 
 
-def unet_dense_step(d, W, state: np.ndarray, ctx: np.ndarray, record: bool = False):
+def unet_dense_step(d, W, state: np.ndarray, ctx: np.ndarray, record: bool = False, record_y: bool = False):
     """Dense step (all L_img tokens, no cache); record=True also returns the K/V of every
-    block [n_blocks][2][L_img][H] (the template cache of this step)."""
+    block [n_blocks][2][L_img][H] (the template cache of this step), record_y=True also the
+    block outputs Y [n_blocks][L_img][H] (the Y variant's cache, fig:transformer-Bottom)."""
     all_idx = np.arange(d.L_img)
     none = np.zeros(0, dtype=np.int64)
     x = np.array(state, dtype=np.float64, copy=True)
     kv = np.zeros((d.n_unet, 2, d.L_img, d.hidden)) if record else None
+    y = np.zeros((d.n_unet, d.L_img, d.hidden)) if record_y else None
     for b in range(d.n_unet):
         x, k, v = unet_block_masked(d, W, b, x, all_idx, none, None, ctx)
         if record:
             kv[b, 0], kv[b, 1] = k, v
-    return (x, kv) if record else x
+        if record_y:
+            y[b] = x
+    out = (x,) + ((kv,) if record else ()) + ((y,) if record_y else ())
+    return out if len(out) > 1 else x
 
 
-def unet_cache_template(d, W, state0: np.ndarray, ctx: np.ndarray, n_steps: int):
+def unet_cache_template(d, W, state0: np.ndarray, ctx: np.ndarray, n_steps: int, record_y: bool = False):
     """Template pass: n_steps dense steps from state0; returns (inputs [n_steps+1][L_img][H],
-    K/V cache [n_steps][n_blocks][2][L_img][H])."""
+    K/V cache [n_steps][n_blocks][2][L_img][H]) (+ Y cache [n_steps][n_blocks][L_img][H])."""
     states = [np.array(state0, np.float64)]
-    cache = []
+    cache, ys = [], []
     for _ in range(n_steps):
-        x, kv = unet_dense_step(d, W, states[-1], ctx, record=True)
-        states.append(x)
-        cache.append(kv)
-    return np.stack(states), np.stack(cache)
+        r = unet_dense_step(d, W, states[-1], ctx, record=True, record_y=True)
+        states.append(r[0])
+        cache.append(r[1])
+        ys.append(r[2])
+    return (np.stack(states), np.stack(cache)) + ((np.stack(ys),) if record_y else ())
+
+
+def unet_kv_from_y(d, W, b: int, u: np.ndarray) -> Tuple[np.ndarray, np.ndarray]:
+    """Y variant: K/V of unmasked rows from their block input u (LN1 + the K/V projections,
+    P:423-426 "replenishing cached activations for the unmasked tokens")."""
+    H, p = d.hidden, f"unet.{b}"
+    h = layernorm_affine(np.asarray(u, np.float64), _w(W, p + ".ln1.g"), _w(W, p + ".ln1.b"), d.ln_eps)
+    kv = linear(h, _w(W, p + ".attn1.qkv.w")[H:], None)
+    return kv[:, :H], kv[:, H:]
+
+
+def unet_edit_step_y(d, W, state: np.ndarray, mask, y_cache_step: np.ndarray, tstate: np.ndarray,
+                     ctx: np.ndarray, y_blocks=None, kv_cache_step: Optional[np.ndarray] = None) -> np.ndarray:
+    """Y-variant (and hybrid) mask-aware step of the level's stack.  For a Y block b the
+    unmasked tokens' block input is the template's Y_{b-1} (block 0: the template's input
+    state tstate of this step); it only feeds their K/V (unet_kv_from_y).  Blocks outside
+    y_blocks (default: all are Y blocks) read K/V from kv_cache_step.  Unmasked rows of the
+    result are untouched."""
+    idx_m, idx_u, n_m = index_build(mask)
+    out = np.array(state, dtype=np.float64, copy=True)
+    if n_m == 0:
+        return out
+    yb = set(range(d.n_unet)) if y_blocks is None else set(y_blocks)
+    x = out[idx_m]
+    for b in range(d.n_unet):
+        if b in yb:
+            u = (np.asarray(tstate, np.float64) if b == 0 else np.asarray(y_cache_step[b - 1], np.float64))[idx_u]
+            ku, vu = unet_kv_from_y(d, W, b, u)
+            blk = np.zeros((2, d.L_img, d.hidden))
+            blk[0][idx_u], blk[1][idx_u] = ku, vu
+        else:
+            blk = kv_cache_step[b]
+        x, _, _ = unet_block_masked(d, W, b, x, idx_m, idx_u, blk, ctx)
+    out[idx_m] = x
+    return out
 
 
 def any_pool2(mask, grid_h: int, grid_w: int) -> np.ndarray:

@@ -230,3 +230,31 @@ def test_levels_any_pool2_matches_oracle():
         assert np.array_equal(levels.any_pool2(m, 64, 64), oracle.any_pool2(m, 64, 64))
     with pytest.raises(ValueError):
         levels.any_pool2(np.zeros(15, np.uint8), 3, 5)
+
+
+def test_y_variant_pins():
+    """Y variant: (1) with a Y cache recorded along the dense trajectory from the same state,
+    the Y step equals the dense step on the masked rows (exactly: the recomputed K/V of the
+    unmasked rows are the dense ones); (2) K/V recomputed from the recorded Y_{b-1} equal the
+    recorded K/V of block b; (3) no Y blocks == the K/V step; (4) a hybrid split equals the
+    dense step too, and the Y cache is really read (other Y rows change the result)."""
+    W = _weights()
+    ctx = _ctx()
+    states, kv, ys = oracle.unet_cache_template(D, W, _state(), ctx, 2, record_y=True)
+    mask = synth.blob_mask_count(D, 80, np.random.default_rng(8))
+    m = mask != 0
+    for s in range(2):
+        out = oracle.unet_edit_step_y(D, W, states[s], mask, ys[s], states[s], ctx)
+        np.testing.assert_allclose(out[m], states[s + 1][m], rtol=1e-12, atol=1e-12)
+        assert np.array_equal(out[~m], states[s][~m])
+        hyb = oracle.unet_edit_step_y(D, W, states[s], mask, ys[s], states[s], ctx, y_blocks=[1], kv_cache_step=kv[s])
+        np.testing.assert_allclose(hyb[m], states[s + 1][m], rtol=1e-12, atol=1e-12)
+    k1, v1 = oracle.unet_kv_from_y(D, W, 1, ys[0][0])
+    np.testing.assert_allclose(k1, kv[0][1][0], rtol=1e-12, atol=1e-12)
+    np.testing.assert_allclose(v1, kv[0][1][1], rtol=1e-12, atol=1e-12)
+    junk = synth.make_cache_kv(D, 4, 1).double().numpy()[0]
+    np.testing.assert_array_equal(oracle.unet_edit_step_y(D, W, states[0], mask, ys[0], states[0], ctx, y_blocks=[],
+                                                          kv_cache_step=junk),
+                                  oracle.unet_edit_step(D, W, states[0], mask, junk, ctx))
+    other = oracle.unet_edit_step_y(D, W, states[0], mask, ys[1], states[0], ctx)
+    assert not np.allclose(other[m], states[1][m])
