@@ -409,7 +409,6 @@ extern "C" ig_status ig_ctx_create(const ig_model_desc* desc, const void* const*
   const int Lall = desc->txt_len + desc->grid_h * desc->grid_w;
   if (o.max_rows <= 0) o.max_rows = o.max_batch * Lall;
   if (desc->n_unet > 0) {
-    if (o.cache_y) return set_err(IG_EUNSUPPORTED, "UNet models: K/V caches only (cache_y)");
     o.max_rows = std::max(o.max_rows, o.max_batch * desc->ctx_len);  // the context rows' K/V projection
   }
 
@@ -1674,7 +1673,7 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
     }
     GemmArgs g{};
     g.A = (const char*)h + (long long)r0 * H * es; g.lda = H;
-    g.B = (const char*)W + (long long)H * H * es; g.ldb = H; g.bias = (const char*)bias + (long long)H * es;
+    g.B = (const char*)W + (long long)H * H * es; g.ldb = H; g.bias = bias ? (const char*)bias + (long long)H * es : nullptr;
     g.C = ctx->Q; g.ldc = H;
     g.M = r1 - r0; g.N = 2 * H; g.K = H; g.epi = EPI_QKV;
     g.ri = ctx->ri; g.ri_off = r0;
@@ -1771,10 +1770,18 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
   // x += SelfAttn(LN1 x) [masked Q x all L_img K/V: fresh rows merged with the cache by mask
   // index]; x += CrossAttn(LN2 x, context K/V computed fresh); x += GEGLU-FF(LN3 x).
   const int Lc = ctx->d.ctx_len, Dc = ctx->d.ctx_dim;
-  auto ln_aff = [&](int b, int which) {  // LayerNorm affine as LN-modulation with (beta, gamma - 1)
-    ProfScope ps(ctx, st, IG_K_LNMOD, 0.0, (double)M * H * (4 + es));
-    launch_ln_mod<T>(ctx->X, H, 0, M, ctx->ri, ctx->unet_ln + ((size_t)b * 3 + which) * 2 * H, 0, 0, H,
+  auto ln_aff = [&](int b, int which, int r0, int r1) {  // LayerNorm affine as LN-modulation (beta, gamma - 1)
+    if (r1 <= r0) return;
+    ProfScope ps(ctx, st, IG_K_LNMOD, 0.0, (double)(r1 - r0) * H * (4 + es));
+    launch_ln_mod<T>(ctx->X, H, r0, r1, ctx->ri, ctx->unet_ln + ((size_t)b * 3 + which) * 2 * H, 0, 0, H,
                      ctx->d.ln_eps, h, H, st);
+    stats.kernel_launches++;
+  };
+  auto ln_aff_y = [&](int b, int buf) {  // Y block: LN1 of the unmasked rows from the staged Y_{b-1}
+    cudaStreamWaitEvent(st, ctx->ev_copy[buf], 0);
+    ProfScope ps(ctx, st, IG_K_LNMOD, 0.0, (double)uy[b] * H * (es + es));
+    launch_ln_mod_staged<T>(ctx->kv_arena, ctx->slot_stride, (long long)buf * ctx->buf_elems, ctx->L, H, M, M + uy[b],
+                            ctx->ri, ctx->unet_ln + (size_t)b * 3 * 2 * H, 0, 0, H, ctx->d.ln_eps, h, H, st);
     stats.kernel_launches++;
   };
   auto cross_kv = [&](const UnetW& u) {  // context rows -> K/V planes of the cross arena
@@ -1802,12 +1809,16 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
       stats.kernel_launches++;
     }
   };
-  auto unet_block = [&](int b, int buf) {
+  // ys: a Y block after the first cached one (unmasked rows [M, M + uy[b]) enter from the staged
+  // Y_{b-1}); Mk: rows through LN1 + the K/V projection (the Y requests' unmasked rows included)
+  auto unet_block = [&](int b, int buf, bool ys, int Mk) {
     const UnetW& u = ctx->unet[b];
     cross_kv(u);  // first: the parity path's positional write also stores (unused) Q rows
-    ln_aff(b, 0);
+    ln_aff(b, 0, 0, ys ? M : Mk);
+    if (ys) ln_aff_y(b, buf);
     wait_copy(buf);
     qkv_proj(0, M, u.qkv, nullptr, nullptr, nullptr, buf);
+    kv_proj(M, M + uy[b], u.qkv, nullptr, nullptr, buf);
     wait_copy_late(buf);
     attn(buf, false);
     record_kv(b, buf);
@@ -1815,7 +1826,7 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
     if (ctx->capturing) ctx->cap_mask |= 1u << buf;
     if (b + R < b1) issue_copy(ctx, sr, dkvg, dkvq, b + R, plan);
     gemm_rows(0, M, cat, ldcat, u.out1.w, u.out1.b, H, H, ctx->X, H, EPI_GATED_RES, ctx->ones, 0);
-    ln_aff(b, 1);
+    ln_aff(b, 1, 0, M);
     gemm_rows(0, M, h, H, u.q2.w, nullptr, H, H, ctx->Q, H, EPI_STORE, nullptr, 0);
     {
       AttnArgs a{};
@@ -1826,7 +1837,7 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
       attention(ctx, a, st, 4.0 * (double)M * Lc * H);
     }
     gemm_rows(0, M, cat, ldcat, u.out2.w, u.out2.b, H, H, ctx->X, H, EPI_GATED_RES, ctx->ones, 0);
-    ln_aff(b, 2);
+    ln_aff(b, 2, 0, M);
     GemmArgs gg{};  // fused: GEGLU in the tcgen05 epilogue (tile-interleaved weight copy)
     gg.A = h; gg.lda = H; gg.B = u.geglu_w_tc; gg.ldb = H; gg.bias = u.geglu_b_tc;
     gg.C = cat + H; gg.ldc = ldcat; gg.M = M; gg.N = 2 * F; gg.K = H; gg.epi = EPI_GEGLU;
@@ -1851,7 +1862,7 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
     const int buf = dense ? R : b % R;
     const bool ys = !dense && y_staged(b);
     if (unet) {
-      unet_block(b, buf);
+      unet_block(b, buf, ys, Mk);
     } else if (b < ctx->d.n_double) {
       const StreamW& wi = ctx->dimg[b];
       const StreamW& wt = ctx->dtxt[b];

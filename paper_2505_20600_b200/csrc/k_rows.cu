@@ -105,8 +105,13 @@ __global__ void build_rows_kernel(const ReqDev* __restrict__ reqs, int n, int L_
     const int tok = R.idx_u[j];
     info.req = q; info.slot = R.slot; info.kvpos = L_txt + tok; info.tok = tok;
     const float* src = R.tlatent + (long long)tok * C;
-    T* dst = Ain + (long long)(r - M_txt) * C;
-    for (int c = lane; c < C; c += 32) dst[c] = from_f<T>(src[c]);
+    if (img_to_x) {
+      float* dst = X + (long long)r * H;
+      for (int c = lane; c < C; c += 32) dst[c] = src[c];
+    } else {
+      T* dst = Ain + (long long)(r - M_txt) * C;
+      for (int c = lane; c < C; c += 32) dst[c] = from_f<T>(src[c]);
+    }
   } else {
     int q = 0;
     while (q + 1 < n && reqs[q + 1].img_row0 <= r) ++q;  // n <= max_batch: linear search

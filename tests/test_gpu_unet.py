@@ -179,3 +179,98 @@ def test_sdxl_level_full_width(which):
     for r in reqs:
         r.free()
     m.close()
+
+
+@pytest.mark.parametrize("dtype", [ig.IG_F32, ig.IG_BF16])
+@pytest.mark.parametrize("tier", [ig.IG_CACHE_HOST, ig.IG_CACHE_DEVICE])
+def test_unet_y_and_hybrid_caches(dtype, tier):
+    """Y (kv_blocks = 0) and hybrid (kv_blocks = 1: blocks {0, 2} Y, block 1 K/V) caches next to
+    a plain K/V cache in one batch, 2 steps, vs the oracle's unet_edit_step_y(y_blocks=)."""
+    from gpu_util import hybrid_planes
+    d = synth.UNET_SMALL
+    rng = np.random.default_rng(31)
+    masks = [synth.blob_mask_count(d, 85, rng), synth.rect_mask_count(d, 45, rng), synth.blob_mask_count(d, 66, rng)]
+    splits = [0, 1, None]
+    base = Model(d, dtype, opts=ig.ig_ctx_opts(4, 0, 2, 1, 0, 0))
+    reqs = [Request(base, 60 + i, mk) for i, mk in enumerate(masks)]
+    tst = torch.stack([synth.make_latent(d, 990 + s) for s in range(2)])  # template input states
+    ms, caches, refs = [], [], []
+    for i, kvb in enumerate(splits):
+        kv = synth.make_cache_kv(d, 30 + i, 2, dtype=TDT[dtype])
+        yv = synth.make_cache_y(d, 30 + i, 2, dtype=TDT[dtype])
+        if kvb is None:
+            c = ig.ig_cache_create(base.ctx, 2, tier)
+            fill_cache(base, c, kv, tst)
+            refs.append((kv.double().numpy(), None, None))
+        else:
+            m = Model(d, dtype, opts=ig.ig_ctx_opts(4, 0, 2, 1, 0, 0, 1, kvb))
+            ms.append(m)
+            ym = set(ig.y_block_modes(d.n_blocks, kvb))
+            c = ig.ig_cache_create(m.ctx, 2, tier)
+            fill_cache(m, c, hybrid_planes(kv, yv, ym), tst)
+            refs.append((kv.double().numpy(), yv.double().numpy(), ym))
+        caches.append(c)
+    for s in range(2):
+        ig.ig_edit_step(base.ctx, [r.req(i, caches[i], s, 0.0, 0.0) for i, r in enumerate(reqs)], 0)
+    torch.cuda.synchronize()
+    W = base.host_weights()
+    tsh = tst.double().numpy()
+    for i, r in enumerate(reqs):
+        x, ctx = r.latent0.double().cpu().numpy(), r.txt.double().cpu().numpy()
+        kvh, yh, ym = refs[i]
+        for s in range(2):
+            if ym is None:
+                x = oracle.unet_edit_step(d, W, x, r.mask_np, kvh[s], ctx)
+            else:
+                x = oracle.unet_edit_step_y(d, W, x, r.mask_np, yh[s], tsh[s], ctx, y_blocks=ym, kv_cache_step=kvh[s])
+        got = r.latent.double().cpu().numpy()
+        ok, worst = ctol(got, x, RTOL[dtype])
+        assert ok, (i, worst)
+        assert np.array_equal(got[r.mask_np == 0], r.latent0.cpu().numpy()[r.mask_np == 0])
+    for c in caches:
+        ig.ig_cache_free(c)
+    for r in reqs:
+        r.free()
+    for m in ms:
+        m.close()
+    base.close()
+
+
+@pytest.mark.parametrize("kv_blocks", [0, 1])
+def test_unet_hybrid_template_recording(kv_blocks):
+    """fp32: ig_cache_template on a cache_y ctx records K/V for the K/V blocks and Y_b where
+    block b or b + 1 is a Y block, against the oracle's dense pass; an edit from the template's
+    own state then stays on the dense trajectory for the masked rows."""
+    from gpu_util import cache_raw_numpy, n_planes, split_hybrid
+    d = synth.UNET_SMALL
+    m = Model(d, ig.IG_F32, opts=ig.ig_ctx_opts(2, 0, 2, 1, 0, 0, 1, kv_blocks))
+    W = m.host_weights()
+    mask = synth.blob_mask_count(d, 77, np.random.default_rng(12))
+    rq = Request(m, 70, mask)
+    st = rq.latent.clone()
+    cache = ig.ig_cache_template(m.ctx, st.data_ptr(), rq.txt.data_ptr(), 0, [1.0, 0.5, 0.0])
+    ym = set(ig.y_block_modes(d.n_blocks, kv_blocks))
+    states, okv, oy = oracle.unet_cache_template(d, W, rq.latent0.double().cpu().numpy(), rq.txt.double().cpu().numpy(),
+                                                 2, record_y=True)
+    raw = cache_raw_numpy(cache, d, 2, n_planes(d.n_blocks, ym), ig.IG_F32)
+    gkv, gy = split_hybrid(raw, d.n_blocks, ym)
+    for b in range(d.n_blocks):
+        if b not in ym:
+            ok, worst = ctol(gkv[:, b], okv[:, b], 1e-4)
+            assert ok, ("kv", b, worst)
+        if b in ym or (b + 1) in ym:
+            ok, worst = ctol(gy[:, b], oy[:, b], 1e-4)
+            assert ok, ("y", b, worst)
+    ok, worst = ctol(st.double().cpu().numpy(), states[-1], 1e-4)
+    assert ok, ("trajectory", worst)
+    for s in range(2):  # edit from the template's own input state at step s
+        x = torch.from_numpy(states[s]).float().cuda().contiguous()
+        rr = ig.make_req(0, x.data_ptr(), rq.mask, cache, s, 0.0, 0.0, rq.txt.data_ptr(), None)
+        ig.ig_edit_step(m.ctx, [rr], 0)
+        torch.cuda.synchronize()
+        got = x.double().cpu().numpy()
+        ok, worst = ctol(got[mask != 0], states[s + 1][mask != 0], 1e-4)
+        assert ok, ("same trajectory", s, worst)
+    ig.ig_cache_free(cache)
+    rq.free()
+    m.close()
