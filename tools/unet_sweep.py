@@ -42,7 +42,7 @@ def step_flops(d, n_rows, n_req):
 
 
 class Level:
-    def __init__(self, d, batch, tier, cache_steps, dev, graphs=0):
+    def __init__(self, d, batch, tier, cache_steps, dev, graphs=0, y=0, kv_blocks=0):
         self.d = d
         self.W = []
         ptrs = []
@@ -50,15 +50,20 @@ class Level:
             t = synth.make_weight(d, name, shape, fan_in, 0, dev, torch.bfloat16).contiguous()
             self.W.append(t)
             ptrs.append(t.data_ptr())
-        opts = ig.ig_ctx_opts(batch, 0, 4, 1, 0, 0, 0, 0, graphs)
+        opts = ig.ig_ctx_opts(batch, 0, 4, 1, 0, 0, y, kv_blocks, graphs)
         self.ctx = ig.ig_ctx_create(ig.make_desc(d, ig.IG_BF16), ptrs, 0, opts)
         self.cache = ig.ig_cache_create(self.ctx, cache_steps, tier)
+        ym = set(ig.y_block_modes(d.n_blocks, kv_blocks)) if y else set()
+        planes = sum((0 if b in ym else 2) + (1 if (b in ym or (b + 1) in ym) else 0) for b in range(d.n_blocks))
+        ptr, nbytes, t = ig.ig_cache_storage(self.cache)
+        plane = d.L_img * d.hidden
         for s in range(cache_steps):  # fill step by step (bounded staging memory)
-            kv = synth.normal(7000 + s, "cache_kv", (1, d.n_blocks, 2, d.L_img, d.hidden), dev).to(torch.bfloat16)
-            ptr, nbytes, t = ig.ig_cache_storage(self.cache)
-            step_bytes = kv.numel() * 2
-            ig.ig_copy(ptr + s * step_bytes, kv.data_ptr(), step_bytes)
+            pl = synth.normal(7000 + s, "cache_planes", (planes, plane), dev).to(torch.bfloat16)
+            ig.ig_copy(ptr + s * planes * plane * 2, pl.data_ptr(), planes * plane * 2)
             torch.cuda.synchronize()
+        lat = synth.normal(7100, "cache_states", (cache_steps, plane), dev).float()  # template input states
+        ig.ig_copy(ptr + cache_steps * planes * plane * 2, lat.data_ptr(), lat.numel() * 4)
+        torch.cuda.synchronize()
         torch.cuda.synchronize()
         self.cache_steps = cache_steps
         self.state = [synth.make_latent(d, 100 + i, dev).contiguous() for i in range(batch)]
@@ -91,6 +96,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=6)  # > NSTAGE: every staging slot's graph captured
     ap.add_argument("--tier", default="device", choices=["device", "host"])
     ap.add_argument("--cache-steps", type=int, default=8)
+    ap.add_argument("--cache", default="kv", choices=["kv", "y"], help="K/V or Y cache (the paper's SDXL form)")
     ap.add_argument("--graphs", type=int, default=-1,
                     help="CUDA graphs of whole steps (default: on for the HBM tier; host-tier DMA sources change per step)")
     args = ap.parse_args()
@@ -98,8 +104,9 @@ def main():
     ig.lib()
     tier = ig.IG_CACHE_DEVICE if args.tier == "device" else ig.IG_CACHE_HOST
     graphs = (1 if args.tier == "device" else 0) if args.graphs < 0 else args.graphs
-    lv = [Level(synth.SDXL_L64, args.batch, tier, args.cache_steps, dev, graphs),
-          Level(synth.SDXL_L32, args.batch, tier, args.cache_steps, dev, graphs)]
+    yc = 1 if args.cache == "y" else 0
+    lv = [Level(synth.SDXL_L64, args.batch, tier, args.cache_steps, dev, graphs, yc),
+          Level(synth.SDXL_L32, args.batch, tier, args.cache_steps, dev, graphs, yc)]
     peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["bf16_tflops_sustained"] \
         if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 1384.7
     stream = torch.cuda.Stream(device=dev)
@@ -153,6 +160,7 @@ def main():
             f_1 = sum(step_flops(L.d, args.batch * L.d.L_img, args.batch) for L in lv)
             p["flop_ratio_dense_over_masked"] = round(f_1 / f_m, 3)
     print(json.dumps({"config": "sdxl_unet_attention_stack", "batch": args.batch, "tier": args.tier, "graphs": graphs,
+                      "cache": args.cache,
                       "cache_steps": args.cache_steps, "points": pts}))
 
 
