@@ -274,3 +274,32 @@ def test_unet_hybrid_template_recording(kv_blocks):
     ig.ig_cache_free(cache)
     rq.free()
     m.close()
+
+
+@pytest.mark.parametrize("tier", [ig.IG_CACHE_HOST, ig.IG_CACHE_DEVICE])
+def test_unet_fp8_cache(tier):
+    """FP8 (e4m3, per (token, head) scale) K/V cache on a UNet context: the oracle
+    mirrors the quantize/dequantize round trip of the same bf16 cache; 2 requests, 2 steps."""
+    d = synth.UNET_SMALL
+    m = Model(d, ig.IG_BF16, opts=ig.ig_ctx_opts(4, 0, 2, 1, 0, 1))
+    W = m.host_weights()
+    rng = np.random.default_rng(41)
+    reqs = [Request(m, 80 + i, mk) for i, mk in
+            enumerate([synth.blob_mask_count(d, 70, rng), synth.rect_mask_count(d, 30, rng)])]
+    kv = synth.make_cache_kv(d, 11, 2, dtype=torch.bfloat16, device="cuda")
+    cache = ig.ig_cache_create(m.ctx, 2, ig.IG_CACHE_HOST)
+    ig.ig_cache_write(m.ctx, cache, kv.data_ptr())
+    if tier == ig.IG_CACHE_DEVICE:
+        dc = ig.ig_cache_clone(m.ctx, cache, ig.IG_CACHE_DEVICE)
+        ig.ig_cache_free(cache)
+        cache = dc
+    kvh = oracle.fp8_kv_roundtrip(kv.float().cpu().numpy(), d.heads)
+    _steps(m, reqs, cache, 2)
+    for r in reqs:
+        want = _oracle_steps(d, W, r, kvh, 2)
+        ok, worst = ctol(r.latent.double().cpu().numpy(), want, 2e-2)
+        assert ok, worst
+    ig.ig_cache_free(cache)
+    for r in reqs:
+        r.free()
+    m.close()

@@ -42,7 +42,7 @@ def step_flops(d, n_rows, n_req):
 
 
 class Level:
-    def __init__(self, d, batch, tier, cache_steps, dev, graphs=0, y=0, kv_blocks=0):
+    def __init__(self, d, batch, tier, cache_steps, dev, graphs=0, y=0, kv_blocks=0, fp8=0):
         self.d = d
         self.W = []
         ptrs = []
@@ -50,8 +50,22 @@ class Level:
             t = synth.make_weight(d, name, shape, fan_in, 0, dev, torch.bfloat16).contiguous()
             self.W.append(t)
             ptrs.append(t.data_ptr())
-        opts = ig.ig_ctx_opts(batch, 0, 4, 1, 0, 0, y, kv_blocks, graphs)
+        opts = ig.ig_ctx_opts(batch, 0, 4, 1, 0, fp8, y, kv_blocks, graphs)
         self.ctx = ig.ig_ctx_create(ig.make_desc(d, ig.IG_BF16), ptrs, 0, opts)
+        self.cache_steps = cache_steps
+        if fp8:  # quantized on the device by ig_cache_write (per (token, head) scales)
+            self.cache = ig.ig_cache_create(self.ctx, cache_steps, ig.IG_CACHE_HOST)
+            kv = torch.empty((cache_steps, d.n_blocks, 2, d.L_img, d.hidden), dtype=torch.bfloat16, device=dev)
+            for s in range(cache_steps):
+                kv[s] = synth.normal(7000 + s, "cache_planes", tuple(kv.shape[1:]), dev).to(torch.bfloat16)
+            ig.ig_cache_write(self.ctx, self.cache, kv.data_ptr())
+            del kv
+            if tier == ig.IG_CACHE_DEVICE:
+                dc = ig.ig_cache_clone(self.ctx, self.cache, tier)
+                ig.ig_cache_free(self.cache)
+                self.cache = dc
+            self._inputs(batch, dev)
+            return
         self.cache = ig.ig_cache_create(self.ctx, cache_steps, tier)
         ym = set(ig.y_block_modes(d.n_blocks, kv_blocks)) if y else set()
         planes = sum((0 if b in ym else 2) + (1 if (b in ym or (b + 1) in ym) else 0) for b in range(d.n_blocks))
@@ -65,7 +79,10 @@ class Level:
         ig.ig_copy(ptr + cache_steps * planes * plane * 2, lat.data_ptr(), lat.numel() * 4)
         torch.cuda.synchronize()
         torch.cuda.synchronize()
-        self.cache_steps = cache_steps
+        self._inputs(batch, dev)
+
+    def _inputs(self, batch, dev):
+        d = self.d
         self.state = [synth.make_latent(d, 100 + i, dev).contiguous() for i in range(batch)]
         self.ctxemb = [synth.make_ctx(d, 100 + i, dev, torch.bfloat16).contiguous() for i in range(batch)]
         self.masks = []
@@ -96,7 +113,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=6)  # > NSTAGE: every staging slot's graph captured
     ap.add_argument("--tier", default="device", choices=["device", "host"])
     ap.add_argument("--cache-steps", type=int, default=8)
-    ap.add_argument("--cache", default="kv", choices=["kv", "y"], help="K/V or Y cache (the paper's SDXL form)")
+    ap.add_argument("--cache", default="kv", choices=["kv", "y", "fp8"], help="K/V, Y (the paper's SDXL form) or FP8 K/V cache")
     ap.add_argument("--graphs", type=int, default=-1,
                     help="CUDA graphs of whole steps (default: on for the HBM tier; host-tier DMA sources change per step)")
     args = ap.parse_args()
@@ -105,8 +122,9 @@ def main():
     tier = ig.IG_CACHE_DEVICE if args.tier == "device" else ig.IG_CACHE_HOST
     graphs = (1 if args.tier == "device" else 0) if args.graphs < 0 else args.graphs
     yc = 1 if args.cache == "y" else 0
-    lv = [Level(synth.SDXL_L64, args.batch, tier, args.cache_steps, dev, graphs, yc),
-          Level(synth.SDXL_L32, args.batch, tier, args.cache_steps, dev, graphs, yc)]
+    f8 = 1 if args.cache == "fp8" else 0
+    lv = [Level(synth.SDXL_L64, args.batch, tier, args.cache_steps, dev, graphs, yc, 0, f8),
+          Level(synth.SDXL_L32, args.batch, tier, args.cache_steps, dev, graphs, yc, 0, f8)]
     peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["bf16_tflops_sustained"] \
         if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 1384.7
     stream = torch.cuda.Stream(device=dev)
