@@ -196,3 +196,37 @@ def unet_macs_per_row(d) -> Dict[str, int]:
     H, F, L, Lc = d.hidden, d.mlp_hidden, d.L_img, d.ctx_len
     return {"linear": 3 * H * H + H * H + H * H + H * H + 2 * F * H + F * H,
             "attn": 2 * L * H + 2 * Lc * H}
+
+
+def unet_edit_step_planned(d, W, state: np.ndarray, mask, tstate: np.ndarray, ctx: np.ndarray, k: int,
+                           kv_cache_step: Optional[np.ndarray] = None, y_cache_step: Optional[np.ndarray] = None,
+                           y_blocks=()) -> np.ndarray:
+    """Algorithm 1 (C-AMB 23) on the UNet stack: the first k blocks run dense — all
+    L_img tokens, the unmasked ones entering from the template's input state tstate of this
+    step, fresh K/V, no cache — and blocks >= k run mask-aware: K/V blocks read kv_cache_step,
+    Y blocks (y_blocks) recompute the unmasked tokens' K/V from their block input (the rows
+    computed by the prefix for block k, else the template's Y_{b-1}).  Unmasked rows of the
+    result are untouched."""
+    idx_m, idx_u, n_m = index_build(mask)
+    out = np.array(state, dtype=np.float64, copy=True)
+    if n_m == 0:
+        return out
+    all_idx = np.arange(d.L_img)
+    none = np.zeros(0, dtype=np.int64)
+    X = np.array(tstate, dtype=np.float64, copy=True)
+    X[idx_m] = out[idx_m]
+    yb = set(y_blocks)
+    for b in range(min(k, d.n_unet)):
+        X, _, _ = unet_block_masked(d, W, b, X, all_idx, none, None, ctx)
+    x = X[idx_m]
+    for b in range(min(k, d.n_unet), d.n_unet):
+        if b in yb:
+            u = X[idx_u] if b == k else np.asarray(y_cache_step[b - 1], np.float64)[idx_u]
+            ku, vu = unet_kv_from_y(d, W, b, u)
+            blk = np.zeros((2, d.L_img, d.hidden))
+            blk[0][idx_u], blk[1][idx_u] = ku, vu
+        else:
+            blk = kv_cache_step[b]
+        x, _, _ = unet_block_masked(d, W, b, x, idx_m, idx_u, blk, ctx)
+    out[idx_m] = x
+    return out

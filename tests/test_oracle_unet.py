@@ -258,3 +258,32 @@ def test_y_variant_pins():
                                   oracle.unet_edit_step(D, W, states[0], mask, junk, ctx))
     other = oracle.unet_edit_step_y(D, W, states[0], mask, ys[1], states[0], ctx)
     assert not np.allclose(other[m], states[1][m])
+
+
+def test_planned_step_pins():
+    """Algorithm-1 dense prefix on the UNet stack: k = 0 is the K/V (resp. hybrid) step; k = N
+    is the dense step on [masked rows of state | unmasked rows of tstate]; with a cache recorded
+    from the same state every k stays on the dense trajectory."""
+    W = _weights()
+    ctx = _ctx()
+    states, kv, ys = oracle.unet_cache_template(D, W, _state(), ctx, 1, record_y=True)
+    mask = synth.rect_mask_count(D, 50, np.random.default_rng(13))
+    m = mask != 0
+    x = _state(rid=7)
+    junk = synth.make_cache_kv(D, 5, 1).double().numpy()[0]
+    np.testing.assert_array_equal(oracle.unet_edit_step_planned(D, W, x, mask, states[0], ctx, 0, kv_cache_step=junk),
+                                  oracle.unet_edit_step(D, W, x, mask, junk, ctx))
+    np.testing.assert_allclose(
+        oracle.unet_edit_step_planned(D, W, x, mask, states[0], ctx, 0, kv_cache_step=junk, y_cache_step=ys[0], y_blocks=[0]),
+        oracle.unet_edit_step_y(D, W, x, mask, ys[0], states[0], ctx, y_blocks=[0], kv_cache_step=junk), rtol=0, atol=0)
+    comb = np.array(states[0])
+    comb[m] = x[m]
+    full = oracle.unet_dense_step(D, W, comb, ctx)
+    got = oracle.unet_edit_step_planned(D, W, x, mask, states[0], ctx, D.n_unet, kv_cache_step=junk)
+    np.testing.assert_allclose(got[m], full[m], rtol=1e-12, atol=1e-12)
+    assert np.array_equal(got[~m], x[~m])
+    for k in range(D.n_unet + 1):
+        for yb in ((), (1,)):
+            out = oracle.unet_edit_step_planned(D, W, states[0], mask, states[0], ctx, k, kv_cache_step=kv[0],
+                                                y_cache_step=ys[0], y_blocks=yb)
+            np.testing.assert_allclose(out[m], states[1][m], rtol=1e-12, atol=1e-12)
