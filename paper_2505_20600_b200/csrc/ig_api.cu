@@ -597,7 +597,7 @@ extern "C" ig_status ig_ctx_create(const ig_model_desc* desc, const void* const*
     if (!okm) { ig_ctx_destroy(ctx); return set_err(IG_ENOMEM, "Y recording staging allocation failed"); }
   }
   // per-step descriptor staging: ReqDev[B] + AttnSeg[2B] + 2 x KvGatherReq[nb * B]
-  ctx->stage_bytes = B * sizeof(ReqDev) + 5 * B * sizeof(AttnSeg) + 2 * (size_t)ctx->nb * B * sizeof(KvGatherReq) + 1024;
+  ctx->stage_bytes = B * sizeof(ReqDev) + 8 * B * sizeof(AttnSeg) + 2 * (size_t)ctx->nb * B * sizeof(KvGatherReq) + 1024;
   for (int i = 0; i < NSTAGE; ++i) {
     if (cudaHostAlloc((void**)&ctx->h_stage[i], ctx->stage_bytes, cudaHostAllocMapped | cudaHostAllocPortable) !=
             cudaSuccess ||
@@ -1152,6 +1152,8 @@ static void issue_copy(ig_ctx* ctx, const std::vector<StepReq>& sr, const KvGath
 // picks a dense block when C_w/o > L + C_w, which is the B200 + PCIe regime.)
 static double block_flops_rows(const ig_ctx* ctx, long long rows) {
   const double H = ctx->H, F = ctx->F;
+  if (ctx->d.n_unet > 0)  // qkv + out + q2 + out2 (6 H^2), GEGLU + out (3 F H); self + cross attention
+    return 2.0 * rows * (6 * H * H + 3 * H * F) + 4.0 * rows * (ctx->L + ctx->d.ctx_len) * H;
   return 2.0 * rows * (3 * H * H + H * H + 2 * H * F) + 4.0 * rows * ctx->L * H;
 }
 
@@ -1333,7 +1335,7 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
   }
   // ---- Algorithm-1 block plan (C-AMB 23): a dense prefix of k blocks ----
   int kplan = 0;
-  if (any_cache && !record && b0 == 0 && b1 == nb && !unet) {  // (UNet: no Algorithm-1 plan yet)
+  if (any_cache && !record && b0 == 0 && b1 == nb) {
     if (ctx->plan_mode == 1) kplan = std::min(ctx->plan_k, nb);
     else if (ctx->plan_mode == 2) kplan = plan_prefix(ctx, sr, plan.dshared);
   }
@@ -1379,12 +1381,17 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
   // attention segments: [0, 2B) the masked-rows step, [2B, 5B) the dense prefix (+ unmasked)
   AttnSeg* hseg = (AttnSeg*)(hs + ctx->o.max_batch * sizeof(ReqDev));
   AttnSeg* hsegf = hseg + 2 * ctx->o.max_batch;
-  KvGatherReq* hkvg = (KvGatherReq*)((char*)hseg + 5 * ctx->o.max_batch * sizeof(AttnSeg));
+  // UNet cross-attention: [5B, 6B) masked rows (cached blocks), [6B, 8B) + unmasked (dense prefix)
+  AttnSeg* hsegc = hseg + 5 * ctx->o.max_batch;
+  AttnSeg* hsegcf = hseg + 6 * ctx->o.max_batch;
+  KvGatherReq* hkvg = (KvGatherReq*)((char*)hseg + 8 * ctx->o.max_batch * sizeof(AttnSeg));
   ReqDev* dreq = (ReqDev*)ds;
   AttnSeg* dseg = (AttnSeg*)(ds + ctx->o.max_batch * sizeof(ReqDev));
   AttnSeg* dsegf = dseg + 2 * ctx->o.max_batch;
-  KvGatherReq* dkvg = (KvGatherReq*)((char*)dseg + 5 * ctx->o.max_batch * sizeof(AttnSeg));
-  int nseg = 0, max_q = 0, nsegf = 0, max_qf = 0;
+  AttnSeg* dsegc = dseg + 5 * ctx->o.max_batch;
+  AttnSeg* dsegcf = dseg + 6 * ctx->o.max_batch;
+  KvGatherReq* dkvg = (KvGatherReq*)((char*)dseg + 8 * ctx->o.max_batch * sizeof(AttnSeg));
+  int nseg = 0, max_q = 0, nsegf = 0, max_qf = 0, nsegc = 0, nsegcf = 0, max_qcf = 0;
   int img_row = M_txt, kvrow = M_y;
   for (int q = 0; q < na; ++q) {
     const ig_edit_req* r = sr[q].r;
@@ -1409,9 +1416,12 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
     if (Lt > 0) { hseg[nseg++] = AttnSeg{q * Lt, Lt, kvb}; max_q = std::max(max_q, Lt); }
     hseg[nseg++] = AttnSeg{img_row, d.n_m, kvb};
     max_q = std::max(max_q, d.n_m);
-    if (unet) {  // cross-attention segments (the dense-prefix slots: UNet steps never plan)
-      hsegf[nsegf++] = AttnSeg{img_row, d.n_m, (long long)q * 2 * ctx->d.ctx_len * H};
-      max_qf = std::max(max_qf, d.n_m);
+    if (unet) {  // cross-attention segments: the request's context K/V in the cross arena
+      const long long ckv = (long long)q * 2 * ctx->d.ctx_len * H;
+      hsegc[nsegc++] = AttnSeg{img_row, d.n_m, ckv};
+      hsegcf[nsegcf++] = AttnSeg{img_row, d.n_m, ckv};
+      if (kplan > 0 && d.n_ui > 0) hsegcf[nsegcf++] = AttnSeg{d.uimg_row0, d.n_ui, ckv};
+      max_qcf = std::max(max_qcf, std::max(d.n_m, kplan > 0 ? d.n_ui : 0));
     }
     if (kplan > 0) {
       if (Lt > 0) hsegf[nsegf++] = AttnSeg{q * Lt, Lt, kvb};
@@ -1422,9 +1432,10 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
     img_row += d.n_m;
     if (!ycache) kvrow += d.n_ui;
   }
-  int npair = 0, npairf = 0;  // attention work items (segment, 256-row query-tile pair)
+  int npair = 0, npairf = 0, npaircf = 0;  // attention work items (segment, 256-row query-tile pair)
   for (int i = 0; i < nseg; ++i) npair += (hseg[i].q_len + 255) / 256;
   for (int i = 0; i < nsegf; ++i) npairf += (hsegf[i].q_len + 255) / 256;
+  for (int i = 0; i < nsegcf; ++i) npaircf += (hsegcf[i].q_len + 255) / 256;
   // copy-lane plan and per-(block, request) gather descriptors (see issue_copy)
   plan.any = any_cache;
   plan.max_nu = max_nu;
@@ -1504,7 +1515,7 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
     if (s2.use_cache && (s2.r->cache->tier != IG_CACHE_DEVICE || ctx->o.copy_mode == 0)) graph_ok = false;
   std::string gkey;
   if (graph_ok) {
-    std::vector<long long> k = {si, kplan, na, M, M_txt, M_full, nseg, max_q, nsegf, max_qf, max_nu,
+    std::vector<long long> k = {si, kplan, na, M, M_txt, M_full, nseg, max_q, nsegf, max_qf, max_nu, nsegcf, max_qcf,
                                 plan.gather, plan.gather_q8, any_cache, (long long)desc_bytes};
     for (int v : uy) k.push_back(v);
     for (auto& s2 : sr) {
@@ -1811,45 +1822,52 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
   };
   // ys: a Y block after the first cached one (unmasked rows [M, M + uy[b]) enter from the staged
   // Y_{b-1}); Mk: rows through LN1 + the K/V projection (the Y requests' unmasked rows included)
-  auto unet_block = [&](int b, int buf, bool ys, int Mk) {
+  // dense: an Algorithm-1 prefix block (all rows [0, M_full), own K/V buffer, no cache)
+  auto unet_block = [&](int b, int buf, bool ys, int Mk, bool dense) {
     const UnetW& u = ctx->unet[b];
+    const int Mc = dense ? M_full : M;
     cross_kv(u);  // first: the parity path's positional write also stores (unused) Q rows
-    ln_aff(b, 0, 0, ys ? M : Mk);
+    ln_aff(b, 0, 0, dense ? M_full : (ys ? M : Mk));
     if (ys) ln_aff_y(b, buf);
-    wait_copy(buf);
-    qkv_proj(0, M, u.qkv, nullptr, nullptr, nullptr, buf);
-    kv_proj(M, M + uy[b], u.qkv, nullptr, nullptr, buf);
-    wait_copy_late(buf);
-    attn(buf, false);
+    if (!dense) wait_copy(buf);
+    qkv_proj(0, Mc, u.qkv, nullptr, nullptr, nullptr, buf);
+    if (!dense) {
+      kv_proj(M, M + uy[b], u.qkv, nullptr, nullptr, buf);
+      wait_copy_late(buf);
+    }
+    attn(buf, dense);
     record_kv(b, buf);
-    cudaEventRecord(ctx->ev_comp[buf], st);
-    if (ctx->capturing) ctx->cap_mask |= 1u << buf;
-    if (b + R < b1) issue_copy(ctx, sr, dkvg, dkvq, b + R, plan);
-    gemm_rows(0, M, cat, ldcat, u.out1.w, u.out1.b, H, H, ctx->X, H, EPI_GATED_RES, ctx->ones, 0);
-    ln_aff(b, 1, 0, M);
-    gemm_rows(0, M, h, H, u.q2.w, nullptr, H, H, ctx->Q, H, EPI_STORE, nullptr, 0);
+    if (!dense) {
+      cudaEventRecord(ctx->ev_comp[buf], st);
+      if (ctx->capturing) ctx->cap_mask |= 1u << buf;
+      if (b + R < b1) issue_copy(ctx, sr, dkvg, dkvq, b + R, plan);
+    }
+    gemm_rows(0, Mc, cat, ldcat, u.out1.w, u.out1.b, H, H, ctx->X, H, EPI_GATED_RES, ctx->ones, 0);
+    ln_aff(b, 1, 0, Mc);
+    gemm_rows(0, Mc, h, H, u.q2.w, nullptr, H, H, ctx->Q, H, EPI_STORE, nullptr, 0);
     {
       AttnArgs a{};
       a.Q = ctx->Q; a.ldq = H; a.O = cat; a.ldo = ldcat; a.kv_arena = ctx->xkv; a.kv_off = 0;
-      a.segs = dsegf; a.nseg = nsegf; a.max_qlen = max_qf; a.n_pairs = npairf; a.q_rows = M;
+      a.segs = dense ? dsegcf : dsegc; a.nseg = dense ? nsegcf : nsegc; a.max_qlen = dense ? max_qcf : max_q;
+      a.n_pairs = dense ? npaircf : npair; a.q_rows = Mc;
       a.L = Lc; a.heads = ctx->d.heads; a.head_dim = ctx->d.head_dim;
       a.scale = 1.0f / sqrtf((float)ctx->d.head_dim);
-      attention(ctx, a, st, 4.0 * (double)M * Lc * H);
+      attention(ctx, a, st, 4.0 * (double)Mc * Lc * H);
     }
-    gemm_rows(0, M, cat, ldcat, u.out2.w, u.out2.b, H, H, ctx->X, H, EPI_GATED_RES, ctx->ones, 0);
-    ln_aff(b, 2, 0, M);
+    gemm_rows(0, Mc, cat, ldcat, u.out2.w, u.out2.b, H, H, ctx->X, H, EPI_GATED_RES, ctx->ones, 0);
+    ln_aff(b, 2, 0, Mc);
     GemmArgs gg{};  // fused: GEGLU in the tcgen05 epilogue (tile-interleaved weight copy)
     gg.A = h; gg.lda = H; gg.B = u.geglu_w_tc; gg.ldb = H; gg.bias = u.geglu_b_tc;
-    gg.C = cat + H; gg.ldc = ldcat; gg.M = M; gg.N = 2 * F; gg.K = H; gg.epi = EPI_GEGLU;
+    gg.C = cat + H; gg.ldc = ldcat; gg.M = Mc; gg.N = 2 * F; gg.K = H; gg.epi = EPI_GEGLU;
     if (u.geglu_w_tc && g_tc_gemm && gemm_tc_supported(gg)) {
       gemm(ctx, gg, st);
     } else {
-      gemm_rows(0, M, h, H, u.geglu.w, u.geglu.b, 2 * F, H, ctx->u2, 2 * F, EPI_STORE, nullptr, 0);
-      ProfScope ps(ctx, st, IG_K_LNMOD, 0.0, (double)M * 3 * F * es);
-      launch_geglu<T>((const T*)ctx->u2, 2 * F, M, F, cat + H, ldcat, st);
+      gemm_rows(0, Mc, h, H, u.geglu.w, u.geglu.b, 2 * F, H, ctx->u2, 2 * F, EPI_STORE, nullptr, 0);
+      ProfScope ps(ctx, st, IG_K_LNMOD, 0.0, (double)Mc * 3 * F * es);
+      launch_geglu<T>((const T*)ctx->u2, 2 * F, Mc, F, cat + H, ldcat, st);
       stats.kernel_launches++;
     }
-    gemm_rows(0, M, cat + H, ldcat, u.ff2.w, u.ff2.b, H, F, ctx->X, H, EPI_GATED_RES, ctx->ones, 0);
+    gemm_rows(0, Mc, cat + H, ldcat, u.ff2.w, u.ff2.b, H, F, ctx->X, H, EPI_GATED_RES, ctx->ones, 0);
   };
 
   // ---- blocks ----
@@ -1862,7 +1880,7 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
     const int buf = dense ? R : b % R;
     const bool ys = !dense && y_staged(b);
     if (unet) {
-      unet_block(b, buf, ys, Mk);
+      unet_block(b, buf, ys, Mk, dense);
     } else if (b < ctx->d.n_double) {
       const StreamW& wi = ctx->dimg[b];
       const StreamW& wt = ctx->dtxt[b];

@@ -303,3 +303,49 @@ def test_unet_fp8_cache(tier):
     for r in reqs:
         r.free()
     m.close()
+
+
+@pytest.mark.parametrize("dtype", [ig.IG_F32, ig.IG_BF16])
+@pytest.mark.parametrize("k", [1, 3])
+def test_unet_dense_prefix(dtype, k):
+    """Algorithm-1 dense prefix (ig_set_plan mode 1, k blocks) on the UNet stack: a K/V-cache
+    request and a hybrid-cache request (blocks {0, 2} Y) in one batch, 2 steps, vs the oracle's
+    unet_edit_step_planned (unmasked rows of the prefix from the template's input state)."""
+    from gpu_util import hybrid_planes
+    d = synth.UNET_SMALL
+    rng = np.random.default_rng(51)
+    masks = [synth.blob_mask_count(d, 90, rng), synth.rect_mask_count(d, 52, rng)]
+    base = Model(d, dtype, opts=ig.ig_ctx_opts(4, 0, 2, 1, 0, 0))
+    hyb = Model(d, dtype, opts=ig.ig_ctx_opts(4, 0, 2, 1, 0, 0, 1, 1))
+    reqs = [Request(base, 90 + i, mk) for i, mk in enumerate(masks)]
+    tst = torch.stack([synth.make_latent(d, 995 + s) for s in range(2)])
+    kv = synth.make_cache_kv(d, 40, 2, dtype=TDT[dtype])
+    yv = synth.make_cache_y(d, 40, 2, dtype=TDT[dtype])
+    ym = set(ig.y_block_modes(d.n_blocks, 1))
+    c_kv = ig.ig_cache_create(base.ctx, 2, ig.IG_CACHE_HOST)
+    fill_cache(base, c_kv, kv, tst)
+    c_hy = ig.ig_cache_create(hyb.ctx, 2, ig.IG_CACHE_HOST)
+    fill_cache(hyb, c_hy, hybrid_planes(kv, yv, ym), tst)
+    ig.ig_set_plan(base.ctx, 1, k)
+    caches = [c_kv, c_hy]
+    for s in range(2):
+        ig.ig_edit_step(base.ctx, [r.req(i, caches[i], s, 0.0, 0.0) for i, r in enumerate(reqs)], 0)
+        assert ig.ig_last_plan(base.ctx) == k
+    torch.cuda.synchronize()
+    W = base.host_weights()
+    kvh, yh, tsh = kv.double().numpy(), yv.double().numpy(), tst.double().numpy()
+    for i, r in enumerate(reqs):
+        x, ctx = r.latent0.double().cpu().numpy(), r.txt.double().cpu().numpy()
+        for s in range(2):
+            x = oracle.unet_edit_step_planned(d, W, x, r.mask_np, tsh[s], ctx, k, kv_cache_step=kvh[s],
+                                              y_cache_step=yh[s], y_blocks=ym if i == 1 else ())
+        got = r.latent.double().cpu().numpy()
+        ok, worst = ctol(got, x, RTOL[dtype])
+        assert ok, (i, worst)
+        assert np.array_equal(got[r.mask_np == 0], r.latent0.cpu().numpy()[r.mask_np == 0])
+    ig.ig_cache_free(c_kv)
+    ig.ig_cache_free(c_hy)
+    for r in reqs:
+        r.free()
+    hyb.close()
+    base.close()
