@@ -214,6 +214,9 @@ struct ig_ctx {
   // eagerly), so the next eager step first re-records them after the graph on its stream
   bool graph_tail = false;
   cudaStream_t graph_st = nullptr;
+  // PDL: the next GEMM may overlap its prologue with the previous kernel only if nothing but a
+  // kernel precedes it on the stream (no event wait, memcpy or step boundary in between)
+  bool pdl_block = true;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   // Algorithm-1 block plan (ig_set_plan): 0 off, 1 forced dense-prefix length, 2 model
   int plan_mode = 0, plan_k = 0, last_plan_k = 0;
@@ -306,13 +309,25 @@ static void CUDART_CB unpin_cb(void* p) {
 static bool g_tc_gemm = true;   // tcgen05 GEMM for bf16 (set false only by IG_TEST_SIMT)
 static bool g_tc_attn = true;
 
+static bool g_pdl = getenv("IG_NO_PDL") == nullptr;  // A/B switch
+
 static void gemm(ig_ctx* ctx, const GemmArgs& g, cudaStream_t st) {
   if (g.M <= 0 || g.N <= 0) return;
   ctx->stats.kernel_launches++;
   ProfScope ps(ctx, st, IG_K_GEMM, 2.0 * g.M * g.N * g.K, 0.0, g.M, g.N, g.K, g.epi);
+  GemmArgs g2 = g;
+  g2.pdl = g_pdl && !ctx->pdl_block && !ctx->prof;  // (profiling brackets launches with events)
+  ctx->pdl_block = false;
   if (ctx->d.dtype == IG_F32) launch_gemm_simt<float>(g, st);
-  else if (g_tc_gemm && gemm_tc_supported(g)) launch_gemm_tc(g, st);
+  else if (g_tc_gemm && gemm_tc_supported(g)) launch_gemm_tc(g2, st);
   else launch_gemm_simt<bf16>(g, st);
+}
+
+// every event wait on the compute stream goes through here: the kernel after it must not be a
+// programmatic (PDL) launch
+static void stream_wait(ig_ctx* ctx, cudaStream_t st, cudaEvent_t ev) {
+  cudaStreamWaitEvent(st, ev, 0);
+  ctx->pdl_block = true;
 }
 
 static void attention(ig_ctx* ctx, const AttnArgs& a, cudaStream_t st, double flops) {
@@ -1251,6 +1266,7 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
   const long long es = (long long)ctx->esz;
   const bool unet = ctx->d.n_unet > 0;
   ctx->stats = ig_stats{};
+  ctx->pdl_block = true;  // the step's first GEMM may follow anything the caller enqueued
   auto t_host0 = std::chrono::steady_clock::now();
   // ---- host validation (nothing enqueued before this passes) ----
   if (n < 0 || n > ctx->o.max_batch) return set_err(IG_EINVAL, "n=%d outside [0, max_batch=%d]", n, ctx->o.max_batch);
@@ -1702,7 +1718,7 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
   // staged Y_{b-1} rows (the copy lane's V-plane landing zone), after waiting for the copy
   auto y_staged = [&](int b) { return uy[b] > 0 && b > kplan; };
   auto ln_mod_y = [&](int b, int buf, int mod_t, int shift_c, int scale_c) {
-    cudaStreamWaitEvent(st, ctx->ev_copy[buf], 0);
+    stream_wait(ctx, st, ctx->ev_copy[buf]);
     const long long off = ctx->mods[mod_t].off;
     ProfScope ps(ctx, st, IG_K_LNMOD, 0.0, (double)uy[b] * H * (es + es));
     launch_ln_mod_staged<T>(ctx->kv_arena, ctx->slot_stride, (long long)buf * ctx->buf_elems, ctx->L, H, M, M + uy[b],
@@ -1715,7 +1731,7 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
     const int yb = b % R;
     const size_t plane = (size_t)ctx->Limg * H * es;
     char* ys = (char*)ctx->yrec + (size_t)yb * plane;
-    cudaStreamWaitEvent(st, ctx->ev_yrec[yb], 0);  // the D2H of block b - R is done
+    stream_wait(ctx, st, ctx->ev_yrec[yb]);  // the D2H of block b - R is done
     launch_rows_to<T>(ctx->X + (long long)M_txt * H, ys, (long long)ctx->Limg * H, st);
     stats.kernel_launches++;
     cudaEventRecord(ctx->ev_comp[yb], st);
@@ -1771,10 +1787,10 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
   // scatter; compacted copies touch only unmasked rows and are awaited right before attention
   const bool late_wait = ctx->o.copy_mode != 0 && !record;
   auto wait_copy = [&](int buf) {
-    if ((any_cache || record) && !late_wait) cudaStreamWaitEvent(st, ctx->ev_copy[buf], 0);
+    if ((any_cache || record) && !late_wait) stream_wait(ctx, st, ctx->ev_copy[buf]);
   };
   auto wait_copy_late = [&](int buf) {
-    if (any_cache && late_wait) cudaStreamWaitEvent(st, ctx->ev_copy[buf], 0);
+    if (any_cache && late_wait) stream_wait(ctx, st, ctx->ev_copy[buf]);
   };
 
   // ---- UNet BasicTransformerBlock (config 5; oracle/unet.py unet_block_masked) ----
@@ -1789,7 +1805,7 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
     stats.kernel_launches++;
   };
   auto ln_aff_y = [&](int b, int buf) {  // Y block: LN1 of the unmasked rows from the staged Y_{b-1}
-    cudaStreamWaitEvent(st, ctx->ev_copy[buf], 0);
+    stream_wait(ctx, st, ctx->ev_copy[buf]);
     ProfScope ps(ctx, st, IG_K_LNMOD, 0.0, (double)uy[b] * H * (es + es));
     launch_ln_mod_staged<T>(ctx->kv_arena, ctx->slot_stride, (long long)buf * ctx->buf_elems, ctx->L, H, M, M + uy[b],
                             ctx->ri, ctx->unet_ln + (size_t)b * 3 * 2 * H, 0, 0, H, ctx->d.ln_eps, h, H, st);
@@ -1974,6 +1990,7 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
   if (record)
     CUDA_TRY(cudaStreamWaitEvent(st, record->y && blk_yrec(record->ymode, b1 - 1) ? ctx->ev_yrec[(b1 - 1) % R]
                                                                                  : ctx->ev_copy[(b1 - 1) % R], 0));
+  ctx->pdl_block = true;
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_err(IG_ECUDA, "step enqueue: %s", cudaGetErrorString(e));
   stats.host_ns = std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - t_host0).count();

@@ -111,6 +111,7 @@ template <int D>
 __global__ void __launch_bounds__(NTHREADS, 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmKV,
                    const AttnArgs a, float scale_log2) {
+  asm volatile("griddepcontrol.launch_dependents;");  // let a PDL GEMM (out-projection) stage its prologue
   using C = AC<D>;
   constexpr int Q_BYTES = C::Q_BYTES, KV_BYTES = C::KV_BYTES, TS = C::TSTRIDE;
   // compact grid: blockIdx.x enumerates the (segment, query-tile pair) work items, decoded

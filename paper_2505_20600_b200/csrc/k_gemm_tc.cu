@@ -314,11 +314,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
     tc::fence_barrier_init();
   }
+  asm volatile("griddepcontrol.launch_dependents;");
   if (warp == 1) tc::tmem_alloc<C::TMEM_COLS>(tmem_slot);
   tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // PDL: inputs of the previous kernel visible
 
   if (warp == 0) {
     if (lane == 0) {  // ===== TMA producer =====
@@ -484,11 +486,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     }
     tc::fence_barrier_init();
   }
+  asm volatile("griddepcontrol.launch_dependents;");
   if (warp == 1) tc::tmem_alloc2<C::TMEM_COLS>(tmem_slot);
   tc::tc_fence_before();
   tc::cluster_sync();
   tc::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // PDL: inputs of the previous kernel visible
 
   if (warp == 0) {
     if (lane == 0) {  // ===== TMA producer (both CTAs) =====
@@ -716,8 +720,18 @@ void launch_gemm_tc(const GemmArgs& g, cudaStream_t st) {
     const int num_m = (g.M + 255) / 256, num_n = (g.N + 255) / 256;
     const int tiles = num_m * num_n;
     const int clusters = tiles < g_num_sms / 2 ? tiles : g_num_sms / 2;
-    gemm_tc2_kernel<<<2 * clusters, NUM_THREADS, Cfg2::SMEM, st>>>(ta, tb, g, num_m, num_n,
-                                                                   raster_group(num_m, 256, g.K));
+    const int G2 = raster_group(num_m, 256, g.K);
+    if (g.pdl) {
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = dim3(2 * clusters); cfg.blockDim = dim3(NUM_THREADS); cfg.dynamicSmemBytes = Cfg2::SMEM; cfg.stream = st;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      at[0].val.programmaticStreamSerializationAllowed = 1;
+      cfg.attrs = at; cfg.numAttrs = 1;
+      cudaLaunchKernelEx(&cfg, gemm_tc2_kernel, ta, tb, g, num_m, num_n, G2);
+    } else {
+      gemm_tc2_kernel<<<2 * clusters, NUM_THREADS, Cfg2::SMEM, st>>>(ta, tb, g, num_m, num_n, G2);
+    }
     return;
   }
   const int BN = wide ? 256 : 128;
@@ -728,8 +742,19 @@ void launch_gemm_tc(const GemmArgs& g, cudaStream_t st) {
   const int tiles = num_m * num_n;
   const int grid = tiles < g_num_sms ? tiles : g_num_sms;
   const int G = raster_group(num_m, BM, g.K);
-  if (wide) gemm_tc_kernel<256><<<grid, NUM_THREADS, Cfg<256>::SMEM, st>>>(ta, tb, g, num_m, num_n, G);
-  else gemm_tc_kernel<128><<<grid, NUM_THREADS, Cfg<128>::SMEM, st>>>(ta, tb, g, num_m, num_n, G);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid); cfg.blockDim = dim3(NUM_THREADS); cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at; cfg.numAttrs = g.pdl ? 1 : 0;
+  if (wide) {
+    cfg.dynamicSmemBytes = Cfg<256>::SMEM;
+    cudaLaunchKernelEx(&cfg, gemm_tc_kernel<256>, ta, tb, g, num_m, num_n, G);
+  } else {
+    cfg.dynamicSmemBytes = Cfg<128>::SMEM;
+    cudaLaunchKernelEx(&cfg, gemm_tc_kernel<128>, ta, tb, g, num_m, num_n, G);
+  }
 }
 
 }  // namespace ig

@@ -179,6 +179,7 @@ __global__ void __launch_bounds__(LN_THREADS) ln_mod_kernel(const float* __restr
                                                             int shift_off, int scale_off, float eps,
                                                             T* __restrict__ h, int ldh) {
   __shared__ float red[LN_THREADS / 32];
+  asm volatile("griddepcontrol.launch_dependents;");  // let a PDL GEMM stage its prologue
   const int r = r0 + blockIdx.x;
   const float* x = X + (long long)r * H;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -257,6 +258,7 @@ __global__ void __launch_bounds__(LN_THREADS) ln_mod_staged_kernel(const T* __re
                                                                    int shift_off, int scale_off, float eps,
                                                                    T* __restrict__ h, int ldh) {
   __shared__ float red[LN_THREADS / 32];
+  asm volatile("griddepcontrol.launch_dependents;");  // let a PDL GEMM stage its prologue
   const int r = r0 + blockIdx.x;
   const RowInfo info = ri[r];
   const T* x = arena + info.slot * slot_stride + buf_off + L * H + (long long)info.kvpos * H;

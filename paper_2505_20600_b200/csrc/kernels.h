@@ -186,6 +186,10 @@ struct GemmArgs {
   int out_f32;                           // EPI_STORE/GELU: 1 => C is fp32
   int precise_gelu;                      // 1 => tanhf instead of MUFU tanh.approx (debug)
   QkvEpi qkv;                            // EPI_QKV only
+  int pdl;                               // 1: programmatic dependent launch (the prologue — barrier
+                                         // init, TMEM alloc, descriptor prefetch — overlaps the
+                                         // previous kernel's tail; griddepcontrol.wait before any
+                                         // global read); only right after another kernel
 };
 template <typename T>
 void launch_gemm_simt(const GemmArgs& g, cudaStream_t st);
