@@ -287,3 +287,23 @@ def test_planned_step_pins():
             out = oracle.unet_edit_step_planned(D, W, states[0], mask, states[0], ctx, k, kv_cache_step=kv[0],
                                                 y_cache_step=ys[0], y_blocks=yb)
             np.testing.assert_allclose(out[m], states[1][m], rtol=1e-12, atol=1e-12)
+
+
+def test_sweep_flop_model_matches_oracle_macs():
+    """tools/unet_sweep.py's algorithmic FLOPs (the config-5 roofline numerator) equal twice the
+    oracle's counted multiply-accumulates of the same step."""
+    import importlib.util
+    import os
+    spec = importlib.util.spec_from_file_location(
+        "unet_sweep", os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools", "unet_sweep.py"))
+    sw = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(sw)
+    W = _weights()
+    ctx = _ctx()
+    cache = synth.make_cache_kv(D, 3, 1).double().numpy()[0]
+    masks = [synth.rect_mask_count(D, 40, np.random.default_rng(0)), synth.blob_mask_count(D, 25, np.random.default_rng(1))]
+    oracle.reset_macs()
+    for mk in masks:
+        oracle.unet_edit_step(D, W, _state(), mk, cache, ctx)
+    macs = oracle.MACS["linear"] + oracle.MACS["attn"]
+    assert sw.step_flops(D, 65, 2) == 2 * macs
