@@ -712,7 +712,14 @@ void gemm_tc_init() { init_driver(); }
 void launch_gemm_tc(const GemmArgs& g, cudaStream_t st) {
   if (g.M <= 0 || g.N <= 0) return;
   init_driver();
-  const bool wide = g.N > 128 || g.epi == EPI_QKV || g.epi == EPI_GEGLU;
+  bool wide = g.N > 128 || g.epi == EPI_QKV || g.epi == EPI_GEGLU;
+  // Small problems (fewer 256 x 256 tiles than a quarter of the SMs, e.g. the single-request
+  // or low-mask-ratio GEMMs): 128 x 128 one-CTA tiles put 4x as many SMs to work.  Only the
+  // tile shape changes — every output is still one full-K accumulation in the same K order —
+  // so results do not depend on the choice (batch invariance holds).
+  static const bool no_small = getenv("IG_GEMM_NO_SMALL") != nullptr;  // A/B switch
+  const long long tiles2 = (long long)((g.M + 255) / 256) * ((g.N + 255) / 256);
+  if (!no_small && wide && g.epi != EPI_GEGLU && tiles2 * 4 < g_num_sms) wide = false;
   if (wide && g_two_cta && g.M > 128) {  // 2-CTA 256 x 256 tiles
     CUtensorMap ta, tb;
     make_tmap(&ta, g.A, g.M, g.K, g.lda, 128);
