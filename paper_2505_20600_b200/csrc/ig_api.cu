@@ -155,6 +155,11 @@ struct ig_ctx {
   RowInfo* ri_c = nullptr;
   void* u2 = nullptr;
   void* geglu_tc = nullptr;
+  // bf16: the next block's cross K/V GEMM runs on a side stream while the current block's
+  // self-attention chain (small-M GEMMs that leave SMs idle) runs on the compute stream; the
+  // cross arena is double-buffered by block parity
+  cudaStream_t xs = nullptr;
+  cudaEvent_t ev_xfork = nullptr, ev_xkv[2] = {}, ev_xuse[2] = {};
   std::vector<ModT> mods;
   long long mod_ld = 0;
   int fmod_t = -1;
@@ -320,6 +325,15 @@ static void gemm(ig_ctx* ctx, const GemmArgs& g, cudaStream_t st) {
   ctx->pdl_block = false;
   if (ctx->d.dtype == IG_F32) launch_gemm_simt<float>(g, st);
   else if (g_tc_gemm && gemm_tc_supported(g)) launch_gemm_tc(g2, st);
+  else launch_gemm_simt<bf16>(g, st);
+}
+
+// a launch on a side stream: never programmatic, leaves the compute stream's PDL state alone
+static void gemm_side(ig_ctx* ctx, const GemmArgs& g, cudaStream_t st) {
+  if (g.M <= 0 || g.N <= 0) return;
+  ctx->stats.kernel_launches++;
+  ProfScope ps(ctx, st, IG_K_GEMM, 2.0 * g.M * g.N * g.K, 0.0, g.M, g.N, g.K, g.epi);
+  if (g_tc_gemm && gemm_tc_supported(g)) launch_gemm_tc(g, st);
   else launch_gemm_simt<bf16>(g, st);
 }
 
@@ -527,7 +541,7 @@ extern "C" ig_status ig_ctx_create(const ig_model_desc* desc, const void* const*
     const int nbu = desc->n_unet, Lc = desc->ctx_len, Dc = desc->ctx_dim;
     okm &= dmalloc((void**)&ctx->unet_ln, (size_t)nbu * 3 * 2 * H * 4);
     okm &= dmalloc((void**)&ctx->ones, (size_t)H * 4);
-    okm &= dmalloc(&ctx->xkv, (size_t)B * 2 * Lc * H * es);
+    okm &= dmalloc(&ctx->xkv, (size_t)2 * B * 2 * Lc * H * es);  // two block-parity halves
     okm &= dmalloc(&ctx->ctxp, (size_t)B * Lc * Dc * es);
     okm &= dmalloc((void**)&ctx->ri_c, (size_t)B * Lc * sizeof(RowInfo));
     okm &= dmalloc(&ctx->u2, (size_t)Mx * 2 * F * es);
@@ -551,6 +565,12 @@ extern "C" ig_status ig_ctx_create(const ig_model_desc* desc, const void* const*
       }
     }
     CUDA_TRY(cudaMemcpy(ctx->unet_ln, lnh.data(), lnh.size() * 4, cudaMemcpyHostToDevice));
+    cudaStreamCreateWithFlags(&ctx->xs, cudaStreamNonBlocking);
+    cudaEventCreateWithFlags(&ctx->ev_xfork, cudaEventDisableTiming);
+    for (int i = 0; i < 2; ++i) {
+      cudaEventCreateWithFlags(&ctx->ev_xkv[i], cudaEventDisableTiming);
+      cudaEventCreateWithFlags(&ctx->ev_xuse[i], cudaEventDisableTiming);
+    }
     CUDA_TRY(cudaMemcpy(ctx->ones, ones.data(), (size_t)H * 4, cudaMemcpyHostToDevice));
     std::vector<RowInfo> ric((size_t)B * Lc);
     for (int q = 0; q < B; ++q)
@@ -664,6 +684,12 @@ extern "C" void ig_ctx_destroy(ig_ctx* ctx) {
   if (ctx->ev_desc) cudaEventDestroy(ctx->ev_desc);
   if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
   if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
+  if (ctx->xs) cudaStreamDestroy(ctx->xs);
+  if (ctx->ev_xfork) cudaEventDestroy(ctx->ev_xfork);
+  for (int i = 0; i < 2; ++i) {
+    if (ctx->ev_xkv[i]) cudaEventDestroy(ctx->ev_xkv[i]);
+    if (ctx->ev_xuse[i]) cudaEventDestroy(ctx->ev_xuse[i]);
+  }
   for (auto& g : ctx->graphs) cudaGraphExecDestroy(g.second.exec);
   for (auto& r : ctx->prof_recs) { ctx->ev_pool.push_back(r.a); ctx->ev_pool.push_back(r.b); }
   for (auto e : ctx->ev_pool) cudaEventDestroy(e);
@@ -1811,17 +1837,35 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
                             ctx->ri, ctx->unet_ln + (size_t)b * 3 * 2 * H, 0, 0, H, ctx->d.ln_eps, h, H, st);
     stats.kernel_launches++;
   };
+  // fused (bf16) path: block b's cross K/V live in arena half b % 2 and are produced on the side
+  // stream one block ahead (xover); parity mode: half 0, on the compute stream
+  static const bool no_xover = getenv("IG_NO_XOVERLAP") != nullptr;  // A/B switch
+  const bool xover = unet && fused_qkv && !no_xover;
+  const long long xhalf = (long long)ctx->o.max_batch * 2 * Lc * H;  // elements per arena half
+  auto xkv_of = [&](int b) { return (char*)ctx->xkv + (xover ? (long long)(b & 1) * xhalf * es : 0); };
+  auto cross_kv_on = [&](const UnetW& u, int b, cudaStream_t s2) {
+    const int Mc = na * Lc;
+    GemmArgs g{};
+    g.A = ctx->ctxp; g.lda = Dc; g.B = u.kv2.w; g.ldb = Dc; g.bias = nullptr;
+    g.C = ctx->Q; g.ldc = H; g.M = Mc; g.N = 2 * H; g.K = Dc; g.epi = EPI_QKV;
+    g.ri = ctx->ri_c; g.ri_off = 0;
+    QkvEpi& e = g.qkv;
+    e.Q = ctx->Q; e.kv_arena = xkv_of(b); e.slot_stride = 2LL * Lc * H; e.buf_off = 0; e.L = Lc; e.H = H;
+    e.head_dim = ctx->d.head_dim; e.col_base = H;
+    if (s2 == st) gemm(ctx, g, st);
+    else gemm_side(ctx, g, s2);
+  };
+  // side stream: produce block b's cross K/V (after block b - 2's cross-attention released the half)
+  auto xissue = [&](int b) {
+    if (b >= b1) return;
+    if (b >= b0 + 2) cudaStreamWaitEvent(ctx->xs, ctx->ev_xuse[b & 1], 0);
+    cross_kv_on(ctx->unet[b], b, ctx->xs);
+    cudaEventRecord(ctx->ev_xkv[b & 1], ctx->xs);
+  };
   auto cross_kv = [&](const UnetW& u) {  // context rows -> K/V planes of the cross arena
     const int Mc = na * Lc;
     if (fused_qkv) {
-      GemmArgs g{};
-      g.A = ctx->ctxp; g.lda = Dc; g.B = u.kv2.w; g.ldb = Dc; g.bias = nullptr;
-      g.C = ctx->Q; g.ldc = H; g.M = Mc; g.N = 2 * H; g.K = Dc; g.epi = EPI_QKV;
-      g.ri = ctx->ri_c; g.ri_off = 0;
-      QkvEpi& e = g.qkv;
-      e.Q = ctx->Q; e.kv_arena = ctx->xkv; e.slot_stride = 2LL * Lc * H; e.buf_off = 0; e.L = Lc; e.H = H;
-      e.head_dim = ctx->d.head_dim; e.col_base = H;
-      gemm(ctx, g, st);
+      cross_kv_on(u, 0, st);
     } else {  // parity mode: K/V GEMM into the [q|k|v] scratch, then the positional write
       GemmArgs g{};
       g.A = ctx->ctxp; g.lda = Dc; g.B = u.kv2.w; g.ldb = Dc;
@@ -1842,7 +1886,8 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
   auto unet_block = [&](int b, int buf, bool ys, int Mk, bool dense) {
     const UnetW& u = ctx->unet[b];
     const int Mc = dense ? M_full : M;
-    cross_kv(u);  // first: the parity path's positional write also stores (unused) Q rows
+    if (xover) xissue(b + 1);  // next block's cross K/V, concurrently with this block's chain
+    else cross_kv(u);  // parity path first: its positional write also stores (unused) Q rows
     ln_aff(b, 0, 0, dense ? M_full : (ys ? M : Mk));
     if (ys) ln_aff_y(b, buf);
     if (!dense) wait_copy(buf);
@@ -1862,13 +1907,15 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
     ln_aff(b, 1, 0, Mc);
     gemm_rows(0, Mc, h, H, u.q2.w, nullptr, H, H, ctx->Q, H, EPI_STORE, nullptr, 0);
     {
+      if (xover) stream_wait(ctx, st, ctx->ev_xkv[b & 1]);
       AttnArgs a{};
-      a.Q = ctx->Q; a.ldq = H; a.O = cat; a.ldo = ldcat; a.kv_arena = ctx->xkv; a.kv_off = 0;
+      a.Q = ctx->Q; a.ldq = H; a.O = cat; a.ldo = ldcat; a.kv_arena = xkv_of(b); a.kv_off = 0;
       a.segs = dense ? dsegcf : dsegc; a.nseg = dense ? nsegcf : nsegc; a.max_qlen = dense ? max_qcf : max_q;
       a.n_pairs = dense ? npaircf : npair; a.q_rows = Mc;
       a.L = Lc; a.heads = ctx->d.heads; a.head_dim = ctx->d.head_dim;
       a.scale = 1.0f / sqrtf((float)ctx->d.head_dim);
       attention(ctx, a, st, 4.0 * (double)Mc * Lc * H);
+      if (xover) cudaEventRecord(ctx->ev_xuse[b & 1], st);
     }
     gemm_rows(0, Mc, cat, ldcat, u.out2.w, u.out2.b, H, H, ctx->X, H, EPI_GATED_RES, ctx->ones, 0);
     ln_aff(b, 2, 0, Mc);
@@ -1886,6 +1933,11 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
     gemm_rows(0, Mc, cat + H, ldcat, u.ff2.w, u.ff2.b, H, F, ctx->X, H, EPI_GATED_RES, ctx->ones, 0);
   };
 
+  if (xover && b0 < b1) {  // fork the side stream after the packed contexts exist
+    cudaEventRecord(ctx->ev_xfork, st);
+    cudaStreamWaitEvent(ctx->xs, ctx->ev_xfork, 0);
+    xissue(b0);
+  }
   // ---- blocks ----
   // Dense-prefix blocks (b < kplan) run every row [0, M_full) with their own K/V buffer (index
   // R, no cache); cached blocks run the masked rows [0, M) with ring buffer b % R.
