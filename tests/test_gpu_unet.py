@@ -349,3 +349,62 @@ def test_unet_dense_prefix(dtype, k):
         r.free()
     hyb.close()
     base.close()
+
+
+@pytest.mark.parametrize("kind", ["kv", "hybrid"])
+def test_unet_load_dedupe_bitwise(kind):
+    """Lockstep UNet requests on one (host-tier cache, step) share staged rows (load
+    deduplication): the batch equals each request alone bit for bit with fewer link bytes."""
+    from gpu_util import hybrid_planes
+    d = synth.UNET_SMALL
+    opts = ig.ig_ctx_opts(4, 0, 2, 1, 0, 0) if kind == "kv" else ig.ig_ctx_opts(4, 0, 2, 1, 0, 0, 1, 1)
+    m = Model(d, ig.IG_BF16, opts=opts)
+    rng = np.random.default_rng(61)
+    masks = [synth.blob_mask_count(d, 90, rng), synth.rect_mask_count(d, 40, rng), synth.blob_mask_count(d, 130, rng)]
+    alone = [Request(m, 290 + i, mk) for i, mk in enumerate(masks)]
+    batch = [Request(m, 290 + i, mk) for i, mk in enumerate(masks)]
+    kv = synth.make_cache_kv(d, 14, 2, dtype=torch.bfloat16)
+    tst = torch.stack([synth.make_latent(d, 996 + s) for s in range(2)])
+    cache = ig.ig_cache_create(m.ctx, 2, ig.IG_CACHE_HOST)
+    if kind == "kv":
+        fill_cache(m, cache, kv, tst)
+    else:
+        ym = set(ig.y_block_modes(d.n_blocks, 1))
+        fill_cache(m, cache, hybrid_planes(kv, synth.make_cache_y(d, 14, 2, dtype=torch.bfloat16), ym), tst)
+    h2d_alone = h2d_batch = 0
+    for s in range(2):
+        for i, r in enumerate(alone):
+            ig.ig_edit_step(m.ctx, [r.req(i, cache, s, 0.0, 0.0)], 0)
+            h2d_alone += ig.ig_last_stats(m.ctx)["h2d_bytes"]
+    for s in range(2):
+        ig.ig_edit_step(m.ctx, [r.req(i, cache, s, 0.0, 0.0) for i, r in enumerate(batch)], 0)
+        h2d_batch += ig.ig_last_stats(m.ctx)["h2d_bytes"]
+    torch.cuda.synchronize()
+    for a, b in zip(alone, batch):
+        assert torch.equal(a.latent, b.latent)
+    assert h2d_batch < h2d_alone
+    ig.ig_cache_free(cache)
+    for r in alone + batch:
+        r.free()
+    m.close()
+
+
+def test_unet_zero_copy_gather_mode():
+    """copy_mode 2 (SM gather straight from pinned host memory) on a UNet context vs the oracle."""
+    d = synth.UNET_SMALL
+    m = Model(d, ig.IG_BF16, opts=ig.ig_ctx_opts(4, 0, 2, 2, 0, 0))
+    W = m.host_weights()
+    rng = np.random.default_rng(71)
+    reqs = [Request(m, 300 + i, mk) for i, mk in enumerate([synth.blob_mask_count(d, 77, rng), synth.rect_mask_count(d, 33, rng)])]
+    kv = synth.make_cache_kv(d, 15, 2, dtype=torch.bfloat16)
+    cache = ig.ig_cache_create(m.ctx, 2, ig.IG_CACHE_HOST)
+    fill_cache(m, cache, kv)
+    _steps(m, reqs, cache, 2)
+    for r in reqs:
+        want = _oracle_steps(d, W, r, kv.double().numpy(), 2)
+        ok, worst = ctol(r.latent.double().cpu().numpy(), want, 2e-2)
+        assert ok, worst
+    ig.ig_cache_free(cache)
+    for r in reqs:
+        r.free()
+    m.close()
