@@ -205,6 +205,7 @@ struct ig_ctx {
   // compute dtype, read by the D2H on the copy stream; ev_yrec guards its reuse (WAR)
   void* yrec = nullptr;
   cudaEvent_t ev_yrec[MAXR] = {};
+  uint8_t* q8yrec = nullptr; float* q8yrec_scl = nullptr;  // FP8 Y recording: [R][2][plane] (+ scales)
   ig_stats stats{};
   std::vector<ig_cache*> zombies;
   // CUDA graphs of whole steps (ig_ctx_opts.use_graphs): keyed by everything that shapes the
@@ -434,7 +435,6 @@ extern "C" ig_status ig_ctx_create(const ig_model_desc* desc, const void* const*
   if (o.prefetch_depth + 1 > MAXR) return set_err(IG_EUNSUPPORTED, "prefetch_depth > %d", MAXR - 1);
   if (o.copy_mode < 0 || o.copy_mode > 2) return set_err(IG_EINVAL, "copy_mode must be 0, 1 or 2");
   if (o.cache_fp8 && desc->dtype != IG_BF16) return set_err(IG_EUNSUPPORTED, "FP8 caches need the bf16 mode");
-  if (o.cache_fp8 && o.cache_y) return set_err(IG_EUNSUPPORTED, "cache_y with cache_fp8 is not supported");
   const int Lall = desc->txt_len + desc->grid_h * desc->grid_w;
   if (o.max_rows <= 0) o.max_rows = o.max_batch * Lall;
   if (desc->n_unet > 0) {
@@ -627,6 +627,10 @@ extern "C" ig_status ig_ctx_create(const ig_model_desc* desc, const void* const*
     okm &= dmalloc((void**)&ctx->q8rec_scl, (size_t)ctx->R * 2 * spl * 4);
     if (!okm) { ig_ctx_destroy(ctx); return set_err(IG_ENOMEM, "fp8 staging allocation failed"); }
   }
+  if (o.cache_y && o.cache_fp8) {
+    okm &= dmalloc((void**)&ctx->q8yrec, (size_t)ctx->R * 2 * ctx->Limg * H);
+    okm &= dmalloc((void**)&ctx->q8yrec_scl, (size_t)ctx->R * 2 * ctx->Limg * desc->heads * 4);
+  }
   if (o.cache_y) {
     okm &= dmalloc(&ctx->yrec, (size_t)ctx->R * ctx->Limg * H * es);
     if (!okm) { ig_ctx_destroy(ctx); return set_err(IG_ENOMEM, "Y recording staging allocation failed"); }
@@ -669,7 +673,8 @@ extern "C" void ig_ctx_destroy(ig_ctx* ctx) {
                   ctx->qkv, ctx->Q, ctx->cat, ctx->Ain, ctx->ri, ctx->kv_arena, ctx->rope_tab,
                   ctx->gv_t1, ctx->gv_t2, ctx->gv_mod, ctx->modw, ctx->modb, ctx->svec_bf,
                   ctx->q8in, ctx->q8in_scl, ctx->q8rec, ctx->q8rec_scl, ctx->yrec, ctx->unet_ln,
-                  ctx->ones, ctx->xkv, ctx->ctxp, ctx->ri_c, ctx->u2, ctx->geglu_tc};
+                  ctx->ones, ctx->xkv, ctx->ctxp, ctx->ri_c, ctx->u2, ctx->geglu_tc,
+                  ctx->q8yrec, ctx->q8yrec_scl};
   for (void* b : bufs) if (b) cudaFree(b);
   for (int i = 0; i < NSTAGE; ++i) {
     if (ctx->h_stage[i]) cudaFreeHost(ctx->h_stage[i]);
@@ -849,7 +854,7 @@ static int step_planes(const std::vector<uint8_t>& m) {
   return n;
 }
 static size_t cache_kv_bytes(const ig_ctx* ctx, int n_steps, int fp8, const std::vector<uint8_t>& m) {
-  if (fp8) return (size_t)n_steps * ctx->nb * 2 * ctx->Limg * ((size_t)ctx->H + 4 * ctx->d.heads);
+  if (fp8) return (size_t)n_steps * step_planes(m) * ctx->Limg * ((size_t)ctx->H + 4 * ctx->d.heads);
   return (size_t)n_steps * step_planes(m) * ctx->Limg * ctx->H * ctx->esz;
 }
 static size_t cache_bytes(const ig_ctx* ctx, int n_steps, int fp8, const std::vector<uint8_t>& m) {
@@ -862,20 +867,22 @@ static const float* cache_latent_dev(const ig_ctx* ctx, const ig_cache* c, int s
   return (const float*)((const char*)c->dptr + ((char*)cache_latent(ctx, c, step) - (char*)c->ptr));
 }
 // data plane (which = 0 K, 1 V, 2 Y) of (step, block) and its scale plane (fp8 caches)
-static char* cache_plane(const ig_ctx* ctx, const ig_cache* c, int step, int b, int which) {
-  const size_t row = c->fp8 ? (size_t)ctx->H : (size_t)ctx->H * ctx->esz;
-  if (!c->y) return (char*)c->ptr + (((size_t)step * ctx->nb + b) * 2 + which) * ctx->Limg * row;
+static size_t plane_index(const ig_ctx* ctx, const ig_cache* c, int step, int b, int which) {
+  if (!c->y) return ((size_t)step * ctx->nb + b) * 2 + which;
   size_t idx = (size_t)step * c->step_planes;
   for (int bb = 0; bb < b; ++bb) idx += planes_of(c->ymode, bb);
   if (which == 2) idx += blk_kv(c->ymode, b) ? 2 : 0;
   else idx += which;
-  return (char*)c->ptr + idx * ctx->Limg * row;
+  return idx;
+}
+static char* cache_plane(const ig_ctx* ctx, const ig_cache* c, int step, int b, int which) {
+  const size_t row = c->fp8 ? (size_t)ctx->H : (size_t)ctx->H * ctx->esz;
+  return (char*)c->ptr + plane_index(ctx, c, step, b, which) * ctx->Limg * row;
 }
 // block b of a request on cache c runs as a Y block (unmasked rows replenished, K/V recomputed)
 static inline bool y_block(const ig_cache* c, int b) { return c && c->y && c->ymode[b]; }
 static float* cache_scales(const ig_ctx* ctx, const ig_cache* c, int step, int b, int which) {
-  return (float*)((char*)c->ptr + c->scale_off +
-                  (((size_t)step * ctx->nb + b) * 2 + which) * ctx->Limg * ctx->d.heads * 4);
+  return (float*)((char*)c->ptr + c->scale_off + plane_index(ctx, c, step, b, which) * ctx->Limg * ctx->d.heads * 4);
 }
 static const char* cache_plane_dev(const ig_ctx* ctx, const ig_cache* c, int step, int b, int which) {
   return (const char*)c->dptr + (cache_plane(ctx, c, step, b, which) - (char*)c->ptr);
@@ -906,7 +913,7 @@ static ig_status cache_create_kind(ig_ctx* ctx, int n_steps, int tier, int fp8, 
   c->ymode = y_modes(ctx->nb, y, c->kv_blocks);
   c->step_planes = step_planes(c->ymode);
   c->bytes = cache_bytes(ctx, n_steps, c->fp8, c->ymode);
-  if (c->fp8) c->scale_off = (size_t)n_steps * ctx->nb * 2 * ctx->Limg * ctx->H;
+  if (c->fp8) c->scale_off = (size_t)n_steps * c->step_planes * ctx->Limg * ctx->H;
   c->lat_off = cache_kv_bytes(ctx, n_steps, c->fp8, c->ymode);
   cudaError_t e;
   if (tier == IG_CACHE_HOST) {
@@ -933,7 +940,6 @@ extern "C" ig_status ig_cache_clone(ig_ctx* ctx, const ig_cache* src, int tier, 
   if (!desc_equal(src->desc, ctx->d)) return set_err(IG_ECACHE_INCOMPAT, "cache built for another model");
   const bool quantize = ctx->o.cache_fp8 && !src->fp8;  // bf16 -> fp8 conversion
   if (!ctx->o.cache_fp8 && src->fp8) return set_err(IG_EUNSUPPORTED, "cannot clone an fp8 cache into bf16");
-  if (quantize && src->y) return set_err(IG_EUNSUPPORTED, "FP8 Y caches are not supported");
   CUDA_TRY(cudaSetDevice(ctx->device));
   ig_cache* c = nullptr;
   ig_status s = cache_create_kind(ctx, src->n_steps, tier, quantize ? 1 : src->fp8, src->y, src->kv_blocks, &c);
@@ -941,6 +947,24 @@ extern "C" ig_status ig_cache_clone(ig_ctx* ctx, const ig_cache* src, int tier, 
   cudaError_t e = cudaSuccess;
   if (!quantize) {
     e = cudaMemcpy(c->ptr, src->ptr, src->bytes, cudaMemcpyDefault);
+  } else if (src->y) {  // Y / hybrid: every plane in storage order -> quantize -> destination
+    const size_t pl = (size_t)ctx->Limg * ctx->H, spl = (size_t)ctx->Limg * ctx->d.heads;
+    void* tmp = nullptr;
+    e = cudaMalloc(&tmp, pl * 2);
+    const size_t np = (size_t)src->n_steps * src->step_planes;
+    for (size_t i = 0; i < np && e == cudaSuccess; ++i) {
+      e = cudaMemcpy(tmp, (const char*)src->ptr + i * pl * 2, pl * 2, cudaMemcpyDefault);
+      if (e != cudaSuccess) break;
+      launch_kv_quant((const bf16*)tmp, (const bf16*)tmp, ctx->Limg, ctx->H, ctx->d.heads, ctx->q8rec, ctx->q8rec + pl,
+                      ctx->q8rec_scl, ctx->q8rec_scl + spl, 0);
+      e = cudaMemcpy((char*)c->ptr + i * pl, ctx->q8rec, pl, cudaMemcpyDefault);
+      if (e == cudaSuccess)
+        e = cudaMemcpy((char*)c->ptr + c->scale_off + i * spl * 4, ctx->q8rec_scl, spl * 4, cudaMemcpyDefault);
+    }
+    if (tmp) cudaFree(tmp);
+    if (e == cudaSuccess)
+      e = cudaMemcpy(cache_latent(ctx, c, 0), cache_latent(ctx, src, 0), (size_t)src->n_steps * ctx->Limg * ctx->C * 4,
+                     cudaMemcpyDefault);
   } else {  // per (step, block): bf16 planes -> device temp -> quantize -> destination
     const size_t pl = (size_t)ctx->Limg * ctx->H, spl = (size_t)ctx->Limg * ctx->d.heads;
     void* tmp = nullptr;
@@ -977,7 +1001,18 @@ extern "C" ig_status ig_cache_write(ig_ctx* ctx, ig_cache* c, const void* kv, co
   if (!c->fp8) {  // the caller's buffer is the storage layout of every step: one copy
     CUDA_TRY(cudaMemcpyAsync(c->ptr, kv, c->lat_off, cudaMemcpyDefault, st));
   }
-  for (int s = 0; s < c->n_steps && c->fp8; ++s)
+  if (c->fp8 && c->y) {  // Y / hybrid: the caller's planes in storage order, one by one
+    const size_t np = (size_t)c->n_steps * c->step_planes;
+    for (size_t i = 0; i < np; ++i) {
+      const bf16* src = (const bf16*)((const char*)kv + i * pl * ctx->esz);
+      launch_kv_quant(src, src, ctx->Limg, ctx->H, ctx->d.heads, ctx->q8rec, ctx->q8rec + pl, ctx->q8rec_scl,
+                      ctx->q8rec_scl + spl, st);
+      CUDA_TRY(cudaMemcpyAsync((char*)c->ptr + i * pl, ctx->q8rec, pl, cudaMemcpyDefault, st));
+      CUDA_TRY(cudaMemcpyAsync((char*)c->ptr + c->scale_off + i * spl * 4, ctx->q8rec_scl, spl * 4, cudaMemcpyDefault, st));
+      CUDA_TRY(cudaStreamSynchronize(st));
+    }
+  }
+  for (int s = 0; s < c->n_steps && c->fp8 && !c->y; ++s)
     for (int b = 0; b < ctx->nb; ++b) {
       const char* src = (const char*)kv + (((size_t)s * ctx->nb + b) * 2) * pl * ctx->esz;
       {
@@ -1073,6 +1108,27 @@ static void issue_copy(ig_ctx* ctx, const std::vector<StepReq>& sr, const KvGath
     const int slot = r->slot;
     const int n_u = ctx->Limg - sr[q].m->n_m;
     long long by = 0;
+    if (y_block(c, b) && c->fp8) {  // FP8 Y block: Y_{b-1} e4m3 runs + scales -> staging V half
+      if (b <= plan.kplan) continue;
+      if (host) {
+        const size_t pl = (size_t)ctx->Limg * ctx->H, spl = (size_t)ctx->Limg * ctx->d.heads * 4;
+        uint8_t* sd = ctx->q8in + ((size_t)slot * ctx->R + buf) * 2 * pl + pl;
+        char* ss = (char*)ctx->q8in_scl + ((size_t)slot * ctx->R + buf) * 2 * spl + spl;
+        const char* src = cache_plane(ctx, c, r->step, b - 1, 2);
+        for (auto& run : sr[q].m->runs) {
+          dsts.push_back(sd + (size_t)run.first * ctx->H);
+          srcs.push_back((void*)(src + (size_t)run.first * ctx->H));
+          sizes.push_back((size_t)run.second * ctx->H);
+        }
+        dsts.push_back(ss);
+        srcs.push_back((void*)cache_scales(ctx, c, r->step, b - 1, 2));
+        sizes.push_back(spl);
+        ctx->stats.h2d_bytes += (long long)n_u * ctx->H + (long long)spl;
+      } else {
+        ctx->stats.d2d_bytes += (long long)n_u * (ctx->H + 4 * ctx->d.heads);
+      }
+      continue;
+    }
     if (y_block(c, b)) {  // Y block: the template's Y_{b-1} rows of the unmasked tokens -> V plane
       if (b <= plan.kplan) continue;  // block 0 / first block after the prefix: computed rows
       const char* src = cache_plane(ctx, c, r->step, b - 1, 2);
@@ -1211,7 +1267,7 @@ static int plan_prefix(ig_ctx* ctx, const std::vector<StepReq>& sr, const std::v
     const long long n_load = n_u - dshared[&s - &sr[0]];  // deduplicated rows cross the link once
     for (int b = 0; b < N; ++b) {
       if (y_block(c, b)) {  // one plane; the K/V projection of the unmasked rows is recomputed
-        if (b > 0) bytes[b] += n_load * ctx->H * (long long)ctx->esz;
+        if (b > 0) bytes[b] += c->fp8 ? n_u * (ctx->H + 4LL * ctx->d.heads) : n_load * ctx->H * (long long)ctx->esz;
         rows_y[b] += n_u;
       } else {
         bytes[b] += c->fp8 ? 2LL * n_u * (ctx->H + 4 * ctx->d.heads) : 2LL * n_load * ctx->H * (long long)ctx->esz;
@@ -1500,7 +1556,23 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
           const ig_cache* c = r->cache;
           char* dst = (char*)ctx->kv_arena + ((size_t)r->slot * ctx->slot_stride + (size_t)(b % R) * ctx->buf_elems) * es;
           const int n_u = ctx->Limg - sr[q].m->n_m;
-          if (c->fp8) {
+          if (c->fp8 && y_block(c, b)) {  // V plane only: dequantize Y_{b-1} rows (after the prefix)
+            if (b > kplan) {
+              gq.idx_u = sr[q].m->idx + ctx->Limg;
+              gq.n_u = n_u;
+              gq.srcK = nullptr;
+              gq.dstV = dst + (size_t)ctx->L * H * es;
+              if (c->tier == IG_CACHE_HOST) {
+                const size_t pl = (size_t)ctx->Limg * H, spl = (size_t)ctx->Limg * ctx->d.heads;
+                const size_t sb = (size_t)r->slot * R + (b % R);
+                gq.srcV = ctx->q8in + sb * 2 * pl + pl;
+                gq.sclV = ctx->q8in_scl + sb * 2 * spl + spl;
+              } else {
+                gq.srcV = cache_plane_dev(ctx, c, r->step, b - 1, 2);
+                gq.sclV = cache_scales_dev(ctx, c, r->step, b - 1, 2);
+              }
+            }
+          } else if (c->fp8) {
             gq.idx_u = sr[q].m->idx + ctx->Limg;
             gq.n_u = n_u;
             gq.dstK = dst;
@@ -1760,6 +1832,21 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
     stream_wait(ctx, st, ctx->ev_yrec[yb]);  // the D2H of block b - R is done
     launch_rows_to<T>(ctx->X + (long long)M_txt * H, ys, (long long)ctx->Limg * H, st);
     stats.kernel_launches++;
+    if (record->fp8) {  // quantize per (token, head) into the FP8 Y staging, then D2H data + scales
+      const size_t pl = (size_t)ctx->Limg * H, spl = (size_t)ctx->Limg * ctx->d.heads;
+      uint8_t* qd = ctx->q8yrec + (size_t)yb * 2 * pl;
+      float* qs = ctx->q8yrec_scl + (size_t)yb * 2 * spl;
+      launch_kv_quant((const bf16*)ys, (const bf16*)ys, ctx->Limg, H, ctx->d.heads, qd, qd + pl, qs, qs + spl, st);
+      stats.kernel_launches++;
+      cudaEventRecord(ctx->ev_comp[yb], st);
+      cudaStreamWaitEvent(ctx->copy_st, ctx->ev_comp[yb], 0);
+      cudaMemcpyAsync(cache_plane(ctx, record, record_step, b, 2), qd, pl, cudaMemcpyDefault, ctx->copy_st);
+      cudaMemcpyAsync(cache_scales(ctx, record, record_step, b, 2), qs, spl * 4, cudaMemcpyDefault, ctx->copy_st);
+      const long long by = (long long)(pl + spl * 4);
+      if (record->tier == IG_CACHE_HOST) stats.d2h_bytes += by; else stats.d2d_bytes += by;
+      cudaEventRecord(ctx->ev_yrec[yb], ctx->copy_st);
+      return;
+    }
     cudaEventRecord(ctx->ev_comp[yb], st);
     cudaStreamWaitEvent(ctx->copy_st, ctx->ev_comp[yb], 0);
     cudaMemcpyAsync(cache_plane(ctx, record, record_step, b, 2), ys, plane, cudaMemcpyDefault, ctx->copy_st);

@@ -389,7 +389,7 @@ __global__ void __launch_bounds__(256) kv_gather_q8_kernel(const KvGatherReq* __
     const int rem = (int)(gw % per_req);
     const int which = rem & 1, j = rem >> 1;
     const KvGatherReq& R = reqs[q];
-    if (j >= R.n_u) continue;
+    if (j >= R.n_u || !(which ? R.srcV : R.srcK)) continue;  // (Y blocks: V plane only)
     const int tok = R.idx_u[j];
     const uint8_t* s = (const uint8_t*)(which ? R.srcV : R.srcK) + (long long)tok * H;
     const float* sc = (which ? R.sclV : R.sclK) + (long long)tok * heads;

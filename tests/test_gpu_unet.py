@@ -408,3 +408,72 @@ def test_unet_zero_copy_gather_mode():
     for r in reqs:
         r.free()
     m.close()
+
+
+@pytest.mark.parametrize("model,kv_blocks", [("unet_small", 0), ("unet_small", 1), ("flux_small", 2)])
+@pytest.mark.parametrize("tier", [ig.IG_CACHE_HOST, ig.IG_CACHE_DEVICE])
+def test_fp8_y_and_hybrid_caches(model, kv_blocks, tier):
+    """FP8 Y / hybrid caches (SURVEY N4 x N2): every plane (K, V and Y) stored as e4m3 with a
+    per (token, head) scale; the oracle mirrors the round trip of the same bf16 planes and runs
+    the Y-variant step (UNet and Flux-structured models), 2 requests, 2 steps."""
+    from gpu_util import hybrid_planes
+    d = synth.MODELS[model]
+    m = Model(d, ig.IG_BF16, opts=ig.ig_ctx_opts(4, 0, 2, 1, 0, 1, 1, kv_blocks))
+    W = m.host_weights()
+    rng = np.random.default_rng(81)
+    reqs = [Request(m, 310 + i, mk) for i, mk in enumerate([synth.blob_mask_count(d, 80, rng), synth.rect_mask_count(d, 36, rng)])]
+    kv = synth.make_cache_kv(d, 16, 2, dtype=torch.bfloat16)
+    yv = synth.make_cache_y(d, 16, 2, dtype=torch.bfloat16)
+    tst = torch.stack([synth.make_latent(d, 997 + s) for s in range(2)])
+    ym = set(ig.y_block_modes(d.n_blocks, kv_blocks))
+    cache = ig.ig_cache_create(m.ctx, 2, ig.IG_CACHE_HOST)
+    fill_cache(m, cache, hybrid_planes(kv, yv, ym), tst)
+    if tier == ig.IG_CACHE_DEVICE:
+        dc = ig.ig_cache_clone(m.ctx, cache, ig.IG_CACHE_DEVICE)
+        ig.ig_cache_free(cache)
+        cache = dc
+    kvq = oracle.fp8_kv_roundtrip(kv.float().numpy(), d.heads)
+    yq = oracle.fp8_kv_roundtrip(yv.float().numpy(), d.heads)
+    tsh = tst.double().numpy()
+    sig = [1.0, 0.7, 0.4]
+    for s in range(2):
+        ig.ig_edit_step(m.ctx, [r.req(i, cache, s, sig[s], sig[s + 1]) for i, r in enumerate(reqs)], 0)
+    torch.cuda.synchronize()
+    for r in reqs:
+        x = r.latent0.double().cpu().numpy()
+        for s in range(2):
+            if d.n_unet:
+                x = oracle.unet_edit_step_y(d, W, x, r.mask_np, yq[s], tsh[s], r.txt.double().cpu().numpy(),
+                                            y_blocks=ym, kv_cache_step=kvq[s])
+            else:
+                _, txt, cond = r.host_inputs()
+                x = oracle.edit_step_y(d, W, x, r.mask_np, yq[s], tsh[s], sig[s], sig[s + 1], txt, cond,
+                                       y_blocks=ym, kv_cache_step=kvq[s])
+        ok, worst = ctol(r.latent.double().cpu().numpy(), x, 2e-2)
+        assert ok, worst
+    ig.ig_cache_free(cache)
+    for r in reqs:
+        r.free()
+    m.close()
+
+
+def test_fp8_hybrid_template_recording_runs():
+    """ig_cache_template on an FP8 hybrid ctx records quantized K/V and Y planes; an edit from the
+    template's own state then stays close to the dense trajectory on the masked rows (FP8
+    rounding of the cached planes is the only difference)."""
+    d = synth.UNET_SMALL
+    m = Model(d, ig.IG_BF16, opts=ig.ig_ctx_opts(2, 0, 2, 1, 0, 1, 1, 1))
+    mask = synth.blob_mask_count(d, 70, np.random.default_rng(91))
+    rq = Request(m, 320, mask)
+    st = rq.latent.clone()
+    x0 = rq.latent.clone()
+    cache = ig.ig_cache_template(m.ctx, st.data_ptr(), rq.txt.data_ptr(), 0, [1.0, 0.5])
+    rr = ig.make_req(0, x0.data_ptr(), rq.mask, cache, 0, 0.0, 0.0, rq.txt.data_ptr(), None)
+    ig.ig_edit_step(m.ctx, [rr], 0)
+    torch.cuda.synchronize()
+    got, dense = x0.double().cpu().numpy(), st.double().cpu().numpy()
+    ok, worst = ctol(got[mask != 0], dense[mask != 0], 5e-2)
+    assert ok, worst
+    ig.ig_cache_free(cache)
+    rq.free()
+    m.close()
