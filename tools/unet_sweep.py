@@ -55,10 +55,13 @@ class Level:
         self.cache_steps = cache_steps
         if fp8:  # quantized on the device by ig_cache_write (per (token, head) scales)
             self.cache = ig.ig_cache_create(self.ctx, cache_steps, ig.IG_CACHE_HOST)
-            kv = torch.empty((cache_steps, d.n_blocks, 2, d.L_img, d.hidden), dtype=torch.bfloat16, device=dev)
+            ym = set(ig.y_block_modes(d.n_blocks, kv_blocks)) if y else set()
+            planes = sum((0 if b in ym else 2) + (1 if (b in ym or (b + 1) in ym) else 0) for b in range(d.n_blocks))
+            kv = torch.empty((cache_steps, planes, d.L_img, d.hidden), dtype=torch.bfloat16, device=dev)
             for s in range(cache_steps):
                 kv[s] = synth.normal(7000 + s, "cache_planes", tuple(kv.shape[1:]), dev).to(torch.bfloat16)
-            ig.ig_cache_write(self.ctx, self.cache, kv.data_ptr())
+            lat = synth.normal(7100, "cache_states", (cache_steps, d.L_img * d.hidden), dev).float()
+            ig.ig_cache_write(self.ctx, self.cache, kv.data_ptr(), lat.data_ptr())
             del kv
             if tier == ig.IG_CACHE_DEVICE:
                 dc = ig.ig_cache_clone(self.ctx, self.cache, tier)
@@ -113,7 +116,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=6)  # > NSTAGE: every staging slot's graph captured
     ap.add_argument("--tier", default="device", choices=["device", "host"])
     ap.add_argument("--cache-steps", type=int, default=8)
-    ap.add_argument("--cache", default="kv", choices=["kv", "y", "fp8"], help="K/V, Y (the paper's SDXL form) or FP8 K/V cache")
+    ap.add_argument("--cache", default="kv", choices=["kv", "y", "fp8", "fp8y"],
+                    help="K/V, Y (the paper's SDXL form), FP8 K/V or FP8 Y cache")
     ap.add_argument("--graphs", type=int, default=-1,
                     help="CUDA graphs of whole steps (default: on for the HBM tier; host-tier DMA sources change per step)")
     args = ap.parse_args()
@@ -121,8 +125,8 @@ def main():
     ig.lib()
     tier = ig.IG_CACHE_DEVICE if args.tier == "device" else ig.IG_CACHE_HOST
     graphs = (1 if args.tier == "device" else 0) if args.graphs < 0 else args.graphs
-    yc = 1 if args.cache == "y" else 0
-    f8 = 1 if args.cache == "fp8" else 0
+    yc = 1 if args.cache in ("y", "fp8y") else 0
+    f8 = 1 if args.cache in ("fp8", "fp8y") else 0
     lv = [Level(synth.SDXL_L64, args.batch, tier, args.cache_steps, dev, graphs, yc, 0, f8),
           Level(synth.SDXL_L32, args.batch, tier, args.cache_steps, dev, graphs, yc, 0, f8)]
     peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["bf16_tflops_sustained"] \
