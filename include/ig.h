@@ -110,7 +110,9 @@ typedef struct {
                        /*     OUTPUT rows of the image tokens [steps][blocks][L_img][H]    */
                        /*     (fig:transformer-Bottom): half the     */
                        /*     bytes of K/V; a step recomputes the unmasked tokens' K/V     */
-                       /*     from them (LN-mod + K/V projection).  Not with cache_fp8.    */
+                       /*     from them (LN-mod + K/V projection).  With cache_fp8 every   */
+                       /*     plane (K, V, Y) is e4m3 + per (token, head) scales, scale     */
+                       /*     planes in the same plane order after all data planes         */
   int cache_kv_blocks; /* with cache_y: hybrid cache — this many blocks keep K/V, the     */
                        /*     other N - cache_kv_blocks are Y blocks (0 = pure Y): the     */
                        /*     first N - kv_blocks entries of the bit-reversal order over   */
