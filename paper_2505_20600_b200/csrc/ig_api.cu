@@ -1703,18 +1703,17 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
   }
   }
   if (!unet) stats.kernel_launches += 7;
-  if (unet) {
-    // the masked rows of the level's hidden state are already in X (build_rows)
-  } else if (rng.X_in) {  // teacher-forced residual rows (+ img_in of the template rows, if any)
+  if (rng.X_in) {  // teacher-forced residual rows (+ img_in of the template rows, if any)
     CUDA_TRY(cudaMemcpyAsync(ctx->X, rng.X_in, (size_t)M * H * 4, cudaMemcpyDeviceToDevice, st));
-    if (M_full > M) {
+    if (M_full > M && !unet) {
       GemmArgs g{};
       g.A = (const char*)ctx->Ain + (long long)(M - M_txt) * C * es; g.lda = C; g.B = ctx->img_in.w; g.ldb = C;
       g.bias = ctx->img_in.b; g.C = ctx->X + (long long)M * H; g.ldc = H; g.M = M_full - M; g.N = H; g.K = C;
       g.epi = EPI_POS; g.ri = ctx->ri; g.ri_off = M; g.pos = ctx->pos_embed; g.pos_ld = H;
       gemm(ctx, g, st);
     }
-  } else {  // img_in (+ SD3 pos_embed) into the fp32 residual X
+  } else if (!unet) {  // img_in (+ SD3 pos_embed) into the fp32 residual X
+    // (UNet: the masked rows of the level's hidden state are already in X, build_rows)
     GemmArgs g{};
     g.A = ctx->Ain; g.lda = C; g.B = ctx->img_in.w; g.ldb = C; g.bias = ctx->img_in.b;
     g.C = ctx->X + (long long)M_txt * H; g.ldc = H; g.M = M_full - M_txt; g.N = H; g.K = C;
@@ -2089,12 +2088,12 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
     }
     record_y(b);
   }
-  if (unet) {  // exit: the stack's output rows back into the level's hidden state
+  if (rng.X_out) {
+    CUDA_TRY(cudaMemcpyAsync(rng.X_out, ctx->X, (size_t)M * H * 4, cudaMemcpyDeviceToDevice, st));
+  } else if (unet) {  // exit: the stack's output rows back into the level's hidden state
     ProfScope ps(ctx, st, IG_K_ROWS, 0.0, 2.0 * M * H * 4);
     launch_scatter_rows(dreq, M, ctx->ri, H, ctx->X, st);
     stats.kernel_launches++;
-  } else if (rng.X_out) {
-    CUDA_TRY(cudaMemcpyAsync(rng.X_out, ctx->X, (size_t)M * H * 4, cudaMemcpyDeviceToDevice, st));
   } else {
     // ---- a11: final layer + Euler scatter ----
     ln_mod(M_txt, M, ctx->fmod_t, 1, 0);  // final chunk order (scale, shift)

@@ -477,3 +477,40 @@ def test_fp8_hybrid_template_recording_runs():
     ig.ig_cache_free(cache)
     rq.free()
     m.close()
+
+
+@pytest.fixture(scope="module")
+def sdxl32():
+    """The full 32x32 SDXL level (60 blocks, C = 1280; 2.1 B bf16 parameters) in the launch
+    configuration tools/unet_sweep.py times (max_batch 8, prefetch depth 4, compacted copies)."""
+    m = Model(synth.SDXL_L32, ig.IG_BF16, opts=ig.ig_ctx_opts(8, 0, 4, 1, 0, 0))
+    yield m
+    m.close()
+
+
+@pytest.mark.parametrize("block,m_ratio", [(0, 0.05), (37, 0.2), (59, 0.6)])
+def test_sdxl32_teacher_forced_block(sdxl32, block, m_ratio):
+    """Full-size SDXL 32x32 blocks through ig_debug_block (teacher-forced input rows, K/V of the
+    unmasked rows from the cache) vs the oracle's unet_block_masked on the same inputs, compared
+    on the block's update (X_out - X_in) with C-TOL 2e-2."""
+    d = synth.SDXL_L32
+    mask = synth.blob_mask_count(d, round(m_ratio * d.L_img), np.random.default_rng(100 + block))
+    rq = Request(sdxl32, 400 + block, mask)
+    kv = synth.make_cache_kv(d, 17, 1, dtype=torch.bfloat16, device="cuda")
+    cache = ig.ig_cache_create(sdxl32.ctx, 1, ig.IG_CACHE_HOST)
+    fill_cache(sdxl32, cache, kv)
+    rows = rq.n_m
+    X_in = synth.normal(960 + block, "X_in_unet", (rows, d.hidden), "cuda").float()
+    X_out = torch.full_like(X_in, float("nan"))
+    ig.ig_debug_block(sdxl32.ctx, rq.req(0, cache, 0, 0.0, 0.0), block, X_in.data_ptr(), X_out.data_ptr())
+    torch.cuda.synchronize()
+    names = {nm for nm, _, _ in synth.weight_table(d) if nm.startswith(f"unet.{block}.")}
+    W = {k: sdxl32.W[k].double().cpu().numpy() for k in names}
+    idx_m, idx_u, _ = oracle.index_build(mask)
+    want, _, _ = oracle.unet_block_masked(d, W, block, X_in.double().cpu().numpy(), idx_m, idx_u,
+                                          kv[0, block].double().cpu().numpy(), rq.txt.double().cpu().numpy())
+    xin = X_in.double().cpu().numpy()
+    ok, worst = ctol(X_out.double().cpu().numpy() - xin, want - xin, 2e-2)
+    assert ok, worst
+    ig.ig_cache_free(cache)
+    rq.free()
