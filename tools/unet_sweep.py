@@ -7,9 +7,11 @@ Both attention levels of SDXL at 1024²: the 64x64 level (10 BasicTransformerBlo
 --batch requests, each with a 64-level mask of n = round(m * 4096) tokens (even ids
 rectangles, odd blobs) and its 32-level mask by 2x2 any-pool (paper_2505_20600_b200.levels).
 One "step" = one ig_edit_step on each level's context (the dense ResBlocks between them are
-outside this path, C-AMB 31).  The K/V cache holds --cache-steps distinct steps (cycled;
-~0.4 GB per step across both levels, larger than L2) in HBM (--tier device, default) or
-pinned host memory (--tier host).
+outside this path, C-AMB 31).  The cache holds --cache-steps (default 8) distinct steps, and
+the batch's requests sit at staggered steps of it (no two on one step: no load deduplication,
+as under continuous batching; ~0.4 GB of K/V per request-step across both levels, far larger
+than L2), in HBM (--tier device, default, replayed as CUDA graphs) or pinned host memory
+(--tier host); --cache kv | y | fp8 | fp8y picks the cache form.
 
     python tools/unet_sweep.py [--ratios 0.01,0.02,...] [--tier device|host] [--batch 8]
 
