@@ -13,9 +13,11 @@ extern "C" {
 /* a6/a9/a10 — C[M,N] = epi(A[M,K] B[N,K]^T + bias[N]) (kernel c).  dtype IG_BF16 runs the
  * tcgen05/TMEM/TMA tensor-core GEMM (fp32 accumulate), IG_F32 the CUDA-core FFMA GEMM.
  * A, B, bias have the given dtype; C is fp32 when out_f32 else dtype.  epi: 0 = store,
- * 1 = GELU-tanh (C-AMB 6).  Row-major with leading dimensions in elements.  IG_BF16
- * requires K % 64 == 0, N % 16 == 0, lda/ldb/ldc multiples of 8 and 16-byte aligned
- * pointers (IG_EUNSUPPORTED otherwise). */
+ * 1 = GELU-tanh (C-AMB 6), 5 = GEGLU (IG_BF16 only; UNet feed-forward, C-AMB 32): B and bias
+ * rows tile-interleaved — every group of 256 rows holds 128 "hidden" rows then their 128 "gate"
+ * rows — and C[M, N/2] (bf16) = hidden * GELU_erf(gate), N % 256 == 0.  Row-major with leading
+ * dimensions in elements.  IG_BF16 requires K % 64 == 0, N % 16 == 0, lda/ldb/ldc multiples
+ * of 8 and 16-byte aligned pointers (IG_EUNSUPPORTED otherwise). */
 ig_status ig_op_gemm(int dtype, const void* A, long long lda, const void* B, long long ldb,
                      const void* bias, void* C, long long ldc, int M, int N, int K, int epi,
                      int out_f32, void* stream);

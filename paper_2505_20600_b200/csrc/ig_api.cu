@@ -2244,7 +2244,8 @@ extern "C" ig_status ig_op_gemm(int dtype, const void* A, long long lda, const v
                                 int out_f32, void* stream) {
   if (!A || !B || !Cp) return set_err(IG_EINVAL, "NULL argument");
   if (M < 0 || N <= 0 || K <= 0) return set_err(IG_EINVAL, "bad shape");
-  if (epi != EPI_STORE && epi != EPI_GELU) return set_err(IG_EINVAL, "ig_op_gemm: epi must be 0 or 1");
+  if (epi != EPI_STORE && epi != EPI_GELU && !(epi == EPI_GEGLU && dtype == IG_BF16 && !out_f32))
+    return set_err(IG_EINVAL, "ig_op_gemm: epi must be 0 or 1 (or 5 = GEGLU, bf16 output)");
   GemmArgs g{};
   g.A = A; g.lda = lda; g.B = B; g.ldb = ldb; g.bias = bias; g.C = Cp; g.ldc = ldc;
   g.M = M; g.N = N; g.K = K; g.epi = epi; g.out_f32 = out_f32;

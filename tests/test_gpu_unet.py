@@ -514,3 +514,23 @@ def test_sdxl32_teacher_forced_block(sdxl32, block, m_ratio):
     assert ok, worst
     ig.ig_cache_free(cache)
     rq.free()
+
+
+@pytest.mark.parametrize("M,F,K", [(1, 128, 64), (300, 256, 128), (1992, 640, 320)])
+def test_op_gemm_geglu_epilogue(M, F, K):
+    """The fused GEGLU epilogue alone (ig_op_gemm epi 5, tile-interleaved weights) vs the oracle's
+    hidden * GELU_erf(gate) on the same bf16 inputs (C-TOL rtol 4e-3: the bf16 output rounding
+    alone is up to 2^-9 relative, the north_star bf16 bar is 2e-2)."""
+    A = synth.uniform(1, "A", (M, K), "cuda").float().to(torch.bfloat16)
+    W = (synth.uniform(2, "W", (2 * F, K), "cuda") / K ** 0.5).float().to(torch.bfloat16)
+    b = synth.uniform(3, "b", (2 * F,), "cuda").float().to(torch.bfloat16)
+    perm = np.array([(128 * (r // 256) + r % 256) if r % 256 < 128 else (F + 128 * (r // 256) + r % 256 - 128)
+                     for r in range(2 * F)])
+    Wi, bi = W[perm].contiguous(), b[perm].contiguous()
+    C = torch.full((M, F), float("nan"), dtype=torch.bfloat16, device="cuda")
+    ig.ig_op_gemm(ig.IG_BF16, A.data_ptr(), K, Wi.data_ptr(), K, bi.data_ptr(), C.data_ptr(), F, M, 2 * F, K, 5, 0, 0)
+    torch.cuda.synchronize()
+    u = oracle.linear(A.double().cpu().numpy(), W.double().cpu().numpy(), b.double().cpu().numpy())
+    want = u[:, :F] * oracle.gelu_erf(u[:, F:])
+    ok, worst = ctol(C.double().cpu().numpy(), want, 4e-3)
+    assert ok, worst

@@ -11,7 +11,7 @@ ap.add_argument("--M", type=int, default=14720)
 ap.add_argument("--N", type=int, default=3072)
 ap.add_argument("--K", type=int, default=3072)
 ap.add_argument("--iters", type=int, default=10)
-ap.add_argument("--epi", type=int, default=0, help="0 store, 1 bias+GELU (fc1)")
+ap.add_argument("--epi", type=int, default=0, help="0 store, 1 bias+GELU (fc1), 5 GEGLU (N/2 outputs)")
 ap.add_argument("--bias", action="store_true")
 args = ap.parse_args()
 res = {}
