@@ -185,6 +185,14 @@ void ig_cache_free(ig_cache* cache);
  * step path).  n_masked may be NULL. */
 ig_status ig_mask_build(ig_ctx* ctx, const uint8_t* mask, void* stream, ig_mask** out,
                         int* n_masked);
+/* a1 from a HOST bitmap (the serving path's admission, no device sync): mask = host uint8
+ * [L_img] (nonzero = masked), read before the call returns.  n_m, the unmasked runs and the
+ * bitmap are derived on the host; the bitmap goes up with one small async copy and kernel (a)
+ * builds idx_m / idx_u on the device, all enqueued on `stream` (stream-ordered allocation).
+ * Steps that use the mask must run on `stream` or be ordered after it.  ig_mask_free of such a
+ * mask is stream-ordered after the last step that read it (the stream must still exist). */
+ig_status ig_mask_build_host(ig_ctx* ctx, const uint8_t* mask, void* stream, ig_mask** out,
+                             int* n_masked);
 /* Device pointers to idx_m [n_m] and idx_u [L_img - n_m] (int32) and n_m. */
 ig_status ig_mask_indices(const ig_mask* mask, const int32_t** idx_m, const int32_t** idx_u,
                           int* n_m);
@@ -286,6 +294,34 @@ ig_status ig_profile_read(ig_ctx* ctx, ig_prof_entry out[IG_K_NCLASS]);
  * not touched.  Synchronous on `stream`. */
 ig_status ig_debug_block(ig_ctx* ctx, const ig_edit_req* req, int block, const float* X_in,
                          float* X_out, void* stream);
+
+/* Merged positional K/V buffer of (slot, block) as the last step left it (SURVEY §8(b) debug
+ * export, T3/T4): the ring buffer block % (prefetch_depth + 1) of the slot, rows [text 0..L_txt-1
+ * | image 0..L_img-1] (C-AMB 8), each plane [L][H] in desc.dtype.  Valid for the last
+ * prefetch_depth + 1 blocks of the last step of that slot (earlier blocks' buffers were reused).
+ * k_out, v_out: dev or host pointers of L*H elements.  Synchronises `stream` and the copy lane. */
+ig_status ig_debug_dump_kv(ig_ctx* ctx, int slot, int block, void* k_out, void* v_out, void* stream);
+
+/* Race tests and fault injection (SPEC S:615 negative control).  Debug only —
+ * every key is 0 in normal operation:
+ *   IG_DBG_SPIN_COPY_NS     the copy lane spins this many ns before each block's cache copy
+ *                           (a slow copy lane: exposes a missing RAW wait)
+ *   IG_DBG_SPIN_COMPUTE_NS  the compute lane spins before each attention (a slow compute lane:
+ *                           exposes a missing WAR wait before a ring buffer is overwritten)
+ *   IG_DBG_DROP_RAW         1 = compute does NOT wait for the copy of a block (negative control)
+ *   IG_DBG_DROP_WAR         1 = the copy lane does NOT wait for the buffer's previous reader
+ *   IG_DBG_CORRUPT_ROW      v > 0: after each block's copy add v to every element of the K and
+ *                           V rows of the first unmasked token of the batch's first cache user
+ *                           (a corrupted cache row: must turn parity red)
+ *   IG_DBG_POISON_RING      immediate (value ignored): synchronise the device and fill every
+ *                           slot's K/V ring with NaN; a correct step re-stages every row it
+ *                           reads, so its result is unchanged
+ * IG_EINVAL on an unknown key or a negative value. */
+typedef enum {
+  IG_DBG_SPIN_COPY_NS = 1, IG_DBG_SPIN_COMPUTE_NS = 2, IG_DBG_DROP_RAW = 3, IG_DBG_DROP_WAR = 4,
+  IG_DBG_CORRUPT_ROW = 5, IG_DBG_POISON_RING = 6
+} ig_debug_key;
+ig_status ig_debug_set(ig_ctx* ctx, int key, long long value);
 
 #ifdef __cplusplus
 }

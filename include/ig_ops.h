@@ -16,8 +16,9 @@ extern "C" {
  * 1 = GELU-tanh (C-AMB 6), 5 = GEGLU (IG_BF16 only; UNet feed-forward, C-AMB 32): B and bias
  * rows tile-interleaved — every group of 256 rows holds 128 "hidden" rows then their 128 "gate"
  * rows — and C[M, N/2] (bf16) = hidden * GELU_erf(gate), N % 256 == 0.  Row-major with leading
- * dimensions in elements.  IG_BF16 requires K % 64 == 0, N % 16 == 0, lda/ldb/ldc multiples
- * of 8 and 16-byte aligned pointers (IG_EUNSUPPORTED otherwise). */
+ * dimensions in elements.  IG_BF16 requires K % 8 == 0 (TMA zero-fills the K tail of the last
+ * 64-wide slice), lda/ldb multiples of 8, ldc a multiple of 8 (bf16 C) or 4 (fp32 C), and
+ * 16-byte aligned pointers (IG_EUNSUPPORTED otherwise); M and N are arbitrary. */
 ig_status ig_op_gemm(int dtype, const void* A, long long lda, const void* B, long long ldb,
                      const void* bias, void* C, long long ldc, int M, int N, int K, int epi,
                      int out_f32, void* stream);
@@ -39,6 +40,13 @@ ig_status ig_op_attention(int dtype, const void* Q, long long ldq, void* O, long
 /* Test/bench I/O helper: cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault) on `stream`
  * followed by a stream synchronisation (any host/device combination, UVA pointers). */
 ig_status ig_copy(void* dst, const void* src, size_t bytes, void* stream);
+
+/* Per-request input staging for the host-buffer path (e.g. a request's text tokens at
+ * admission): an SM-driven copy of `bytes` from PINNED host memory `src` (cudaHostAlloc /
+ * cudaHostRegister'ed, device-mapped) into device memory `dst`, enqueued on `stream`.  Unlike a
+ * cudaMemcpyAsync it does not queue on the copy engines behind the cache prefetch.  IG_EINVAL
+ * if src is not pinned host memory. */
+ig_status ig_stage_input(void* dst, const void* src, size_t bytes, void* stream);
 
 #ifdef __cplusplus
 }

@@ -14,6 +14,7 @@
 #include <cstdio>
 #include <cstring>
 #include <cstdlib>
+#include <cstdint>
 #include <mutex>
 #include <chrono>
 #include <string>
@@ -110,6 +111,10 @@ struct ig_mask {
   std::vector<uint8_t> bits;              // host: 1 = masked (load deduplication)
   uint8_t* bits_dev = nullptr;            // device copy of bits
   int32_t* idx = nullptr;  // device: idx_m at [0, L_img), idx_u at [L_img, 2 L_img), n_m at [2 L_img]
+  bool async_alloc = false;                 // ig_mask_build_host: idx + bits_dev are ONE stream-ordered allocation
+  cudaStream_t build_st = nullptr;          // stream of the build
+  mutable cudaStream_t last_st = nullptr;   // compute stream of the last step that read the mask
+  mutable bool used = false;
 };
 
 struct ig_cache {
@@ -207,7 +212,12 @@ struct ig_ctx {
   cudaEvent_t ev_yrec[MAXR] = {};
   uint8_t* q8yrec = nullptr; float* q8yrec_scl = nullptr;  // FP8 Y recording: [R][2][plane] (+ scales)
   ig_stats stats{};
-  std::vector<ig_cache*> zombies;
+  // first enqueue failure of the copy lane inside the current step (checked at the step's end:
+  // a rejected DMA leaves ring rows stale, so the step must not report success)
+  cudaError_t copy_err = cudaSuccess;
+  size_t copy_err_idx = 0;
+  // ig_debug_set keys (race tests and fault injection; all 0 in normal operation)
+  long long dbg[8] = {};
   // CUDA graphs of whole steps (ig_ctx_opts.use_graphs): keyed by everything that shapes the
   // launches (row counts, plan, staging slot, cache kinds); the per-step data (sigmas, step
   // indices, cache plane pointers, latents) live in the descriptors the graph itself pulls
@@ -292,16 +302,31 @@ static void free_cache_now(ig_cache* c) {
   delete c;
 }
 
-static void reap_zombies(ig_ctx* ctx) {
-  auto& z = ctx->zombies;
-  for (size_t i = 0; i < z.size();) {
-    if (z[i]->pins.load() == 0) {
-      free_cache_now(z[i]);
-      z.erase(z.begin() + i);
+// caches freed while a step still pinned them (ig_cache_free is deferred); reaped
+// by later ig_cache_free / ig_edit_step / ig_ctx_destroy calls once their pins dropped
+static std::mutex g_zombie_mu;
+static std::vector<ig_cache*> g_zombies;
+
+static void reap_zombies_locked(int device) {
+  for (size_t i = 0; i < g_zombies.size();) {
+    ig_cache* z = g_zombies[i];
+    if ((device < 0 || z->device == device) && z->pins.load() == 0) {
+      int cur = 0;
+      cudaGetDevice(&cur);
+      const int dev = z->device;
+      if (dev != cur) cudaSetDevice(dev);
+      free_cache_now(z);
+      if (dev != cur) cudaSetDevice(cur);
+      g_zombies.erase(g_zombies.begin() + i);
     } else {
       ++i;
     }
   }
+}
+
+static void reap_zombies(ig_ctx* ctx) {
+  std::lock_guard<std::mutex> lk(g_zombie_mu);
+  reap_zombies_locked(ctx->device);
 }
 
 static void CUDART_CB unpin_cb(void* p) {
@@ -667,8 +692,8 @@ extern "C" ig_status ig_ctx_create(const ig_model_desc* desc, const void* const*
 extern "C" void ig_ctx_destroy(ig_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
-  cudaDeviceSynchronize();
-  for (auto* z : ctx->zombies) free_cache_now(z);
+  cudaDeviceSynchronize();  // every enqueued step (and its unpin callback) has finished
+  reap_zombies(ctx);
   void* bufs[] = {ctx->X, ctx->vel, ctx->temb, ctx->tmp, ctx->vec, ctx->svec, ctx->modbuf, ctx->h,
                   ctx->qkv, ctx->Q, ctx->cat, ctx->Ain, ctx->ri, ctx->kv_arena, ctx->rope_tab,
                   ctx->gv_t1, ctx->gv_t2, ctx->gv_mod, ctx->modw, ctx->modb, ctx->svec_bf,
@@ -802,10 +827,57 @@ extern "C" ig_status ig_mask_indices(const ig_mask* m, const int32_t** idx_m, co
   return IG_OK;
 }
 
+extern "C" ig_status ig_mask_build_host(ig_ctx* ctx, const uint8_t* mask, void* stream, ig_mask** out,
+                                        int* n_masked) {
+  if (!ctx || !mask || !out) return set_err(IG_EINVAL, "NULL argument");
+  *out = nullptr;
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  const int L = ctx->Limg;
+  ig_mask* m = new ig_mask();
+  m->L_img = L;
+  m->bits.resize(L);
+  int n = 0;
+  for (int i = 0; i < L; ++i) { m->bits[i] = mask[i] != 0; n += m->bits[i]; }
+  for (int i = 0; i < L;) {  // unmasked runs for the compacted DMA copy (copy_mode 1)
+    if (m->bits[i]) { ++i; continue; }
+    int j = i;
+    while (j < L && !m->bits[j]) ++j;
+    m->runs.push_back({i, j - i});
+    i = j;
+  }
+  // one stream-ordered allocation: idx_m | idx_u | n_m (int32), then the bitmap (u8)
+  const size_t idx_bytes = ((size_t)(2 * L + 1) * sizeof(int32_t) + 15) & ~(size_t)15;
+  void* base = nullptr;
+  cudaError_t e = cudaMallocAsync(&base, idx_bytes + L, st);
+  if (e == cudaSuccess) {
+    m->idx = (int32_t*)base;
+    m->bits_dev = (uint8_t*)base + idx_bytes;
+    // pageable source: the call returns once the bytes are staged (no device sync)
+    e = cudaMemcpyAsync(m->bits_dev, m->bits.data(), L, cudaMemcpyHostToDevice, st);
+  }
+  if (e != cudaSuccess) {
+    if (base) cudaFreeAsync(base, st);
+    delete m;
+    return set_err(IG_ECUDA, "mask build: %s", cudaGetErrorString(e));
+  }
+  launch_mask_index(m->bits_dev, L, m->idx, m->idx + L, m->idx + 2 * L, st);
+  m->async_alloc = true;
+  m->build_st = st;
+  m->n_m = n;
+  if (n_masked) *n_masked = n;
+  *out = m;
+  return IG_OK;
+}
+
 extern "C" void ig_mask_free(ig_mask* m) {
   if (!m) return;
-  cudaFree(m->idx);
-  if (m->bits_dev) cudaFree(m->bits_dev);
+  if (m->async_alloc) {  // stream-ordered: after the last step that read the mask (no device sync)
+    cudaFreeAsync(m->idx, m->used ? m->last_st : m->build_st);
+  } else {
+    cudaFree(m->idx);
+    if (m->bits_dev) cudaFree(m->bits_dev);
+  }
   delete m;
 }
 
@@ -926,9 +998,9 @@ static ig_status cache_create_kind(ig_ctx* ctx, int n_steps, int tier, int fp8, 
   if (e != cudaSuccess) {
     cudaGetLastError();
     if (c->ptr) { if (tier == IG_CACHE_HOST) cudaFreeHost(c->ptr); else cudaFree(c->ptr); }
+    const size_t bytes = c->bytes;
     delete c;
-    return set_err(IG_ENOMEM, "cache allocation of %zu bytes failed: %s", c->bytes,
-                   cudaGetErrorString(e));
+    return set_err(IG_ENOMEM, "cache allocation of %zu bytes failed: %s", bytes, cudaGetErrorString(e));
   }
   *out = c;
   return IG_OK;
@@ -1040,17 +1112,10 @@ extern "C" ig_status ig_cache_storage(ig_cache* c, void** ptr, size_t* bytes, in
   return IG_OK;
 }
 
-static std::mutex g_zombie_mu;
-static std::vector<ig_cache*> g_zombies;  // caches freed while pinned (no ctx at hand)
-
 extern "C" void ig_cache_free(ig_cache* c) {
   if (!c) return;
   std::lock_guard<std::mutex> lk(g_zombie_mu);
-  // reap earlier zombies whose pins dropped
-  for (size_t i = 0; i < g_zombies.size();) {
-    if (g_zombies[i]->pins.load() == 0) { free_cache_now(g_zombies[i]); g_zombies.erase(g_zombies.begin() + i); }
-    else ++i;
-  }
+  reap_zombies_locked(-1);  // earlier zombies whose pins dropped
   if (c->pins.load() == 0) free_cache_now(c);
   else { c->zombie = true; g_zombies.push_back(c); }
 }
@@ -1081,8 +1146,13 @@ struct CopyPlan {
   std::vector<int> dsrc;                                // per request: source index or -1
   std::vector<std::vector<std::pair<int, int>>> druns;  // per member: runs of U_r \ U_src
   std::vector<int> dshared;                             // per member: |U_r ∩ U_src|
+  std::vector<const ig_cache*> dcache;                  // per dedupe entry: the cache its pair shares
   DedupeArgs dd{};
 };
+
+static inline void note_copy(ig_ctx* ctx, cudaError_t e) {
+  if (e != cudaSuccess && ctx->copy_err == cudaSuccess) ctx->copy_err = e;
+}
 
 static void issue_copy(ig_ctx* ctx, const std::vector<StepReq>& sr, const KvGatherReq* kvg_dev,
                        const KvGatherReq* kvq_dev, int b, const CopyPlan& plan) {
@@ -1090,7 +1160,9 @@ static void issue_copy(ig_ctx* ctx, const std::vector<StepReq>& sr, const KvGath
   const int buf = b % ctx->R;
   // inside a graph capture only this step's records are visible; earlier steps completed
   // before the graph starts (same stream)
-  if (!ctx->capturing || (ctx->cap_mask >> buf & 1u)) cudaStreamWaitEvent(ctx->copy_st, ctx->ev_comp[buf], 0);
+  if ((!ctx->capturing || (ctx->cap_mask >> buf & 1u)) && !ctx->dbg[IG_DBG_DROP_WAR])
+    cudaStreamWaitEvent(ctx->copy_st, ctx->ev_comp[buf], 0);
+  if (ctx->dbg[IG_DBG_SPIN_COPY_NS]) launch_spin((unsigned long long)ctx->dbg[IG_DBG_SPIN_COPY_NS], ctx->copy_st);
   const long long by0 = ctx->stats.h2d_bytes + ctx->stats.d2d_bytes;
   ProfScope ps(ctx, ctx->copy_st, IG_K_COPY, 0.0, 0.0, b);
   const int n = (int)sr.size();
@@ -1138,7 +1210,7 @@ static void issue_copy(ig_ctx* ctx, const std::vector<StepReq>& sr, const KvGath
       if (gathered) {
         by = (long long)n_u * row;  // SM gather kernel below
       } else if (ctx->o.copy_mode == 0) {
-        cudaMemcpyAsync(dst, src, (size_t)ctx->Limg * row, cudaMemcpyDefault, ctx->copy_st);
+        note_copy(ctx, cudaMemcpyAsync(dst, src, (size_t)ctx->Limg * row, cudaMemcpyDefault, ctx->copy_st));
         by = (long long)ctx->Limg * row;
       } else {
         const bool dd = !plan.dsrc.empty() && plan.dsrc[q] >= 0;
@@ -1180,9 +1252,10 @@ static void issue_copy(ig_ctx* ctx, const std::vector<StepReq>& sr, const KvGath
       pf = ig_ctx::Pref{};
       if (!prefetched) {
         char* dst = (char*)ctx->kv_arena + ((size_t)slot * ctx->slot_stride + (size_t)buf * ctx->buf_elems) * ctx->esz;
-        cudaMemcpyAsync(dst + txt_off, cache_plane(ctx, c, r->step, b, 0), plane, cudaMemcpyDefault, ctx->copy_st);
-        cudaMemcpyAsync(dst + vplane + txt_off, cache_plane(ctx, c, r->step, b, 1), plane, cudaMemcpyDefault,
-                        ctx->copy_st);
+        note_copy(ctx, cudaMemcpyAsync(dst + txt_off, cache_plane(ctx, c, r->step, b, 0), plane, cudaMemcpyDefault,
+                                       ctx->copy_st));
+        note_copy(ctx, cudaMemcpyAsync(dst + vplane + txt_off, cache_plane(ctx, c, r->step, b, 1), plane,
+                                       cudaMemcpyDefault, ctx->copy_st));
         by = 2 * (long long)plane;
       }
     } else if (host && ctx->o.copy_mode == 1) {  // DMA runs straight into the ring
@@ -1212,17 +1285,27 @@ static void issue_copy(ig_ctx* ctx, const std::vector<StepReq>& sr, const KvGath
     constexpr size_t CHUNKC = 128;  // bounded batches (very large batches crash driver 580)
     for (size_t i = 0; i < sizes.size(); i += CHUNKC) {
       const size_t cnt = std::min(CHUNKC, sizes.size() - i);
-      cudaMemcpyBatchAsync(dsts.data() + i, srcs.data() + i, sizes.data() + i, cnt, &attr, &attr_idx, 1, &fail,
-                           ctx->copy_st);
+      fail = SIZE_MAX;
+      const cudaError_t ce = cudaMemcpyBatchAsync(dsts.data() + i, srcs.data() + i, sizes.data() + i, cnt, &attr,
+                                                  &attr_idx, 1, &fail, ctx->copy_st);
+      if (ce != cudaSuccess && ctx->copy_err == cudaSuccess) {
+        ctx->copy_err = ce;
+        ctx->copy_err_idx = i + (fail == SIZE_MAX ? 0 : fail);
+      }
     }
   }
   if (plan.dd.n > 0) {  // rows shared with an earlier same-(cache, step) request: HBM -> HBM
-    const ig_cache* c0 = nullptr;
-    for (int q = 0; q < n && !c0; ++q) if (plan.dsrc[q] >= 0) c0 = sr[q].r->cache;
-    if (!(y_block(c0, b) && b <= plan.kplan)) {
-      DedupeArgs dd = plan.dd;
-      dd.buf_off = (long long)buf * ctx->buf_elems;
-      dd.v_only = y_block(c0, b) ? 1 : 0;
+    // per entry from ITS cache (entries of one batch may sit on caches of different kinds)
+    DedupeArgs dd = plan.dd;
+    dd.buf_off = (long long)buf * ctx->buf_elems;
+    int live = 0;
+    for (int i = 0; i < dd.n; ++i) {
+      const ig_cache* ce = plan.dcache[i];
+      dd.e[i].v_only = y_block(ce, b) ? 1 : 0;
+      dd.e[i].skip = (y_block(ce, b) && b <= plan.kplan) ? 1 : 0;
+      live += !dd.e[i].skip;
+    }
+    if (live) {
       ctx->stats.kernel_launches++;
       launch_kv_dedupe(dd, ctx->copy_st);
     }
@@ -1234,6 +1317,15 @@ static void issue_copy(ig_ctx* ctx, const std::vector<StepReq>& sr, const KvGath
   if (plan.gather_q8) {
     ctx->stats.kernel_launches++;
     launch_kv_gather_q8(kvq_dev + (size_t)b * n, n, plan.max_nu, ctx->Lt, ctx->H, ctx->d.heads, ctx->copy_st);
+  }
+  if (ctx->dbg[IG_DBG_CORRUPT_ROW]) {  // fault injection: one staged cached row of the first cache user
+    for (int q = 0; q < n; ++q) {
+      if (!sr[q].use_cache || sr[q].m->n_m >= ctx->Limg) continue;
+      char* dst = (char*)ctx->kv_arena + ((size_t)sr[q].r->slot * ctx->slot_stride + (size_t)buf * ctx->buf_elems) * ctx->esz;
+      launch_corrupt_row(dst, (long long)ctx->L * ctx->H, sr[q].m->idx + ctx->Limg, ctx->Lt, ctx->H, (int)ctx->esz,
+                         (float)ctx->dbg[IG_DBG_CORRUPT_ROW], ctx->copy_st);
+      break;
+    }
   }
   ps.bytes = (double)(ctx->stats.h2d_bytes + ctx->stats.d2d_bytes - by0);
   cudaEventRecord(ctx->ev_copy[buf], ctx->copy_st);
@@ -1348,6 +1440,7 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
   const long long es = (long long)ctx->esz;
   const bool unet = ctx->d.n_unet > 0;
   ctx->stats = ig_stats{};
+  ctx->copy_err = cudaSuccess;
   ctx->pdl_block = true;  // the step's first GEMM may follow anything the caller enqueued
   auto t_host0 = std::chrono::steady_clock::now();
   // ---- host validation (nothing enqueued before this passes) ----
@@ -1420,6 +1513,7 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
           e.bits0 = sr[q0].m->bits_dev;
           e.slot0 = sr[q0].r->slot;
           e.slot = sr[q].r->slot;
+          plan.dcache.push_back(sr[q].r->cache);
           plan.dd.max_nu = std::max(plan.dd.max_nu, e.n_u);
           break;
         }
@@ -1663,6 +1757,7 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
     CUDA_TRY(cudaMemcpyAsync(ds + off, hs + off, bytes, cudaMemcpyHostToDevice, ctx->copy_st));
   }
   for (auto& s : sr) if (s.use_cache) { s.r->cache->pins.fetch_add(1); }
+  for (auto& s : sr) { s.m->used = true; s.m->last_st = st; }
 
   // ---- prefetch the first R cached blocks (copy lane); dense-prefix blocks need no cache ----
   const int bc0 = std::max(b0, kplan);
@@ -1815,7 +1910,7 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
   // staged Y_{b-1} rows (the copy lane's V-plane landing zone), after waiting for the copy
   auto y_staged = [&](int b) { return uy[b] > 0 && b > kplan; };
   auto ln_mod_y = [&](int b, int buf, int mod_t, int shift_c, int scale_c) {
-    stream_wait(ctx, st, ctx->ev_copy[buf]);
+    if (!ctx->dbg[IG_DBG_DROP_RAW]) stream_wait(ctx, st, ctx->ev_copy[buf]);
     const long long off = ctx->mods[mod_t].off;
     ProfScope ps(ctx, st, IG_K_LNMOD, 0.0, (double)uy[b] * H * (es + es));
     launch_ln_mod_staged<T>(ctx->kv_arena, ctx->slot_stride, (long long)buf * ctx->buf_elems, ctx->L, H, M, M + uy[b],
@@ -1853,6 +1948,10 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
     cudaEventRecord(ctx->ev_yrec[yb], ctx->copy_st);
   };
   auto attn = [&](int buf, bool dense) {
+    if (ctx->dbg[IG_DBG_SPIN_COMPUTE_NS]) {  // slow compute lane (WAR race test)
+      launch_spin((unsigned long long)ctx->dbg[IG_DBG_SPIN_COMPUTE_NS], st);
+      ctx->pdl_block = true;
+    }
     AttnArgs a{};
     a.Q = ctx->Q; a.ldq = H; a.O = cat; a.ldo = ldcat; a.kv_arena = ctx->kv_arena;
     a.kv_off = (long long)buf * ctx->buf_elems;
@@ -1898,11 +1997,12 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
   // full-L copies also write the masked rows, so they must land before the fresh K/V
   // scatter; compacted copies touch only unmasked rows and are awaited right before attention
   const bool late_wait = ctx->o.copy_mode != 0 && !record;
+  const bool drop_raw = ctx->dbg[IG_DBG_DROP_RAW] != 0;  // negative control of the race tests
   auto wait_copy = [&](int buf) {
-    if ((any_cache || record) && !late_wait) stream_wait(ctx, st, ctx->ev_copy[buf]);
+    if ((any_cache || record) && !late_wait && !(drop_raw && !record)) stream_wait(ctx, st, ctx->ev_copy[buf]);
   };
   auto wait_copy_late = [&](int buf) {
-    if (any_cache && late_wait) stream_wait(ctx, st, ctx->ev_copy[buf]);
+    if (any_cache && late_wait && !drop_raw) stream_wait(ctx, st, ctx->ev_copy[buf]);
   };
 
   // ---- UNet BasicTransformerBlock (config 5; oracle/unet.py unet_block_masked) ----
@@ -2129,6 +2229,12 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
     CUDA_TRY(cudaStreamWaitEvent(st, record->y && blk_yrec(record->ymode, b1 - 1) ? ctx->ev_yrec[(b1 - 1) % R]
                                                                                  : ctx->ev_copy[(b1 - 1) % R], 0));
   ctx->pdl_block = true;
+  if (ctx->copy_err != cudaSuccess) {
+    const cudaError_t ce = ctx->copy_err;
+    ctx->copy_err = cudaSuccess;
+    cudaGetLastError();
+    return set_err(IG_ECUDA, "cache prefetch enqueue failed (copy %zu): %s", ctx->copy_err_idx, cudaGetErrorString(ce));
+  }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_err(IG_ECUDA, "step enqueue: %s", cudaGetErrorString(e));
   stats.host_ns = std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - t_host0).count();
@@ -2210,6 +2316,39 @@ extern "C" ig_status ig_cache_template(ig_ctx* ctx, float* latent, const void* t
   return IG_OK;
 }
 
+extern "C" ig_status ig_debug_set(ig_ctx* ctx, int key, long long value) {
+  if (!ctx) return set_err(IG_EINVAL, "ctx is NULL");
+  if (key <= 0 || key > IG_DBG_POISON_RING) return set_err(IG_EINVAL, "unknown debug key %d", key);
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  if (key == IG_DBG_POISON_RING) {  // immediate: every ring buffer of every slot -> NaN
+    CUDA_TRY(cudaDeviceSynchronize());
+    flush_graph_tail(ctx);
+    CUDA_TRY(cudaMemset(ctx->kv_arena, 0xFF, (size_t)ctx->o.max_batch * ctx->slot_stride * ctx->esz));
+    CUDA_TRY(cudaDeviceSynchronize());
+    for (auto& p : ctx->pref) p = ig_ctx::Pref{};
+    return IG_OK;
+  }
+  if (value < 0) return set_err(IG_EINVAL, "debug value must be >= 0");
+  ctx->dbg[key] = value;
+  return IG_OK;
+}
+
+extern "C" ig_status ig_debug_dump_kv(ig_ctx* ctx, int slot, int block, void* k_out, void* v_out, void* stream) {
+  if (!ctx || !k_out || !v_out) return set_err(IG_EINVAL, "NULL argument");
+  if (slot < 0 || slot >= ctx->o.max_batch) return set_err(IG_EINVAL, "slot %d out of range", slot);
+  if (block < 0 || block >= ctx->nb) return set_err(IG_EINVAL, "block %d out of range", block);
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t plane = (size_t)ctx->L * ctx->H * ctx->esz;
+  const char* src = (const char*)ctx->kv_arena + ((size_t)slot * ctx->slot_stride + (size_t)(block % ctx->R) * ctx->buf_elems) * ctx->esz;
+  CUDA_TRY(cudaStreamSynchronize(st));
+  CUDA_TRY(cudaStreamSynchronize(ctx->copy_st));
+  CUDA_TRY(cudaMemcpyAsync(k_out, src, plane, cudaMemcpyDefault, st));
+  CUDA_TRY(cudaMemcpyAsync(v_out, src + plane, plane, cudaMemcpyDefault, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return IG_OK;
+}
+
 extern "C" ig_status ig_prefetch_layer(ig_ctx* ctx, const ig_edit_req* r, int layer) {
   if (!ctx || !r) return set_err(IG_EINVAL, "NULL argument");
   if (layer < 0 || layer >= ctx->nb) return set_err(IG_EINVAL, "layer %d out of range", layer);
@@ -2287,6 +2426,7 @@ extern "C" ig_status ig_op_attention(int dtype, const void* Q, long long ldq, vo
                                      const void* kv, const int32_t* segs, int nseg, int L, int heads,
                                      int head_dim, void* stream) {
   if (!Q || !O || !kv || !segs || nseg <= 0 || L <= 0 || heads <= 0) return set_err(IG_EINVAL, "bad argument");
+  if (dtype != IG_F32 && dtype != IG_BF16) return set_err(IG_EINVAL, "bad dtype");
   if (head_dim != 16 && head_dim != 64 && head_dim != 128) return set_err(IG_EUNSUPPORTED, "head_dim");
   std::vector<AttnSeg> hs(nseg);
   int maxq = 0;
@@ -2319,6 +2459,19 @@ extern "C" ig_status ig_op_attention(int dtype, const void* Q, long long ldq, vo
   }
   CUDA_TRY(cudaFreeAsync(dsegs, st));
   CUDA_TRY(cudaStreamSynchronize(st));  // host segment vector lifetime
+  CUDA_TRY(cudaGetLastError());
+  return IG_OK;
+}
+
+extern "C" ig_status ig_stage_input(void* dst, const void* src, size_t bytes, void* stream) {
+  if ((!dst || !src) && bytes) return set_err(IG_EINVAL, "NULL argument");
+  if (bytes == 0) return IG_OK;
+  cudaPointerAttributes pa{};
+  if (cudaPointerGetAttributes(&pa, src) != cudaSuccess || pa.type != cudaMemoryTypeHost || !pa.devicePointer) {
+    cudaGetLastError();
+    return set_err(IG_EINVAL, "ig_stage_input: src must be pinned (page-locked, mapped) host memory");
+  }
+  launch_copy_bytes(dst, pa.devicePointer, bytes, (cudaStream_t)stream);
   CUDA_TRY(cudaGetLastError());
   return IG_OK;
 }

@@ -310,6 +310,7 @@ template void launch_rows_to<bf16>(const float*, void*, long long, cudaStream_t)
 __global__ void __launch_bounds__(256) kv_dedupe_kernel(const DedupeArgs a) {
   const int ent = blockIdx.y;
   const DedupeEnt& d = a.e[ent];
+  if (d.skip) return;
   const int lane = threadIdx.x & 31;
   const int warps = (gridDim.x * blockDim.x) >> 5;
   const long long row_bytes = (long long)a.H * a.es;
@@ -318,7 +319,7 @@ __global__ void __launch_bounds__(256) kv_dedupe_kernel(const DedupeArgs a) {
   for (int j = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; j < d.n_u; j += warps) {
     const int tok = d.idx_u[j];
     if (d.bits0[tok]) continue;  // masked in the source: loaded over the link for this member
-    for (int plane = a.v_only; plane < 2; ++plane) {
+    for (int plane = d.v_only; plane < 2; ++plane) {
       const long long off = (a.buf_off + plane * a.L * a.H + (long long)(a.Lt + tok) * a.H) * a.es;
       const int4* src = reinterpret_cast<const int4*>(arena + d.slot0 * a.slot_stride * a.es + off);
       int4* dst = reinterpret_cast<int4*>(arena + d.slot * a.slot_stride * a.es + off);
@@ -509,4 +510,45 @@ void launch_permute_geglu_rows(const bf16* src, bf16* dst, int F, int K, cudaStr
   permute_geglu_kernel<<<2 * F, 256, 0, st>>>(src, dst, F, K);
 }
 
+}  // namespace ig
+
+// ======================================================================================
+// Debug / fault-injection kernels (ig_debug_set; SURVEY §4 T5 race tests, S:615 negative
+// control).  Never launched unless a debug key is set.
+// ======================================================================================
+namespace ig {
+__global__ void spin_kernel(unsigned long long ns) {
+  if (threadIdx.x != 0) return;
+  unsigned long long t0, t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  do {
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  } while (t - t0 < ns);
+}
+
+void launch_spin(unsigned long long ns, cudaStream_t st) {
+  if (ns) spin_kernel<<<1, 32, 0, st>>>(ns);
+}
+
+// plane rows [Lt + idx_u[0]] of K and V (elements of size es) += add
+__global__ void corrupt_row_kernel(char* plane_k, long long vplane_elems, const int32_t* idx_u, int Lt, int H, int es,
+                                   float add) {
+  const int tok = idx_u[0];
+  for (int c = threadIdx.x; c < H; c += blockDim.x)
+    for (int w = 0; w < 2; ++w) {
+      const long long off = w * vplane_elems + (long long)(Lt + tok) * H + c;
+      if (es == 2) {
+        bf16* p = reinterpret_cast<bf16*>(plane_k) + off;
+        *p = __float2bfloat16(__bfloat162float(*p) + add);
+      } else {
+        float* p = reinterpret_cast<float*>(plane_k) + off;
+        *p += add;
+      }
+    }
+}
+
+void launch_corrupt_row(void* plane_k, long long vplane_elems, const int32_t* idx_u, int Lt, int H, int es,
+                        float add, cudaStream_t st) {
+  corrupt_row_kernel<<<1, 256, 0, st>>>((char*)plane_k, vplane_elems, idx_u, Lt, H, es, add);
+}
 }  // namespace ig

@@ -113,6 +113,11 @@ void launch_kv_gather(const KvGatherReq* reqs_dev, int n, int max_nu, int L_txt,
 
 // dst[0, n) = src[0, n) by SM loads (src may be mapped pinned host memory), 16-byte vectors
 void launch_copy_bytes(void* dst, const void* src, size_t n, cudaStream_t st);
+// debug / fault injection (ig_debug_set): a one-thread spin of `ns` nanoseconds on a stream,
+// and +add on the K and V rows of the token idx_u[0] of one positional K/V buffer
+void launch_spin(unsigned long long ns, cudaStream_t st);
+void launch_corrupt_row(void* plane_k, long long vplane_elems, const int32_t* idx_u, int Lt, int H, int es,
+                        float add, cudaStream_t st);
 
 // ---- Y variant (k_rows.cu) ------------------------------------------------------
 // LN-modulation of rows [r0, r1) read from the staged Y rows (V plane, position ri[r].kvpos of
@@ -133,13 +138,15 @@ struct DedupeEnt {
   const int32_t* idx_u; int n_u;
   const uint8_t* bits0;  // source request's mask bitmap (1 = masked)
   int slot0, slot;
+  int v_only;            // per block, from the entry's own cache: 1 = Y block (V landing plane only)
+  int skip;              // per block: 1 = nothing staged for this entry (Y block inside the prefix)
 };
 constexpr int MAX_DEDUPE = 16;
 struct DedupeArgs {
   DedupeEnt e[MAX_DEDUPE];
   int n, max_nu;
   void* arena; long long slot_stride, buf_off, L;
-  int Lt, H, es, v_only;
+  int Lt, H, es;
 };
 void launch_kv_dedupe(const DedupeArgs& a, cudaStream_t st);
 

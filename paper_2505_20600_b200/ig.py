@@ -25,7 +25,10 @@ EXPORTS = ["ig_weight_count", "ig_ctx_create", "ig_ctx_destroy", "ig_cache_creat
            "ig_mask_indices", "ig_mask_free", "ig_edit_step", "ig_prefetch_layer",
            "ig_last_error", "ig_last_stats", "ig_op_gemm", "ig_op_gemm_gated", "ig_op_attention", "ig_copy",
            "ig_profile_enable", "ig_profile_read", "ig_debug_block", "ig_cache_clone", "ig_cache_write",
-           "ig_set_plan", "ig_last_plan"]
+           "ig_set_plan", "ig_last_plan", "ig_debug_set", "ig_debug_dump_kv",
+           "ig_mask_build_host", "ig_stage_input"]
+IG_DBG_SPIN_COPY_NS, IG_DBG_SPIN_COMPUTE_NS, IG_DBG_DROP_RAW, IG_DBG_DROP_WAR = 1, 2, 3, 4
+IG_DBG_CORRUPT_ROW, IG_DBG_POISON_RING = 5, 6
 KCLASS = ["gemm", "attn", "lnmod", "qkvpost", "cond", "rows", "copy"]
 
 
@@ -113,6 +116,10 @@ def lib():
         L.ig_last_plan.argtypes = [vp]
         L.ig_debug_block.argtypes = [vp, P(ig_edit_req), i, vp, vp, vp]
         L.ig_profile_read.argtypes = [vp, P(ig_prof_entry)]
+        L.ig_debug_set.argtypes = [vp, i, ll]
+        L.ig_mask_build_host.argtypes = [vp, vp, vp, P(vp), P(i)]
+        L.ig_stage_input.argtypes = [vp, vp, ctypes.c_size_t, vp]
+        L.ig_debug_dump_kv.argtypes = [vp, i, i, vp, vp, vp]
         for name in EXPORTS:
             if name not in ("ig_ctx_destroy", "ig_cache_free", "ig_mask_free", "ig_last_error",
                             "ig_weight_count", "ig_last_plan"):
@@ -160,6 +167,23 @@ def ig_mask_build(ctx: int, mask_ptr: int, stream: int = 0):
     out, n = ctypes.c_void_p(), ctypes.c_int()
     _check(lib().ig_mask_build(ctx, mask_ptr, stream, ctypes.byref(out), ctypes.byref(n)))
     return out.value, n.value
+
+
+def ig_mask_build_host(ctx: int, mask_u8, stream: int = 0):
+    """mask_u8: a host buffer of L_img bytes (numpy uint8 array or ctypes address)."""
+    if hasattr(mask_u8, "ctypes"):
+        import numpy as _np
+        mask_u8 = _np.ascontiguousarray(mask_u8, dtype=_np.uint8)
+        ptr = mask_u8.ctypes.data
+    else:
+        ptr = int(mask_u8)
+    out, n = ctypes.c_void_p(), ctypes.c_int()
+    _check(lib().ig_mask_build_host(ctx, ptr, stream, ctypes.byref(out), ctypes.byref(n)))
+    return out.value, n.value
+
+
+def ig_stage_input(dst: int, src: int, nbytes: int, stream: int = 0):
+    _check(lib().ig_stage_input(dst, src, nbytes, stream))
 
 
 def ig_mask_indices(mask: int):
@@ -252,6 +276,14 @@ def ig_profile_read(ctx: int) -> dict:
 
 def ig_debug_block(ctx: int, req: ig_edit_req, block: int, X_in: int, X_out: int, stream: int = 0):
     _check(lib().ig_debug_block(ctx, ctypes.byref(req), block, X_in, X_out, stream))
+
+
+def ig_debug_set(ctx: int, key: int, value: int = 0):
+    _check(lib().ig_debug_set(ctx, key, value))
+
+
+def ig_debug_dump_kv(ctx: int, slot: int, block: int, k_out: int, v_out: int, stream: int = 0):
+    _check(lib().ig_debug_dump_kv(ctx, slot, block, k_out, v_out, stream))
 
 
 def ig_cache_clone(ctx: int, cache: int, tier: int) -> int:

@@ -705,3 +705,44 @@ def test_load_dedupe_same_template_and_step(kind):
     for r in alone + batch:
         r.free()
     m.close()
+
+
+def test_load_dedupe_mixed_cache_kinds():
+    """Two dedupe groups in one batch, one on a hybrid host cache and one on a pure K/V host
+    cache (the skip / V-only decision is per group, from the group's own cache).
+    Order [hyb, kv, hyb, kv] puts the hybrid group first, so a batch-wide decision taken from it
+    would skip the K plane of the K/V group's shared rows at every Y block.  Each request must
+    equal itself run alone, bit for bit."""
+    from gpu_util import hybrid_planes
+    d = synth.FLUX_SMALL
+    sig = [1.0, 0.7, 0.4]
+    m = Model(d, ig.IG_BF16, opts=ig.ig_ctx_opts(4, 0, 2, 1, 0, 0))
+    mh = Model(d, ig.IG_BF16, opts=ig.ig_ctx_opts(4, 0, 2, 1, 0, 0, 1, 2))
+    rng = np.random.default_rng(53)
+    masks = [synth.blob_mask_count(d, 90, rng), synth.rect_mask_count(d, 40, rng),
+             synth.blob_mask_count(d, 130, rng), synth.rect_mask_count(d, 70, rng)]
+    alone = [Request(m, 200 + i, mk) for i, mk in enumerate(masks)]
+    batch = [Request(m, 200 + i, mk) for i, mk in enumerate(masks)]
+    tlat = torch.stack([synth.make_latent(d, 996 + s) for s in range(2)])
+    kvc = ig.ig_cache_create(m.ctx, 2, ig.IG_CACHE_HOST)
+    fill_cache(m, kvc, synth.make_cache_kv(d, 14, 2, dtype=torch.bfloat16), tlat)
+    ym = set(ig.y_block_modes(d.n_blocks, 2))
+    hyc = ig.ig_cache_create(mh.ctx, 2, ig.IG_CACHE_HOST)
+    kv2 = synth.make_cache_kv(d, 15, 2, dtype=torch.bfloat16)
+    fill_cache(mh, hyc, hybrid_planes(kv2, synth.make_cache_y(d, 15, 2, dtype=torch.bfloat16), ym), tlat)
+    caches = [hyc, kvc, hyc, kvc]
+    for s in range(2):
+        for i, r in enumerate(alone):
+            ig.ig_edit_step(m.ctx, [r.req(i, caches[i], s, sig[s], sig[s + 1])], 0)
+    for s in range(2):
+        ig.ig_edit_step(m.ctx, [r.req(i, caches[i], s, sig[s], sig[s + 1]) for i, r in enumerate(batch)], 0)
+        assert ig.ig_last_stats(m.ctx)["d2d_bytes"] > 0  # both groups deduplicated
+    torch.cuda.synchronize()
+    for i, (a, b) in enumerate(zip(alone, batch)):
+        assert torch.equal(a.latent, b.latent), i
+    ig.ig_cache_free(kvc)
+    ig.ig_cache_free(hyc)
+    for r in alone + batch:
+        r.free()
+    mh.close()
+    m.close()
