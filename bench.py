@@ -130,43 +130,70 @@ def make_mask(d, rid):
 
 
 class Req:
-    def __init__(self, ig, ctx, d, rid, dev, dense=False):
+    """A request's inputs.  Its mask handle is built at ADMISSION (inside the timed window, by
+    ig_mask_build_host on the step stream: no device sync) and freed when it leaves."""
+
+    def __init__(self, ig, ctx, d, rid, dev, dense=False, host_inputs=False):
         self.rid = rid
         self.latent = synth.make_latent(d, rid, dev).contiguous()
         self.txt = synth.make_txt(d, rid, dev, torch.bfloat16).contiguous()
         self.cond = synth.make_cond(d, rid, dev).contiguous()
+        if host_inputs:  # the public API's host-buffer path: pinned host latents / text / cond
+            self.latent = self.latent.cpu().pin_memory()
+            self.txt = self.txt.cpu().pin_memory()
+            self.cond = self.cond.cpu().pin_memory()
         mk = np.ones(d.L_img, np.uint8) if dense else make_mask(d, rid)
-        self.mask_np = mk
-        self.mask_dev = torch.from_numpy(mk).to(dev)
-        self.mask, self.n_m = ig.ig_mask_build(ctx, self.mask_dev.data_ptr(), 0)  # admission
+        self.mask_np = np.ascontiguousarray(mk, dtype=np.uint8)
+        self.n_m = int(self.mask_np.sum())
+        self.mask = None
         self.step = 0
 
 
 class Batch:
-    """Continuous batching at saturation: max_batch slots, staggered start steps."""
+    """Continuous batching at saturation: max_batch slots, staggered start steps; a request that
+    finishes its last step leaves (mask freed, stream-ordered) and the next one is admitted into
+    the same slot (mask built from the host bitmap; with host inputs its text tokens and cond
+    vector are staged into the slot's device buffers) — all on the step stream."""
 
-    def __init__(self, ig, ctx, d, dev, max_batch, pool_size, rid0, dense=False, lockstep=False):
-        self.ig, self.ctx, self.d = ig, ctx, d
-        self.pool = [Req(ig, ctx, d, rid0 + i, dev, dense) for i in range(pool_size)]
+    def __init__(self, ig, ctx, d, dev, max_batch, pool_size, rid0, stream, dense=False, lockstep=False,
+                 host_inputs=False):
+        self.ig, self.ctx, self.d, self.stream = ig, ctx, d, stream
+        self.host_inputs = host_inputs
+        self.pool = [Req(ig, ctx, d, rid0 + i, dev, dense, host_inputs) for i in range(pool_size)]
+        if host_inputs:
+            self.txt_slot = [torch.empty(d.txt_len, d.hidden, dtype=torch.bfloat16, device=dev) for _ in range(max_batch)]
+            self.cond_slot = [torch.empty(d.hidden, dtype=torch.float32, device=dev) for _ in range(max_batch)]
         self.next = 0
         self.slots = []
+        self.admit_bytes = 0
         for s in range(max_batch):
-            r = self._admit()
+            r = self._admit(s)
             r.step = 0 if lockstep else (s * N_STEPS) // max_batch
             self.slots.append(r)
         self.completed = 0
 
-    def _admit(self):
+    def _admit(self, slot):
         r = self.pool[self.next % len(self.pool)]
         self.next += 1
         r.step = 0
+        st = self.stream.cuda_stream
+        r.mask, _ = self.ig.ig_mask_build_host(self.ctx, r.mask_np, st)
+        self.admit_bytes += r.mask_np.nbytes
+        if self.host_inputs:
+            nt, nc = r.txt.numel() * 2, r.cond.numel() * 4
+            self.ig.ig_stage_input(self.txt_slot[slot].data_ptr(), r.txt.data_ptr(), nt, st)
+            self.ig.ig_stage_input(self.cond_slot[slot].data_ptr(), r.cond.data_ptr(), nc, st)
+            self.admit_bytes += nt + nc
         return r
 
-    def reqs(self, cache, sig, host=None):
-        return [self.ig.make_req(i, (host[r.rid] if host else r.latent).data_ptr(), r.mask, cache, r.step,
-                                 float(sig[r.step]),
-                                 float(sig[r.step + 1]), r.txt.data_ptr(), r.cond.data_ptr())
-                for i, r in enumerate(self.slots)]
+    def reqs(self, cache, sig):
+        out = []
+        for i, r in enumerate(self.slots):
+            txt = self.txt_slot[i] if self.host_inputs else r.txt
+            cond = self.cond_slot[i] if self.host_inputs else r.cond
+            out.append(self.ig.make_req(i, r.latent.data_ptr(), r.mask, cache, r.step, float(sig[r.step]),
+                                        float(sig[r.step + 1]), txt.data_ptr(), cond.data_ptr()))
+        return out
 
     def advance(self):
         done = 0
@@ -174,13 +201,23 @@ class Batch:
             r.step += 1
             if r.step == N_STEPS:
                 done += 1
-                self.slots[i] = self._admit()
+                self.ig.ig_mask_free(r.mask)  # stream-ordered after the step that last read it
+                r.mask = None
+                self.slots[i] = self._admit(i)
         self.completed += done
         return len(self.slots)  # request-steps done this step
 
+    def close(self):
+        for r in self.slots:
+            if r.mask:
+                self.ig.ig_mask_free(r.mask)
+                r.mask = None
 
-def run_loop(ig, ctx, batch, cache, sig, steps, stream, profile=False, e2e=None):
-    """Runs `steps` batch steps on `stream`; returns (ms, request_steps, launches, stats)."""
+
+def run_loop(ig, ctx, batch, cache, sig, steps, stream, profile=False):
+    """Runs `steps` batch steps on `stream` (admissions of joining requests included); returns
+    a Leg.  With profile=True every libig launch is bracketed by CUDA events (diagnostic legs
+    only: the headline value is timed without them)."""
     launches, rsteps = 0, 0
     h2d = d2h = 0
     evs, plans = [], []
@@ -190,30 +227,32 @@ def run_loop(ig, ctx, batch, cache, sig, steps, stream, profile=False, e2e=None)
     end = torch.cuda.Event(enable_timing=True)
     if profile:
         ig.ig_profile_enable(ctx, True)
+    batch.admit_bytes = 0
     start.record(stream)
     for _ in range(steps):
         e0 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        # e2e: the public API on HOST buffers — each request's latent lives in pinned host memory
-        # and the step's gather/scatter kernels read its masked rows and write the updated rows
-        # in place over the host link (no device copy of the latent exists)
-        ig.ig_edit_step(ctx, batch.reqs(cache, sig, e2e), stream.cuda_stream)
+        # host-buffer path (e2e): each request's latent lives in pinned host memory and the step's
+        # gather/scatter kernels read its masked rows and write the updated rows in place over the
+        # host link (no device copy of the latent exists)
+        ig.ig_edit_step(ctx, batch.reqs(cache, sig), stream.cuda_stream)
         plans.append(ig.ig_last_plan(ctx))
         alg_flops += sum(request_step_flops(batch.d, r.n_m) for r in batch.slots)
         st = ig.ig_last_stats(ctx)
         host_s += st["host_ns"] * 1e-9  # library enqueue time, back-pressure waits excluded
         launches += st["kernel_launches"]
         h2d += st["h2d_bytes"]
-        if e2e is not None:
+        if batch.host_inputs:
             rows = sum(r.n_m for r in batch.slots) * batch.d.lat_ch * 4
             h2d += 2 * rows  # masked latent rows read by the gather and by the Euler update
             d2h += rows      # updated masked rows written back
         e1 = torch.cuda.Event(enable_timing=True)
         e1.record(stream)
         evs.append((e0, e1))
-        rsteps += batch.advance()
+        rsteps += batch.advance()  # leaving requests' masks freed, joiners admitted (on the stream)
     end.record(stream)
     end.synchronize()
+    h2d += batch.admit_bytes  # joiners' bitmaps (+ text tokens / cond vectors on the host path)
     prof = ig.ig_profile_read(ctx) if profile else None
     if profile:
         ig.ig_profile_enable(ctx, False)
@@ -268,13 +307,12 @@ def fit_latency(ig, ctx, d, dev, stream, link_gbs):
     from paper_2505_20600_b200.placement import block_flops, fit_ols
     pts = []
     for nb_ in (2, 4):
-        bt = Batch(ig, ctx, d, dev, nb_, nb_, rid0=900000 + nb_, dense=True)
+        bt = Batch(ig, ctx, d, dev, nb_, nb_, 900000 + nb_, stream, dense=True)
         run_loop(ig, ctx, bt, None, synth.flow_sigmas(N_STEPS), 1, stream)
         lg = run_loop(ig, ctx, bt, None, synth.flow_sigmas(N_STEPS), 2, stream)
         per_block_ms = statistics.median(lg.per_step) / d.n_blocks
         pts.append((nb_ * block_flops(d, d.L_img), per_block_ms * 1e-3))
-        for r in bt.pool:
-            ig.ig_mask_free(r.mask)
+        bt.close()
     a_c, b_c, _ = fit_ols([p[0] for p in pts], [p[1] for p in pts])
     return a_c, max(b_c, 0.0), 1.0 / (link_gbs * 1e9), 0.0
 
@@ -349,39 +387,105 @@ def torch_dense_block_ms(d, dev, rows, iters=5):
     return e0.elapsed_time(e1) / iters
 
 
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def cpu_baseline(d):
+    """The float64 oracle as it stands, on this box's host cores (a reported baseline, SURVEY
+    §8(d)): one Flux double + one single block (all threads; extrapolated to images/s), one
+    single block on ONE thread, one SD3-medium block at m = 0.3, and the tiny config end to end."""
+    import oracle
+    from threadpoolctl import threadpool_limits
     td, ts, n_m = oracle_sample(d, 0.2)
     step_s = d.n_double * td + d.n_single * ts
+    W = oracle_weights(d)
+    with threadpool_limits(1):
+        t0 = time.perf_counter()
+        H = d.hidden
+        rng = np.random.default_rng(1)
+        mask = synth.rect_mask_count(d, n_m, rng)
+        idx_m, idx_u, _ = oracle.index_build(mask)
+        oracle.single_block_masked(d, W, 0, rng.standard_normal((d.txt_len + n_m, H)), rng.standard_normal(H),
+                                   idx_m, idx_u, rng.standard_normal((2, d.L_img, H)))
+        ts1 = time.perf_counter() - t0
+    # SD3-medium block (config 2), m = 0.3, all threads
+    sd3 = synth.SD3
+    names = {n for n, _, _ in synth.weight_table(sd3) if n.startswith("double.0.")}
+    Ws = {k: v.double().numpy() for k, v in synth.make_weights(sd3, 0, "cpu", torch.bfloat16, names=names).items()}
+    rng = np.random.default_rng(2)
+    mask = synth.blob_mask_count(sd3, int(round(0.3 * sd3.L_img)), rng)
+    idx_m, idx_u, nm3 = oracle.index_build(mask)
+    t0 = time.perf_counter()
+    oracle.double_block_masked(sd3, Ws, 0, rng.standard_normal((sd3.txt_len, sd3.hidden)),
+                               rng.standard_normal((nm3, sd3.hidden)), rng.standard_normal(sd3.hidden),
+                               idx_m, idx_u, rng.standard_normal((2, sd3.L_img, sd3.hidden)))
+    t_sd3 = time.perf_counter() - t0
+    # tiny config end to end (config 1): record the 2-step template, then the 2 edit steps
+    tiny = synth.TINY
+    Wt = {k: v.double().numpy() for k, v in synth.make_weights(tiny, 0).items()}
+    lat = synth.make_latent(tiny, 0).double().numpy()
+    txt = synth.make_txt(tiny, 0).double().numpy()
+    cond = synth.make_cond(tiny, 0).double().numpy()
+    sig = [1.0, 0.5, 0.0]
+    t0 = time.perf_counter()
+    _, cache, _ = oracle.cache_template(tiny, Wt, lat, txt, cond, sig)
+    x = lat
+    for st_ in range(2):
+        x = oracle.edit_step(tiny, Wt, x, synth.tiny_rect_mask(), cache[st_], sig[st_], sig[st_ + 1], txt, cond)
+    t_tiny = time.perf_counter() - t0
     return {"value": 1.0 / (N_STEPS * step_s), "unit": "images/s", "cores": cpu_cores(), "kind": "oracle",
+            "cpu_model": cpu_model(),
             "sample": f"float64 NumPy oracle: one Flux double block ({td:.2f} s) + one single block "
-                      f"({ts:.2f} s), 1 request, m=0.2 (n_m={n_m}); extrapolated x(19 double + 38 single) "
-                      f"x 28 steps per image"}
+                      f"({ts:.2f} s), 1 request, m=0.2 (n_m={n_m}), all cores; extrapolated x(19 double + 38 single) "
+                      f"x 28 steps per image",
+            "flux_single_block_1_thread_s": round(ts1, 3),
+            "flux_step_extrapolated_s": round(step_s, 2),
+            "sd3_block_m0.3_s": round(t_sd3, 3),
+            "tiny_config_e2e_s": round(t_tiny, 3),
+            "tiny_note": "config 1: 2-step dense template recording + 2 masked edit steps (fp64)"}
+
+
+def workload_config(d, args, world):
+    """The workload (identical for our arm at every N and for the reference arm)."""
+    return {"workload": f"{d.name} ({d.L_img} img + {d.txt_len} txt tokens, 1024^2), 28-step flow schedule, "
+                        f"continuous batching max_batch {args.max_batch} per GPU (staggered steps, a finished "
+                        f"request leaves and a new one joins), masks m~U[{args.mask_lo},{args.mask_hi}] "
+                        f"({'rect/blob' if args.mask_kind == 'mixed' else 'blob'})",
+            "global_batch": args.max_batch * world, "seq_len": d.L, "parallelism": f"replica{world}"}
 
 
 def run_reference(args, rank):
+    """--impl reference: the float64 oracle as it stands on the host cores, on a bounded sample
+    of the same workload (one Flux double + one single block per step at the mix's mean m),
+    extrapolated to images/s.  Under torchrun only rank 0 runs it."""
     if rank != 0:
         return
-    d = synth.FLUX
+    d = synth.MODELS[args.model]
     W = oracle_weights(d)
     per = []
+    m_mean = 0.5 * (args.mask_lo + args.mask_hi)
     for i in range(args.warmup + args.steps):
-        td, ts, n_m = oracle_sample(d, 0.325, seed=i, W=W)
+        td, ts, n_m = oracle_sample(d, m_mean, seed=i, W=W)
         if i >= args.warmup:
             per.append((td, ts))
     td = float(np.mean([p[0] for p in per]))
     ts = float(np.mean([p[1] for p in per]))
     img_s = 1.0 / (N_STEPS * (d.n_double * td + d.n_single * ts))
-    cb = {"value": img_s, "unit": "images/s", "cores": cpu_cores(), "kind": "oracle",
-          "sample": "per step: one Flux double + one single block, 1 request at m=0.325, float64 "
+    cb = {"value": img_s, "unit": "images/s", "cores": cpu_cores(), "kind": "oracle", "cpu_model": cpu_model(),
+          "sample": f"per step: one Flux double + one single block, 1 request at m={m_mean:.3f}, float64 "
                     "oracle; extrapolated x(19+38) blocks x 28 steps"}
     print(json.dumps({"impl": "reference", "metric": METRIC, "value": img_s, "unit": "images/s",
                       "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
                       "ms_per_step": 1e3 * (td + ts), "higher_is_better": True, "scaling": "weak",
                       "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                      "config": {"workload": "flux1_dev 1024^2 (4096 img + 512 txt tokens), 28-step flow schedule, "
-                                             "masks m~U[0.05,0.60] (mean 0.325); float64 oracle on a bounded sample",
-                                 "global_batch": 1, "seq_len": d.L, "parallelism": "cpu"},
-                      "cpu_baseline": cb,
+                      "config": workload_config(d, args, 1), "cpu_baseline": cb,
                       "e2e": {"value": img_s, "unit": "images/s", "h2d_bytes_per_step": 0,
                               "d2h_bytes_per_step": 0}}))
 
@@ -394,7 +498,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=4)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--max-batch", type=int, default=8)
-    ap.add_argument("--tier", default=None, choices=["host", "device"])
+    ap.add_argument("--tier", default="host", choices=["host", "device"])
     ap.add_argument("--copy-mode", type=int, default=1)
     ap.add_argument("--depth", type=int, default=8)
     ap.add_argument("--plan", default="model", help="Algorithm-1 dense prefix: model | none | <k>")
@@ -405,10 +509,9 @@ def main():
     ap.add_argument("--no-hbm-tier", action="store_true", help="skip the HBM-resident template run")
     ap.add_argument("--no-fp8", action="store_true", help="skip the FP8-cache run")
     ap.add_argument("--no-y", action="store_true", help="skip the other-cache-kind runs")
-    ap.add_argument("--no-profile", action="store_true", help="no per-launch event timing in the timed window")
+    ap.add_argument("--no-prof-leg", action="store_true", help="skip the profiled (per-kernel) leg")
     ap.add_argument("--no-lockstep", action="store_true", help="skip the lockstep (deduplicated loads) run")
-    ap.add_argument("--graphs", action="store_true",
-                    help="replay steps as CUDA graphs (HBM-resident caches; needs --no-profile to take effect)")
+    ap.add_argument("--graphs", action="store_true", help="replay steps as CUDA graphs (HBM-resident caches)")
     ap.add_argument("--cache", default=None, choices=["kv", "hybrid", "y"],
                     help="headline cache kind: K/V, hybrid K/V + Y (interleaved Y blocks), Y")
     ap.add_argument("--kv-blocks", type=int, default=-1, help="hybrid: blocks keeping K/V (-1: latency-model choice)")
@@ -438,7 +541,7 @@ def main():
     from paper_2505_20600_b200 import ig
     ig.lib()
     d = synth.MODELS[args.model]
-    tier = args.tier or ("host" if world == 1 else "device")
+    tier = args.tier  # the same tier and cache kind at every N (weak scaling of one workload)
     hbm, pk_burst, pk_sus, pk_src = peaks()
 
     t_setup = time.time()
@@ -464,16 +567,40 @@ def main():
         o = ig.ig_ctx_opts(args.max_batch, args.max_batch * d.L, args.depth, args.copy_mode, 0, 0, 1, kv_blocks)
         return ig.ig_ctx_create(ig.make_desc(d, ig.IG_BF16), ptrs, local, o)
 
-    # Algorithm-1/2 latency models fitted on this GPU; the hybrid split point
-    a_c, b_c, a_l, b_l = fit_latency(ig, ctx_kv, d, dev, stream, link_peak)
-    kv_auto = choose_kv_blocks(d, a_c, b_c, a_l, args.max_batch, 0.5 * (args.mask_lo + args.mask_hi))
+    # Algorithm-1/2 latency models fitted on this GPU; the hybrid split point.  Under
+    # torchrun rank 0's fit is broadcast so that every rank uses the same cache layout.
+    fit = list(fit_latency(ig, ctx_kv, d, dev, stream, link_peak))
+    kv_auto = choose_kv_blocks(d, fit[0], fit[1], fit[2], args.max_batch, 0.5 * (args.mask_lo + args.mask_hi))
+    if world > 1:
+        t = torch.tensor(fit + [float(kv_auto)], dtype=torch.float64, device=dev if not share else "cpu")
+        torch.distributed.broadcast(t, 0)
+        fit, kv_auto = [float(x) for x in t[:4]], int(t[4])
+    a_c, b_c, a_l, b_l = fit
     # default: the hybrid split for a host-tier cache (the link is the other lane); plain K/V
     # when the cache is HBM-resident (the loads are on-chip gathers, Y would only add compute)
     cache_kind = args.cache or ("hybrid" if tier == "host" else "kv")
     kv_blocks = {"kv": None, "y": 0}.get(cache_kind, kv_auto if args.kv_blocks < 0 else args.kv_blocks)
     ctx = ctx_kv if kv_blocks is None else make_y_ctx(kv_blocks)
     t0 = time.time()
-    cache = record(ctx, tier)
+    seg = None
+    if world > 1 and tier == "host":
+        # one host copy of the template per box, mapped by every rank: rank 0
+        # records it into a shared segment, the others attach after it finished
+        from paper_2505_20600_b200.shared_cache import SharedSegment, share_handle
+        nbytes = ig.ig_cache_bytes(ctx, N_STEPS)
+        if rank == 0:
+            seg = SharedSegment.create(nbytes, "ig_flux_template")
+            cache = ig.ig_cache_attach(ctx, N_STEPS, seg.address, nbytes)
+            tl = synth.make_latent(d, 10 ** 6, dev)
+            ig.ig_cache_template_into(ctx, tl.data_ptr(), tt.data_ptr(), tc.data_ptr(), sig, cache, 0)
+        handle = share_handle(seg, rank)
+        if rank != 0:
+            seg = SharedSegment.attach(handle)
+            cache = ig.ig_cache_attach(ctx, N_STEPS, seg.address, nbytes)
+        cache_mem = "one shared pinned host segment per box (memfd, cudaHostRegister per rank)"
+    else:
+        cache = record(ctx, tier)
+        cache_mem = "pinned host (cudaHostAlloc)" if tier == "host" else "HBM"
     t_template = time.time() - t0
     torch.cuda.synchronize()
 
@@ -484,7 +611,7 @@ def main():
         torch.cuda.synchronize()
 
     def reduce_max_sum(ms_, rs_):
-        t = torch.tensor([ms_, float(rs_)], dtype=torch.float64, device=dev)
+        t = torch.tensor([ms_, float(rs_)], dtype=torch.float64, device=dev if not share else "cpu")
         if world > 1:
             mx = t.clone()
             torch.distributed.all_reduce(mx, op=torch.distributed.ReduceOp.MAX)
@@ -493,70 +620,77 @@ def main():
             return float(mx[0]), float(sm[1])
         return ms_, float(rs_)
 
-    def leg(c, cch, profile=True, e2e=False, clk=None, lockstep=False):
+    def leg(c, cch, profile=False, host_inputs=False, clk=None, lockstep=False):
         """One measured configuration: a fresh batch replaying the same request sequence,
-        W warm-up steps, then K timed steps between barriers."""
-        bt = Batch(ig, c, d, dev, args.max_batch, pool, rid0=rank * 100000, lockstep=lockstep)
+        W warm-up steps, then K timed steps between barriers (admissions inside the window)."""
+        bt = Batch(ig, c, d, dev, args.max_batch, pool, rank * 100000, stream, lockstep=lockstep,
+                   host_inputs=host_inputs)
         run_loop(ig, c, bt, cch, sig, args.warmup, stream)
-        hb = {r.rid: r.latent.detach().cpu().pin_memory() for r in bt.pool} if e2e else None
         barrier()
         if clk:
             clk.start()
-        lg = run_loop(ig, c, bt, cch, sig, args.steps, stream, profile=profile, e2e=hb)
+        lg = run_loop(ig, c, bt, cch, sig, args.steps, stream, profile=profile)
         barrier()
         lg.clk = clk.stop() if clk else None
         lg.ms_max, lg.rs_all = reduce_max_sum(lg.ms, lg.rsteps)
         lg.value = lg.rs_all / N_STEPS / (lg.ms_max / 1e3)
-        for r in bt.pool:
-            ig.ig_mask_free(r.mask)
+        bt.close()
+        torch.cuda.synchronize()
         return lg
 
     def summary(lg):
-        return {"value": round(lg.value, 4), "unit": "images/s", "ms_per_step": round(lg.ms / args.steps, 3),
-                "gemm_tflops": round(lg.tflops("gemm"), 1), "attn_tflops": round(lg.tflops("attn"), 1),
-                "host_link_GBps": round(lg.h2d / (lg.ms * 1e-3) / 1e9, 2),
-                "plan_k": {"min": min(lg.plans), "max": max(lg.plans),
-                           "mean": round(float(np.mean(lg.plans)), 2)},
-                "alg_tensor_frac": round(lg.alg_flops / (lg.ms * 1e-3) / 1e12 / pk_sus, 4),
-                "copy_lane_busy": round(lg.prof["copy"]["ms"] / lg.ms, 4),
-                "kernel_share_of_step": {k: round(v["ms"] / lg.ms, 4) for k, v in lg.prof.items() if k != "copy"}}
+        out = {"value": round(lg.value, 4), "unit": "images/s", "ms_per_step": round(lg.ms / args.steps, 3),
+               "host_link_GBps": round(lg.h2d / (lg.ms * 1e-3) / 1e9, 2),
+               "plan_k": {"min": min(lg.plans), "max": max(lg.plans), "mean": round(float(np.mean(lg.plans)), 2)},
+               "alg_tensor_frac": round(lg.alg_flops / (lg.ms * 1e-3) / 1e12 / pk_sus, 4)}
+        if lg.prof:
+            out.update({"gemm_tflops": round(lg.tflops("gemm"), 1), "attn_tflops": round(lg.tflops("attn"), 1),
+                        "copy_lane_busy": round(lg.prof["copy"]["ms"] / lg.ms, 4)})
+        return out
 
-    # the headline: the mask-aware step with the per-step dense-prefix plan (N1), cache in
-    # pinned host memory
     plan_mode = {"model": 2, "none": 0}.get(args.plan, 1)
-    ig.ig_set_plan(ctx, plan_mode, 0 if plan_mode != 1 else int(args.plan), a_c, b_c, a_l, b_l)
-    main_leg = leg(ctx, cache, clk=Clocks(local), profile=not args.no_profile)
-    if main_leg.prof is None:  # --no-profile (diagnostic): no per-kernel numbers
-        main_leg.prof = {k: {"ms": 0.0, "flops": 0.0, "bytes": 0.0, "launches": 0} for k in ig.KCLASS}
-    ms, ms_max, value, prof, per_step = main_leg.ms, main_leg.ms_max, main_leg.value, main_leg.prof, main_leg.per_step
+
+    def set_plan(c, mode=None):
+        m_ = plan_mode if mode is None else mode
+        ig.ig_set_plan(c, m_, 0 if m_ != 1 else int(args.plan), a_c, b_c, a_l, b_l)
+
+    # ---- the headline: the mask-aware step with the per-step dense-prefix plan (N1), cache in
+    # pinned host memory, timed with NO per-launch instrumentation
+    set_plan(ctx)
+    main_leg = leg(ctx, cache, clk=Clocks(local))
+    ms, ms_max, value, per_step = main_leg.ms, main_leg.ms_max, main_leg.value, main_leg.per_step
     launches, h2d, clk = main_leg.launches, main_leg.h2d, main_leg.clk
 
-    # end to end through the public API with host buffers (latent H2D + D2H every step)
+    # ---- the same workload through the public API's HOST-buffer path: latents, text tokens and
+    # cond vectors in pinned host memory (masked latent rows gathered / updated over the link,
+    # text + cond staged into device slots at admission); otherwise identical to the headline
     e2e = None
     if not args.no_e2e:
-        le = leg(ctx, cache, profile=False, e2e=True)
+        le = leg(ctx, cache, host_inputs=True)
         e2e = {"value": le.value, "unit": "images/s",
-               "h2d_bytes_per_step": int(le.h2d / args.steps), "d2h_bytes_per_step": int(le.d2h / args.steps)}
+               "h2d_bytes_per_step": int(le.h2d / args.steps), "d2h_bytes_per_step": int(le.d2h / args.steps),
+               "note": "h2d counts the cache bytes the step streams from host memory, the masked latent rows "
+                       "read over the link, and the joiners' mask bitmaps, text tokens and cond vectors"}
 
-    # the same workload without the plan (every block uses the cache: the K/V variant alone)
-    noplan = None
-    if plan_mode != 0 and tier == "host" and world == 1:
-        ig.ig_set_plan(ctx, 0, 0, 0.0, 0.0, 0.0, 0.0)
-        noplan = summary(leg(ctx, cache))
-        ig.ig_set_plan(ctx, plan_mode, 0 if plan_mode != 1 else int(args.plan), a_c, b_c, a_l, b_l)
+    # ---- per-kernel roofline: the same workload again with every launch bracketed by events
+    prof = None
+    if not args.no_prof_leg:
+        pl = leg(ctx, cache, profile=True)
+        prof_ms, prof = pl.ms, pl.prof
+        prof_leg = pl
 
-    # the same workload with the template cache resident in HBM (hot-template tier, SURVEY N4)
-    hbm = None
+    ablation = None
+    hbm = lockstep = fp8 = None
+    alt = {}
+    # ---- the same workload with the template cache resident in HBM (hot-template tier, N4)
     if tier == "host" and not args.no_hbm_tier and world == 1:
         dcache = ig.ig_cache_clone(ctx, cache, ig.IG_CACHE_DEVICE)
-        ig.ig_set_plan(ctx, 0, 0, 0.0, 0.0, 0.0, 0.0)  # nothing to balance: no host link
+        set_plan(ctx, 0)  # nothing to balance: no host link
         hbm = summary(leg(ctx, dcache))
-        ig.ig_set_plan(ctx, plan_mode, 0 if plan_mode != 1 else int(args.plan), a_c, b_c, a_l, b_l)
+        set_plan(ctx)
         ig.ig_cache_free(dcache)
 
-    # a lockstep batch (all requests on the same template and step, e.g. a burst of edits of one
-    # hot template): requests share their staged rows (load deduplication, SURVEY N4)
-    lockstep = None
+    # ---- a lockstep batch (all requests on one template step): load deduplication (N4)
     if tier == "host" and world == 1 and not args.no_lockstep:
         ls = leg(ctx, cache, lockstep=True)
         lockstep = summary(ls)
@@ -565,130 +699,153 @@ def main():
                             "replaced by lockstep); rows already staged by an earlier request of the batch are "
                             "copied HBM->HBM instead of crossing the host link")
 
-    ig.ig_cache_free(cache)  # host memory for the next legs' templates
+    if seg is None:
+        ig.ig_cache_free(cache)  # host memory for the next legs' templates
+        cache = None
 
-    # FP8 (e4m3) K/V cache in pinned host memory (SURVEY N4 byte reducer): a context whose
-    # caches are e4m3 + per-(token, head) scales, recorded directly; same request sequence
-    fp8 = None
+    # ---- N1 ablation on the north-star K/V form (fig:pipeline_load P:541-560):
+    # sequential loading vs the pipelined ring vs the Algorithm-1 plan, pure K/V cache from host
+    if tier == "host" and world == 1:
+        ca = record(ctx_kv, "host")
+        ablation = {}
+        ig.ig_debug_set(ctx_kv, ig.IG_DBG_SEQUENTIAL, 1)
+        set_plan(ctx_kv, 0)
+        ablation["sequential_load"] = summary(leg(ctx_kv, ca))
+        ig.ig_debug_set(ctx_kv, ig.IG_DBG_SEQUENTIAL, 0)
+        ablation["pipelined_ring"] = summary(leg(ctx_kv, ca))
+        set_plan(ctx_kv)
+        ablation["pipelined_planned"] = summary(leg(ctx_kv, ca, profile=True))
+        ablation["note"] = ("pure bf16 K/V cache (the north-star form) from pinned host memory: sequential = "
+                            "block b's copy starts after block b-1 computed (no overlap); pipelined = ring of "
+                            f"{args.depth + 1} buffers, copies run ahead; planned = + Algorithm-1 dense prefix")
+        ig.ig_cache_free(ca)
+        set_plan(ctx_kv, 0)
+
+    # ---- FP8 (e4m3) K/V cache in pinned host memory (N4 byte reducer)
     if tier == "host" and not args.no_fp8 and world == 1:
         opts8 = ig.ig_ctx_opts(args.max_batch, args.max_batch * d.L, args.depth, args.copy_mode, 0, 1)
         ctx8 = ig.ig_ctx_create(ig.make_desc(d, ig.IG_BF16), ptrs, local, opts8)
         cache8 = record(ctx8, "host")
-        ig.ig_set_plan(ctx8, plan_mode, 0 if plan_mode != 1 else int(args.plan), a_c, b_c, a_l, b_l)
+        set_plan(ctx8)
         fp8 = summary(leg(ctx8, cache8))
         fp8["note"] = ("same workload, K/V cache stored as e4m3 + fp32 scale per (token, head): "
                        "half the host-link bytes")
         ig.ig_cache_free(cache8)
         ig.ig_ctx_destroy(ctx8)
 
-    # the other cache kinds on the same workload: K/V only (fig:transformer_alter) when the
-    # headline uses a Y/hybrid cache, the hybrid K/V + Y cache otherwise
-    alt = {}
-    if tier == "host" and not args.no_y and world == 1:
-        kinds = [("kv_cache_host_tier", None)] if kv_blocks is not None else [("hybrid_cache_host_tier", kv_auto)]
-        if kv_blocks != 0:
-            kinds.append(("y_cache_host_tier", 0))
-        for name, yf in kinds:
-            cx = ctx_kv if yf is None else make_y_ctx(yf)
-            ca = record(cx, "host")
-            ig.ig_set_plan(cx, plan_mode, 0 if plan_mode != 1 else int(args.plan), a_c, b_c, a_l, b_l)
-            alt[name] = summary(leg(cx, ca))
-            alt[name]["kv_blocks"] = yf
-            ig.ig_cache_free(ca)
-            if cx is not ctx_kv:
-                ig.ig_set_plan(cx, 0, 0, 0.0, 0.0, 0.0, 0.0)
-                ig.ig_ctx_destroy(cx)
+    # ---- the pure Y cache (the paper's primary form) on the same workload
+    if tier == "host" and not args.no_y and world == 1 and kv_blocks != 0:
+        cx = make_y_ctx(0)
+        ca = record(cx, "host")
+        set_plan(cx)
+        alt["y_cache_host_tier"] = summary(leg(cx, ca))
+        ig.ig_cache_free(ca)
+        ig.ig_ctx_destroy(cx)
 
-    # dense comparison step (all-ones masks, no cache) on the same GPUs and kernels
+    # ---- dense comparison step (all-ones masks, no cache) on the same GPUs and kernels
     dense = None
     torch_ctx = None
     if args.dense_steps > 0:
-        dbatch = Batch(ig, ctx_kv, d, dev, args.max_batch, args.max_batch + 2, rid0=rank * 100000 + 50000, dense=True)
+        dbatch = Batch(ig, ctx_kv, d, dev, args.max_batch, args.max_batch + 2, rank * 100000 + 50000, stream,
+                       dense=True)
         run_loop(ig, ctx_kv, dbatch, None, sig, 1, stream)
         barrier()
         ld = run_loop(ig, ctx_kv, dbatch, None, sig, args.dense_steps, stream)
         barrier()
+        dbatch.close()
         ms_d, rs_d = reduce_max_sum(ld.ms, ld.rsteps)
         dense = rs_d / N_STEPS / (ms_d / 1e3)
         dense_block_ms = ld.ms / args.dense_steps / d.n_blocks
-        torch_ctx = None
         if world == 1 and d.n_single > 0:
             torch_ctx = {"torch_single_block_ms": round(torch_dense_block_ms(d, dev, args.max_batch * d.L), 3),
                          "ours_dense_step_ms_per_block": round(dense_block_ms, 3),
                          "note": "context only: plain PyTorch (cuBLAS + SDPA) Flux single block over the dense "
                                  "batch; ours = whole dense step / blocks (includes conditioning, RoPE, QK-norm)"}
 
+    if seg is not None:
+        barrier()
+        ig.ig_cache_free(cache)
+        barrier()
+        seg.close()
+
     if rank != 0:
         if world > 1:
             torch.distributed.barrier()
         return
     traffic = {}
-    tp = os.path.join(ROOT, "profiles", "gemm_traffic.json")
-    if os.path.exists(tp):
-        traffic = json.load(open(tp))
-    gemm_tf = main_leg.tflops("gemm")
-    attn_tf = main_leg.tflops("attn")
-    exec_flops = prof["gemm"]["flops"] + prof["attn"]["flops"]
+    for tp in ("r02_gemm_traffic.json", "gemm_traffic.json"):
+        pth = os.path.join(ROOT, "profiles", tp)
+        if os.path.exists(pth):
+            traffic = json.load(open(pth))
+            break
+    cfg = workload_config(d, args, world)
+    cfg["impl"] = (f"{'K/V' if kv_blocks is None else ('Y' if kv_blocks == 0 else f'hybrid K/V+Y ({kv_blocks} K/V blocks, {d.n_blocks - kv_blocks} Y blocks interleaved)')} "
+                   f"cache tier={tier} ({cache_mem}) copy_mode={args.copy_mode} depth={args.depth} plan={args.plan}")
+    cfg["l2"] = "inputs larger than L2 (23.7 GB weights + ~2 GB cached K/V/Y per request-step streamed)"
     step_ms = ms / args.steps
-    shares = {k: round(v["ms"] / args.steps / step_ms, 4) for k, v in prof.items() if k != "copy"}
     out = {
         "metric": METRIC, "value": round(value, 4), "unit": "images/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
-        "data": "synthetic",
-        "config": {"workload": f"{d.name} ({d.L_img} img + {d.txt_len} txt tokens), 28-step flow schedule, "
-                               f"continuous batching max_batch {args.max_batch}, masks m~U[{args.mask_lo},{args.mask_hi}] "
-                               f"({'rect/blob' if args.mask_kind == 'mixed' else 'blob'}), "
-                               f"{'K/V' if kv_blocks is None else ('Y' if kv_blocks == 0 else f'hybrid K/V+Y ({kv_blocks} K/V blocks, {d.n_blocks - kv_blocks} Y blocks interleaved)')} "
-                               f"cache tier={tier} copy_mode={args.copy_mode} depth={args.depth} plan={args.plan}",
-                   "global_batch": args.max_batch * world, "seq_len": d.L, "parallelism": f"replica{world}",
-                   "l2": "inputs larger than L2 (23.7 GB weights + 2.9 GB K/V per request-step streamed)"},
-        "roofline": {"bound": "tensor", "kernel": "gemm_tc (tcgen05 bf16)", "achieved": round(gemm_tf, 1),
-                     "peak": pk_sus, "unit": "TFLOP/s", "frac": round(gemm_tf / pk_sus, 4),
-                     "traffic": traffic.get("dram_bytes_per_launch"),
-                     "traffic_note": traffic.get("note"),
-                     "peak_kind": f"bf16 sustained ({pk_src})",
-                     "frac_of_burst": round(gemm_tf / pk_burst, 4)},
-        "attn_roofline": {"achieved": round(attn_tf, 1), "unit": "TFLOP/s", "frac": round(attn_tf / pk_sus, 4)},
-        "kernel_share_of_step": shares,
-        "compute_lane_busy": round(sum(v["ms"] for k, v in prof.items() if k != "copy") / ms, 4),
-        "step_roofline": {"bound": "tensor", "unit": "TFLOP/s", "peak": pk_sus,
-                          "alg_tflop_per_step": round(main_leg.alg_flops / args.steps / 1e12, 2),
-                          "achieved": round(main_leg.alg_flops / (ms * 1e-3) / 1e12, 1),
-                          "frac": round(main_leg.alg_flops / (ms * 1e-3) / 1e12 / pk_sus, 4),
-                          "executed_frac": round(exec_flops / (ms * 1e-3) / 1e12 / pk_sus, 4),
-                          "note": "all-cache algorithmic FLOPs (Table 1 scaling, SURVEY 8(d) F(m)) of the "
-                                  "request-steps in the window / window time; executed_frac counts the "
-                                  "FLOPs actually run (dense-prefix blocks included)"},
-        "plan": {"mode": args.plan, "k": {"min": min(main_leg.plans), "max": max(main_leg.plans),
-                                          "mean": round(float(np.mean(main_leg.plans)), 2)},
-                 "latency_model": {"comp_s_per_tflop": round(a_c * 1e12, 6), "comp_s": round(b_c, 6),
-                                   "load_s_per_GB": round(a_l * 1e9, 6), "load_s": b_l}},
-        "no_plan_host_tier": noplan,
-        "per_step_ms": {"median": round(statistics.median(per_step), 3),
-                        "p10": round(float(np.percentile(per_step, 10)), 3),
-                        "p90": round(float(np.percentile(per_step, 90)), 3)},
-        "dense_images_per_s": round(dense, 4) if dense else None,
-        "dense_vs_torch_context": torch_ctx,
-        "speedup_vs_dense": round(value / dense, 3) if dense else None,
-        "host_link": {"achieved_GBps": round(h2d / (ms * 1e-3) / 1e9, 2), "peak_GBps": link_peak,
-                      "frac": round(h2d / (ms * 1e-3) / 1e9 / link_peak, 4) if link_peak else None,
-                      "peak_kind": "pinned H2D cudaMemcpyAsync 512 MiB x8, measured in this run",
-                      "copy_lane_busy": round(prof["copy"]["ms"] / ms, 4) if prof["copy"]["ms"] else None,
-                      "GBps_while_busy": round(prof["copy"]["bytes"] / (prof["copy"]["ms"] * 1e-3) / 1e9, 2)
-                      if prof["copy"]["ms"] else None},
-        "hbm_tier": hbm,
-        "fp8_cache_host_tier": fp8,
-        "lockstep_dedupe_host_tier": lockstep,
-        **alt,
-        "speedup_hbm_tier_vs_dense": round(hbm["value"] / dense, 3) if (hbm and dense) else None,
-        "gpu_launches": int(launches),
-        "host_enqueue_ms_per_step": round(main_leg.host_ms_per_step, 3),
-        "clocks": clk,
-        "e2e": e2e,
-        "setup_s": {"total": round(time.time() - t_setup, 1), "template": round(t_template, 1)},
-        "paper_context": "InstGenIE m=0.2 speedups 1.3x SD2.1 (A10), 2.2x SDXL / 1.9x Flux (H800) (P:1003)",
+        "data": "synthetic (random-init Flux.1-dev-shaped weights, seeded latents / text / masks)",
+        "config": cfg,
     }
+    if prof is not None:
+        gemm_tf, attn_tf = prof_leg.tflops("gemm"), prof_leg.tflops("attn")
+        exec_flops = prof["gemm"]["flops"] + prof["attn"]["flops"]
+        out["roofline"] = {"bound": "tensor", "kernel": "gemm_tc2/gemm_tc (tcgen05 bf16)", "achieved": round(gemm_tf, 1),
+                           "peak": pk_sus, "unit": "TFLOP/s", "frac": round(gemm_tf / pk_sus, 4),
+                           "traffic": traffic.get("dram_bytes_per_launch"),
+                           "traffic_note": traffic.get("note"),
+                           "peak_kind": f"bf16 sustained ({pk_src}; kernels timed inside a seconds-long step)",
+                           "frac_of_burst": round(gemm_tf / pk_burst, 4),
+                           "measured_in": "profiled leg: same workload, every launch bracketed by CUDA events"}
+        out["attn_roofline"] = {"achieved": round(attn_tf, 1), "unit": "TFLOP/s", "frac": round(attn_tf / pk_sus, 4)}
+        out["kernel_share_of_step"] = {k: round(v["ms"] / prof_ms, 4) for k, v in prof.items() if k != "copy"}
+        out["compute_lane_busy"] = round(sum(v["ms"] for k, v in prof.items() if k != "copy") / prof_ms, 4)
+        out["profiled_leg"] = {"value": round(prof_leg.value, 4), "ms_per_step": round(prof_ms / args.steps, 3),
+                               "executed_tensor_frac": round(exec_flops / (prof_ms * 1e-3) / 1e12 / pk_sus, 4),
+                               "copy_lane_busy": round(prof["copy"]["ms"] / prof_ms, 4),
+                               "copy_GBps_while_busy": round(prof["copy"]["bytes"] / (prof["copy"]["ms"] * 1e-3) / 1e9, 2)
+                               if prof["copy"]["ms"] else None}
+    out["step_roofline"] = {"bound": "tensor", "unit": "TFLOP/s", "peak": pk_sus,
+                            "alg_tflop_per_step": round(main_leg.alg_flops / args.steps / 1e12, 2),
+                            "achieved": round(main_leg.alg_flops / (ms * 1e-3) / 1e12, 1),
+                            "frac": round(main_leg.alg_flops / (ms * 1e-3) / 1e12 / pk_sus, 4),
+                            "frac_of_burst": round(main_leg.alg_flops / (ms * 1e-3) / 1e12 / pk_burst, 4),
+                            "note": "all-cache algorithmic FLOPs (Table 1 scaling, SURVEY 8(d) F(m)) of the "
+                                    "request-steps in the headline window / window time"}
+    out["plan"] = {"mode": args.plan, "k": {"min": min(main_leg.plans), "max": max(main_leg.plans),
+                                            "mean": round(float(np.mean(main_leg.plans)), 2)},
+                   "latency_model": {"comp_s_per_tflop": round(a_c * 1e12, 6), "comp_s": round(b_c, 6),
+                                     "load_s_per_GB": round(a_l * 1e9, 6), "load_s": b_l}}
+    out["per_step_ms"] = {"median": round(statistics.median(per_step), 3),
+                          "p10": round(float(np.percentile(per_step, 10)), 3),
+                          "p90": round(float(np.percentile(per_step, 90)), 3)}
+    out["dense_images_per_s"] = round(dense, 4) if dense else None
+    out["speedup_vs_dense"] = round(value / dense, 3) if dense else None
+    out["host_link"] = {"achieved_GBps": round(h2d / (ms * 1e-3) / 1e9, 2), "peak_GBps": link_peak,
+                        "frac": round(h2d / (ms * 1e-3) / 1e9 / link_peak, 4) if link_peak else None,
+                        "peak_kind": "pinned H2D cudaMemcpyAsync 512 MiB x8, measured in this run"}
+    # the cache forms side by side, the north-star K/V form first (SURVEY §8(d) feasibility)
+    if ablation is not None:
+        out["cache_forms_host_tier"] = {
+            "kv_bf16_planned (north-star form)": ablation["pipelined_planned"],
+            "fp8_kv": fp8,
+            "hybrid_kv_y (headline)": {"value": round(value, 4), "ms_per_step": round(step_ms, 3)},
+            "y_bf16": alt.get("y_cache_host_tier"),
+        }
+        out["n1_ablation"] = ablation
+    out["hbm_tier"] = hbm
+    out["lockstep_dedupe_host_tier"] = lockstep
+    out["dense_vs_torch_context"] = torch_ctx
+    out["speedup_hbm_tier_vs_dense"] = round(hbm["value"] / dense, 3) if (hbm and dense) else None
+    out["gpu_launches"] = int(launches)
+    out["host_enqueue_ms_per_step"] = round(main_leg.host_ms_per_step, 3)
+    out["clocks"] = clk
+    out["e2e"] = e2e
+    out["setup_s"] = {"total": round(time.time() - t_setup, 1), "template": round(t_template, 1)}
+    out["paper_context"] = "InstGenIE m=0.2 speedups 1.3x SD2.1 (A10), 2.2x SDXL / 1.9x Flux (H800) (P:1003)"
     if not args.no_cpu_baseline and world == 1:
         out["cpu_baseline"] = cpu_baseline(d)
     print(json.dumps(out))

@@ -161,6 +161,26 @@ ig_status ig_cache_template(ig_ctx* ctx, float* latent, const void* txt, const f
                             const float* sigmas, int n_steps, int tier, void* stream,
                             ig_cache** out);
 
+/* Record the template into an EXISTING cache (e.g. one attached to a shared-memory segment by
+ * ig_cache_attach: one host copy per box, written once, read by every GPU's
+ * process).  Same semantics as ig_cache_template; the cache must have this ctx's cache kind
+ * (K/V, Y or hybrid split; bf16 or fp8) and at least n_steps steps, and no enqueued step may
+ * read it.  Synchronises `stream`. */
+ig_status ig_cache_template_into(ig_ctx* ctx, float* latent, const void* txt, const float* cond_vec,
+                                 const float* sigmas, int n_steps, ig_cache* cache, void* stream);
+
+/* Bytes of a cache of this ctx's cache kind for n_steps steps (planes + per-step template
+ * latents; the size to give a shared segment for ig_cache_attach). */
+ig_status ig_cache_bytes(const ig_ctx* ctx, int n_steps, size_t* bytes);
+
+/* A host-tier cache on CALLER-OWNED host memory (SURVEY §8(e) "template caches live once in host
+ * shared memory; each process maps them with cudaHostRegister"): host_mem (>= ig_cache_bytes,
+ * e.g. a POSIX shared-memory mapping that several processes map) is page-locked and mapped with
+ * cudaHostRegister; the layout is exactly ig_cache_create's.  ig_cache_free unregisters it and
+ * never frees it.  Contents are whatever the memory holds (record it with
+ * ig_cache_template_into in one process, attach in the others after that finished). */
+ig_status ig_cache_attach(ig_ctx* ctx, int n_steps, void* host_mem, size_t bytes, ig_cache** out);
+
 /* Copy of a cache into another tier (e.g. an HBM-resident hot template) in the
  * cache format of `ctx` (a bf16 cache cloned by a cache_fp8 ctx is quantized per (token,
  * head) on the device).  Same schedule.  Synchronous. */
@@ -316,10 +336,13 @@ ig_status ig_debug_dump_kv(ig_ctx* ctx, int slot, int block, void* k_out, void* 
  *   IG_DBG_POISON_RING      immediate (value ignored): synchronise the device and fill every
  *                           slot's K/V ring with NaN; a correct step re-stages every row it
  *                           reads, so its result is unchanged
+ *   IG_DBG_SEQUENTIAL       1 = sequential loading (the ablation of P:299-300 / fig:pipeline_load):
+ *                           block b's cache copy starts only after block b-1 finished computing
+ *                           and block b waits for it — no copy/compute overlap
  * IG_EINVAL on an unknown key or a negative value. */
 typedef enum {
   IG_DBG_SPIN_COPY_NS = 1, IG_DBG_SPIN_COMPUTE_NS = 2, IG_DBG_DROP_RAW = 3, IG_DBG_DROP_WAR = 4,
-  IG_DBG_CORRUPT_ROW = 5, IG_DBG_POISON_RING = 6
+  IG_DBG_CORRUPT_ROW = 5, IG_DBG_POISON_RING = 6, IG_DBG_SEQUENTIAL = 7
 } ig_debug_key;
 ig_status ig_debug_set(ig_ctx* ctx, int key, long long value);
 

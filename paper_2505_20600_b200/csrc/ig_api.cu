@@ -131,6 +131,7 @@ struct ig_cache {
                             // dense prefix: unmasked rows enter from the template's trajectory)
   void* ptr = nullptr;     // pinned host (mapped) or device
   void* dptr = nullptr;    // device-visible pointer (== ptr with UVA)
+  bool registered = false; // caller-provided host memory (ig_cache_attach): unregistered, never freed
   size_t bytes = 0;
   mutable std::atomic<int> pins{0};
   std::atomic<bool> zombie{false};
@@ -296,7 +297,8 @@ extern "C" int ig_weight_count(const ig_model_desc* d) {
 static void free_cache_now(ig_cache* c) {
   if (!c) return;
   if (c->ptr) {
-    if (c->tier == IG_CACHE_HOST) cudaFreeHost(c->ptr);
+    if (c->registered) cudaHostUnregister(c->ptr);
+    else if (c->tier == IG_CACHE_HOST) cudaFreeHost(c->ptr);
     else cudaFree(c->ptr);
   }
   delete c;
@@ -1002,6 +1004,49 @@ static ig_status cache_create_kind(ig_ctx* ctx, int n_steps, int tier, int fp8, 
     delete c;
     return set_err(IG_ENOMEM, "cache allocation of %zu bytes failed: %s", bytes, cudaGetErrorString(e));
   }
+  *out = c;
+  return IG_OK;
+}
+
+extern "C" ig_status ig_cache_bytes(const ig_ctx* ctx, int n_steps, size_t* bytes) {
+  if (!ctx || !bytes) return set_err(IG_EINVAL, "NULL argument");
+  if (n_steps <= 0) return set_err(IG_EINVAL, "n_steps must be positive");
+  const std::vector<uint8_t> m = y_modes(ctx->nb, ctx->o.cache_y, ctx->o.cache_y ? ctx->o.cache_kv_blocks : ctx->nb);
+  *bytes = cache_bytes(ctx, n_steps, ctx->o.cache_fp8, m);
+  return IG_OK;
+}
+
+extern "C" ig_status ig_cache_attach(ig_ctx* ctx, int n_steps, void* host_mem, size_t bytes, ig_cache** out) {
+  if (!ctx || !host_mem || !out) return set_err(IG_EINVAL, "NULL argument");
+  *out = nullptr;
+  if (n_steps <= 0) return set_err(IG_EINVAL, "n_steps must be positive");
+  size_t need = 0;
+  ig_status s = ig_cache_bytes(ctx, n_steps, &need);
+  if (s != IG_OK) return s;
+  if (bytes < need) return set_err(IG_EINVAL, "host_mem holds %zu bytes, the cache needs %zu", bytes, need);
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  ig_cache* c = new ig_cache();
+  c->desc = ctx->d;
+  c->n_steps = n_steps;
+  c->tier = IG_CACHE_HOST;
+  c->device = ctx->device;
+  c->fp8 = ctx->o.cache_fp8;
+  c->y = ctx->o.cache_y;
+  c->kv_blocks = c->y ? std::max(0, std::min(ctx->o.cache_kv_blocks, ctx->nb)) : ctx->nb;
+  c->ymode = y_modes(ctx->nb, c->y, c->kv_blocks);
+  c->step_planes = step_planes(c->ymode);
+  c->bytes = need;
+  if (c->fp8) c->scale_off = (size_t)n_steps * c->step_planes * ctx->Limg * ctx->H;
+  c->lat_off = cache_kv_bytes(ctx, n_steps, c->fp8, c->ymode);
+  cudaError_t e = cudaHostRegister(host_mem, need, cudaHostRegisterMapped | cudaHostRegisterPortable);
+  if (e == cudaSuccess) e = cudaHostGetDevicePointer(&c->dptr, host_mem, 0);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    delete c;
+    return set_err(IG_ECUDA, "cudaHostRegister of %zu bytes failed: %s", need, cudaGetErrorString(e));
+  }
+  c->ptr = host_mem;
+  c->registered = true;
   *out = c;
   return IG_OK;
 }
@@ -1761,7 +1806,11 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
 
   // ---- prefetch the first R cached blocks (copy lane); dense-prefix blocks need no cache ----
   const int bc0 = std::max(b0, kplan);
-  for (int b = bc0; b < std::min(bc0 + R, b1); ++b) issue_copy(ctx, sr, dkvg, dkvq, b, plan);
+  // sequential loading (Algorithm-1 ablation, fig:pipeline_load): block b's cache copy
+  // starts only after block b-1 finished computing, and block b waits for it (no overlap)
+  const bool seq_load = ctx->dbg[IG_DBG_SEQUENTIAL] != 0 && !record;
+  if (!seq_load)
+    for (int b = bc0; b < std::min(bc0 + R, b1); ++b) issue_copy(ctx, sr, dkvg, dkvq, b, plan);
 
   T* h = (T*)ctx->h;
   T* qkv = (T*)ctx->qkv;
@@ -2087,7 +2136,7 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
     if (!dense) {
       cudaEventRecord(ctx->ev_comp[buf], st);
       if (ctx->capturing) ctx->cap_mask |= 1u << buf;
-      if (b + R < b1) issue_copy(ctx, sr, dkvg, dkvq, b + R, plan);
+      if (b + R < b1 && !seq_load) issue_copy(ctx, sr, dkvg, dkvq, b + R, plan);
     }
     gemm_rows(0, Mc, cat, ldcat, u.out1.w, u.out1.b, H, H, ctx->X, H, EPI_GATED_RES, ctx->ones, 0);
     ln_aff(b, 1, 0, Mc);
@@ -2133,6 +2182,10 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
     const int Mk = dense ? M_full : M + uy[b];  // rows through LN-mod and the K/V projection
     const int buf = dense ? R : b % R;
     const bool ys = !dense && y_staged(b);
+    if (seq_load && !dense && any_cache) {
+      cudaEventRecord(ctx->ev_comp[buf], st);  // everything enqueued so far (block b-1) ...
+      issue_copy(ctx, sr, dkvg, dkvq, b, plan);  // ... precedes this block's copy
+    }
     if (unet) {
       unet_block(b, buf, ys, Mk, dense);
     } else if (b < ctx->d.n_double) {
@@ -2151,7 +2204,7 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
       if (!dense) {
         cudaEventRecord(ctx->ev_comp[buf], st);
         if (ctx->capturing) ctx->cap_mask |= 1u << buf;
-        if (b + R < b1) issue_copy(ctx, sr, dkvg, dkvq, b + R, plan);
+        if (b + R < b1 && !seq_load) issue_copy(ctx, sr, dkvg, dkvq, b + R, plan);
       }
       const long long gi = ctx->mods[wi.mod_t].off;
       gemm_rows(M_txt, Mc, cat, ldcat, wi.proj.w, wi.proj.b, H, H, ctx->X, H, EPI_GATED_RES, mod + gi + 2 * H, 0);
@@ -2181,7 +2234,7 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
       if (!dense) {
         cudaEventRecord(ctx->ev_comp[buf], st);
         if (ctx->capturing) ctx->cap_mask |= 1u << buf;
-        if (b + R < b1) issue_copy(ctx, sr, dkvg, dkvq, b + R, plan);
+        if (b + R < b1 && !seq_load) issue_copy(ctx, sr, dkvg, dkvq, b + R, plan);
       }
       const long long gs = ctx->mods[ws.mod_t].off;
       gemm_rows(0, Mc, cat, ldcat, ws.lin2.w, ws.lin2.b, H, H + F, ctx->X, H, EPI_GATED_RES, mod + gs + 2 * H, 0);
@@ -2279,6 +2332,33 @@ extern "C" ig_status ig_edit_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, v
   return s;
 }
 
+static ig_status template_record(ig_ctx* ctx, float* latent, const void* txt, const float* cond_vec,
+                                 const float* sigmas, int n_steps, ig_cache* c, cudaStream_t st) {
+  ig_mask* ones = nullptr;
+  ig_status s = get_ones_mask(ctx, &ones);
+  if (s != IG_OK) return s;
+  ig_stats total{};
+  for (int k = 0; k < n_steps; ++k) {
+    ig_edit_req r{};
+    r.slot = 0; r.latent = latent; r.mask = ones; r.cache = nullptr; r.step = k;
+    r.sigma = sigmas[k]; r.sigma_next = sigmas[k + 1]; r.txt = txt; r.cond_vec = cond_vec;
+    cudaError_t el = cudaMemcpyAsync(cache_latent(ctx, c, k), latent, (size_t)ctx->Limg * ctx->C * 4,
+                                     cudaMemcpyDefault, st);  // the template's input latent of step k
+    if (el != cudaSuccess) return set_err(IG_ECUDA, "cache_template: %s", cudaGetErrorString(el));
+    s = step_dispatch(ctx, &r, 1, st, c, k);
+    if (s != IG_OK) return s;
+    total.kernel_launches += ctx->stats.kernel_launches;
+    total.d2h_bytes += ctx->stats.d2h_bytes;
+    total.d2d_bytes += ctx->stats.d2d_bytes;
+    total.rows += ctx->stats.rows;
+  }
+  cudaError_t e = cudaStreamSynchronize(st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->copy_st);
+  if (e != cudaSuccess) return set_err(IG_ECUDA, "cache_template: %s", cudaGetErrorString(e));
+  ctx->stats = total;
+  return IG_OK;
+}
+
 extern "C" ig_status ig_cache_template(ig_ctx* ctx, float* latent, const void* txt, const float* cond_vec,
                                        const float* sigmas, int n_steps, int tier, void* stream,
                                        ig_cache** out) {
@@ -2287,38 +2367,34 @@ extern "C" ig_status ig_cache_template(ig_ctx* ctx, float* latent, const void* t
   *out = nullptr;
   if (n_steps <= 0) return set_err(IG_EINVAL, "n_steps must be positive");
   CUDA_TRY(cudaSetDevice(ctx->device));
-  ig_mask* ones = nullptr;
-  ig_status s = get_ones_mask(ctx, &ones);
-  if (s != IG_OK) return s;
   ig_cache* c = nullptr;
-  if ((s = ig_cache_create(ctx, n_steps, tier, &c)) != IG_OK) return s;
-  cudaStream_t st = (cudaStream_t)stream;
-  ig_stats total{};
-  for (int k = 0; k < n_steps; ++k) {
-    ig_edit_req r{};
-    r.slot = 0; r.latent = latent; r.mask = ones; r.cache = nullptr; r.step = k;
-    r.sigma = sigmas[k]; r.sigma_next = sigmas[k + 1]; r.txt = txt; r.cond_vec = cond_vec;
-    cudaError_t el = cudaMemcpyAsync(cache_latent(ctx, c, k), latent, (size_t)ctx->Limg * ctx->C * 4,
-                                     cudaMemcpyDefault, st);  // the template's input latent of step k
-    if (el != cudaSuccess) { free_cache_now(c); return set_err(IG_ECUDA, "cache_template: %s", cudaGetErrorString(el)); }
-    s = step_dispatch(ctx, &r, 1, st, c, k);
-    if (s != IG_OK) { free_cache_now(c); return s; }
-    total.kernel_launches += ctx->stats.kernel_launches;
-    total.d2h_bytes += ctx->stats.d2h_bytes;
-    total.d2d_bytes += ctx->stats.d2d_bytes;
-    total.rows += ctx->stats.rows;
-  }
-  cudaError_t e = cudaStreamSynchronize(st);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->copy_st);
-  if (e != cudaSuccess) { free_cache_now(c); return set_err(IG_ECUDA, "cache_template: %s", cudaGetErrorString(e)); }
-  ctx->stats = total;
+  ig_status s = ig_cache_create(ctx, n_steps, tier, &c);
+  if (s != IG_OK) return s;
+  s = template_record(ctx, latent, txt, cond_vec, sigmas, n_steps, c, (cudaStream_t)stream);
+  if (s != IG_OK) { free_cache_now(c); return s; }
   *out = c;
   return IG_OK;
 }
 
+extern "C" ig_status ig_cache_template_into(ig_ctx* ctx, float* latent, const void* txt, const float* cond_vec,
+                                            const float* sigmas, int n_steps, ig_cache* cache, void* stream) {
+  if (!ctx || !latent || (!cond_vec && ctx->d.n_unet == 0) || !sigmas || !cache ||
+      ((ctx->Lt > 0 || ctx->d.n_unet > 0) && !txt))
+    return set_err(IG_EINVAL, "NULL argument");
+  if (!desc_equal(cache->desc, ctx->d)) return set_err(IG_ECACHE_INCOMPAT, "cache built for another model");
+  if (n_steps <= 0 || n_steps > cache->n_steps)
+    return set_err(IG_ECACHE_INCOMPAT, "n_steps %d outside the cache schedule [1, %d]", n_steps, cache->n_steps);
+  if (cache->y != ctx->o.cache_y || cache->fp8 != ctx->o.cache_fp8 ||
+      (cache->y && cache->kv_blocks != std::max(0, std::min(ctx->o.cache_kv_blocks, ctx->nb))))
+    return set_err(IG_ECACHE_INCOMPAT, "cache kind differs from the ctx's cache options");
+  if (cache->pins.load() != 0) return set_err(IG_EINVAL, "cache is in use by an enqueued step");
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  return template_record(ctx, latent, txt, cond_vec, sigmas, n_steps, cache, (cudaStream_t)stream);
+}
+
 extern "C" ig_status ig_debug_set(ig_ctx* ctx, int key, long long value) {
   if (!ctx) return set_err(IG_EINVAL, "ctx is NULL");
-  if (key <= 0 || key > IG_DBG_POISON_RING) return set_err(IG_EINVAL, "unknown debug key %d", key);
+  if (key <= 0 || key > IG_DBG_SEQUENTIAL) return set_err(IG_EINVAL, "unknown debug key %d", key);
   CUDA_TRY(cudaSetDevice(ctx->device));
   if (key == IG_DBG_POISON_RING) {  // immediate: every ring buffer of every slot -> NaN
     CUDA_TRY(cudaDeviceSynchronize());

@@ -26,9 +26,10 @@ EXPORTS = ["ig_weight_count", "ig_ctx_create", "ig_ctx_destroy", "ig_cache_creat
            "ig_last_error", "ig_last_stats", "ig_op_gemm", "ig_op_gemm_gated", "ig_op_attention", "ig_copy",
            "ig_profile_enable", "ig_profile_read", "ig_debug_block", "ig_cache_clone", "ig_cache_write",
            "ig_set_plan", "ig_last_plan", "ig_debug_set", "ig_debug_dump_kv",
-           "ig_mask_build_host", "ig_stage_input"]
+           "ig_mask_build_host", "ig_stage_input", "ig_cache_template_into", "ig_cache_bytes",
+           "ig_cache_attach"]
 IG_DBG_SPIN_COPY_NS, IG_DBG_SPIN_COMPUTE_NS, IG_DBG_DROP_RAW, IG_DBG_DROP_WAR = 1, 2, 3, 4
-IG_DBG_CORRUPT_ROW, IG_DBG_POISON_RING = 5, 6
+IG_DBG_CORRUPT_ROW, IG_DBG_POISON_RING, IG_DBG_SEQUENTIAL = 5, 6, 7
 KCLASS = ["gemm", "attn", "lnmod", "qkvpost", "cond", "rows", "copy"]
 
 
@@ -119,6 +120,9 @@ def lib():
         L.ig_debug_set.argtypes = [vp, i, ll]
         L.ig_mask_build_host.argtypes = [vp, vp, vp, P(vp), P(i)]
         L.ig_stage_input.argtypes = [vp, vp, ctypes.c_size_t, vp]
+        L.ig_cache_template_into.argtypes = [vp, vp, vp, vp, P(ctypes.c_float), i, vp, vp]
+        L.ig_cache_bytes.argtypes = [vp, i, P(ctypes.c_size_t)]
+        L.ig_cache_attach.argtypes = [vp, i, vp, ctypes.c_size_t, P(vp)]
         L.ig_debug_dump_kv.argtypes = [vp, i, i, vp, vp, vp]
         for name in EXPORTS:
             if name not in ("ig_ctx_destroy", "ig_cache_free", "ig_mask_free", "ig_last_error",
@@ -208,6 +212,24 @@ def ig_cache_template(ctx: int, latent_ptr: int, txt_ptr: int, cond_ptr: int,
     out = ctypes.c_void_p()
     _check(lib().ig_cache_template(ctx, latent_ptr, txt_ptr, cond_ptr, s, len(sigmas) - 1, tier,
                                    stream, ctypes.byref(out)))
+    return out.value
+
+
+def ig_cache_template_into(ctx: int, latent_ptr: int, txt_ptr: int, cond_ptr: int,
+                           sigmas: Sequence[float], cache: int, stream: int = 0):
+    s = (ctypes.c_float * len(sigmas))(*[float(x) for x in sigmas])
+    _check(lib().ig_cache_template_into(ctx, latent_ptr, txt_ptr, cond_ptr, s, len(sigmas) - 1, cache, stream))
+
+
+def ig_cache_bytes(ctx: int, n_steps: int) -> int:
+    b = ctypes.c_size_t()
+    _check(lib().ig_cache_bytes(ctx, n_steps, ctypes.byref(b)))
+    return b.value
+
+
+def ig_cache_attach(ctx: int, n_steps: int, host_ptr: int, nbytes: int) -> int:
+    out = ctypes.c_void_p()
+    _check(lib().ig_cache_attach(ctx, n_steps, host_ptr, nbytes, ctypes.byref(out)))
     return out.value
 
 

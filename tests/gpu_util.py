@@ -20,6 +20,23 @@ def ctol(g, o, rtol, atol_mult=1.0):
     return bool(ok.all()), worst
 
 
+def ctol_channels(g, o, rtol, groups=None):
+    """C-TOL for a GATED block update X += g (.) f (DESIGN C-AMB 22, bf16 error model): channel j
+    of the update is the gate g_j times an ungated output, so its rounding error scales with that
+    channel's own magnitude; atol_j = rtol * RMS over rows of o[:, j].  Elementwise
+    |g - o| <= rtol |o| + atol_j.  groups: row ranges with their own gates (a double block's text
+    and image streams); each gets its own per-channel atol.  Returns (ok, worst ratio)."""
+    g = np.asarray(g, np.float64)
+    o = np.asarray(o, np.float64)
+    if groups:
+        res = [ctol_channels(g[a:b], o[a:b], rtol) for a, b in groups if b > a]
+        return all(r[0] for r in res), max(r[1] for r in res)
+    atol = rtol * np.sqrt(np.mean(o * o, axis=0, keepdims=True))
+    err = np.abs(g - o)
+    bound = rtol * np.abs(o) + atol + 1e-300
+    return bool((err <= bound).all()), float(np.max(err / bound))
+
+
 class Model:
     """Synthetic weights on the device + an ig context."""
 

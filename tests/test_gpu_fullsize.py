@@ -15,7 +15,7 @@ import torch
 import oracle
 import synth
 from paper_2505_20600_b200 import ig
-from gpu_util import Model, Request, ctol
+from gpu_util import Model, Request, ctol, ctol_channels
 
 pytestmark = pytest.mark.gpu
 
@@ -78,12 +78,14 @@ def test_flux_teacher_forced_block(flux, block, m_ratio, kind):
     got = X_out.double().cpu().numpy()
     assert np.isfinite(got).all()
     dg, do = got - Xh, ref - Xh
-    # C-TOL-full (DESIGN.md C-AMB 22): normwise ||g-o||/||o|| <= rtol and elementwise
-    # |g-o| <= rtol |o| + 2 rtol RMS(o).  At ~4M elements the elementwise max sits ~12x the
-    # normwise error (measured: normwise 2.4e-3, p99.99 1.9e-2 RMS, max 3.6e-2 RMS).
+    # C-TOL for a gated update (DESIGN.md C-AMB 22): normwise ||g-o||/||o|| <= rtol and the
+    # elementwise bound with atol per output channel (the gate scales each channel's error)
     normwise = np.linalg.norm(dg - do) / np.linalg.norm(do)
     assert normwise <= 2e-2, normwise
-    ok, worst = ctol(dg, do, 2e-2, atol_mult=2.0)
+    grp = [(0, D.txt_len), (D.txt_len, len(dg))] if block < D.n_double else None
+    ok, worst = ctol_channels(dg, do, 2e-2, grp)
+    ok1, worst1 = ctol(dg, do, 2e-2)
+    print(f"\nC-TOL per-channel atol worst {worst:.3f}; tensor-RMS atol worst {worst1:.3f}")
     err = np.abs(dg - do)
     rms = np.sqrt(np.mean(do * do))
     i, j = np.unravel_index(np.argmax(err), err.shape)
@@ -136,7 +138,10 @@ def test_flux_teacher_forced_y_block(flux, block):
     dg, do = got - Xh, ref - Xh
     normwise = np.linalg.norm(dg - do) / np.linalg.norm(do)
     assert normwise <= 2e-2, normwise
-    ok, worst = ctol(dg, do, 2e-2, atol_mult=2.0)
+    grp = [(0, D.txt_len), (D.txt_len, len(dg))] if block < D.n_double else None
+    ok, worst = ctol_channels(dg, do, 2e-2, grp)
+    print(f"\nY block {block}: C-TOL per-channel atol worst {worst:.3f}; tensor-RMS atol worst "
+          f"{ctol(dg, do, 2e-2)[1]:.3f}")
     assert ok, ("update", worst)
     ig.ig_cache_free(cache)
     rq.free()
@@ -250,7 +255,10 @@ def test_sd3_teacher_forced_blocks():
             dg, do = dg[d.txt_len:], do[d.txt_len:]
         normwise = np.linalg.norm(dg - do) / np.linalg.norm(do)
         assert normwise <= 2e-2, (block, normwise)
-        ok, worst = ctol(dg, do, 2e-2, atol_mult=2.0)
+        grp = None if block == d.n_blocks - 1 else [(0, d.txt_len), (d.txt_len, len(dg))]
+        ok, worst = ctol_channels(dg, do, 2e-2, grp)
+        print(f"\nSD3 block {block}: C-TOL per-channel atol worst {worst:.3f}; tensor-RMS atol worst "
+              f"{ctol(dg, do, 2e-2)[1]:.3f}")
         assert ok, (block, worst)
     ig.ig_cache_free(cache)
     rq.free()
