@@ -511,6 +511,7 @@ def main():
     ap.add_argument("--no-y", action="store_true", help="skip the other-cache-kind runs")
     ap.add_argument("--no-prof-leg", action="store_true", help="skip the profiled (per-kernel) leg")
     ap.add_argument("--no-lockstep", action="store_true", help="skip the lockstep (deduplicated loads) run")
+    ap.add_argument("--no-ablation", action="store_true", help="skip the N1 sequential/pipelined/planned legs")
     ap.add_argument("--graphs", action="store_true", help="replay steps as CUDA graphs (HBM-resident caches)")
     ap.add_argument("--cache", default=None, choices=["kv", "hybrid", "y"],
                     help="headline cache kind: K/V, hybrid K/V + Y (interleaved Y blocks), Y")
@@ -705,7 +706,7 @@ def main():
 
     # ---- N1 ablation on the north-star K/V form (fig:pipeline_load P:541-560):
     # sequential loading vs the pipelined ring vs the Algorithm-1 plan, pure K/V cache from host
-    if tier == "host" and world == 1:
+    if tier == "host" and world == 1 and not args.no_ablation:
         ca = record(ctx_kv, "host")
         ablation = {}
         ig.ig_debug_set(ctx_kv, ig.IG_DBG_SEQUENTIAL, 1)

@@ -1,6 +1,6 @@
 """Build libig.so in-tree with nvcc for sm_100a (B200).  Used by __graft_entry__.build().
 
-    python -m paper_2505_20600_b200.build [--debug]
+    python -m paper_2505_20600_b200.build [--debug] [--out PATH] [--define NAME[=VAL]]...
 """
 import concurrent.futures as cf
 import os
@@ -22,15 +22,22 @@ def sources():
     return sorted(f for f in os.listdir(CSRC) if f.endswith(".cu"))
 
 
+def _objdir(extra):
+    if not extra:
+        return OBJ
+    import hashlib
+    return OBJ + "_" + hashlib.sha1(" ".join(extra).encode()).hexdigest()[:10]
+
+
 def _compile(src, extra):
-    obj = os.path.join(OBJ, src[:-3] + ".o")
+    obj = os.path.join(_objdir(extra), src[:-3] + ".o")
     cmd = [NVCC] + ARCH + FLAGS + extra + ["-c", os.path.join(CSRC, src), "-o", obj]
     p = subprocess.run(cmd, capture_output=True, text=True)
     return src, obj, p.returncode, p.stdout + p.stderr
 
 
 def build(verbose=False, extra=(), out=None):
-    os.makedirs(OBJ, exist_ok=True)
+    os.makedirs(_objdir(list(extra)), exist_ok=True)
     os.makedirs(os.path.dirname(LIB), exist_ok=True)
     extra = list(extra)
     objs, logs = [], {}
@@ -63,4 +70,7 @@ if __name__ == "__main__":
     out = None
     if "--out" in sys.argv:
         out = sys.argv[sys.argv.index("--out") + 1]
+    for i, a in enumerate(sys.argv):  # A/B variants: --define NAME[=VALUE] (repeatable)
+        if a == "--define":
+            ex.append("-D" + sys.argv[i + 1])
     print(build(verbose="-v" in sys.argv, extra=ex, out=out))

@@ -15,7 +15,11 @@
 #include <cstring>
 #include <cstdlib>
 #include <cstdint>
+#include <condition_variable>
+#include <deque>
+#include <functional>
 #include <mutex>
+#include <thread>
 #include <chrono>
 #include <string>
 #include <unordered_map>
@@ -218,7 +222,22 @@ struct ig_ctx {
   cudaError_t copy_err = cudaSuccess;
   size_t copy_err_idx = 0;
   // ig_debug_set keys (race tests and fault injection; all 0 in normal operation)
-  long long dbg[8] = {};
+  long long dbg[9] = {};
+  // Copy-lane host thread: the cache-prefetch enqueues (cudaMemcpyBatchAsync of the unmasked
+  // runs, gathers, dedupe) run on their own host thread, so the compute launches are never
+  // stuck behind the copy engines' queue back-pressure.  Jobs run in order; the compute thread
+  // waits (host side) only for the job that recorded the ring event it is about to wait on.
+  struct CopyLane {
+    std::thread thr;
+    std::mutex mu;
+    std::condition_variable cv, cv_done;
+    std::deque<std::function<void()>> q;
+    long long pushed = 0, done = 0;
+    bool stop = false;
+  } lane;
+  bool lane_on = false;        // this step issues copies through the thread
+  ig_stats cstats{};           // copy-lane counters of the current step (merged after the drain)
+  std::vector<long long> job_of_block;  // per block: lane job that issued its copy (-1: inline / none)
   // CUDA graphs of whole steps (ig_ctx_opts.use_graphs): keyed by everything that shapes the
   // launches (row counts, plan, staging slot, cache kinds); the per-step data (sigmas, step
   // indices, cache plane pointers, latents) live in the descriptors the graph itself pulls
@@ -441,6 +460,7 @@ static ig_status build_rope_table(ig_ctx* ctx) {
 }
 
 extern "C" void ig_ctx_destroy(ig_ctx* ctx);
+static void lane_stop(ig_ctx* ctx);
 
 extern "C" ig_status ig_ctx_create(const ig_model_desc* desc, const void* const* weights,
                                    int n_weights, int device, const ig_ctx_opts* opts,
@@ -694,6 +714,7 @@ extern "C" ig_status ig_ctx_create(const ig_model_desc* desc, const void* const*
 extern "C" void ig_ctx_destroy(ig_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
+  lane_stop(ctx);
   cudaDeviceSynchronize();  // every enqueued step (and its unpin callback) has finished
   reap_zombies(ctx);
   void* bufs[] = {ctx->X, ctx->vel, ctx->temb, ctx->tmp, ctx->vec, ctx->svec, ctx->modbuf, ctx->h,
@@ -1195,20 +1216,79 @@ struct CopyPlan {
   DedupeArgs dd{};
 };
 
+static void lane_main(ig_ctx* ctx) {
+  cudaSetDevice(ctx->device);
+  auto& L = ctx->lane;
+  for (;;) {
+    std::function<void()> job;
+    {
+      std::unique_lock<std::mutex> lk(L.mu);
+      L.cv.wait(lk, [&] { return L.stop || !L.q.empty(); });
+      if (L.q.empty()) return;  // stop requested and drained
+      job = std::move(L.q.front());
+      L.q.pop_front();
+    }
+    job();
+    {
+      std::lock_guard<std::mutex> lk(L.mu);
+      ++L.done;
+    }
+    L.cv_done.notify_all();
+  }
+}
+
+static long long lane_push(ig_ctx* ctx, std::function<void()> fn) {
+  auto& L = ctx->lane;
+  if (!L.thr.joinable()) L.thr = std::thread(lane_main, ctx);
+  long long seq;
+  {
+    std::lock_guard<std::mutex> lk(L.mu);
+    L.q.push_back(std::move(fn));
+    seq = ++L.pushed;
+  }
+  L.cv.notify_one();
+  return seq;
+}
+
+static void lane_wait(ig_ctx* ctx, long long seq) {  // until job `seq` (1-based) has run
+  auto& L = ctx->lane;
+  std::unique_lock<std::mutex> lk(L.mu);
+  L.cv_done.wait(lk, [&] { return L.done >= seq; });
+}
+
+static void lane_drain(ig_ctx* ctx) {
+  long long seq;
+  {
+    std::lock_guard<std::mutex> lk(ctx->lane.mu);
+    seq = ctx->lane.pushed;
+  }
+  lane_wait(ctx, seq);
+}
+
+static void lane_stop(ig_ctx* ctx) {
+  auto& L = ctx->lane;
+  if (!L.thr.joinable()) return;
+  {
+    std::lock_guard<std::mutex> lk(L.mu);
+    L.stop = true;
+  }
+  L.cv.notify_all();
+  L.thr.join();
+}
+
 static inline void note_copy(ig_ctx* ctx, cudaError_t e) {
   if (e != cudaSuccess && ctx->copy_err == cudaSuccess) ctx->copy_err = e;
 }
 
-static void issue_copy(ig_ctx* ctx, const std::vector<StepReq>& sr, const KvGatherReq* kvg_dev,
-                       const KvGatherReq* kvq_dev, int b, const CopyPlan& plan) {
-  if (!plan.any) return;
+static void issue_copy_now(ig_ctx* ctx, const std::vector<StepReq>& sr, const KvGatherReq* kvg_dev,
+                           const KvGatherReq* kvq_dev, int b, const CopyPlan& plan, ig_stats& cs) {
   const int buf = b % ctx->R;
   // inside a graph capture only this step's records are visible; earlier steps completed
   // before the graph starts (same stream)
   if ((!ctx->capturing || (ctx->cap_mask >> buf & 1u)) && !ctx->dbg[IG_DBG_DROP_WAR])
     cudaStreamWaitEvent(ctx->copy_st, ctx->ev_comp[buf], 0);
   if (ctx->dbg[IG_DBG_SPIN_COPY_NS]) launch_spin((unsigned long long)ctx->dbg[IG_DBG_SPIN_COPY_NS], ctx->copy_st);
-  const long long by0 = ctx->stats.h2d_bytes + ctx->stats.d2d_bytes;
+  const long long by0 = cs.h2d_bytes + cs.d2d_bytes;
   ProfScope ps(ctx, ctx->copy_st, IG_K_COPY, 0.0, 0.0, b);
   const int n = (int)sr.size();
   const size_t row = (size_t)ctx->H * ctx->esz;
@@ -1240,9 +1320,9 @@ static void issue_copy(ig_ctx* ctx, const std::vector<StepReq>& sr, const KvGath
         dsts.push_back(ss);
         srcs.push_back((void*)cache_scales(ctx, c, r->step, b - 1, 2));
         sizes.push_back(spl);
-        ctx->stats.h2d_bytes += (long long)n_u * ctx->H + (long long)spl;
+        cs.h2d_bytes += (long long)n_u * ctx->H + (long long)spl;
       } else {
-        ctx->stats.d2d_bytes += (long long)n_u * (ctx->H + 4 * ctx->d.heads);
+        cs.d2d_bytes += (long long)n_u * (ctx->H + 4 * ctx->d.heads);
       }
       continue;
     }
@@ -1266,9 +1346,9 @@ static void issue_copy(ig_ctx* ctx, const std::vector<StepReq>& sr, const KvGath
           sizes.push_back((size_t)run.second * row);
         }
         by = (long long)(dd ? n_u - plan.dshared[q] : n_u) * row;
-        if (dd) ctx->stats.d2d_bytes += (long long)plan.dshared[q] * row;
+        if (dd) cs.d2d_bytes += (long long)plan.dshared[q] * row;
       }
-      if (host) ctx->stats.h2d_bytes += by; else ctx->stats.d2d_bytes += by;
+      if (host) cs.h2d_bytes += by; else cs.d2d_bytes += by;
       continue;
     }
     if (c->fp8) {
@@ -1316,11 +1396,11 @@ static void issue_copy(ig_ctx* ctx, const std::vector<StepReq>& sr, const KvGath
         }
       }
       by = 2LL * (dd ? n_u - plan.dshared[q] : n_u) * row;
-      if (dd) ctx->stats.d2d_bytes += 2LL * plan.dshared[q] * row;
+      if (dd) cs.d2d_bytes += 2LL * plan.dshared[q] * row;
     } else {
       by = 2LL * n_u * row;  // SM gather kernel below
     }
-    if (host) ctx->stats.h2d_bytes += by; else ctx->stats.d2d_bytes += by;
+    if (host) cs.h2d_bytes += by; else cs.d2d_bytes += by;
   }
   if (!sizes.empty()) {
     cudaMemcpyAttributes attr{};
@@ -1351,16 +1431,16 @@ static void issue_copy(ig_ctx* ctx, const std::vector<StepReq>& sr, const KvGath
       live += !dd.e[i].skip;
     }
     if (live) {
-      ctx->stats.kernel_launches++;
+      cs.kernel_launches++;
       launch_kv_dedupe(dd, ctx->copy_st);
     }
   }
   if (plan.gather) {
-    ctx->stats.kernel_launches++;
+    cs.kernel_launches++;
     launch_kv_gather(kvg_dev + (size_t)b * n, n, plan.max_nu, ctx->Lt, ctx->H, (int)ctx->esz, ctx->copy_st);
   }
   if (plan.gather_q8) {
-    ctx->stats.kernel_launches++;
+    cs.kernel_launches++;
     launch_kv_gather_q8(kvq_dev + (size_t)b * n, n, plan.max_nu, ctx->Lt, ctx->H, ctx->d.heads, ctx->copy_st);
   }
   if (ctx->dbg[IG_DBG_CORRUPT_ROW]) {  // fault injection: one staged cached row of the first cache user
@@ -1372,8 +1452,26 @@ static void issue_copy(ig_ctx* ctx, const std::vector<StepReq>& sr, const KvGath
       break;
     }
   }
-  ps.bytes = (double)(ctx->stats.h2d_bytes + ctx->stats.d2d_bytes - by0);
+  ps.bytes = (double)(cs.h2d_bytes + cs.d2d_bytes - by0);
   cudaEventRecord(ctx->ev_copy[buf], ctx->copy_st);
+}
+
+// Issue block b's cache copy: on the copy-lane thread when the step runs threaded (the job
+// captures the step's request list, which outlives every job: the step drains the lane before
+// it returns), else inline.
+static void issue_copy(ig_ctx* ctx, const std::vector<StepReq>& sr, const KvGatherReq* kvg_dev,
+                       const KvGatherReq* kvq_dev, int b, const CopyPlan& plan) {
+  if (!plan.any) return;
+  if (!ctx->lane_on) {
+    issue_copy_now(ctx, sr, kvg_dev, kvq_dev, b, plan, ctx->stats);
+    return;
+  }
+  const std::vector<StepReq>* srp = &sr;
+  const CopyPlan* pp = &plan;
+  const long long seq = lane_push(ctx, [ctx, srp, kvg_dev, kvq_dev, b, pp] {
+    issue_copy_now(ctx, *srp, kvg_dev, kvq_dev, b, *pp, ctx->cstats);
+  });
+  if (b >= 0 && b < (int)ctx->job_of_block.size()) ctx->job_of_block[b] = seq;
 }
 
 // ---- Algorithm 1 planner on B200 ----------------------------------------------
@@ -1796,10 +1894,38 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
     ctx->cap_mask = 0;
   }
   if (!ctx->capturing) flush_graph_tail(ctx);  // eager step after a graph
+  // copy lane on its own host thread for host-tier caches (DMA back-pressure), inline otherwise
+  // and whenever the main thread itself touches the copy stream (recording, capture, profiling)
+  {
+    static const bool no_lane = getenv("IG_NO_COPY_THREAD") != nullptr;  // A/B switch
+    bool any_host = false;
+    for (auto& s2 : sr) any_host |= s2.use_cache && s2.r->cache->tier == IG_CACHE_HOST;
+    ctx->lane_on = !no_lane && any_host && !ctx->prof && !ctx->capturing && !record && !rng.X_in;
+    ctx->cstats = ig_stats{};
+    ctx->job_of_block.assign(nb, -1);
+  }
+  struct LaneGuard {  // every exit path drains the lane before sr / plan go out of scope
+    ig_ctx* c;
+    ~LaneGuard() {
+      if (!c->lane_on) return;
+      lane_drain(c);
+      c->stats.h2d_bytes += c->cstats.h2d_bytes;
+      c->stats.d2d_bytes += c->cstats.d2d_bytes;
+      c->stats.kernel_launches += c->cstats.kernel_launches;
+      c->cstats = ig_stats{};
+      c->lane_on = false;
+    }
+  } lane_guard{ctx};
   launch_copy_bytes(ds, ctx->m_stage[si], desc_bytes, st);
   if (plan.gather || plan.gather_q8) {
     const size_t off = (char*)hkvg - hs, bytes = (char*)(hkvq + (size_t)nb * na) - (char*)hkvg;
-    CUDA_TRY(cudaMemcpyAsync(ds + off, hs + off, bytes, cudaMemcpyHostToDevice, ctx->copy_st));
+    if (ctx->lane_on) {
+      lane_push(ctx, [ctx, ds, hs, off, bytes] {
+        note_copy(ctx, cudaMemcpyAsync(ds + off, hs + off, bytes, cudaMemcpyHostToDevice, ctx->copy_st));
+      });
+    } else {
+      CUDA_TRY(cudaMemcpyAsync(ds + off, hs + off, bytes, cudaMemcpyHostToDevice, ctx->copy_st));
+    }
   }
   for (auto& s : sr) if (s.use_cache) { s.r->cache->pins.fetch_add(1); }
   for (auto& s : sr) { s.m->used = true; s.m->last_st = st; }
@@ -1958,8 +2084,15 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
   // Y blocks after the first cached one: LN-modulation of the unmasked rows straight from the
   // staged Y_{b-1} rows (the copy lane's V-plane landing zone), after waiting for the copy
   auto y_staged = [&](int b) { return uy[b] > 0 && b > kplan; };
+  int cur_b = 0;  // block being enqueued (the lane job that recorded its ring event must have run)
+  auto lane_ready = [&]() {
+    if (ctx->lane_on && ctx->job_of_block[cur_b] > 0) lane_wait(ctx, ctx->job_of_block[cur_b]);
+  };
   auto ln_mod_y = [&](int b, int buf, int mod_t, int shift_c, int scale_c) {
-    if (!ctx->dbg[IG_DBG_DROP_RAW]) stream_wait(ctx, st, ctx->ev_copy[buf]);
+    if (!ctx->dbg[IG_DBG_DROP_RAW]) {
+      lane_ready();
+      stream_wait(ctx, st, ctx->ev_copy[buf]);
+    }
     const long long off = ctx->mods[mod_t].off;
     ProfScope ps(ctx, st, IG_K_LNMOD, 0.0, (double)uy[b] * H * (es + es));
     launch_ln_mod_staged<T>(ctx->kv_arena, ctx->slot_stride, (long long)buf * ctx->buf_elems, ctx->L, H, M, M + uy[b],
@@ -2048,10 +2181,16 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
   const bool late_wait = ctx->o.copy_mode != 0 && !record;
   const bool drop_raw = ctx->dbg[IG_DBG_DROP_RAW] != 0;  // negative control of the race tests
   auto wait_copy = [&](int buf) {
-    if ((any_cache || record) && !late_wait && !(drop_raw && !record)) stream_wait(ctx, st, ctx->ev_copy[buf]);
+    if ((any_cache || record) && !late_wait && !(drop_raw && !record)) {
+      lane_ready();
+      stream_wait(ctx, st, ctx->ev_copy[buf]);
+    }
   };
   auto wait_copy_late = [&](int buf) {
-    if (any_cache && late_wait && !drop_raw) stream_wait(ctx, st, ctx->ev_copy[buf]);
+    if (any_cache && late_wait && !drop_raw) {
+      lane_ready();
+      stream_wait(ctx, st, ctx->ev_copy[buf]);
+    }
   };
 
   // ---- UNet BasicTransformerBlock (config 5; oracle/unet.py unet_block_masked) ----
@@ -2066,6 +2205,7 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
     stats.kernel_launches++;
   };
   auto ln_aff_y = [&](int b, int buf) {  // Y block: LN1 of the unmasked rows from the staged Y_{b-1}
+    lane_ready();
     stream_wait(ctx, st, ctx->ev_copy[buf]);
     ProfScope ps(ctx, st, IG_K_LNMOD, 0.0, (double)uy[b] * H * (es + es));
     launch_ln_mod_staged<T>(ctx->kv_arena, ctx->slot_stride, (long long)buf * ctx->buf_elems, ctx->L, H, M, M + uy[b],
@@ -2182,6 +2322,7 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
     const int Mk = dense ? M_full : M + uy[b];  // rows through LN-mod and the K/V projection
     const int buf = dense ? R : b % R;
     const bool ys = !dense && y_staged(b);
+    cur_b = b;
     if (seq_load && !dense && any_cache) {
       cudaEventRecord(ctx->ev_comp[buf], st);  // everything enqueued so far (block b-1) ...
       issue_copy(ctx, sr, dkvg, dkvq, b, plan);  // ... precedes this block's copy
@@ -2282,6 +2423,14 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
     CUDA_TRY(cudaStreamWaitEvent(st, record->y && blk_yrec(record->ymode, b1 - 1) ? ctx->ev_yrec[(b1 - 1) % R]
                                                                                  : ctx->ev_copy[(b1 - 1) % R], 0));
   ctx->pdl_block = true;
+  if (ctx->lane_on) {  // every copy of this step enqueued (the jobs reference sr / plan)
+    lane_drain(ctx);
+    stats.h2d_bytes += ctx->cstats.h2d_bytes;
+    stats.d2d_bytes += ctx->cstats.d2d_bytes;
+    stats.kernel_launches += ctx->cstats.kernel_launches;
+    ctx->cstats = ig_stats{};
+    ctx->lane_on = false;
+  }
   if (ctx->copy_err != cudaSuccess) {
     const cudaError_t ce = ctx->copy_err;
     ctx->copy_err = cudaSuccess;

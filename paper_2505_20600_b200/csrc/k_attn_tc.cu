@@ -52,6 +52,12 @@ constexpr float RESCALE_THRESHOLD = 8.0f;       // log2 units
 #ifndef POLY_AT
 #define POLY_AT(i) (((i) & 15) == 15)
 #endif  // pairs per key tile on ex2_poly2 (measured: MUFU is not the limiter; 0 is fastest)
+#ifndef ATTN_MAX3
+#define ATTN_MAX3 0       // row max with 3-input FMNMX3 (half the max-phase instructions)
+#endif
+#ifndef ATTN_ST_CHUNKS
+#define ATTN_ST_CHUNKS 1  // P stored to TMEM in 1, 2 or 4 pieces as the exps complete
+#endif
 
 struct Bars {
   uint64_t q_full;
@@ -75,6 +81,12 @@ __device__ long long g_trace[5][2][40];
 #else
 #define TRACE(ev, t, j) do { } while (0)
 #endif
+
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+  float r;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
 
 __device__ __forceinline__ float ex2_fast(float x) {
   float y;
@@ -272,12 +284,20 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           for (int i = 0; i < 128; ++i)
             if (i >= valid) r[i] = __float_as_uint(-INFINITY);
         }
+#if ATTN_MAX3
+#pragma unroll
+        for (int i = 0; i < 128; i += 16)
+#pragma unroll
+          for (int u = 0; u < 8; ++u) pm[u] = fmax3(pm[u], __uint_as_float(r[i + u]), __uint_as_float(r[i + 8 + u]));
+        const float mx = fmax3(fmax3(pm[0], pm[1], pm[2]), fmax3(pm[3], pm[4], pm[5]), fmaxf(pm[6], pm[7]));
+#else
 #pragma unroll
         for (int i = 0; i < 128; i += 8)
 #pragma unroll
           for (int u = 0; u < 8; ++u) pm[u] = fmaxf(pm[u], __uint_as_float(r[i + u]));
         const float mx = fmaxf(fmaxf(fmaxf(pm[0], pm[1]), fmaxf(pm[2], pm[3])),
                                fmaxf(fmaxf(pm[4], pm[5]), fmaxf(pm[6], pm[7])));
+#endif
         // scores in log2 units: s * scale * log2(e).  Keep the stale max unless it grew by
         // more than the threshold (per row).
         const float mxs = mx * scale_log2;
@@ -288,18 +308,30 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         float2 acc[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) acc[u] = make_float2(0.f, 0.f);
+        // P_t(j) goes back to TMEM in ATTN_ST_CHUNKS pieces, each stored as soon as its exps are
+        // done, so the stores overlap the remaining exps
+        constexpr int PCH = 64 / ATTN_ST_CHUNKS;  // packed bf16x2 words per chunk
 #pragma unroll
-        for (int i = 0; i < 64; ++i) {  // in-place pack: r[i] <- bf16x2(p[2i], p[2i+1])
-          const float2 x = __ffma2_rn(make_float2(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1])), sc2, nm2);
-          const float2 pp = POLY_AT(i) ? ex2_poly2(x) : make_float2(ex2_fast(x.x), ex2_fast(x.y));
-          acc[i & 3] = __fadd2_rn(acc[i & 3], pp);
-          r[i] = pack_bf16(pp.x, pp.y);
+        for (int c = 0; c < ATTN_ST_CHUNKS; ++c) {
+#pragma unroll
+          for (int i = c * PCH; i < (c + 1) * PCH; ++i) {  // in-place pack: r[i] <- bf16x2(p[2i], p[2i+1])
+            const float2 x = __ffma2_rn(make_float2(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1])), sc2, nm2);
+            const float2 pp = POLY_AT(i) ? ex2_poly2(x) : make_float2(ex2_fast(x.x), ex2_fast(x.y));
+            acc[i & 3] = __fadd2_rn(acc[i & 3], pp);
+            r[i] = pack_bf16(pp.x, pp.y);
+          }
+          if (PCH == 64) {
+            tc::tmem_st32(tS + 0, &r[0]);
+            tc::tmem_st32(tS + 32, &r[32]);
+          } else if (PCH == 32) {
+            tc::tmem_st32(tS + c * 32, &r[c * 32]);
+          } else {
+            tc::tmem_st16(tS + c * 16, *reinterpret_cast<const uint32_t(*)[16]>(&r[c * 16]));
+          }
         }
         const float2 s01 = __fadd2_rn(acc[0], acc[1]), s23 = __fadd2_rn(acc[2], acc[3]);
         const float2 s4 = __fadd2_rn(s01, s23);
         const float sum = s4.x + s4.y;
-        tc::tmem_st32(tS + 0, &r[0]);
-        tc::tmem_st32(tS + 32, &r[32]);
         if (j > 0 && __any_sync(0xffffffffu, m_use > m)) {
 #pragma unroll 1
           for (int c = 0; c < D; c += 32) {
