@@ -181,6 +181,18 @@ ig_status ig_cache_bytes(const ig_ctx* ctx, int n_steps, size_t* bytes);
  * ig_cache_template_into in one process, attach in the others after that finished). */
 ig_status ig_cache_attach(ig_ctx* ctx, int n_steps, void* host_mem, size_t bytes, ig_cache** out);
 
+/* Peer-HBM template pool (P:622-634 cache hierarchy, template reuse P:263-267): an
+ * HBM-tier cache (IG_CACHE_DEVICE) of one process is exported as an opaque handle of
+ * IG_CACHE_HANDLE_BYTES bytes (CUDA IPC); another process imports it on its own ctx — on another
+ * GPU the copy lane then reads the cached rows from the owner's HBM over NVLink (peer access)
+ * instead of streaming them from host memory over PCIe.  The importer's ctx must have the same
+ * cache kind (ig_cache_bytes must match: IG_ECACHE_INCOMPAT otherwise); ig_cache_free of an
+ * imported cache closes the mapping (the owner keeps the storage, and must outlive importers).
+ * IG_EUNSUPPORTED when the two devices cannot access each other. */
+#define IG_CACHE_HANDLE_BYTES 128
+ig_status ig_cache_export(const ig_cache* cache, void* handle, size_t handle_bytes);
+ig_status ig_cache_import(ig_ctx* ctx, const void* handle, ig_cache** out);
+
 /* Copy of a cache into another tier (e.g. an HBM-resident hot template) in the
  * cache format of `ctx` (a bf16 cache cloned by a cache_fp8 ctx is quantized per (token,
  * head) on the device).  Same schedule.  Synchronous. */

@@ -136,6 +136,8 @@ struct ig_cache {
   void* ptr = nullptr;     // pinned host (mapped) or device
   void* dptr = nullptr;    // device-visible pointer (== ptr with UVA)
   bool registered = false; // caller-provided host memory (ig_cache_attach): unregistered, never freed
+  bool imported = false;   // another process's HBM cache opened by IPC (ig_cache_import): closed, never freed
+  int owner_device = -1;   // device that holds the storage (peer tier: != device)
   size_t bytes = 0;
   mutable std::atomic<int> pins{0};
   std::atomic<bool> zombie{false};
@@ -317,6 +319,7 @@ static void free_cache_now(ig_cache* c) {
   if (!c) return;
   if (c->ptr) {
     if (c->registered) cudaHostUnregister(c->ptr);
+    else if (c->imported) cudaIpcCloseMemHandle(c->ptr);
     else if (c->tier == IG_CACHE_HOST) cudaFreeHost(c->ptr);
     else cudaFree(c->ptr);
   }
@@ -1068,6 +1071,78 @@ extern "C" ig_status ig_cache_attach(ig_ctx* ctx, int n_steps, void* host_mem, s
   }
   c->ptr = host_mem;
   c->registered = true;
+  *out = c;
+  return IG_OK;
+}
+
+// ---- peer-HBM template pool: a device-tier cache held in one GPU's HBM, opened by
+// the processes of the other GPUs through CUDA IPC and read over NVLink (peer access) by the
+// copy lane's gather kernel instead of crossing the host link
+typedef struct { char bytes[64]; } ig_ipc_raw;
+static_assert(sizeof(cudaIpcMemHandle_t) <= 64, "IPC handle size");
+
+extern "C" ig_status ig_cache_export(const ig_cache* c, void* handle, size_t handle_bytes) {
+  if (!c || !handle) return set_err(IG_EINVAL, "NULL argument");
+  if (handle_bytes < IG_CACHE_HANDLE_BYTES) return set_err(IG_EINVAL, "handle buffer < %d bytes", IG_CACHE_HANDLE_BYTES);
+  if (c->tier != IG_CACHE_DEVICE || c->imported || c->registered)
+    return set_err(IG_EINVAL, "only an HBM-tier cache allocated by this process can be exported");
+  CUDA_TRY(cudaSetDevice(c->device));
+  cudaIpcMemHandle_t h;
+  CUDA_TRY(cudaIpcGetMemHandle(&h, c->ptr));
+  // layout: IPC handle, then the schedule length, the storage device and the byte count
+  memset(handle, 0, IG_CACHE_HANDLE_BYTES);
+  memcpy(handle, &h, sizeof(h));
+  int32_t meta[2] = {c->n_steps, c->device};
+  memcpy((char*)handle + 64, meta, sizeof(meta));
+  uint64_t by = c->bytes;
+  memcpy((char*)handle + 72, &by, sizeof(by));
+  return IG_OK;
+}
+
+extern "C" ig_status ig_cache_import(ig_ctx* ctx, const void* handle, ig_cache** out) {
+  if (!ctx || !handle || !out) return set_err(IG_EINVAL, "NULL argument");
+  *out = nullptr;
+  int32_t meta[2];
+  memcpy(meta, (const char*)handle + 64, sizeof(meta));
+  uint64_t by = 0;
+  memcpy(&by, (const char*)handle + 72, sizeof(by));
+  const int n_steps = meta[0], owner = meta[1];
+  if (n_steps <= 0) return set_err(IG_EINVAL, "bad cache handle");
+  size_t need = 0;
+  ig_status s = ig_cache_bytes(ctx, n_steps, &need);
+  if (s != IG_OK) return s;
+  if ((size_t)by != need)
+    return set_err(IG_ECACHE_INCOMPAT, "exported cache holds %llu bytes, this ctx's cache kind needs %zu",
+                   (unsigned long long)by, need);
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  if (owner != ctx->device) {  // read the peer's HBM over NVLink: enable peer access (idempotent)
+    int can = 0;
+    CUDA_TRY(cudaDeviceCanAccessPeer(&can, ctx->device, owner));
+    if (!can) return set_err(IG_EUNSUPPORTED, "device %d cannot access peer %d", ctx->device, owner);
+    cudaError_t pe = cudaDeviceEnablePeerAccess(owner, 0);
+    if (pe != cudaSuccess && pe != cudaErrorPeerAccessAlreadyEnabled) return set_err(IG_ECUDA, "peer access: %s", cudaGetErrorString(pe));
+    cudaGetLastError();
+  }
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  void* p = nullptr;
+  CUDA_TRY(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+  ig_cache* c = new ig_cache();
+  c->desc = ctx->d;
+  c->n_steps = n_steps;
+  c->tier = IG_CACHE_DEVICE;
+  c->device = ctx->device;
+  c->owner_device = owner;
+  c->fp8 = ctx->o.cache_fp8;
+  c->y = ctx->o.cache_y;
+  c->kv_blocks = c->y ? std::max(0, std::min(ctx->o.cache_kv_blocks, ctx->nb)) : ctx->nb;
+  c->ymode = y_modes(ctx->nb, c->y, c->kv_blocks);
+  c->step_planes = step_planes(c->ymode);
+  c->bytes = need;
+  if (c->fp8) c->scale_off = (size_t)n_steps * c->step_planes * ctx->Limg * ctx->H;
+  c->lat_off = cache_kv_bytes(ctx, n_steps, c->fp8, c->ymode);
+  c->ptr = c->dptr = p;
+  c->imported = true;
   *out = c;
   return IG_OK;
 }

@@ -55,6 +55,15 @@ constexpr float RESCALE_THRESHOLD = 8.0f;       // log2 units
 #ifndef ATTN_MAX3
 #define ATTN_MAX3 0       // row max with 3-input FMNMX3 (half the max-phase instructions)
 #endif
+#ifndef ATTN_SETMAXNREG
+#define ATTN_SETMAXNREG 0  // per-warpgroup register split (producer/MMA low, softmax high)
+#endif
+#ifndef ATTN_REGS_PRODUCER
+#define ATTN_REGS_PRODUCER 56
+#endif
+#ifndef ATTN_REGS_SOFTMAX
+#define ATTN_REGS_SOFTMAX 224
+#endif
 #ifndef ATTN_ST_CHUNKS
 #define ATTN_ST_CHUNKS 1  // P stored to TMEM in 1, 2 or 4 pieces as the exps complete
 #endif
@@ -173,6 +182,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   __syncthreads();
   tc::tc_fence_after();
   const uint32_t tmem = bar->tmem;
+#if ATTN_SETMAXNREG
+  // register split per warpgroup (setmaxnreg): the TMA / MMA warpgroup needs few registers, the
+  // two softmax warpgroups hold a 128-column row of S each (no spills, more ILP for the exps)
+  if (warp < 4) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(ATTN_REGS_PRODUCER));
+  else asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(ATTN_REGS_SOFTMAX));
+#endif
 
   if (warp == 0) {
     if (lane == 0) {  // ===== TMA producer =====

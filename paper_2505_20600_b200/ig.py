@@ -27,7 +27,8 @@ EXPORTS = ["ig_weight_count", "ig_ctx_create", "ig_ctx_destroy", "ig_cache_creat
            "ig_profile_enable", "ig_profile_read", "ig_debug_block", "ig_cache_clone", "ig_cache_write",
            "ig_set_plan", "ig_last_plan", "ig_debug_set", "ig_debug_dump_kv",
            "ig_mask_build_host", "ig_stage_input", "ig_cache_template_into", "ig_cache_bytes",
-           "ig_cache_attach"]
+           "ig_cache_attach", "ig_cache_export", "ig_cache_import"]
+IG_CACHE_HANDLE_BYTES = 128
 IG_DBG_SPIN_COPY_NS, IG_DBG_SPIN_COMPUTE_NS, IG_DBG_DROP_RAW, IG_DBG_DROP_WAR = 1, 2, 3, 4
 IG_DBG_CORRUPT_ROW, IG_DBG_POISON_RING, IG_DBG_SEQUENTIAL = 5, 6, 7
 KCLASS = ["gemm", "attn", "lnmod", "qkvpost", "cond", "rows", "copy"]
@@ -123,6 +124,8 @@ def lib():
         L.ig_cache_template_into.argtypes = [vp, vp, vp, vp, P(ctypes.c_float), i, vp, vp]
         L.ig_cache_bytes.argtypes = [vp, i, P(ctypes.c_size_t)]
         L.ig_cache_attach.argtypes = [vp, i, vp, ctypes.c_size_t, P(vp)]
+        L.ig_cache_export.argtypes = [vp, vp, ctypes.c_size_t]
+        L.ig_cache_import.argtypes = [vp, vp, P(vp)]
         L.ig_debug_dump_kv.argtypes = [vp, i, i, vp, vp, vp]
         for name in EXPORTS:
             if name not in ("ig_ctx_destroy", "ig_cache_free", "ig_mask_free", "ig_last_error",
@@ -230,6 +233,19 @@ def ig_cache_bytes(ctx: int, n_steps: int) -> int:
 def ig_cache_attach(ctx: int, n_steps: int, host_ptr: int, nbytes: int) -> int:
     out = ctypes.c_void_p()
     _check(lib().ig_cache_attach(ctx, n_steps, host_ptr, nbytes, ctypes.byref(out)))
+    return out.value
+
+
+def ig_cache_export(cache: int) -> bytes:
+    buf = ctypes.create_string_buffer(IG_CACHE_HANDLE_BYTES)
+    _check(lib().ig_cache_export(cache, buf, IG_CACHE_HANDLE_BYTES))
+    return buf.raw
+
+
+def ig_cache_import(ctx: int, handle: bytes) -> int:
+    buf = ctypes.create_string_buffer(bytes(handle), IG_CACHE_HANDLE_BYTES)
+    out = ctypes.c_void_p()
+    _check(lib().ig_cache_import(ctx, buf, ctypes.byref(out)))
     return out.value
 
 

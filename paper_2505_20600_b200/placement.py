@@ -149,28 +149,56 @@ class Worker:
 
 
 class Placement:
+    """Algorithm 2 over n_workers GPU replicas.  uplinks (optional): the host-link uplink each
+    worker's GPU sits behind (e.g. GPUs sharing a PCIe switch, from `nvidia-smi topo -m` and the
+    concurrent-H2D probe, tools/probe_box.py --concurrent), with uplink_load_slope the seconds
+    per byte of one uplink shared by all its GPUs (SURVEY §8(e) "add a per-uplink term to a_l so
+    the policy pairs high-m with low-m requests on siblings").  A worker's per-block load time is
+    then max(Load(own bytes), uplink_load_slope * bytes of every worker on its uplink)."""
+
     def __init__(self, desc, model: LatencyModel, n_workers: int, max_batch: int = 8,
-                 elem_bytes: int = 2, tie: str = "<="):
+                 elem_bytes: int = 2, tie: str = "<=", uplinks: Optional[Sequence[int]] = None,
+                 uplink_load_slope: float = 0.0):
         self.desc, self.model, self.max_batch = desc, model, max_batch
         self.elem_bytes, self.tie = elem_bytes, tie
         self.workers = [Worker(i) for i in range(n_workers)]
         self.N = desc.n_double + desc.n_single
         self.L_img = desc.grid_h * desc.grid_w
+        self.uplinks = list(uplinks) if uplinks is not None else None
+        self.uplink_load_slope = uplink_load_slope
 
-    def batch_latency(self, batch: Sequence[int]) -> float:
+    def _bytes(self, batch: Sequence[int]) -> float:
+        return sum(block_load_bytes(self.desc, n, self.elem_bytes) for n in batch)
+
+    def batch_latency(self, batch: Sequence[int], wid: Optional[int] = None) -> float:
         """dp(batch, Comp, Load): Algorithm 1 over the blocks of one step of the batch, with
         C_w = Comp(sum of masked-batch FLOPs), C_w/o = Comp(dense FLOPs of the batch) and
-        L = Load(sum of cached bytes) per block (the batch sums compute and bytes)."""
+        L = Load(sum of cached bytes) per block (the batch sums compute and bytes); with
+        uplinks, L is at least the shared uplink's time for all its workers' bytes."""
         if not batch:
             return 0.0
         f_w = sum(block_flops(self.desc, n) for n in batch)
         f_wo = sum(block_flops(self.desc, self.L_img) for _ in batch)
-        b = sum(block_load_bytes(self.desc, n, self.elem_bytes) for n in batch)
-        return algorithm1(self.N, self.model.comp(f_w), self.model.comp(f_wo), self.model.load(b),
-                          self.tie)[3]
+        b = self._bytes(batch)
+        load = self.model.load(b)
+        if self.uplinks is not None and wid is not None and self.uplink_load_slope > 0 and b > 0:
+            shared = b + sum(self._bytes(w.running) for w in self.workers
+                             if w.wid != wid and self.uplinks[w.wid] == self.uplinks[wid])
+            load = max(load, self.uplink_load_slope * shared)
+        return algorithm1(self.N, self.model.comp(f_w), self.model.comp(f_wo), load, self.tie)[3]
 
     def calc_cost(self, n_m: int, w: Worker) -> float:
-        return self.batch_latency(w.running + [n_m])
+        """Algorithm 2's cost: the step latency of w's batch with the request added; with
+        uplinks, the slowest step among the workers behind w's uplink (adding bytes to w also
+        slows its siblings' loads)."""
+        if self.uplinks is None or self.uplink_load_slope <= 0:
+            return self.batch_latency(w.running + [n_m], w.wid)
+        w.running.append(n_m)
+        try:
+            return max(self.batch_latency(o.running, o.wid) for o in self.workers
+                       if self.uplinks[o.wid] == self.uplinks[w.wid])
+        finally:
+            w.running.pop()
 
     def route(self, n_m: int) -> int:
         cands = [w for w in self.workers if len(w.running) < self.max_batch] or self.workers

@@ -343,3 +343,55 @@ def test_gemm_rows_bitwise_across_tile_paths(M_small, N, K, epi):
         if epi == 1:
             ref = torch.nn.functional.gelu(ref, approximate="tanh")
         assert torch.allclose(Cs.float(), ref, rtol=2e-2, atol=2e-2 * ref.pow(2).mean().sqrt().item())
+
+
+# ------------------------------------------------------------------ peer-HBM template pool (N4)
+def _ipc_child(handle, q):
+    import sys as _s
+    import os as _o
+    _s.path.insert(0, _o.path.dirname(_o.path.abspath(__file__)))
+    import torch as _t
+    import synth as _sy
+    from paper_2505_20600_b200 import ig as _ig
+    from gpu_util import Model as _M
+    _t.cuda.set_device(0)
+    m = _M(D, _ig.IG_BF16, opts=_ig.ig_ctx_opts(4, 0, 2, 1, 0))
+    cache = _ig.ig_cache_import(m.ctx, handle)
+    mem = Member(m, 91, _mask(91))
+    sig = _sy.flow_sigmas(N_SCHED)
+    mem.step = 2
+    _ig.ig_edit_step(m.ctx, [mem.req(0, cache, sig)], 0)
+    _t.cuda.synchronize()
+    q.put(mem.latent.cpu().numpy().tobytes())
+    _ig.ig_cache_free(cache)
+    _ig.ig_mask_free(mem.mask)
+    m.close()
+
+
+def test_peer_pool_cache_import_in_another_process():
+    """A device-tier cache exported by this process (CUDA IPC) and imported by a second process
+    (here on the same GPU; across GPUs the copy lane's gather then reads the owner's HBM over
+    NVLink): the importer's edit step equals the owner's on its own cache, bit for bit."""
+    import multiprocessing as mp
+    m = Model(D, ig.IG_BF16, opts=ig.ig_ctx_opts(4, 0, 2, 1, 0))
+    kv = synth.make_cache_kv(D, 30, N_SCHED, dtype=torch.bfloat16)
+    tlat = torch.stack([synth.make_latent(D, 1100 + s) for s in range(N_SCHED)])
+    cache = ig.ig_cache_create(m.ctx, N_SCHED, ig.IG_CACHE_DEVICE)
+    fill_cache(m, cache, kv, tlat)
+    handle = ig.ig_cache_export(cache)
+    ctx_mp = mp.get_context("spawn")
+    q = ctx_mp.Queue()
+    p = ctx_mp.Process(target=_ipc_child, args=(handle, q))
+    p.start()
+    got = q.get(timeout=300)
+    p.join(timeout=120)
+    assert p.exitcode == 0
+    mem = Member(m, 91, _mask(91))
+    mem.step = 2
+    ig.ig_edit_step(m.ctx, [mem.req(0, cache, synth.flow_sigmas(N_SCHED))], 0)
+    torch.cuda.synchronize()
+    assert mem.latent.cpu().numpy().tobytes() == got
+    assert not torch.equal(mem.latent, mem.latent0)
+    ig.ig_mask_free(mem.mask)
+    ig.ig_cache_free(cache)
+    m.close()

@@ -144,3 +144,21 @@ def test_dispatch_gloo_world2():
     ids = sorted(i for r in got for i, _ in got[r])
     assert ids == list(range(20))                       # every request exactly once
     assert got[0] and got[1]                            # both replicas used
+
+
+def test_uplink_term_steers_link_heavy_requests_off_a_loaded_uplink():
+    """Workers 0 and 1 share one host uplink (as fast as ONE GPU's link), worker 2 has its own
+    (SURVEY §8(e) uplink term).  Worker 0 already streams low-m (link-heavy) requests.  A new
+    link-heavy request costs the same on the idle workers 1 and 2 without the uplink term (ties
+    go to the lowest id: worker 1); with it, worker 1's loads would share worker 0's uplink, so
+    Algorithm 2 picks worker 2."""
+    m = _model()
+    heavy = [120, 150, 100]  # n_m of ~3%: 97% of the K/V rows cross the link
+    plain = P.Placement(synth.FLUX, m, 3, max_batch=8)
+    aware = P.Placement(synth.FLUX, m, 3, max_batch=8, uplinks=[0, 0, 1], uplink_load_slope=m.load_slope)
+    for pl in (plain, aware):
+        pl.workers[0].running.extend(heavy)
+    assert plain.route(130) == 1
+    assert aware.route(130) == 2
+    # the shared uplink binds: the sibling's predicted step is slower than the same batch alone
+    assert aware.batch_latency([130], 1) > aware.batch_latency([130], 2)
