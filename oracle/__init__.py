@@ -12,3 +12,4 @@ Citations: P:n = PAPER.md line n, S:n = SPEC.md line n, C-AMB k = DESIGN.md read
 """
 from .instgenie import *  # noqa: F401,F403
 from .unet import *  # noqa: F401,F403,E402
+from .unet_full import *  # noqa: F401,F403,E402

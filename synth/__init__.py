@@ -351,3 +351,175 @@ def mixed_mask(d: ModelDesc, rid: int, lo: float = 0.05, hi: float = 0.60) -> np
 def tiny_rect_mask() -> np.ndarray:
     """Config 1: rectangle rows 4-11 x cols 4-11 on the 16x16 grid (64 tokens, 25%)."""
     return rect_mask(TINY, 4, 12, 4, 12)
+
+
+# --------------------------------------------------------------------------------------
+# Whole SDXL-shaped UNet (BASELINE config 5, SURVEY N2): conv_in -> 3 down levels (ResBlocks,
+# Transformer2Ds at levels 1 and 2, stride-2 downsamplers) -> mid (ResBlock, Transformer2D,
+# ResBlock) -> 3 up levels (ResBlocks on [h | skip] concatenations, Transformer2Ds, nearest x2
+# upsamplers + conv) -> GroupNorm, SiLU, conv_out.  Data only: shapes and the weight table.
+# --------------------------------------------------------------------------------------
+@dataclasses.dataclass(frozen=True)
+class UNetDesc:
+    name: str
+    lat_ch: int             # latent channels (4)
+    grid: int               # latent H = W (128 for 1024^2)
+    ch: Tuple[int, int, int]       # channels per level (320, 640, 1280)
+    depth: Tuple[int, int, int]    # transformer blocks per Transformer2D per level (0, 2, 10)
+    head_dim: int = 64
+    ctx_len: int = 77
+    ctx_dim: int = 2048
+    n_res: int = 2          # ResBlocks per down level (up levels: n_res + 1)
+    gn_groups: int = 32
+    gn_eps: float = 1e-5    # ResBlock / output GroupNorm
+    t2d_gn_eps: float = 1e-6
+    ln_eps: float = 1e-5    # LayerNorms inside the transformer blocks
+
+    @property
+    def temb_dim(self) -> int:
+        return 4 * self.ch[0]
+
+    def level_grid(self, lvl: int) -> int:
+        return self.grid >> lvl
+
+
+def unet_resblocks(u: UNetDesc):
+    """(prefix, level, c_in, c_out, has_t2d) of every ResBlock in execution order, with the
+    channel bookkeeping of the skip concatenations on the up path (SDXL / diffusers layout)."""
+    out = []
+    skips = [u.ch[0]]  # conv_in output
+    c = u.ch[0]
+    for lvl in range(3):
+        for r in range(u.n_res):
+            out.append((f"down.{lvl}.res.{r}", lvl, c, u.ch[lvl], u.depth[lvl] > 0))
+            c = u.ch[lvl]
+            skips.append(c)
+        if lvl < 2:
+            skips.append(c)  # downsampler output
+    out.append(("mid.res.0", 2, c, c, True))
+    out.append(("mid.res.1", 2, c, c, False))
+    for j, lvl in enumerate((2, 1, 0)):
+        for r in range(u.n_res + 1):
+            cs = skips.pop()
+            out.append((f"up.{j}.res.{r}", lvl, c + cs, u.ch[lvl], u.depth[lvl] > 0))
+            c = u.ch[lvl]
+    return out
+
+
+def unet_t2ds(u: UNetDesc):
+    """(prefix, level, channels, depth) of every Transformer2D in execution order."""
+    out = []
+    for lvl in range(3):
+        if u.depth[lvl]:
+            for r in range(u.n_res):
+                out.append((f"down.{lvl}.attn.{r}", lvl, u.ch[lvl], u.depth[lvl]))
+    out.append(("mid.attn.0", 2, u.ch[2], u.depth[2]))
+    for j, lvl in enumerate((2, 1, 0)):
+        if u.depth[lvl]:
+            for r in range(u.n_res + 1):
+                out.append((f"up.{j}.attn.{r}", lvl, u.ch[lvl], u.depth[lvl]))
+    return out
+
+
+def unet_full_weight_table(u: UNetDesc) -> List[Tuple[str, Tuple[int, ...], int]]:
+    """(name, shape, fan_in) in the fixed C-ABI order (include/ig_unet.h).  Convolutions are
+    [C_out, 3 * 3 * C_in] with k = (ky * 3 + kx) * C_in + c (K-major, the implicit-GEMM B
+    operand); linears [out, in] + bias; GroupNorm / LayerNorm gains and shifts [C]."""
+    t: List[Tuple[str, Tuple[int, ...], int]] = []
+
+    def lin(name, out_, in_, bias=True):
+        t.append((name + ".w", (out_, in_), in_))
+        if bias:
+            t.append((name + ".b", (out_,), in_))
+
+    def conv(name, cin, cout):
+        t.append((name + ".w", (cout, 9 * cin), 9 * cin))
+        t.append((name + ".b", (cout,), 9 * cin))
+
+    def gn(name, c):
+        t.append((name + ".g", (c,), 0))
+        t.append((name + ".b", (c,), 0))
+
+    E = u.temb_dim
+    lin("time.lin1", E, u.ch[0])
+    lin("time.lin2", E, E)
+    conv("conv_in", u.lat_ch, u.ch[0])
+    res = {p: (ci, co) for p, _, ci, co, _ in unet_resblocks(u)}
+    t2d = {p: (c, dep) for p, _, c, dep in unet_t2ds(u)}
+    order = []
+    for lvl in range(3):
+        for r in range(u.n_res):
+            order.append(f"down.{lvl}.res.{r}")
+            if u.depth[lvl]:
+                order.append(f"down.{lvl}.attn.{r}")
+        if lvl < 2:
+            order.append(f"down.{lvl}.downsample")
+    order += ["mid.res.0", "mid.attn.0", "mid.res.1"]
+    for j, lvl in enumerate((2, 1, 0)):
+        for r in range(u.n_res + 1):
+            order.append(f"up.{j}.res.{r}")
+            if u.depth[lvl]:
+                order.append(f"up.{j}.attn.{r}")
+        if lvl > 0:
+            order.append(f"up.{j}.upsample")
+    for p in order:
+        if p in res:
+            ci, co = res[p]
+            gn(p + ".gn1", ci)
+            conv(p + ".conv1", ci, co)
+            lin(p + ".temb", co, E)
+            gn(p + ".gn2", co)
+            conv(p + ".conv2", co, co)
+            if ci != co:
+                lin(p + ".skip", co, ci)
+        elif p in t2d:
+            c, dep = t2d[p]
+            gn(p + ".gn", c)
+            lin(p + ".proj_in", c, c)
+            F = 4 * c
+            for i in range(dep):
+                q = f"{p}.blk.{i}"
+                t += [(q + ".ln1.g", (c,), 0), (q + ".ln1.b", (c,), 0)]
+                t.append((q + ".attn1.qkv.w", (3 * c, c), c))
+                lin(q + ".attn1.out", c, c)
+                t += [(q + ".ln2.g", (c,), 0), (q + ".ln2.b", (c,), 0)]
+                t.append((q + ".attn2.q.w", (c, c), c))
+                t.append((q + ".attn2.kv.w", (2 * c, u.ctx_dim), u.ctx_dim))
+                lin(q + ".attn2.out", c, c)
+                t += [(q + ".ln3.g", (c,), 0), (q + ".ln3.b", (c,), 0)]
+                lin(q + ".ff.geglu", 2 * F, c)
+                lin(q + ".ff.out", c, F)
+            lin(p + ".proj_out", c, c)
+        else:  # resampler conv
+            lvl = int(p.split(".")[1])
+            c = u.ch[lvl] if p.startswith("down") else u.ch[(2, 1, 0)[lvl]]
+            conv(p + ".conv", c, c)
+    gn("out.gn", u.ch[0])
+    conv("conv_out", u.ch[0], u.lat_ch)
+    return t
+
+
+def make_unet_full_weights(u: UNetDesc, seed: int = 0, device="cpu", dtype=torch.float32, names=None):
+    """uniform(+-1/sqrt(fan_in)) matrices and biases; GroupNorm / LayerNorm gains 1 + 0.1 u and
+    shifts 0.1 u (the same recipe as the attention stack, C-AMB 20)."""
+    out = {}
+    for name, shape, fan_in in unet_full_weight_table(u):
+        if names is not None and name not in names:
+            continue
+        if fan_in == 0:  # norm gain / shift
+            v = uniform(seed, "unetfull." + name, shape, device) * 0.1 + (1.0 if name.endswith(".g") else 0.0)
+        else:
+            v = uniform(seed, "unetfull." + name, shape, device) * (1.0 / math.sqrt(fan_in))
+        out[name] = v.to(torch.float32).to(dtype)
+    return out
+
+
+def make_unet_latent(u: UNetDesc, rid: int, device="cpu") -> torch.Tensor:
+    """Request latent [grid * grid, lat_ch] fp32 (tokens = latent pixels, row-major)."""
+    return normal(rid, "unet_latent", (u.grid * u.grid, u.lat_ch), device).to(torch.float32)
+
+
+UNET_FULL_TINY = UNetDesc("unet_full_tiny", 4, 16, (64, 64, 128), (0, 1, 1), head_dim=64, ctx_len=7, ctx_dim=64)
+UNET_FULL_SMALL = UNetDesc("unet_full_small", 4, 32, (64, 128, 128), (0, 2, 2), head_dim=64, ctx_len=13, ctx_dim=64)
+SDXL_UNET = UNetDesc("sdxl_unet", 4, 128, (320, 640, 1280), (0, 2, 10))
+UNET_FULL = {u.name: u for u in (UNET_FULL_TINY, UNET_FULL_SMALL, SDXL_UNET)}
