@@ -193,6 +193,7 @@ ig_status ig_cache_attach(ig_ctx* ctx, int n_steps, void* host_mem, size_t bytes
 ig_status ig_cache_export(const ig_cache* cache, void* handle, size_t handle_bytes);
 ig_status ig_cache_import(ig_ctx* ctx, const void* handle, ig_cache** out);
 
+
 /* Copy of a cache into another tier (e.g. an HBM-resident hot template) in the
  * cache format of `ctx` (a bf16 cache cloned by a cache_fp8 ctx is quantized per (token,
  * head) on the device).  Same schedule.  Synchronous. */
@@ -269,6 +270,13 @@ ig_status ig_edit_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, void* stream
  * layer event.  ig_edit_step consumes a layer that was prefetched this way instead of
  * copying it again (only for layers < prefetch_depth of the next step). */
 ig_status ig_prefetch_layer(ig_ctx* ctx, const ig_edit_req* req, int layer);
+
+/* One step of a template recording (ig_cache_template's loop body, for callers that drive their
+ * own sampler — e.g. the whole-UNet runtime recording each Transformer2D's K/V): the dense step
+ * of req->latent (every token; req->mask / req->cache ignored) with every block's K/V (or Y)
+ * written to entry `step` of `cache`, and req->latent copied in as the step's template input.
+ * Enqueued on `stream`. */
+ig_status ig_record_step(ig_ctx* ctx, const ig_edit_req* req, ig_cache* cache, int step, void* stream);
 
 const char* ig_last_error(void);
 

@@ -28,6 +28,7 @@
 #include "../../include/ig.h"
 #include "../../include/ig_ops.h"
 #include "kernels.h"
+#include "ig_internal.h"
 
 using namespace ig;
 
@@ -69,6 +70,11 @@ static ig_status set_err(ig_status s, const char* fmt, ...) {
   } while (0)
 
 extern "C" const char* ig_last_error(void) { return g_err.c_str(); }
+
+ig_status ig_internal_err(ig_status s, const char* msg) {
+  g_err = msg;
+  return s;
+}
 
 // ----------------------------------------------------------------------------------------
 // structures
@@ -853,13 +859,13 @@ extern "C" ig_status ig_mask_indices(const ig_mask* m, const int32_t** idx_m, co
   return IG_OK;
 }
 
-extern "C" ig_status ig_mask_build_host(ig_ctx* ctx, const uint8_t* mask, void* stream, ig_mask** out,
-                                        int* n_masked) {
-  if (!ctx || !mask || !out) return set_err(IG_EINVAL, "NULL argument");
+// host-bitmap mask build for a token grid of L tokens (also used by the whole-UNet runtime for
+// its per-level masks, ig_internal.h)
+ig_status ig_mask_build_host_L(int device, int L, const uint8_t* mask, void* stream, ig_mask** out, int* n_masked) {
+  if (!mask || !out || L <= 0) return set_err(IG_EINVAL, "NULL argument");
   *out = nullptr;
-  CUDA_TRY(cudaSetDevice(ctx->device));
+  CUDA_TRY(cudaSetDevice(device));
   cudaStream_t st = (cudaStream_t)stream;
-  const int L = ctx->Limg;
   ig_mask* m = new ig_mask();
   m->L_img = L;
   m->bits.resize(L);
@@ -894,6 +900,12 @@ extern "C" ig_status ig_mask_build_host(ig_ctx* ctx, const uint8_t* mask, void* 
   if (n_masked) *n_masked = n;
   *out = m;
   return IG_OK;
+}
+
+extern "C" ig_status ig_mask_build_host(ig_ctx* ctx, const uint8_t* mask, void* stream, ig_mask** out,
+                                        int* n_masked) {
+  if (!ctx) return set_err(IG_EINVAL, "NULL argument");
+  return ig_mask_build_host_L(ctx->device, ctx->Limg, mask, stream, out, n_masked);
 }
 
 extern "C" void ig_mask_free(ig_mask* m) {
@@ -2581,6 +2593,24 @@ static ig_status template_record(ig_ctx* ctx, float* latent, const void* txt, co
   if (e != cudaSuccess) return set_err(IG_ECUDA, "cache_template: %s", cudaGetErrorString(e));
   ctx->stats = total;
   return IG_OK;
+}
+
+extern "C" ig_status ig_record_step(ig_ctx* ctx, const ig_edit_req* req, ig_cache* cache, int step, void* stream) {
+  if (!ctx || !req || !cache || !req->latent || (!req->cond_vec && ctx->d.n_unet == 0) ||
+      ((ctx->Lt > 0 || ctx->d.n_unet > 0) && !req->txt))
+    return set_err(IG_EINVAL, "NULL argument");
+  if (!desc_equal(cache->desc, ctx->d)) return set_err(IG_ECACHE_INCOMPAT, "cache built for another model");
+  if (step < 0 || step >= cache->n_steps) return set_err(IG_ECACHE_INCOMPAT, "step %d outside the cache schedule", step);
+  if (cache->y != ctx->o.cache_y || cache->fp8 != ctx->o.cache_fp8) return set_err(IG_ECACHE_INCOMPAT, "cache kind differs from the ctx's");
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  ig_mask* ones = nullptr;
+  ig_status s = get_ones_mask(ctx, &ones);
+  if (s != IG_OK) return s;
+  cudaStream_t st = (cudaStream_t)stream;
+  ig_edit_req r = *req;
+  r.slot = 0; r.mask = ones; r.cache = nullptr; r.step = step;
+  CUDA_TRY(cudaMemcpyAsync(cache_latent(ctx, cache, step), r.latent, (size_t)ctx->Limg * ctx->C * 4, cudaMemcpyDefault, st));
+  return step_dispatch(ctx, &r, 1, st, cache, step);
 }
 
 extern "C" ig_status ig_cache_template(ig_ctx* ctx, float* latent, const void* txt, const float* cond_vec,

@@ -1,0 +1,8 @@
+// ig_internal.h — libig functions shared between its translation units (not part of the ABI).
+#pragma once
+#include "../../include/ig.h"
+
+// a1 on a host bitmap for a grid of L tokens (ig_mask_build_host without a model context)
+ig_status ig_mask_build_host_L(int device, int L, const uint8_t* mask, void* stream, ig_mask** out, int* n_masked);
+// set the thread-local message returned by ig_last_error() (other translation units' errors)
+ig_status ig_internal_err(ig_status s, const char* msg);

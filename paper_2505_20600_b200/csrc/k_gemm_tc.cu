@@ -201,9 +201,26 @@ __device__ __forceinline__ void epilogue_chunk(const GemmArgs& g, int row, int c
     }
     case EPI_POS: {
       float* x = reinterpret_cast<float*>(g.C) + (long long)row * g.ldc + col0;
-      const bf16* pos = g.pos ? reinterpret_cast<const bf16*>(g.pos) + (long long)info->tok * g.pos_ld + col0 : nullptr;
+      const long long prow = g.pos_div > 0 ? (long long)(g.ri_off + row) / g.pos_div : (long long)info->tok;
+      const bf16* pos = g.pos ? reinterpret_cast<const bf16*>(g.pos) + prow * g.pos_ld + col0 : nullptr;
       for (int i = 0; i < 32; ++i)
         if (col0 + i < g.N) x[i] = v[i] + (pos ? __bfloat162float(pos[i]) : 0.f);
+      break;
+    }
+    case EPI_ADDRES: {
+      float* x = reinterpret_cast<float*>(g.C) + (long long)row * g.ldc + col0;
+      const float* rs = g.res + (long long)row * g.ldc + col0;
+      if (full) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const float4 a = __ldg(reinterpret_cast<const float4*>(rs) + q);
+          reinterpret_cast<float4*>(x)[q] = make_float4(v[4 * q] + a.x, v[4 * q + 1] + a.y, v[4 * q + 2] + a.z,
+                                                        v[4 * q + 3] + a.w);
+        }
+      } else {
+        for (int i = 0; i < 32; ++i)
+          if (col0 + i < g.N) x[i] = v[i] + rs[i];
+      }
       break;
     }
   }
@@ -282,7 +299,7 @@ __device__ __forceinline__ void epilogue_qkv_head(const GemmArgs& g, int row, in
   }
 }
 
-template <int BN>
+template <int BN, bool CONV = false>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const GemmArgs g, int num_m, int num_n, int G) {
@@ -333,7 +350,26 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         for (int kb = 0; kb < num_k; ++kb) {
           tc::mbar_wait(&empty[stage], phase ^ 1);
           tc::mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
-          tc::tma_load_2d(sA + stage * C::A_BYTES, &tmA, &full[stage], kb * BK, m0);
+          if constexpr (CONV) {
+            // k-block kb = (tap, 64-channel chunk); the tile's 128 output pixels are 128 / box
+            // runs of `box` consecutive pixels of one image row, each a contiguous run of the
+            // zero-padded input shifted by the tap: one TMA box per run
+            const int cch = g.conv_cin >> 6;
+            const int tap = kb / cch, cb = kb - tap * cch;
+            const int dy = tap / 3, dx = tap - dy * 3;
+            const int W = g.conv_W, H = g.conv_H, Wp = W + 2;
+            const int box = W < BM ? W : BM;
+            const long long HW = (long long)H * W;
+            for (int r = 0; r < BM / box; ++r) {
+              const long long p = (long long)m0 + r * box;
+              const long long n = p / HW, rem = p - n * HW;
+              const long long y = rem / W, x = rem - y * W;
+              const long long prow = n * (H + 2) * (long long)Wp + (y + dy) * Wp + (x + dx);
+              tc::tma_load_2d(sA + stage * C::A_BYTES + r * box * 128, &tmA, &full[stage], cb * BK, (int)prow);
+            }
+          } else {
+            tc::tma_load_2d(sA + stage * C::A_BYTES, &tmA, &full[stage], kb * BK, m0);
+          }
           tc::tma_load_2d(sB + stage * C::B_BYTES, &tmB, &full[stage], kb * BK, n0);
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
         }
@@ -635,6 +671,8 @@ void init_driver() {
     cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
     cudaFuncSetAttribute(gemm_tc_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<256>::SMEM);
     cudaFuncSetAttribute(gemm_tc_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<128>::SMEM);
+    cudaFuncSetAttribute(gemm_tc_kernel<256, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<256>::SMEM);
+    cudaFuncSetAttribute(gemm_tc_kernel<128, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<128>::SMEM);
     cudaFuncSetAttribute(gemm_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg2::SMEM);
     g_two_cta = getenv("IG_GEMM_1CTA") == nullptr;
   });
@@ -700,6 +738,7 @@ bool gemm_tc_supported(const GemmArgs& g) {
   } else if (g.epi != EPI_QKV) {
     if (!al16(g.C) || (g.ldc & 3)) return false;
     if (g.epi == EPI_GATED_RES && (!al16(g.gate) || (g.gate_ld & 3))) return false;
+    if (g.epi == EPI_ADDRES && !al16(g.res)) return false;
   }
   if (g.bias && !al16(g.bias)) return false;
   if (g.epi == EPI_QKV && ((g.qkv.head_dim != 128 && g.qkv.head_dim != 64) || (g.qkv.H % 64) || g.N + g.qkv.col_base != 3 * g.qkv.H))
@@ -762,6 +801,34 @@ void launch_gemm_tc(const GemmArgs& g, cudaStream_t st) {
     cfg.dynamicSmemBytes = Cfg<128>::SMEM;
     cudaLaunchKernelEx(&cfg, gemm_tc_kernel<128>, ta, tb, g, num_m, num_n, G);
   }
+}
+
+bool conv3x3_tc_supported(int H, int W, int cin) {
+  if (cin % 64 || H <= 0 || W <= 0) return false;
+  const bool wok = (W == 8 || W == 16 || W == 32 || W == 64 || W == 128 || W % 128 == 0);
+  return wok && ((long long)H * W) % BM == 0;
+}
+
+void launch_conv3x3_tc(const GemmArgs& g, cudaStream_t st) {
+  if (g.M <= 0 || g.N <= 0) return;
+  init_driver();
+  const int box = g.conv_W < BM ? g.conv_W : BM;
+  const long long images = g.M / ((long long)g.conv_H * g.conv_W);
+  const long long prows = images * (g.conv_H + 2) * (long long)(g.conv_W + 2);
+  CUtensorMap ta, tb;
+  make_tmap(&ta, g.A, prows, g.conv_cin, g.conv_cin, box);  // padded input rows, box of one run
+  // N > 128 takes 128 x 256 tiles, else 128 x 128 (C_out 320 / 640: 128 x 128 wastes less)
+  const bool wide = g.N >= 256 && g.N % 256 == 0;
+  const int BN = wide ? 256 : 128;
+  make_tmap(&tb, g.B, g.N, g.K, g.ldb, BN);
+  const int num_m = (g.M + BM - 1) / BM, num_n = (g.N + BN - 1) / BN;
+  const int tiles = num_m * num_n;
+  const int grid = tiles < g_num_sms ? tiles : g_num_sms;
+  const int G = raster_group(num_m, BM, g.K);
+  if (wide)
+    gemm_tc_kernel<256, true><<<grid, NUM_THREADS, Cfg<256>::SMEM, st>>>(ta, tb, g, num_m, num_n, G);
+  else
+    gemm_tc_kernel<128, true><<<grid, NUM_THREADS, Cfg<128>::SMEM, st>>>(ta, tb, g, num_m, num_n, G);
 }
 
 }  // namespace ig

@@ -165,6 +165,7 @@ enum Epi : int {
   EPI_GEGLU = 5,      // tcgen05 only, B/bias rows tile-interleaved (permute_geglu_rows): every
                       // 256-column tile holds 128 hidden columns then their 128 gate columns;
                       // C[r, n0/2 + j] = (acc_j + b_j) * gelu_erf(acc_{128+j} + b_{128+j}) (TOut)
+  EPI_ADDRES = 6,     // C[r, c] = acc + b + res[r, c]  (C and res fp32, leading dimension ldc)
 };
 // Extra arguments of the fused QKV epilogue (a6: norm, RoPE and the positional merge done
 // on the fp32 accumulators, one bf16 rounding per output).
@@ -193,6 +194,10 @@ struct GemmArgs {
   int out_f32;                           // EPI_STORE/GELU: 1 => C is fp32
   int precise_gelu;                      // 1 => tanhf instead of MUFU tanh.approx (debug)
   QkvEpi qkv;                            // EPI_QKV only
+  int pos_div;                           // EPI_POS: > 0 => table row (ri_off + row) / pos_div
+                                         // (a per-image vector, e.g. a ResBlock's timestep term)
+  const float* res;                      // EPI_ADDRES residual source
+  int conv_H, conv_W, conv_cin;          // implicit 3x3 conv (launch_conv3x3_tc), else 0
   int pdl;                               // 1: programmatic dependent launch (the prologue — barrier
                                          // init, TMEM alloc, descriptor prefetch — overlaps the
                                          // previous kernel's tail; griddepcontrol.wait before any
@@ -203,6 +208,14 @@ void launch_gemm_simt(const GemmArgs& g, cudaStream_t st);
 // tcgen05/TMEM/TMA bf16 GEMM (returns false if the shape is unsupported)
 bool gemm_tc_supported(const GemmArgs& g);
 void launch_gemm_tc(const GemmArgs& g, cudaStream_t st);
+// Implicit-GEMM 3x3 convolution (stride 1, zero padding 1) on tcgen05: output pixels m of
+// N images [H, W] (NHWC rows, M = N*H*W) x C_out = sum over the 9 taps and C_in of the
+// zero-PADDED input A [N][H+2][W+2][C_in] (bf16) times B [C_out][9*C_in] (k = tap*C_in + c).
+// The A tile of 128 output pixels at tap (dy, dx) is 128/W contiguous runs of the padded
+// buffer, each one TMA box.  Needs C_in % 64 == 0, W in {8,16,32,64,128} or W % 128 == 0,
+// (H*W) % 128 == 0 (conv3x3_tc_supported).  g.A = padded buffer, g.K = 9*C_in.
+bool conv3x3_tc_supported(int H, int W, int cin);
+void launch_conv3x3_tc(const GemmArgs& g, cudaStream_t st);
 
 // ---- a8 attention (k_attn_simt.cu / k_attn_tc.cu) ---------------------------------------
 struct AttnArgs {

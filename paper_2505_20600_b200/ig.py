@@ -27,7 +27,9 @@ EXPORTS = ["ig_weight_count", "ig_ctx_create", "ig_ctx_destroy", "ig_cache_creat
            "ig_profile_enable", "ig_profile_read", "ig_debug_block", "ig_cache_clone", "ig_cache_write",
            "ig_set_plan", "ig_last_plan", "ig_debug_set", "ig_debug_dump_kv",
            "ig_mask_build_host", "ig_stage_input", "ig_cache_template_into", "ig_cache_bytes",
-           "ig_cache_attach", "ig_cache_export", "ig_cache_import"]
+           "ig_cache_attach", "ig_cache_export", "ig_cache_import", "ig_record_step",
+           "ig_unet_weight_count", "ig_unet_create", "ig_unet_destroy", "ig_unet_mask_build",
+           "ig_unet_mask_free", "ig_unet_template", "ig_unet_cache_free", "ig_unet_step", "ig_unet_last_stats"]
 IG_CACHE_HANDLE_BYTES = 128
 IG_DBG_SPIN_COPY_NS, IG_DBG_SPIN_COMPUTE_NS, IG_DBG_DROP_RAW, IG_DBG_DROP_WAR = 1, 2, 3, 4
 IG_DBG_CORRUPT_ROW, IG_DBG_POISON_RING, IG_DBG_SEQUENTIAL = 5, 6, 7
@@ -65,6 +67,19 @@ class ig_edit_req(ctypes.Structure):
                 ("cache", ctypes.c_void_p), ("step", ctypes.c_int), ("sigma", ctypes.c_float),
                 ("sigma_next", ctypes.c_float), ("txt", ctypes.c_void_p),
                 ("cond_vec", ctypes.c_void_p)]
+
+
+class ig_unet_desc(ctypes.Structure):
+    _fields_ = [("lat_ch", ctypes.c_int), ("grid", ctypes.c_int), ("ch", ctypes.c_int * 3),
+                ("depth", ctypes.c_int * 3), ("head_dim", ctypes.c_int), ("ctx_len", ctypes.c_int),
+                ("ctx_dim", ctypes.c_int), ("n_res", ctypes.c_int), ("gn_groups", ctypes.c_int),
+                ("gn_eps", ctypes.c_float), ("t2d_gn_eps", ctypes.c_float), ("ln_eps", ctypes.c_float)]
+
+
+class ig_unet_req(ctypes.Structure):
+    _fields_ = [("latent", ctypes.c_void_p), ("mask", ctypes.c_void_p), ("cache", ctypes.c_void_p),
+                ("step", ctypes.c_int), ("sigma", ctypes.c_float), ("sigma_next", ctypes.c_float),
+                ("ctx", ctypes.c_void_p), ("cond", ctypes.c_void_p)]
 
 
 class ig_stats(ctypes.Structure):
@@ -125,11 +140,26 @@ def lib():
         L.ig_cache_bytes.argtypes = [vp, i, P(ctypes.c_size_t)]
         L.ig_cache_attach.argtypes = [vp, i, vp, ctypes.c_size_t, P(vp)]
         L.ig_cache_export.argtypes = [vp, vp, ctypes.c_size_t]
+        L.ig_record_step.argtypes = [vp, P(ig_edit_req), vp, i, vp]
+        L.ig_unet_weight_count.argtypes = [P(ig_unet_desc)]
+        L.ig_unet_weight_count.restype = i
+        L.ig_unet_create.argtypes = [P(ig_unet_desc), P(vp), i, i, i, i, P(vp)]
+        L.ig_unet_destroy.argtypes = [vp]
+        L.ig_unet_destroy.restype = None
+        L.ig_unet_mask_build.argtypes = [vp, vp, vp, P(vp), P(i)]
+        L.ig_unet_mask_free.argtypes = [vp]
+        L.ig_unet_mask_free.restype = None
+        L.ig_unet_template.argtypes = [vp, vp, vp, vp, P(ctypes.c_float), i, i, vp, P(vp)]
+        L.ig_unet_cache_free.argtypes = [vp]
+        L.ig_unet_cache_free.restype = None
+        L.ig_unet_step.argtypes = [vp, P(ig_unet_req), i, vp]
+        L.ig_unet_last_stats.argtypes = [vp, P(ig_stats)]
         L.ig_cache_import.argtypes = [vp, vp, P(vp)]
         L.ig_debug_dump_kv.argtypes = [vp, i, i, vp, vp, vp]
         for name in EXPORTS:
             if name not in ("ig_ctx_destroy", "ig_cache_free", "ig_mask_free", "ig_last_error",
-                            "ig_weight_count", "ig_last_plan"):
+                            "ig_weight_count", "ig_last_plan", "ig_unet_weight_count", "ig_unet_destroy",
+                            "ig_unet_mask_free", "ig_unet_cache_free"):
                 getattr(L, name).restype = ctypes.c_int
         _lib = L
     return _lib
@@ -355,3 +385,74 @@ def y_block_modes(n_blocks: int, kv_blocks: int):
             out.append(v)
         k += 1
     return sorted(out)
+
+
+# ---------------------------------------------------------------------------- whole UNet
+def ig_record_step(ctx: int, req: ig_edit_req, cache: int, step: int, stream: int = 0):
+    _check(lib().ig_record_step(ctx, ctypes.byref(req), cache, step, stream))
+
+
+def make_unet_desc(u) -> ig_unet_desc:
+    d = ig_unet_desc()
+    d.lat_ch, d.grid = u.lat_ch, u.grid
+    d.ch = (ctypes.c_int * 3)(*u.ch)
+    d.depth = (ctypes.c_int * 3)(*u.depth)
+    d.head_dim, d.ctx_len, d.ctx_dim, d.n_res, d.gn_groups = u.head_dim, u.ctx_len, u.ctx_dim, u.n_res, u.gn_groups
+    d.gn_eps, d.t2d_gn_eps, d.ln_eps = u.gn_eps, u.t2d_gn_eps, u.ln_eps
+    return d
+
+
+def ig_unet_weight_count(desc: ig_unet_desc) -> int:
+    return lib().ig_unet_weight_count(ctypes.byref(desc))
+
+
+def ig_unet_create(desc: ig_unet_desc, weight_ptrs, device: int = 0, max_batch: int = 8, prefetch_depth: int = 2) -> int:
+    arr = (ctypes.c_void_p * len(weight_ptrs))(*weight_ptrs)
+    out = ctypes.c_void_p()
+    _check(lib().ig_unet_create(ctypes.byref(desc), arr, len(weight_ptrs), device, max_batch, prefetch_depth,
+                                ctypes.byref(out)))
+    return out.value
+
+
+def ig_unet_destroy(u: int):
+    lib().ig_unet_destroy(u)
+
+
+def ig_unet_mask_build(u: int, mask_u8, stream: int = 0):
+    import numpy as _np
+    m = _np.ascontiguousarray(mask_u8, dtype=_np.uint8)
+    out, n = ctypes.c_void_p(), ctypes.c_int()
+    _check(lib().ig_unet_mask_build(u, m.ctypes.data, stream, ctypes.byref(out), ctypes.byref(n)))
+    return out.value, n.value
+
+
+def ig_unet_mask_free(m: int):
+    lib().ig_unet_mask_free(m)
+
+
+def ig_unet_template(u: int, latent_ptr: int, ctx_ptr: int, cond_ptr: int, sigmas, tier: int = IG_CACHE_DEVICE,
+                     stream: int = 0) -> int:
+    s = (ctypes.c_float * len(sigmas))(*[float(x) for x in sigmas])
+    out = ctypes.c_void_p()
+    _check(lib().ig_unet_template(u, latent_ptr, ctx_ptr, cond_ptr or None, s, len(sigmas) - 1, tier, stream,
+                                  ctypes.byref(out)))
+    return out.value
+
+
+def ig_unet_cache_free(c: int):
+    lib().ig_unet_cache_free(c)
+
+
+def make_unet_req(latent, mask, cache, step, sigma, sigma_next, ctx, cond=None) -> ig_unet_req:
+    return ig_unet_req(latent, mask, cache or None, step, sigma, sigma_next, ctx, cond or None)
+
+
+def ig_unet_step(u: int, reqs, stream: int = 0):
+    arr = (ig_unet_req * max(1, len(reqs)))(*reqs)
+    _check(lib().ig_unet_step(u, arr, len(reqs), stream))
+
+
+def ig_unet_last_stats(u: int) -> dict:
+    s = ig_stats()
+    _check(lib().ig_unet_last_stats(u, ctypes.byref(s)))
+    return {f: getattr(s, f) for f, _ in ig_stats._fields_}

@@ -69,3 +69,9 @@ def test_unet_desc_passes_host_validation(name):
     with pytest.raises(ig.IgError) as e:
         ig.ig_ctx_create(ig.make_desc(m, ig.IG_BF16), [1] * len(synth.weight_table(m)))
     assert e.value.name not in ("IG_EINVAL", "IG_EUNSUPPORTED"), str(e.value)
+
+
+@pytest.mark.parametrize("name", list(synth.UNET_FULL))
+def test_unet_weight_count_matches_table(name):
+    u = synth.UNET_FULL[name]
+    assert ig.ig_unet_weight_count(ig.make_unet_desc(u)) == len(synth.unet_full_weight_table(u))
