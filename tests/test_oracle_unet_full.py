@@ -209,3 +209,19 @@ def test_transformer2d_masked_full_mask_is_dense(tiny):
     mask[5:30] = 1
     got = oracle.t2d_masked(U, W, p, lvl, dep, x, mask, kv, dense, ctx)  # same-input cache
     np.testing.assert_allclose(got, dense, rtol=1e-11, atol=1e-11)
+
+
+def test_sweep_tool_flop_model_matches_oracle_macs():
+    """tools/unet_full_sweep.py's FLOP model (its own arithmetic: the tool may not import the
+    oracle) equals 2x the oracle's MAC counter for the dense step of the SDXL shape, and the
+    Transformer2Ds' share of the dense step is in the paper's range (82% for SDXL)."""
+    import sys, os
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools"))
+    import unet_full_sweep as T
+    u = synth.SDXL_UNET
+    macs = oracle.unet_full_macs(u)
+    assert T.dense_conv_macs(u) == macs["conv"]
+    ones = np.ones(u.grid * u.grid, np.uint8)
+    assert abs(T.flops(u, ones) - 2 * (macs["conv"] + macs["t2d"])) <= 1e-9 * T.flops(u, ones)
+    share = macs["t2d"] / (macs["conv"] + macs["t2d"])
+    assert 0.7 < share < 0.85
