@@ -41,6 +41,15 @@ ig_status ig_op_attention(int dtype, const void* Q, long long ldq, void* O, long
  * followed by a stream synchronisation (any host/device combination, UVA pointers). */
 ig_status ig_copy(void* dst, const void* src, size_t bytes, void* stream);
 
+/* Whole-UNet 3x3 convolution (stride 1, zero padding 1; include/ig_unet.h): y [N*H*W][C_out] fp32
+ * (NHWC rows) = conv(x) + bias, x_padded = bf16 [N][H+2][W+2][C_in] with zero borders, w = bf16
+ * [C_out][9*C_in] (k = (ky*3 + kx)*C_in + c), bias bf16 [C_out] or NULL.  Implicit-GEMM tcgen05
+ * kernel when C_in % 64 == 0, W in {8,16,32,64,128} or W % 128 == 0 and (H*W) % 128 == 0
+ * (2-CTA 256x256 tiles when C_out % 256 == 0, else 128x128); otherwise im2col + the tcgen05
+ * GEMM.  C_in % 8 == 0, C_out % 4 == 0 (IG_EINVAL / IG_EUNSUPPORTED otherwise). */
+ig_status ig_op_conv3x3(const void* x_padded, int n_img, int H, int W, int cin, const void* w, const void* bias,
+                        int cout, float* y, void* stream);
+
 /* Per-request input staging for the host-buffer path (e.g. a request's text tokens at
  * admission): an SM-driven copy of `bytes` from PINNED host memory `src` (cudaHostAlloc /
  * cudaHostRegister'ed, device-mapped) into device memory `dst`, enqueued on `stream`.  Unlike a

@@ -29,6 +29,7 @@
 #include "../../include/ig_ops.h"
 #include "kernels.h"
 #include "ig_internal.h"
+#include "unet_kernels.h"
 
 using namespace ig;
 
@@ -2789,6 +2790,31 @@ extern "C" ig_status ig_op_attention(int dtype, const void* Q, long long ldq, vo
   }
   CUDA_TRY(cudaFreeAsync(dsegs, st));
   CUDA_TRY(cudaStreamSynchronize(st));  // host segment vector lifetime
+  CUDA_TRY(cudaGetLastError());
+  return IG_OK;
+}
+
+extern "C" ig_status ig_op_conv3x3(const void* x_padded, int n_img, int H, int W, int cin, const void* w,
+                                   const void* bias, int cout, float* y, void* stream) {
+  if (!x_padded || !w || !y) return set_err(IG_EINVAL, "NULL argument");
+  if (n_img <= 0 || H <= 0 || W <= 0 || cin <= 0 || cout <= 0 || cin % 8)
+    return set_err(IG_EINVAL, "bad shape (C_in must be a multiple of 8)");
+  cudaStream_t st = (cudaStream_t)stream;
+  GemmArgs g{};
+  g.B = w; g.ldb = 9LL * cin; g.bias = bias; g.C = y; g.ldc = cout;
+  g.M = n_img * H * W; g.N = cout; g.K = 9 * cin; g.epi = EPI_STORE; g.out_f32 = 1;
+  if (cout % 4) return set_err(IG_EUNSUPPORTED, "C_out must be a multiple of 4");
+  if (conv3x3_tc_supported(H, W, cin)) {
+    g.A = x_padded; g.lda = cin; g.conv_H = H; g.conv_W = W; g.conv_cin = cin;
+    launch_conv3x3_tc(g, st);
+  } else {  // im2col of the padded input + the tcgen05 GEMM
+    bf16* col = nullptr;
+    CUDA_TRY(cudaMallocAsync((void**)&col, (size_t)g.M * 9 * cin * 2, st));
+    launch_im2col_padded((const bf16*)x_padded, cin, n_img, H, W, 9 * cin, col, st);
+    g.A = col; g.lda = 9LL * cin;
+    launch_gemm_tc(g, st);
+    CUDA_TRY(cudaFreeAsync(col, st));
+  }
   CUDA_TRY(cudaGetLastError());
   return IG_OK;
 }

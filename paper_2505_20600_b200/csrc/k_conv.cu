@@ -28,15 +28,23 @@ __global__ void __launch_bounds__(256) gn_partial_kernel(const float* __restrict
   float* ssum = sm;
   float* ssq = sm + C;
   for (int c = threadIdx.x; c < C; c += blockDim.x) {
-    float s = 0.f, q = 0.f;
-    for (int p = p0; p < p1; ++p) {
-      const long long row = (long long)n * P + p;
-      const float v = c < C1 ? x1[row * C1 + c] : x2[row * C2 + (c - C1)];
-      s += v;
-      q = fmaf(v, v, q);
+    const float* base = c < C1 ? x1 + c : x2 + (c - C1);
+    const long long ld = c < C1 ? C1 : C2;
+    float s0 = 0.f, q0 = 0.f, s1 = 0.f, q1 = 0.f;
+    int p = p0;
+#pragma unroll 4
+    for (; p + 1 < p1; p += 2) {  // two independent chains, loads in flight
+      const float v0 = base[((long long)n * P + p) * ld];
+      const float v1 = base[((long long)n * P + p + 1) * ld];
+      s0 += v0; q0 = fmaf(v0, v0, q0);
+      s1 += v1; q1 = fmaf(v1, v1, q1);
     }
-    ssum[c] = s;
-    ssq[c] = q;
+    if (p < p1) {
+      const float v0 = base[((long long)n * P + p) * ld];
+      s0 += v0; q0 = fmaf(v0, v0, q0);
+    }
+    ssum[c] = s0 + s1;
+    ssq[c] = q0 + q1;
   }
   __syncthreads();
   const int cg = C / G;
@@ -74,17 +82,28 @@ void launch_gn_stats(const float* x1, int C1, const float* x2, int C2, int N, in
 
 __device__ __forceinline__ float silu_f(float v) { return v / (1.f + __expf(-v)); }
 
+// per (image, channel) affine coefficients of GroupNorm: y = x * a + b with
+// a = rstd_g * gamma_c, b = beta_c - mean_g * rstd_g * gamma_c
+__global__ void gn_coef_kernel(const float2* __restrict__ stats, const bf16* __restrict__ gamma, const bf16* __restrict__ beta,
+                               int G, int C, float2* __restrict__ coef) {
+  const int n = blockIdx.x, cg = C / G;
+  for (int c = threadIdx.x; c < C; c += blockDim.x) {
+    const float2 s = stats[n * G + c / cg];
+    const float a = s.y * __bfloat162float(gamma[c]);
+    coef[n * C + c] = make_float2(a, __bfloat162float(beta[c]) - s.x * a);
+  }
+}
+
 // dst: zero-padded NHWC bf16 [N][H+2][W+2][C] (every element written: the borders are zeros,
-// so one buffer can be reused with any channel count); value = act(GN([x1 | x2]))
+// so one buffer can be reused with any channel count); value = act(GN([x1 | x2])); 8 channels
+// per thread (C1 % 8 == 0: a vector never straddles the two sources)
 __global__ void __launch_bounds__(256) gn_apply_padded_kernel(const float* __restrict__ x1, int C1,
                                                               const float* __restrict__ x2, int C2,
-                                                              const float2* __restrict__ stats, const bf16* __restrict__ gamma,
-                                                              const bf16* __restrict__ beta, int G, int do_silu, int N,
+                                                              const float2* __restrict__ coef, int do_silu, int N,
                                                               int H, int W, bf16* __restrict__ dst) {
   const int C = C1 + C2;
-  const int cv = C / 8;  // 8-channel vectors (C % 8 == 0)
+  const int cv = C / 8;
   const long long total = (long long)N * (H + 2) * (W + 2) * cv;
-  const int cg = C / G;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
     const int v = (int)(i % cv);
     const long long pp = i / cv;
@@ -95,21 +114,25 @@ __global__ void __launch_bounds__(256) gn_apply_padded_kernel(const float* __res
     uint4 out = make_uint4(0, 0, 0, 0);
     if (yy >= 1 && yy <= H && xx >= 1 && xx <= W) {
       const long long row = ((long long)n * H + (yy - 1)) * W + (xx - 1);
+      const int c0 = v * 8;
+      const float4* src = c0 < C1 ? reinterpret_cast<const float4*>(x1 + row * C1 + c0)
+                                  : reinterpret_cast<const float4*>(x2 + row * C2 + (c0 - C1));
+      const float4 a = src[0], b = src[1];
+      const float xv[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+      const float4* cf = reinterpret_cast<const float4*>(coef + (long long)n * C + c0);
+      float y[8];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float4 k = cf[q];
+        y[2 * q] = fmaf(xv[2 * q], k.x, k.y);
+        y[2 * q + 1] = fmaf(xv[2 * q + 1], k.z, k.w);
+      }
       uint32_t* w = reinterpret_cast<uint32_t*>(&out);
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        float y[2];
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int c = v * 8 + 2 * e + h;
-          float a = c < C1 ? x1[row * C1 + c] : x2[row * C2 + (c - C1)];
-          if (stats) {
-            const float2 s = stats[n * G + c / cg];
-            a = (a - s.x) * s.y * __bfloat162float(gamma[c]) + __bfloat162float(beta[c]);
-          }
-          y[h] = do_silu ? silu_f(a) : a;
-        }
-        __nv_bfloat162 p = __floats2bfloat162_rn(y[0], y[1]);
+        const float u0 = do_silu ? silu_f(y[2 * e]) : y[2 * e];
+        const float u1 = do_silu ? silu_f(y[2 * e + 1]) : y[2 * e + 1];
+        __nv_bfloat162 p = __floats2bfloat162_rn(u0, u1);
         w[e] = *reinterpret_cast<uint32_t*>(&p);
       }
     }
@@ -118,10 +141,12 @@ __global__ void __launch_bounds__(256) gn_apply_padded_kernel(const float* __res
 }
 
 void launch_gn_apply_padded(const float* x1, int C1, const float* x2, int C2, const float2* stats, const bf16* gamma,
-                            const bf16* beta, int G, int do_silu, int N, int H, int W, bf16* dst, cudaStream_t st) {
+                            const bf16* beta, int G, int do_silu, int N, int H, int W, bf16* dst, float2* coef,
+                            cudaStream_t st) {
+  gn_coef_kernel<<<N, 256, 0, st>>>(stats, gamma, beta, G, C1 + C2, coef);
   const long long total = (long long)N * (H + 2) * (W + 2) * ((C1 + C2) / 8);
   const int blocks = (int)std::min<long long>((total + 255) / 256, 148 * 16);
-  gn_apply_padded_kernel<<<blocks, 256, 0, st>>>(x1, C1, x2, C2, stats, gamma, beta, G, do_silu, N, H, W, dst);
+  gn_apply_padded_kernel<<<blocks, 256, 0, st>>>(x1, C1, x2, C2, coef, do_silu, N, H, W, dst);
 }
 
 // nearest x2 upsampling of x fp32 [N][H][W][C] into zero-padded bf16 [N][2H+2][2W+2][C]
@@ -187,9 +212,49 @@ __global__ void __launch_bounds__(256) im2col_kernel(const float* __restrict__ x
   }
 }
 
+// 8 consecutive k (one tap, 8 channels) per thread: two float4 loads, one 16-byte store
+__global__ void __launch_bounds__(256) im2col8_kernel(const float* __restrict__ x, int C, int N, int H, int W, int s,
+                                                      int Kp, bf16* __restrict__ dst) {
+  const int Ho = (H - 1) / s + 1, Wo = (W - 1) / s + 1;
+  const int kv = Kp / 8;
+  const long long total = (long long)N * Ho * Wo * kv;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+    const int k = (int)(i % kv) * 8;
+    const long long m = i / kv;
+    uint4 out = make_uint4(0, 0, 0, 0);
+    if (k < 9 * C) {
+      const int tap = k / C, c = k - tap * C;
+      const int ky = tap / 3, kx = tap - ky * 3;
+      const int xo = (int)(m % Wo);
+      const long long t = m / Wo;
+      const int yo = (int)(t % Ho);
+      const int n = (int)(t / Ho);
+      const int yi = yo * s + ky - 1, xi = xo * s + kx - 1;
+      if (yi >= 0 && yi < H && xi >= 0 && xi < W) {
+        const float4* p = reinterpret_cast<const float4*>(x + (((long long)n * H + yi) * W + xi) * C + c);
+        const float4 a = p[0], b = p[1];
+        uint32_t* w = reinterpret_cast<uint32_t*>(&out);
+        __nv_bfloat162 q0 = __floats2bfloat162_rn(a.x, a.y), q1 = __floats2bfloat162_rn(a.z, a.w);
+        __nv_bfloat162 q2 = __floats2bfloat162_rn(b.x, b.y), q3 = __floats2bfloat162_rn(b.z, b.w);
+        w[0] = *reinterpret_cast<uint32_t*>(&q0);
+        w[1] = *reinterpret_cast<uint32_t*>(&q1);
+        w[2] = *reinterpret_cast<uint32_t*>(&q2);
+        w[3] = *reinterpret_cast<uint32_t*>(&q3);
+      }
+    }
+    reinterpret_cast<uint4*>(dst)[i] = out;
+  }
+}
+
 void launch_im2col(const float* x, int C, int N, int H, int W, int stride, const float* scale, int Kp, bf16* dst,
                    cudaStream_t st) {
   const int Ho = (H - 1) / stride + 1, Wo = (W - 1) / stride + 1;
+  if (!scale && C % 8 == 0 && Kp % 8 == 0) {
+    const long long total = (long long)N * Ho * Wo * (Kp / 8);
+    const int blocks = (int)std::min<long long>((total + 255) / 256, 148 * 16);
+    im2col8_kernel<<<blocks, 256, 0, st>>>(x, C, N, H, W, stride, Kp, dst);
+    return;
+  }
   const long long total = (long long)N * Ho * Wo * Kp;
   const int blocks = (int)std::min<long long>((total + 255) / 256, 148 * 16);
   im2col_kernel<<<blocks, 256, 0, st>>>(x, C, N, H, W, stride, scale, Kp, dst);
@@ -386,16 +451,27 @@ void launch_unet_euler(const UReq* rq, const URows* rl, int n, int max_rows, int
 // plain bf16 copy of the [x1 | x2] concatenation (the 1x1 skip projection's A operand)
 __global__ void cat_bf16_kernel(const float* __restrict__ x1, int C1, const float* __restrict__ x2, int C2, long long rows,
                                 bf16* __restrict__ dst) {
-  const int C = C1 + C2;
-  const long long total = rows * C;
+  const int C = C1 + C2, cv = C / 8;  // C1 % 8 == 0: 8-channel vectors never straddle
+  const long long total = rows * cv;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
-    const long long row = i / C;
-    const int c = (int)(i - row * C);
-    dst[i] = __float2bfloat16_rn(c < C1 ? x1[row * C1 + c] : x2[row * C2 + (c - C1)]);
+    const long long row = i / cv;
+    const int c = (int)(i - row * cv) * 8;
+    const float4* p = c < C1 ? reinterpret_cast<const float4*>(x1 + row * C1 + c)
+                             : reinterpret_cast<const float4*>(x2 + row * C2 + (c - C1));
+    const float4 a = p[0], b = p[1];
+    uint4 out;
+    uint32_t* w = reinterpret_cast<uint32_t*>(&out);
+    __nv_bfloat162 q0 = __floats2bfloat162_rn(a.x, a.y), q1 = __floats2bfloat162_rn(a.z, a.w);
+    __nv_bfloat162 q2 = __floats2bfloat162_rn(b.x, b.y), q3 = __floats2bfloat162_rn(b.z, b.w);
+    w[0] = *reinterpret_cast<uint32_t*>(&q0);
+    w[1] = *reinterpret_cast<uint32_t*>(&q1);
+    w[2] = *reinterpret_cast<uint32_t*>(&q2);
+    w[3] = *reinterpret_cast<uint32_t*>(&q3);
+    reinterpret_cast<uint4*>(dst)[i] = out;
   }
 }
 void launch_cat_bf16(const float* x1, int C1, const float* x2, int C2, long long rows, bf16* dst, cudaStream_t st) {
-  const long long total = rows * (C1 + C2);
+  const long long total = rows * ((C1 + C2) / 8);
   cat_bf16_kernel<<<(int)std::min<long long>((total + 255) / 256, 148 * 16), 256, 0, st>>>(x1, C1, x2, C2, rows, dst);
 }
 

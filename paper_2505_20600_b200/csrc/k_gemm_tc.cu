@@ -347,6 +347,21 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         int mb, nb;
         tile_coords(t, num_m, num_n, G, mb, nb);
         const int m0 = mb * BM, n0 = nb * BN;
+        // implicit conv: the padded-input row of every run's first pixel at tap (0, 0), computed
+        // once per tile (64-bit divisions per k-block would bound the single producer thread)
+        int cbox = 1, cbase[16];
+        if constexpr (CONV) {
+          const int W = g.conv_W, H = g.conv_H;
+          cbox = W < BM ? W : BM;
+          const long long HW = (long long)H * W;
+          for (int r = 0; r < BM / cbox; ++r) {
+            const long long p = (long long)m0 + r * cbox;
+            const long long n = p / HW, rem = p - n * HW;
+            const long long y = rem / W, x = rem - y * W;
+            cbase[r] = (int)(n * (H + 2) * (long long)(W + 2) + y * (W + 2) + x);
+          }
+        }
+        int tap = 0, cb = 0;
         for (int kb = 0; kb < num_k; ++kb) {
           tc::mbar_wait(&empty[stage], phase ^ 1);
           tc::mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
@@ -354,19 +369,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             // k-block kb = (tap, 64-channel chunk); the tile's 128 output pixels are 128 / box
             // runs of `box` consecutive pixels of one image row, each a contiguous run of the
             // zero-padded input shifted by the tap: one TMA box per run
-            const int cch = g.conv_cin >> 6;
-            const int tap = kb / cch, cb = kb - tap * cch;
             const int dy = tap / 3, dx = tap - dy * 3;
-            const int W = g.conv_W, H = g.conv_H, Wp = W + 2;
-            const int box = W < BM ? W : BM;
-            const long long HW = (long long)H * W;
-            for (int r = 0; r < BM / box; ++r) {
-              const long long p = (long long)m0 + r * box;
-              const long long n = p / HW, rem = p - n * HW;
-              const long long y = rem / W, x = rem - y * W;
-              const long long prow = n * (H + 2) * (long long)Wp + (y + dy) * Wp + (x + dx);
-              tc::tma_load_2d(sA + stage * C::A_BYTES + r * box * 128, &tmA, &full[stage], cb * BK, (int)prow);
-            }
+            const int shift = dy * (g.conv_W + 2) + dx;
+            for (int r = 0; r < BM / cbox; ++r)
+              tc::tma_load_2d(sA + stage * C::A_BYTES + r * cbox * 128, &tmA, &full[stage], cb * BK, cbase[r] + shift);
+            if (++cb == (g.conv_cin >> 6)) { cb = 0; ++tap; }
           } else {
             tc::tma_load_2d(sA + stage * C::A_BYTES, &tmA, &full[stage], kb * BK, m0);
           }
@@ -487,6 +494,7 @@ struct Cfg2 {
   static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256 + 2 * 256 * 2 /*bias slices*/;
 };
 
+template <bool CONV = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     const GemmArgs g, int num_m, int num_n, int G) {
@@ -538,10 +546,31 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         int mb, nb;
         tile_coords(t, num_m, num_n, G, mb, nb);
         const int m0 = mb * 256 + rank * 128, n0 = nb * BN + rank * 128;
+        int cbox = 1, cbase[16];  // implicit conv: runs of this CTA's 128 output pixels (see gemm_tc_kernel)
+        if constexpr (CONV) {
+          const int W = g.conv_W, H = g.conv_H;
+          cbox = W < 128 ? W : 128;
+          const long long HW = (long long)H * W;
+          for (int r = 0; r < 128 / cbox; ++r) {
+            const long long p = (long long)m0 + r * cbox;
+            const long long n = p / HW, rem = p - n * HW;
+            const long long y = rem / W, x = rem - y * W;
+            cbase[r] = (int)(n * (H + 2) * (long long)(W + 2) + y * (W + 2) + x);
+          }
+        }
+        int tap = 0, cb = 0;
         for (int kb = 0; kb < num_k; ++kb) {
           tc::mbar_wait(&empty[stage], phase ^ 1);
           if (rank == 0) tc::mbar_arrive_expect_tx(&full[stage], 2 * C::STAGE_BYTES);
-          tc::tma_load_2d_2sm(sA + stage * C::A_BYTES, &tmA, &full[stage], kb * BK, m0);
+          if constexpr (CONV) {
+            const int dy = tap / 3, dx = tap - dy * 3;
+            const int shift = dy * (g.conv_W + 2) + dx;
+            for (int r = 0; r < 128 / cbox; ++r)
+              tc::tma_load_2d_2sm(sA + stage * C::A_BYTES + r * cbox * 128, &tmA, &full[stage], cb * BK, cbase[r] + shift);
+            if (++cb == (g.conv_cin >> 6)) { cb = 0; ++tap; }
+          } else {
+            tc::tma_load_2d_2sm(sA + stage * C::A_BYTES, &tmA, &full[stage], kb * BK, m0);
+          }
           tc::tma_load_2d_2sm(sB + stage * C::B_BYTES, &tmB, &full[stage], kb * BK, n0);
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
         }
@@ -673,7 +702,8 @@ void init_driver() {
     cudaFuncSetAttribute(gemm_tc_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<128>::SMEM);
     cudaFuncSetAttribute(gemm_tc_kernel<256, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<256>::SMEM);
     cudaFuncSetAttribute(gemm_tc_kernel<128, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<128>::SMEM);
-    cudaFuncSetAttribute(gemm_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg2::SMEM);
+    cudaFuncSetAttribute(gemm_tc2_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg2::SMEM);
+    cudaFuncSetAttribute(gemm_tc2_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg2::SMEM);
     g_two_cta = getenv("IG_GEMM_1CTA") == nullptr;
   });
 }
@@ -774,9 +804,9 @@ void launch_gemm_tc(const GemmArgs& g, cudaStream_t st) {
       at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
       at[0].val.programmaticStreamSerializationAllowed = 1;
       cfg.attrs = at; cfg.numAttrs = 1;
-      cudaLaunchKernelEx(&cfg, gemm_tc2_kernel, ta, tb, g, num_m, num_n, G2);
+      cudaLaunchKernelEx(&cfg, gemm_tc2_kernel<false>, ta, tb, g, num_m, num_n, G2);
     } else {
-      gemm_tc2_kernel<<<2 * clusters, NUM_THREADS, Cfg2::SMEM, st>>>(ta, tb, g, num_m, num_n, G2);
+      gemm_tc2_kernel<false><<<2 * clusters, NUM_THREADS, Cfg2::SMEM, st>>>(ta, tb, g, num_m, num_n, G2);
     }
     return;
   }
@@ -817,7 +847,19 @@ void launch_conv3x3_tc(const GemmArgs& g, cudaStream_t st) {
   const long long prows = images * (g.conv_H + 2) * (long long)(g.conv_W + 2);
   CUtensorMap ta, tb;
   make_tmap(&ta, g.A, prows, g.conv_cin, g.conv_cin, box);  // padded input rows, box of one run
-  // N > 128 takes 128 x 256 tiles, else 128 x 128 (C_out 320 / 640: 128 x 128 wastes less)
+  // C_out a multiple of 256 (1280): 2-CTA 256 x 256 tiles (half the B operand per SM), like the
+  // projections; else 128 x 128 one-CTA tiles (C_out 320 / 640: no half-empty 256-column tile)
+  static const bool conv_1cta = getenv("IG_CONV_1CTA") != nullptr;  // A/B switch
+  if (!conv_1cta && g_two_cta && g.N % 256 == 0 && g.M > 128) {
+    CUtensorMap tb2;
+    make_tmap(&tb2, g.B, g.N, g.K, g.ldb, 128);
+    const int num_m = (g.M + 255) / 256, num_n = g.N / 256;
+    const int tiles = num_m * num_n;
+    const int clusters = tiles < g_num_sms / 2 ? tiles : g_num_sms / 2;
+    gemm_tc2_kernel<true><<<2 * clusters, NUM_THREADS, Cfg2::SMEM, st>>>(ta, tb2, g, num_m, num_n,
+                                                                         raster_group(num_m, 256, g.K));
+    return;
+  }
   const bool wide = g.N >= 256 && g.N % 256 == 0;
   const int BN = wide ? 256 : 128;
   make_tmap(&tb, g.B, g.N, g.K, g.ldb, BN);

@@ -113,7 +113,7 @@ struct ig_unet {
   bf16* catb = nullptr;           // [x1 | x2] bf16 (skip projection operand)
   float* pk1 = nullptr;           // packed fp32 rows (proj_in / proj_out outputs)
   float* T[3] = {};               // per level: the stacks' per-request state [B][P][C] fp32
-  float2 *gpart = nullptr, *gstats = nullptr;
+  float2 *gpart = nullptr, *gstats = nullptr, *gcoef = nullptr;
   size_t pad_elems = 0, col_elems = 0;
   ig_mask* ones[3] = {};
   // per-step descriptors (pinned mapped host -> device)
@@ -332,6 +332,11 @@ extern "C" ig_status ig_unet_create(const ig_unet_desc* desc, const void* const*
   ok &= dm((void**)&u->tproj, (size_t)B * tot * 2);
   ok &= dm((void**)&u->gpart, (size_t)B * ((u->P[0] + 63) / 64) * d.gn_groups * sizeof(float2));
   ok &= dm((void**)&u->gstats, (size_t)B * d.gn_groups * sizeof(float2));
+  {
+    int cm = 0;
+    for (auto& r : u->res) cm = std::max(cm, std::max(r.ci, r.co));
+    ok &= dm((void**)&u->gcoef, (size_t)B * cm * sizeof(float2));
+  }
   // the down path's skip tensors
   {
     int c = d.ch[0];
@@ -376,7 +381,7 @@ extern "C" void ig_unet_destroy(ig_unet* u) {
   }
   for (float* p : u->skip_buf) if (p) cudaFree(p);
   void* bufs[] = {u->tw, u->tb, u->conv_in_w, u->gv, u->sinu, u->tv1, u->tv2, u->pad, u->col, u->catb, u->pk1,
-                  u->lat, u->eps, u->scale, u->tsilu, u->tproj, u->gpart, u->gstats, u->d_desc};
+                  u->lat, u->eps, u->scale, u->tsilu, u->tproj, u->gpart, u->gstats, u->gcoef, u->d_desc};
   for (void* b : bufs) if (b) cudaFree(b);
   if (u->h_desc) cudaFreeHost(u->h_desc);
   if (u->ev_desc) cudaEventDestroy(u->ev_desc);
@@ -486,14 +491,14 @@ void resblock(Ctx& c, const Res& r, const float* x1, int C1, const float* x2, in
   ig_unet* u = c.u;
   const int g = u->d.grid >> r.lvl, P = u->P[r.lvl];
   gn_stats(u, c.st, x1, C1, x2, C2, c.n, P, u->d.gn_eps);
-  launch_gn_apply_padded(x1, C1, x2, C2, u->gstats, r.gn1g, r.gn1b, u->d.gn_groups, 1, c.n, g, g, u->pad, c.st);
-  u->stats.kernel_launches++;
+  launch_gn_apply_padded(x1, C1, x2, C2, u->gstats, r.gn1g, r.gn1b, u->d.gn_groups, 1, c.n, g, g, u->pad, u->gcoef, c.st);
+  u->stats.kernel_launches += 2;
   GemmArgs a{};
   a.C = h1; a.ldc = r.co; a.epi = EPI_POS; a.pos = u->tproj + r.temb_off; a.pos_ld = u->t_ld; a.pos_div = P;
   conv(u, c.st, c.n, g, g, r.ci, r.conv1, a);
   gn_stats(u, c.st, h1, r.co, nullptr, 0, c.n, P, u->d.gn_eps);
-  launch_gn_apply_padded(h1, r.co, nullptr, 0, u->gstats, r.gn2g, r.gn2b, u->d.gn_groups, 1, c.n, g, g, u->pad, c.st);
-  u->stats.kernel_launches++;
+  launch_gn_apply_padded(h1, r.co, nullptr, 0, u->gstats, r.gn2g, r.gn2b, u->d.gn_groups, 1, c.n, g, g, u->pad, u->gcoef, c.st);
+  u->stats.kernel_launches += 2;
   const float* res = x1;
   if (r.ci != r.co) {  // 1x1 (linear) skip projection of [x1 | x2]
     launch_cat_bf16(x1, C1, x2, C2, (long long)c.n * P, u->catb, c.st);
@@ -658,8 +663,8 @@ ig_status forward(Ctx& c) {
   // ---- out: GN -> SiLU -> conv_out -> eps; Euler on the masked latent rows
   gn_stats(u, st, h, d.ch[0], nullptr, 0, n, u->P[0], d.gn_eps);
   launch_gn_apply_padded(h, d.ch[0], nullptr, 0, u->gstats, u->out_gng, u->out_gnb, d.gn_groups, 1, n, d.grid, d.grid,
-                         u->pad, st);
-  u->stats.kernel_launches++;
+                         u->pad, u->gcoef, st);
+  u->stats.kernel_launches += 2;
   GemmArgs go{};
   go.C = u->eps; go.ldc = d.lat_ch; go.epi = EPI_STORE; go.out_f32 = 1;
   conv(u, st, n, d.grid, d.grid, d.ch[0], u->conv_out, go);

@@ -20,8 +20,10 @@ struct URows {           // a request's row list at one level
 
 void launch_gn_stats(const float* x1, int C1, const float* x2, int C2, int N, int P, int G, float eps,
                      float2* partial, float2* stats, cudaStream_t st);
+// coef: scratch [N][C1 + C2] float2 (per image and channel GroupNorm affine)
 void launch_gn_apply_padded(const float* x1, int C1, const float* x2, int C2, const float2* stats, const bf16* gamma,
-                            const bf16* beta, int G, int do_silu, int N, int H, int W, bf16* dst, cudaStream_t st);
+                            const bf16* beta, int G, int do_silu, int N, int H, int W, bf16* dst, float2* coef,
+                            cudaStream_t st);
 void launch_upsample_padded(const float* x, int C, int N, int H, int W, bf16* dst, cudaStream_t st);
 void launch_im2col(const float* x, int C, int N, int H, int W, int stride, const float* scale, int Kp, bf16* dst,
                    cudaStream_t st);

@@ -29,7 +29,8 @@ EXPORTS = ["ig_weight_count", "ig_ctx_create", "ig_ctx_destroy", "ig_cache_creat
            "ig_mask_build_host", "ig_stage_input", "ig_cache_template_into", "ig_cache_bytes",
            "ig_cache_attach", "ig_cache_export", "ig_cache_import", "ig_record_step",
            "ig_unet_weight_count", "ig_unet_create", "ig_unet_destroy", "ig_unet_mask_build",
-           "ig_unet_mask_free", "ig_unet_template", "ig_unet_cache_free", "ig_unet_step", "ig_unet_last_stats"]
+           "ig_unet_mask_free", "ig_unet_template", "ig_unet_cache_free", "ig_unet_step", "ig_unet_last_stats",
+           "ig_op_conv3x3"]
 IG_CACHE_HANDLE_BYTES = 128
 IG_DBG_SPIN_COPY_NS, IG_DBG_SPIN_COMPUTE_NS, IG_DBG_DROP_RAW, IG_DBG_DROP_WAR = 1, 2, 3, 4
 IG_DBG_CORRUPT_ROW, IG_DBG_POISON_RING, IG_DBG_SEQUENTIAL = 5, 6, 7
@@ -141,6 +142,7 @@ def lib():
         L.ig_cache_attach.argtypes = [vp, i, vp, ctypes.c_size_t, P(vp)]
         L.ig_cache_export.argtypes = [vp, vp, ctypes.c_size_t]
         L.ig_record_step.argtypes = [vp, P(ig_edit_req), vp, i, vp]
+        L.ig_op_conv3x3.argtypes = [vp, i, i, i, i, vp, vp, i, vp, vp]
         L.ig_unet_weight_count.argtypes = [P(ig_unet_desc)]
         L.ig_unet_weight_count.restype = i
         L.ig_unet_create.argtypes = [P(ig_unet_desc), P(vp), i, i, i, i, P(vp)]
@@ -456,3 +458,8 @@ def ig_unet_last_stats(u: int) -> dict:
     s = ig_stats()
     _check(lib().ig_unet_last_stats(u, ctypes.byref(s)))
     return {f: getattr(s, f) for f, _ in ig_stats._fields_}
+
+
+def ig_op_conv3x3(x_padded: int, n_img: int, H: int, W: int, cin: int, w: int, bias: int, cout: int, y: int,
+                  stream: int = 0):
+    _check(lib().ig_op_conv3x3(x_padded, n_img, H, W, cin, w, bias or None, cout, y, stream))

@@ -136,3 +136,26 @@ def test_same_input_cache_is_bitwise_dense_and_empty_mask_untouched(unet):
     ig.ig_unet_mask_free(mh)
     ig.ig_unet_mask_free(zh)
     ig.ig_unet_cache_free(cache)
+
+
+@pytest.mark.parametrize("n,H,W,cin,cout", [(2, 32, 32, 128, 256), (1, 64, 64, 64, 320), (1, 128, 128, 64, 128),
+                                            (3, 16, 8, 64, 64), (2, 8, 8, 64, 128), (1, 32, 32, 1280, 1280),
+                                            (1, 4, 4, 64, 64)])
+def test_conv3x3_vs_torch(n, H, W, cin, cout):
+    """ig_op_conv3x3 (implicit-GEMM tcgen05 conv: 1-CTA and 2-CTA tiles, every run width; im2col
+    fallback for (H*W) % 128 != 0) against torch conv2d in fp32 on the same bf16 inputs."""
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    torch.backends.cudnn.allow_tf32 = False  # a true fp32 reference
+    g = torch.Generator(device="cuda").manual_seed(H * W + cin + cout)
+    x = torch.randn(n, H, W, cin, device="cuda", generator=g).bfloat16()
+    w = (torch.randn(cout, 3, 3, cin, device="cuda", generator=g) / (9 * cin) ** 0.5).bfloat16()
+    b = torch.randn(cout, device="cuda", generator=g).bfloat16()
+    xp = torch.nn.functional.pad(x, (0, 0, 1, 1, 1, 1)).contiguous()
+    y = torch.empty(n * H * W, cout, device="cuda", dtype=torch.float32)
+    ig.ig_op_conv3x3(xp.data_ptr(), n, H, W, cin, w.data_ptr(), b.data_ptr(), cout, y.data_ptr())
+    torch.cuda.synchronize()
+    ref = torch.nn.functional.conv2d(x.float().permute(0, 3, 1, 2), w.float().permute(0, 3, 1, 2), b.float(),
+                                     padding=1).permute(0, 2, 3, 1).reshape(n * H * W, cout)
+    ok, worst = ctol(y.cpu().numpy(), ref.cpu().numpy(), 1e-3)
+    assert ok, worst
