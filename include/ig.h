@@ -98,9 +98,11 @@ typedef struct {
                        /* max_batch * L)                                                  */
   int prefetch_depth;  /* D: layers the copy lane runs ahead of compute (default 2)       */
   int copy_mode;       /* 0 = full-L per-layer cudaMemcpyAsync (all L_img rows),          */
-                       /* 1 = compacted: only unmasked rows — host-tier caches as runs of  */
-                       /*     the unmasked index list, batched cudaMemcpyBatchAsync per    */
-                       /*     layer (copy engines); HBM-tier caches via the SM gather      */
+                       /* 1 = compacted: only unmasked rows — host-tier caches by the copy */
+                       /*     engines, one cudaMemcpyAsync / cudaMemcpy2DAsync per strided */
+                       /*     group of unmasked runs (a group may also cover a few masked  */
+                       /*     rows; the step then waits for the copy before the fresh K/V  */
+                       /*     merge); HBM-tier caches via the SM gather                    */
                        /* 2 = compacted: zero-copy SM gather kernel on the copy stream     */
   int debug_checks;    /* 1 = check the latent for non-finite values after each step     */
   int cache_fp8;       /* 1 = caches created by this ctx store K/V as e4m3 with a fp32   */
@@ -294,6 +296,16 @@ ig_status ig_set_plan(ig_ctx* ctx, int mode, int k, double comp_s_per_flop, doub
 /* Prefix length chosen by the last ig_edit_step. */
 int ig_last_plan(const ig_ctx* ctx);
 
+/* Host-only helper (no device, no ctx): the strided DMA groups the copy lane issues for a
+ * host-tier cache under copy_mode 1 (a7; P:546-552 block-wise loading of the cached rows).
+ * mask: L bytes, nonzero = masked token (raster order).  groups: cap x 4 ints per group
+ * {start, len, stride, count} in token rows — the group moves rows [start + i*stride,
+ * start + i*stride + len) for i < count.  Every unmasked token is covered exactly once; the
+ * masked rows also covered are the merged gaps (<= 2 rows between two unmasked runs) plus at
+ * most (the group's run rows + 64) / 8 per group.  *n_groups is always set;
+ * IG_EINVAL when it exceeds cap (nothing written) or on a NULL / bad argument. */
+ig_status ig_plan_copy_groups(const uint8_t* mask, int L, int* groups, int cap, int* n_groups);
+
 /* Counters of the last ig_edit_step / ig_cache_template call on this ctx. */
 typedef struct {
   long long kernel_launches;  /* libig kernels enqueued                      */
@@ -303,6 +315,7 @@ typedef struct {
   long long rows;             /* packed query rows M                         */
   long long host_ns;          /* host time spent enqueueing the call, not counting the wait for
                                  a free descriptor slot (back-pressure from the GPU)            */
+  long long dma_calls;        /* copy-engine calls the copy lane issued (copy_mode 1 groups)  */
 } ig_stats;
 ig_status ig_last_stats(const ig_ctx* ctx, ig_stats* out);
 

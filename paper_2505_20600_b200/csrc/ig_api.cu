@@ -114,11 +114,76 @@ struct ModT {
 };
 constexpr int NSTAGE = 4;
 constexpr int MAXR = 32;  // max ring depth R = D + 1
+
+// a7 host tier, copy_mode 1: the unmasked runs of a mask (raster order over the token grid)
+// covered by strided groups, one DMA call each: group g moves token rows
+// [start + i * stride, start + i * stride + len) for i < count (cudaMemcpy2DAsync when
+// count > 1).  Runs separated by at most COPY_MAX_GAP masked rows are merged first (a noisy
+// mask edge would otherwise cost one call per stray token); then a rectangle's runs (equal
+// length, one image row apart) form one group, and the runs around a blob are grouped as long
+// as the masked rows a group also covers stay within ~1/8 of the rows it must copy.  Those extra rows carry template values that the block's
+// fresh K/V overwrite: the compute lane waits for the copy before the QKV epilogue's positional
+// merge (early wait).
+struct CopyGroup {
+  int start, len, stride, count;
+};
+struct Copy2D {  // one DMA call: `height` rows of `width` bytes, `pitch` apart on both sides
+  void* dst;
+  const void* src;
+  size_t width, height, pitch;
+};
+constexpr int COPY_MAX_GAP = 2;  // masked gaps of <= 2 rows inside a merged run (noisy mask edges)
+void make_copy_groups(const std::vector<std::pair<int, int>>& exact_runs, int L, std::vector<CopyGroup>& out) {
+  out.clear();
+  std::vector<std::pair<int, int>> runs;  // runs separated by short masked gaps merged
+  for (const auto& r : exact_runs) {
+    if (!runs.empty() && r.first - (runs.back().first + runs.back().second) <= COPY_MAX_GAP)
+      runs.back().second = r.first + r.second - runs.back().first;
+    else
+      runs.push_back(r);
+  }
+  size_t i = 0;
+  int cov_end = 0;  // end of the previous group's last row: groups never overlap
+  while (i < runs.size()) {
+    CopyGroup g{runs[i].first, runs[i].second, 0, 1};
+    long long exact = runs[i].second;
+    size_t j = i + 1;
+    if (j < runs.size()) {
+      const int stride = runs[j].first - runs[i].first;
+      int base = g.start, top = g.start + g.len;  // row k covers [base + k stride, top + k stride)
+      for (; j < runs.size(); ++j) {
+        const int k = (int)(j - i);
+        const int s = runs[j].first - k * stride, e = runs[j].first + runs[j].second - k * stride;
+        const int nb = std::min(base, s), nt = std::max(top, e);
+        const long long ex = exact + runs[j].second;
+        const long long cover = (long long)(nt - nb) * (k + 1);
+        const int next = j + 1 < runs.size() ? runs[j + 1].first : L;  // the last row stops before it
+        if (nb < cov_end || nt - nb > stride || nt + (long long)k * stride > next || 8 * (cover - ex) > ex + 64) break;
+        base = nb;
+        top = nt;
+        exact = ex;
+      }
+      if (j - i > 1) g = CopyGroup{base, top - base, stride, (int)(j - i)};
+      else j = i + 1;
+    }
+    out.push_back(g);
+    cov_end = g.start + (g.count - 1) * g.stride + g.len;
+    i = j;
+  }
+}
+// DMA calls for one plane: groups over token rows of `row` bytes between positional buffers
+void push_group_copies(std::vector<Copy2D>& v, char* dst, const char* src, size_t row,
+                       const std::vector<CopyGroup>& groups) {
+  for (const CopyGroup& g : groups)
+    v.push_back(Copy2D{dst + (size_t)g.start * row, src + (size_t)g.start * row, (size_t)g.len * row,
+                       (size_t)g.count, (size_t)g.stride * row});
+}
 }  // namespace
 
 struct ig_mask {
   int L_img = 0, n_m = 0;
   std::vector<std::pair<int, int>> runs;  // host: maximal runs (start, len) of unmasked tokens
+  std::vector<CopyGroup> groups;          // host: strided DMA groups covering `runs` (copy_mode 1)
   std::vector<uint8_t> bits;              // host: 1 = masked (load deduplication)
   uint8_t* bits_dev = nullptr;            // device copy of bits
   int32_t* idx = nullptr;  // device: idx_m at [0, L_img), idx_u at [L_img, 2 L_img), n_m at [2 L_img]
@@ -214,12 +279,11 @@ struct ig_ctx {
   struct Pref { const ig_cache* c = nullptr; int step = -1; };
   std::vector<Pref> pref;  // [max_batch * R]
   ig_mask* ones_mask = nullptr;
-  std::vector<void*> b_dst, b_src;  // batched-copy scratch (copy_mode 1)
+  std::vector<Copy2D> b_copies;      // copy-lane scratch (copy_mode 1): one DMA call each
   // FP8 cache staging (cache_fp8): per (slot, ring buffer) e4m3 rows + scales landed by the DMA
   // lane before the dequantizing gather into the bf16 ring; per ring buffer for recording
   uint8_t* q8in = nullptr;  float* q8in_scl = nullptr;
   uint8_t* q8rec = nullptr; float* q8rec_scl = nullptr;
-  std::vector<size_t> b_size;
   // Y recording staging (cache_y): per ring buffer the block output's image rows in the
   // compute dtype, read by the D2H on the copy stream; ev_yrec guards its reuse (WAR)
   void* yrec = nullptr;
@@ -232,7 +296,7 @@ struct ig_ctx {
   size_t copy_err_idx = 0;
   // ig_debug_set keys (race tests and fault injection; all 0 in normal operation)
   long long dbg[9] = {};
-  // Copy-lane host thread: the cache-prefetch enqueues (cudaMemcpyBatchAsync of the unmasked
+  // Copy-lane host thread: the cache-prefetch enqueues (strided DMA copies of the unmasked
   // runs, gathers, dedupe) run on their own host thread, so the compute launches are never
   // stuck behind the copy engines' queue back-pressure.  Jobs run in order; the compute thread
   // waits (host side) only for the job that recorded the ring event it is about to wait on.
@@ -800,6 +864,29 @@ extern "C" ig_status ig_profile_read(ig_ctx* ctx, ig_prof_entry out[IG_K_NCLASS]
   return IG_OK;
 }
 
+extern "C" ig_status ig_plan_copy_groups(const uint8_t* mask, int L, int* groups, int cap, int* n_groups) {
+  if (!mask || !n_groups || L <= 0 || cap < 0 || (cap > 0 && !groups)) return set_err(IG_EINVAL, "bad argument");
+  std::vector<std::pair<int, int>> runs;
+  for (int i = 0; i < L;) {
+    if (mask[i]) { ++i; continue; }
+    int j = i;
+    while (j < L && !mask[j]) ++j;
+    runs.push_back({i, j - i});
+    i = j;
+  }
+  std::vector<CopyGroup> g;
+  make_copy_groups(runs, L, g);
+  *n_groups = (int)g.size();
+  if ((int)g.size() > cap) return set_err(IG_EINVAL, "%d groups exceed cap %d", (int)g.size(), cap);
+  for (size_t k = 0; k < g.size(); ++k) {
+    groups[4 * k + 0] = g[k].start;
+    groups[4 * k + 1] = g[k].len;
+    groups[4 * k + 2] = g[k].stride;
+    groups[4 * k + 3] = g[k].count;
+  }
+  return IG_OK;
+}
+
 extern "C" ig_status ig_last_stats(const ig_ctx* ctx, ig_stats* out) {
   if (!ctx || !out) return set_err(IG_EINVAL, "NULL argument");
   *out = ctx->stats;
@@ -839,6 +926,7 @@ extern "C" ig_status ig_mask_build(ig_ctx* ctx, const uint8_t* mask, void* strea
     m->runs.push_back({i, j - i});
     i = j;
   }
+  make_copy_groups(m->runs, ctx->Limg, m->groups);
   if (e != cudaSuccess) {
     cudaFree(m->idx);
     if (m->bits_dev) cudaFree(m->bits_dev);
@@ -879,6 +967,7 @@ ig_status ig_mask_build_host_L(int device, int L, const uint8_t* mask, void* str
     m->runs.push_back({i, j - i});
     i = j;
   }
+  make_copy_groups(m->runs, L, m->groups);
   // one stream-ordered allocation: idx_m | idx_u | n_m (int32), then the bitmap (u8)
   const size_t idx_bytes = ((size_t)(2 * L + 1) * sizeof(int32_t) + 15) & ~(size_t)15;
   void* base = nullptr;
@@ -1299,6 +1388,7 @@ struct CopyPlan {
   // HBM -> HBM from its ring buffer (kv_dedupe_kernel)
   std::vector<int> dsrc;                                // per request: source index or -1
   std::vector<std::vector<std::pair<int, int>>> druns;  // per member: runs of U_r \ U_src
+  std::vector<std::vector<CopyGroup>> dgroups;          // per member: DMA groups covering druns
   std::vector<int> dshared;                             // per member: |U_r ∩ U_src|
   std::vector<const ig_cache*> dcache;                  // per dedupe entry: the cache its pair shares
   DedupeArgs dd{};
@@ -1381,10 +1471,8 @@ static void issue_copy_now(ig_ctx* ctx, const std::vector<StepReq>& sr, const Kv
   const int n = (int)sr.size();
   const size_t row = (size_t)ctx->H * ctx->esz;
   const size_t txt_off = (size_t)ctx->Lt * row, vplane = (size_t)ctx->L * row;
-  std::vector<void*>& dsts = ctx->b_dst;
-  std::vector<void*>& srcs = ctx->b_src;
-  std::vector<size_t>& sizes = ctx->b_size;
-  dsts.clear(); srcs.clear(); sizes.clear();
+  std::vector<Copy2D>& cps = ctx->b_copies;
+  cps.clear();
   for (int q = 0; q < n; ++q) {
     if (!sr[q].use_cache) continue;
     const ig_edit_req* r = sr[q].r;
@@ -1400,14 +1488,8 @@ static void issue_copy_now(ig_ctx* ctx, const std::vector<StepReq>& sr, const Kv
         uint8_t* sd = ctx->q8in + ((size_t)slot * ctx->R + buf) * 2 * pl + pl;
         char* ss = (char*)ctx->q8in_scl + ((size_t)slot * ctx->R + buf) * 2 * spl + spl;
         const char* src = cache_plane(ctx, c, r->step, b - 1, 2);
-        for (auto& run : sr[q].m->runs) {
-          dsts.push_back(sd + (size_t)run.first * ctx->H);
-          srcs.push_back((void*)(src + (size_t)run.first * ctx->H));
-          sizes.push_back((size_t)run.second * ctx->H);
-        }
-        dsts.push_back(ss);
-        srcs.push_back((void*)cache_scales(ctx, c, r->step, b - 1, 2));
-        sizes.push_back(spl);
+        push_group_copies(cps, (char*)sd, src, (size_t)ctx->H, sr[q].m->groups);
+        cps.push_back(Copy2D{ss, cache_scales(ctx, c, r->step, b - 1, 2), spl, 1, spl});
         cs.h2d_bytes += (long long)n_u * ctx->H + (long long)spl;
       } else {
         cs.d2d_bytes += (long long)n_u * (ctx->H + 4 * ctx->d.heads);
@@ -1427,12 +1509,7 @@ static void issue_copy_now(ig_ctx* ctx, const std::vector<StepReq>& sr, const Kv
         by = (long long)ctx->Limg * row;
       } else {
         const bool dd = !plan.dsrc.empty() && plan.dsrc[q] >= 0;
-        for (auto& run : dd ? plan.druns[q] : sr[q].m->runs) {
-          const size_t off = (size_t)run.first * row;
-          dsts.push_back(dst + off);
-          srcs.push_back((void*)(src + off));
-          sizes.push_back((size_t)run.second * row);
-        }
+        push_group_copies(cps, dst, src, row, dd ? plan.dgroups[q] : sr[q].m->groups);
         by = (long long)(dd ? n_u - plan.dshared[q] : n_u) * row;
         if (dd) cs.d2d_bytes += (long long)plan.dshared[q] * row;
       }
@@ -1447,14 +1524,8 @@ static void issue_copy_now(ig_ctx* ctx, const std::vector<StepReq>& sr, const Kv
         char* ss = (char*)ctx->q8in_scl + ((size_t)slot * ctx->R + buf) * 2 * spl;
         for (int w = 0; w < 2; ++w) {
           const char* src = cache_plane(ctx, c, r->step, b, w);
-          for (auto& run : sr[q].m->runs) {
-            dsts.push_back(sd + w * pl + (size_t)run.first * ctx->H);
-            srcs.push_back((void*)(src + (size_t)run.first * ctx->H));
-            sizes.push_back((size_t)run.second * ctx->H);
-          }
-          dsts.push_back(ss + w * spl);
-          srcs.push_back((void*)cache_scales(ctx, c, r->step, b, w));
-          sizes.push_back(spl);
+          push_group_copies(cps, (char*)(sd + w * pl), src, (size_t)ctx->H, sr[q].m->groups);
+          cps.push_back(Copy2D{ss + w * spl, cache_scales(ctx, c, r->step, b, w), spl, 1, spl});
         }
         by = 2LL * n_u * ctx->H + 2LL * ctx->Limg * ctx->d.heads * 4;
       }
@@ -1474,15 +1545,9 @@ static void issue_copy_now(ig_ctx* ctx, const std::vector<StepReq>& sr, const Kv
     } else if (host && ctx->o.copy_mode == 1) {  // DMA runs straight into the ring
       char* dst = (char*)ctx->kv_arena + ((size_t)slot * ctx->slot_stride + (size_t)buf * ctx->buf_elems) * ctx->esz;
       const bool dd = !plan.dsrc.empty() && plan.dsrc[q] >= 0;
-      for (int w = 0; w < 2; ++w) {
-        const char* src = cache_plane(ctx, c, r->step, b, w);
-        for (auto& run : dd ? plan.druns[q] : sr[q].m->runs) {
-          const size_t off = (size_t)run.first * row;
-          dsts.push_back(dst + w * vplane + txt_off + off);
-          srcs.push_back((void*)(src + off));
-          sizes.push_back((size_t)run.second * row);
-        }
-      }
+      for (int w = 0; w < 2; ++w)
+        push_group_copies(cps, dst + w * vplane + txt_off, cache_plane(ctx, c, r->step, b, w), row,
+                          dd ? plan.dgroups[q] : sr[q].m->groups);
       by = 2LL * (dd ? n_u - plan.dshared[q] : n_u) * row;
       if (dd) cs.d2d_bytes += 2LL * plan.dshared[q] * row;
     } else {
@@ -1490,23 +1555,18 @@ static void issue_copy_now(ig_ctx* ctx, const std::vector<StepReq>& sr, const Kv
     }
     if (host) cs.h2d_bytes += by; else cs.d2d_bytes += by;
   }
-  if (!sizes.empty()) {
-    cudaMemcpyAttributes attr{};
-    attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-    attr.flags = cudaMemcpyFlagPreferOverlapWithCompute;
-    size_t attr_idx = 0, fail = 0;
-    constexpr size_t CHUNKC = 128;  // bounded batches (very large batches crash driver 580)
-    for (size_t i = 0; i < sizes.size(); i += CHUNKC) {
-      const size_t cnt = std::min(CHUNKC, sizes.size() - i);
-      fail = SIZE_MAX;
-      const cudaError_t ce = cudaMemcpyBatchAsync(dsts.data() + i, srcs.data() + i, sizes.data() + i, cnt, &attr,
-                                                  &attr_idx, 1, &fail, ctx->copy_st);
-      if (ce != cudaSuccess && ctx->copy_err == cudaSuccess) {
-        ctx->copy_err = ce;
-        ctx->copy_err_idx = i + (fail == SIZE_MAX ? 0 : fail);
-      }
+  for (size_t i = 0; i < cps.size(); ++i) {  // one DMA call per group (copy engines)
+    const Copy2D& cp = cps[i];
+    const cudaError_t ce =
+        cp.height == 1 ? cudaMemcpyAsync(cp.dst, cp.src, cp.width, cudaMemcpyDefault, ctx->copy_st)
+                       : cudaMemcpy2DAsync(cp.dst, cp.pitch, cp.src, cp.pitch, cp.width, cp.height, cudaMemcpyDefault,
+                                           ctx->copy_st);
+    if (ce != cudaSuccess && ctx->copy_err == cudaSuccess) {
+      ctx->copy_err = ce;
+      ctx->copy_err_idx = i;
     }
   }
+  cs.dma_calls += (long long)cps.size();
   if (plan.dd.n > 0) {  // rows shared with an earlier same-(cache, step) request: HBM -> HBM
     // per entry from ITS cache (entries of one batch may sit on caches of different kinds)
     DedupeArgs dd = plan.dd;
@@ -1719,6 +1779,7 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
     };
     plan.dsrc.assign(na, -1);
     plan.druns.assign(na, {});
+    plan.dgroups.assign(na, {});
     plan.dshared.assign(na, 0);
     for (int q = 0; q < na && !no_dedupe; ++q) {
       if (!dedupable(q)) continue;
@@ -1736,6 +1797,7 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
             runs.push_back({i, j - i});
             i = j;
           }
+          make_copy_groups(runs, ctx->Limg, plan.dgroups[q]);
           plan.dsrc[q] = q0;
           plan.dshared[q] = shared;
           DedupeEnt& e = plan.dd.e[plan.dd.n++];
@@ -2000,6 +2062,7 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
       c->stats.h2d_bytes += c->cstats.h2d_bytes;
       c->stats.d2d_bytes += c->cstats.d2d_bytes;
       c->stats.kernel_launches += c->cstats.kernel_launches;
+      c->stats.dma_calls += c->cstats.dma_calls;
       c->cstats = ig_stats{};
       c->lane_on = false;
     }
@@ -2264,9 +2327,13 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
     }
     cudaEventRecord(ctx->ev_copy[buf], ctx->copy_st);
   };
-  // full-L copies also write the masked rows, so they must land before the fresh K/V
-  // scatter; compacted copies touch only unmasked rows and are awaited right before attention
-  const bool late_wait = ctx->o.copy_mode != 0 && !record;
+  // full-L copies (copy_mode 0) and the host tier's strided DMA groups (copy_mode 1, which may
+  // cover masked rows) also write masked rows, so they must land before the fresh K/V merge;
+  // the SM gathers touch only unmasked rows and are awaited right before attention
+  bool host_dma = false;
+  for (auto& q : sr)
+    host_dma |= q.use_cache && q.r->cache->tier == IG_CACHE_HOST && ctx->o.copy_mode == 1;
+  const bool late_wait = ctx->o.copy_mode != 0 && !record && !host_dma;
   const bool drop_raw = ctx->dbg[IG_DBG_DROP_RAW] != 0;  // negative control of the race tests
   auto wait_copy = [&](int buf) {
     if ((any_cache || record) && !late_wait && !(drop_raw && !record)) {
@@ -2516,6 +2583,7 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
     stats.h2d_bytes += ctx->cstats.h2d_bytes;
     stats.d2d_bytes += ctx->cstats.d2d_bytes;
     stats.kernel_launches += ctx->cstats.kernel_launches;
+    stats.dma_calls += ctx->cstats.dma_calls;
     ctx->cstats = ig_stats{};
     ctx->lane_on = false;
   }

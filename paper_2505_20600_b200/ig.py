@@ -30,7 +30,7 @@ EXPORTS = ["ig_weight_count", "ig_ctx_create", "ig_ctx_destroy", "ig_cache_creat
            "ig_cache_attach", "ig_cache_export", "ig_cache_import", "ig_record_step",
            "ig_unet_weight_count", "ig_unet_create", "ig_unet_destroy", "ig_unet_mask_build",
            "ig_unet_mask_free", "ig_unet_template", "ig_unet_cache_free", "ig_unet_step", "ig_unet_last_stats",
-           "ig_op_conv3x3"]
+           "ig_op_conv3x3", "ig_plan_copy_groups"]
 IG_CACHE_HANDLE_BYTES = 128
 IG_DBG_SPIN_COPY_NS, IG_DBG_SPIN_COMPUTE_NS, IG_DBG_DROP_RAW, IG_DBG_DROP_WAR = 1, 2, 3, 4
 IG_DBG_CORRUPT_ROW, IG_DBG_POISON_RING, IG_DBG_SEQUENTIAL = 5, 6, 7
@@ -86,7 +86,8 @@ class ig_unet_req(ctypes.Structure):
 class ig_stats(ctypes.Structure):
     _fields_ = [("kernel_launches", ctypes.c_longlong), ("h2d_bytes", ctypes.c_longlong),
                 ("d2d_bytes", ctypes.c_longlong), ("d2h_bytes", ctypes.c_longlong),
-                ("rows", ctypes.c_longlong), ("host_ns", ctypes.c_longlong)]
+                ("rows", ctypes.c_longlong), ("host_ns", ctypes.c_longlong),
+                ("dma_calls", ctypes.c_longlong)]
 
 
 class ig_prof_entry(ctypes.Structure):
@@ -122,6 +123,7 @@ def lib():
         L.ig_last_error.restype = ctypes.c_char_p
         L.ig_last_plan.restype = ctypes.c_int
         L.ig_last_stats.argtypes = [vp, P(ig_stats)]
+        L.ig_plan_copy_groups.argtypes = [vp, i, P(ctypes.c_int), i, P(i)]
         L.ig_op_gemm.argtypes = [i, vp, ll, vp, ll, vp, vp, ll, i, i, i, i, i, vp]
         L.ig_op_attention.argtypes = [i, vp, ll, vp, ll, vp, P(ctypes.c_int32), i, i, i, i, vp]
         L.ig_copy.argtypes = [vp, vp, ctypes.c_size_t, vp]
@@ -306,6 +308,17 @@ def ig_prefetch_layer(ctx: int, req: ig_edit_req, layer: int):
 
 def ig_last_error() -> str:
     return lib().ig_last_error().decode()
+
+
+def ig_plan_copy_groups(mask_u8) -> list:
+    """Host-only: the copy lane's strided DMA groups [(start, len, stride, count)] for a mask."""
+    import numpy as _np
+    m = _np.ascontiguousarray(mask_u8, dtype=_np.uint8).reshape(-1)
+    cap = m.size + 1
+    buf = (ctypes.c_int * (4 * cap))()
+    n = ctypes.c_int()
+    _check(lib().ig_plan_copy_groups(m.ctypes.data, int(m.size), buf, cap, ctypes.byref(n)))
+    return [tuple(buf[4 * k:4 * k + 4]) for k in range(n.value)]
 
 
 def ig_last_stats(ctx: int) -> dict:
