@@ -296,15 +296,17 @@ ig_status ig_set_plan(ig_ctx* ctx, int mode, int k, double comp_s_per_flop, doub
 /* Prefix length chosen by the last ig_edit_step. */
 int ig_last_plan(const ig_ctx* ctx);
 
-/* Host-only helper (no device, no ctx): the strided DMA groups the copy lane issues for a
+/* Host-only helper (no device, no ctx): the copy-engine calls the copy lane issues for a
  * host-tier cache under copy_mode 1 (a7; P:546-552 block-wise loading of the cached rows).
- * mask: L bytes, nonzero = masked token (raster order).  groups: cap x 4 ints per group
- * {start, len, stride, count} in token rows — the group moves rows [start + i*stride,
- * start + i*stride + len) for i < count.  Every unmasked token is covered exactly once; the
- * masked rows also covered are the merged gaps (<= 2 rows between two unmasked runs) plus at
- * most (the group's run rows + 64) / 8 per group.  *n_groups is always set;
- * IG_EINVAL when it exceeds cap (nothing written) or on a NULL / bad argument. */
-ig_status ig_plan_copy_groups(const uint8_t* mask, int L, int* groups, int cap, int* n_groups);
+ * mask: L bytes, nonzero = masked token (raster order over a grid W tokens wide; W = 0 if
+ * unknown).  row_bytes: one K (or V) row.  groups: cap x 4 ints per group {start, len, stride,
+ * count} in token rows — one call moves rows [start + i*stride, start + i*stride + len) for
+ * i < count, of the K and the V plane.  Every unmasked token is covered exactly once; masked
+ * rows are covered only where that is cheaper than another call (a call costs the link time of
+ * ~275 KB, so the plan minimises calls x 275 KB / (2 row_bytes) + masked rows copied).
+ * *n_groups is always set; IG_EINVAL when it exceeds cap (nothing written) or on a bad
+ * argument. */
+ig_status ig_plan_copy_groups(const uint8_t* mask, int L, int W, int row_bytes, int* groups, int cap, int* n_groups);
 
 /* Counters of the last ig_edit_step / ig_cache_template call on this ctx. */
 typedef struct {

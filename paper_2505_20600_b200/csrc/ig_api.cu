@@ -116,67 +116,140 @@ constexpr int NSTAGE = 4;
 constexpr int MAXR = 32;  // max ring depth R = D + 1
 
 // a7 host tier, copy_mode 1: the unmasked runs of a mask (raster order over the token grid)
-// covered by strided groups, one DMA call each: group g moves token rows
-// [start + i * stride, start + i * stride + len) for i < count (cudaMemcpy2DAsync when
-// count > 1).  Runs separated by at most COPY_MAX_GAP masked rows are merged first (a noisy
-// mask edge would otherwise cost one call per stray token); then a rectangle's runs (equal
-// length, one image row apart) form one group, and the runs around a blob are grouped as long
-// as the masked rows a group also covers stay within ~1/8 of the rows it must copy.  Those extra rows carry template values that the block's
-// fresh K/V overwrite: the compute lane waits for the copy before the QKV epilogue's positional
-// merge (early wait).
+// are covered by groups, ONE copy-engine call each: group g moves token rows
+// [start + i * stride, start + i * stride + len) for i < count (a 1-D span when count == 1,
+// cudaMemcpy2DAsync rows otherwise; the K and V planes of a group together in one
+// cudaMemcpy3DAsync when the plane strides allow).  A copy-engine call costs ~5 us whatever its
+// size (tools/dma_probe.py on this pool: 6 KB copies run at 1.2 GB/s, a 2-D copy of 64 rows of
+// 24 KB at 48 GB/s, the link peaks at 55.5 GB/s), i.e. as much link time as ~275 KB of
+// payload, so the grouping is a shortest path over the runs: cost = calls x call_rows + masked
+// rows copied (also planned with masked gaps < call_rows / 3 pre-merged; the cheaper plan wins).  Candidate groups over runs i..j: the contiguous span [s_i, e_j), or strided
+// rows with stride s_{i+1} - s_i or the grid width W (a rectangle's runs, or the rows around a
+// blob).  Masked rows a group also covers carry template values that the block's fresh K/V
+// overwrite: the compute lane waits for the copy before the QKV epilogue's positional merge
+// (early wait).
 struct CopyGroup {
   int start, len, stride, count;
 };
-struct Copy2D {  // one DMA call: `height` rows of `width` bytes, `pitch` apart on both sides
-  void* dst;
+struct CopyOp {  // one copy-engine call: `height` rows of `width` bytes, `pitch` apart, on
+  void* dst;     // `planes` planes (src_plane / dst_plane bytes apart)
   const void* src;
   size_t width, height, pitch;
+  int planes;
+  size_t src_plane, dst_plane;
 };
-constexpr int COPY_MAX_GAP = 2;  // masked gaps of <= 2 rows inside a merged run (noisy mask edges)
-void make_copy_groups(const std::vector<std::pair<int, int>>& exact_runs, int L, std::vector<CopyGroup>& out) {
-  out.clear();
-  std::vector<std::pair<int, int>> runs;  // runs separated by short masked gaps merged
-  for (const auto& r : exact_runs) {
-    if (!runs.empty() && r.first - (runs.back().first + runs.back().second) <= COPY_MAX_GAP)
-      runs.back().second = r.first + r.second - runs.back().first;
-    else
-      runs.push_back(r);
-  }
-  size_t i = 0;
-  int cov_end = 0;  // end of the previous group's last row: groups never overlap
-  while (i < runs.size()) {
-    CopyGroup g{runs[i].first, runs[i].second, 0, 1};
-    long long exact = runs[i].second;
-    size_t j = i + 1;
-    if (j < runs.size()) {
-      const int stride = runs[j].first - runs[i].first;
-      int base = g.start, top = g.start + g.len;  // row k covers [base + k stride, top + k stride)
-      for (; j < runs.size(); ++j) {
-        const int k = (int)(j - i);
-        const int s = runs[j].first - k * stride, e = runs[j].first + runs[j].second - k * stride;
-        const int nb = std::min(base, s), nt = std::max(top, e);
-        const long long ex = exact + runs[j].second;
-        const long long cover = (long long)(nt - nb) * (k + 1);
-        const int next = j + 1 < runs.size() ? runs[j + 1].first : L;  // the last row stops before it
-        if (nb < cov_end || nt - nb > stride || nt + (long long)k * stride > next || 8 * (cover - ex) > ex + 64) break;
-        base = nb;
-        top = nt;
-        exact = ex;
-      }
-      if (j - i > 1) g = CopyGroup{base, top - base, stride, (int)(j - i)};
-      else j = i + 1;
-    }
-    out.push_back(g);
-    cov_end = g.start + (g.count - 1) * g.stride + g.len;
-    i = j;
-  }
+constexpr double DMA_CALL_BYTES = 275e3;  // link payload equivalent of one call's fixed cost
+int copy_call_rows(size_t row_bytes, int planes) {
+  return std::max(1, (int)std::lround(DMA_CALL_BYTES / ((double)row_bytes * std::max(planes, 1))));
 }
-// DMA calls for one plane: groups over token rows of `row` bytes between positional buffers
-void push_group_copies(std::vector<Copy2D>& v, char* dst, const char* src, size_t row,
-                       const std::vector<CopyGroup>& groups) {
+// shortest path over `runs`; returns calls x call_rows + rows copied beyond the runs
+long long copy_groups_dp(const std::vector<std::pair<int, int>>& runs, int L, int W, int call_rows,
+                         std::vector<CopyGroup>& out) {
+  out.clear();
+  const int n = (int)runs.size();
+  if (n == 0) return 0;
+  const long long INF = (long long)1 << 60;
+  std::vector<long long> best(n + 1, INF);
+  std::vector<CopyGroup> pick(n + 1);
+  std::vector<int> from(n + 1, 0);
+  best[0] = 0;
+  auto S = [&](int k) { return runs[k].first; };
+  auto E = [&](int k) { return runs[k].first + runs[k].second; };
+  for (int i = 0; i < n; ++i) {
+    if (best[i] >= INF) continue;
+    long long exact = 0;
+    for (int j = i; j < n; ++j) {  // contiguous span over runs i..j
+      exact += runs[j].second;
+      const long long c = best[i] + call_rows + (E(j) - S(i) - exact);
+      if (c < best[j + 1]) {
+        best[j + 1] = c;
+        pick[j + 1] = CopyGroup{S(i), E(j) - S(i), 0, 1};
+        from[j + 1] = i;
+      }
+    }
+    if (i + 1 >= n) continue;
+    const int cand[2] = {S(i + 1) - S(i), W};
+    for (int ci = 0; ci < 2; ++ci) {
+      const int stride = cand[ci];
+      if (stride <= 0 || (ci == 1 && stride == cand[0])) continue;
+      const int lo_lim = i > 0 ? E(i - 1) : 0;  // row 0 must not reach the previous run
+      int base = S(i), top = E(i);
+      exact = runs[i].second;
+      for (int j = i + 1; j < n; ++j) {
+        const int k = j - i;
+        base = std::min(base, S(j) - k * stride);
+        top = std::max(top, E(j) - k * stride);
+        if (top - base > stride || base < lo_lim) break;  // rows would overlap / reach run i-1
+        exact += runs[j].second;
+        const long long last_end = (long long)top + (long long)k * stride;
+        if (last_end > (j + 1 < n ? S(j + 1) : L)) continue;  // last row reaches the next run
+        const long long c = best[i] + call_rows + ((long long)(top - base) * (k + 1) - exact);
+        if (c < best[j + 1]) {
+          best[j + 1] = c;
+          pick[j + 1] = CopyGroup{base, top - base, stride, k + 1};
+          from[j + 1] = i;
+        }
+      }
+    }
+  }
+  for (int j = n; j > 0; j = from[j]) out.push_back(pick[j]);
+  std::reverse(out.begin(), out.end());
+  return best[n];
+}
+void make_copy_groups(const std::vector<std::pair<int, int>>& runs, int L, int W, int call_rows,
+                      std::vector<CopyGroup>& out) {
+  const long long c0 = copy_groups_dp(runs, L, W, call_rows, out);
+  // a noisy mask edge leaves many short runs that the strided candidates cannot follow: also
+  // plan over the runs with masked gaps < call_rows / 3 merged (copying such a gap is cheaper
+  // than a call) and keep the cheaper plan, both costed against the exact runs
+  std::vector<std::pair<int, int>> merged;
+  long long gap_rows = 0;
+  for (const auto& r : runs) {
+    const int gap = merged.empty() ? 0 : r.first - (merged.back().first + merged.back().second);
+    if (!merged.empty() && 3 * gap < call_rows) {
+      merged.back().second = r.first + r.second - merged.back().first;
+      gap_rows += gap;
+    } else {
+      merged.push_back(r);
+    }
+  }
+  if (merged.size() == runs.size()) return;
+  std::vector<CopyGroup> alt;
+  const long long c1 = copy_groups_dp(merged, L, W, call_rows, alt) + gap_rows;
+  if (c1 < c0) out.swap(alt);
+}
+// copy-engine calls for `planes` planes of token rows of `row` bytes between positional buffers
+void push_group_copies(std::vector<CopyOp>& v, char* dst, const char* src, size_t row,
+                       const std::vector<CopyGroup>& groups, int planes = 1, size_t src_plane = 0,
+                       size_t dst_plane = 0) {
   for (const CopyGroup& g : groups)
-    v.push_back(Copy2D{dst + (size_t)g.start * row, src + (size_t)g.start * row, (size_t)g.len * row,
-                       (size_t)g.count, (size_t)g.stride * row});
+    v.push_back(CopyOp{dst + (size_t)g.start * row, src + (size_t)g.start * row, (size_t)g.len * row,
+                       (size_t)g.count, (size_t)(g.count > 1 ? g.stride : g.len) * row, planes, src_plane,
+                       dst_plane});
+}
+cudaError_t issue_copy_op(const CopyOp& c, cudaStream_t st) {
+  if (c.planes == 2) {
+    // both planes in one 3-D copy when each plane stride is a whole number of row pitches
+    // (1-D spans: pitch = the plane stride itself)
+    const bool span = c.height == 1;
+    const size_t sp = span ? c.src_plane : c.pitch, dp = span ? c.dst_plane : c.pitch;
+    if (c.src_plane % sp == 0 && c.dst_plane % dp == 0) {
+      cudaMemcpy3DParms p{};
+      p.srcPtr = make_cudaPitchedPtr(const_cast<void*>(c.src), sp, c.width, c.src_plane / sp);
+      p.dstPtr = make_cudaPitchedPtr(c.dst, dp, c.width, c.dst_plane / dp);
+      p.extent = make_cudaExtent(c.width, c.height, 2);
+      p.kind = cudaMemcpyDefault;
+      return cudaMemcpy3DAsync(&p, st);
+    }
+  }
+  cudaError_t e = cudaSuccess;
+  for (int w = 0; w < c.planes && e == cudaSuccess; ++w) {
+    char* d = (char*)c.dst + w * c.dst_plane;
+    const char* s = (const char*)c.src + w * c.src_plane;
+    e = c.height == 1 ? cudaMemcpyAsync(d, s, c.width, cudaMemcpyDefault, st)
+                      : cudaMemcpy2DAsync(d, c.pitch, s, c.pitch, c.width, c.height, cudaMemcpyDefault, st);
+  }
+  return e;
 }
 }  // namespace
 
@@ -279,7 +352,7 @@ struct ig_ctx {
   struct Pref { const ig_cache* c = nullptr; int step = -1; };
   std::vector<Pref> pref;  // [max_batch * R]
   ig_mask* ones_mask = nullptr;
-  std::vector<Copy2D> b_copies;      // copy-lane scratch (copy_mode 1): one DMA call each
+  std::vector<CopyOp> b_copies;      // copy-lane scratch (copy_mode 1): one copy-engine call each
   // FP8 cache staging (cache_fp8): per (slot, ring buffer) e4m3 rows + scales landed by the DMA
   // lane before the dequantizing gather into the bf16 ring; per ring buffer for recording
   uint8_t* q8in = nullptr;  float* q8in_scl = nullptr;
@@ -864,8 +937,10 @@ extern "C" ig_status ig_profile_read(ig_ctx* ctx, ig_prof_entry out[IG_K_NCLASS]
   return IG_OK;
 }
 
-extern "C" ig_status ig_plan_copy_groups(const uint8_t* mask, int L, int* groups, int cap, int* n_groups) {
-  if (!mask || !n_groups || L <= 0 || cap < 0 || (cap > 0 && !groups)) return set_err(IG_EINVAL, "bad argument");
+extern "C" ig_status ig_plan_copy_groups(const uint8_t* mask, int L, int W, int row_bytes, int* groups, int cap,
+                                         int* n_groups) {
+  if (!mask || !n_groups || L <= 0 || W < 0 || row_bytes <= 0 || cap < 0 || (cap > 0 && !groups))
+    return set_err(IG_EINVAL, "bad argument");
   std::vector<std::pair<int, int>> runs;
   for (int i = 0; i < L;) {
     if (mask[i]) { ++i; continue; }
@@ -875,7 +950,7 @@ extern "C" ig_status ig_plan_copy_groups(const uint8_t* mask, int L, int* groups
     i = j;
   }
   std::vector<CopyGroup> g;
-  make_copy_groups(runs, L, g);
+  make_copy_groups(runs, L, W, copy_call_rows((size_t)row_bytes, 2), g);
   *n_groups = (int)g.size();
   if ((int)g.size() > cap) return set_err(IG_EINVAL, "%d groups exceed cap %d", (int)g.size(), cap);
   for (size_t k = 0; k < g.size(); ++k) {
@@ -926,7 +1001,7 @@ extern "C" ig_status ig_mask_build(ig_ctx* ctx, const uint8_t* mask, void* strea
     m->runs.push_back({i, j - i});
     i = j;
   }
-  make_copy_groups(m->runs, ctx->Limg, m->groups);
+  make_copy_groups(m->runs, ctx->Limg, ctx->d.grid_w, copy_call_rows((size_t)ctx->H * ctx->esz, 2), m->groups);
   if (e != cudaSuccess) {
     cudaFree(m->idx);
     if (m->bits_dev) cudaFree(m->bits_dev);
@@ -950,7 +1025,8 @@ extern "C" ig_status ig_mask_indices(const ig_mask* m, const int32_t** idx_m, co
 
 // host-bitmap mask build for a token grid of L tokens (also used by the whole-UNet runtime for
 // its per-level masks, ig_internal.h)
-ig_status ig_mask_build_host_L(int device, int L, const uint8_t* mask, void* stream, ig_mask** out, int* n_masked) {
+ig_status ig_mask_build_host_L(int device, int L, const uint8_t* mask, void* stream, ig_mask** out, int* n_masked,
+                               int W, int row_bytes) {
   if (!mask || !out || L <= 0) return set_err(IG_EINVAL, "NULL argument");
   *out = nullptr;
   CUDA_TRY(cudaSetDevice(device));
@@ -967,7 +1043,7 @@ ig_status ig_mask_build_host_L(int device, int L, const uint8_t* mask, void* str
     m->runs.push_back({i, j - i});
     i = j;
   }
-  make_copy_groups(m->runs, L, m->groups);
+  make_copy_groups(m->runs, L, W, copy_call_rows(row_bytes > 0 ? (size_t)row_bytes : 6144, 2), m->groups);
   // one stream-ordered allocation: idx_m | idx_u | n_m (int32), then the bitmap (u8)
   const size_t idx_bytes = ((size_t)(2 * L + 1) * sizeof(int32_t) + 15) & ~(size_t)15;
   void* base = nullptr;
@@ -995,7 +1071,8 @@ ig_status ig_mask_build_host_L(int device, int L, const uint8_t* mask, void* str
 extern "C" ig_status ig_mask_build_host(ig_ctx* ctx, const uint8_t* mask, void* stream, ig_mask** out,
                                         int* n_masked) {
   if (!ctx) return set_err(IG_EINVAL, "NULL argument");
-  return ig_mask_build_host_L(ctx->device, ctx->Limg, mask, stream, out, n_masked);
+  return ig_mask_build_host_L(ctx->device, ctx->Limg, mask, stream, out, n_masked, ctx->d.grid_w,
+                              (int)(ctx->H * ctx->esz));
 }
 
 extern "C" void ig_mask_free(ig_mask* m) {
@@ -1471,7 +1548,7 @@ static void issue_copy_now(ig_ctx* ctx, const std::vector<StepReq>& sr, const Kv
   const int n = (int)sr.size();
   const size_t row = (size_t)ctx->H * ctx->esz;
   const size_t txt_off = (size_t)ctx->Lt * row, vplane = (size_t)ctx->L * row;
-  std::vector<Copy2D>& cps = ctx->b_copies;
+  std::vector<CopyOp>& cps = ctx->b_copies;
   cps.clear();
   for (int q = 0; q < n; ++q) {
     if (!sr[q].use_cache) continue;
@@ -1489,7 +1566,7 @@ static void issue_copy_now(ig_ctx* ctx, const std::vector<StepReq>& sr, const Kv
         char* ss = (char*)ctx->q8in_scl + ((size_t)slot * ctx->R + buf) * 2 * spl + spl;
         const char* src = cache_plane(ctx, c, r->step, b - 1, 2);
         push_group_copies(cps, (char*)sd, src, (size_t)ctx->H, sr[q].m->groups);
-        cps.push_back(Copy2D{ss, cache_scales(ctx, c, r->step, b - 1, 2), spl, 1, spl});
+        cps.push_back(CopyOp{ss, cache_scales(ctx, c, r->step, b - 1, 2), spl, 1, spl, 1, 0, 0});
         cs.h2d_bytes += (long long)n_u * ctx->H + (long long)spl;
       } else {
         cs.d2d_bytes += (long long)n_u * (ctx->H + 4 * ctx->d.heads);
@@ -1525,7 +1602,7 @@ static void issue_copy_now(ig_ctx* ctx, const std::vector<StepReq>& sr, const Kv
         for (int w = 0; w < 2; ++w) {
           const char* src = cache_plane(ctx, c, r->step, b, w);
           push_group_copies(cps, (char*)(sd + w * pl), src, (size_t)ctx->H, sr[q].m->groups);
-          cps.push_back(Copy2D{ss + w * spl, cache_scales(ctx, c, r->step, b, w), spl, 1, spl});
+          cps.push_back(CopyOp{ss + w * spl, cache_scales(ctx, c, r->step, b, w), spl, 1, spl, 1, 0, 0});
         }
         by = 2LL * n_u * ctx->H + 2LL * ctx->Limg * ctx->d.heads * 4;
       }
@@ -1545,9 +1622,9 @@ static void issue_copy_now(ig_ctx* ctx, const std::vector<StepReq>& sr, const Kv
     } else if (host && ctx->o.copy_mode == 1) {  // DMA runs straight into the ring
       char* dst = (char*)ctx->kv_arena + ((size_t)slot * ctx->slot_stride + (size_t)buf * ctx->buf_elems) * ctx->esz;
       const bool dd = !plan.dsrc.empty() && plan.dsrc[q] >= 0;
-      for (int w = 0; w < 2; ++w)
-        push_group_copies(cps, dst + w * vplane + txt_off, cache_plane(ctx, c, r->step, b, w), row,
-                          dd ? plan.dgroups[q] : sr[q].m->groups);
+      const char* srcK = cache_plane(ctx, c, r->step, b, 0);
+      const size_t splane = (size_t)(cache_plane(ctx, c, r->step, b, 1) - srcK);  // V plane after K
+      push_group_copies(cps, dst + txt_off, srcK, row, dd ? plan.dgroups[q] : sr[q].m->groups, 2, splane, vplane);
       by = 2LL * (dd ? n_u - plan.dshared[q] : n_u) * row;
       if (dd) cs.d2d_bytes += 2LL * plan.dshared[q] * row;
     } else {
@@ -1556,11 +1633,7 @@ static void issue_copy_now(ig_ctx* ctx, const std::vector<StepReq>& sr, const Kv
     if (host) cs.h2d_bytes += by; else cs.d2d_bytes += by;
   }
   for (size_t i = 0; i < cps.size(); ++i) {  // one DMA call per group (copy engines)
-    const Copy2D& cp = cps[i];
-    const cudaError_t ce =
-        cp.height == 1 ? cudaMemcpyAsync(cp.dst, cp.src, cp.width, cudaMemcpyDefault, ctx->copy_st)
-                       : cudaMemcpy2DAsync(cp.dst, cp.pitch, cp.src, cp.pitch, cp.width, cp.height, cudaMemcpyDefault,
-                                           ctx->copy_st);
+    const cudaError_t ce = issue_copy_op(cps[i], ctx->copy_st);
     if (ce != cudaSuccess && ctx->copy_err == cudaSuccess) {
       ctx->copy_err = ce;
       ctx->copy_err_idx = i;
@@ -1777,6 +1850,7 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
       const ig_cache* c = sr[q].use_cache ? sr[q].r->cache : nullptr;
       return c && c->tier == IG_CACHE_HOST && !c->fp8 && ctx->o.copy_mode == 1;
     };
+    const size_t row_b = (size_t)H * es;
     plan.dsrc.assign(na, -1);
     plan.druns.assign(na, {});
     plan.dgroups.assign(na, {});
@@ -1797,7 +1871,7 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
             runs.push_back({i, j - i});
             i = j;
           }
-          make_copy_groups(runs, ctx->Limg, plan.dgroups[q]);
+          make_copy_groups(runs, ctx->Limg, ctx->d.grid_w, copy_call_rows(row_b, 2), plan.dgroups[q]);
           plan.dsrc[q] = q0;
           plan.dshared[q] = shared;
           DedupeEnt& e = plan.dd.e[plan.dd.n++];

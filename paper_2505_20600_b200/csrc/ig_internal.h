@@ -2,7 +2,9 @@
 #pragma once
 #include "../../include/ig.h"
 
-// a1 on a host bitmap for a grid of L tokens (ig_mask_build_host without a model context)
-ig_status ig_mask_build_host_L(int device, int L, const uint8_t* mask, void* stream, ig_mask** out, int* n_masked);
+// a1 on a host bitmap for a grid of L tokens (ig_mask_build_host without a model context); W =
+// grid width in tokens and row_bytes = one K/V row, for the copy lane's DMA grouping (0: unknown)
+ig_status ig_mask_build_host_L(int device, int L, const uint8_t* mask, void* stream, ig_mask** out, int* n_masked,
+                               int W = 0, int row_bytes = 0);
 // set the thread-local message returned by ig_last_error() (other translation units' errors)
 ig_status ig_internal_err(ig_status s, const char* msg);

@@ -408,7 +408,8 @@ extern "C" ig_status ig_unet_mask_build(ig_unet* u, const uint8_t* mask, void* s
   ig_unet_mask* m = new ig_unet_mask();
   for (int l = 0; l < 3; ++l) {
     m->P[l] = u->P[l];
-    ig_status s = ig_mask_build_host_L(u->device, u->P[l], lv[l].data(), stream, &m->m[l], &m->n_m[l]);
+    ig_status s = ig_mask_build_host_L(u->device, u->P[l], lv[l].data(), stream, &m->m[l], &m->n_m[l], u->G[l],
+                                       u->d.ch[l] * 2);
     if (s != IG_OK) {
       const std::string msg = ig_last_error();
       ig_unet_mask_free(m);

@@ -123,7 +123,7 @@ def lib():
         L.ig_last_error.restype = ctypes.c_char_p
         L.ig_last_plan.restype = ctypes.c_int
         L.ig_last_stats.argtypes = [vp, P(ig_stats)]
-        L.ig_plan_copy_groups.argtypes = [vp, i, P(ctypes.c_int), i, P(i)]
+        L.ig_plan_copy_groups.argtypes = [vp, i, i, i, P(ctypes.c_int), i, P(i)]
         L.ig_op_gemm.argtypes = [i, vp, ll, vp, ll, vp, vp, ll, i, i, i, i, i, vp]
         L.ig_op_attention.argtypes = [i, vp, ll, vp, ll, vp, P(ctypes.c_int32), i, i, i, i, vp]
         L.ig_copy.argtypes = [vp, vp, ctypes.c_size_t, vp]
@@ -310,14 +310,14 @@ def ig_last_error() -> str:
     return lib().ig_last_error().decode()
 
 
-def ig_plan_copy_groups(mask_u8) -> list:
-    """Host-only: the copy lane's strided DMA groups [(start, len, stride, count)] for a mask."""
+def ig_plan_copy_groups(mask_u8, W: int = 0, row_bytes: int = 6144) -> list:
+    """Host-only: the copy lane's DMA groups [(start, len, stride, count)] for a mask."""
     import numpy as _np
     m = _np.ascontiguousarray(mask_u8, dtype=_np.uint8).reshape(-1)
     cap = m.size + 1
     buf = (ctypes.c_int * (4 * cap))()
     n = ctypes.c_int()
-    _check(lib().ig_plan_copy_groups(m.ctypes.data, int(m.size), buf, cap, ctypes.byref(n)))
+    _check(lib().ig_plan_copy_groups(m.ctypes.data, int(m.size), int(W), int(row_bytes), buf, cap, ctypes.byref(n)))
     return [tuple(buf[4 * k:4 * k + 4]) for k in range(n.value)]
 
 

@@ -59,6 +59,36 @@ for wt, ht in ((30, 30), (50, 40), (10, 64), (4, 64)):
             return w * ht
         return c
     run(f"2d_{wt}tok_x{ht}", [mk2(i) for i in range(n)])
+# 3-D: the K and V planes of one group in ONE call (depth 2), spans and strided rows
+class PP(ctypes.Structure):
+    _fields_ = [("ptr", vp), ("pitch", sz), ("xsize", sz), ("ysize", sz)]
+class Pos(ctypes.Structure):
+    _fields_ = [("x", sz), ("y", sz), ("z", sz)]
+class Ext(ctypes.Structure):
+    _fields_ = [("width", sz), ("height", sz), ("depth", sz)]
+class P3(ctypes.Structure):
+    _fields_ = [("srcArray", vp), ("srcPos", Pos), ("srcPtr", PP), ("dstArray", vp), ("dstPos", Pos),
+                ("dstPtr", PP), ("extent", Ext), ("kind", ctypes.c_int)]
+rt.cudaMemcpy3DAsync.argtypes = [ctypes.POINTER(P3), vp]
+splane, dplane = 4096 * 6144, 4608 * 6144
+for wt, ht in ((1, 1), (8, 1), (64, 1), (30, 30), (4, 64)):
+    w = wt * 6144
+    span = ht == 1
+    n = min(300, NB // (2 * dplane + pitch * ht) // 1)
+    def mk3(i, w=w, ht=ht, span=span):
+        def c():
+            p3 = P3()
+            off = (i % 8) * pitch * 2
+            sp_, dp_ = (splane, dplane) if span else (pitch, pitch)
+            p3.srcPtr = PP(hp + off, sp_, w, splane // sp_)
+            p3.dstPtr = PP(dp + off, dp_, w, dplane // dp_)
+            p3.extent = Ext(w, ht, 2)
+            p3.kind = 4
+            e = rt.cudaMemcpy3DAsync(ctypes.byref(p3), sp)
+            assert e == 0, e
+            return 2 * w * ht
+        return c
+    run(f"3d_kv_{wt}tok_x{ht}", [mk3(i) for i in range(n)])
 # one big copy: the link's ceiling
 run("1d_512MB", [lambda: (rt.cudaMemcpyAsync(dp, hp, 512 << 20, 4, sp), 512 << 20)[1]])
 print(json.dumps(out))
