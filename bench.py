@@ -284,7 +284,24 @@ def request_step_flops(d, n_m):
     return d.n_blocks * block_flops(d, n_m)
 
 
-def choose_kv_blocks(d, a_c, b_c, a_l, max_batch, mean_m):
+def dma_inflation(ig, d, copy_mode, n_sample=64):
+    """Link-time rows per unmasked row of the host-tier DMA plan (copy_mode 1) over a sample of
+    the workload's masks: (rows the copy-engine calls move + calls x the per-call cost in rows)
+    / unmasked rows (ig.h ig_plan_copy_groups; ~5 us per call, tools/dma_probe.py)."""
+    if copy_mode != 1:
+        return 1.0
+    row = d.hidden * 2
+    cr = max(1, round(275e3 / (2 * row)))
+    cost = exact = 0
+    for rid in range(n_sample):
+        m = np.asarray(make_mask(d, rid), np.uint8).reshape(-1)
+        g = ig.ig_plan_copy_groups(m, d.grid_w, row)
+        cost += sum(ln * c for _, ln, _, c in g) + cr * len(g)
+        exact += int((m == 0).sum())
+    return cost / max(exact, 1)
+
+
+def choose_kv_blocks(d, a_c, b_c, a_l, max_batch, mean_m, inflation=1.0):
     """Hybrid split: s blocks move K/V (two planes), the other N - s (interleaved) move Y (one
     plane) and recompute the unmasked rows' K/V (4 n_u H^2 flops, x1.1 for the LN-modulation
     of those rows; measured: 57 Y blocks add ~45 ms to a ~215 ms step = 1.08x the model).  Under the fitted linear models pick the s that balances
@@ -295,7 +312,7 @@ def choose_kv_blocks(d, a_c, b_c, a_l, max_batch, mean_m):
     n_u = max_batch * (d.L_img - n_m)
     cw = a_c * max_batch * block_flops(d, n_m) + b_c
     cw_y = cw + 1.1 * a_c * 4.0 * n_u * H * H
-    lt, lt_y = a_l * 2 * n_u * H * 2, a_l * n_u * H * 2
+    lt, lt_y = inflation * a_l * 2 * n_u * H * 2, inflation * a_l * n_u * H * 2
     best = min(range(N + 1), key=lambda s_: (max(s_ * cw + (N - s_) * cw_y, s_ * lt + max(0, N - s_ - (s_ == 0)) * lt_y), -s_))
     return best
 
@@ -571,7 +588,8 @@ def main():
     # Algorithm-1/2 latency models fitted on this GPU; the hybrid split point.  Under
     # torchrun rank 0's fit is broadcast so that every rank uses the same cache layout.
     fit = list(fit_latency(ig, ctx_kv, d, dev, stream, link_peak))
-    kv_auto = choose_kv_blocks(d, fit[0], fit[1], fit[2], args.max_batch, 0.5 * (args.mask_lo + args.mask_hi))
+    infl = dma_inflation(ig, d, args.copy_mode if tier == "host" else 0)
+    kv_auto = choose_kv_blocks(d, fit[0], fit[1], fit[2], args.max_batch, 0.5 * (args.mask_lo + args.mask_hi), infl)
     if world > 1:
         t = torch.tensor(fit + [float(kv_auto)], dtype=torch.float64, device=dev if not share else "cpu")
         torch.distributed.broadcast(t, 0)

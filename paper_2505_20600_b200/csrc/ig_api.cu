@@ -196,8 +196,11 @@ long long copy_groups_dp(const std::vector<std::pair<int, int>>& runs, int L, in
   std::reverse(out.begin(), out.end());
   return best[n];
 }
-void make_copy_groups(const std::vector<std::pair<int, int>>& runs, int L, int W, int call_rows,
-                      std::vector<CopyGroup>& out) {
+// returns the plan's link-time rows: rows moved + calls x call_rows
+long long make_copy_groups(const std::vector<std::pair<int, int>>& runs, int L, int W, int call_rows,
+                           std::vector<CopyGroup>& out) {
+  long long exact = 0;
+  for (const auto& r : runs) exact += r.second;
   const long long c0 = copy_groups_dp(runs, L, W, call_rows, out);
   // a noisy mask edge leaves many short runs that the strided candidates cannot follow: also
   // plan over the runs with masked gaps < call_rows / 3 merged (copying such a gap is cheaper
@@ -213,10 +216,11 @@ void make_copy_groups(const std::vector<std::pair<int, int>>& runs, int L, int W
       merged.push_back(r);
     }
   }
-  if (merged.size() == runs.size()) return;
+  if (merged.size() == runs.size()) return exact + c0;
   std::vector<CopyGroup> alt;
   const long long c1 = copy_groups_dp(merged, L, W, call_rows, alt) + gap_rows;
   if (c1 < c0) out.swap(alt);
+  return exact + std::min(c0, c1);
 }
 // copy-engine calls for `planes` planes of token rows of `row` bytes between positional buffers
 void push_group_copies(std::vector<CopyOp>& v, char* dst, const char* src, size_t row,
@@ -257,6 +261,7 @@ struct ig_mask {
   int L_img = 0, n_m = 0;
   std::vector<std::pair<int, int>> runs;  // host: maximal runs (start, len) of unmasked tokens
   std::vector<CopyGroup> groups;          // host: strided DMA groups covering `runs` (copy_mode 1)
+  long long dma_rows = 0;                 // rows the groups move + calls x call_rows (link-time rows)
   std::vector<uint8_t> bits;              // host: 1 = masked (load deduplication)
   uint8_t* bits_dev = nullptr;            // device copy of bits
   int32_t* idx = nullptr;  // device: idx_m at [0, L_img), idx_u at [L_img, 2 L_img), n_m at [2 L_img]
@@ -1001,7 +1006,8 @@ extern "C" ig_status ig_mask_build(ig_ctx* ctx, const uint8_t* mask, void* strea
     m->runs.push_back({i, j - i});
     i = j;
   }
-  make_copy_groups(m->runs, ctx->Limg, ctx->d.grid_w, copy_call_rows((size_t)ctx->H * ctx->esz, 2), m->groups);
+  m->dma_rows = make_copy_groups(m->runs, ctx->Limg, ctx->d.grid_w, copy_call_rows((size_t)ctx->H * ctx->esz, 2),
+                                 m->groups);
   if (e != cudaSuccess) {
     cudaFree(m->idx);
     if (m->bits_dev) cudaFree(m->bits_dev);
@@ -1043,7 +1049,7 @@ ig_status ig_mask_build_host_L(int device, int L, const uint8_t* mask, void* str
     m->runs.push_back({i, j - i});
     i = j;
   }
-  make_copy_groups(m->runs, L, W, copy_call_rows(row_bytes > 0 ? (size_t)row_bytes : 6144, 2), m->groups);
+  m->dma_rows = make_copy_groups(m->runs, L, W, copy_call_rows(row_bytes > 0 ? (size_t)row_bytes : 6144, 2), m->groups);
   // one stream-ordered allocation: idx_m | idx_u | n_m (int32), then the bitmap (u8)
   const size_t idx_bytes = ((size_t)(2 * L + 1) * sizeof(int32_t) + 15) & ~(size_t)15;
   void* base = nullptr;
@@ -1720,7 +1726,10 @@ static int plan_prefix(ig_ctx* ctx, const std::vector<StepReq>& sr, const std::v
     if (!s.use_cache) continue;
     const ig_cache* c = s.r->cache;
     const long long n_u = ctx->Limg - s.m->n_m;
-    const long long n_load = n_u - dshared[&s - &sr[0]];  // deduplicated rows cross the link once
+    long long n_load = n_u - dshared[&s - &sr[0]];  // deduplicated rows cross the link once
+    // host-tier DMA groups: the link time of the rows they move plus the calls' fixed cost
+    if (c->tier == IG_CACHE_HOST && ctx->o.copy_mode == 1 && n_u > 0 && s.m->dma_rows > 0)
+      n_load = (long long)((double)n_load * (double)s.m->dma_rows / (double)n_u);
     for (int b = 0; b < N; ++b) {
       if (y_block(c, b)) {  // one plane; the K/V projection of the unmasked rows is recomputed
         if (b > 0) bytes[b] += c->fp8 ? n_u * (ctx->H + 4LL * ctx->d.heads) : n_load * ctx->H * (long long)ctx->esz;
