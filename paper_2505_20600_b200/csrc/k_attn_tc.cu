@@ -64,6 +64,9 @@ constexpr float RESCALE_THRESHOLD = 8.0f;       // log2 units
 #ifndef ATTN_REGS_SOFTMAX
 #define ATTN_REGS_SOFTMAX 224
 #endif
+#ifndef ATTN_SPLIT_S
+#define ATTN_SPLIT_S 1  // S_t(j+1) in two N = 64 halves, the first issued as soon as S_t(j) is loaded
+#endif
 #ifndef ATTN_ST_CHUNKS
 #define ATTN_ST_CHUNKS 1  // P stored to TMEM in 1, 2 or 4 pieces as the exps complete
 #endif
@@ -71,7 +74,7 @@ constexpr float RESCALE_THRESHOLD = 8.0f;       // log2 units
 struct Bars {
   uint64_t q_full;
   uint64_t k_full[KSTAGES], k_empty[KSTAGES], v_full[VSTAGES], v_empty[VSTAGES];
-  uint64_t s_full[2], p_full[2], o_done[2];
+  uint64_t s_full[2], p_full[2], o_done[2], s_used[2];
   uint32_t tmem;
 };
 
@@ -174,6 +177,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       tc::mbar_init(&bar->s_full[t], 1);
       tc::mbar_init(&bar->p_full[t], 4);
       tc::mbar_init(&bar->o_done[t], 1);
+      tc::mbar_init(&bar->s_used[t], 4);
     }
     tc::fence_barrier_init();
   }
@@ -235,6 +239,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         }
         tc::mma_commit(&bar->s_full[t]);
       };
+      // P_t(j) lives in the upper 64 columns of the S_t region (bf16 pairs), so the lower half
+      // of S_t(j+1) (keys 0..63 of the next tile) can be computed while softmax t still works on
+      // S_t(j) (as soon as it has loaded it); only the upper half waits behind PV_t(j)
+      constexpr uint32_t POFF = ATTN_SPLIT_S ? 64 : 0;
       auto issue_PV = [&](int t, int j) {
         TRACE(0, t, j);  // MMA warp starts waiting for P_t(j)
         tc::mbar_wait(&bar->p_full[t], j & 1);
@@ -243,9 +251,22 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         const uint32_t v_addr = tc::smem_u32(sV + (j % VSTAGES) * KV_BYTES);
 #pragma unroll
         for (int k = 0; k < BKV / 16; ++k)
-          tc::mma_bf16_ts(tmem + t * TS + 128, tmem + t * TS + k * 8,
+          tc::mma_bf16_ts(tmem + t * TS + 128, tmem + t * TS + POFF + k * 8,
                           tc::sdesc_sw128(v_addr + k * 2048, CHUNK, 1024), idO, (j | k) != 0);
       };
+#if ATTN_SPLIT_S
+      constexpr uint32_t idS64 = tc::idesc_bf16(BQ, 64, 0);
+      auto issue_S_half = [&](int t, int j, int half) {  // keys [64 half, 64 half + 64) of tile j
+        const uint32_t q_addr = tc::smem_u32(sQ + t * Q_BYTES);
+        const uint32_t k_addr = tc::smem_u32(sK + (j % KSTAGES) * KV_BYTES) + half * 8192;
+#pragma unroll
+        for (int k = 0; k < D / 16; ++k) {
+          const uint32_t off = (k >> 2) * CHUNK + (k & 3) * 32;
+          tc::mma_bf16_ss(tmem + t * TS + half * 64, tc::sdesc_sw128(q_addr + off, 16, 1024),
+                          tc::sdesc_sw128(k_addr + off, 16, 1024), idS64, k != 0);
+        }
+      };
+#endif
       tc::mbar_wait(&bar->k_full[0], 0);
       tc::tc_fence_after();
       for (int t = 0; t < ntiles; ++t) issue_S(t, 0);
@@ -255,6 +276,21 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         tc::mbar_wait(&bar->v_full[j % VSTAGES], (j / VSTAGES) & 1);
         tc::tc_fence_after();
         for (int t = 0; t < ntiles; ++t) {
+#if ATTN_SPLIT_S
+          if (more) {
+            if (t == 0) tc::mbar_wait(&bar->k_full[(j + 1) % KSTAGES], ((j + 1) / KSTAGES) & 1);
+            tc::mbar_wait(&bar->s_used[t], j & 1);  // softmax t has S_t(j) in registers
+            tc::tc_fence_after();
+            issue_S_half(t, j + 1, 0);
+          }
+          issue_PV(t, j);
+          if (more) {
+            issue_S_half(t, j + 1, 1);
+            tc::mma_commit(&bar->s_full[t]);
+          } else {
+            tc::mma_commit(&bar->o_done[t]);
+          }
+#else
           issue_PV(t, j);
           if (more) {
             if (t == 0) {
@@ -265,6 +301,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           } else {
             tc::mma_commit(&bar->o_done[t]);
           }
+#endif
         }
         tc::mma_commit(&bar->v_empty[j % VSTAGES]);
         if (more) tc::mma_commit(&bar->k_empty[(j + 1) % KSTAGES]);
@@ -289,6 +326,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         tc::tmem_ld32(tS + 64, *reinterpret_cast<uint32_t(*)[32]>(&r[64]));
         tc::tmem_ld32(tS + 96, *reinterpret_cast<uint32_t(*)[32]>(&r[96]));
         tc::tmem_ld_wait();
+#if ATTN_SPLIT_S
+        tc::tc_fence_before();  // S_t(j) is in registers: the MMA warp may overwrite its lower half
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&bar->s_used[t]);
+#endif
         const int valid = a.L - j * BKV;  // keys >= L are masked (ragged last tile only)
         // row max as 8 independent partial chains (latency, one warp per SMSP in this phase)
         float pm[8];
@@ -335,13 +377,14 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             acc[i & 3] = __fadd2_rn(acc[i & 3], pp);
             r[i] = pack_bf16(pp.x, pp.y);
           }
+          const uint32_t tP = tS + (ATTN_SPLIT_S ? 64 : 0);  // P_t(j): bf16 pairs, 64 columns
           if (PCH == 64) {
-            tc::tmem_st32(tS + 0, &r[0]);
-            tc::tmem_st32(tS + 32, &r[32]);
+            tc::tmem_st32(tP + 0, &r[0]);
+            tc::tmem_st32(tP + 32, &r[32]);
           } else if (PCH == 32) {
-            tc::tmem_st32(tS + c * 32, &r[c * 32]);
+            tc::tmem_st32(tP + c * 32, &r[c * 32]);
           } else {
-            tc::tmem_st16(tS + c * 16, *reinterpret_cast<const uint32_t(*)[16]>(&r[c * 16]));
+            tc::tmem_st16(tP + c * 16, *reinterpret_cast<const uint32_t(*)[16]>(&r[c * 16]));
           }
         }
         const float2 s01 = __fadd2_rn(acc[0], acc[1]), s23 = __fadd2_rn(acc[2], acc[3]);

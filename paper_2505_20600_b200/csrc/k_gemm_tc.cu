@@ -485,21 +485,25 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 // traffic versus the 1-CTA 128 x 256 tile.  Only the leader CTA issues MMAs; commits are
 // multicast to both CTAs; each CTA's epilogue warps drain their own TMEM (rows 128r..128r+127)
 // and release the accumulator to the leader with a cluster-scope mbarrier arrive.
+// BN = 256, or 160 for N = 160 k (320 / 640 / 1280-wide UNet projections and convolutions):
+// narrower tiles cut the N padding and the last-wave quantisation when a 256-wide grid has only
+// 2-3 waves (launch_gemm_tc picks the tile by the wave count; per-element math unchanged).
+template <int BN>
 struct Cfg2 {
-  static constexpr int STAGES = 6;
+  static constexpr int STAGES = BN == 256 ? 6 : 8;
   static constexpr int A_BYTES = 128 * BK * 2;
-  static constexpr int B_BYTES = 128 * BK * 2;
+  static constexpr int B_BYTES = (BN / 2) * BK * 2;  // this CTA's half of the B tile
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int TMEM_COLS = 512;
   static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256 + 2 * 256 * 2 /*bias slices*/;
 };
 
-template <bool CONV = false>
+template <bool CONV = false, int BN = 256>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     const GemmArgs g, int num_m, int num_n, int G) {
-  using C = Cfg2;
-  constexpr int BN = 256;
+  static_assert(BN % 32 == 0 && (BN / 2) % 8 == 0 && BN <= 256, "2-CTA tile width");
+  using C = Cfg2<BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
@@ -545,7 +549,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       for (int t = cluster; t < num_tiles; t += nclusters) {
         int mb, nb;
         tile_coords(t, num_m, num_n, G, mb, nb);
-        const int m0 = mb * 256 + rank * 128, n0 = nb * BN + rank * 128;
+        const int m0 = mb * 256 + rank * 128, n0 = nb * BN + rank * (BN / 2);
         int cbox = 1, cbase[16];  // implicit conv: runs of this CTA's 128 output pixels (see gemm_tc_kernel)
         if constexpr (CONV) {
           const int W = g.conv_W, H = g.conv_H;
@@ -630,7 +634,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       if (row < g.M && g.ri && (g.epi == EPI_GATED_RES || g.epi == EPI_POS || g.epi == EPI_QKV))
         info = g.ri[g.ri_off + row];
       const uint32_t tbase = tmem_base + ((uint32_t)(quad * 32) << 16) + acc * BN;
-      if (g.epi == EPI_QKV) {
+      if (BN == 256 && g.epi == EPI_QKV) {
         if (g.qkv.head_dim == 128) {
 #pragma unroll 1
           for (int c = 0; c < BN; c += 128) {
@@ -650,7 +654,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
             if (row < g.M && n0 + c < g.N) epilogue_qkv_head<64>(g, row, n0 + c, v, info, BIAS_AT(c));
           }
         }
-      } else if (g.epi == EPI_GEGLU) {
+      } else if (BN == 256 && g.epi == EPI_GEGLU) {
 #pragma unroll 1
         for (int c = 0; c < 128; c += 32) {
           uint32_t ra[32], rg[32];
@@ -702,8 +706,10 @@ void init_driver() {
     cudaFuncSetAttribute(gemm_tc_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<128>::SMEM);
     cudaFuncSetAttribute(gemm_tc_kernel<256, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<256>::SMEM);
     cudaFuncSetAttribute(gemm_tc_kernel<128, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<128>::SMEM);
-    cudaFuncSetAttribute(gemm_tc2_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg2::SMEM);
-    cudaFuncSetAttribute(gemm_tc2_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg2::SMEM);
+    cudaFuncSetAttribute(gemm_tc2_kernel<false, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg2<256>::SMEM);
+    cudaFuncSetAttribute(gemm_tc2_kernel<true, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg2<256>::SMEM);
+    cudaFuncSetAttribute(gemm_tc2_kernel<false, 160>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg2<160>::SMEM);
+    cudaFuncSetAttribute(gemm_tc2_kernel<true, 160>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg2<160>::SMEM);
     g_two_cta = getenv("IG_GEMM_1CTA") == nullptr;
   });
 }
@@ -758,6 +764,21 @@ int raster_group(int num_m, int rows, int K) {
   return (int)G;
 }
 
+// 2-CTA tile width: 160 when it needs fewer (waves x width) tensor cycles than 256 — a 256-wide
+// grid of only a few waves loses its partial last wave, and N = 320 / 640 pads a 256 tile by a
+// third (a 10% margin keeps 256's lower per-flop B traffic and epilogue overhead otherwise).
+// Tile shape only: every output is still one full-K accumulation in the same K order.
+int tile2_width(long long M, long long N, bool narrow_ok) {
+  static const bool no160 = getenv("IG_GEMM_NO_BN160") != nullptr;  // A/B switch
+  if (!narrow_ok || no160) return 256;
+  const long long num_m = (M + 255) / 256, slots = g_num_sms / 2;
+  auto cost = [&](long long bn) {
+    const long long tiles = num_m * ((N + bn - 1) / bn);
+    return ((tiles + slots - 1) / slots) * bn;
+  };
+  return 10 * cost(160) < 9 * cost(256) ? 160 : 256;
+}
+
 bool gemm_tc_supported(const GemmArgs& g) {
   auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
   if (!al16(g.A) || !al16(g.B) || (g.lda & 7) || (g.ldb & 7) || (g.K & 7)) return false;
@@ -789,24 +810,27 @@ void launch_gemm_tc(const GemmArgs& g, cudaStream_t st) {
   static const bool no_small = getenv("IG_GEMM_NO_SMALL") != nullptr;  // A/B switch
   const long long tiles2 = (long long)((g.M + 255) / 256) * ((g.N + 255) / 256);
   if (!no_small && wide && g.epi != EPI_GEGLU && tiles2 * 4 < g_num_sms) wide = false;
-  if (wide && g_two_cta && g.M > 128) {  // 2-CTA 256 x 256 tiles
+  if (wide && g_two_cta && g.M > 128) {  // 2-CTA 256 x BN tiles
+    const int BN2 = tile2_width(g.M, g.N, g.epi != EPI_QKV && g.epi != EPI_GEGLU);
     CUtensorMap ta, tb;
     make_tmap(&ta, g.A, g.M, g.K, g.lda, 128);
-    make_tmap(&tb, g.B, g.N, g.K, g.ldb, 128);
-    const int num_m = (g.M + 255) / 256, num_n = (g.N + 255) / 256;
+    make_tmap(&tb, g.B, g.N, g.K, g.ldb, BN2 / 2);
+    const int num_m = (g.M + 255) / 256, num_n = (g.N + BN2 - 1) / BN2;
     const int tiles = num_m * num_n;
     const int clusters = tiles < g_num_sms / 2 ? tiles : g_num_sms / 2;
     const int G2 = raster_group(num_m, 256, g.K);
-    if (g.pdl) {
-      cudaLaunchConfig_t cfg{};
-      cfg.gridDim = dim3(2 * clusters); cfg.blockDim = dim3(NUM_THREADS); cfg.dynamicSmemBytes = Cfg2::SMEM; cfg.stream = st;
-      cudaLaunchAttribute at[1];
-      at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-      at[0].val.programmaticStreamSerializationAllowed = 1;
-      cfg.attrs = at; cfg.numAttrs = 1;
-      cudaLaunchKernelEx(&cfg, gemm_tc2_kernel<false>, ta, tb, g, num_m, num_n, G2);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(2 * clusters); cfg.blockDim = dim3(NUM_THREADS); cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at; cfg.numAttrs = g.pdl ? 1 : 0;
+    if (BN2 == 160) {
+      cfg.dynamicSmemBytes = Cfg2<160>::SMEM;
+      cudaLaunchKernelEx(&cfg, gemm_tc2_kernel<false, 160>, ta, tb, g, num_m, num_n, G2);
     } else {
-      gemm_tc2_kernel<false><<<2 * clusters, NUM_THREADS, Cfg2::SMEM, st>>>(ta, tb, g, num_m, num_n, G2);
+      cfg.dynamicSmemBytes = Cfg2<256>::SMEM;
+      cudaLaunchKernelEx(&cfg, gemm_tc2_kernel<false, 256>, ta, tb, g, num_m, num_n, G2);
     }
     return;
   }
@@ -850,14 +874,19 @@ void launch_conv3x3_tc(const GemmArgs& g, cudaStream_t st) {
   // C_out a multiple of 256 (1280): 2-CTA 256 x 256 tiles (half the B operand per SM), like the
   // projections; else 128 x 128 one-CTA tiles (C_out 320 / 640: no half-empty 256-column tile)
   static const bool conv_1cta = getenv("IG_CONV_1CTA") != nullptr;  // A/B switch
-  if (!conv_1cta && g_two_cta && g.N % 256 == 0 && g.M > 128) {
+  if (!conv_1cta && g_two_cta && (g.N % 256 == 0 || g.N % 160 == 0) && g.M > 128) {
+    const int BN2 = tile2_width(g.M, g.N, true);
     CUtensorMap tb2;
-    make_tmap(&tb2, g.B, g.N, g.K, g.ldb, 128);
-    const int num_m = (g.M + 255) / 256, num_n = g.N / 256;
+    make_tmap(&tb2, g.B, g.N, g.K, g.ldb, BN2 / 2);
+    const int num_m = (g.M + 255) / 256, num_n = (g.N + BN2 - 1) / BN2;
     const int tiles = num_m * num_n;
     const int clusters = tiles < g_num_sms / 2 ? tiles : g_num_sms / 2;
-    gemm_tc2_kernel<true><<<2 * clusters, NUM_THREADS, Cfg2::SMEM, st>>>(ta, tb2, g, num_m, num_n,
-                                                                         raster_group(num_m, 256, g.K));
+    if (BN2 == 160)
+      gemm_tc2_kernel<true, 160><<<2 * clusters, NUM_THREADS, Cfg2<160>::SMEM, st>>>(ta, tb2, g, num_m, num_n,
+                                                                                  raster_group(num_m, 256, g.K));
+    else
+      gemm_tc2_kernel<true, 256><<<2 * clusters, NUM_THREADS, Cfg2<256>::SMEM, st>>>(ta, tb2, g, num_m, num_n,
+                                                                                  raster_group(num_m, 256, g.K));
     return;
   }
   const bool wide = g.N >= 256 && g.N % 256 == 0;

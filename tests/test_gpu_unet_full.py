@@ -140,10 +140,12 @@ def test_same_input_cache_is_bitwise_dense_and_empty_mask_untouched(unet):
 
 @pytest.mark.parametrize("n,H,W,cin,cout", [(2, 32, 32, 128, 256), (1, 64, 64, 64, 320), (1, 128, 128, 64, 128),
                                             (3, 16, 8, 64, 64), (2, 8, 8, 64, 128), (1, 32, 32, 1280, 1280),
-                                            (1, 4, 4, 64, 64)])
+                                            (1, 4, 4, 64, 64), (4, 32, 32, 1280, 1280), (2, 64, 64, 640, 640),
+                                            (2, 128, 128, 320, 320)])
 def test_conv3x3_vs_torch(n, H, W, cin, cout):
-    """ig_op_conv3x3 (implicit-GEMM tcgen05 conv: 1-CTA and 2-CTA tiles, every run width; im2col
-    fallback for (H*W) % 128 != 0) against torch conv2d in fp32 on the same bf16 inputs."""
+    """ig_op_conv3x3 (implicit-GEMM tcgen05 conv: 1-CTA, 2-CTA 256x256 and 256x160 tiles, every run
+    width; im2col fallback for (H*W) % 128 != 0) against torch conv2d in fp32 on the same bf16
+    inputs."""
     if not torch.cuda.is_available():
         pytest.skip("no GPU")
     torch.backends.cudnn.allow_tf32 = False  # a true fp32 reference

@@ -64,6 +64,8 @@ def main():
     ap.add_argument("--tier", default="device", choices=["device", "host"])
     ap.add_argument("--ms", default="0.01,0.05,0.1,0.2,0.3,0.5,0.8,1.0")
     ap.add_argument("--out", default=None)
+    ap.add_argument("--profile", action="store_true",
+                    help="bracket the timed steps with cudaProfilerStart/Stop (ncu --profile-from-start off)")
     args = ap.parse_args()
     u = synth.UNET_FULL[args.model]
     dev = torch.device("cuda", 0)
@@ -103,11 +105,15 @@ def main():
             ig.ig_unet_step(h, reqs(t), stream.cuda_stream)
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+        if args.profile:
+            torch.cuda.profiler.start()
         e0.record(stream)
         for t in range(args.steps):
             ig.ig_unet_step(h, reqs(t), stream.cuda_stream)
         e1.record(stream)
         e1.synchronize()
+        if args.profile:
+            torch.cuda.profiler.stop()
         ms = e0.elapsed_time(e1) / args.steps
         st = ig.ig_unet_last_stats(h)
         fl = sum(flops(u, mk) for mk in masks)
