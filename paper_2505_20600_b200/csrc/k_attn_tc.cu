@@ -51,7 +51,12 @@ constexpr float RESCALE_THRESHOLD = 8.0f;       // log2 units
 // (ncu A/B, batch-8 shape: 0.939 vs 0.954 ms; 8 or 16 pairs in 64 are slower)
 #ifndef POLY_AT
 #define POLY_AT(i) (((i) & 15) == 15)
-#endif  // pairs per key tile on ex2_poly2 (measured: MUFU is not the limiter; 0 is fastest)
+#endif
+// d = 64 does half the MMA work per score, so the MUFU exp2 rate (16 / clk / SM) bounds the
+// softmax at about twice the MMA time: move a larger share of the pairs to the FMA pipe
+#ifndef POLY64_AT
+#define POLY64_AT(i) (((i) & 7) >= 5)
+#endif
 #ifndef ATTN_MAX3
 #define ATTN_MAX3 0       // row max with 3-input FMNMX3 (half the max-phase instructions)
 #endif
@@ -65,7 +70,7 @@ constexpr float RESCALE_THRESHOLD = 8.0f;       // log2 units
 #define ATTN_REGS_SOFTMAX 224
 #endif
 #ifndef ATTN_SPLIT_S
-#define ATTN_SPLIT_S 1  // S_t(j+1) in two N = 64 halves, the first issued as soon as S_t(j) is loaded
+#define ATTN_SPLIT_S 0  // 1: S_t(j+1) in two N = 64 halves, the first issued once S_t(j) is loaded (measured slower)
 #endif
 #ifndef ATTN_ST_CHUNKS
 #define ATTN_ST_CHUNKS 1  // P stored to TMEM in 1, 2 or 4 pieces as the exps complete
@@ -373,7 +378,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 #pragma unroll
           for (int i = c * PCH; i < (c + 1) * PCH; ++i) {  // in-place pack: r[i] <- bf16x2(p[2i], p[2i+1])
             const float2 x = __ffma2_rn(make_float2(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1])), sc2, nm2);
-            const float2 pp = POLY_AT(i) ? ex2_poly2(x) : make_float2(ex2_fast(x.x), ex2_fast(x.y));
+            const bool poly = D == 64 ? POLY64_AT(i) : POLY_AT(i);
+            const float2 pp = poly ? ex2_poly2(x) : make_float2(ex2_fast(x.x), ex2_fast(x.y));
             acc[i & 3] = __fadd2_rn(acc[i & 3], pp);
             r[i] = pack_bf16(pp.x, pp.y);
           }

@@ -55,6 +55,44 @@ __global__ void __launch_bounds__(256) gn_partial_kernel(const float* __restrict
   }
 }
 
+// float4 variant (C1 % 4 == 0, C2 % 4 == 0): work item = (channel quad, pixel lane); each
+// thread walks its lane's pixels of the chunk with 16-byte loads (a warp reads 512 contiguous
+// bytes of one pixel row), lanes combined through shared memory in a fixed order
+__global__ void __launch_bounds__(256) gn_partial4_kernel(const float* __restrict__ x1, int C1, const float* __restrict__ x2,
+                                                          int C2, int P, int G, float2* __restrict__ part) {
+  extern __shared__ float4 sm4[];  // [PL][CV] sums, then [PL][CV] sums of squares
+  const int C = C1 + C2, CV = C >> 2;
+  const int PL = CV >= (int)blockDim.x ? 1 : (int)blockDim.x / CV;
+  const int n = blockIdx.y, chunk = blockIdx.x;
+  const int p0 = chunk * GN_CHUNK, p1 = min(P, p0 + GN_CHUNK);
+  float4* ssum = sm4;
+  float4* ssq = sm4 + PL * CV;
+  for (int w = threadIdx.x; w < CV * PL; w += blockDim.x) {
+    const int cv = w % CV, pl = w / CV, c = 4 * cv;
+    const float* base = c < C1 ? x1 + c : x2 + (c - C1);
+    const long long ld = c < C1 ? C1 : C2;
+    float4 s = make_float4(0.f, 0.f, 0.f, 0.f), q = s;
+#pragma unroll 4
+    for (int p = p0 + pl; p < p1; p += PL) {
+      const float4 v = __ldg(reinterpret_cast<const float4*>(base + ((long long)n * P + p) * ld));
+      s.x += v.x; s.y += v.y; s.z += v.z; s.w += v.w;
+      q.x = fmaf(v.x, v.x, q.x); q.y = fmaf(v.y, v.y, q.y); q.z = fmaf(v.z, v.z, q.z); q.w = fmaf(v.w, v.w, q.w);
+    }
+    ssum[pl * CV + cv] = s;
+    ssq[pl * CV + cv] = q;
+  }
+  __syncthreads();
+  const int cg = C / G;
+  const float* fs = reinterpret_cast<const float*>(ssum);
+  const float* fq = reinterpret_cast<const float*>(ssq);
+  for (int gi = threadIdx.x; gi < G; gi += blockDim.x) {
+    float s = 0.f, q = 0.f;
+    for (int pl = 0; pl < PL; ++pl)
+      for (int c = gi * cg; c < (gi + 1) * cg; ++c) { s += fs[pl * C + c]; q += fq[pl * C + c]; }
+    part[((long long)n * gridDim.x + chunk) * G + gi] = make_float2(s, q);
+  }
+}
+
 __global__ void gn_finalize_kernel(const float2* __restrict__ part, int nchunk, int G, long long count, float eps,
                                    float2* __restrict__ stats) {
   const int n = blockIdx.x;
@@ -76,7 +114,12 @@ void launch_gn_stats(const float* x1, int C1, const float* x2, int C2, int N, in
                      float2* partial, float2* stats, cudaStream_t st) {
   const int nchunk = (P + GN_CHUNK - 1) / GN_CHUNK;
   const int C = C1 + C2;
-  gn_partial_kernel<<<dim3(nchunk, N), 256, 2 * C * sizeof(float), st>>>(x1, C1, x2, C2, P, G, partial);
+  if (C1 % 4 == 0 && C2 % 4 == 0) {
+    const int CV = C / 4, PL = CV >= 256 ? 1 : 256 / CV;
+    gn_partial4_kernel<<<dim3(nchunk, N), 256, 2 * PL * CV * sizeof(float4), st>>>(x1, C1, x2, C2, P, G, partial);
+  } else {
+    gn_partial_kernel<<<dim3(nchunk, N), 256, 2 * C * sizeof(float), st>>>(x1, C1, x2, C2, P, G, partial);
+  }
   gn_finalize_kernel<<<N, 64, 0, st>>>(partial, nchunk, G, (long long)P * (C / G), eps, stats);
 }
 

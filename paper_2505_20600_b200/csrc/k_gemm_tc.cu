@@ -203,8 +203,25 @@ __device__ __forceinline__ void epilogue_chunk(const GemmArgs& g, int row, int c
       float* x = reinterpret_cast<float*>(g.C) + (long long)row * g.ldc + col0;
       const long long prow = g.pos_div > 0 ? (long long)(g.ri_off + row) / g.pos_div : (long long)info->tok;
       const bf16* pos = g.pos ? reinterpret_cast<const bf16*>(g.pos) + prow * g.pos_ld + col0 : nullptr;
-      for (int i = 0; i < 32; ++i)
-        if (col0 + i < g.N) x[i] = v[i] + (pos ? __bfloat162float(pos[i]) : 0.f);
+      if (full && (reinterpret_cast<uintptr_t>(pos) & 15) == 0) {  // 16-byte vectors (conv epilogues)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          float2 p[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+          if (pos) {
+            const uint4 u = __ldg(reinterpret_cast<const uint4*>(pos) + q);
+            const __nv_bfloat162* hb = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) p[e] = __bfloat1622float2(hb[e]);
+          }
+          reinterpret_cast<float4*>(x)[2 * q] =
+              make_float4(v[8 * q] + p[0].x, v[8 * q + 1] + p[0].y, v[8 * q + 2] + p[1].x, v[8 * q + 3] + p[1].y);
+          reinterpret_cast<float4*>(x)[2 * q + 1] =
+              make_float4(v[8 * q + 4] + p[2].x, v[8 * q + 5] + p[2].y, v[8 * q + 6] + p[3].x, v[8 * q + 7] + p[3].y);
+        }
+      } else {
+        for (int i = 0; i < 32; ++i)
+          if (col0 + i < g.N) x[i] = v[i] + (pos ? __bfloat162float(pos[i]) : 0.f);
+      }
       break;
     }
     case EPI_ADDRES: {
@@ -513,7 +530,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
   uint64_t* tfull = empty + C::STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  bf16* sbias = reinterpret_cast<bf16*>(smem + C::STAGES * C::STAGE_BYTES + 256);  // [2][BN]
+  bf16* sbias = reinterpret_cast<bf16*>(smem + C::STAGES * C::STAGE_BYTES + 256);  // [2][256]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = tc::cluster_ctarank();
@@ -618,7 +635,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       // the tile's bias slice -> shared memory (one 4-byte load per epilogue thread), so the
       // chunks below read it at shared-memory latency instead of one global round trip each;
       // double-buffered by accumulator, and the per-tile barrier keeps warps within one tile
-      bf16* sb = sbias + acc * BN;
+      bf16* sb = sbias + acc * 256;  // slice stride 256 whatever BN: every thread writes 2 of 256 entries
       const bf16* gbias = reinterpret_cast<const bf16*>(g.bias);
       if (gbias) {
         const int i = 2 * ((warp - 4) * 32 + lane);

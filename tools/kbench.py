@@ -13,6 +13,11 @@ ap.add_argument("--K", type=int, default=3072)
 ap.add_argument("--iters", type=int, default=10)
 ap.add_argument("--epi", type=int, default=0, help="0 store, 1 bias+GELU (fc1), 5 GEGLU (N/2 outputs)")
 ap.add_argument("--bias", action="store_true")
+ap.add_argument("--dh", type=int, default=128, help="attention head dim (64: SD3 / UNet)")
+ap.add_argument("--heads", type=int, default=24)
+ap.add_argument("--L", type=int, default=4608, help="attention keys per request")
+ap.add_argument("--qlens", default="512,1843", help="query segments per request (comma list)")
+ap.add_argument("--nreq", type=int, default=8)
 args = ap.parse_args()
 res = {}
 def timeit(fn, iters):
@@ -50,16 +55,17 @@ if "gated" in args.which:  # out-projection shape: fp32 residual += gate * (A B^
                                             gate.data_ptr(), M, N, K, 0), args.iters)
     res["gated"] = {"M": M, "N": N, "K": K, "ms": ms, "tflops": 2 * M * N * K / ms / 1e9}
 if "attn" in args.which:
-    heads, dh, L = 24, 128, 4608
-    qlens = [512, 1843] * 8
+    heads, dh, L = args.heads, args.dh, args.L
+    qlens = [int(x) for x in args.qlens.split(",")] * args.nreq
     H = heads * dh
     M = sum(qlens)
     Q = torch.randn(M, H, device="cuda", dtype=torch.bfloat16)
-    kv = torch.randn(8, 2, L, H, device="cuda", dtype=torch.bfloat16)
+    kv = torch.randn(args.nreq, 2, L, H, device="cuda", dtype=torch.bfloat16)
     O = torch.empty(M, H, device="cuda", dtype=torch.bfloat16)
     segs, s = [], 0
+    per = len(args.qlens.split(","))
     for i, q in enumerate(qlens):
-        segs.append((s, q, i // 2)); s += q
+        segs.append((s, q, i // per)); s += q
     rep = int(os.environ.get("IG_OP_REPEAT", "20"))
     os.environ["IG_OP_REPEAT"] = str(rep)
     ms = timeit(lambda: ig.ig_op_attention(ig.IG_BF16, Q.data_ptr(), H, O.data_ptr(), H, kv.data_ptr(), segs, L, heads, dh, 0), args.iters) / rep
