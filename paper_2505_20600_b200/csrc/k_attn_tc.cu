@@ -55,7 +55,7 @@ constexpr float RESCALE_THRESHOLD = 8.0f;       // log2 units
 // d = 64 does half the MMA work per score, so the MUFU exp2 rate (16 / clk / SM) bounds the
 // softmax at about twice the MMA time: move a larger share of the pairs to the FMA pipe
 #ifndef POLY64_AT
-#define POLY64_AT(i) (((i) & 7) >= 5)
+#define POLY64_AT(i) 0  // measured (ncu cycles, UNet shapes): every poly share tried (1/4 .. 5/8) is slower
 #endif
 #ifndef ATTN_MAX3
 #define ATTN_MAX3 0       // row max with 3-input FMNMX3 (half the max-phase instructions)
