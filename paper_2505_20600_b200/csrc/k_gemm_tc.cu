@@ -26,6 +26,8 @@ namespace {
 constexpr int BM = 128, BK = 64;
 constexpr int NUM_THREADS = 256;
 
+// EPI_GATED_RES staging (gated_reduce_chunk): per epilogue warp two [32 rows][32 fp32] tiles
+constexpr int EPI_RED_BYTES = 4 * 2 * 32 * 32 * 4;
 template <int BN>
 struct Cfg {
   static constexpr int STAGES = BN == 256 ? 4 : 6;
@@ -33,7 +35,7 @@ struct Cfg {
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int TMEM_COLS = 2 * BN;  // double-buffered fp32 accumulator
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + EPI_RED_BYTES + 1024 /*align*/ + 256 /*barriers*/;
 };
 
 // GELU-tanh with the MUFU tanh (rel. error ~2^-11, below the bf16 output rounding 2^-8)
@@ -171,34 +173,7 @@ __device__ __forceinline__ void epilogue_chunk(const GemmArgs& g, int row, int c
       }
       break;
     }
-    case EPI_GATED_RES: {
-      float* x = reinterpret_cast<float*>(g.C) + (long long)row * g.ldc + col0;
-      const float* gt = g.gate + (long long)info->req * g.gate_ld + col0;
-      if (full) {
-        // issue every load of the chunk before any store (the compiler cannot reorder the
-        // residual loads across the stores on its own: x and gate may alias)
-        float4 xv[8], gv[8];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          xv[q] = __ldcs(reinterpret_cast<const float4*>(x) + q);
-          gv[q] = __ldg(reinterpret_cast<const float4*>(gt) + q);
-        }
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {  // packed f32x2 FMAs (issue-bound epilogue)
-          const float2 lo = __ffma2_rn(make_float2(gv[q].x, gv[q].y), make_float2(v[4 * q], v[4 * q + 1]),
-                                       make_float2(xv[q].x, xv[q].y));
-          const float2 hi = __ffma2_rn(make_float2(gv[q].z, gv[q].w), make_float2(v[4 * q + 2], v[4 * q + 3]),
-                                       make_float2(xv[q].z, xv[q].w));
-          xv[q] = make_float4(lo.x, lo.y, hi.x, hi.y);
-        }
-#pragma unroll
-        for (int q = 0; q < 8; ++q) __stcs(reinterpret_cast<float4*>(x) + q, xv[q]);
-      } else {
-        for (int i = 0; i < 32; ++i)
-          if (col0 + i < g.N) x[i] += gt[i] * v[i];
-      }
-      break;
-    }
+    // EPI_GATED_RES: gated_reduce_chunk (TMA reduce-add), never reaches this function
     case EPI_POS: {
       float* x = reinterpret_cast<float*>(g.C) + (long long)row * g.ldc + col0;
       const long long prow = g.pos_div > 0 ? (long long)(g.ri_off + row) / g.pos_div : (long long)info->tok;
@@ -240,6 +215,71 @@ __device__ __forceinline__ void epilogue_chunk(const GemmArgs& g, int row, int c
       }
       break;
     }
+  }
+}
+
+// EPI_GATED_RES through the TMA unit: t = rn(gate * (acc + bias)) per element goes into this
+// warp's [32 rows x 32 cols] staging tile (16-byte chunk q of row r at slot q ^ (r & 7): the
+// SWIZZLE_128B pattern of the map) and one cp.reduce.async.bulk .add.f32 adds the tile into the
+// fp32 residual in L2 — coalesced, and no residual loads on the SMs (rows >= M / cols >= N fall
+// outside the map).  Both GEMM kernels use it, so every tile path rounds x + t identically (batch
+// invariance).  The caller has issued tcgen05.ld of r; two staging buffers alternate per warp
+// (`cnt` counts the warp's chunks), and a buffer is rewritten only after the reduce issued from
+// it two chunks earlier has read it.
+__device__ __forceinline__ void gated_reduce_chunk(const GemmArgs& g, const CUtensorMap* tmX, int lane, int row0,
+                                                   int col0, uint32_t (&r)[32], int req, const bf16* bchunk,
+                                                   float4* wbuf, int& cnt) {
+  const int k = cnt++;
+  if (k >= 2) {
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+    __syncwarp();
+  }
+  tc::tmem_ld_wait();
+  const bool full = col0 + 32 <= g.N;
+  float v[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+  if (bchunk) {
+    if (full) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        uint4 u = reinterpret_cast<const uint4*>(bchunk)[q];
+        const __nv_bfloat162* hb = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float2 y = __fadd2_rn(make_float2(v[q * 8 + 2 * e], v[q * 8 + 2 * e + 1]), __bfloat1622float2(hb[e]));
+          v[q * 8 + 2 * e] = y.x;
+          v[q * 8 + 2 * e + 1] = y.y;
+        }
+      }
+    } else {
+      for (int i = 0; i < 32; ++i)
+        if (col0 + i < g.N) v[i] = __fadd_rn(v[i], __bfloat162float(bchunk[i]));
+    }
+  }
+  const float* grow = g.gate + (long long)req * g.gate_ld + col0;
+  float4* buf = wbuf + (k & 1) * 256;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    float4 gv = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (full) {
+      gv = __ldg(reinterpret_cast<const float4*>(grow) + q);
+    } else {
+      float* gp = reinterpret_cast<float*>(&gv);
+      for (int e = 0; e < 4; ++e)
+        if (col0 + 4 * q + e < g.N) gp[e] = grow[4 * q + e];
+    }
+    const float2 lo = __fmul2_rn(make_float2(gv.x, gv.y), make_float2(v[4 * q], v[4 * q + 1]));
+    const float2 hi = __fmul2_rn(make_float2(gv.z, gv.w), make_float2(v[4 * q + 2], v[4 * q + 3]));
+    buf[lane * 8 + (q ^ (lane & 7))] = make_float4(lo.x, lo.y, hi.x, hi.y);
+  }
+  tc::fence_proxy_async_smem();
+  __syncwarp();
+  if (lane == 0) {
+    asm volatile("cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.bulk_group [%0, {%2, %3}], [%1];"
+                 ::"l"(reinterpret_cast<uint64_t>(tmX)), "r"(tc::smem_u32(buf)), "r"(col0), "r"(row0)
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
   }
 }
 
@@ -319,13 +359,14 @@ __device__ __forceinline__ void epilogue_qkv_head(const GemmArgs& g, int row, in
 template <int BN, bool CONV = false>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                   const GemmArgs g, int num_m, int num_n, int G) {
+                   const __grid_constant__ CUtensorMap tmX, const GemmArgs g, int num_m, int num_n, int G) {
   using C = Cfg<BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + C::STAGES * C::A_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
+  uint8_t* sred = smem + C::STAGES * C::STAGE_BYTES;  // [4 warps][2][32][32] fp32, 1024-aligned
+  uint64_t* full = reinterpret_cast<uint64_t*>(sred + EPI_RED_BYTES);
   uint64_t* empty = full + C::STAGES;
   uint64_t* tfull = empty + C::STAGES;
   uint64_t* tempty = tfull + 2;
@@ -430,6 +471,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
   } else if (warp >= 4) {  // ===== epilogue =====
     const int quad = warp & 3;
+    int red_cnt = 0;  // EPI_GATED_RES chunks reduced so far (staging buffer parity)
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
@@ -474,6 +516,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           tc::tmem_ld_wait();
           if (row < g.M && n0 + c < g.N) epilogue_geglu(g, row, n0 / 2 + c, ra, rg, BIAS_AT(c), BIAS_AT(128 + c));
         }
+      } else if (g.epi == EPI_GATED_RES) {
+#pragma unroll 1
+        for (int c = 0; c < BN; c += 32) {
+          if (n0 + c >= g.N) break;  // warp-uniform
+          uint32_t r[32];
+          tc::tmem_ld32(tbase + c, r);
+          gated_reduce_chunk(g, &tmX, lane, m0 + quad * 32, n0 + c, r, info.req, BIAS_AT(c),
+                             reinterpret_cast<float4*>(sred) + quad * 2 * 256, red_cnt);
+        }
       } else {
 #pragma unroll 1
         for (int c = 0; c < BN; c += 32) {
@@ -490,6 +541,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
   }
+  if (warp >= 4 && lane == 0 && g.epi == EPI_GATED_RES) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   tc::tc_fence_before();
   __syncthreads();
   if (warp == 1) tc::tmem_dealloc<C::TMEM_COLS>(tmem_base);
@@ -507,30 +559,31 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 // 2-3 waves (launch_gemm_tc picks the tile by the wave count; per-element math unchanged).
 template <int BN>
 struct Cfg2 {
-  static constexpr int STAGES = BN == 256 ? 6 : 8;
+  static constexpr int STAGES = BN == 256 ? 6 : 7;
   static constexpr int A_BYTES = 128 * BK * 2;
   static constexpr int B_BYTES = (BN / 2) * BK * 2;  // this CTA's half of the B tile
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int TMEM_COLS = 512;
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256 + 2 * 256 * 2 /*bias slices*/;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + EPI_RED_BYTES + 1024 + 256 + 2 * 256 * 2 /*bias slices*/;
 };
 
 template <bool CONV = false, int BN = 256>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                    const GemmArgs g, int num_m, int num_n, int G) {
+                    const __grid_constant__ CUtensorMap tmX, const GemmArgs g, int num_m, int num_n, int G) {
   static_assert(BN % 32 == 0 && (BN / 2) % 8 == 0 && BN <= 256, "2-CTA tile width");
   using C = Cfg2<BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + C::STAGES * C::A_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
+  uint8_t* sred = smem + C::STAGES * C::STAGE_BYTES;  // [4 warps][2][32][32] fp32, 1024-aligned
+  uint64_t* full = reinterpret_cast<uint64_t*>(sred + EPI_RED_BYTES);
   uint64_t* empty = full + C::STAGES;
   uint64_t* tfull = empty + C::STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  bf16* sbias = reinterpret_cast<bf16*>(smem + C::STAGES * C::STAGE_BYTES + 256);  // [2][256]
+  bf16* sbias = reinterpret_cast<bf16*>(sred + EPI_RED_BYTES + 256);  // [2][256]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = tc::cluster_ctarank();
@@ -541,6 +594,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
   if (warp == 0 && lane == 0) {
     tc::tma_prefetch_desc(&tmA);
     tc::tma_prefetch_desc(&tmB);
+    if (g.epi == EPI_GATED_RES) tc::tma_prefetch_desc(&tmX);
     for (int s = 0; s < C::STAGES; ++s) {
       tc::mbar_init(&full[s], 1);
       tc::mbar_init(&empty[s], 1);
@@ -626,6 +680,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     }
   } else if (warp >= 4) {  // ===== epilogue (both CTAs, own TMEM rows) =====
     const int quad = warp & 3;
+    int red_cnt = 0;  // EPI_GATED_RES chunks reduced so far (staging buffer parity)
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int t = cluster; t < num_tiles; t += nclusters) {
@@ -680,6 +735,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
           tc::tmem_ld_wait();
           if (row < g.M && n0 + c < g.N) epilogue_geglu(g, row, n0 / 2 + c, ra, rg, BIAS_AT(c), BIAS_AT(128 + c));
         }
+      } else if (g.epi == EPI_GATED_RES) {
+#pragma unroll 1
+        for (int c = 0; c < BN; c += 32) {
+          if (n0 + c >= g.N) break;  // warp-uniform
+          uint32_t r[32];
+          tc::tmem_ld32(tbase + c, r);
+          gated_reduce_chunk(g, &tmX, lane, m0 + quad * 32, n0 + c, r, info.req, gbias ? sb + c : nullptr,
+                             reinterpret_cast<float4*>(sred) + quad * 2 * 256, red_cnt);
+        }
       } else {
 #pragma unroll 1
         for (int c = 0; c < BN; c += 32) {
@@ -699,6 +763,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
   }
+  if (warp >= 4 && lane == 0 && g.epi == EPI_GATED_RES) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   tc::tc_fence_before();
   tc::cluster_sync();
   if (warp == 1) tc::tmem_dealloc2<C::TMEM_COLS>(tmem_base);
@@ -769,6 +834,25 @@ bool encode_tmap(CUtensorMap* m, const void* ptr, long long rows, long long cols
                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
+}
+// fp32 [rows, cols] (ld floats) map with a 32 x 32 box, 128-byte swizzle: the target of the gated
+// residual's TMA reduce-add
+bool make_tmap_f32(CUtensorMap* m, const void* ptr, long long rows, long long cols, long long ld) {
+  thread_local std::unordered_map<TmapKey, CUtensorMap, TmapHash> cache;
+  const TmapKey k{ptr, rows, cols, ld, -32};
+  auto it = cache.find(k);
+  if (it != cache.end()) { *m = it->second; return true; }
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * 4)};
+  cuuint32_t box[2] = {32, 32};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return false;
+  if (cache.size() > 8192) cache.clear();
+  cache.emplace(k, *m);
+  return true;
 }
 }  // namespace
 
@@ -842,12 +926,14 @@ void launch_gemm_tc(const GemmArgs& g, cudaStream_t st) {
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at; cfg.numAttrs = g.pdl ? 1 : 0;
+    CUtensorMap tx = tb;  // the residual map (EPI_GATED_RES only; any valid map otherwise)
+    if (g.epi == EPI_GATED_RES) make_tmap_f32(&tx, g.C, g.M, g.N, g.ldc);
     if (BN2 == 160) {
       cfg.dynamicSmemBytes = Cfg2<160>::SMEM;
-      cudaLaunchKernelEx(&cfg, gemm_tc2_kernel<false, 160>, ta, tb, g, num_m, num_n, G2);
+      cudaLaunchKernelEx(&cfg, gemm_tc2_kernel<false, 160>, ta, tb, tx, g, num_m, num_n, G2);
     } else {
       cfg.dynamicSmemBytes = Cfg2<256>::SMEM;
-      cudaLaunchKernelEx(&cfg, gemm_tc2_kernel<false, 256>, ta, tb, g, num_m, num_n, G2);
+      cudaLaunchKernelEx(&cfg, gemm_tc2_kernel<false, 256>, ta, tb, tx, g, num_m, num_n, G2);
     }
     return;
   }
@@ -865,12 +951,14 @@ void launch_gemm_tc(const GemmArgs& g, cudaStream_t st) {
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at; cfg.numAttrs = g.pdl ? 1 : 0;
+  CUtensorMap tx = tb;  // the residual map (EPI_GATED_RES only; any valid map otherwise)
+  if (g.epi == EPI_GATED_RES) make_tmap_f32(&tx, g.C, g.M, g.N, g.ldc);
   if (wide) {
     cfg.dynamicSmemBytes = Cfg<256>::SMEM;
-    cudaLaunchKernelEx(&cfg, gemm_tc_kernel<256>, ta, tb, g, num_m, num_n, G);
+    cudaLaunchKernelEx(&cfg, gemm_tc_kernel<256>, ta, tb, tx, g, num_m, num_n, G);
   } else {
     cfg.dynamicSmemBytes = Cfg<128>::SMEM;
-    cudaLaunchKernelEx(&cfg, gemm_tc_kernel<128>, ta, tb, g, num_m, num_n, G);
+    cudaLaunchKernelEx(&cfg, gemm_tc_kernel<128>, ta, tb, tx, g, num_m, num_n, G);
   }
 }
 
@@ -899,10 +987,10 @@ void launch_conv3x3_tc(const GemmArgs& g, cudaStream_t st) {
     const int tiles = num_m * num_n;
     const int clusters = tiles < g_num_sms / 2 ? tiles : g_num_sms / 2;
     if (BN2 == 160)
-      gemm_tc2_kernel<true, 160><<<2 * clusters, NUM_THREADS, Cfg2<160>::SMEM, st>>>(ta, tb2, g, num_m, num_n,
+      gemm_tc2_kernel<true, 160><<<2 * clusters, NUM_THREADS, Cfg2<160>::SMEM, st>>>(ta, tb2, tb2, g, num_m, num_n,
                                                                                   raster_group(num_m, 256, g.K));
     else
-      gemm_tc2_kernel<true, 256><<<2 * clusters, NUM_THREADS, Cfg2<256>::SMEM, st>>>(ta, tb2, g, num_m, num_n,
+      gemm_tc2_kernel<true, 256><<<2 * clusters, NUM_THREADS, Cfg2<256>::SMEM, st>>>(ta, tb2, tb2, g, num_m, num_n,
                                                                                   raster_group(num_m, 256, g.K));
     return;
   }
@@ -914,9 +1002,9 @@ void launch_conv3x3_tc(const GemmArgs& g, cudaStream_t st) {
   const int grid = tiles < g_num_sms ? tiles : g_num_sms;
   const int G = raster_group(num_m, BM, g.K);
   if (wide)
-    gemm_tc_kernel<256, true><<<grid, NUM_THREADS, Cfg<256>::SMEM, st>>>(ta, tb, g, num_m, num_n, G);
+    gemm_tc_kernel<256, true><<<grid, NUM_THREADS, Cfg<256>::SMEM, st>>>(ta, tb, tb, g, num_m, num_n, G);
   else
-    gemm_tc_kernel<128, true><<<grid, NUM_THREADS, Cfg<128>::SMEM, st>>>(ta, tb, g, num_m, num_n, G);
+    gemm_tc_kernel<128, true><<<grid, NUM_THREADS, Cfg<128>::SMEM, st>>>(ta, tb, tb, g, num_m, num_n, G);
 }
 
 }  // namespace ig
