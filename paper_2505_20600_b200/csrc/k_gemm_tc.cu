@@ -97,15 +97,12 @@ __device__ __forceinline__ void epilogue_geglu(const GemmArgs& g, int row, int o
   }
 }
 
-// epilogue for one 32-column chunk of one row held in registers
-template <int BN>
-// bchunk: this chunk's 32 bias values (global memory, or the tile's bias slice staged in shared
-// memory by the 2-CTA kernel), nullptr without bias
-__device__ __forceinline__ void epilogue_chunk(const GemmArgs& g, int row, int col0, const uint32_t (&r)[32],
-                                               const RowInfo* info, const bf16* bchunk) {
-  float v[32];
-#pragma unroll
-  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+// epilogue math of one 32-column chunk of one row, in registers: bias, then GELU / positional or
+// per-image term (EPI_POS) / residual (EPI_ADDRES).  bchunk: this chunk's 32 bias values (global
+// memory, or the tile's bias slice staged in shared memory by the 2-CTA kernel), nullptr
+// without bias.  Row-dependent loads only for rows < M.
+__device__ __forceinline__ void chunk_math(const GemmArgs& g, int row, int col0, float (&v)[32], const RowInfo& info,
+                                           const bf16* bchunk) {
   const bool full = col0 + 32 <= g.N;
   if (bchunk) {
     if (full) {
@@ -127,95 +124,174 @@ __device__ __forceinline__ void epilogue_chunk(const GemmArgs& g, int row, int c
         if (col0 + i < g.N) v[i] += __bfloat162float(bchunk[i]);
     }
   }
-  switch (g.epi) {
-    case EPI_GELU:
+  if (g.epi == EPI_GELU) {
+    if (g.precise_gelu) {
 #pragma unroll
-      if (g.precise_gelu) {
-        for (int i = 0; i < 32; ++i) v[i] = gelu_tanh(v[i]);
-      } else {
+      for (int i = 0; i < 32; ++i) v[i] = gelu_tanh(v[i]);
+    } else {
 #pragma unroll
-        for (int i = 0; i < 32; i += 2) {
-          const float2 y = gelu_tanh_fast2(make_float2(v[i], v[i + 1]));
-          v[i] = y.x;
-          v[i + 1] = y.y;
-        }
+      for (int i = 0; i < 32; i += 2) {
+        const float2 y = gelu_tanh_fast2(make_float2(v[i], v[i + 1]));
+        v[i] = y.x;
+        v[i + 1] = y.y;
       }
-      // fallthrough
-    case EPI_STORE: {
-      if (g.out_f32) {
-        float* c = reinterpret_cast<float*>(g.C) + (long long)row * g.ldc + col0;
-        if (full) {
-#pragma unroll
-          for (int q = 0; q < 8; ++q)
-            reinterpret_cast<float4*>(c)[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-        } else {
-          for (int i = 0; i < 32; ++i)
-            if (col0 + i < g.N) c[i] = v[i];
-        }
-      } else {
-        bf16* c = reinterpret_cast<bf16*>(g.C) + (long long)row * g.ldc + col0;
-        if (full) {
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            uint4 u;
-            uint32_t* w = reinterpret_cast<uint32_t*>(&u);
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              __nv_bfloat162 p = __floats2bfloat162_rn(v[q * 8 + 2 * e], v[q * 8 + 2 * e + 1]);
-              w[e] = *reinterpret_cast<uint32_t*>(&p);
-            }
-            reinterpret_cast<uint4*>(c)[q] = u;
-          }
-        } else {
-          for (int i = 0; i < 32; ++i)
-            if (col0 + i < g.N) c[i] = __float2bfloat16_rn(v[i]);
-        }
-      }
-      break;
     }
-    // EPI_GATED_RES: gated_reduce_chunk (TMA reduce-add), never reaches this function
-    case EPI_POS: {
-      float* x = reinterpret_cast<float*>(g.C) + (long long)row * g.ldc + col0;
-      const long long prow = g.pos_div > 0 ? (long long)(g.ri_off + row) / g.pos_div : (long long)info->tok;
-      const bf16* pos = g.pos ? reinterpret_cast<const bf16*>(g.pos) + prow * g.pos_ld + col0 : nullptr;
-      if (full && (reinterpret_cast<uintptr_t>(pos) & 15) == 0) {  // 16-byte vectors (conv epilogues)
+  } else if (g.epi == EPI_POS && row < g.M && g.pos) {
+    const long long prow = g.pos_div > 0 ? (long long)(g.ri_off + row) / g.pos_div : (long long)info.tok;
+    const bf16* pos = reinterpret_cast<const bf16*>(g.pos) + prow * g.pos_ld + col0;
+    if (full && (reinterpret_cast<uintptr_t>(pos) & 15) == 0) {
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          float2 p[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
-          if (pos) {
-            const uint4 u = __ldg(reinterpret_cast<const uint4*>(pos) + q);
-            const __nv_bfloat162* hb = reinterpret_cast<const __nv_bfloat162*>(&u);
+      for (int q = 0; q < 4; ++q) {
+        const uint4 u = __ldg(reinterpret_cast<const uint4*>(pos) + q);
+        const __nv_bfloat162* hb = reinterpret_cast<const __nv_bfloat162*>(&u);
 #pragma unroll
-            for (int e = 0; e < 4; ++e) p[e] = __bfloat1622float2(hb[e]);
-          }
-          reinterpret_cast<float4*>(x)[2 * q] =
-              make_float4(v[8 * q] + p[0].x, v[8 * q + 1] + p[0].y, v[8 * q + 2] + p[1].x, v[8 * q + 3] + p[1].y);
-          reinterpret_cast<float4*>(x)[2 * q + 1] =
-              make_float4(v[8 * q + 4] + p[2].x, v[8 * q + 5] + p[2].y, v[8 * q + 6] + p[3].x, v[8 * q + 7] + p[3].y);
+        for (int e = 0; e < 4; ++e) {
+          const float2 p = __bfloat1622float2(hb[e]);
+          v[8 * q + 2 * e] += p.x;
+          v[8 * q + 2 * e + 1] += p.y;
         }
-      } else {
-        for (int i = 0; i < 32; ++i)
-          if (col0 + i < g.N) x[i] = v[i] + (pos ? __bfloat162float(pos[i]) : 0.f);
       }
-      break;
+    } else {
+      for (int i = 0; i < 32; ++i)
+        if (col0 + i < g.N) v[i] += __bfloat162float(pos[i]);
     }
-    case EPI_ADDRES: {
-      float* x = reinterpret_cast<float*>(g.C) + (long long)row * g.ldc + col0;
-      const float* rs = g.res + (long long)row * g.ldc + col0;
-      if (full) {
+  } else if (g.epi == EPI_ADDRES && row < g.M) {
+    const float* rs = g.res + (long long)row * g.ldc + col0;
+    if (full) {
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          const float4 a = __ldg(reinterpret_cast<const float4*>(rs) + q);
-          reinterpret_cast<float4*>(x)[q] = make_float4(v[4 * q] + a.x, v[4 * q + 1] + a.y, v[4 * q + 2] + a.z,
-                                                        v[4 * q + 3] + a.w);
-        }
-      } else {
-        for (int i = 0; i < 32; ++i)
-          if (col0 + i < g.N) x[i] = v[i] + rs[i];
+      for (int q = 0; q < 8; ++q) {
+        const float4 a = __ldg(reinterpret_cast<const float4*>(rs) + q);
+        v[4 * q] += a.x; v[4 * q + 1] += a.y; v[4 * q + 2] += a.z; v[4 * q + 3] += a.w;
       }
-      break;
+    } else {
+      for (int i = 0; i < 32; ++i)
+        if (col0 + i < g.N) v[i] += rs[i];
     }
   }
+}
+
+// thread-per-row stores of one chunk (bf16 outputs of 160-wide tiles; the TMA paths below
+// cover the rest)
+template <int BN>
+__device__ __forceinline__ void epilogue_chunk(const GemmArgs& g, int row, int col0, const uint32_t (&r)[32],
+                                               const RowInfo* info, const bf16* bchunk) {
+  float v[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+  const bool full = col0 + 32 <= g.N;
+  chunk_math(g, row, col0, v, *info, bchunk);
+  if (g.out_f32 || g.epi == EPI_POS || g.epi == EPI_ADDRES) {
+    float* c = reinterpret_cast<float*>(g.C) + (long long)row * g.ldc + col0;
+    if (full) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        reinterpret_cast<float4*>(c)[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+    } else {
+      for (int i = 0; i < 32; ++i)
+        if (col0 + i < g.N) c[i] = v[i];
+    }
+  } else {
+    bf16* c = reinterpret_cast<bf16*>(g.C) + (long long)row * g.ldc + col0;
+    if (full) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        uint4 u;
+        uint32_t* w = reinterpret_cast<uint32_t*>(&u);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          __nv_bfloat162 p = __floats2bfloat162_rn(v[q * 8 + 2 * e], v[q * 8 + 2 * e + 1]);
+          w[e] = *reinterpret_cast<uint32_t*>(&p);
+        }
+        reinterpret_cast<uint4*>(c)[q] = u;
+      }
+    } else {
+      for (int i = 0; i < 32; ++i)
+        if (col0 + i < g.N) c[i] = __float2bfloat16_rn(v[i]);
+    }
+  }
+}
+
+__device__ __forceinline__ bool tma_out_f32(const GemmArgs& g) {
+  return ((g.epi == EPI_STORE || g.epi == EPI_GELU) && g.out_f32) || g.epi == EPI_POS || g.epi == EPI_ADDRES;
+}
+__device__ __forceinline__ bool tma_out_bf16(const GemmArgs& g) {
+  return (g.epi == EPI_STORE || g.epi == EPI_GELU) && !g.out_f32;
+}
+// Stores through the TMA unit: a warp's 32 rows x 128 bytes (32 fp32 or 64 bf16 columns) are
+// staged in shared memory in the SWIZZLE_128B layout of the output map (16-byte chunk q of row
+// r at slot q ^ (r & 7)) and written by one cp.async.bulk.tensor store — full 128-byte rows per
+// transaction instead of 32 scattered 16-byte pieces per warp instruction; rows >= M and
+// columns >= N fall outside the map.  Two staging buffers per warp alternate (`cnt`), reused
+// after the bulk group issued from them has been read.
+__device__ __forceinline__ void tma_stage_wait(int lane, int& cnt, int& k) {
+  k = cnt++;
+  if (k >= 2) {
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+    __syncwarp();
+  }
+}
+__device__ __forceinline__ void tma_stage_issue(const CUtensorMap* tm, int lane, float4* buf, int col0, int row0,
+                                                bool reduce_add) {
+  tc::fence_proxy_async_smem();
+  __syncwarp();
+  if (lane == 0) {
+    if (reduce_add)
+      asm volatile("cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.bulk_group [%0, {%2, %3}], [%1];"
+                   ::"l"(reinterpret_cast<uint64_t>(tm)), "r"(tc::smem_u32(buf)), "r"(col0), "r"(row0)
+                   : "memory");
+    else
+      asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];"
+                   ::"l"(reinterpret_cast<uint64_t>(tm)), "r"(tc::smem_u32(buf)), "r"(col0), "r"(row0)
+                   : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+  }
+}
+// fp32 output (EPI_STORE / EPI_GELU with out_f32, EPI_POS, EPI_ADDRES): 32 columns
+__device__ __forceinline__ void tma_store_f32(const GemmArgs& g, const CUtensorMap* tm, int lane, int row0, int col0,
+                                              const uint32_t (&r)[32], const RowInfo& info, const bf16* bchunk,
+                                              float4* wbuf, int& cnt) {
+  int k;
+  tma_stage_wait(lane, cnt, k);
+  tc::tmem_ld_wait();
+  float v[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+  chunk_math(g, row0 + lane, col0, v, info, bchunk);
+  float4* buf = wbuf + (k & 1) * 256;
+#pragma unroll
+  for (int q = 0; q < 8; ++q)
+    buf[lane * 8 + (q ^ (lane & 7))] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+  tma_stage_issue(tm, lane, buf, col0, row0, false);
+}
+// bf16 output (EPI_STORE / EPI_GELU): 64 columns from two TMEM chunks
+__device__ __forceinline__ void tma_store_bf16(const GemmArgs& g, const CUtensorMap* tm, int lane, int row0, int col0,
+                                               const uint32_t (&r0)[32], const uint32_t (&r1)[32], const RowInfo& info,
+                                               const bf16* b0, const bf16* b1, float4* wbuf, int& cnt) {
+  int k;
+  tma_stage_wait(lane, cnt, k);
+  tc::tmem_ld_wait();
+  float4* buf = wbuf + (k & 1) * 256;
+  uint4* ubuf = reinterpret_cast<uint4*>(buf);
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    float v[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(h ? r1[i] : r0[i]);
+    chunk_math(g, row0 + lane, col0 + 32 * h, v, info, h ? b1 : b0);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      uint4 u;
+      uint32_t* w = reinterpret_cast<uint32_t*>(&u);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        __nv_bfloat162 p = __floats2bfloat162_rn(v[q * 8 + 2 * e], v[q * 8 + 2 * e + 1]);
+        w[e] = *reinterpret_cast<uint32_t*>(&p);
+      }
+      const int qq = 4 * h + q;
+      ubuf[lane * 8 + (qq ^ (lane & 7))] = u;
+    }
+  }
+  tma_stage_issue(tm, lane, buf, col0, row0, false);
 }
 
 // EPI_GATED_RES through the TMA unit: t = rn(gate * (acc + bias)) per element goes into this
@@ -525,6 +601,25 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           gated_reduce_chunk(g, &tmX, lane, m0 + quad * 32, n0 + c, r, info.req, BIAS_AT(c),
                              reinterpret_cast<float4*>(sred) + quad * 2 * 256, red_cnt);
         }
+      } else if (tma_out_f32(g)) {
+#pragma unroll 1
+        for (int c = 0; c < BN; c += 32) {
+          if (n0 + c >= g.N) break;  // warp-uniform
+          uint32_t r[32];
+          tc::tmem_ld32(tbase + c, r);
+          tma_store_f32(g, &tmX, lane, m0 + quad * 32, n0 + c, r, info, BIAS_AT(c),
+                        reinterpret_cast<float4*>(sred) + quad * 2 * 256, red_cnt);
+        }
+      } else if (BN % 64 == 0 && tma_out_bf16(g)) {
+#pragma unroll 1
+        for (int c = 0; c < BN; c += 64) {
+          if (n0 + c >= g.N) break;  // warp-uniform
+          uint32_t r0[32], r1[32];
+          tc::tmem_ld32(tbase + c, r0);
+          tc::tmem_ld32(tbase + c + 32, r1);
+          tma_store_bf16(g, &tmX, lane, m0 + quad * 32, n0 + c, r0, r1, info, BIAS_AT(c), BIAS_AT(c + 32),
+                         reinterpret_cast<float4*>(sred) + quad * 2 * 256, red_cnt);
+        }
       } else {
 #pragma unroll 1
         for (int c = 0; c < BN; c += 32) {
@@ -541,7 +636,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
   }
-  if (warp >= 4 && lane == 0 && g.epi == EPI_GATED_RES) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  if (warp >= 4 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // TMA stores / reduces
   tc::tc_fence_before();
   __syncthreads();
   if (warp == 1) tc::tmem_dealloc<C::TMEM_COLS>(tmem_base);
@@ -594,7 +689,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
   if (warp == 0 && lane == 0) {
     tc::tma_prefetch_desc(&tmA);
     tc::tma_prefetch_desc(&tmB);
-    if (g.epi == EPI_GATED_RES) tc::tma_prefetch_desc(&tmX);
+    if (g.epi != EPI_QKV && g.epi != EPI_GEGLU) tc::tma_prefetch_desc(&tmX);
     for (int s = 0; s < C::STAGES; ++s) {
       tc::mbar_init(&full[s], 1);
       tc::mbar_init(&empty[s], 1);
@@ -744,6 +839,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
           gated_reduce_chunk(g, &tmX, lane, m0 + quad * 32, n0 + c, r, info.req, gbias ? sb + c : nullptr,
                              reinterpret_cast<float4*>(sred) + quad * 2 * 256, red_cnt);
         }
+      } else if (tma_out_f32(g)) {
+#pragma unroll 1
+        for (int c = 0; c < BN; c += 32) {
+          if (n0 + c >= g.N) break;  // warp-uniform
+          uint32_t r[32];
+          tc::tmem_ld32(tbase + c, r);
+          tma_store_f32(g, &tmX, lane, m0 + quad * 32, n0 + c, r, info, BIAS_AT(c),
+                        reinterpret_cast<float4*>(sred) + quad * 2 * 256, red_cnt);
+        }
+      } else if (BN % 64 == 0 && tma_out_bf16(g)) {
+#pragma unroll 1
+        for (int c = 0; c < BN; c += 64) {
+          if (n0 + c >= g.N) break;  // warp-uniform
+          uint32_t r0[32], r1[32];
+          tc::tmem_ld32(tbase + c, r0);
+          tc::tmem_ld32(tbase + c + 32, r1);
+          tma_store_bf16(g, &tmX, lane, m0 + quad * 32, n0 + c, r0, r1, info, BIAS_AT(c), BIAS_AT(c + 32),
+                         reinterpret_cast<float4*>(sred) + quad * 2 * 256, red_cnt);
+        }
       } else {
 #pragma unroll 1
         for (int c = 0; c < BN; c += 32) {
@@ -763,7 +877,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
   }
-  if (warp >= 4 && lane == 0 && g.epi == EPI_GATED_RES) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  if (warp >= 4 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // TMA stores / reduces
   tc::tc_fence_before();
   tc::cluster_sync();
   if (warp == 1) tc::tmem_dealloc2<C::TMEM_COLS>(tmem_base);
@@ -854,6 +968,17 @@ bool make_tmap_f32(CUtensorMap* m, const void* ptr, long long rows, long long co
   cache.emplace(k, *m);
   return true;
 }
+// the output map of the TMA epilogues: fp32 32 x 32 boxes (gated residual reduce-add, fp32 stores)
+// or bf16 64-column x 32-row boxes (bf16 stores); `fallback` (any valid map) otherwise
+CUtensorMap out_map(const GemmArgs& g, const CUtensorMap& fallback) {
+  CUtensorMap m = fallback;
+  const bool f32 = g.epi == EPI_GATED_RES || g.epi == EPI_POS || g.epi == EPI_ADDRES ||
+                   ((g.epi == EPI_STORE || g.epi == EPI_GELU) && g.out_f32);
+  const bool b16 = (g.epi == EPI_STORE || g.epi == EPI_GELU) && !g.out_f32;
+  if (f32) make_tmap_f32(&m, g.C, g.M, g.N, g.ldc);
+  else if (b16) make_tmap(&m, g.C, g.M, g.N, g.ldc, 32);
+  return m;
+}
 }  // namespace
 
 // m-blocks per raster group: keep the group's A band (G * rows * K * 2 bytes) around 32 MB
@@ -926,8 +1051,7 @@ void launch_gemm_tc(const GemmArgs& g, cudaStream_t st) {
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at; cfg.numAttrs = g.pdl ? 1 : 0;
-    CUtensorMap tx = tb;  // the residual map (EPI_GATED_RES only; any valid map otherwise)
-    if (g.epi == EPI_GATED_RES) make_tmap_f32(&tx, g.C, g.M, g.N, g.ldc);
+    const CUtensorMap tx = out_map(g, tb);
     if (BN2 == 160) {
       cfg.dynamicSmemBytes = Cfg2<160>::SMEM;
       cudaLaunchKernelEx(&cfg, gemm_tc2_kernel<false, 160>, ta, tb, tx, g, num_m, num_n, G2);
@@ -951,8 +1075,7 @@ void launch_gemm_tc(const GemmArgs& g, cudaStream_t st) {
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at; cfg.numAttrs = g.pdl ? 1 : 0;
-  CUtensorMap tx = tb;  // the residual map (EPI_GATED_RES only; any valid map otherwise)
-  if (g.epi == EPI_GATED_RES) make_tmap_f32(&tx, g.C, g.M, g.N, g.ldc);
+  const CUtensorMap tx = out_map(g, tb);
   if (wide) {
     cfg.dynamicSmemBytes = Cfg<256>::SMEM;
     cudaLaunchKernelEx(&cfg, gemm_tc_kernel<256>, ta, tb, tx, g, num_m, num_n, G);
@@ -987,10 +1110,10 @@ void launch_conv3x3_tc(const GemmArgs& g, cudaStream_t st) {
     const int tiles = num_m * num_n;
     const int clusters = tiles < g_num_sms / 2 ? tiles : g_num_sms / 2;
     if (BN2 == 160)
-      gemm_tc2_kernel<true, 160><<<2 * clusters, NUM_THREADS, Cfg2<160>::SMEM, st>>>(ta, tb2, tb2, g, num_m, num_n,
+      gemm_tc2_kernel<true, 160><<<2 * clusters, NUM_THREADS, Cfg2<160>::SMEM, st>>>(ta, tb2, out_map(g, tb2), g, num_m, num_n,
                                                                                   raster_group(num_m, 256, g.K));
     else
-      gemm_tc2_kernel<true, 256><<<2 * clusters, NUM_THREADS, Cfg2<256>::SMEM, st>>>(ta, tb2, tb2, g, num_m, num_n,
+      gemm_tc2_kernel<true, 256><<<2 * clusters, NUM_THREADS, Cfg2<256>::SMEM, st>>>(ta, tb2, out_map(g, tb2), g, num_m, num_n,
                                                                                   raster_group(num_m, 256, g.K));
     return;
   }
@@ -1002,9 +1125,9 @@ void launch_conv3x3_tc(const GemmArgs& g, cudaStream_t st) {
   const int grid = tiles < g_num_sms ? tiles : g_num_sms;
   const int G = raster_group(num_m, BM, g.K);
   if (wide)
-    gemm_tc_kernel<256, true><<<grid, NUM_THREADS, Cfg<256>::SMEM, st>>>(ta, tb, tb, g, num_m, num_n, G);
+    gemm_tc_kernel<256, true><<<grid, NUM_THREADS, Cfg<256>::SMEM, st>>>(ta, tb, out_map(g, tb), g, num_m, num_n, G);
   else
-    gemm_tc_kernel<128, true><<<grid, NUM_THREADS, Cfg<128>::SMEM, st>>>(ta, tb, tb, g, num_m, num_n, G);
+    gemm_tc_kernel<128, true><<<grid, NUM_THREADS, Cfg<128>::SMEM, st>>>(ta, tb, out_map(g, tb), g, num_m, num_n, G);
 }
 
 }  // namespace ig
