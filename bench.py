@@ -485,7 +485,8 @@ def cpu_baseline(d):
 
 def workload_config(d, args, world):
     """The workload (identical for our arm at every N and for the reference arm)."""
-    return {"workload": f"{d.name} ({d.L_img} img + {d.txt_len} txt tokens, 1024^2), 28-step flow schedule, "
+    res = d.grid_h * 16  # 8x VAE downsampling x 2x2 patches per token
+    return {"workload": f"{d.name} ({d.L_img} img + {d.txt_len} txt tokens, {res}x{res}), 28-step flow schedule, "
                         f"continuous batching max_batch {args.max_batch} per GPU (staggered steps, a finished "
                         f"request leaves and a new one joins), masks m~U[{args.mask_lo},{args.mask_hi}] "
                         f"({'rect/blob' if args.mask_kind == 'mixed' else 'blob'})",

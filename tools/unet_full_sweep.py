@@ -64,6 +64,7 @@ def main():
     ap.add_argument("--tier", default="device", choices=["device", "host"])
     ap.add_argument("--ms", default="0.01,0.05,0.1,0.2,0.3,0.5,0.8,1.0")
     ap.add_argument("--out", default=None)
+    ap.add_argument("--depth", type=int, default=2, help="copy-lane ring depth of each Transformer2D")
     ap.add_argument("--profile", action="store_true",
                     help="bracket the timed steps with cudaProfilerStart/Stop (ncu --profile-from-start off)")
     args = ap.parse_args()
@@ -72,7 +73,7 @@ def main():
     torch.cuda.set_device(0)
     W = [synth.make_unet_full_weights(u, device=dev, dtype=torch.bfloat16, names={n})[n].contiguous()
          for n, _, _ in synth.unet_full_weight_table(u)]  # drawn on the device (2.6 B parameters)
-    h = ig.ig_unet_create(ig.make_unet_desc(u), [t.data_ptr() for t in W], 0, args.batch, 2)
+    h = ig.ig_unet_create(ig.make_unet_desc(u), [t.data_ptr() for t in W], 0, args.batch, args.depth)
     sig = synth.flow_sigmas(N_SCHED)
     stream = torch.cuda.Stream()
     tl = synth.make_unet_latent(u, 10 ** 6).to(dev)
@@ -127,7 +128,8 @@ def main():
     if dense:
         for r in res:
             r["speedup_vs_dense"] = round(dense[0]["ms_per_step"] / r["ms_per_step"], 3)
-    out = {"model": u.name, "grid": u.grid, "batch": args.batch, "tier": args.tier, "template_s": round(t_tpl, 1),
+    out = {"model": u.name, "grid": u.grid, "batch": args.batch, "tier": args.tier, "depth": args.depth,
+           "template_s": round(t_tpl, 1),
            "note": "whole SDXL-shaped UNet at 1024^2 (latent 128x128x4): Transformer2Ds mask-aware on the "
                    "level's masked tokens (K/V + output caches), ResBlocks / resamplers / convs dense; "
                    "requests at distinct steps of one template; m=1.0 is the dense step", "sweep": res}
