@@ -448,32 +448,26 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         int mb, nb;
         tile_coords(t, num_m, num_n, G, mb, nb);
         const int m0 = mb * BM, n0 = nb * BN;
-        // implicit conv: the padded-input row of every run's first pixel at tap (0, 0), computed
-        // once per tile (64-bit divisions per k-block would bound the single producer thread)
-        int cbox = 1, cbase[16];
+        // implicit conv: the tile's 128 output pixels are 128 / min(W, 128) whole image rows (or
+        // one 128-pixel run of a wider row) of one image: (image, row, column) of its first pixel,
+        // once per tile
+        int cn = 0, cy = 0, cx = 0;
         if constexpr (CONV) {
-          const int W = g.conv_W, H = g.conv_H;
-          cbox = W < BM ? W : BM;
-          const long long HW = (long long)H * W;
-          for (int r = 0; r < BM / cbox; ++r) {
-            const long long p = (long long)m0 + r * cbox;
-            const long long n = p / HW, rem = p - n * HW;
-            const long long y = rem / W, x = rem - y * W;
-            cbase[r] = (int)(n * (H + 2) * (long long)(W + 2) + y * (W + 2) + x);
-          }
+          const long long HW = (long long)g.conv_H * g.conv_W;
+          cn = (int)(m0 / HW);
+          const int rem = (int)(m0 - cn * HW);
+          cy = rem / g.conv_W;
+          cx = rem - cy * g.conv_W;
         }
         int tap = 0, cb = 0;
         for (int kb = 0; kb < num_k; ++kb) {
           tc::mbar_wait(&empty[stage], phase ^ 1);
           tc::mbar_arrive_expect_tx(&full[stage], C::STAGE_BYTES);
           if constexpr (CONV) {
-            // k-block kb = (tap, 64-channel chunk); the tile's 128 output pixels are 128 / box
-            // runs of `box` consecutive pixels of one image row, each a contiguous run of the
-            // zero-padded input shifted by the tap: one TMA box per run
+            // k-block kb = (tap, 64-channel chunk): ONE 4-D box {64 channels, run, rows, 1} of the
+            // zero-padded input at the tap's offset (padded (y + dy, x + dx) = output (y, x) tap)
             const int dy = tap / 3, dx = tap - dy * 3;
-            const int shift = dy * (g.conv_W + 2) + dx;
-            for (int r = 0; r < BM / cbox; ++r)
-              tc::tma_load_2d(sA + stage * C::A_BYTES + r * cbox * 128, &tmA, &full[stage], cb * BK, cbase[r] + shift);
+            tc::tma_load_4d(sA + stage * C::A_BYTES, &tmA, &full[stage], cb * BK, cx + dx, cy + dy, cn);
             if (++cb == (g.conv_cin >> 6)) { cb = 0; ++tap; }
           } else {
             tc::tma_load_2d(sA + stage * C::A_BYTES, &tmA, &full[stage], kb * BK, m0);
@@ -673,17 +667,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         int mb, nb;
         tile_coords(t, num_m, num_n, G, mb, nb);
         const int m0 = mb * 256 + rank * 128, n0 = nb * BN + rank * (BN / 2);
-        int cbox = 1, cbase[16];  // implicit conv: runs of this CTA's 128 output pixels (see gemm_tc_kernel)
+        int cn = 0, cy = 0, cx = 0;  // implicit conv: first output pixel of this CTA's 128 (see gemm_tc_kernel)
         if constexpr (CONV) {
-          const int W = g.conv_W, H = g.conv_H;
-          cbox = W < 128 ? W : 128;
-          const long long HW = (long long)H * W;
-          for (int r = 0; r < 128 / cbox; ++r) {
-            const long long p = (long long)m0 + r * cbox;
-            const long long n = p / HW, rem = p - n * HW;
-            const long long y = rem / W, x = rem - y * W;
-            cbase[r] = (int)(n * (H + 2) * (long long)(W + 2) + y * (W + 2) + x);
-          }
+          const long long HW = (long long)g.conv_H * g.conv_W;
+          cn = (int)(m0 / HW);
+          const int rem = (int)(m0 - cn * HW);
+          cy = rem / g.conv_W;
+          cx = rem - cy * g.conv_W;
         }
         int tap = 0, cb = 0;
         for (int kb = 0; kb < num_k; ++kb) {
@@ -691,9 +681,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
           if (rank == 0) tc::mbar_arrive_expect_tx(&full[stage], 2 * C::STAGE_BYTES);
           if constexpr (CONV) {
             const int dy = tap / 3, dx = tap - dy * 3;
-            const int shift = dy * (g.conv_W + 2) + dx;
-            for (int r = 0; r < 128 / cbox; ++r)
-              tc::tma_load_2d_2sm(sA + stage * C::A_BYTES + r * cbox * 128, &tmA, &full[stage], cb * BK, cbase[r] + shift);
+            tc::tma_load_4d_2sm(sA + stage * C::A_BYTES, &tmA, &full[stage], cb * BK, cx + dx, cy + dy, cn);
             if (++cb == (g.conv_cin >> 6)) { cb = 0; ++tap; }
           } else {
             tc::tma_load_2d_2sm(sA + stage * C::A_BYTES, &tmA, &full[stage], kb * BK, m0);
@@ -915,6 +903,28 @@ bool make_tmap_f32(CUtensorMap* m, const void* ptr, long long rows, long long co
   cache.emplace(k, *m);
   return true;
 }
+// implicit-conv A operand: the zero-padded NHWC input as a 4-D map {C_in, W + 2, H + 2, N} with a
+// {64, min(W, 128), 128 / min(W, 128), 1} box: a tile's 128 output pixels at one tap and one
+// 64-channel chunk in ONE TMA load (rows of the box skip the 2 padding pixels between image rows)
+bool make_tmap_conv(CUtensorMap* m, const void* ptr, long long n, int H, int W, int cin) {
+  thread_local std::unordered_map<TmapKey, CUtensorMap, TmapHash> cache;
+  const TmapKey k{ptr, n * (H + 2), (long long)(W + 2), cin, -4};
+  auto it = cache.find(k);
+  if (it != cache.end()) { *m = it->second; return true; }
+  const int bw = W < BM ? W : BM;
+  cuuint64_t dims[4] = {(cuuint64_t)cin, (cuuint64_t)(W + 2), (cuuint64_t)(H + 2), (cuuint64_t)n};
+  cuuint64_t strides[3] = {(cuuint64_t)cin * 2, (cuuint64_t)cin * 2 * (W + 2), (cuuint64_t)cin * 2 * (W + 2) * (H + 2)};
+  cuuint32_t box[4] = {64, (cuuint32_t)bw, (cuuint32_t)(BM / bw), 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(ptr), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return false;
+  if (cache.size() > 8192) cache.clear();
+  cache.emplace(k, *m);
+  return true;
+}
+
 // the output map of the TMA epilogues: fp32 32 x 32 boxes (gated residual reduce-add, fp32
 // stores); `fallback` (any valid map) otherwise
 CUtensorMap out_map(const GemmArgs& g, const CUtensorMap& fallback) {
@@ -1039,11 +1049,9 @@ bool conv3x3_tc_supported(int H, int W, int cin) {
 void launch_conv3x3_tc(const GemmArgs& g, cudaStream_t st) {
   if (g.M <= 0 || g.N <= 0) return;
   init_driver();
-  const int box = g.conv_W < BM ? g.conv_W : BM;
   const long long images = g.M / ((long long)g.conv_H * g.conv_W);
-  const long long prows = images * (g.conv_H + 2) * (long long)(g.conv_W + 2);
   CUtensorMap ta, tb;
-  make_tmap(&ta, g.A, prows, g.conv_cin, g.conv_cin, box);  // padded input rows, box of one run
+  make_tmap_conv(&ta, g.A, images, g.conv_H, g.conv_W, g.conv_cin);  // padded input, 4-D box per tile
   // C_out a multiple of 256 (1280): 2-CTA 256 x 256 tiles (half the B operand per SM), like the
   // projections; else 128 x 128 one-CTA tiles (C_out 320 / 640: no half-empty 256-column tile)
   static const bool conv_1cta = getenv("IG_CONV_1CTA") != nullptr;  // A/B switch
