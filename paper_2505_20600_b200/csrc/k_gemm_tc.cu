@@ -600,9 +600,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 // traffic versus the 1-CTA 128 x 256 tile.  Only the leader CTA issues MMAs; commits are
 // multicast to both CTAs; each CTA's epilogue warps drain their own TMEM (rows 128r..128r+127)
 // and release the accumulator to the leader with a cluster-scope mbarrier arrive.
-// BN = 256, or 160 for N = 160 k (320 / 640 / 1280-wide UNet projections and convolutions):
-// narrower tiles cut the N padding and the last-wave quantisation when a 256-wide grid has only
-// 2-3 waves (launch_gemm_tc picks the tile by the wave count; per-element math unchanged).
+// BN: tile width (256; a 256 x 160 variant measured no faster than 256 even where it needs fewer
+// wave-cycles — its N = 160 MMAs cost about as much as N = 256 — and was removed)
 template <int BN>
 struct Cfg2 {
   static constexpr int STAGES = BN == 256 ? 6 : 7;
@@ -839,8 +838,6 @@ void init_driver() {
     cudaFuncSetAttribute(gemm_tc_kernel<128, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<128>::SMEM);
     cudaFuncSetAttribute(gemm_tc2_kernel<false, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg2<256>::SMEM);
     cudaFuncSetAttribute(gemm_tc2_kernel<true, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg2<256>::SMEM);
-    cudaFuncSetAttribute(gemm_tc2_kernel<false, 160>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg2<160>::SMEM);
-    cudaFuncSetAttribute(gemm_tc2_kernel<true, 160>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg2<160>::SMEM);
     g_two_cta = getenv("IG_GEMM_1CTA") == nullptr;
   });
 }
@@ -945,21 +942,6 @@ int raster_group(int num_m, int rows, int K) {
   return (int)G;
 }
 
-// 2-CTA tile width: 160 when it needs fewer (waves x width) tensor cycles than 256 — a 256-wide
-// grid of only a few waves loses its partial last wave, and N = 320 / 640 pads a 256 tile by a
-// third (a 10% margin keeps 256's lower per-flop B traffic and epilogue overhead otherwise).
-// Tile shape only: every output is still one full-K accumulation in the same K order.
-int tile2_width(long long M, long long N, bool narrow_ok) {
-  static const bool no160 = getenv("IG_GEMM_NO_BN160") != nullptr;  // A/B switch
-  if (!narrow_ok || no160) return 256;
-  const long long num_m = (M + 255) / 256, slots = g_num_sms / 2;
-  auto cost = [&](long long bn) {
-    const long long tiles = num_m * ((N + bn - 1) / bn);
-    return ((tiles + slots - 1) / slots) * bn;
-  };
-  return 10 * cost(160) < 9 * cost(256) ? 160 : 256;
-}
-
 bool gemm_tc_supported(const GemmArgs& g) {
   auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
   if (!al16(g.A) || !al16(g.B) || (g.lda & 7) || (g.ldb & 7) || (g.K & 7)) return false;
@@ -992,7 +974,7 @@ void launch_gemm_tc(const GemmArgs& g, cudaStream_t st) {
   const long long tiles2 = (long long)((g.M + 255) / 256) * ((g.N + 255) / 256);
   if (!no_small && wide && g.epi != EPI_GEGLU && tiles2 * 4 < g_num_sms) wide = false;
   if (wide && g_two_cta && g.M > 128) {  // 2-CTA 256 x BN tiles
-    const int BN2 = tile2_width(g.M, g.N, g.epi != EPI_QKV && g.epi != EPI_GEGLU);
+    constexpr int BN2 = 256;
     CUtensorMap ta, tb;
     make_tmap(&ta, g.A, g.M, g.K, g.lda, 128);
     make_tmap(&tb, g.B, g.N, g.K, g.ldb, BN2 / 2);
@@ -1007,13 +989,8 @@ void launch_gemm_tc(const GemmArgs& g, cudaStream_t st) {
     at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at; cfg.numAttrs = g.pdl ? 1 : 0;
     const CUtensorMap tx = out_map(g, tb);
-    if (BN2 == 160) {
-      cfg.dynamicSmemBytes = Cfg2<160>::SMEM;
-      cudaLaunchKernelEx(&cfg, gemm_tc2_kernel<false, 160>, ta, tb, tx, g, num_m, num_n, G2);
-    } else {
-      cfg.dynamicSmemBytes = Cfg2<256>::SMEM;
-      cudaLaunchKernelEx(&cfg, gemm_tc2_kernel<false, 256>, ta, tb, tx, g, num_m, num_n, G2);
-    }
+    cfg.dynamicSmemBytes = Cfg2<256>::SMEM;
+    cudaLaunchKernelEx(&cfg, gemm_tc2_kernel<false, 256>, ta, tb, tx, g, num_m, num_n, G2);
     return;
   }
   const int BN = wide ? 256 : 128;
@@ -1055,19 +1032,18 @@ void launch_conv3x3_tc(const GemmArgs& g, cudaStream_t st) {
   // C_out a multiple of 256 (1280): 2-CTA 256 x 256 tiles (half the B operand per SM), like the
   // projections; else 128 x 128 one-CTA tiles (C_out 320 / 640: no half-empty 256-column tile)
   static const bool conv_1cta = getenv("IG_CONV_1CTA") != nullptr;  // A/B switch
-  if (!conv_1cta && g_two_cta && (g.N % 256 == 0 || g.N % 160 == 0) && g.M > 128) {
-    const int BN2 = tile2_width(g.M, g.N, true);
+  // C_out >= 256: 2-CTA 256 x 256 tiles, the last one partial for C_out = 320 / 640 (measured:
+  // as fast as or faster than 256 x 160 tiles, whose N = 160 MMAs cost about as much as N = 256
+  // — ncu cycles in profiles/r02_bn160_ab_cycles.txt — and than 128 x 128 one-CTA tiles)
+  if (!conv_1cta && g_two_cta && g.N >= 256 && g.M > 128) {
+    constexpr int BN2 = 256;
     CUtensorMap tb2;
     make_tmap(&tb2, g.B, g.N, g.K, g.ldb, BN2 / 2);
     const int num_m = (g.M + 255) / 256, num_n = (g.N + BN2 - 1) / BN2;
     const int tiles = num_m * num_n;
     const int clusters = tiles < g_num_sms / 2 ? tiles : g_num_sms / 2;
-    if (BN2 == 160)
-      gemm_tc2_kernel<true, 160><<<2 * clusters, NUM_THREADS, Cfg2<160>::SMEM, st>>>(ta, tb2, out_map(g, tb2), g, num_m, num_n,
-                                                                                  raster_group(num_m, 256, g.K));
-    else
-      gemm_tc2_kernel<true, 256><<<2 * clusters, NUM_THREADS, Cfg2<256>::SMEM, st>>>(ta, tb2, out_map(g, tb2), g, num_m, num_n,
-                                                                                  raster_group(num_m, 256, g.K));
+    gemm_tc2_kernel<true, 256><<<2 * clusters, NUM_THREADS, Cfg2<256>::SMEM, st>>>(ta, tb2, out_map(g, tb2), g, num_m, num_n,
+                                                                                raster_group(num_m, 256, g.K));
     return;
   }
   const bool wide = g.N >= 256 && g.N % 256 == 0;
