@@ -30,7 +30,7 @@ constexpr int NUM_THREADS = 256;
 constexpr int EPI_RED_BYTES = 4 * 2 * 32 * 32 * 4;
 template <int BN>
 struct Cfg {
-  static constexpr int STAGES = BN == 256 ? 4 : 6;
+  static constexpr int STAGES = BN == 256 ? 4 : (BN == 128 ? 6 : 8);
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
@@ -834,6 +834,7 @@ void init_driver() {
     cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
     cudaFuncSetAttribute(gemm_tc_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<256>::SMEM);
     cudaFuncSetAttribute(gemm_tc_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<128>::SMEM);
+    cudaFuncSetAttribute(gemm_tc_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<64>::SMEM);
     cudaFuncSetAttribute(gemm_tc_kernel<256, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<256>::SMEM);
     cudaFuncSetAttribute(gemm_tc_kernel<128, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<128>::SMEM);
     cudaFuncSetAttribute(gemm_tc2_kernel<false, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg2<256>::SMEM);
@@ -993,7 +994,15 @@ void launch_gemm_tc(const GemmArgs& g, cudaStream_t st) {
     cudaLaunchKernelEx(&cfg, gemm_tc2_kernel<false, 256>, ta, tb, tx, g, num_m, num_n, G2);
     return;
   }
-  const int BN = wide ? 256 : 128;
+  // Still fewer 128 x 128 tiles than half the SMs (single-request SD3 out-projections / fc2:
+  // 36-48 tiles of K = 1536-6144, one long k-loop each on a third of the GPU): 128 x 64 tiles
+  // double the CTAs.  Tile shape only (same full-K order per output), so batch invariance holds;
+  // the QKV / GEGLU epilogues need whole heads / paired halves (>= 128 columns).
+  static const bool no_bn64 = getenv("IG_GEMM_NO_BN64") != nullptr;  // A/B switch
+  const long long tiles1 = (long long)((g.M + BM - 1) / BM) * ((g.N + 127) / 128);
+  const bool narrow = !wide && !no_bn64 && !no_small && g.epi != EPI_QKV && g.epi != EPI_GEGLU &&
+                      tiles1 * 2 <= g_num_sms;
+  const int BN = wide ? 256 : (narrow ? 64 : 128);
   CUtensorMap ta, tb;
   make_tmap(&ta, g.A, g.M, g.K, g.lda, BM);
   make_tmap(&tb, g.B, g.N, g.K, g.ldb, BN);
@@ -1011,6 +1020,9 @@ void launch_gemm_tc(const GemmArgs& g, cudaStream_t st) {
   if (wide) {
     cfg.dynamicSmemBytes = Cfg<256>::SMEM;
     cudaLaunchKernelEx(&cfg, gemm_tc_kernel<256>, ta, tb, tx, g, num_m, num_n, G);
+  } else if (narrow) {
+    cfg.dynamicSmemBytes = Cfg<64>::SMEM;
+    cudaLaunchKernelEx(&cfg, gemm_tc_kernel<64>, ta, tb, tx, g, num_m, num_n, G);
   } else {
     cfg.dynamicSmemBytes = Cfg<128>::SMEM;
     cudaLaunchKernelEx(&cfg, gemm_tc_kernel<128>, ta, tb, tx, g, num_m, num_n, G);

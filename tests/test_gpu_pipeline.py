@@ -314,12 +314,13 @@ def test_debug_dump_kv_is_the_positional_merge():
 @pytest.mark.parametrize("M_small,N,K,epi,M_big", [(300, 3072, 3072, 0, 14720), (100, 21504, 3072, 1, 14720),
                                                   (700, 3072, 12288, 2, 14720), (60, 9216, 3072, 0, 14720),
                                                   (300, 1280, 1280, 0, 8192), (700, 1280, 5120, 2, 8192),
-                                                  (1000, 640, 640, 1, 32768)])
+                                                  (1000, 640, 640, 1, 32768), (449, 1536, 6144, 2, 14720),
+                                                  (300, 1536, 1536, 0, 8192)])
 def test_gemm_rows_bitwise_across_tile_paths(M_small, N, K, epi, M_big):
     """The same A rows through a small-M GEMM (1-CTA 128x128 tiles when the 2-CTA grid would be
-    under SMs/4, or 128x256 tiles at M <= 128) and inside a large-M GEMM (2-CTA 256x256 tiles, or
-    256x160 tiles for the UNet widths N = 640 / 1280 at few waves) give bitwise equal outputs:
-    every output is one full-K accumulation in the same K order."""
+    under SMs/4, 128x64 tiles when even those are under SMs/2 — the single-request SD3 shapes —
+    or 128x256 tiles at M <= 128) and inside a large-M GEMM (2-CTA 256x256 tiles) give bitwise
+    equal outputs: every output is one full-K accumulation in the same K order."""
     g = torch.Generator(device="cuda").manual_seed(N + K + epi)
     A = (torch.randn(M_big, K, device="cuda", generator=g) / 4).bfloat16()
     B = (torch.randn(N, K, device="cuda", generator=g) / K ** 0.5).bfloat16()
