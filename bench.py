@@ -830,6 +830,7 @@ def main():
         out["roofline"] = {"bound": "tensor", "kernel": "gemm_tc2/gemm_tc (tcgen05 bf16)", "achieved": round(gemm_tf, 1),
                            "peak": pk_sus, "unit": "TFLOP/s", "frac": round(gemm_tf / pk_sus, 4),
                            "traffic": traffic.get("dram_bytes_per_launch"),
+                           "traffic_algorithmic": traffic.get("algorithmic_bytes_per_launch"),
                            "traffic_note": traffic.get("note"),
                            "peak_kind": f"bf16 sustained ({pk_src}; kernels timed inside a seconds-long step)",
                            "frac_of_burst": round(gemm_tf / pk_burst, 4),
