@@ -57,6 +57,28 @@ ig_status ig_op_conv3x3(const void* x_padded, int n_img, int H, int W, int cin, 
  * if src is not pinned host memory. */
 ig_status ig_stage_input(void* dst, const void* src, size_t bytes, void* stream);
 
+/* Process-wide tuning knobs of libig (one struct instead of scattered switches).  Every field is
+ * a 0/1 flag unless stated; defaults are the measured-best settings (profiles/).
+ * The first ig_tuning_get / ig_tuning_set or libig launch seeds the struct from the environment
+ * (the variable named per field, for A/B tools that cannot call the ABI); ig_tuning_set replaces
+ * it.  Changes apply to launches enqueued after the call; CUDA graphs of steps captured earlier
+ * keep the configuration they were captured with.  No field changes results except precise_gelu
+ * (a different GELU approximation) — tile shapes and launch mechanics are batch-invariant. */
+typedef struct ig_tuning {
+  int pdl;              /* programmatic dependent launch of GEMMs after a kernel (1; env IG_NO_PDL) */
+  int copy_thread;      /* copy-lane enqueues on their own host thread (1; env IG_NO_COPY_THREAD) */
+  int load_dedupe;      /* host-tier load dedupe across requests on one (template, step) (1; IG_NO_DEDUPE) */
+  int cross_kv_overlap; /* UNet: next block's cross-attention K/V GEMM on a side stream (1; IG_NO_XOVERLAP) */
+  int gemm_two_cta;     /* 2-CTA 256x256 tiles for large GEMMs and convs (1; IG_GEMM_1CTA) */
+  int gemm_small_tiles; /* 128x128 one-CTA tiles below SMs/4 2-CTA tiles (1; IG_GEMM_NO_SMALL) */
+  int gemm_bn64;        /* 128x64 tiles below SMs/2 128x128 tiles (1; IG_GEMM_NO_BN64) */
+  int conv_two_cta;     /* implicit conv: 2-CTA tiles for C_out >= 256 (1; IG_CONV_1CTA) */
+  int precise_gelu;     /* debug: libm erf / tanh GELU instead of the MUFU forms (0; IG_PRECISE_GELU) */
+  int op_repeat;        /* ig_op_attention: launches per call, benchmarking aid (1; IG_OP_REPEAT=n) */
+} ig_tuning;
+ig_status ig_tuning_get(ig_tuning* out);       /* IG_EINVAL if out is NULL */
+ig_status ig_tuning_set(const ig_tuning* t);   /* IG_EINVAL if t is NULL or op_repeat < 1 */
+
 #ifdef __cplusplus
 }
 #endif

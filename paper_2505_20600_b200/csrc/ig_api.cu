@@ -513,14 +513,13 @@ static void CUDART_CB unpin_cb(void* p) {
 static bool g_tc_gemm = true;   // tcgen05 GEMM for bf16 (set false only by IG_TEST_SIMT)
 static bool g_tc_attn = true;
 
-static bool g_pdl = getenv("IG_NO_PDL") == nullptr;  // A/B switch
 
 static void gemm(ig_ctx* ctx, const GemmArgs& g, cudaStream_t st) {
   if (g.M <= 0 || g.N <= 0) return;
   ctx->stats.kernel_launches++;
   ProfScope ps(ctx, st, IG_K_GEMM, 2.0 * g.M * g.N * g.K, 0.0, g.M, g.N, g.K, g.epi);
   GemmArgs g2 = g;
-  g2.pdl = g_pdl && !ctx->pdl_block && !ctx->prof;  // (profiling brackets launches with events)
+  g2.pdl = ig_tuning_ref().pdl && !ctx->pdl_block && !ctx->prof;  // (profiling brackets launches with events)
   ctx->pdl_block = false;
   if (ctx->d.dtype == IG_F32) launch_gemm_simt<float>(g, st);
   else if (g_tc_gemm && gemm_tc_supported(g)) launch_gemm_tc(g2, st);
@@ -1854,7 +1853,7 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
   }
   CopyPlan plan;
   {
-    static const bool no_dedupe = getenv("IG_NO_DEDUPE") != nullptr;  // A/B switch
+    const bool no_dedupe = !ig_tuning_ref().load_dedupe;
     auto dedupable = [&](int q) {
       const ig_cache* c = sr[q].use_cache ? sr[q].r->cache : nullptr;
       return c && c->tier == IG_CACHE_HOST && !c->fp8 && ctx->o.copy_mode == 1;
@@ -2130,7 +2129,7 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
   // copy lane on its own host thread for host-tier caches (DMA back-pressure), inline otherwise
   // and whenever the main thread itself touches the copy stream (recording, capture, profiling)
   {
-    static const bool no_lane = getenv("IG_NO_COPY_THREAD") != nullptr;  // A/B switch
+    const bool no_lane = !ig_tuning_ref().copy_thread;
     bool any_host = false;
     for (auto& s2 : sr) any_host |= s2.use_cache && s2.r->cache->tier == IG_CACHE_HOST;
     ctx->lane_on = !no_lane && any_host && !ctx->prof && !ctx->capturing && !record && !rng.X_in;
@@ -2242,8 +2241,7 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
     g.B = B; g.ldb = K; g.bias = bias;
     g.M = r1 - r0; g.N = N; g.K = K; g.epi = epi; g.out_f32 = out_f32;
     g.ri = ctx->ri; g.ri_off = r0;
-    static const bool precise_gelu = getenv("IG_PRECISE_GELU") != nullptr;  // debug switch, read once
-    g.precise_gelu = precise_gelu;
+    g.precise_gelu = ig_tuning_ref().precise_gelu != 0;
     if (epi == EPI_GATED_RES) {
       g.C = (float*)Cp + (long long)r0 * ldc; g.gate = gate; g.gate_ld = mld;
     } else {
@@ -2452,7 +2450,7 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
   };
   // fused (bf16) path: block b's cross K/V live in arena half b % 2 and are produced on the side
   // stream one block ahead (xover); parity mode: half 0, on the compute stream
-  static const bool no_xover = getenv("IG_NO_XOVERLAP") != nullptr;  // A/B switch
+  const bool no_xover = !ig_tuning_ref().cross_kv_overlap;
   const bool xover = unet && fused_qkv && !no_xover;
   const long long xhalf = (long long)ctx->o.max_batch * 2 * Lc * H;  // elements per arena half
   auto xkv_of = [&](int b) { return (char*)ctx->xkv + (xover ? (long long)(b & 1) * xhalf * es : 0); };
@@ -2930,8 +2928,7 @@ extern "C" ig_status ig_op_attention(int dtype, const void* Q, long long ldq, vo
   for (auto& s : hs) qrows = std::max(qrows, s.q_start + s.q_len);
   a.q_rows = qrows;
   a.scale = 1.0f / sqrtf((float)head_dim);
-  const char* rep_env = getenv("IG_OP_REPEAT");  // benchmarking aid: launch the kernel N times
-  const int rep = rep_env ? std::max(1, atoi(rep_env)) : 1;
+  const int rep = ig_tuning_ref().op_repeat;  // benchmarking aid: launch the kernel N times
   for (int it = 0; it < rep; ++it) {
     if (dtype == IG_F32) launch_attn_simt<float>(a, st);
     else if (dtype == IG_BF16) {
@@ -2988,5 +2985,47 @@ extern "C" ig_status ig_copy(void* dst, const void* src, size_t bytes, void* str
   cudaStream_t st = (cudaStream_t)stream;
   CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, st));
   CUDA_TRY(cudaStreamSynchronize(st));
+  return IG_OK;
+}
+
+// ---- process-wide tuning (include/ig_ops.h) ------------------------------------------------
+static std::mutex g_tuning_mu;
+static ig_tuning g_tuning;
+static std::atomic<bool> g_tuning_init{false};
+static void tuning_seed_locked() {
+  if (g_tuning_init.load(std::memory_order_relaxed)) return;
+  auto off = [](const char* v) { return getenv(v) != nullptr ? 0 : 1; };
+  g_tuning.pdl = off("IG_NO_PDL");
+  g_tuning.copy_thread = off("IG_NO_COPY_THREAD");
+  g_tuning.load_dedupe = off("IG_NO_DEDUPE");
+  g_tuning.cross_kv_overlap = off("IG_NO_XOVERLAP");
+  g_tuning.gemm_two_cta = off("IG_GEMM_1CTA");
+  g_tuning.gemm_small_tiles = off("IG_GEMM_NO_SMALL");
+  g_tuning.gemm_bn64 = off("IG_GEMM_NO_BN64");
+  g_tuning.conv_two_cta = off("IG_CONV_1CTA");
+  g_tuning.precise_gelu = getenv("IG_PRECISE_GELU") != nullptr ? 1 : 0;
+  const char* rep = getenv("IG_OP_REPEAT");
+  g_tuning.op_repeat = rep ? std::max(1, atoi(rep)) : 1;
+  g_tuning_init.store(true, std::memory_order_release);
+}
+const ig_tuning& ig_tuning_ref() {
+  if (!g_tuning_init.load(std::memory_order_acquire)) {
+    std::lock_guard<std::mutex> lk(g_tuning_mu);
+    tuning_seed_locked();
+  }
+  return g_tuning;
+}
+extern "C" ig_status ig_tuning_get(ig_tuning* out) {
+  if (!out) return set_err(IG_EINVAL, "ig_tuning_get: null");
+  std::lock_guard<std::mutex> lk(g_tuning_mu);
+  tuning_seed_locked();
+  *out = g_tuning;
+  return IG_OK;
+}
+extern "C" ig_status ig_tuning_set(const ig_tuning* t) {
+  if (!t || t->op_repeat < 1) return set_err(IG_EINVAL, "ig_tuning_set: null or op_repeat < 1");
+  std::lock_guard<std::mutex> lk(g_tuning_mu);
+  g_tuning = *t;
+  g_tuning_init.store(true, std::memory_order_release);
   return IG_OK;
 }

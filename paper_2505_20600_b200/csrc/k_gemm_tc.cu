@@ -18,6 +18,7 @@
 #include <unordered_map>
 #include <cstdlib>
 #include "kernels.h"
+#include "ig_internal.h"
 #include "tc_common.cuh"
 
 namespace ig {
@@ -821,7 +822,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 std::once_flag g_encode_once;
 int g_num_sms = 0;
-bool g_two_cta = true;
 
 void init_driver() {
   std::call_once(g_encode_once, [] {
@@ -839,7 +839,6 @@ void init_driver() {
     cudaFuncSetAttribute(gemm_tc_kernel<128, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<128>::SMEM);
     cudaFuncSetAttribute(gemm_tc2_kernel<false, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg2<256>::SMEM);
     cudaFuncSetAttribute(gemm_tc2_kernel<true, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg2<256>::SMEM);
-    g_two_cta = getenv("IG_GEMM_1CTA") == nullptr;
   });
 }
 
@@ -971,10 +970,11 @@ void launch_gemm_tc(const GemmArgs& g, cudaStream_t st) {
   // or low-mask-ratio GEMMs): 128 x 128 one-CTA tiles put 4x as many SMs to work.  Only the
   // tile shape changes — every output is still one full-K accumulation in the same K order —
   // so results do not depend on the choice (batch invariance holds).
-  static const bool no_small = getenv("IG_GEMM_NO_SMALL") != nullptr;  // A/B switch
+  const ig_tuning& tun = ig_tuning_ref();
+  const bool no_small = !tun.gemm_small_tiles;
   const long long tiles2 = (long long)((g.M + 255) / 256) * ((g.N + 255) / 256);
   if (!no_small && wide && g.epi != EPI_GEGLU && tiles2 * 4 < g_num_sms) wide = false;
-  if (wide && g_two_cta && g.M > 128) {  // 2-CTA 256 x BN tiles
+  if (wide && tun.gemm_two_cta && g.M > 128) {  // 2-CTA 256 x BN tiles
     constexpr int BN2 = 256;
     CUtensorMap ta, tb;
     make_tmap(&ta, g.A, g.M, g.K, g.lda, 128);
@@ -998,7 +998,7 @@ void launch_gemm_tc(const GemmArgs& g, cudaStream_t st) {
   // 36-48 tiles of K = 1536-6144, one long k-loop each on a third of the GPU): 128 x 64 tiles
   // double the CTAs.  Tile shape only (same full-K order per output), so batch invariance holds;
   // the QKV / GEGLU epilogues need whole heads / paired halves (>= 128 columns).
-  static const bool no_bn64 = getenv("IG_GEMM_NO_BN64") != nullptr;  // A/B switch
+  const bool no_bn64 = !tun.gemm_bn64;
   const long long tiles1 = (long long)((g.M + BM - 1) / BM) * ((g.N + 127) / 128);
   const bool narrow = !wide && !no_bn64 && !no_small && g.epi != EPI_QKV && g.epi != EPI_GEGLU &&
                       tiles1 * 2 <= g_num_sms;
@@ -1043,11 +1043,12 @@ void launch_conv3x3_tc(const GemmArgs& g, cudaStream_t st) {
   make_tmap_conv(&ta, g.A, images, g.conv_H, g.conv_W, g.conv_cin);  // padded input, 4-D box per tile
   // C_out a multiple of 256 (1280): 2-CTA 256 x 256 tiles (half the B operand per SM), like the
   // projections; else 128 x 128 one-CTA tiles (C_out 320 / 640: no half-empty 256-column tile)
-  static const bool conv_1cta = getenv("IG_CONV_1CTA") != nullptr;  // A/B switch
+  const ig_tuning& tun = ig_tuning_ref();
+  const bool conv_1cta = !tun.conv_two_cta;
   // C_out >= 256: 2-CTA 256 x 256 tiles, the last one partial for C_out = 320 / 640 (measured:
   // as fast as or faster than 256 x 160 tiles, whose N = 160 MMAs cost about as much as N = 256
   // — ncu cycles in profiles/r02_bn160_ab_cycles.txt — and than 128 x 128 one-CTA tiles)
-  if (!conv_1cta && g_two_cta && g.N >= 256 && g.M > 128) {
+  if (!conv_1cta && tun.gemm_two_cta && g.N >= 256 && g.M > 128) {
     constexpr int BN2 = 256;
     CUtensorMap tb2;
     make_tmap(&tb2, g.B, g.N, g.K, g.ldb, BN2 / 2);

@@ -28,6 +28,7 @@ EXPORTS = ["ig_weight_count", "ig_ctx_create", "ig_ctx_destroy", "ig_cache_creat
            "ig_set_plan", "ig_last_plan", "ig_debug_set", "ig_debug_dump_kv",
            "ig_mask_build_host", "ig_stage_input", "ig_cache_template_into", "ig_cache_bytes",
            "ig_cache_attach", "ig_cache_export", "ig_cache_import", "ig_record_step",
+           "ig_tuning_get", "ig_tuning_set",
            "ig_unet_weight_count", "ig_unet_create", "ig_unet_destroy", "ig_unet_mask_build",
            "ig_unet_mask_free", "ig_unet_template", "ig_unet_cache_free", "ig_unet_step", "ig_unet_last_stats",
            "ig_op_conv3x3", "ig_plan_copy_groups"]
@@ -95,6 +96,14 @@ class ig_prof_entry(ctypes.Structure):
                 ("flops", ctypes.c_double), ("bytes", ctypes.c_double)]
 
 
+
+class ig_tuning(ctypes.Structure):
+    """include/ig_ops.h ig_tuning: process-wide libig knobs (see the header for each field)."""
+    _fields_ = [(n, ctypes.c_int) for n in ("pdl", "copy_thread", "load_dedupe", "cross_kv_overlap",
+                                            "gemm_two_cta", "gemm_small_tiles", "gemm_bn64", "conv_two_cta",
+                                            "precise_gelu", "op_repeat")]
+
+
 def lib():
     """Load libig.so (in-tree).  Raises if it is missing: there is no other path."""
     global _lib
@@ -139,6 +148,8 @@ def lib():
         L.ig_debug_set.argtypes = [vp, i, ll]
         L.ig_mask_build_host.argtypes = [vp, vp, vp, P(vp), P(i)]
         L.ig_stage_input.argtypes = [vp, vp, ctypes.c_size_t, vp]
+        L.ig_tuning_get.argtypes = [P(ig_tuning)]
+        L.ig_tuning_set.argtypes = [P(ig_tuning)]
         L.ig_cache_template_into.argtypes = [vp, vp, vp, vp, P(ctypes.c_float), i, vp, vp]
         L.ig_cache_bytes.argtypes = [vp, i, P(ctypes.c_size_t)]
         L.ig_cache_attach.argtypes = [vp, i, vp, ctypes.c_size_t, P(vp)]
@@ -476,3 +487,13 @@ def ig_unet_last_stats(u: int) -> dict:
 def ig_op_conv3x3(x_padded: int, n_img: int, H: int, W: int, cin: int, w: int, bias: int, cout: int, y: int,
                   stream: int = 0):
     _check(lib().ig_op_conv3x3(x_padded, n_img, H, W, cin, w, bias or None, cout, y, stream))
+
+
+def ig_tuning_get() -> "ig_tuning":
+    t = ig_tuning()
+    _check(lib().ig_tuning_get(ctypes.byref(t)))
+    return t
+
+
+def ig_tuning_set(t: "ig_tuning"):
+    _check(lib().ig_tuning_set(ctypes.byref(t)))

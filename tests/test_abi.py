@@ -75,3 +75,23 @@ def test_unet_desc_passes_host_validation(name):
 def test_unet_weight_count_matches_table(name):
     u = synth.UNET_FULL[name]
     assert ig.ig_unet_weight_count(ig.make_unet_desc(u)) == len(synth.unet_full_weight_table(u))
+
+
+def test_tuning_struct_roundtrip_without_gpu():
+    """ig_tuning (include/ig_ops.h): defaults are the measured-best settings, set/get round-trips,
+    op_repeat < 1 is rejected; no CUDA call is involved."""
+    t0 = ig.ig_tuning_get()
+    names = [f for f, _ in ig.ig_tuning._fields_]
+    assert ctypes.sizeof(ig.ig_tuning) == 4 * len(names)
+    t = ig.ig_tuning_get()
+    t.gemm_bn64 = 0
+    t.op_repeat = 3
+    ig.ig_tuning_set(t)
+    got = ig.ig_tuning_get()
+    assert got.gemm_bn64 == 0 and got.op_repeat == 3
+    bad = ig.ig_tuning_get()
+    bad.op_repeat = 0
+    with pytest.raises(Exception):
+        ig.ig_tuning_set(bad)
+    ig.ig_tuning_set(t0)
+    assert [getattr(ig.ig_tuning_get(), n) for n in names] == [getattr(t0, n) for n in names]
