@@ -457,22 +457,70 @@ def test_fp8_y_and_hybrid_caches(model, kv_blocks, tier):
     m.close()
 
 
-def test_fp8_hybrid_template_recording_runs():
-    """ig_cache_template on an FP8 hybrid ctx records quantized K/V and Y planes; an edit from the
-    template's own state then stays close to the dense trajectory on the masked rows (FP8
-    rounding of the cached planes is the only difference)."""
+def _e4m3_to_f32(b: np.ndarray) -> np.ndarray:
+    """OCP e4m3 (bias 7, no infinities; 0x7f / 0xff NaN) -> float32, written from the format."""
+    b = b.astype(np.int32)
+    sgn = np.where(b & 0x80, -1.0, 1.0)
+    e, m = (b >> 3) & 0xF, b & 0x7
+    val = np.where(e == 0, m / 8.0 * 2.0 ** -6, (1.0 + m / 8.0) * 2.0 ** (e.astype(np.float64) - 7))
+    val = np.where((b & 0x7F) == 0x7F, np.nan, val)
+    return (sgn * val).astype(np.float32)
+
+
+def _bf16_rne(x: np.ndarray) -> np.ndarray:
+    u = np.asarray(x, np.float32).view(np.uint32).astype(np.uint64)
+    u = (u + 0x7FFF + ((u >> 16) & 1)) & 0xFFFF0000
+    return u.astype(np.uint32).view(np.float32)
+
+
+def test_fp8_hybrid_template_recording_vs_oracle():
+    """ig_cache_template on an FP8 hybrid ctx (include/ig.h cache_fp8 + cache_y + cache_kv_blocks):
+    the recorded planes, read back and dequantized as the header defines (e4m3 data planes, then
+    fp32 scales per (token, head) in plane order; x' = bf16(q * scale)), (1) match the oracle's
+    dense template (unet_cache_template) within e4m3 rounding, and (2) drive the GPU edit step to
+    the oracle's Y-variant step (unet_edit_step_y) on those same planes within the bf16 bar."""
+    from gpu_util import n_planes, split_hybrid
+    import ctypes
     d = synth.UNET_SMALL
-    m = Model(d, ig.IG_BF16, opts=ig.ig_ctx_opts(2, 0, 2, 1, 0, 1, 1, 1))
+    kv_blocks = 1
+    m = Model(d, ig.IG_BF16, opts=ig.ig_ctx_opts(2, 0, 2, 1, 0, 1, 1, kv_blocks))
+    W = m.host_weights()
     mask = synth.blob_mask_count(d, 70, np.random.default_rng(91))
     rq = Request(m, 320, mask)
     st = rq.latent.clone()
     x0 = rq.latent.clone()
+    state0 = x0.double().cpu().numpy()
+    ctx_np = rq.txt.double().cpu().numpy()
     cache = ig.ig_cache_template(m.ctx, st.data_ptr(), rq.txt.data_ptr(), 0, [1.0, 0.5])
+    torch.cuda.synchronize()
+    ym = set(ig.y_block_modes(d.n_blocks, kv_blocks))
+    P, L, H = n_planes(d.n_blocks, ym), d.L_img, d.hidden
+    ptr, _, tier = ig.ig_cache_storage(cache)
+    assert tier == ig.IG_CACHE_HOST
+    nq = P * L * H
+    q = np.frombuffer((ctypes.c_char * nq).from_address(ptr), dtype=np.uint8).copy().reshape(1, P, L, H)
+    scl = np.frombuffer((ctypes.c_char * (P * L * d.heads * 4)).from_address(ptr + nq), dtype=np.float32)
+    scl = scl.copy().reshape(1, P, L, d.heads)
+    deq = _bf16_rne(_e4m3_to_f32(q) * np.repeat(scl, H // d.heads, axis=3)).astype(np.float64)
+    assert np.isfinite(deq).all()
+    kv_g, y_g = split_hybrid(deq, d.n_blocks, ym)
+    # (1) recording vs the oracle's dense template, within e4m3 rounding (3 mantissa bits: a
+    # relative step of 2^-3, so ~2^-4 max rounding error; 2^-3 per element leaves room for one
+    # flipped rounding of a bf16-vs-fp64 input) plus the per-(token, head) scale's subnormal floor
+    _, kv_o, y_o = oracle.unet_cache_template(d, W, state0, ctx_np, 1, record_y=True)
+    for b in range(d.n_blocks):
+        pairs = ([(y_g[0, b], y_o[0, b])] if (b in ym or b + 1 in ym) else []) + \
+                ([(kv_g[0, b, 0], kv_o[0, b, 0]), (kv_g[0, b, 1], kv_o[0, b, 1])] if b not in ym else [])
+        for g, o in pairs:
+            amax = np.abs(o).reshape(L, d.heads, -1).max(axis=2).repeat(H // d.heads, axis=1)
+            assert (np.abs(g - o) <= 0.125 * np.abs(o) + amax / 448.0 * 2.0 ** -6 + 2e-2 * amax).all(), b
+            assert np.linalg.norm(g - o) <= 0.06 * np.linalg.norm(o), b
+    # (2) the GPU edit on its recorded FP8 template vs the oracle on the same (dequantized) planes
     rr = ig.make_req(0, x0.data_ptr(), rq.mask, cache, 0, 0.0, 0.0, rq.txt.data_ptr(), None)
     ig.ig_edit_step(m.ctx, [rr], 0)
     torch.cuda.synchronize()
-    got, dense = x0.double().cpu().numpy(), st.double().cpu().numpy()
-    ok, worst = ctol(got[mask != 0], dense[mask != 0], 5e-2)
+    want = oracle.unet_edit_step_y(d, W, state0, mask, y_g[0], state0, ctx_np, y_blocks=ym, kv_cache_step=kv_g[0])
+    ok, worst = ctol(x0.double().cpu().numpy(), want, 2e-2)
     assert ok, worst
     ig.ig_cache_free(cache)
     rq.free()
