@@ -347,6 +347,7 @@ struct ig_ctx {
   char* h_stage[NSTAGE] = {};
   char* d_stage[NSTAGE] = {};
   char* m_stage[NSTAGE] = {};  // device (UVA) view of the mapped pinned h_stage
+  char* d_gstage = nullptr;    // graph-mode steps: one fixed device descriptor slot (see run_step)
   cudaEvent_t ev_stage[NSTAGE] = {};
   int stage_i = 0;
   RowInfo* ri = nullptr;
@@ -845,6 +846,10 @@ extern "C" ig_status ig_ctx_create(const ig_model_desc* desc, const void* const*
     }
     cudaEventCreateWithFlags(&ctx->ev_stage[i], cudaEventDisableTiming);
   }
+  if (cudaMalloc((void**)&ctx->d_gstage, ctx->stage_bytes) != cudaSuccess) {
+    ig_ctx_destroy(ctx);
+    return set_err(IG_ENOMEM, "staging allocation failed");
+  }
   cudaStreamCreateWithFlags(&ctx->copy_st, cudaStreamNonBlocking);
   for (int i = 0; i < MAXR; ++i) {
     cudaEventCreateWithFlags(&ctx->ev_copy[i], cudaEventDisableTiming);
@@ -880,6 +885,7 @@ extern "C" void ig_ctx_destroy(ig_ctx* ctx) {
     if (ctx->d_stage[i]) cudaFree(ctx->d_stage[i]);
     if (ctx->ev_stage[i]) cudaEventDestroy(ctx->ev_stage[i]);
   }
+  if (ctx->d_gstage) cudaFree(ctx->d_gstage);
   for (int i = 0; i < MAXR; ++i) {
     if (ctx->ev_copy[i]) cudaEventDestroy(ctx->ev_copy[i]);
     if (ctx->ev_comp[i]) cudaEventDestroy(ctx->ev_comp[i]);
@@ -1943,7 +1949,15 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
     t_host0 += std::chrono::steady_clock::now() - w0;  // back-pressure is not enqueue time
   }
   char* hs = ctx->h_stage[si];
-  char* ds = ctx->d_stage[si];
+  // a step that runs as a CUDA graph reads its descriptors from ONE fixed device slot, filled from
+  // this step's pinned slot just before the graph launch: the graph then does not depend on which
+  // of the NSTAGE host slots was used (before: NSTAGE captures per step shape — a new request cost
+  // 4+ captures and instantiations, ~100 ms, against ~150 ms of SD3 steps)
+  bool graph_ok = ctx->o.use_graphs && st != nullptr && !record && !rng.X_in && !rng.X_out && !ctx->prof &&
+                  b0 == 0 && b1 == nb;
+  for (auto& s2 : sr)
+    if (s2.use_cache && (s2.r->cache->tier != IG_CACHE_DEVICE || ctx->o.copy_mode == 0)) graph_ok = false;
+  char* ds = graph_ok ? ctx->d_gstage : ctx->d_stage[si];
   ReqDev* hreq = (ReqDev*)hs;
   // attention segments: [0, 2B) the masked-rows step, [2B, 5B) the dense prefix (+ unmasked)
   AttnSeg* hseg = (AttnSeg*)(hs + ctx->o.max_batch * sizeof(ReqDev));
@@ -2092,13 +2106,15 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
   // ---- CUDA graph of the step (device-tier caches / no cache only: host-tier DMA sources
   // change every step) ----
   // (the legacy default stream cannot be captured)
-  bool graph_ok = ctx->o.use_graphs && st != nullptr && !record && !rng.X_in && !rng.X_out && !ctx->prof &&
-                  b0 == 0 && b1 == nb;
-  for (auto& s2 : sr)
-    if (s2.use_cache && (s2.r->cache->tier != IG_CACHE_DEVICE || ctx->o.copy_mode == 0)) graph_ok = false;
   std::string gkey;
   if (graph_ok) {
-    std::vector<long long> k = {si, kplan, na, M, M_txt, M_full, nseg, max_q, nsegf, max_qf, max_nu, nsegcf, max_qcf,
+    // this step's descriptors -> the fixed graph slot, stream-ordered after the previous step
+    launch_copy_bytes(ds, ctx->m_stage[si], desc_bytes, st);
+    if (plan.gather || plan.gather_q8) {
+      const size_t off = (char*)hkvg - hs, bytes = (char*)(hkvq + (size_t)nb * na) - (char*)hkvg;
+      CUDA_TRY(cudaMemcpyAsync(ds + off, hs + off, bytes, cudaMemcpyHostToDevice, st));
+    }
+    std::vector<long long> k = {kplan, na, M, M_txt, M_full, nseg, max_q, nsegf, max_qf, max_nu, nsegcf, max_qcf,
                                 plan.gather, plan.gather_q8, any_cache, (long long)desc_bytes};
     for (int v : uy) k.push_back(v);
     for (auto& s2 : sr) {
@@ -2149,8 +2165,8 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
       c->lane_on = false;
     }
   } lane_guard{ctx};
-  launch_copy_bytes(ds, ctx->m_stage[si], desc_bytes, st);
-  if (plan.gather || plan.gather_q8) {
+  if (!graph_ok) launch_copy_bytes(ds, ctx->m_stage[si], desc_bytes, st);
+  if (!graph_ok && (plan.gather || plan.gather_q8)) {
     const size_t off = (char*)hkvg - hs, bytes = (char*)(hkvq + (size_t)nb * na) - (char*)hkvg;
     if (ctx->lane_on) {
       lane_push(ctx, [ctx, ds, hs, off, bytes] {

@@ -54,14 +54,17 @@ constexpr float RESCALE_THRESHOLD = 8.0f;       // log2 units
 #endif
 // d = 64 does half the MMA work per score, so the MUFU exp2 rate (16 / clk / SM) bounds the
 // softmax at about twice the MMA time: move a larger share of the pairs to the FMA pipe
+// (round 2, without the register split every share 1/4 .. 5/8 was slower — it spilled; with
+// setmaxnreg 1 in 4 pairs is 5% fewer cycles at the UNet / SD3 shapes, 3 in 8 and 1 in 2 less
+// good: profiles/r02_attn_restructure_ab.md)
 #ifndef POLY64_AT
-#define POLY64_AT(i) 0  // measured (ncu cycles, UNet shapes): every poly share tried (1/4 .. 5/8) is slower
+#define POLY64_AT(i) (((i) & 3) == 3)
 #endif
 #ifndef ATTN_MAX3
 #define ATTN_MAX3 0       // row max with 3-input FMNMX3 (half the max-phase instructions)
 #endif
 #ifndef ATTN_SETMAXNREG
-#define ATTN_SETMAXNREG 0  // per-warpgroup register split (producer/MMA low, softmax high)
+#define ATTN_SETMAXNREG 1  // per-warpgroup register split (producer/MMA low, softmax high)
 #endif
 #ifndef ATTN_REGS_PRODUCER
 #define ATTN_REGS_PRODUCER 56
@@ -191,14 +194,20 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   __syncthreads();
   tc::tc_fence_after();
   const uint32_t tmem = bar->tmem;
+  // register split per warpgroup (setmaxnreg, ATTN_SETMAXNREG): the TMA / MMA warpgroup needs few
+  // registers, the two softmax warpgroups hold a 128-column row of S each.  Each role executes its
+  // own setmaxnreg inside its branch (a dec / inc before a merge point makes ptxas compile the
+  // merged code for the smaller count)
 #if ATTN_SETMAXNREG
-  // register split per warpgroup (setmaxnreg): the TMA / MMA warpgroup needs few registers, the
-  // two softmax warpgroups hold a 128-column row of S each (no spills, more ILP for the exps)
-  if (warp < 4) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(ATTN_REGS_PRODUCER));
-  else asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(ATTN_REGS_SOFTMAX));
+#define REG_DEC() asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(ATTN_REGS_PRODUCER))
+#define REG_INC() asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(ATTN_REGS_SOFTMAX))
+#else
+#define REG_DEC() do { } while (0)
+#define REG_INC() do { } while (0)
 #endif
 
   if (warp == 0) {
+    REG_DEC();
     if (lane == 0) {  // ===== TMA producer =====
       const int qrow = seg.q_start + q0;
       tc::mbar_arrive_expect_tx(&bar->q_full, (has_b ? 2 : 1) * Q_BYTES);
@@ -217,6 +226,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       }
     }
   } else if (warp == 2) {
+    REG_DEC();
     if (lane == 0) {  // ===== TMA producer, V ring =====
       for (int j = 0; j < nkv; ++j) {
         const int s = j % VSTAGES;
@@ -228,6 +238,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       }
     }
   } else if (warp == 1) {
+    REG_DEC();
     if (lane == 0) {  // ===== MMA issuer =====
       constexpr uint32_t idS = tc::idesc_bf16(BQ, BKV, 0);
       constexpr uint32_t idO = tc::idesc_bf16(BQ, D, 1);  // B = V is MN-major
@@ -313,6 +324,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       }
     }
   } else if (warp >= 4) {  // ===== softmax / correction / epilogue, tile t =====
+    REG_INC();
     const int t = (warp - 4) >> 2;
     if (t == 0 || has_b) {
       const int quad = warp & 3;
@@ -439,6 +451,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         }
       }
     }
+  } else {
+    REG_DEC();  // warp 3: idle
   }
   tc::tc_fence_before();
   __syncthreads();
