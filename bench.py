@@ -245,7 +245,9 @@ def run_loop(ig, ctx, batch, cache, sig, steps, stream, profile=False):
         # host-buffer path (e2e): each request's latent lives in pinned host memory and the step's
         # gather/scatter kernels read its masked rows and write the updated rows in place over the
         # host link (no device copy of the latent exists)
+        t_h0 = time.perf_counter()
         ig.ig_edit_step(ctx, batch.reqs(cache, sig), stream.cuda_stream)
+        t_h1 = time.perf_counter()
         plans.append(ig.ig_last_plan(ctx))
         alg_flops += sum(request_step_flops(batch.d, r.n_m) for r in batch.slots)
         st = ig.ig_last_stats(ctx)
@@ -263,7 +265,11 @@ def run_loop(ig, ctx, batch, cache, sig, steps, stream, profile=False):
             torch.cuda.synchronize()
             torch.cuda.profiler.stop()
             _PROFILED_ONE = True
+        t_h2 = time.perf_counter()
         rsteps += batch.advance()  # leaving requests' masks freed, joiners admitted (on the stream)
+        if os.environ.get("IG_BENCH_STEP_TRACE"):
+            print(f"step {si}: ig_edit_step host {1e3 * (t_h1 - t_h0):.2f} ms, advance "
+                  f"{1e3 * (time.perf_counter() - t_h2):.2f} ms", file=sys.stderr)
     end.record(stream)
     end.synchronize()
     h2d += batch.admit_bytes  # joiners' bitmaps (+ text tokens / cond vectors on the host path)
@@ -271,6 +277,10 @@ def run_loop(ig, ctx, batch, cache, sig, steps, stream, profile=False):
     if profile:
         ig.ig_profile_enable(ctx, False)
     per_step = [a.elapsed_time(b) for a, b in evs]
+    if os.environ.get("IG_BENCH_STEP_TRACE"):
+        gaps = [evs[i][1].elapsed_time(evs[i + 1][0]) for i in range(len(evs) - 1)]
+        print("device ms per step:", [round(x, 2) for x in per_step], "\ngaps between steps:",
+              [round(x, 2) for x in gaps], file=sys.stderr)
     lg = Leg(start.elapsed_time(end), rsteps, launches, per_step, prof, h2d, d2h, plans, alg_flops)
     lg.host_ms_per_step = 1e3 * host_s / max(steps, 1)
     return lg

@@ -1,0 +1,7 @@
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_unet.py tests/test_gpu_pipeline.py -x -q -m gpu -k "graph" > gpurun_out/r3c35_tests.log 2>&1; echo tests rc=$?; tail -2 gpurun_out/r3c35_tests.log
+A="--model sd3_medium --max-batch 1 --tier device --graphs --mask-kind blob --mask-lo 0.1 --mask-hi 0.5 --steps 56 --warmup 8 --no-e2e --no-hbm-tier --no-fp8 --no-y --no-lockstep --no-ablation --no-cpu-baseline --dense-steps 8 --no-prof-leg"
+for r in 1 2 3 4; do
+IG_GRAPH_TRACE=1 timeout 900 python bench.py $A > gpurun_out/r3c35_sd3_$r.log 2> gpurun_out/r3c35_sd3_$r.err; echo "run $r" rc=$?; tail -1 gpurun_out/r3c35_sd3_$r.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['value'], d['ms_per_step'], d['per_step_ms'], d.get('speedup_vs_dense'))"
+grep -E "IG_GRAPH_TRACE: capture" gpurun_out/r3c35_sd3_$r.err | tail -3
+done
