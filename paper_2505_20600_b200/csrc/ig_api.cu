@@ -2675,7 +2675,11 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
           exec = git->second.exec;
           ctx->graphs.erase(git);
         } else {
-          (void)cudaGetLastError();  // a topology mismatch is not an error of the step
+          // a topology mismatch is not an error of the step; the stale candidate is dropped so
+          // that a partially updated exec can never be replayed under its old key
+          (void)cudaGetLastError();
+          cudaGraphExecDestroy(git->second.exec);
+          ctx->graphs.erase(git);
         }
       }
     }
