@@ -2674,6 +2674,10 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
         if (cudaGraphExecUpdate(git->second.exec, graph, &info) == cudaSuccess) {
           exec = git->second.exec;
           ctx->graphs.erase(git);
+#ifdef IG_GRAPH_UPDATE_TRACE
+          fprintf(stderr, "IG_GRAPH_UPDATE_TRACE: step %llu updated a graph last used at step %llu\n", step_no,
+                  cand[i].first);
+#endif
         } else {
           // a topology mismatch is not an error of the step; the stale candidate is dropped so
           // that a partially updated exec can never be replayed under its old key

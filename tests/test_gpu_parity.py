@@ -664,6 +664,41 @@ def test_cuda_graph_steps_bitwise_equal_eager():
     eager.close()
 
 
+def test_cuda_graph_update_on_new_shapes_bitwise_equal_eager():
+    """A new step shape updates a stale graph of the same topology in place (cudaGraphExecUpdate)
+    instead of instantiating: three phases of 5 steps, each with two fresh requests (new masks, so
+    new row counts / keys; same cache kinds, so the same kernel sequence) — phases 2 and 3 find
+    phase 1's / 2's graphs stale — and every latent equals the eager path bitwise."""
+    d = synth.FLUX_SMALL
+    sig = synth.flow_sigmas(8)
+    eager = Model(d, ig.IG_BF16, opts=ig.ig_ctx_opts(4, 0, 2, 1, 0, 0))
+    ptrs = [eager.W[n].data_ptr() for n, _, _ in synth.weight_table(d)]
+    gctx = ig.ig_ctx_create(eager.desc, ptrs, 0, ig.ig_ctx_opts(4, 0, 2, 1, 0, 0, 0, 0, 1))
+    kv = synth.make_cache_kv(d, 13, 8, dtype=torch.bfloat16)
+    tlat = torch.stack([synth.make_latent(d, 970 + s) for s in range(8)])
+    kvc = ig.ig_cache_create(eager.ctx, 8, ig.IG_CACHE_DEVICE)
+    fill_cache(eager, kvc, kv, tlat)
+    stream = torch.cuda.Stream()
+    rng = np.random.default_rng(43)
+    for phase in range(3):
+        masks = [synth.blob_mask_count(d, int(rng.integers(30, 110)), rng), synth.rect_mask_count(d, int(rng.integers(20, 60)), rng)]
+        ra = [Request(eager, 300 + 10 * phase + i, mk) for i, mk in enumerate(masks)]
+        rb = [Request(eager, 300 + 10 * phase + i, mk) for i, mk in enumerate(masks)]
+        for s in range(5):
+            for ctx, rs in ((eager.ctx, ra), (gctx, rb)):
+                ig.ig_edit_step(ctx, [rs[i].req(i, kvc, s, float(sig[s]), float(sig[s + 1])) for i in range(2)],
+                                stream.cuda_stream)
+        torch.cuda.synchronize()
+        for a, b in zip(ra, rb):
+            assert torch.equal(a.latent, b.latent), phase
+            assert not torch.equal(a.latent, a.latent0)
+        for r in ra + rb:
+            r.free()
+    ig.ig_cache_free(kvc)
+    ig.ig_ctx_destroy(gctx)
+    eager.close()
+
+
 @pytest.mark.parametrize("kind", ["kv", "hybrid"])
 def test_load_dedupe_same_template_and_step(kind):
     """Requests on the same (host-tier cache, step) share their staged rows (SURVEY N4 load
