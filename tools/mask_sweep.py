@@ -48,7 +48,7 @@ def main():
         for m in [float(x) for x in args.ratios.split(",")]:
             bench.MASKS.update(lo=m, hi=m, kind="mixed")
             dense = m >= 1.0
-            bt = bench.Batch(ig, ctx, d, dev, args.max_batch, pool, rid0=7000, dense=dense)
+            bt = bench.Batch(ig, ctx, d, dev, args.max_batch, pool, rid0=7000, stream=stream, dense=dense)
             bench.run_loop(ig, ctx, bt, None if dense else cache, sig, args.warmup, stream)
             lg = bench.run_loop(ig, ctx, bt, None if dense else cache, sig, args.steps, stream, profile=True)
             ms = lg.ms / args.steps
@@ -58,8 +58,8 @@ def main():
                                   "alg_tflop_per_request_step": round(f / 1e12, 3),
                                   "host_link_GBps": round(lg.h2d / (lg.ms * 1e-3) / 1e9, 2),
                                   "gemm_tflops": round(lg.tflops("gemm"), 1), "attn_tflops": round(lg.tflops("attn"), 1)})
-            for r in bt.pool:
-                ig.ig_mask_free(r.mask)
+            torch.cuda.synchronize()
+            bt.close()
             print(json.dumps(out["points"][-1]), flush=True)
             if dense:
                 break
