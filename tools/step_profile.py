@@ -1,7 +1,8 @@
 """One representative Flux batch step for ncu: 8 requests (masks m~U[.05,.6]) against a 2-step
 template cache in pinned host memory; the profiled step is wrapped in an NVTX range
 'profile_step' (use: ncu --nvtx --nvtx-include 'profile_step/' ...).
-Env: COPY_MODE (1), KV_BLOCKS (-1 = K/V cache; else hybrid K/V blocks), PLAN_K (0), DEPTH (8)."""
+Env: COPY_MODE (1), KV_BLOCKS (-1 = K/V cache; else hybrid K/V blocks), PLAN_K (0), DEPTH (8).
+(bench.py's IG_BENCH_PROFILE_STEP=1 brackets a steady-state step of the real headline loop instead.)"""
 import sys, os
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
@@ -22,8 +23,8 @@ if int(os.environ.get("PLAN_K", "0")) > 0:
 sig = synth.flow_sigmas(28)
 tl = synth.make_latent(d, 10 ** 6, dev); tt = synth.make_txt(d, 10 ** 6, dev, torch.bfloat16); tc = synth.make_cond(d, 10 ** 6, dev)
 cache = ig.ig_cache_template(ctx, tl.data_ptr(), tt.data_ptr(), tc.data_ptr(), sig[:3], ig.IG_CACHE_HOST, 0)
-b = Batch(ig, ctx, d, dev, 8, 12, 0)
 stream = torch.cuda.Stream()
+b = Batch(ig, ctx, d, dev, 8, 12, 0, stream)
 def step():
     reqs = b.reqs(cache, sig)
     for r in reqs:
