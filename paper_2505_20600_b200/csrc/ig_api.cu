@@ -321,6 +321,10 @@ struct ig_ctx {
   // self-attention chain (small-M GEMMs that leave SMs idle) runs on the compute stream; the
   // cross arena is double-buffered by block parity
   cudaStream_t xs = nullptr;
+  // double blocks: the text stream's ops run on ts concurrently with the image stream's (disjoint
+  // rows of X / h / Q / cat; ig_tuning.txt_overlap)
+  cudaStream_t ts = nullptr;
+  cudaEvent_t ev_tfork[2] = {}, ev_tjoin[2] = {};
   cudaEvent_t ev_xfork = nullptr, ev_xkv[2] = {}, ev_xuse[2] = {};
   std::vector<ModT> mods;
   long long mod_ld = 0;
@@ -852,6 +856,11 @@ extern "C" ig_status ig_ctx_create(const ig_model_desc* desc, const void* const*
     return set_err(IG_ENOMEM, "staging allocation failed");
   }
   cudaStreamCreateWithFlags(&ctx->copy_st, cudaStreamNonBlocking);
+  cudaStreamCreateWithFlags(&ctx->ts, cudaStreamNonBlocking);
+  for (int i = 0; i < 2; ++i) {
+    cudaEventCreateWithFlags(&ctx->ev_tfork[i], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&ctx->ev_tjoin[i], cudaEventDisableTiming);
+  }
   for (int i = 0; i < MAXR; ++i) {
     cudaEventCreateWithFlags(&ctx->ev_copy[i], cudaEventDisableTiming);
     cudaEventCreateWithFlags(&ctx->ev_comp[i], cudaEventDisableTiming);
@@ -896,6 +905,11 @@ extern "C" void ig_ctx_destroy(ig_ctx* ctx) {
   if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
   if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
   if (ctx->xs) cudaStreamDestroy(ctx->xs);
+  if (ctx->ts) cudaStreamDestroy(ctx->ts);
+  for (int i = 0; i < 2; ++i) {
+    if (ctx->ev_tfork[i]) cudaEventDestroy(ctx->ev_tfork[i]);
+    if (ctx->ev_tjoin[i]) cudaEventDestroy(ctx->ev_tjoin[i]);
+  }
   if (ctx->ev_xfork) cudaEventDestroy(ctx->ev_xfork);
   for (int i = 0; i < 2; ++i) {
     if (ctx->ev_xkv[i]) cudaEventDestroy(ctx->ev_xkv[i]);
@@ -2587,13 +2601,32 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
     } else if (b < ctx->d.n_double) {
       const StreamW& wi = ctx->dimg[b];
       const StreamW& wt = ctx->dtxt[b];
+      // text-stream ops on ts, concurrent with the image stream's (rows [0, M_txt) vs [M_txt, Mc))
+      const bool tov = ig_tuning_ref().txt_overlap && Lt > 0 && M_txt > 0;
+      auto on_ts = [&](int k, auto&& issue) {
+        cudaEventRecord(ctx->ev_tfork[k], st);
+        cudaStreamWaitEvent(ctx->ts, ctx->ev_tfork[k], 0);
+        cudaStream_t st0 = st;
+        st = ctx->ts;
+        ctx->pdl_block = true;
+        issue();
+        cudaEventRecord(ctx->ev_tjoin[k], st);
+        st = st0;
+        ctx->pdl_block = true;
+      };
+      auto txt_pre = [&] {
+        ln_mod(0, M_txt, wt.mod_t, wt.pre_only ? 1 : 0, wt.pre_only ? 0 : 1);
+        qkv_proj(0, M_txt, wt.qkv.w, wt.qkv.b, wt.qg, wt.kg, buf);
+      };
+      if (tov) on_ts(0, txt_pre);
       ln_mod(M_txt, ys ? M : Mk, wi.mod_t, 0, 1);
       if (ys) ln_mod_y(b, buf, wi.mod_t, 0, 1);
-      if (Lt) ln_mod(0, M_txt, wt.mod_t, wt.pre_only ? 1 : 0, wt.pre_only ? 0 : 1);
+      if (Lt && !tov) ln_mod(0, M_txt, wt.mod_t, wt.pre_only ? 1 : 0, wt.pre_only ? 0 : 1);
       if (!dense) wait_copy(buf);
       qkv_proj(M_txt, Mc, wi.qkv.w, wi.qkv.b, wi.qg, wi.kg, buf);
       if (!dense) kv_proj(M, M + uy[b], wi.qkv.w, wi.qkv.b, wi.kg, buf);
-      if (Lt) qkv_proj(0, M_txt, wt.qkv.w, wt.qkv.b, wt.qg, wt.kg, buf);
+      if (Lt && !tov) qkv_proj(0, M_txt, wt.qkv.w, wt.qkv.b, wt.qg, wt.kg, buf);
+      if (tov) stream_wait(ctx, st, ctx->ev_tjoin[0]);
       if (!dense) wait_copy_late(buf);
       attn(buf, dense);
       record_kv(b, buf);
@@ -2603,17 +2636,21 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
         if (b + R < b1 && !seq_load) issue_copy(ctx, sr, dkvg, dkvq, b + R, plan);
       }
       const long long gi = ctx->mods[wi.mod_t].off;
-      gemm_rows(M_txt, Mc, cat, ldcat, wi.proj.w, wi.proj.b, H, H, ctx->X, H, EPI_GATED_RES, mod + gi + 2 * H, 0);
-      ln_mod(M_txt, Mc, wi.mod_t, 3, 4);
-      gemm_rows(M_txt, Mc, h, H, wi.fc1.w, wi.fc1.b, F, H, cat + H, ldcat, EPI_GELU, nullptr, 0);
-      gemm_rows(M_txt, Mc, cat + H, ldcat, wi.fc2.w, wi.fc2.b, H, F, ctx->X, H, EPI_GATED_RES, mod + gi + 5 * H, 0);
-      if (Lt && !wt.pre_only) {
+      auto txt_post = [&] {
         const long long gt = ctx->mods[wt.mod_t].off;
         gemm_rows(0, M_txt, cat, ldcat, wt.proj.w, wt.proj.b, H, H, ctx->X, H, EPI_GATED_RES, mod + gt + 2 * H, 0);
         ln_mod(0, M_txt, wt.mod_t, 3, 4);
         gemm_rows(0, M_txt, h, H, wt.fc1.w, wt.fc1.b, F, H, cat + H, ldcat, EPI_GELU, nullptr, 0);
         gemm_rows(0, M_txt, cat + H, ldcat, wt.fc2.w, wt.fc2.b, H, F, ctx->X, H, EPI_GATED_RES, mod + gt + 5 * H, 0);
-      }
+      };
+      const bool tpost = Lt && !wt.pre_only;
+      if (tov && tpost) on_ts(1, txt_post);
+      gemm_rows(M_txt, Mc, cat, ldcat, wi.proj.w, wi.proj.b, H, H, ctx->X, H, EPI_GATED_RES, mod + gi + 2 * H, 0);
+      ln_mod(M_txt, Mc, wi.mod_t, 3, 4);
+      gemm_rows(M_txt, Mc, h, H, wi.fc1.w, wi.fc1.b, F, H, cat + H, ldcat, EPI_GELU, nullptr, 0);
+      gemm_rows(M_txt, Mc, cat + H, ldcat, wi.fc2.w, wi.fc2.b, H, F, ctx->X, H, EPI_GATED_RES, mod + gi + 5 * H, 0);
+      if (tov && tpost) stream_wait(ctx, st, ctx->ev_tjoin[1]);
+      else if (tpost) txt_post();
     } else {
       const SingleW& ws = ctx->sgl[b - ctx->d.n_double];
       ln_mod(0, ys ? M : Mk, ws.mod_t, 0, 1);
@@ -3054,6 +3091,7 @@ static void tuning_seed_locked() {
   g_tuning.precise_gelu = getenv("IG_PRECISE_GELU") != nullptr ? 1 : 0;
   const char* rep = getenv("IG_OP_REPEAT");
   g_tuning.op_repeat = rep ? std::max(1, atoi(rep)) : 1;
+  g_tuning.txt_overlap = off("IG_NO_TXT_OVERLAP");
   g_tuning_init.store(true, std::memory_order_release);
 }
 const ig_tuning& ig_tuning_ref() {

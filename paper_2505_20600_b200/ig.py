@@ -101,7 +101,7 @@ class ig_tuning(ctypes.Structure):
     """include/ig_ops.h ig_tuning: process-wide libig knobs (see the header for each field)."""
     _fields_ = [(n, ctypes.c_int) for n in ("pdl", "copy_thread", "load_dedupe", "cross_kv_overlap",
                                             "gemm_two_cta", "gemm_small_tiles", "gemm_bn64", "conv_two_cta",
-                                            "precise_gelu", "op_repeat")]
+                                            "precise_gelu", "op_repeat", "txt_overlap")]
 
 
 def lib():
