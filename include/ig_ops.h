@@ -76,7 +76,7 @@ typedef struct ig_tuning {
   int precise_gelu;     /* debug: libm erf / tanh GELU instead of the MUFU forms (0; IG_PRECISE_GELU) */
   int op_repeat;        /* ig_op_attention: launches per call, benchmarking aid (1; IG_OP_REPEAT=n) */
   int txt_overlap;      /* double blocks: text-stream ops on a side stream, concurrent with the image
-                           stream's (1; IG_NO_TXT_OVERLAP) */
+                           stream's, for steps of <= 4096 rows outside profiling (1; IG_NO_TXT_OVERLAP) */
 } ig_tuning;
 ig_status ig_tuning_get(ig_tuning* out);       /* IG_EINVAL if out is NULL */
 ig_status ig_tuning_set(const ig_tuning* t);   /* IG_EINVAL if t is NULL or op_repeat < 1 */

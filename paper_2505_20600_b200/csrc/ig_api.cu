@@ -2602,7 +2602,10 @@ static ig_status run_step(ig_ctx* ctx, const ig_edit_req* reqs, int n, cudaStrea
       const StreamW& wi = ctx->dimg[b];
       const StreamW& wt = ctx->dtxt[b];
       // text-stream ops on ts, concurrent with the image stream's (rows [0, M_txt) vs [M_txt, Mc))
-      const bool tov = ig_tuning_ref().txt_overlap && Lt > 0 && M_txt > 0;
+      // only for small problems (below ~4k rows a stream's GEMMs leave most SMs idle; a batch of
+      // 8 Flux requests fills the GPU with either stream: measured neutral), and never in a
+      // profiled step (per-launch events would time two streams sharing the SMs)
+      const bool tov = ig_tuning_ref().txt_overlap && Lt > 0 && M_txt > 0 && Mc <= 4096 && !ctx->prof;
       auto on_ts = [&](int k, auto&& issue) {
         cudaEventRecord(ctx->ev_tfork[k], st);
         cudaStreamWaitEvent(ctx->ts, ctx->ev_tfork[k], 0);
